@@ -1,0 +1,308 @@
+"""ctypes loader for the CPU oracle (oracle/fgs_oracle.cpp) and the reference build.
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and bench.py's
+CPU-baseline leg, never by the product package.
+
+Two libraries:
+  * ``oracle/_build/libfgs_oracle.so`` — the restatement (parity / libm modes).
+  * ``oracle/_ref/libomnisplat_ref.so`` — the reference's own headers compiled against the
+    repo's Eigen-subset shim (built here by oracle/Makefile when /root/reference exists; the
+    built .so travels to the GPU box). ``ref_available()`` says whether it is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "libfgs_oracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libomnisplat_ref.so")
+
+MODE_PARITY = 0
+MODE_LIBM = 1
+
+_lib = None
+_ref = None
+
+
+def build(quiet=True):
+    """Build the oracle (and, when /root/reference is mounted, the reference) via make."""
+    subprocess.run(["make", "-C", HERE] + (["-s"] if quiet else []), check=True)
+
+
+def _p(a, ct):
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32, dp, fp = C.c_void_p, C.c_int64, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_float)
+        for name, rp in (("orc_render_f32", fp), ("orc_render_f64", dp)):
+            fn = getattr(L, name)
+            fn.restype = vp
+            fn.argtypes = [i64, rp, rp, rp, rp, rp, dp, rp, i32, i32, i32]
+        for name, rp in (("orc_backward_f32", fp), ("orc_backward_f64", dp)):
+            fn = getattr(L, name)
+            fn.restype = i32
+            fn.argtypes = [vp, i64, rp, rp, dp, i32, i32, i32, rp]
+        L.orc_free.argtypes = [vp]
+        L.orc_sizes.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.orc_stats.argtypes = [vp, dp]
+        L.orc_get.restype = i64
+        L.orc_get.argtypes = [vp, C.c_char_p, vp]
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_bruteforce_render_f64.restype = i32
+        L.orc_bruteforce_render_f64.argtypes = [i64, dp, dp, dp, dp, dp, dp, dp, i32, dp, dp]
+        L.orc_bruteforce_intersections.restype = C.c_uint64
+        L.orc_bruteforce_intersections.argtypes = [i64, dp, C.POINTER(C.c_int32), i32, i32]
+        L.orc_project_f64.restype = i32
+        L.orc_project_f64.argtypes = [dp, dp, dp, dp, i32]
+        L.orc_project_f32.restype = i32
+        L.orc_project_f32.argtypes = [dp, fp, fp, fp, i32]
+        L.orc_jacobian_grad_f64.argtypes = [dp, dp, dp]
+        L.orc_build_covariance_f64.restype = i32
+        L.orc_build_covariance_f64.argtypes = [dp, dp, dp]
+        L.orc_build_covariance_backward_f64.restype = i32
+        L.orc_build_covariance_backward_f64.argtypes = [dp, dp, dp, dp, dp]
+        L.orc_eval_sh_f64.argtypes = [dp, dp, i32, dp]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def ref_lib():
+    """The reference headers compiled against the Eigen shim (same C entry points as the
+    restatement's render/backward/get/stats, prefixed ``ref_``)."""
+    global _ref
+    if _ref is None:
+        if not ref_available():
+            raise FileNotFoundError(REF_PATH)
+        L = C.CDLL(REF_PATH)
+        vp, i64, i32, dp, fp = C.c_void_p, C.c_int64, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_float)
+        for name, rp in (("ref_render_f32", fp), ("ref_render_f64", dp)):
+            fn = getattr(L, name)
+            fn.restype = vp
+            fn.argtypes = [i64, rp, rp, rp, rp, rp, dp, rp, i32, i32]
+        for name, rp in (("ref_backward_f32", fp), ("ref_backward_f64", dp)):
+            fn = getattr(L, name)
+            fn.restype = i32
+            fn.argtypes = [vp, i64, rp, rp, dp, i32, rp]
+        L.ref_free.argtypes = [vp]
+        L.ref_sizes.argtypes = [vp, C.POINTER(C.c_int64)]
+        L.ref_stats.argtypes = [vp, dp]
+        L.ref_get.restype = i64
+        L.ref_get.argtypes = [vp, C.c_char_p, vp]
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_bruteforce_render_f64.restype = i32
+        L.ref_bruteforce_render_f64.argtypes = [i64, dp, dp, dp, dp, dp, dp, dp, i32, dp]
+        _ref = L
+    return _ref
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+_DTYPES = {
+    "state": np.int32, "radius": np.int32, "source": np.int32,
+    "refs": np.uint32, "offsets": np.uint32, "key_tile": np.uint32, "key_splat": np.uint32,
+    "key_depth": np.uint64, "count": np.uint16,
+}
+
+
+@dataclass
+class Result:
+    """A forward render held by the oracle (ForwardContext analogue)."""
+
+    handle: int
+    dtype: type
+    n: int
+    num_splats: int
+    num_intersections: int
+    tiles_x: int
+    tiles_y: int
+    width: int
+    height: int
+    prefix: str = "orc"
+
+    def _L(self):
+        return lib() if self.prefix == "orc" else ref_lib()
+
+    def get(self, name):
+        L = self._L()
+        fn = L.orc_get if self.prefix == "orc" else L.ref_get
+        cnt = fn(self.handle, name.encode(), None)
+        if cnt < 0:
+            raise KeyError(name)
+        out = np.empty(cnt, _DTYPES.get(name, self.dtype))
+        fn(self.handle, name.encode(), out.ctypes.data_as(C.c_void_p))
+        return out
+
+    def stats(self) -> dict:
+        out = np.zeros(11, np.float64)
+        (self._L().orc_stats if self.prefix == "orc" else self._L().ref_stats)(self.handle, _p(out, C.c_double))
+        keys = ["num_intersections", "num_splats", "num_culled", "num_degenerate", "preprocess_ms",
+                "binning_ms", "sort_ms", "raster_ms", "peak_aux_bytes", "e_eval", "e_contrib"]
+        return dict(zip(keys, out.tolist()))
+
+    @property
+    def image(self):
+        return self.get("image").reshape(self.height, self.width, 3)
+
+    def close(self):
+        if self.handle:
+            (self._L().orc_free if self.prefix == "orc" else self._L().ref_free)(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _scene_arrays(scene, dtype):
+    s = scene.astype(dtype)
+    return s, [s.means, s.rotations, s.log_scales, s.opacity_logits, s.sh]
+
+
+def render(scene, camera, sh_degree=3, background=None, dtype=np.float32, threads=0, mode=MODE_PARITY,
+           impl="orc") -> Result:
+    """Reference ``render<S>`` (inc/splatting.hpp:330-374) on the oracle (``impl='orc'``) or on
+    the reference build (``impl='ref'``; always libm transcendentals)."""
+    ct = C.c_float if dtype == np.float32 else C.c_double
+    s, arrs = _scene_arrays(scene, dtype)
+    bg = np.asarray(s.background if background is None else background, dtype)
+    cam = camera.to_array()
+    if impl == "orc":
+        L = lib()
+        fn = L.orc_render_f32 if dtype == np.float32 else L.orc_render_f64
+        h = fn(s.n, *[_p(a, ct) for a in arrs], _p(cam, C.c_double), _p(bg, ct), sh_degree, threads, mode)
+        err = L.orc_last_error
+        sizes_fn = L.orc_sizes
+    else:
+        L = ref_lib()
+        fn = L.ref_render_f32 if dtype == np.float32 else L.ref_render_f64
+        h = fn(s.n, *[_p(a, ct) for a in arrs], _p(cam, C.c_double), _p(bg, ct), sh_degree, threads)
+        err = L.ref_last_error
+        sizes_fn = L.ref_sizes
+    if not h:
+        raise OracleError(err().decode())
+    sz = np.zeros(7, np.int64)
+    sizes_fn(h, sz.ctypes.data_as(C.POINTER(C.c_int64)))
+    return Result(h, dtype, int(sz[0]), int(sz[1]), int(sz[2]), int(sz[3]), int(sz[4]), int(sz[5]),
+                  int(sz[6]), impl)
+
+
+def backward(res: Result, n, dl_dimage, full_sh=True, jacobian_grad_scale=None, threads=0,
+             mode=MODE_PARITY, want_splat_grads=False):
+    """Reference ``backward<S>`` (inc/gradients.hpp:207-267). Returns (grads[n,59], splat_grads
+    [num_splats,9] or None)."""
+    dtype = res.dtype
+    ct = C.c_float if dtype == np.float32 else C.c_double
+    dl = np.ascontiguousarray(dl_dimage, dtype).reshape(-1)
+    grads = np.zeros((n, 59), dtype)
+    sg = np.zeros((res.num_splats, 9), dtype) if want_splat_grads else None
+    jgs = None if jacobian_grad_scale is None else np.asarray(jacobian_grad_scale, np.float64)
+    jp = _p(jgs, C.c_double) if jgs is not None else None
+    if res.prefix == "orc":
+        L = lib()
+        fn = L.orc_backward_f32 if dtype == np.float32 else L.orc_backward_f64
+        rc = fn(res.handle, n, _p(dl, ct), _p(grads, ct), jp, int(full_sh), threads, mode,
+                _p(sg, ct) if sg is not None else None)
+        err = L.orc_last_error
+    else:
+        L = ref_lib()
+        fn = L.ref_backward_f32 if dtype == np.float32 else L.ref_backward_f64
+        rc = fn(res.handle, n, _p(dl, ct), _p(grads, ct), jp, threads, _p(sg, ct) if sg is not None else None)
+        err = L.ref_last_error
+    if rc != 0:
+        raise OracleError(err().decode())
+    return grads, sg
+
+
+def bruteforce_render(scene, camera, sh_degree=0, background=None, impl="orc"):
+    """inc/oracle.hpp:231-270 in double. Returns (image[H,W,3], transmittance[H,W])."""
+    s, arrs = _scene_arrays(scene, np.float64)
+    bg = np.asarray(s.background if background is None else background, np.float64)
+    cam = camera.to_array()
+    img = np.zeros((camera.height, camera.width, 3))
+    tr = np.zeros((camera.height, camera.width))
+    dp = C.c_double
+    if impl == "orc":
+        L = lib()
+        rc = L.orc_bruteforce_render_f64(s.n, *[_p(a, dp) for a in arrs], _p(cam, dp), _p(bg, dp), sh_degree,
+                                         _p(img, dp), _p(tr, dp))
+        err = L.orc_last_error
+    else:
+        L = ref_lib()
+        rc = L.ref_bruteforce_render_f64(s.n, *[_p(a, dp) for a in arrs], _p(cam, dp), _p(bg, dp), sh_degree,
+                                         _p(img, dp))
+        err = L.ref_last_error
+    if rc != 0:
+        raise OracleError(err().decode())
+    return img, tr
+
+
+def bruteforce_intersections(mean_px, radius, width, height) -> int:
+    m = np.ascontiguousarray(mean_px, np.float64).reshape(-1)
+    r = np.ascontiguousarray(radius, np.int32)
+    return int(lib().orc_bruteforce_intersections(len(r), _p(m, C.c_double), _p(r, C.c_int32), width, height))
+
+
+def project(camera, p, force=0):
+    """cameras.hpp:139-177 in double: (visible, pixel[2], jacobian[2,3])."""
+    cam = camera.to_array()
+    pt = np.ascontiguousarray(p, np.float64)
+    px = np.zeros(2)
+    j = np.zeros((2, 3))
+    v = lib().orc_project_f64(_p(cam, C.c_double), _p(pt, C.c_double), _p(px, C.c_double), _p(j, C.c_double), force)
+    return bool(v), px, j
+
+
+def jacobian_grad(camera, p):
+    cam = camera.to_array()
+    pt = np.ascontiguousarray(p, np.float64)
+    out = np.zeros((3, 2, 3))
+    lib().orc_jacobian_grad_f64(_p(cam, C.c_double), _p(pt, C.c_double), _p(out, C.c_double))
+    return out
+
+
+def build_covariance(q, s):
+    q = np.ascontiguousarray(q, np.float64)
+    s = np.ascontiguousarray(s, np.float64)
+    out = np.zeros((3, 3))
+    if lib().orc_build_covariance_f64(_p(q, C.c_double), _p(s, C.c_double), _p(out, C.c_double)) != 0:
+        raise ValueError(lib().orc_last_error().decode())
+    return out
+
+
+def build_covariance_backward(q, s, g):
+    q = np.ascontiguousarray(q, np.float64)
+    s = np.ascontiguousarray(s, np.float64)
+    g = np.ascontiguousarray(g, np.float64)
+    dq = np.zeros(4)
+    ds = np.zeros(3)
+    if lib().orc_build_covariance_backward_f64(_p(q, C.c_double), _p(s, C.c_double), _p(g, C.c_double),
+                                               _p(dq, C.c_double), _p(ds, C.c_double)) != 0:
+        raise ValueError(lib().orc_last_error().decode())
+    return dq, ds
+
+
+def eval_sh(sh48, d, degree):
+    sh = np.ascontiguousarray(sh48, np.float64)
+    dd = np.ascontiguousarray(d, np.float64)
+    out = np.zeros(3)
+    lib().orc_eval_sh_f64(_p(sh, C.c_double), _p(dd, C.c_double), degree, _p(out, C.c_double))
+    return out

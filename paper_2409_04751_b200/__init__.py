@@ -1,0 +1,4 @@
+"""B200-native Fisheye-GS rasterizer."""
+from .types import (Camera, Scene, RenderOptions, RenderStats, BackwardOptions, GRAD_STRIDE, GRAD_SLICES,
+                    CAMERA_FISHEYE, CAMERA_PINHOLE, CAMERA_PANORAMA)
+from . import synthetic
