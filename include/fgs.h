@@ -1,0 +1,143 @@
+/*
+ * fgs.h — C ABI of the B200-native Fisheye-GS rasterizer (libfgs.so).
+ *
+ * Drop-in for the reference's render/backward path (omnisplat, a header-only C++ API):
+ *   render<S>(scene, camera, options) -> {image, stats, context}
+ *       /root/reference/proj/include/omnisplat/splatting.hpp:330-374
+ *   backward<S>(scene, camera, context, dL/dimage, options) -> GradientBuffer
+ *       /root/reference/proj/include/omnisplat/gradients.hpp:207-267
+ * The reference has no FFI of its own; this header is what its C++ callers (cmd_render /
+ * cmd_bench in src/cli.cpp:130,153; train in inc/optimize.hpp:247,264) bind instead, through
+ * the C++ wrapper in include/fgs.hpp. See INTEGRATION.md.
+ *
+ * Conventions
+ *  - fp32 throughout. Plain pointers + sizes; no CUDA or torch types in signatures
+ *    (streams are passed as void* = cudaStream_t).
+ *  - Scene layout (structure of arrays, one array per field, N Gaussians):
+ *      means N*3, rotations N*4 (w,x,y,z, unnormalised), log_scales N*3,
+ *      opacity_logits N, sh N*48 with per-Gaussian order [channel*16 + basis]
+ *    (= the reference's Gaussian3D fields, inc/model.hpp:18-36, ShCoeffs column-major).
+ *  - Image and dL/dimage: H*W*3 row-major RGB (ImageBuffer, inc/model.hpp:53-92).
+ *  - Gradients: five arrays matching the scene fields; pointing them at consecutive blocks of
+ *    one 59*N buffer (means, rotations, log_scales, opacities, sh) makes multi-view gradient
+ *    sums a single all-reduce.
+ *  - The forward state (ForwardContext, inc/splatting.hpp:309-321) lives in the context; one
+ *    context serves one forward/backward pair at a time. Contexts are not thread-safe.
+ *  - Errors are status codes; the C++ wrapper rethrows the reference's exception types.
+ */
+#ifndef FGS_H_
+#define FGS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  FGS_OK = 0,
+  FGS_EINVAL = 1,             /* bad shape / context-camera-scene mismatch (std::invalid_argument) */
+  FGS_EDEGENERATE_QUAT = 2,   /* zero-norm quaternion (inc/model.hpp:98, "degenerate rotation") */
+  FGS_ECUDA = 3,              /* CUDA runtime error */
+  FGS_ENOMEM = 4,             /* device allocation failed */
+  FGS_ESTATE = 5              /* backward without a matching forward */
+};
+
+enum { FGS_CAMERA_PINHOLE = 0, FGS_CAMERA_FISHEYE = 1, FGS_CAMERA_PANORAMA = 2 };
+
+/* Camera (inc/cameras.hpp:29-74). Only FGS_CAMERA_FISHEYE is implemented on the GPU path. */
+typedef struct fgs_camera {
+  int32_t model;
+  int32_t width, height;
+  float fx, fy, cx, cy;
+  float rotation_wc[9];    /* row-major, world -> camera */
+  float translation_wc[3];
+  float fov_max;           /* culling half-angle; culled beyond fov_max + 10 deg */
+} fgs_camera;
+
+typedef struct fgs_gaussians {
+  int64_t n;
+  const float* means;
+  const float* rotations;
+  const float* log_scales;
+  const float* opacity_logits;
+  const float* sh;
+} fgs_gaussians;
+
+typedef struct fgs_gradients {
+  float* d_means;            /* N*3 */
+  float* d_rotations;        /* N*4 */
+  float* d_log_scales;       /* N*3 */
+  float* d_opacity_logits;   /* N   */
+  float* d_sh;               /* N*48 */
+} fgs_gradients;
+
+/* RenderOptions (inc/splatting.hpp:50-55). */
+typedef struct fgs_render_options {
+  int32_t sh_degree;         /* 0..3 */
+  int32_t use_background;    /* 0: scene background = black (the reference Scene default) */
+  float background[3];
+} fgs_render_options;
+
+/* BackwardOptions (inc/gradients.hpp:57-63) plus build switches. */
+typedef struct fgs_backward_options {
+  float jacobian_grad_scale[3]; /* mutation hook; {1,1,1} normally */
+  int32_t full_sh;              /* 1: all 48 SH gradients; 0: DC only (reference) */
+  int32_t accumulate;           /* 1: add into the gradient arrays (multi-view sums) */
+} fgs_backward_options;
+
+/* RenderStats (inc/splatting.hpp:41-48); stage times from CUDA events. */
+typedef struct fgs_stats {
+  uint64_t num_intersections;
+  uint32_t num_splats, num_culled, num_degenerate;
+  double preprocess_ms, binning_ms, sort_ms, raster_ms;
+  uint64_t peak_aux_bytes;
+} fgs_stats;
+
+typedef struct fgs_context fgs_context;
+
+int fgs_create(int device, fgs_context** out);
+int fgs_destroy(fgs_context* ctx);
+/* Stream for all subsequent work (cudaStream_t; NULL = legacy default stream). */
+int fgs_set_stream(fgs_context* ctx, void* stream);
+const char* fgs_last_error(const fgs_context* ctx);
+
+/* Device-resident forward: all pointers are device memory. `radii` (N int32, 0 = culled or
+ * degenerate) and `stats` may be NULL; a non-NULL `stats` synchronises the stream. */
+int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats);
+
+/* Device-resident backward for the last forward of this context. */
+int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                 const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
+
+/* Host-buffer variants with the reference's calling convention: inputs and outputs in host
+ * memory, host<->device copies included; blocking. */
+int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                    const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats);
+int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                      const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
+
+/* Flags: FGS_FLAG_COUNTERS makes the forward blend count E_eval / E_contrib (atomics; slower);
+ * FGS_FLAG_KEEP_KEYS keeps what "key_*" exports need. Default 0. */
+enum { FGS_FLAG_COUNTERS = 1, FGS_FLAG_KEEP_KEYS = 2 };
+int fgs_set_flags(fgs_context* ctx, uint32_t flags);
+
+/* Parity/debug export of the last forward's state into host memory. Names:
+ *   "state" int32[N] (0 culled, 1 kept, 2 degenerate), "mean_px" f32[N*2], "conic" f32[N*3],
+ *   "depth" f32[N], "radius" int32[N], "color" f32[N*3], "alpha" f32[N],
+ *   "key_tile"/"key_depth"/"key_gauss" u32[I] (pre-sort keys, reference emission order),
+ *   "sorted_gauss" u32[I], "sorted_tile" u32[I], "sorted_depth" u32[I], "offsets" u32[T+1],
+ *   "final_T" f32[H*W], "last" u32[H*W], "counters" u64[4] (E_eval, E_contrib, 0, 0).
+ * Returns the number of bytes (dst may be NULL to query), or -1 for an unknown name. */
+int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst_bytes);
+
+/* Counters of the last forward: [n, num_splats, num_intersections, tiles_x, tiles_y, width, height,
+ * num_culled, num_degenerate]. */
+int fgs_last_counts(const fgs_context* ctx, int64_t out[9]);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FGS_H_ */

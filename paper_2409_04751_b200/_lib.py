@@ -1,0 +1,85 @@
+"""ctypes binding of the C ABI in include/fgs.h (libfgs.so, built in-tree).
+
+There is no fallback: if the library is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfgs.so")
+
+FGS_OK, FGS_EINVAL, FGS_EDEGENERATE_QUAT, FGS_ECUDA, FGS_ENOMEM, FGS_ESTATE = range(6)
+FGS_FLAG_COUNTERS, FGS_FLAG_KEEP_KEYS = 1, 2
+
+
+class fgs_camera(C.Structure):
+    _fields_ = [("model", C.c_int32), ("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_float),
+                ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float), ("rotation_wc", C.c_float * 9),
+                ("translation_wc", C.c_float * 3), ("fov_max", C.c_float)]
+
+
+class fgs_gaussians(C.Structure):
+    _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("rotations", C.c_void_p), ("log_scales", C.c_void_p),
+                ("opacity_logits", C.c_void_p), ("sh", C.c_void_p)]
+
+
+class fgs_gradients(C.Structure):
+    _fields_ = [("d_means", C.c_void_p), ("d_rotations", C.c_void_p), ("d_log_scales", C.c_void_p),
+                ("d_opacity_logits", C.c_void_p), ("d_sh", C.c_void_p)]
+
+
+class fgs_render_options(C.Structure):
+    _fields_ = [("sh_degree", C.c_int32), ("use_background", C.c_int32), ("background", C.c_float * 3)]
+
+
+class fgs_backward_options(C.Structure):
+    _fields_ = [("jacobian_grad_scale", C.c_float * 3), ("full_sh", C.c_int32), ("accumulate", C.c_int32)]
+
+
+class fgs_stats(C.Structure):
+    _fields_ = [("num_intersections", C.c_uint64), ("num_splats", C.c_uint32), ("num_culled", C.c_uint32),
+                ("num_degenerate", C.c_uint32), ("preprocess_ms", C.c_double), ("binning_ms", C.c_double),
+                ("sort_ms", C.c_double), ("raster_ms", C.c_double), ("peak_aux_bytes", C.c_uint64)]
+
+
+EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs_forward", "fgs_backward",
+           "fgs_render_host", "fgs_backward_host", "fgs_set_flags", "fgs_debug_get", "fgs_last_counts"]
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libfgs.so and declare its signatures. Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with `python -m paper_2409_04751_b200.build` "
+                           "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    vp, i32 = C.c_void_p, C.c_int
+    P = C.POINTER
+    L.fgs_create.argtypes = [i32, P(vp)]
+    L.fgs_create.restype = i32
+    L.fgs_destroy.argtypes = [vp]
+    L.fgs_destroy.restype = i32
+    L.fgs_set_stream.argtypes = [vp, vp]
+    L.fgs_set_stream.restype = i32
+    L.fgs_set_flags.argtypes = [vp, C.c_uint32]
+    L.fgs_set_flags.restype = i32
+    L.fgs_last_error.argtypes = [vp]
+    L.fgs_last_error.restype = C.c_char_p
+    fwd = [vp, P(fgs_gaussians), P(fgs_camera), P(fgs_render_options), vp, vp, P(fgs_stats)]
+    bwd = [vp, P(fgs_gaussians), P(fgs_camera), vp, P(fgs_backward_options), P(fgs_gradients)]
+    for name, args in (("fgs_forward", fwd), ("fgs_render_host", fwd), ("fgs_backward", bwd),
+                       ("fgs_backward_host", bwd)):
+        getattr(L, name).argtypes = args
+        getattr(L, name).restype = i32
+    L.fgs_debug_get.argtypes = [vp, C.c_char_p, vp, C.c_int64]
+    L.fgs_debug_get.restype = C.c_int64
+    L.fgs_last_counts.argtypes = [vp, P(C.c_int64)]
+    L.fgs_last_counts.restype = i32
+    _lib = L
+    return L

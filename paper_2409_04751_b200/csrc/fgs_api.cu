@@ -1,0 +1,560 @@
+// fgs_api.cu — the C ABI (include/fgs.h): context, device memory, stage orchestration.
+//
+// Forward (reference render, inc/splatting.hpp:330-374):
+//   K1 preprocess -> level-1 onesweep sort of Gaussians by depth key -> rank scan
+//   -> [one 8-byte D2H read of the intersection count + error flag]
+//   -> duplicate (depth-rank order) -> level-2 onesweep sort by tile -> tile ranges -> K3 blend.
+// Backward (reference backward, inc/gradients.hpp:207-267):
+//   K4a reverse blend (per-intersection partials) -> K4b preprocess backward.
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fgs.h"
+#include "fgs_kernels.h"
+
+namespace {
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = n + n / 4 + 64;
+    cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return e;
+    }
+    cap = want;
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct fgs_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t flags = 0;
+  std::string err;
+
+  // per Gaussian
+  DevBuf<float4> rec0, rec1;
+  DevBuf<float> rec2;
+  DevBuf<uint8_t> state;
+  DevBuf<uint32_t> dkey, dkey_a, dkey_b, iota, perm_a, perm_b, touched, rank, offsets, block_sums;
+  DevBuf<ushort4> rect;
+  DevBuf<int32_t> radii;
+  // per intersection
+  DevBuf<uint32_t> tkey, emit, tkey_a, tkey_b, emit_a, emit_b, emit_gauss, sorted_gauss;
+  DevBuf<float> partials;
+  // per tile / pixel
+  DevBuf<uint32_t> tile_offsets, last;
+  DevBuf<float> final_T;
+  // sort scratch
+  DevBuf<uint32_t> hist, lookback, sort_counters;
+  // misc device scalars: [0] total I, [1] error flag, [2..3] state counts
+  DevBuf<uint32_t> scalars;
+  DevBuf<unsigned long long> counters;
+  uint32_t* h_scalars = nullptr;  // pinned
+  // host-call staging
+  DevBuf<float> h_means, h_rot, h_ls, h_op, h_sh, h_img, h_dl, h_grad;
+  DevBuf<int32_t> h_radii;
+  cudaEvent_t ev[5] = {};
+
+  // last forward
+  bool have_fwd = false;
+  int64_t n = 0;
+  fgs_camera cam{};
+  int sh_degree = 3;
+  float bg[3] = {0, 0, 0};
+  fgs::DevCamera dcam{};
+  int tiles_x = 0, tiles_y = 0;
+  int64_t num_isect = 0;
+  uint32_t num_splats = 0, num_degenerate = 0, num_culled = 0;
+  uint32_t* perm = nullptr;          // level-1 result values
+  uint32_t* sorted_tiles = nullptr;  // level-2 result keys
+  uint32_t* sorted_emit = nullptr;   // level-2 result values
+  size_t aux_bytes = 0;
+};
+
+namespace {
+
+int fail(fgs_context* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(fgs_context* c, cudaError_t e, const char* where) {
+  return fail(c, e == cudaErrorMemoryAllocation ? FGS_ENOMEM : FGS_ECUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define FGS_CHECK(expr)                                   \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr); \
+  } while (0)
+
+fgs::DevCamera make_dev_camera(const fgs_camera& c) {
+  fgs::DevCamera d{};
+  d.width = c.width;
+  d.height = c.height;
+  d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy;
+  for (int i = 0; i < 9; ++i) d.W[i] = c.rotation_wc[i];
+  for (int i = 0; i < 3; ++i) d.b[i] = c.translation_wc[i];
+  d.fov_max = c.fov_max;
+  // center = -W^T b (inc/cameras.hpp:60), summed left to right in float, no contraction
+  for (int r = 0; r < 3; ++r) {
+    volatile float acc = (-c.rotation_wc[0 * 3 + r]) * c.translation_wc[0];
+    volatile float t1 = (-c.rotation_wc[1 * 3 + r]) * c.translation_wc[1];
+    acc = acc + t1;
+    volatile float t2 = (-c.rotation_wc[2 * 3 + r]) * c.translation_wc[2];
+    acc = acc + t2;
+    d.center[r] = acc;
+  }
+  return d;
+}
+
+bool same_camera(const fgs_camera& a, const fgs_camera& b) {
+  // the fields the reference compares (inc/gradients.hpp:213-217)
+  if (a.model != b.model || a.width != b.width || a.height != b.height || a.fx != b.fx || a.fy != b.fy ||
+      a.cx != b.cx || a.cy != b.cy)
+    return false;
+  for (int i = 0; i < 9; ++i)
+    if (a.rotation_wc[i] != b.rotation_wc[i]) return false;
+  for (int i = 0; i < 3; ++i)
+    if (a.translation_wc[i] != b.translation_wc[i]) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fgs_create(int device, fgs_context** out) {
+  if (!out) return FGS_EINVAL;
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return FGS_ECUDA;
+  auto* ctx = new fgs_context();
+  ctx->device = device;
+  e = cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
+  if (e != cudaSuccess) {
+    delete ctx;
+    return FGS_ECUDA;
+  }
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(4) != cudaSuccess ||
+      ctx->hist.ensure(4 * 256) != cudaSuccess || ctx->sort_counters.ensure(8) != cudaSuccess) {
+    fgs_destroy(ctx);
+    return FGS_ENOMEM;
+  }
+  *out = ctx;
+  return FGS_OK;
+}
+
+int fgs_destroy(fgs_context* ctx) {
+  if (!ctx) return FGS_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  else cudaDeviceSynchronize();
+  for (auto* b : {&ctx->rec2, &ctx->final_T, &ctx->partials, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
+                  &ctx->h_sh, &ctx->h_img, &ctx->h_dl, &ctx->h_grad})
+    b->release();
+  ctx->rec0.release();
+  ctx->rec1.release();
+  ctx->state.release();
+  for (auto* b : {&ctx->dkey, &ctx->dkey_a, &ctx->dkey_b, &ctx->iota, &ctx->perm_a, &ctx->perm_b, &ctx->touched,
+                  &ctx->rank, &ctx->offsets, &ctx->block_sums, &ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b,
+                  &ctx->emit_a, &ctx->emit_b, &ctx->emit_gauss, &ctx->sorted_gauss, &ctx->tile_offsets, &ctx->last,
+                  &ctx->hist, &ctx->lookback, &ctx->sort_counters, &ctx->scalars})
+    b->release();
+  ctx->rect.release();
+  ctx->radii.release();
+  ctx->h_radii.release();
+  ctx->counters.release();
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
+  delete ctx;
+  return FGS_OK;
+}
+
+int fgs_set_stream(fgs_context* ctx, void* stream) {
+  if (!ctx) return FGS_EINVAL;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return FGS_OK;
+}
+
+int fgs_set_flags(fgs_context* ctx, uint32_t flags) {
+  if (!ctx) return FGS_EINVAL;
+  ctx->flags = flags;
+  return FGS_OK;
+}
+
+const char* fgs_last_error(const fgs_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int fgs_last_counts(const fgs_context* ctx, int64_t out[9]) {
+  if (!ctx || !out) return FGS_EINVAL;
+  out[0] = ctx->n;
+  out[1] = ctx->num_splats;
+  out[2] = ctx->num_isect;
+  out[3] = ctx->tiles_x;
+  out[4] = ctx->tiles_y;
+  out[5] = ctx->cam.width;
+  out[6] = ctx->cam.height;
+  out[7] = ctx->num_culled;
+  out[8] = ctx->num_degenerate;
+  return FGS_OK;
+}
+
+int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
+  if (!ctx) return FGS_EINVAL;
+  if (!scene || !camera || !image) return fail(ctx, FGS_EINVAL, "forward: null argument");
+  if (camera->model != FGS_CAMERA_FISHEYE)
+    return fail(ctx, FGS_EINVAL, "forward: only the equidistant fisheye camera is implemented on the GPU path");
+  if (camera->width <= 0 || camera->height <= 0) return fail(ctx, FGS_EINVAL, "forward: empty image");
+  const int sh_degree = options ? options->sh_degree : 3;
+  if (sh_degree < 0 || sh_degree > 3) return fail(ctx, FGS_EINVAL, "forward: sh_degree must be 0..3");
+  const int64_t n = scene->n;
+  if (n < 0 || n >= (int64_t(1) << 31)) return fail(ctx, FGS_EINVAL, "forward: scene size out of range");
+  if (n > 0 && (!scene->means || !scene->rotations || !scene->log_scales || !scene->opacity_logits || !scene->sh))
+    return fail(ctx, FGS_EINVAL, "forward: null scene array");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  ctx->have_fwd = false;
+
+  const int W = camera->width, H = camera->height;
+  const int tiles_x = (W + fgs::kTile - 1) / fgs::kTile, tiles_y = (H + fgs::kTile - 1) / fgs::kTile;
+  const int num_tiles = tiles_x * tiles_y;
+  const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
+  const size_t npix = static_cast<size_t>(W) * H;
+  FGS_CHECK(ctx->rec0.ensure(nn));
+  FGS_CHECK(ctx->rec1.ensure(nn));
+  FGS_CHECK(ctx->rec2.ensure(nn));
+  FGS_CHECK(ctx->state.ensure(nn));
+  for (auto* b : {&ctx->dkey, &ctx->dkey_a, &ctx->dkey_b, &ctx->iota, &ctx->perm_a, &ctx->perm_b, &ctx->touched,
+                  &ctx->rank, &ctx->offsets})
+    FGS_CHECK(b->ensure(nn));
+  FGS_CHECK(ctx->block_sums.ensure(nn / 1024 + 2));
+  FGS_CHECK(ctx->rect.ensure(nn));
+  FGS_CHECK(ctx->radii.ensure(nn));
+  FGS_CHECK(ctx->tile_offsets.ensure(num_tiles + 1));
+  FGS_CHECK(ctx->last.ensure(npix));
+  FGS_CHECK(ctx->final_T.ensure(npix));
+  FGS_CHECK(ctx->lookback.ensure(static_cast<size_t>(4) * 256 * (nn / fgs::kSortTile + 1)));
+
+  ctx->n = n;
+  ctx->cam = *camera;
+  ctx->sh_degree = sh_degree;
+  for (int k = 0; k < 3; ++k) ctx->bg[k] = (options && options->use_background) ? options->background[k] : 0.0f;
+  ctx->dcam = make_dev_camera(*camera);
+  ctx->tiles_x = tiles_x;
+  ctx->tiles_y = tiles_y;
+
+  fgs::SortScratch ss{ctx->hist.p, ctx->lookback.p, ctx->sort_counters.p, 0};
+  const bool timing = stats != nullptr;
+  if (timing) cudaEventRecord(ctx->ev[0], st);
+
+  FGS_CHECK(cudaMemsetAsync(ctx->scalars.p, 0, 16 * sizeof(uint32_t), st));
+  if (ctx->flags & FGS_FLAG_COUNTERS) FGS_CHECK(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), st));
+  if (n > 0) {
+    fgs::PreprocessArgs pa{};
+    pa.n = n;
+    pa.cam = ctx->dcam;
+    pa.sh_degree = sh_degree;
+    pa.tiles_x = tiles_x;
+    pa.tiles_y = tiles_y;
+    pa.means = scene->means;
+    pa.rotations = scene->rotations;
+    pa.log_scales = scene->log_scales;
+    pa.opacity = scene->opacity_logits;
+    pa.sh = scene->sh;
+    pa.rec0 = ctx->rec0.p;
+    pa.rec1 = ctx->rec1.p;
+    pa.rec2 = ctx->rec2.p;
+    pa.state = ctx->state.p;
+    pa.depth_key = ctx->dkey.p;
+    pa.gauss_iota = ctx->iota.p;
+    pa.touched = ctx->touched.p;
+    pa.rect = ctx->rect.p;
+    pa.radii = ctx->radii.p;
+    pa.error_flag = reinterpret_cast<int*>(ctx->scalars.p + 1);
+    pa.state_counts = ctx->scalars.p + 2;
+    fgs::preprocess_kernel<<<fgs::div_up(static_cast<int>(n), 256), 256, 0, st>>>(pa);
+  }
+  if (timing) cudaEventRecord(ctx->ev[1], st);
+  // level 1: Gaussians by depth key (stable; ties keep source order)
+  const fgs::SortResult l1 = fgs::radix_sort_pairs(ctx->dkey.p, ctx->iota.p, ctx->dkey_a.p, ctx->perm_a.p,
+                                                   ctx->dkey_b.p, ctx->perm_b.p, static_cast<int>(n), 4, ss, st);
+  ctx->perm = l1.vals;
+  if (n > 0)
+    fgs::rank_scan(ctx->perm, ctx->touched.p, ctx->offsets.p, ctx->rank.p, ctx->block_sums.p, ctx->scalars.p,
+                   static_cast<int>(n), st);
+  FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, ctx->scalars.p, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  FGS_CHECK(cudaStreamSynchronize(st));
+  FGS_CHECK(cudaGetLastError());
+  if (ctx->h_scalars[1]) return fail(ctx, FGS_EDEGENERATE_QUAT, "degenerate rotation: quaternion has zero norm");
+  const int64_t I = ctx->h_scalars[0];
+  ctx->num_isect = I;
+  ctx->num_splats = ctx->h_scalars[2];
+  ctx->num_degenerate = ctx->h_scalars[3];
+  ctx->num_culled = static_cast<uint32_t>(n) - ctx->num_splats - ctx->num_degenerate;
+  if (I >= (int64_t(1) << 30)) return fail(ctx, FGS_ENOMEM, "forward: intersection count exceeds 2^30");
+
+  const size_t ni = static_cast<size_t>(I > 0 ? I : 1);
+  for (auto* b : {&ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b, &ctx->emit_a, &ctx->emit_b, &ctx->emit_gauss,
+                  &ctx->sorted_gauss})
+    FGS_CHECK(b->ensure(ni));
+  FGS_CHECK(ctx->lookback.ensure(static_cast<size_t>(4) * 256 * (ni / fgs::kSortTile + 1)));
+  ss.lookback = ctx->lookback.p;
+  if (n > 0)
+    fgs::duplicate(ctx->perm, ctx->offsets.p, ctx->touched.p, ctx->rect.p, tiles_x, ctx->tkey.p, ctx->emit.p,
+                   ctx->emit_gauss.p, static_cast<int>(n), st);
+  if (timing) cudaEventRecord(ctx->ev[2], st);
+  const int passes2 = num_tiles <= 256 ? 1 : (num_tiles <= 65536 ? 2 : 3);
+  const fgs::SortResult l2 = fgs::radix_sort_pairs(ctx->tkey.p, ctx->emit.p, ctx->tkey_a.p, ctx->emit_a.p,
+                                                   ctx->tkey_b.p, ctx->emit_b.p, static_cast<int>(I), passes2, ss, st);
+  ctx->sorted_tiles = l2.keys;
+  ctx->sorted_emit = l2.vals;
+  fgs::tile_ranges(ctx->sorted_tiles, ctx->sorted_emit, ctx->emit_gauss.p, ctx->tile_offsets.p, ctx->sorted_gauss.p,
+                   static_cast<int>(I), num_tiles, st);
+  if (timing) cudaEventRecord(ctx->ev[3], st);
+
+  fgs::BlendArgs ba{};
+  ba.width = W;
+  ba.height = H;
+  ba.tiles_x = tiles_x;
+  ba.tiles_y = tiles_y;
+  ba.tile_offsets = ctx->tile_offsets.p;
+  ba.sorted_gauss = ctx->sorted_gauss.p;
+  ba.sorted_emit = ctx->sorted_emit;
+  ba.rec = {ctx->rec0.p, ctx->rec1.p, ctx->rec2.p};
+  for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
+  ba.image = image;
+  ba.final_T = ctx->final_T.p;
+  ba.last = ctx->last.p;
+  ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
+  fgs::blend_forward(ba, st);
+  if (radii && n > 0) FGS_CHECK(cudaMemcpyAsync(radii, ctx->radii.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+  if (timing) cudaEventRecord(ctx->ev[4], st);
+  FGS_CHECK(cudaGetLastError());
+
+  ctx->aux_bytes = nn * (16 + 16 + 4 + 1 + 4 * 9 + 8 + 4) + ni * 4 * 8 + (num_tiles + 1) * 4 + npix * 8;
+  ctx->have_fwd = true;
+  if (stats) {
+    FGS_CHECK(cudaEventSynchronize(ctx->ev[4]));
+    float ms[4];
+    for (int s = 0; s < 4; ++s) cudaEventElapsedTime(&ms[s], ctx->ev[s], ctx->ev[s + 1]);
+    stats->num_intersections = static_cast<uint64_t>(I);
+    stats->num_splats = ctx->num_splats;
+    stats->num_culled = ctx->num_culled;
+    stats->num_degenerate = ctx->num_degenerate;
+    stats->preprocess_ms = ms[0];
+    stats->binning_ms = ms[1];
+    stats->sort_ms = ms[2];
+    stats->raster_ms = ms[3];
+    stats->peak_aux_bytes = ctx->aux_bytes;
+  }
+  return FGS_OK;
+}
+
+int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, const float* dl_dimage,
+                 const fgs_backward_options* options, fgs_gradients* grads) {
+  if (!ctx) return FGS_EINVAL;
+  if (!scene || !camera || !dl_dimage || !grads) return fail(ctx, FGS_EINVAL, "backward: null argument");
+  if (!ctx->have_fwd) return fail(ctx, FGS_ESTATE, "backward: no forward context");
+  if (scene->n != ctx->n) return fail(ctx, FGS_EINVAL, "backward: forward context was built for a different scene");
+  if (!same_camera(*camera, ctx->cam))
+    return fail(ctx, FGS_EINVAL, "backward: forward context was built for a different camera");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int64_t n = ctx->n, I = ctx->num_isect;
+  if (n == 0) return FGS_OK;
+  FGS_CHECK(ctx->partials.ensure(static_cast<size_t>(I > 0 ? I : 1) * 9));
+
+  fgs::BlendArgs ba{};
+  ba.width = ctx->cam.width;
+  ba.height = ctx->cam.height;
+  ba.tiles_x = ctx->tiles_x;
+  ba.tiles_y = ctx->tiles_y;
+  ba.tile_offsets = ctx->tile_offsets.p;
+  ba.sorted_gauss = ctx->sorted_gauss.p;
+  ba.sorted_emit = ctx->sorted_emit;
+  ba.rec = {ctx->rec0.p, ctx->rec1.p, ctx->rec2.p};
+  for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
+  ba.final_T = ctx->final_T.p;
+  ba.last = ctx->last.p;
+  ba.dl_dimage = dl_dimage;
+  ba.partials = ctx->partials.p;
+  if (I > 0) fgs::blend_backward(ba, st);
+
+  fgs::PreprocessBackwardArgs pb{};
+  pb.n = n;
+  pb.cam = ctx->dcam;
+  pb.sh_degree = ctx->sh_degree;
+  pb.full_sh = options ? options->full_sh : 1;
+  pb.accumulate = options ? options->accumulate : 0;
+  for (int k = 0; k < 3; ++k) pb.jac_grad_scale[k] = options ? options->jacobian_grad_scale[k] : 1.0f;
+  pb.means = scene->means;
+  pb.rotations = scene->rotations;
+  pb.log_scales = scene->log_scales;
+  pb.opacity = scene->opacity_logits;
+  pb.sh = scene->sh;
+  pb.state = ctx->state.p;
+  pb.touched = ctx->touched.p;
+  pb.rank = ctx->rank.p;
+  pb.offsets = ctx->offsets.p;
+  pb.partials = ctx->partials.p;
+  pb.d_means = grads->d_means;
+  pb.d_rotations = grads->d_rotations;
+  pb.d_log_scales = grads->d_log_scales;
+  pb.d_opacity = grads->d_opacity_logits;
+  pb.d_sh = grads->d_sh;
+  fgs::preprocess_backward_kernel<<<fgs::div_up(static_cast<int>(n), 128), 128, 0, st>>>(pb);
+  FGS_CHECK(cudaGetLastError());
+  return FGS_OK;
+}
+
+int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                    const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
+  if (!ctx) return FGS_EINVAL;
+  if (!scene || !camera || !image) return fail(ctx, FGS_EINVAL, "render: null argument");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const size_t n = static_cast<size_t>(scene->n > 0 ? scene->n : 0), nn = n ? n : 1;
+  const size_t npix = static_cast<size_t>(camera->width) * camera->height;
+  FGS_CHECK(ctx->h_means.ensure(nn * 3));
+  FGS_CHECK(ctx->h_rot.ensure(nn * 4));
+  FGS_CHECK(ctx->h_ls.ensure(nn * 3));
+  FGS_CHECK(ctx->h_op.ensure(nn));
+  FGS_CHECK(ctx->h_sh.ensure(nn * 48));
+  FGS_CHECK(ctx->h_img.ensure(npix * 3));
+  FGS_CHECK(ctx->h_radii.ensure(nn));
+  if (n) {
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_means.p, scene->means, n * 3 * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_rot.p, scene->rotations, n * 4 * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_ls.p, scene->log_scales, n * 3 * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_op.p, scene->opacity_logits, n * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_sh.p, scene->sh, n * 48 * 4, cudaMemcpyHostToDevice, st));
+  }
+  fgs_gaussians dev{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
+  int rc = fgs_forward(ctx, &dev, camera, options, ctx->h_img.p, radii ? ctx->h_radii.p : nullptr, stats);
+  if (rc != FGS_OK) return rc;
+  FGS_CHECK(cudaMemcpyAsync(image, ctx->h_img.p, npix * 3 * 4, cudaMemcpyDeviceToHost, st));
+  if (radii && n) FGS_CHECK(cudaMemcpyAsync(radii, ctx->h_radii.p, n * 4, cudaMemcpyDeviceToHost, st));
+  FGS_CHECK(cudaStreamSynchronize(st));
+  return FGS_OK;
+}
+
+int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, const float* dl_dimage,
+                      const fgs_backward_options* options, fgs_gradients* grads) {
+  if (!ctx) return FGS_EINVAL;
+  if (!scene || !camera || !dl_dimage || !grads) return fail(ctx, FGS_EINVAL, "backward: null argument");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const size_t n = static_cast<size_t>(ctx->n), nn = n ? n : 1;
+  const size_t npix = static_cast<size_t>(camera->width) * camera->height;
+  if (static_cast<int64_t>(n) != scene->n)
+    return fail(ctx, FGS_EINVAL, "backward: forward context was built for a different scene");
+  // The scene arrays were uploaded by the matching fgs_render_host call; re-upload only if the
+  // caller's pointers differ is not knowable, so upload again (the reference takes the scene
+  // by value on every call).
+  if (n) {
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_means.p, scene->means, n * 3 * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_rot.p, scene->rotations, n * 4 * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_ls.p, scene->log_scales, n * 3 * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_op.p, scene->opacity_logits, n * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_sh.p, scene->sh, n * 48 * 4, cudaMemcpyHostToDevice, st));
+  }
+  FGS_CHECK(ctx->h_dl.ensure(npix * 3));
+  FGS_CHECK(ctx->h_grad.ensure(nn * 59));
+  FGS_CHECK(cudaMemcpyAsync(ctx->h_dl.p, dl_dimage, npix * 3 * 4, cudaMemcpyHostToDevice, st));
+  float* g = ctx->h_grad.p;
+  fgs_gradients dg{g, g + 3 * nn, g + 7 * nn, g + 10 * nn, g + 11 * nn};
+  const bool acc = options && options->accumulate;
+  if (acc && n) {
+    FGS_CHECK(cudaMemcpyAsync(dg.d_means, grads->d_means, n * 3 * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(dg.d_rotations, grads->d_rotations, n * 4 * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(dg.d_log_scales, grads->d_log_scales, n * 3 * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(dg.d_opacity_logits, grads->d_opacity_logits, n * 4, cudaMemcpyHostToDevice, st));
+    FGS_CHECK(cudaMemcpyAsync(dg.d_sh, grads->d_sh, n * 48 * 4, cudaMemcpyHostToDevice, st));
+  }
+  fgs_gaussians dev{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
+  int rc = fgs_backward(ctx, &dev, camera, ctx->h_dl.p, options, &dg);
+  if (rc != FGS_OK) return rc;
+  if (n) {
+    FGS_CHECK(cudaMemcpyAsync(grads->d_means, dg.d_means, n * 3 * 4, cudaMemcpyDeviceToHost, st));
+    FGS_CHECK(cudaMemcpyAsync(grads->d_rotations, dg.d_rotations, n * 4 * 4, cudaMemcpyDeviceToHost, st));
+    FGS_CHECK(cudaMemcpyAsync(grads->d_log_scales, dg.d_log_scales, n * 3 * 4, cudaMemcpyDeviceToHost, st));
+    FGS_CHECK(cudaMemcpyAsync(grads->d_opacity_logits, dg.d_opacity_logits, n * 4, cudaMemcpyDeviceToHost, st));
+    FGS_CHECK(cudaMemcpyAsync(grads->d_sh, dg.d_sh, n * 48 * 4, cudaMemcpyDeviceToHost, st));
+  }
+  FGS_CHECK(cudaStreamSynchronize(st));
+  return FGS_OK;
+}
+
+int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst_bytes) {
+  if (!ctx || !name || !ctx->have_fwd) return -1;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return -1;
+  cudaStream_t st = ctx->stream;
+  const std::string nm(name);
+  const size_t n = static_cast<size_t>(ctx->n), I = static_cast<size_t>(ctx->num_isect);
+  const size_t npix = static_cast<size_t>(ctx->cam.width) * ctx->cam.height;
+  const size_t nt = static_cast<size_t>(ctx->tiles_x) * ctx->tiles_y;
+  auto copy = [&](const void* src, size_t bytes) -> int64_t {
+    if (!dst) return static_cast<int64_t>(bytes);
+    if (static_cast<int64_t>(bytes) > dst_bytes) return -1;
+    if (bytes && cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) return -1;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
+    return static_cast<int64_t>(bytes);
+  };
+  if (nm == "state_u8") return copy(ctx->state.p, n);
+  if (nm == "rec0") return copy(ctx->rec0.p, n * 16);
+  if (nm == "rec1") return copy(ctx->rec1.p, n * 16);
+  if (nm == "rec2") return copy(ctx->rec2.p, n * 4);
+  if (nm == "depth_key") return copy(ctx->dkey.p, n * 4);
+  if (nm == "radius") return copy(ctx->radii.p, n * 4);
+  if (nm == "touched") return copy(ctx->touched.p, n * 4);
+  if (nm == "perm") return copy(ctx->perm, n * 4);
+  if (nm == "rank") return copy(ctx->rank.p, n * 4);
+  if (nm == "rank_offsets") return copy(ctx->offsets.p, n * 4);
+  if (nm == "sorted_gauss") return copy(ctx->sorted_gauss.p, I * 4);
+  if (nm == "sorted_tile") return copy(ctx->sorted_tiles, I * 4);
+  if (nm == "sorted_emit") return copy(ctx->sorted_emit, I * 4);
+  if (nm == "offsets") return copy(ctx->tile_offsets.p, (nt + 1) * 4);
+  if (nm == "final_T") return copy(ctx->final_T.p, npix * 4);
+  if (nm == "last") return copy(ctx->last.p, npix * 4);
+  if (nm == "counters") return copy(ctx->counters.p, 2 * sizeof(unsigned long long));
+  if (nm == "key_tile" || nm == "key_depth" || nm == "key_gauss") {
+    if (!dst) return static_cast<int64_t>(I * 4);
+    // Recompute the reference's pre-sort emission order (source order) on demand.
+    DevBuf<uint32_t> kt, kd, kg, off, bs, tot;
+    if (kt.ensure(I + 1) || kd.ensure(I + 1) || kg.ensure(I + 1) || off.ensure(n + 1) || bs.ensure(n / 1024 + 2) ||
+        tot.ensure(1))
+      return -1;
+    fgs::debug_source_order_keys(ctx->touched.p, ctx->rect.p, ctx->dkey.p, ctx->tiles_x, static_cast<int>(n), off.p,
+                                 bs.p, tot.p, kt.p, kd.p, kg.p, st);
+    const uint32_t* src = nm == "key_tile" ? kt.p : (nm == "key_depth" ? kd.p : kg.p);
+    const int64_t r = copy(src, I * 4);
+    for (auto* b : {&kt, &kd, &kg, &off, &bs, &tot}) b->release();
+    return r;
+  }
+  return -1;
+}
+
+}  // extern "C"

@@ -1,0 +1,530 @@
+// preprocess.cu — K1 (fisheye preprocess) and K4b (preprocess backward), sm_100a.
+//
+// Compiled with --fmad=false: every expression below is evaluated in the reference's
+// operation order with IEEE-rounded fp32 ops (division and sqrt are IEEE by default), so the
+// per-Gaussian outputs (pixel mean, radius, depth, conic, colour, alpha) are bit-identical to
+// the oracle's parity mode (oracle/fgs_oracle.cpp), and hence the tile/depth keys are too.
+// atan2f/expf use the correctly rounded definition (double evaluation, one rounding).
+//
+// Reference: /root/reference/proj/include/omnisplat/
+//   preprocess            splatting.hpp:68-139
+//   project (fisheye)     cameras.hpp:139-177, fisheye_terms :99-128, jacobian :180-212
+//   build_covariance      model.hpp:95-140; eval_sh model.hpp:187-215; sigmoid core.hpp:30-36
+//   backward per splat    gradients.hpp:226-264, covariance_projection_backward :186-202,
+//                         projection_jacobian_grad cameras.hpp:217-271,
+//                         build_covariance_backward model.hpp:144-171
+
+#include "fgs_common.cuh"
+#include "fgs_kernels.h"
+
+namespace fgs {
+
+namespace {
+
+constexpr double kC0 = 0.28209479177387814;
+constexpr double kC1 = 0.4886025119029199;
+constexpr double kC2_0 = 1.0925484305920792, kC2_1 = -1.0925484305920792, kC2_2 = 0.31539156525252005,
+                 kC2_3 = -1.0925484305920792, kC2_4 = 0.5462742152960396;
+constexpr double kC3_0 = -0.5900435899266435, kC3_1 = 2.890611442640554, kC3_2 = -0.4570457994644658,
+                 kC3_3 = 0.3731763325901154, kC3_4 = -0.4570457994644658, kC3_5 = 1.445305721320277,
+                 kC3_6 = -0.5900435899266435;
+
+struct Terms {
+  float g, u, U;
+};
+
+// cameras.hpp:107-128 (AxisMode::Auto)
+__device__ __forceinline__ Terms fisheye_terms(float lz2, float z) {
+  const float z2 = z * z;
+  Terms t;
+  if (z > 0.0f && lz2 < kFisheyeSeriesW2 * z2) {
+    const float w2 = lz2 / z2;
+    const float z3 = z2 * z, z5 = z3 * z2;
+    t.g = (1.0f - w2 / 3.0f + w2 * w2 / 5.0f - w2 * w2 * w2 / 7.0f) / z;
+    t.u = (-2.0f / 3.0f + 4.0f / 5.0f * w2 - 6.0f / 7.0f * w2 * w2) / z3;
+    t.U = (8.0f / 5.0f - 24.0f / 7.0f * w2 + 16.0f / 3.0f * w2 * w2) / z5;
+  } else {
+    const float lz = sqrtf(lz2);
+    const float r2 = lz2 + z2;
+    const float theta = cr_atan2f(lz, z);
+    t.g = theta / lz;
+    t.u = z / (lz2 * r2) - theta / (lz2 * lz);
+    t.U = 3.0f * theta / (lz2 * lz2 * lz) - z / (r2 * lz2 * lz2) - 2.0f * z * (r2 + lz2) / (lz2 * lz2 * r2 * r2);
+  }
+  return t;
+}
+
+// cameras.hpp:191-198
+__device__ __forceinline__ void fisheye_jacobian(const float p[3], const DevCamera& cam, float j[2][3]) {
+  const float x = p[0], y = p[1], z = p[2];
+  const float lz2 = x * x + y * y;
+  const float r2 = lz2 + z * z;
+  const Terms t = fisheye_terms(lz2, z);
+  const float fx = cam.fx, fy = cam.fy;
+  j[0][0] = fx * (t.g + x * x * t.u);
+  j[0][1] = fx * x * y * t.u;
+  j[0][2] = -fx * x / r2;
+  j[1][0] = fy * x * y * t.u;
+  j[1][1] = fy * (t.g + y * y * t.u);
+  j[1][2] = -fy * y / r2;
+}
+
+// cameras.hpp:232-247
+__device__ __forceinline__ void fisheye_jacobian_grad(const float p[3], const DevCamera& cam, float d[3][2][3]) {
+  const float x = p[0], y = p[1], z = p[2];
+  const float lz2 = x * x + y * y;
+  const float r2 = lz2 + z * z;
+  const float ir4 = 1.0f / (r2 * r2);
+  const Terms t = fisheye_terms(lz2, z);
+  const float fx = cam.fx, fy = cam.fy;
+  const float x2 = x * x, y2 = y * y;
+  const float ux = t.u + x2 * t.U;
+  const float uy = t.u + y2 * t.U;
+  d[0][0][0] = fx * x * (3.0f * t.u + x2 * t.U); d[0][0][1] = fx * y * ux; d[0][0][2] = fx * (2.0f * x2 - r2) * ir4;
+  d[0][1][0] = fy * y * ux; d[0][1][1] = fy * x * uy; d[0][1][2] = 2.0f * fy * x * y * ir4;
+  d[1][0][0] = fx * y * ux; d[1][0][1] = fx * x * uy; d[1][0][2] = 2.0f * fx * x * y * ir4;
+  d[1][1][0] = fy * x * uy; d[1][1][1] = fy * y * (3.0f * t.u + y2 * t.U); d[1][1][2] = fy * (2.0f * y2 - r2) * ir4;
+  d[2][0][0] = fx * (2.0f * x2 - r2) * ir4; d[2][0][1] = 2.0f * fx * x * y * ir4; d[2][0][2] = 2.0f * fx * x * z * ir4;
+  d[2][1][0] = 2.0f * fy * x * y * ir4; d[2][1][1] = fy * (2.0f * y2 - r2) * ir4; d[2][1][2] = 2.0f * fy * y * z * ir4;
+}
+
+// cameras.hpp:76-79
+__device__ __forceinline__ void world_to_camera(const DevCamera& cam, const float m[3], float mu[3]) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r) mu[r] = cam.W[r * 3 + 0] * m[0] + cam.W[r * 3 + 1] * m[1] + cam.W[r * 3 + 2] * m[2] + cam.b[r];
+}
+
+// model.hpp:95-106; returns false for a zero-norm quaternion
+__device__ __forceinline__ bool quat_to_rot(const float4 q, float r[3][3]) {
+  const float n2 = q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w;
+  if (!(n2 > 0.0f)) return false;
+  const float n = sqrtf(n2);
+  const float w = q.x / n, x = q.y / n, y = q.z / n, z = q.w / n;
+  r[0][0] = 1.0f - 2.0f * (y * y + z * z); r[0][1] = 2.0f * (x * y - w * z); r[0][2] = 2.0f * (x * z + w * y);
+  r[1][0] = 2.0f * (x * y + w * z); r[1][1] = 1.0f - 2.0f * (x * x + z * z); r[1][2] = 2.0f * (y * z - w * x);
+  r[2][0] = 2.0f * (x * z - w * y); r[2][1] = 2.0f * (y * z + w * x); r[2][2] = 1.0f - 2.0f * (x * x + y * y);
+  return true;
+}
+
+// model.hpp:127-140
+__device__ __forceinline__ bool build_covariance(const float4 q, const float s[3], float sigma[3][3]) {
+  float r[3][3];
+  if (!quat_to_rot(q, r)) return false;
+  const float sc[3] = {cr_expf(s[0]), cr_expf(s[1]), cr_expf(s[2])};
+  float m[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) m[i][j] = r[i][j] * sc[j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = i; j < 3; ++j) {
+      const float v = m[i][0] * m[j][0] + m[i][1] * m[j][1] + m[i][2] * m[j][2];
+      sigma[i][j] = v;
+      sigma[j][i] = v;
+    }
+  return true;
+}
+
+// core.hpp:30-36
+__device__ __forceinline__ float sigmoid(float x) {
+  if (x >= 0.0f) return 1.0f / (1.0f + cr_expf(-x));
+  const float e = cr_expf(x);
+  return e / (1.0f + e);
+}
+
+// model.hpp:187-215 — SH basis factors Y[j] in the reference's association order.
+__device__ __forceinline__ void sh_basis(const float d[3], int degree, float Y[16]) {
+  const float x = d[0], y = d[1], z = d[2];
+  Y[0] = float(kC0);
+  if (degree >= 1) {
+    Y[1] = -float(kC1) * y; Y[2] = float(kC1) * z; Y[3] = -float(kC1) * x;
+  }
+  if (degree >= 2) {
+    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    Y[4] = float(kC2_0) * xy; Y[5] = float(kC2_1) * yz; Y[6] = float(kC2_2) * (2.0f * zz - xx - yy);
+    Y[7] = float(kC2_3) * xz; Y[8] = float(kC2_4) * (xx - yy);
+    if (degree >= 3) {
+      Y[9] = float(kC3_0) * y * (3.0f * xx - yy);
+      Y[10] = float(kC3_1) * xy * z;
+      Y[11] = float(kC3_2) * y * (4.0f * zz - xx - yy);
+      Y[12] = float(kC3_3) * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+      Y[13] = float(kC3_4) * x * (4.0f * zz - xx - yy);
+      Y[14] = float(kC3_5) * z * (xx - yy);
+      Y[15] = float(kC3_6) * x * (xx - yy);
+    }
+  }
+}
+
+// Colour for one channel: reference grouping (C0*s0) + ((Y1 s1 + Y2 s2) - (C1 x) s3) + ...
+// Y[3] = (-C1) x = -(C1 x) exactly, so "a - (C1 x) s3" == "a + Y3 s3" bit for bit.
+__device__ __forceinline__ float sh_channel(const float* k, const float Y[16], int degree) {
+  float v = Y[0] * k[0];
+  if (degree >= 1) {
+    const float t1 = Y[1] * k[1] + Y[2] * k[2] + Y[3] * k[3];
+    v = v + t1;
+    if (degree >= 2) {
+      const float t2 = Y[4] * k[4] + Y[5] * k[5] + Y[6] * k[6] + Y[7] * k[7] + Y[8] * k[8];
+      v = v + t2;
+      if (degree >= 3) {
+        const float t3 = Y[9] * k[9] + Y[10] * k[10] + Y[11] * k[11] + Y[12] * k[12] + Y[13] * k[13] +
+                         Y[14] * k[14] + Y[15] * k[15];
+        v = v + t3;
+      }
+    }
+  }
+  v = v + 0.5f;
+  return fmaxf(v, 0.0f);
+}
+
+__device__ __forceinline__ void load_sh(const float* __restrict__ sh, int64_t g, int degree, float k[48]) {
+  const float* p = sh + g * 48;
+  if (degree == 0) {
+    k[0] = __ldg(p);
+    k[16] = __ldg(p + 16);
+    k[32] = __ldg(p + 32);
+    return;
+  }
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    const float4 v = __ldg(p4 + i);
+    k[4 * i + 0] = v.x; k[4 * i + 1] = v.y; k[4 * i + 2] = v.z; k[4 * i + 3] = v.w;
+  }
+}
+
+__device__ __forceinline__ void view_dir(const DevCamera& cam, const float m[3], float dir[3]) {
+  const float v0 = m[0] - cam.center[0], v1 = m[1] - cam.center[1], v2 = m[2] - cam.center[2];
+  const float n2 = v0 * v0 + v1 * v1 + v2 * v2;
+  dir[0] = v0; dir[1] = v1; dir[2] = v2;
+  if (n2 > 0.0f) {
+    const float n = sqrtf(n2);
+    dir[0] = v0 / n; dir[1] = v1 / n; dir[2] = v2 / n;
+  }
+}
+
+__device__ __forceinline__ uint32_t depth_key_bits(float d) {
+  const uint32_t u = __float_as_uint(d);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// Projected covariance + conic for a visible Gaussian: returns 0 kept-candidate, 2 degenerate.
+struct Proj {
+  float mu[3];
+  float pix[2];
+  float j[2][3];
+  float t[2][3];
+  float sigma[3][3];
+  float sp[2][2];
+  float det;
+};
+
+// splatting.hpp:83-97. Returns -1 invisible, 2 degenerate, 1 ok, 3 zero quaternion.
+__device__ __forceinline__ int project_covariance(const DevCamera& cam, const float m[3], const float4 q,
+                                                  const float ls[3], Proj& P) {
+  world_to_camera(cam, m, P.mu);
+  const float x = P.mu[0], y = P.mu[1], z = P.mu[2];
+  const float r2 = x * x + y * y + z * z;
+  if (r2 < 1e-24f) return -1;
+  const float lz2 = x * x + y * y;
+  if (z < 0.0f && lz2 < 1e-24f * z * z) return -1;
+  const float theta = cr_atan2f(sqrtf(lz2), z);
+  if (!(theta <= cam.fov_max + kFisheyeCullMargin)) return -1;
+  const float g = fisheye_terms(lz2, z).g;
+  P.pix[0] = cam.cx + cam.fx * g * x;
+  P.pix[1] = cam.cy + cam.fy * g * y;
+  fisheye_jacobian(P.mu, cam, P.j);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) P.t[i][c] = P.j[i][0] * cam.W[0 * 3 + c] + P.j[i][1] * cam.W[1 * 3 + c] + P.j[i][2] * cam.W[2 * 3 + c];
+  if (!build_covariance(q, ls, P.sigma)) return 3;
+  float ts[2][3];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) ts[i][c] = P.t[i][0] * P.sigma[0][c] + P.t[i][1] * P.sigma[1][c] + P.t[i][2] * P.sigma[2][c];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) P.sp[i][c] = ts[i][0] * P.t[c][0] + ts[i][1] * P.t[c][1] + ts[i][2] * P.t[c][2];
+  P.sp[0][0] += kCovarianceDilation;
+  P.sp[1][1] += kCovarianceDilation;
+  P.det = P.sp[0][0] * P.sp[1][1] - P.sp[0][1] * P.sp[1][0];
+  if (!(P.det > 0.0f)) return 2;
+  return 1;
+}
+
+}  // namespace
+
+// K1 body for one Gaussian.
+__device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t i, unsigned* s_counts) {
+  const DevCamera& cam = a.cam;
+  const float m[3] = {__ldg(a.means + 3 * i), __ldg(a.means + 3 * i + 1), __ldg(a.means + 3 * i + 2)};
+  const float4 q = __ldg(reinterpret_cast<const float4*>(a.rotations) + i);
+  const float ls[3] = {__ldg(a.log_scales + 3 * i), __ldg(a.log_scales + 3 * i + 1), __ldg(a.log_scales + 3 * i + 2)};
+
+  uint8_t state = 0;
+  uint32_t key = 0xFFFFFFFFu, touched = 0;
+  int radius = 0;
+  ushort4 rect = make_ushort4(1, 0, 1, 0);
+  float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+  float r2v = 0.f;
+
+  Proj P;
+  const int pc = project_covariance(cam, m, q, ls, P);
+  if (pc == 3) {
+    *a.error_flag = 1;
+  } else if (pc == 2) {
+    state = 2;
+  } else if (pc == 1) {
+    const float det = P.det;
+    const float mid = (P.sp[0][0] + P.sp[1][1]) / 2.0f;
+    const float lambda_max = mid + sqrtf(fmaxf(mid * mid - det, 0.0f));
+    radius = static_cast<int>(ceilf(kRadiusSigma * sqrtf(lambda_max)));
+    const float mx = P.pix[0], my = P.pix[1], rf = static_cast<float>(radius);
+    if (!(mx + rf < 0.0f || mx - rf > static_cast<float>(cam.width) || my + rf < 0.0f ||
+          my - rf > static_cast<float>(cam.height))) {
+      state = 1;
+      const float ca = P.sp[1][1] / det, cb = -P.sp[0][1] / det, cc = P.sp[0][0] / det;
+      const float depth = sqrtf(P.mu[0] * P.mu[0] + P.mu[1] * P.mu[1] + P.mu[2] * P.mu[2]);
+      float dir[3];
+      view_dir(cam, m, dir);
+      float Y[16];
+      sh_basis(dir, a.sh_degree, Y);
+      float k[48];
+      load_sh(a.sh, i, a.sh_degree, k);
+      const float col0 = sh_channel(k, Y, a.sh_degree);
+      const float col1 = sh_channel(k + 16, Y, a.sh_degree);
+      const float col2 = sh_channel(k + 32, Y, a.sh_degree);
+      const float alpha = sigmoid(__ldg(a.opacity + i));
+      r0 = make_float4(mx, my, ca, cb);
+      r1 = make_float4(cc, alpha, col0, col1);
+      r2v = col2;
+      key = depth_key_bits(depth);
+      // splatting.hpp:211-214 — inclusive, floor, clamped
+      const int tx0 = max(0, static_cast<int>(floorf((mx - rf) / 16.0f)));
+      const int tx1 = min(a.tiles_x - 1, static_cast<int>(floorf((mx + rf) / 16.0f)));
+      const int ty0 = max(0, static_cast<int>(floorf((my - rf) / 16.0f)));
+      const int ty1 = min(a.tiles_y - 1, static_cast<int>(floorf((my + rf) / 16.0f)));
+      if (tx1 >= tx0 && ty1 >= ty0) {
+        touched = static_cast<uint32_t>((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+        rect = make_ushort4(tx0, tx1, ty0, ty1);
+      }
+    }
+  }
+  a.rec0[i] = r0;
+  a.rec1[i] = r1;
+  a.rec2[i] = r2v;
+  a.state[i] = state;
+  a.depth_key[i] = key;
+  a.gauss_iota[i] = static_cast<uint32_t>(i);
+  a.touched[i] = touched;
+  a.rect[i] = rect;
+  a.radii[i] = state == 1 ? radius : 0;
+  if (state == 1) atomicAdd(s_counts, 1u);
+  if (state == 2) atomicAdd(s_counts + 1, 1u);
+}
+
+
+// K1: one thread per Gaussian.
+__global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a) {
+  __shared__ unsigned s_counts[2];
+  if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < a.n) preprocess_one(a, i, s_counts);
+  __syncthreads();
+  if (threadIdx.x < 2 && s_counts[threadIdx.x]) atomicAdd(a.state_counts + threadIdx.x, s_counts[threadIdx.x]);
+}
+
+// K4b: per Gaussian, after the blend backward wrote per-intersection partials (9 floats) at
+// their emission slots [offset[rank[g]], +touched[g]) in ascending tile order.
+__global__ void __launch_bounds__(128) preprocess_backward_kernel(PreprocessBackwardArgs a) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const uint8_t state = a.state[i];
+  float out[59];
+#pragma unroll
+  for (int k = 0; k < 59; ++k) out[k] = 0.0f;
+  if (state == 1) {
+    // gradients.hpp:161-173 — per-splat sum over tiles in ascending tile order
+    float sg[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
+    const uint32_t cnt = a.touched[i];
+    if (cnt) {
+      const uint32_t base = a.offsets[a.rank[i]];
+      for (uint32_t e = base; e < base + cnt; ++e) {
+        const float* p = a.partials + int64_t(e) * 9;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) sg[k] = sg[k] + p[k];
+      }
+    }
+    const DevCamera& cam = a.cam;
+    const float m[3] = {__ldg(a.means + 3 * i), __ldg(a.means + 3 * i + 1), __ldg(a.means + 3 * i + 2)};
+    const float4 q = __ldg(reinterpret_cast<const float4*>(a.rotations) + i);
+    const float ls[3] = {__ldg(a.log_scales + 3 * i), __ldg(a.log_scales + 3 * i + 1), __ldg(a.log_scales + 3 * i + 2)};
+    Proj P;
+    project_covariance(cam, m, q, ls, P);
+    const float det = P.det;
+    const float conic[3] = {P.sp[1][1] / det, -P.sp[0][1] / det, P.sp[0][0] / det};
+    // mean_backward (gradients.hpp:177-181): J^T dmean_px
+    float direct[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) direct[k] = P.j[0][k] * sg[0] + P.j[1][k] * sg[1];
+    // gradients.hpp:239-243: dSigma_p = (-Q) Gq Q, b-slot cotangent halved
+    const float nq[2][2] = {{-conic[0], -conic[1]}, {-conic[1], -conic[2]}};
+    const float Q[2][2] = {{conic[0], conic[1]}, {conic[1], conic[2]}};
+    const float gq[2][2] = {{sg[2], sg[3] / 2.0f}, {sg[3] / 2.0f, sg[4]}};
+    float tmp[2][2], dsp[2][2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) tmp[r][c] = nq[r][0] * gq[0][c] + nq[r][1] * gq[1][c];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) dsp[r][c] = tmp[r][0] * Q[0][c] + tmp[r][1] * Q[1][c];
+    // covariance_projection_backward (gradients.hpp:186-202)
+    float a32[3][2], dsig[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) a32[r][c] = P.t[0][r] * dsp[0][c] + P.t[1][r] * dsp[1][c];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) dsig[r][c] = a32[r][0] * P.t[0][c] + a32[r][1] * P.t[1][c];
+    const float gs[2][2] = {{dsp[0][0] + dsp[0][0], dsp[0][1] + dsp[1][0]}, {dsp[1][0] + dsp[0][1], dsp[1][1] + dsp[1][1]}};
+    float b23[2][3], dldt[2][3], dldj[2][3];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) b23[r][c] = gs[r][0] * P.t[0][c] + gs[r][1] * P.t[1][c];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) dldt[r][c] = b23[r][0] * P.sigma[0][c] + b23[r][1] * P.sigma[1][c] + b23[r][2] * P.sigma[2][c];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) dldj[r][c] = dldt[r][0] * cam.W[c * 3 + 0] + dldt[r][1] * cam.W[c * 3 + 1] + dldt[r][2] * cam.W[c * 3 + 2];
+    float dj[3][2][3];
+    fisheye_jacobian_grad(P.mu, cam, dj);
+    float cov[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      // cwiseProduct().sum() in column-major storage order
+      const float s = dldj[0][0] * dj[k][0][0] + dldj[1][0] * dj[k][1][0] + dldj[0][1] * dj[k][0][1] +
+                      dldj[1][1] * dj[k][1][1] + dldj[0][2] * dj[k][0][2] + dldj[1][2] * dj[k][1][2];
+      cov[k] = a.jac_grad_scale[k] * s;
+    }
+    // build_covariance_backward (model.hpp:144-171)
+    {
+      const float n2 = q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w;
+      const float n = sqrtf(n2);
+      const float qn[4] = {q.x / n, q.y / n, q.z / n, q.w / n};
+      float r[3][3];
+      quat_to_rot(q, r);
+      const float sc[3] = {cr_expf(ls[0]), cr_expf(ls[1]), cr_expf(ls[2])};
+      float mm[3][3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) mm[u][v] = r[u][v] * sc[v];
+      float gsym[3][3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) gsym[u][v] = dsig[u][v] + dsig[v][u];
+      float dm[3][3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) dm[u][v] = gsym[u][0] * mm[0][v] + gsym[u][1] * mm[1][v] + gsym[u][2] * mm[2][v];
+      float dr[3][3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int v = 0; v < 3; ++v) dr[u][v] = dm[u][v] * sc[v];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) out[7 + u] = sc[u] * (r[0][u] * dm[0][u] + r[1][u] * dm[1][u] + r[2][u] * dm[2][u]);
+      const float w = qn[0], x = qn[1], y = qn[2], z = qn[3];
+      // rotation_quaternion_partials (model.hpp:111-121), each entry * 2; the sum runs over
+      // the 3x3 product in column-major order (cwiseProduct().sum()).
+      auto colsum = [&](float p00, float p01, float p02, float p10, float p11, float p12, float p20, float p21,
+                        float p22) {
+        float acc = dr[0][0] * (p00 * 2.0f);
+        acc = acc + dr[1][0] * (p10 * 2.0f);
+        acc = acc + dr[2][0] * (p20 * 2.0f);
+        acc = acc + dr[0][1] * (p01 * 2.0f);
+        acc = acc + dr[1][1] * (p11 * 2.0f);
+        acc = acc + dr[2][1] * (p21 * 2.0f);
+        acc = acc + dr[0][2] * (p02 * 2.0f);
+        acc = acc + dr[1][2] * (p12 * 2.0f);
+        acc = acc + dr[2][2] * (p22 * 2.0f);
+        return acc;
+      };
+      float dqn[4];
+      dqn[0] = colsum(0.0f, -z, y, z, 0.0f, -x, -y, x, 0.0f);
+      dqn[1] = colsum(0.0f, y, z, y, -2.0f * x, -w, z, w, -2.0f * x);
+      dqn[2] = colsum(-2.0f * y, x, w, x, 0.0f, z, -w, z, -2.0f * y);
+      dqn[3] = colsum(-2.0f * z, -w, x, w, -2.0f * z, y, x, y, 0.0f);
+      const float dot = qn[0] * dqn[0] + qn[1] * dqn[1] + qn[2] * dqn[2] + qn[3] * dqn[3];
+#pragma unroll
+      for (int kq = 0; kq < 4; ++kq) out[3 + kq] = (dqn[kq] - qn[kq] * dot) / n;
+    }
+    // gradients.hpp:251-252
+    const float v[3] = {direct[0] + cov[0], direct[1] + cov[1], direct[2] + cov[2]};
+#pragma unroll
+    for (int r = 0; r < 3; ++r) out[r] = cam.W[0 * 3 + r] * v[0] + cam.W[1 * 3 + r] * v[1] + cam.W[2 * 3 + r] * v[2];
+    const float al = sigmoid(__ldg(a.opacity + i));
+    out[10] = sg[8] * al * (1.0f - al);
+    // SH: eval_sh_dc_backward (model.hpp:219-227) + higher bands (build extension)
+    float dir[3];
+    view_dir(cam, m, dir);
+    float Y[16];
+    sh_basis(dir, a.sh_degree, Y);
+    float k[48];
+    load_sh(a.sh, i, a.sh_degree, k);
+    const int nb = a.full_sh ? (a.sh_degree + 1) * (a.sh_degree + 1) : 1;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const float col = sh_channel(k + 16 * ch, Y, a.sh_degree);
+      if (!(col > 0.0f)) continue;
+      const float dc = sg[5 + ch];
+      out[11 + 16 * ch] = float(kC0) * dc;
+      for (int jb = 1; jb < nb; ++jb) out[11 + 16 * ch + jb] = Y[jb] * dc;
+    }
+  }
+  // write (field-major arrays)
+  float* dm = a.d_means + 3 * i;
+  float* drt = a.d_rotations + 4 * i;
+  float* dls = a.d_log_scales + 3 * i;
+  float* dsh = a.d_sh + 48 * i;
+  if (a.accumulate) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dm[k] += out[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) drt[k] += out[3 + k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dls[k] += out[7 + k];
+    a.d_opacity[i] += out[10];
+#pragma unroll
+    for (int k = 0; k < 48; ++k) dsh[k] += out[11 + k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dm[k] = out[k];
+    reinterpret_cast<float4*>(drt)[0] = make_float4(out[3], out[4], out[5], out[6]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dls[k] = out[7 + k];
+    a.d_opacity[i] = out[10];
+#pragma unroll
+    for (int k = 0; k < 12; ++k)
+      reinterpret_cast<float4*>(dsh)[k] = make_float4(out[11 + 4 * k], out[12 + 4 * k], out[13 + 4 * k], out[14 + 4 * k]);
+  }
+}
+
+}  // namespace fgs

@@ -1,0 +1,150 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle in parity mode.
+
+Bars (BASELINE.json north_star): tile/depth key lists, sorted order and per-tile ranges
+bit-exact; image max-abs <= 1e-3 per channel and PSNR >= 60 dB; gradients <= 1e-3 relative
+L2 per parameter group. Per-Gaussian preprocess outputs are additionally checked bit-exact.
+"""
+import numpy as np
+import pytest
+
+from tests._helpers import GROUPS, psnr, rel_l2, small_fisheye, to_device
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-3
+PSNR_MIN = 60.0
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def rast():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2409_04751_b200 import Rasterizer
+
+    return Rasterizer(0)
+
+
+def run_gpu(rast, scene, cam, deg, dl=None, full_sh=True):
+    import torch
+    from paper_2409_04751_b200 import BackwardOptions, RenderOptions, grads_as_rows
+
+    ds = to_device(scene)
+    radii = torch.zeros(scene.n, dtype=torch.int32, device="cuda")
+    img, stats = rast.forward(ds, cam, RenderOptions(sh_degree=deg, background=scene.background), radii=radii,
+                              want_stats=True)
+    torch.cuda.synchronize()
+    out = {"image": img.cpu().numpy(), "stats": stats, "radii": radii.cpu().numpy(), "splats": rast.splats(),
+           "counts": rast.counts()}
+    if dl is not None:
+        g = rast.backward(ds, cam, torch.from_numpy(dl).cuda(), BackwardOptions(full_sh=full_sh))
+        torch.cuda.synchronize()
+        out["grads"] = grads_as_rows(g, scene.n)
+    return out
+
+
+def run_oracle(oracle, scene, cam, deg, dl=None, full_sh=True):
+    res = oracle.render(scene, cam, sh_degree=deg, mode=oracle.MODE_PARITY)
+    out = {"res": res, "image": res.image}
+    if dl is not None:
+        out["grads"], _ = oracle.backward(res, scene.n, dl, full_sh=full_sh, mode=oracle.MODE_PARITY)
+    return out
+
+
+def check_preprocess(g, o, scene):
+    res = o["res"]
+    state = res.get("state")
+    np.testing.assert_array_equal(g["splats"]["state"], state)
+    src = res.get("source")
+    sp = g["splats"]
+    for name in ("mean_px", "conic", "color", "alpha", "depth"):
+        got = sp[name][src].reshape(-1)
+        ref = res.get(name).reshape(-1)
+        bad = np.flatnonzero(got.view(np.uint32) != ref.view(np.uint32))
+        assert bad.size == 0, f"{name}: {bad.size} mismatches, first {got[bad[:5]]} vs {ref[bad[:5]]}"
+    np.testing.assert_array_equal(sp["radius"][src], res.get("radius"))
+    np.testing.assert_array_equal(g["radii"][src], res.get("radius"))
+    assert (g["radii"][state != 1] == 0).all()
+
+
+def check_keys(rast, o):
+    res = o["res"]
+    src = res.get("source")
+    kt = rast.debug("key_tile")
+    kd = rast.debug("key_depth")
+    kg = rast.debug("key_gauss")
+    np.testing.assert_array_equal(kt, res.get("key_tile"))
+    np.testing.assert_array_equal(kd.astype(np.uint64), res.get("key_depth"))
+    np.testing.assert_array_equal(kg, src[res.get("key_splat")])
+    # sorted (tile, depth, source) sequence and per-tile ranges
+    np.testing.assert_array_equal(rast.debug("sorted_gauss"), src[res.get("refs")])
+    np.testing.assert_array_equal(rast.debug("offsets"), res.get("offsets"))
+    off = res.get("offsets")
+    tiles = np.repeat(np.arange(len(off) - 1, dtype=np.uint32), np.diff(off))
+    np.testing.assert_array_equal(rast.debug("sorted_tile"), tiles)
+
+
+def check_image(g, o):
+    err = np.abs(g["image"].astype(np.float64) - o["image"]).max()
+    p = psnr(g["image"], o["image"])
+    assert err <= IMG_TOL, f"image max-abs {err}"
+    assert p >= PSNR_MIN, f"PSNR {p}"
+
+
+def check_grads(g, o, groups=("mean", "rotation", "log_scale", "opacity", "sh_dc", "sh_rest")):
+    errs = {k: rel_l2(g["grads"][:, GROUPS[k]], o["grads"][:, GROUPS[k]]) for k in groups}
+    bad = {k: v for k, v in errs.items() if not v <= GRAD_TOL}
+    assert not bad, f"gradient rel-L2 over {GRAD_TOL}: {bad} (all: {errs})"
+    return errs
+
+
+def test_cfg0_forward_parity(rast, oracle_mod):
+    from paper_2409_04751_b200 import synthetic
+
+    scene, deg, cams, _ = synthetic.config(0)
+    g = run_gpu(rast, scene, cams[0], deg)
+    o = run_oracle(oracle_mod, scene, cams[0], deg)
+    check_preprocess(g, o, scene)
+    check_keys(rast, o)
+    check_image(g, o)
+    st = g["stats"]
+    assert st.num_intersections == o["res"].num_intersections
+    assert st.num_splats == o["res"].num_splats
+
+
+@pytest.mark.parametrize("cfg,n", [(1, 20000), (2, 50000)])
+def test_full_res_fwd_bwd_parity(rast, oracle_mod, cfg, n):
+    from paper_2409_04751_b200 import synthetic
+
+    scene, deg, cams, dls = synthetic.config(cfg, n=n)
+    g = run_gpu(rast, scene, cams[0], deg, dls[0])
+    o = run_oracle(oracle_mod, scene, cams[0], deg, dls[0])
+    check_preprocess(g, o, scene)
+    check_keys(rast, o)
+    check_image(g, o)
+    check_grads(g, o)
+
+
+def test_rotated_camera_parity(rast, oracle_mod):
+    from paper_2409_04751_b200 import synthetic
+
+    scene, deg, cams, dls = synthetic.config(4, n=30000, views=2)
+    for cam, dl in zip(cams, dls):
+        g = run_gpu(rast, scene, cam, deg, dl)
+        o = run_oracle(oracle_mod, scene, cam, deg, dl)
+        check_preprocess(g, o, scene)
+        check_keys(rast, o)
+        check_image(g, o)
+        check_grads(g, o)
+
+
+def test_reference_dc_only_grads(rast, oracle_mod):
+    """full_sh=False reproduces the reference's DC-only GradientBuffer layout."""
+    from paper_2409_04751_b200 import synthetic
+
+    scene, deg, cams, dls = synthetic.config(1, n=5000)
+    g = run_gpu(rast, scene, cams[0], deg, dls[0], full_sh=False)
+    o = run_oracle(oracle_mod, scene, cams[0], deg, dls[0], full_sh=False)
+    assert np.all(g["grads"][:, GROUPS["sh_rest"]] == 0)
+    check_grads(g, o, ("mean", "rotation", "log_scale", "opacity", "sh_dc"))
