@@ -84,6 +84,8 @@ typedef struct fgs_backward_options {
   float jacobian_grad_scale[3]; /* mutation hook; {1,1,1} normally */
   int32_t full_sh;              /* 1: all 48 SH gradients; 0: DC only (reference) */
   int32_t accumulate;           /* 1: add into the gradient arrays (multi-view sums) */
+  int32_t sh_view_dir_grad;     /* 1: add colour -> view direction -> mean (the reference omits it,
+                                   inc/gradients.hpp:255-262); 0 (default) = reference parity */
 } fgs_backward_options;
 
 /* RenderStats (inc/splatting.hpp:41-48); stage times from CUDA events. */

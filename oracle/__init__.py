@@ -52,7 +52,7 @@ def lib():
         for name, rp in (("orc_backward_f32", fp), ("orc_backward_f64", dp)):
             fn = getattr(L, name)
             fn.restype = i32
-            fn.argtypes = [vp, i64, rp, rp, dp, i32, i32, i32, rp]
+            fn.argtypes = [vp, i64, rp, rp, dp, i32, i32, i32, i32, rp]
         L.orc_free.argtypes = [vp]
         L.orc_sizes.argtypes = [vp, C.POINTER(C.c_int64)]
         L.orc_stats.argtypes = [vp, dp]
@@ -73,6 +73,10 @@ def lib():
         L.orc_build_covariance_backward_f64.restype = i32
         L.orc_build_covariance_backward_f64.argtypes = [dp, dp, dp, dp, dp]
         L.orc_eval_sh_f64.argtypes = [dp, dp, i32, dp]
+        L.orc_splats_render_f64.restype = vp
+        L.orc_splats_render_f64.argtypes = [i64, dp, dp, dp, C.POINTER(C.c_int32), dp, dp, i32, i32, dp, i32]
+        L.orc_splats_backward_f64.restype = i32
+        L.orc_splats_backward_f64.argtypes = [vp, dp, dp, i32]
         _lib = L
     return _lib
 
@@ -206,7 +210,7 @@ def render(scene, camera, sh_degree=3, background=None, dtype=np.float32, thread
 
 
 def backward(res: Result, n, dl_dimage, full_sh=True, jacobian_grad_scale=None, threads=0,
-             mode=MODE_PARITY, want_splat_grads=False):
+             mode=MODE_PARITY, want_splat_grads=False, sh_view_dir_grad=False):
     """Reference ``backward<S>`` (inc/gradients.hpp:207-267). Returns (grads[n,59], splat_grads
     [num_splats,9] or None)."""
     dtype = res.dtype
@@ -219,7 +223,7 @@ def backward(res: Result, n, dl_dimage, full_sh=True, jacobian_grad_scale=None, 
     if res.prefix == "orc":
         L = lib()
         fn = L.orc_backward_f32 if dtype == np.float32 else L.orc_backward_f64
-        rc = fn(res.handle, n, _p(dl, ct), _p(grads, ct), jp, int(full_sh), threads, mode,
+        rc = fn(res.handle, n, _p(dl, ct), _p(grads, ct), jp, int(full_sh), int(sh_view_dir_grad), threads, mode,
                 _p(sg, ct) if sg is not None else None)
         err = L.orc_last_error
     else:
@@ -305,4 +309,28 @@ def eval_sh(sh48, d, degree):
     dd = np.ascontiguousarray(d, np.float64)
     out = np.zeros(3)
     lib().orc_eval_sh_f64(_p(sh, C.c_double), _p(dd, C.c_double), degree, _p(out, C.c_double))
+    return out
+
+
+def splats_render(mean_px, conic, depth, radius, color, alpha, width, height, background=(0, 0, 0), threads=0):
+    """bin_and_sort + rasterize (inc/splatting.hpp:196-306) over explicit splats, in double."""
+    f = lambda a, k: np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1, k) if k > 1 else np.asarray(a, np.float64).reshape(-1))
+    m, c, d, col, al = f(mean_px, 2), f(conic, 3), f(depth, 1), f(color, 3), f(alpha, 1)
+    r = np.ascontiguousarray(radius, np.int32).reshape(-1)
+    bg = np.asarray(background, np.float64)
+    dp = C.c_double
+    L = lib()
+    h = L.orc_splats_render_f64(len(r), _p(m, dp), _p(c, dp), _p(d, dp), _p(r, C.c_int32), _p(col, dp), _p(al, dp),
+                                width, height, _p(bg, dp), threads)
+    sz = np.zeros(7, np.int64)
+    L.orc_sizes(h, sz.ctypes.data_as(C.POINTER(C.c_int64)))
+    return Result(h, np.float64, int(sz[0]), int(sz[1]), int(sz[2]), int(sz[3]), int(sz[4]), int(sz[5]), int(sz[6]))
+
+
+def splats_backward(res: Result, dl_dimage, threads=0):
+    """rasterize_backward (inc/gradients.hpp:69-175) -> (num_splats, 9) splat gradients."""
+    dl = np.ascontiguousarray(dl_dimage, np.float64).reshape(-1)
+    out = np.zeros((res.num_splats, 9))
+    if lib().orc_splats_backward_f64(res.handle, _p(dl, C.c_double), _p(out, C.c_double), threads) != 0:
+        raise OracleError(lib().orc_last_error().decode())
     return out

@@ -470,6 +470,35 @@ inline void eval_sh(const S* sh, const S dir[3], int degree, S out[3], S* basis 
   }
 }
 
+// Build extension (not in the reference): d colour_c / d dir for the SH view-direction
+// path, dY_j/d(x, y, z) of the basis above. Used only when sh_view_dir_grad is on.
+template <typename S>
+inline void sh_basis_grad(const S dir[3], int degree, S dY[16][3]) {
+  const S x = dir[0], y = dir[1], z = dir[2];
+  for (int j = 0; j < 16; ++j) dY[j][0] = dY[j][1] = dY[j][2] = S(0);
+  if (degree < 1) return;
+  const S c1 = S(kC1);
+  dY[1][1] = -c1; dY[2][2] = c1; dY[3][0] = -c1;
+  if (degree < 2) return;
+  const S a0 = S(kC2[0]), a1 = S(kC2[1]), a2 = S(kC2[2]), a3 = S(kC2[3]), a4 = S(kC2[4]);
+  dY[4][0] = a0 * y; dY[4][1] = a0 * x;
+  dY[5][1] = a1 * z; dY[5][2] = a1 * y;
+  dY[6][0] = S(-2) * a2 * x; dY[6][1] = S(-2) * a2 * y; dY[6][2] = S(4) * a2 * z;
+  dY[7][0] = a3 * z; dY[7][2] = a3 * x;
+  dY[8][0] = S(2) * a4 * x; dY[8][1] = S(-2) * a4 * y;
+  if (degree < 3) return;
+  const S b0 = S(kC3[0]), b1 = S(kC3[1]), b2 = S(kC3[2]), b3 = S(kC3[3]), b4 = S(kC3[4]), b5 = S(kC3[5]),
+          b6 = S(kC3[6]);
+  const S xx = x * x, yy = y * y, zz = z * z;
+  dY[9][0] = S(6) * b0 * x * y; dY[9][1] = b0 * (S(3) * xx - S(3) * yy);
+  dY[10][0] = b1 * y * z; dY[10][1] = b1 * x * z; dY[10][2] = b1 * x * y;
+  dY[11][0] = S(-2) * b2 * x * y; dY[11][1] = b2 * (S(4) * zz - xx - S(3) * yy); dY[11][2] = S(8) * b2 * y * z;
+  dY[12][0] = S(-6) * b3 * x * z; dY[12][1] = S(-6) * b3 * y * z; dY[12][2] = b3 * (S(6) * zz - S(3) * xx - S(3) * yy);
+  dY[13][0] = b4 * (S(4) * zz - S(3) * xx - yy); dY[13][1] = S(-2) * b4 * x * y; dY[13][2] = S(8) * b4 * x * z;
+  dY[14][0] = S(2) * b5 * x * z; dY[14][1] = S(-2) * b5 * y * z; dY[14][2] = b5 * (xx - yy);
+  dY[15][0] = b6 * (S(3) * xx - yy); dY[15][1] = S(-2) * b6 * x * y;
+}
+
 // inc/core.hpp:30-36
 template <typename S>
 inline S sigmoid(S x) {
@@ -847,7 +876,7 @@ constexpr int kGradStride = 59;  // mean 3, rotation 4, log_scale 3, opacity 1, 
 // inc/gradients.hpp:207-267. full_sh != 0 adds the 45 higher-band SH gradients (not in
 // the reference, which returns DC only: inc/gradients.hpp:262, inc/model.hpp:219-227).
 template <typename S>
-void backward(const Ctx<S>& c, const S* dl, S* grads, const S jgs[3], int full_sh, int threads,
+void backward(const Ctx<S>& c, const S* dl, S* grads, const S jgs[3], int full_sh, int view_dir, int threads,
               std::vector<SplatGrad<S>>* sg_out) {
   std::vector<SplatGrad<S>> sg;
   rasterize_backward(c, dl, sg, threads);
@@ -915,6 +944,22 @@ void backward(const Ctx<S>& c, const S* dl, S* grads, const S jgs[3], int full_s
       if (!(color[ch] > S(0))) continue;                        // inc/model.hpp:224-225
       g[11 + ch * 16 + 0] = S(kC0) * sg[i].color[ch];
       for (int jb = 1; jb < nb; ++jb) g[11 + ch * 16 + jb] = basis[jb] * sg[i].color[ch];
+    }
+    if (view_dir && c.sh_degree > 0 && vn2 > S(0)) {
+      // colour -> dir -> mean (omitted by the reference, inc/gradients.hpp:255-262)
+      S dY[16][3];
+      sh_basis_grad(dir, c.sh_degree, dY);
+      const int nbd = (c.sh_degree + 1) * (c.sh_degree + 1);
+      S ddir[3] = {0, 0, 0};
+      for (int ch = 0; ch < 3; ++ch) {
+        if (!(color[ch] > S(0))) continue;
+        const S* k = &c.scene.sh[src * 48 + ch * 16];
+        for (int jb = 1; jb < nbd; ++jb)
+          for (int a = 0; a < 3; ++a) ddir[a] += sg[i].color[ch] * k[jb] * dY[jb][a];
+      }
+      const S nrm = std::sqrt(vn2);
+      const S dd = dir[0] * ddir[0] + dir[1] * ddir[1] + dir[2] * ddir[2];
+      for (int a = 0; a < 3; ++a) g[a] += (ddir[a] - dir[a] * dd) / nrm;
     }
   }, threads);
   if (sg_out) sg_out->swap(sg);
@@ -1217,7 +1262,7 @@ int64_t orc_get(void* h, const char* name, void* dst) {
 // Returns 0 on success, -1 on error (orc_last_error()).
 #define ORC_BACKWARD_IMPL(S, NAME)                                                                      \
   int NAME(void* h, int64_t n, const S* dl_dimage, S* grads, const double* jac_grad_scale, int full_sh, \
-           int threads, int mode, S* splat_grads) {                                                     \
+           int view_dir, int threads, int mode, S* splat_grads) {                                       \
     auto* a = static_cast<AnyCtx*>(h);                                                                  \
     if (!a || a->is_double != (sizeof(S) == 8)) { g_err = "backward: context precision mismatch"; return -1; } \
     auto* c = static_cast<Ctx<S>*>(a->p);                                                               \
@@ -1227,7 +1272,7 @@ int64_t orc_get(void* h, const char* name, void* dst) {
                       S(jac_grad_scale ? jac_grad_scale[2] : 1.0)};                                     \
     try {                                                                                               \
       std::vector<SplatGrad<S>> sg;                                                                     \
-      backward(*c, dl_dimage, grads, jgs, full_sh, threads, &sg);                                       \
+      backward(*c, dl_dimage, grads, jgs, full_sh, view_dir, threads, &sg);                                       \
       if (splat_grads)                                                                                  \
         for (size_t i = 0; i < sg.size(); ++i) {                                                        \
           S* o = splat_grads + i * 9;                                                                   \
@@ -1314,6 +1359,53 @@ int orc_build_covariance_backward_f64(const double* q, const double* s, const do
 }
 void orc_eval_sh_f64(const double* sh48, const double* dir, int degree, double* out3) {
   eval_sh(sh48, dir, degree, out3);
+}
+
+// Splat-level entry (the reference tests' hand-built Splat2D lists, e.g. simple_splat in
+// tests/test_splatting.cpp:44-54): bin_and_sort + rasterize over given splats, double precision.
+void* orc_splats_render_f64(int64_t nv, const double* mean_px, const double* conic, const double* depth,
+                            const int32_t* radius, const double* color, const double* alpha, int width, int height,
+                            const double* bg, int threads) {
+  auto* c = new Ctx<double>();
+  c->cam.model = CAM_PINHOLE;
+  c->cam.width = width;
+  c->cam.height = height;
+  c->scene.n = nv;
+  for (int k = 0; k < 3; ++k) c->bg[k] = bg ? bg[k] : 0.0;
+  for (int64_t i = 0; i < nv; ++i) {
+    Splat<double> s;
+    s.mean_px[0] = mean_px[2 * i]; s.mean_px[1] = mean_px[2 * i + 1];
+    for (int k = 0; k < 3; ++k) { s.conic[k] = conic[3 * i + k]; s.color[k] = color[3 * i + k]; }
+    s.depth = depth[i];
+    s.radius = radius[i];
+    s.alpha = alpha[i];
+    s.source = static_cast<int>(i);
+    c->splats.push_back(s);
+    c->cam_points.insert(c->cam_points.end(), {0.0, 0.0, 1.0});
+  }
+  c->state.assign(nv, 1);
+  bin_and_sort(*c);
+  rasterize(*c, threads);
+  auto* a = new AnyCtx();
+  a->is_double = 1;
+  a->p = c;
+  return a;
+}
+
+// rasterize_backward only (inc/gradients.hpp:69-175): splat_grads num_splats x 9.
+int orc_splats_backward_f64(void* h, const double* dl, double* splat_grads, int threads) {
+  auto* a = static_cast<AnyCtx*>(h);
+  if (!a || !a->is_double) { g_err = "precision mismatch"; return -1; }
+  auto* c = static_cast<Ctx<double>*>(a->p);
+  std::vector<SplatGrad<double>> sg;
+  rasterize_backward(*c, dl, sg, threads);
+  for (size_t i = 0; i < sg.size(); ++i) {
+    double* o = splat_grads + i * 9;
+    o[0] = sg[i].mean_px[0]; o[1] = sg[i].mean_px[1];
+    for (int k = 0; k < 3; ++k) { o[2 + k] = sg[i].conic[k]; o[5 + k] = sg[i].color[k]; }
+    o[8] = sg[i].alpha;
+  }
+  return 0;
 }
 
 }  // extern "C"

@@ -35,7 +35,8 @@ class fgs_render_options(C.Structure):
 
 
 class fgs_backward_options(C.Structure):
-    _fields_ = [("jacobian_grad_scale", C.c_float * 3), ("full_sh", C.c_int32), ("accumulate", C.c_int32)]
+    _fields_ = [("jacobian_grad_scale", C.c_float * 3), ("full_sh", C.c_int32), ("accumulate", C.c_int32),
+                ("sh_view_dir_grad", C.c_int32)]
 
 
 class fgs_stats(C.Structure):

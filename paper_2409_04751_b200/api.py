@@ -67,6 +67,7 @@ def _backward_options(opts: Optional[BackwardOptions], accumulate: bool) -> _lib
         o.jacobian_grad_scale[k] = float(opts.jacobian_grad_scale[k])
     o.full_sh = 1 if opts.full_sh else 0
     o.accumulate = 1 if accumulate else 0
+    o.sh_view_dir_grad = 1 if opts.sh_view_dir_grad else 0
     return o
 
 

@@ -409,6 +409,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.sh_degree = ctx->sh_degree;
   pb.full_sh = options ? options->full_sh : 1;
   pb.accumulate = options ? options->accumulate : 0;
+  pb.view_dir = options ? options->sh_view_dir_grad : 0;
   for (int k = 0; k < 3; ++k) pb.jac_grad_scale[k] = options ? options->jacobian_grad_scale[k] : 1.0f;
   pb.means = scene->means;
   pb.rotations = scene->rotations;

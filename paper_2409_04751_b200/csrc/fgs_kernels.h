@@ -37,6 +37,7 @@ struct PreprocessBackwardArgs {
   int sh_degree;
   int full_sh;
   int accumulate;
+  int view_dir;
   float jac_grad_scale[3];
   const float* means;
   const float* rotations;

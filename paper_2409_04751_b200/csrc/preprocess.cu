@@ -178,6 +178,34 @@ __device__ __forceinline__ float sh_channel(const float* k, const float Y[16], i
   return fmaxf(v, 0.0f);
 }
 
+// d colour / d dir for one channel (SH view-direction path, build extension), accumulated
+// into ddir: sum_j k_j * dY_j/d(x,y,z) * dcolour.
+__device__ __forceinline__ void sh_dir_grad(const float d[3], int degree, const float* k, float dc, float ddir[3]) {
+  const float x = d[0], y = d[1], z = d[2];
+  const float c1 = float(kC1);
+  float gx = -c1 * k[3], gy = -c1 * k[1], gz = c1 * k[2];
+  if (degree >= 2) {
+    const float a0 = float(kC2_0), a1 = float(kC2_1), a2 = float(kC2_2), a3 = float(kC2_3), a4 = float(kC2_4);
+    gx += a0 * y * k[4] - 2.0f * a2 * x * k[6] + a3 * z * k[7] + 2.0f * a4 * x * k[8];
+    gy += a0 * x * k[4] + a1 * z * k[5] - 2.0f * a2 * y * k[6] - 2.0f * a4 * y * k[8];
+    gz += a1 * y * k[5] + 4.0f * a2 * z * k[6] + a3 * x * k[7];
+    if (degree >= 3) {
+      const float b0 = float(kC3_0), b1 = float(kC3_1), b2 = float(kC3_2), b3 = float(kC3_3), b4 = float(kC3_4),
+                  b5 = float(kC3_5), b6 = float(kC3_6);
+      const float xx = x * x, yy = y * y, zz = z * z;
+      gx += 6.0f * b0 * x * y * k[9] + b1 * y * z * k[10] - 2.0f * b2 * x * y * k[11] - 6.0f * b3 * x * z * k[12] +
+            b4 * (4.0f * zz - 3.0f * xx - yy) * k[13] + 2.0f * b5 * x * z * k[14] + b6 * (3.0f * xx - yy) * k[15];
+      gy += b0 * (3.0f * xx - 3.0f * yy) * k[9] + b1 * x * z * k[10] + b2 * (4.0f * zz - xx - 3.0f * yy) * k[11] -
+            6.0f * b3 * y * z * k[12] - 2.0f * b4 * x * y * k[13] - 2.0f * b5 * y * z * k[14] - 2.0f * b6 * x * y * k[15];
+      gz += b1 * x * y * k[10] + 8.0f * b2 * y * z * k[11] + b3 * (6.0f * zz - 3.0f * xx - 3.0f * yy) * k[12] +
+            8.0f * b4 * x * z * k[13] + b5 * (xx - yy) * k[14];
+    }
+  }
+  ddir[0] += gx * dc;
+  ddir[1] += gy * dc;
+  ddir[2] += gz * dc;
+}
+
 __device__ __forceinline__ void load_sh(const float* __restrict__ sh, int64_t g, int degree, float k[48]) {
   const float* p = sh + g * 48;
   if (degree == 0) {
@@ -490,13 +518,27 @@ __global__ void __launch_bounds__(128) preprocess_backward_kernel(PreprocessBack
     float k[48];
     load_sh(a.sh, i, a.sh_degree, k);
     const int nb = a.full_sh ? (a.sh_degree + 1) * (a.sh_degree + 1) : 1;
+    float ddir[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
       const float col = sh_channel(k + 16 * ch, Y, a.sh_degree);
       if (!(col > 0.0f)) continue;
       const float dc = sg[5 + ch];
       out[11 + 16 * ch] = float(kC0) * dc;
-      for (int jb = 1; jb < nb; ++jb) out[11 + 16 * ch + jb] = Y[jb] * dc;
+#pragma unroll
+      for (int jb = 1; jb < 16; ++jb)
+        if (jb < nb) out[11 + 16 * ch + jb] = Y[jb] * dc;
+      if (a.view_dir && a.sh_degree > 0) sh_dir_grad(dir, a.sh_degree, k + 16 * ch, dc, ddir);
+    }
+    if (a.view_dir && a.sh_degree > 0) {
+      // colour -> view direction -> mean (not in the reference; opt-in)
+      const float v0 = m[0] - cam.center[0], v1 = m[1] - cam.center[1], v2 = m[2] - cam.center[2];
+      const float nrm = sqrtf(v0 * v0 + v1 * v1 + v2 * v2);
+      if (nrm > 0.0f) {
+        const float dd = dir[0] * ddir[0] + dir[1] * ddir[1] + dir[2] * ddir[2];
+#pragma unroll
+        for (int q2 = 0; q2 < 3; ++q2) out[q2] += (ddir[q2] - dir[q2] * dd) / nrm;
+      }
     }
   }
   // write (field-major arrays)

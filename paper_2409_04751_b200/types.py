@@ -153,7 +153,10 @@ class BackwardOptions:
 
     ``jacobian_grad_scale`` is the reference's mutation hook. ``full_sh`` (default on)
     returns all 48 SH gradients; off reproduces the reference's DC-only buffer.
+    ``sh_view_dir_grad`` (default off, for reference parity) adds the colour -> view-direction
+    -> mean term the reference omits (gradients.hpp:255-262).
     """
 
     jacobian_grad_scale: tuple = (1.0, 1.0, 1.0)
     full_sh: bool = True
+    sh_view_dir_grad: bool = False

@@ -1,0 +1,181 @@
+"""GPU edge cases and API behaviour through the C ABI (reference error semantics, empty and
+all-culled scenes, ragged image sizes, determinism, multi-view accumulation, host path)."""
+import math
+
+import numpy as np
+import pytest
+
+from tests._helpers import GROUPS, rel_l2, small_fisheye, to_device
+from tests.golden.make_golden import spherical_scene
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rast():
+    import torch
+
+    assert torch.cuda.is_available()
+    from paper_2409_04751_b200 import Rasterizer
+
+    return Rasterizer(0)
+
+
+def fwd(rast, scene, cam, deg=3):
+    import torch
+    from paper_2409_04751_b200 import RenderOptions
+
+    img, st = rast.forward(to_device(scene), cam, RenderOptions(sh_degree=deg, background=scene.background),
+                           want_stats=True)
+    torch.cuda.synchronize()
+    return img.cpu().numpy(), st
+
+
+def test_empty_scene_is_background(rast):  # test_splatting.cpp:191-199
+    from paper_2409_04751_b200 import Scene
+
+    sc = Scene(np.zeros((0, 3), np.float32), np.zeros((0, 4), np.float32), np.zeros((0, 3), np.float32),
+               np.zeros(0, np.float32), np.zeros((0, 48), np.float32), np.array([0.3, 0.5, 0.7], np.float32))
+    img, st = fwd(rast, sc, small_fisheye(48, 32))
+    assert st.num_intersections == 0
+    assert (img == np.array([0.3, 0.5, 0.7], np.float32)).all()
+
+
+def test_all_culled_scene(rast):
+    sc = spherical_scene(100, 2)
+    sc.means[:] = np.array([0, 0, -5.0], np.float32)  # on the backward axis
+    img, st = fwd(rast, sc, small_fisheye())
+    assert st.num_intersections == 0 and st.num_splats == 0 and st.num_culled == 100
+    assert (img == sc.background).all()
+
+
+def test_degenerate_quaternion_raises(rast):  # model.hpp:98
+    from paper_2409_04751_b200 import InvalidArgument
+
+    sc = spherical_scene(200, 3)
+    cam = small_fisheye()
+    import oracle
+
+    res = oracle.render(sc, cam)
+    i = int(res.get("source")[0])
+    sc.rotations[i] = 0
+    with pytest.raises(InvalidArgument, match="degenerate rotation"):
+        fwd(rast, sc, cam)
+
+
+def test_backward_rejects_mismatched_context(rast):  # test_gradients.cpp:287-299
+    import torch
+    from paper_2409_04751_b200 import InvalidArgument
+
+    sc = spherical_scene(300, 4)
+    cam = small_fisheye()
+    fwd(rast, sc, cam)
+    dl = torch.zeros((cam.height, cam.width, 3), device="cuda")
+    with pytest.raises(InvalidArgument, match="different scene"):
+        rast.backward(to_device(sc.subset(slice(0, 299))), cam, dl)
+    cam2 = small_fisheye()
+    cam2.fx += 1.0
+    with pytest.raises(InvalidArgument, match="different camera"):
+        rast.backward(to_device(sc), cam2, dl)
+    with pytest.raises(InvalidArgument, match="shape"):
+        rast.backward(to_device(sc), cam, torch.zeros((2, 2, 3), device="cuda"))
+
+
+@pytest.mark.parametrize("wh", [(256, 256), (100, 37), (17, 16), (1752, 1168)])
+def test_ragged_sizes_and_tile_edges(rast, oracle_mod, wh):
+    """W, H multiples of 16 exercise the zero-tile splat (mx - r == W passes the cull,
+    splatting.hpp:107-108 / 211-214); odd sizes exercise partial edge tiles."""
+    w, h = wh
+    sc = spherical_scene(3000, 5)
+    cam = small_fisheye(w, h)
+    img, st = fwd(rast, sc, cam)
+    res = oracle_mod.render(sc, cam, sh_degree=3)
+    assert st.num_intersections == res.num_intersections and st.num_splats == res.num_splats
+    np.testing.assert_array_equal(rast.debug("offsets"), res.get("offsets"))
+    assert np.abs(img.astype(np.float64) - res.image).max() <= 1e-3
+
+
+def test_forward_and_backward_are_deterministic(rast):
+    import torch
+    from paper_2409_04751_b200 import BackwardOptions, RenderOptions
+
+    from paper_2409_04751_b200 import synthetic
+
+    sc, deg, cams, dls = synthetic.config(2, n=60000)
+    ds = to_device(sc)
+    dl = torch.from_numpy(dls[0]).cuda()
+    outs = []
+    for _ in range(3):
+        img, _ = rast.forward(ds, cams[0], RenderOptions(sh_degree=deg))
+        g = rast.backward(ds, cams[0], dl, BackwardOptions())
+        torch.cuda.synchronize()
+        outs.append((img.cpu().numpy().tobytes(), g.cpu().numpy().tobytes()))
+    assert outs[0] == outs[1] == outs[2]
+
+
+def test_multiview_accumulate_equals_sum(rast):
+    import torch
+    from paper_2409_04751_b200 import BackwardOptions, RenderOptions, synthetic
+
+    sc, deg, cams, dls = synthetic.config(4, n=20000, views=3)
+    ds = to_device(sc)
+    acc = torch.zeros(59 * sc.n, device="cuda")
+    singles = []
+    for i, (c, d) in enumerate(zip(cams, dls)):
+        rast.forward(ds, c, RenderOptions(sh_degree=deg))
+        dl = torch.from_numpy(d).cuda()
+        rast.backward(ds, c, dl, BackwardOptions(), grads=acc, accumulate=i > 0)
+        rast.forward(ds, c, RenderOptions(sh_degree=deg))
+        singles.append(rast.backward(ds, c, dl, BackwardOptions()).double())
+    torch.cuda.synchronize()
+    ref = sum(singles)
+    assert (torch.linalg.norm(acc.double() - ref) / torch.linalg.norm(ref)).item() < 1e-6
+
+
+def test_host_path_equals_device_path(rast):
+    import torch
+    from paper_2409_04751_b200 import BackwardOptions, RenderOptions, backward, render, synthetic
+    from paper_2409_04751_b200.api import grads_as_rows
+
+    sc, deg, cams, dls = synthetic.config(1, n=8000)
+    res = render(sc, cams[0], RenderOptions(sh_degree=deg), rasterizer=rast)
+    g_host = backward(sc, cams[0], res, dls[0], BackwardOptions())
+    ds = to_device(sc)
+    img, _ = rast.forward(ds, cams[0], RenderOptions(sh_degree=deg))
+    g_dev = rast.backward(ds, cams[0], torch.from_numpy(dls[0]).cuda(), BackwardOptions())
+    torch.cuda.synchronize()
+    assert res.image.tobytes() == img.cpu().numpy().tobytes()
+    np.testing.assert_array_equal(g_host["mean"], grads_as_rows(g_dev, sc.n)[:, 0:3])
+    assert (res.radii > 0).sum() == res.stats.num_splats
+
+
+def test_view_dir_gradient_matches_oracle(rast, oracle_mod):
+    import torch
+    from paper_2409_04751_b200 import BackwardOptions, RenderOptions, grads_as_rows, synthetic
+
+    sc, deg, cams, dls = synthetic.config(4, n=20000, views=1)
+    ds = to_device(sc)
+    rast.forward(ds, cams[0], RenderOptions(sh_degree=deg))
+    g = rast.backward(ds, cams[0], torch.from_numpy(dls[0]).cuda(), BackwardOptions(sh_view_dir_grad=True))
+    torch.cuda.synchronize()
+    res = oracle_mod.render(sc, cams[0], sh_degree=deg)
+    ref, _ = oracle_mod.backward(res, sc.n, dls[0], sh_view_dir_grad=True)
+    got = grads_as_rows(g, sc.n)
+    for k in ("mean", "rotation", "log_scale", "opacity", "sh_dc", "sh_rest"):
+        assert rel_l2(got[:, GROUPS[k]], ref[:, GROUPS[k]]) <= 1e-3, k
+
+
+def test_counters_match_oracle(rast, oracle_mod):
+    """E_eval / E_contrib (the blend's work counters) match the oracle."""
+    from paper_2409_04751_b200 import _lib, synthetic
+
+    sc, deg, cams, _ = synthetic.config(0)
+    rast.set_flags(_lib.FGS_FLAG_COUNTERS)
+    try:
+        fwd(rast, sc, cams[0], deg)
+        ev, ec = rast.debug("counters", np.uint64)
+    finally:
+        rast.set_flags(0)
+    st = oracle_mod.render(sc, cams[0], sh_degree=deg).stats()
+    assert int(ec) == int(st["e_contrib"])
+    assert int(ev) == int(st["e_eval"])
