@@ -121,9 +121,19 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
                       const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
 
 /* Flags: FGS_FLAG_COUNTERS makes the forward blend count E_eval / E_contrib (atomics; slower);
- * FGS_FLAG_KEEP_KEYS keeps what "key_*" exports need. Default 0. */
-enum { FGS_FLAG_COUNTERS = 1, FGS_FLAG_KEEP_KEYS = 2 };
+ * FGS_FLAG_TIMING records CUDA events around every stage (read with fgs_timing). Default 0. */
+enum { FGS_FLAG_COUNTERS = 1, FGS_FLAG_KEEP_KEYS = 2, FGS_FLAG_TIMING = 4 };
 int fgs_set_flags(fgs_context* ctx, uint32_t flags);
+
+/* Device time per stage accumulated from CUDA events while FGS_FLAG_TIMING is set, and the
+ * number of kernels this context launched, since the last reset:
+ *   ms[0..5] = preprocess, binning, sort, raster, raster_backward, preprocess_backward;
+ *   calls[0] = forward calls timed, calls[1] = backward calls timed. Synchronises. */
+int fgs_timing(fgs_context* ctx, double ms[6], uint64_t calls[2], uint64_t* launches, int reset);
+
+/* Diagnostic: FP32 pipe throughput (non-FMA fp32 op/s) of this device, measured with a
+ * FMUL/FADD probe kernel; the denominator of the blend kernels' roofline. */
+int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s);
 
 /* Parity/debug export of the last forward's state into host memory. Names:
  *   "state" int32[N] (0 culled, 1 kept, 2 degenerate), "mean_px" f32[N*2], "conic" f32[N*3],

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfgs.so")
 
 FGS_OK, FGS_EINVAL, FGS_EDEGENERATE_QUAT, FGS_ECUDA, FGS_ENOMEM, FGS_ESTATE = range(6)
-FGS_FLAG_COUNTERS, FGS_FLAG_KEEP_KEYS = 1, 2
+FGS_FLAG_COUNTERS, FGS_FLAG_KEEP_KEYS, FGS_FLAG_TIMING = 1, 2, 4
 
 
 class fgs_camera(C.Structure):
@@ -46,7 +46,8 @@ class fgs_stats(C.Structure):
 
 
 EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs_forward", "fgs_backward",
-           "fgs_render_host", "fgs_backward_host", "fgs_set_flags", "fgs_debug_get", "fgs_last_counts"]
+           "fgs_render_host", "fgs_backward_host", "fgs_set_flags", "fgs_debug_get", "fgs_last_counts",
+           "fgs_timing", "fgs_measure_fp32_peak"]
 
 _lib = None
 
@@ -82,5 +83,9 @@ def load(path: str = LIB_PATH):
     L.fgs_debug_get.restype = C.c_int64
     L.fgs_last_counts.argtypes = [vp, P(C.c_int64)]
     L.fgs_last_counts.restype = i32
+    L.fgs_timing.argtypes = [vp, P(C.c_double), P(C.c_uint64), P(C.c_uint64), i32]
+    L.fgs_timing.restype = i32
+    L.fgs_measure_fp32_peak.argtypes = [vp, P(C.c_double)]
+    L.fgs_measure_fp32_peak.restype = i32
     _lib = L
     return L

@@ -201,6 +201,21 @@ class Rasterizer:
             raise FgsError(f"debug_get({name}) failed")
         return out
 
+    def timing(self, reset: bool = False) -> dict:
+        """Stage times (ms, summed) and kernel launches recorded since the last reset."""
+        ms = (C.c_double * 6)()
+        calls = (C.c_uint64 * 2)()
+        launches = C.c_uint64()
+        self._check(self._L.fgs_timing(self._h, ms, calls, C.byref(launches), int(reset)))
+        keys = ["preprocess", "binning", "sort", "raster", "raster_backward", "preprocess_backward"]
+        return {"ms": dict(zip(keys, list(ms))), "forward_calls": calls[0], "backward_calls": calls[1],
+                "launches": launches.value}
+
+    def fp32_peak(self) -> float:
+        v = C.c_double()
+        self._check(self._L.fgs_measure_fp32_peak(self._h, C.byref(v)))
+        return v.value
+
     def counts(self) -> dict:
         a = (C.c_int64 * 9)()
         self._check(self._L.fgs_last_counts(self._h, a))

@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256) debug_keys_kernel(const uint32_t* __restr
 SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_a, uint32_t* vals_a,
                             uint32_t* keys_b, uint32_t* vals_b, int n, int passes, const SortScratch& s,
                             cudaStream_t st) {
-  SortResult r{const_cast<uint32_t*>(keys_in), const_cast<uint32_t*>(vals_in)};
+  SortResult r{const_cast<uint32_t*>(keys_in), const_cast<uint32_t*>(vals_in), 0};
   if (n <= 0 || passes <= 0) return r;
   const int tiles = div_up(n, kSortTile);
   cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * 256 * passes, st);
@@ -347,6 +347,7 @@ SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, ui
     default: radix_hist_kernel<4><<<hist_grid, 256, 0, st>>>(keys_in, n, s.hist); break;
   }
   radix_hist_scan_kernel<<<passes, 256, 0, st>>>(s.hist);
+  r.launches = 2 + passes;
   const uint32_t *ki = keys_in, *vi = vals_in;
   for (int p = 0; p < passes; ++p) {
     uint32_t* ko = (p & 1) ? keys_a : keys_b;
@@ -362,29 +363,32 @@ SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, ui
   return r;
 }
 
-void rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, uint32_t* rank, uint32_t* block_sums,
-               uint32_t* total_out, int n, cudaStream_t st) {
+int rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, uint32_t* rank, uint32_t* block_sums,
+              uint32_t* total_out, int n, cudaStream_t st) {
   const int nb = max(1, div_up(n, kScanTile));
   scan_block_sums_kernel<<<nb, kScanThreads, 0, st>>>(perm, touched, block_sums, n);
   scan_top_kernel<<<1, 1024, 0, st>>>(block_sums, nb, total_out);
   scan_apply_kernel<<<nb, kScanThreads, 0, st>>>(perm, touched, block_sums, offsets, rank, n);
+  return 3;
 }
 
-void duplicate(const uint32_t* perm, const uint32_t* offsets, const uint32_t* touched, const ushort4* rect, int tiles_x,
-               uint32_t* tile_keys, uint32_t* emit_vals, uint32_t* emit_gauss, int n, cudaStream_t st) {
-  if (n <= 0) return;
+int duplicate(const uint32_t* perm, const uint32_t* offsets, const uint32_t* touched, const ushort4* rect, int tiles_x,
+              uint32_t* tile_keys, uint32_t* emit_vals, uint32_t* emit_gauss, int n, cudaStream_t st) {
+  if (n <= 0) return 0;
   duplicate_kernel<<<div_up(n, 256), 256, 0, st>>>(perm, offsets, touched, rect, tiles_x, tile_keys, emit_vals,
                                                    emit_gauss, n);
+  return 1;
 }
 
-void tile_ranges(const uint32_t* sorted_tiles, const uint32_t* sorted_emit, const uint32_t* emit_gauss,
-                 uint32_t* tile_offsets, uint32_t* sorted_gauss, int num_isect, int num_tiles, cudaStream_t st) {
+int tile_ranges(const uint32_t* sorted_tiles, const uint32_t* sorted_emit, const uint32_t* emit_gauss,
+                uint32_t* tile_offsets, uint32_t* sorted_gauss, int num_isect, int num_tiles, cudaStream_t st) {
   if (num_isect <= 0) {
     cudaMemsetAsync(tile_offsets, 0, sizeof(uint32_t) * (num_tiles + 1), st);
-    return;
+    return 0;
   }
   tile_ranges_kernel<<<div_up(num_isect, 256), 256, 0, st>>>(sorted_tiles, sorted_emit, emit_gauss, tile_offsets,
                                                              sorted_gauss, num_isect, num_tiles);
+  return 1;
 }
 
 void debug_source_order_keys(const uint32_t* touched, const ushort4* rect, const uint32_t* depth_key, int tiles_x,

@@ -73,6 +73,15 @@ struct fgs_context {
   DevBuf<float> h_means, h_rot, h_ls, h_op, h_sh, h_img, h_dl, h_grad;
   DevBuf<int32_t> h_radii;
   cudaEvent_t ev[5] = {};
+  // stage timing (FGS_FLAG_TIMING): event sets pending accumulation
+  struct EventSet {
+    cudaEvent_t e[5];
+    int kind;  // 0 forward (4 intervals -> ms[0..3]), 1 backward (2 intervals -> ms[4..5])
+  };
+  std::vector<EventSet> pending, spare;
+  double acc_ms[6] = {0, 0, 0, 0, 0, 0};
+  uint64_t acc_calls[2] = {0, 0};
+  uint64_t launches = 0;
 
   // last forward
   bool have_fwd = false;
@@ -126,6 +135,35 @@ fgs::DevCamera make_dev_camera(const fgs_camera& c) {
     d.center[r] = acc;
   }
   return d;
+}
+
+fgs_context::EventSet* take_set(fgs_context* ctx, int kind) {
+  fgs_context::EventSet es{};
+  if (!ctx->spare.empty()) {
+    es = ctx->spare.back();
+    ctx->spare.pop_back();
+  } else {
+    for (auto& e : es.e) cudaEventCreate(&e);
+  }
+  es.kind = kind;
+  ctx->pending.push_back(es);
+  return &ctx->pending.back();
+}
+
+void drain_sets(fgs_context* ctx, size_t keep) {
+  while (ctx->pending.size() > keep) {
+    fgs_context::EventSet es = ctx->pending.front();
+    ctx->pending.erase(ctx->pending.begin());
+    const int nint = es.kind == 0 ? 4 : 2;
+    cudaEventSynchronize(es.e[nint]);
+    for (int k = 0; k < nint; ++k) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, es.e[k], es.e[k + 1]);
+      ctx->acc_ms[(es.kind == 0 ? 0 : 4) + k] += ms;
+    }
+    ctx->acc_calls[es.kind] += 1;
+    ctx->spare.push_back(es);
+  }
 }
 
 bool same_camera(const fgs_camera& a, const fgs_camera& b) {
@@ -188,6 +226,9 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->counters.release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
+  for (auto* v : {&ctx->pending, &ctx->spare})
+    for (auto& es : *v)
+      for (auto& e : es.e) cudaEventDestroy(e);
   if (ctx->h_scalars) cudaFreeHost(ctx->h_scalars);
   delete ctx;
   return FGS_OK;
@@ -267,8 +308,11 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ctx->tiles_y = tiles_y;
 
   fgs::SortScratch ss{ctx->hist.p, ctx->lookback.p, ctx->sort_counters.p, 0};
-  const bool timing = stats != nullptr;
-  if (timing) cudaEventRecord(ctx->ev[0], st);
+  const bool timing = stats != nullptr || (ctx->flags & FGS_FLAG_TIMING);
+  if (ctx->pending.size() > 64) drain_sets(ctx, 8);
+  cudaEvent_t* ev = timing ? take_set(ctx, 0)->e : ctx->ev;
+  if (timing) cudaEventRecord(ev[0], st);
+  uint64_t launches = 0;
 
   FGS_CHECK(cudaMemsetAsync(ctx->scalars.p, 0, 16 * sizeof(uint32_t), st));
   if (ctx->flags & FGS_FLAG_COUNTERS) FGS_CHECK(cudaMemsetAsync(ctx->counters.p, 0, 4 * sizeof(unsigned long long), st));
@@ -296,14 +340,16 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.error_flag = reinterpret_cast<int*>(ctx->scalars.p + 1);
     pa.state_counts = ctx->scalars.p + 2;
     fgs::preprocess_kernel<<<fgs::div_up(static_cast<int>(n), 256), 256, 0, st>>>(pa);
+    ++launches;
   }
-  if (timing) cudaEventRecord(ctx->ev[1], st);
+  if (timing) cudaEventRecord(ev[1], st);
   // level 1: Gaussians by depth key (stable; ties keep source order)
   const fgs::SortResult l1 = fgs::radix_sort_pairs(ctx->dkey.p, ctx->iota.p, ctx->dkey_a.p, ctx->perm_a.p,
                                                    ctx->dkey_b.p, ctx->perm_b.p, static_cast<int>(n), 4, ss, st);
   ctx->perm = l1.vals;
+  launches += l1.launches;
   if (n > 0)
-    fgs::rank_scan(ctx->perm, ctx->touched.p, ctx->offsets.p, ctx->rank.p, ctx->block_sums.p, ctx->scalars.p,
+    launches += fgs::rank_scan(ctx->perm, ctx->touched.p, ctx->offsets.p, ctx->rank.p, ctx->block_sums.p, ctx->scalars.p,
                    static_cast<int>(n), st);
   FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, ctx->scalars.p, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   FGS_CHECK(cudaStreamSynchronize(st));
@@ -323,17 +369,18 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   FGS_CHECK(ctx->lookback.ensure(static_cast<size_t>(4) * 256 * (ni / fgs::kSortTile + 1)));
   ss.lookback = ctx->lookback.p;
   if (n > 0)
-    fgs::duplicate(ctx->perm, ctx->offsets.p, ctx->touched.p, ctx->rect.p, tiles_x, ctx->tkey.p, ctx->emit.p,
+    launches += fgs::duplicate(ctx->perm, ctx->offsets.p, ctx->touched.p, ctx->rect.p, tiles_x, ctx->tkey.p, ctx->emit.p,
                    ctx->emit_gauss.p, static_cast<int>(n), st);
-  if (timing) cudaEventRecord(ctx->ev[2], st);
+  if (timing) cudaEventRecord(ev[2], st);
   const int passes2 = num_tiles <= 256 ? 1 : (num_tiles <= 65536 ? 2 : 3);
   const fgs::SortResult l2 = fgs::radix_sort_pairs(ctx->tkey.p, ctx->emit.p, ctx->tkey_a.p, ctx->emit_a.p,
                                                    ctx->tkey_b.p, ctx->emit_b.p, static_cast<int>(I), passes2, ss, st);
   ctx->sorted_tiles = l2.keys;
   ctx->sorted_emit = l2.vals;
-  fgs::tile_ranges(ctx->sorted_tiles, ctx->sorted_emit, ctx->emit_gauss.p, ctx->tile_offsets.p, ctx->sorted_gauss.p,
+  launches += l2.launches;
+  launches += fgs::tile_ranges(ctx->sorted_tiles, ctx->sorted_emit, ctx->emit_gauss.p, ctx->tile_offsets.p, ctx->sorted_gauss.p,
                    static_cast<int>(I), num_tiles, st);
-  if (timing) cudaEventRecord(ctx->ev[3], st);
+  if (timing) cudaEventRecord(ev[3], st);
 
   fgs::BlendArgs ba{};
   ba.width = W;
@@ -349,17 +396,22 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;
   ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
-  fgs::blend_forward(ba, st);
+  launches += fgs::blend_forward(ba, st);
+  if (timing) cudaEventRecord(ev[4], st);
   if (radii && n > 0) FGS_CHECK(cudaMemcpyAsync(radii, ctx->radii.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
-  if (timing) cudaEventRecord(ctx->ev[4], st);
   FGS_CHECK(cudaGetLastError());
+  ctx->launches += launches;
 
   ctx->aux_bytes = nn * (16 + 16 + 4 + 1 + 4 * 9 + 8 + 4) + ni * 4 * 8 + (num_tiles + 1) * 4 + npix * 8;
   ctx->have_fwd = true;
   if (stats) {
-    FGS_CHECK(cudaEventSynchronize(ctx->ev[4]));
+    FGS_CHECK(cudaEventSynchronize(ev[4]));
     float ms[4];
-    for (int s = 0; s < 4; ++s) cudaEventElapsedTime(&ms[s], ctx->ev[s], ctx->ev[s + 1]);
+    for (int s = 0; s < 4; ++s) cudaEventElapsedTime(&ms[s], ev[s], ev[s + 1]);
+    if (!(ctx->flags & FGS_FLAG_TIMING)) {  // stats-only timing: recycle the set now
+      ctx->spare.push_back(ctx->pending.back());
+      ctx->pending.pop_back();
+    }
     stats->num_intersections = static_cast<uint64_t>(I);
     stats->num_splats = ctx->num_splats;
     stats->num_culled = ctx->num_culled;
@@ -401,7 +453,12 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   ba.last = ctx->last.p;
   ba.dl_dimage = dl_dimage;
   ba.partials = ctx->partials.p;
-  if (I > 0) fgs::blend_backward(ba, st);
+  const bool timing = (ctx->flags & FGS_FLAG_TIMING) != 0;
+  if (timing && ctx->pending.size() > 64) drain_sets(ctx, 8);
+  cudaEvent_t* ev = timing ? take_set(ctx, 1)->e : nullptr;
+  if (timing) cudaEventRecord(ev[0], st);
+  if (I > 0) ctx->launches += fgs::blend_backward(ba, st);
+  if (timing) cudaEventRecord(ev[1], st);
 
   fgs::PreprocessBackwardArgs pb{};
   pb.n = n;
@@ -427,6 +484,8 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.d_opacity = grads->d_opacity_logits;
   pb.d_sh = grads->d_sh;
   fgs::preprocess_backward_kernel<<<fgs::div_up(static_cast<int>(n), 128), 128, 0, st>>>(pb);
+  ++ctx->launches;
+  if (timing) cudaEventRecord(ev[2], st);
   FGS_CHECK(cudaGetLastError());
   return FGS_OK;
 }
@@ -506,6 +565,33 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
     FGS_CHECK(cudaMemcpyAsync(grads->d_sh, dg.d_sh, n * 48 * 4, cudaMemcpyDeviceToHost, st));
   }
   FGS_CHECK(cudaStreamSynchronize(st));
+  return FGS_OK;
+}
+
+int fgs_timing(fgs_context* ctx, double ms[6], uint64_t calls[2], uint64_t* launches, int reset) {
+  if (!ctx) return FGS_EINVAL;
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  drain_sets(ctx, 0);
+  if (ms)
+    for (int k = 0; k < 6; ++k) ms[k] = ctx->acc_ms[k];
+  if (calls) {
+    calls[0] = ctx->acc_calls[0];
+    calls[1] = ctx->acc_calls[1];
+  }
+  if (launches) *launches = ctx->launches;
+  if (reset) {
+    for (double& v : ctx->acc_ms) v = 0.0;
+    ctx->acc_calls[0] = ctx->acc_calls[1] = 0;
+    ctx->launches = 0;
+  }
+  return FGS_OK;
+}
+
+int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s) {
+  if (!ctx || !ops_per_s) return FGS_EINVAL;
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  *ops_per_s = fgs::fp32_peak_probe(ctx->stream);
+  FGS_CHECK(cudaGetLastError());
   return FGS_OK;
 }
 

@@ -92,6 +92,7 @@ constexpr int kMaxPasses = 4;
 struct SortResult {
   uint32_t* keys;
   uint32_t* vals;
+  int launches;
 };
 SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_a, uint32_t* vals_a,
                             uint32_t* keys_b, uint32_t* vals_b, int n, int passes, const SortScratch& s,
@@ -99,13 +100,13 @@ SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, ui
 
 // Exclusive scan of touched[perm[r]] over ranks r; writes offsets[r], rank[perm[r]] = r,
 // block sums and the total (total_out, device).
-void rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, uint32_t* rank, uint32_t* block_sums,
+int rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, uint32_t* rank, uint32_t* block_sums,
                uint32_t* total_out, int n, cudaStream_t st);
 // Emit (tile key, emission slot, gaussian) per intersection in depth-rank order.
-void duplicate(const uint32_t* perm, const uint32_t* offsets, const uint32_t* touched, const ushort4* rect,
+int duplicate(const uint32_t* perm, const uint32_t* offsets, const uint32_t* touched, const ushort4* rect,
                int tiles_x, uint32_t* tile_keys, uint32_t* emit_vals, uint32_t* emit_gauss, int n, cudaStream_t st);
 // Per-tile ranges from sorted tile keys; sorted_gauss[k] = emit_gauss[sorted_emit[k]].
-void tile_ranges(const uint32_t* sorted_tiles, const uint32_t* sorted_emit, const uint32_t* emit_gauss,
+int tile_ranges(const uint32_t* sorted_tiles, const uint32_t* sorted_emit, const uint32_t* emit_gauss,
                  uint32_t* tile_offsets, uint32_t* sorted_gauss, int num_isect, int num_tiles, cudaStream_t st);
 // Debug: reference emission order keys (source order, ty-major, tx-minor).
 void debug_source_order_keys(const uint32_t* touched, const ushort4* rect, const uint32_t* depth_key, int tiles_x,
@@ -113,7 +114,9 @@ void debug_source_order_keys(const uint32_t* touched, const ushort4* rect, const
                              uint32_t* key_tile, uint32_t* key_depth, uint32_t* key_gauss, cudaStream_t st);
 
 // ---- blend (raster.cu) ----
-void blend_forward(const BlendArgs& a, cudaStream_t st);
-void blend_backward(const BlendArgs& a, cudaStream_t st);
+int blend_forward(const BlendArgs& a, cudaStream_t st);
+int blend_backward(const BlendArgs& a, cudaStream_t st);
+// FP32 pipe probe: returns achieved non-FMA fp32 op/s (FMUL + FADD, no contraction).
+double fp32_peak_probe(cudaStream_t st);
 
 }  // namespace fgs

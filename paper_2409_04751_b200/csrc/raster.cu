@@ -16,6 +16,8 @@
 // They are summed over the tile's pixels in a fixed order (warp shuffle tree, then warps in
 // order) and written to the intersection's emission slot: no atomics, deterministic.
 
+#include <algorithm>
+
 #include "fgs_kernels.h"
 
 namespace fgs {
@@ -220,12 +222,60 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
 
 }  // namespace
 
-void blend_forward(const BlendArgs& a, cudaStream_t st) {
+int blend_forward(const BlendArgs& a, cudaStream_t st) {
   blend_forward_kernel<<<a.tiles_x * a.tiles_y, kBlend, 0, st>>>(a);
+  return 1;
 }
 
-void blend_backward(const BlendArgs& a, cudaStream_t st) {
+int blend_backward(const BlendArgs& a, cudaStream_t st) {
   blend_backward_kernel<<<a.tiles_x * a.tiles_y, kBlend, 0, st>>>(a);
+  return 1;
+}
+
+namespace {
+// 8 independent FMUL->FADD chains per thread, rounding intrinsics so nothing contracts to FFMA.
+__global__ void __launch_bounds__(256) fp32_probe_kernel(float* out, int iters) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0f + 1e-3f * (threadIdx.x + k);
+  const float m = 0.9999f, c = 1e-4f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __fadd_rn(__fmul_rn(a[k], m), c);
+  }
+  float s = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678f) out[0] = s;  // keep the chains alive
+}
+}  // namespace
+
+double fp32_peak_probe(cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* out = nullptr;
+  cudaMalloc(&out, sizeof(float));
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fp32_probe_kernel<<<blocks, threads, 0, st>>>(out, 64);  // warm-up
+  double best = 0.0;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0, st);
+    fp32_probe_kernel<<<blocks, threads, 0, st>>>(out, iters);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = 2.0 * 8.0 * iters * double(blocks) * threads;
+    if (ms > 0) best = std::max(best, ops / (ms * 1e-3));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return best;
 }
 
 }  // namespace fgs
