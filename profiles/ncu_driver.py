@@ -1,0 +1,35 @@
+"""Short driver for ncu captures: config 2 (1M Gaussians, 1752x1168), 3 forward passes then
+3 forward+backward passes on cuda:0. Exits 0 on success (run plain before ncu)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+
+    from paper_2409_04751_b200 import BackwardOptions, Rasterizer, RenderOptions, synthetic
+    from paper_2409_04751_b200.types import Scene
+
+    cfg = int(os.environ.get("FGS_CFG", "2"))
+    scene, deg, cams, dls = synthetic.config(cfg)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    ds = Scene(t(scene.means), t(scene.rotations), t(scene.log_scales), t(scene.opacity_logits), t(scene.sh),
+               scene.background)
+    r = Rasterizer(0)
+    cam = cams[0]
+    dl = t(dls[0]) if dls else torch.randn((cam.height, cam.width, 3), device="cuda")
+    for _ in range(3):
+        r.forward(ds, cam, RenderOptions(sh_degree=deg))
+    for _ in range(3):
+        r.forward(ds, cam, RenderOptions(sh_degree=deg))
+        r.backward(ds, cam, dl, BackwardOptions())
+    torch.cuda.synchronize()
+    print("ok")
+
+
+if __name__ == "__main__":
+    main()
