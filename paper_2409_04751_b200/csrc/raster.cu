@@ -24,61 +24,124 @@ namespace fgs {
 
 namespace {
 
-constexpr int kBlend = 256;
-constexpr int kBwdBatch = 128;
+constexpr int kBlend = 256;     // threads per tile CTA = pixels per tile
+constexpr int kBwdBatch = 128;  // splats per backward batch
+constexpr int kWarps = kBlend / 32;
 
+// Warp w of a tile owns the 8x4 pixel block at (8*(w&1), 4*(w>>1)); lane l the pixel
+// (l&7, l>>3) inside it. Square-ish blocks make the per-warp culling below tight.
+__device__ __forceinline__ void pixel_of(int tid, int& lx, int& ly) {
+  const int w = tid >> 5, l = tid & 31;
+  lx = ((w & 1) << 3) + (l & 7);
+  ly = ((w >> 1) << 2) + (l >> 3);
+}
+
+// Conservative per-warp visibility of one splat: bit w is set unless no pixel centre of warp
+// w's 8x4 block can reach alpha >= 1/255. alpha(d) = alpha_max * exp(-q(d)/2) with
+// q = a dx^2 + 2b dx dy + c dy^2, so alpha >= 1/255 needs q <= 2 ln(255 alpha_max), whose
+// bounding box has half-extents sqrt(2 tau Sigma_xx), sqrt(2 tau Sigma_yy) (Sigma = Q^-1).
+// The box is inflated (0.1% + 1e-3 px) far beyond fp32 rounding of the blend's power, so a
+// culled (pixel, splat) pair is exactly one the reference would `continue` on: the image and
+// every decision are unchanged; only evaluations that cannot contribute are skipped.
+__device__ __forceinline__ uint32_t warp_mask(float4 r0, float4 r1, float tile_x0, float tile_y0) {
+  const float a = r0.z, b = r0.w, c = r1.x, amax = r1.y;
+  if (!(amax >= kAlphaSkip)) return 0u;
+  const float det = a * c - b * b;
+  if (!(det > 0.0f) || !(a > 0.0f) || !(c > 0.0f)) return 0xFFu;
+  const float tau2 = 2.0f * __logf(255.0f * amax) * 1.002f + 1e-3f;
+  const float ex = sqrtf(fmaxf(tau2 * c / det, 0.0f)) * 1.001f + 1e-3f;
+  const float ey = sqrtf(fmaxf(tau2 * a / det, 0.0f)) * 1.001f + 1e-3f;
+  // box in tile-local pixel-centre coordinates
+  const float x0 = r0.x - ex - tile_x0, x1 = r0.x + ex - tile_x0;
+  const float y0 = r0.y - ey - tile_y0, y1 = r0.y + ey - tile_y0;
+  uint32_t m = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    const float bx0 = ((w & 1) << 3) + 0.5f, bx1 = bx0 + 7.0f;
+    const float by0 = ((w >> 1) << 2) + 0.5f, by1 = by0 + 3.0f;
+    if (x1 >= bx0 && x0 <= bx1 && y1 >= by0 && y0 <= by1) m |= 1u << w;
+  }
+  return m;
+}
+
+// Each warp compacts the batch indices whose mask has its bit into s_list[warp][...].
+__device__ __forceinline__ int build_list(const uint8_t* s_mask, int cnt, int warp, int lane, uint8_t* list) {
+  int n = 0;
+  for (int c0 = 0; c0 < cnt; c0 += 32) {
+    const int j = c0 + lane;
+    const bool on = j < cnt && ((s_mask[j] >> warp) & 1u);
+    const uint32_t bal = __ballot_sync(0xffffffffu, on);
+    if (on) list[n + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint8_t>(j);
+    n += __popc(bal);
+  }
+  __syncwarp();
+  return n;
+}
+
+template <bool COUNTERS>
 __global__ void __launch_bounds__(kBlend) blend_forward_kernel(BlendArgs a) {
   __shared__ float4 s0[kBlend];
   __shared__ float4 s1[kBlend];
   __shared__ float s2[kBlend];
+  __shared__ uint8_t s_mask[kBlend];
+  __shared__ uint8_t s_list[kWarps][kBlend];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-  const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int lx, ly;
+  pixel_of(threadIdx.x, lx, ly);
+  const int px = tx * kTile + lx, py = ty * kTile + ly;
   const bool inside = px < a.width && py < a.height;
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
   const float fx = static_cast<float>(px) + 0.5f, fy = static_cast<float>(py) + 0.5f;
+  const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  uint32_t last = lo;
+  uint32_t last = lo, stop_k = hi;
   bool done = !inside;
-  unsigned long long n_eval = 0, n_contrib = 0;
+  uint32_t n_contrib = 0;
 
   for (uint32_t base = lo; base < hi; base += kBlend) {
     if (__syncthreads_count(done) == kBlend) break;
     const uint32_t k = base + threadIdx.x;
     if (k < hi) {
       const uint32_t g = __ldg(a.sorted_gauss + k);
-      s0[threadIdx.x] = __ldg(a.rec.rec0 + g);
-      s1[threadIdx.x] = __ldg(a.rec.rec1 + g);
+      const float4 r0 = __ldg(a.rec.rec0 + g);
+      const float4 r1 = __ldg(a.rec.rec1 + g);
+      s0[threadIdx.x] = r0;
+      s1[threadIdx.x] = r1;
       s2[threadIdx.x] = __ldg(a.rec.rec2 + g);
+      s_mask[threadIdx.x] = static_cast<uint8_t>(warp_mask(r0, r1, tile_x0, tile_y0));
     }
     __syncthreads();
-    if (!done) {
-      const int cnt = static_cast<int>(min(static_cast<uint32_t>(kBlend), hi - base));
-      for (int j = 0; j < cnt; ++j) {
-        if (a.counters) ++n_eval;
-        const float4 r0 = s0[j];
-        const float dx = __fsub_rn(fx, r0.x);
-        const float dy = __fsub_rn(fy, r0.y);
-        const float c = s1[j].x;
-        const float power = blend_power(r0.z, r0.w, c, dx, dy);
-        if (power > 0.0f || power < kPowerFloor) continue;
-        const float4 r1 = s1[j];
-        float e;
-        const float alpha = fminf(kAlphaClamp, alpha_raw(r1.y, power, &e));
-        if (alpha < kAlphaSkip) continue;
-        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-        if (Tn < kTransmittanceStop) {
-          done = true;
-          break;
-        }
-        const float w = __fmul_rn(alpha, T);
-        C0 = fmaf(r1.z, w, C0);
-        C1 = fmaf(r1.w, w, C1);
-        C2 = fmaf(s2[j], w, C2);
-        T = Tn;
-        last = base + j + 1;
-        if (a.counters) ++n_contrib;
+    const int cnt = static_cast<int>(min(static_cast<uint32_t>(kBlend), hi - base));
+    if (__all_sync(0xffffffffu, done)) continue;
+    const int nl = build_list(s_mask, cnt, warp, lane, s_list[warp]);
+    for (int i = 0; i < nl; ++i) {
+      if (__all_sync(0xffffffffu, done)) break;
+      if (done) continue;
+      const int j = s_list[warp][i];
+      const float4 r0 = s0[j];
+      const float dx = __fsub_rn(fx, r0.x);
+      const float dy = __fsub_rn(fy, r0.y);
+      const float4 r1 = s1[j];
+      const float power = blend_power(r0.z, r0.w, r1.x, dx, dy);
+      if (power > 0.0f || power < kPowerFloor) continue;
+      float e;
+      const float alpha = fminf(kAlphaClamp, alpha_raw(r1.y, power, &e));
+      if (alpha < kAlphaSkip) continue;
+      const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
+      if (Tn < kTransmittanceStop) {
+        done = true;
+        stop_k = base + j;
+        continue;
       }
+      const float w = __fmul_rn(alpha, T);
+      C0 = fmaf(r1.z, w, C0);
+      C1 = fmaf(r1.w, w, C1);
+      C2 = fmaf(s2[j], w, C2);
+      T = Tn;
+      last = base + j + 1;
+      if (COUNTERS) ++n_contrib;
     }
   }
   if (inside) {
@@ -88,9 +151,12 @@ __global__ void __launch_bounds__(kBlend) blend_forward_kernel(BlendArgs a) {
     a.image[pix * 3 + 2] = C2 + T * a.bg[2];
     a.final_T[pix] = T;
     a.last[pix] = last;
-    if (a.counters) {
+    if (COUNTERS) {
+      // E_eval as the reference counts it: k-loop iterations entered, including the one
+      // that terminates (inc/splatting.hpp:282-292).
+      const unsigned long long n_eval = (stop_k < hi) ? (stop_k - lo + 1) : (hi - lo);
       atomicAdd(a.counters + 0, n_eval);
-      atomicAdd(a.counters + 1, n_contrib);
+      atomicAdd(a.counters + 1, static_cast<unsigned long long>(n_contrib));
     }
   }
 }
@@ -102,20 +168,25 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
-  constexpr int NW = kBlend / 32;
   __shared__ float4 s0[kBwdBatch];
   __shared__ float4 s1[kBwdBatch];
   __shared__ float s2[kBwdBatch];
   __shared__ uint32_t s_emit[kBwdBatch];
-  __shared__ float s_part[NW][kBwdBatch][9];
+  __shared__ uint8_t s_mask[kBwdBatch];
+  __shared__ uint8_t s_list[kWarps][kBwdBatch];
+  __shared__ float s_part[kWarps][kBwdBatch][9];
   __shared__ uint32_t s_max_last;
+  __shared__ uint32_t s_wl[kWarps];
 
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-  const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int lx, ly;
+  pixel_of(threadIdx.x, lx, ly);
+  const int px = tx * kTile + lx, py = ty * kTile + ly;
   const bool inside = px < a.width && py < a.height;
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
   if (threadIdx.x == 0) s_max_last = lo;
   __syncthreads();
 
@@ -129,7 +200,11 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     dl0 = a.dl_dimage[pix * 3 + 0];
     dl1 = a.dl_dimage[pix * 3 + 1];
     dl2 = a.dl_dimage[pix * 3 + 2];
-    atomicMax(&s_max_last, last);
+  }
+  const uint32_t warp_last = __reduce_max_sync(0xffffffffu, last);
+  if (lane == 0) {
+    atomicMax(&s_max_last, warp_last);
+    s_wl[warp] = warp_last;
   }
   float sf0 = T * a.bg[0], sf1 = T * a.bg[1], sf2 = T * a.bg[2];
   __syncthreads();
@@ -149,13 +224,20 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     if (threadIdx.x < cnt) {
       const uint32_t k = bstart + threadIdx.x;
       const uint32_t g = __ldg(a.sorted_gauss + k);
-      s0[threadIdx.x] = __ldg(a.rec.rec0 + g);
-      s1[threadIdx.x] = __ldg(a.rec.rec1 + g);
+      const float4 r0 = __ldg(a.rec.rec0 + g);
+      const float4 r1 = __ldg(a.rec.rec1 + g);
+      s0[threadIdx.x] = r0;
+      s1[threadIdx.x] = r1;
       s2[threadIdx.x] = __ldg(a.rec.rec2 + g);
       s_emit[threadIdx.x] = __ldg(a.sorted_emit + k);
+      s_mask[threadIdx.x] = static_cast<uint8_t>(warp_mask(r0, r1, tile_x0, tile_y0));
     }
     __syncthreads();
-    for (int j = cnt - 1; j >= 0; --j) {
+    // a warp whose pixels all stopped before an entry cannot take a gradient from it
+    const int wcnt = static_cast<int>(min(static_cast<int64_t>(cnt), static_cast<int64_t>(warp_last) - bstart));
+    const int nl = wcnt > 0 ? build_list(s_mask, wcnt, warp, lane, s_list[warp]) : 0;
+    for (int i = nl - 1; i >= 0; --i) {
+      const int j = s_list[warp][i];
       const uint32_t k = bstart + j;
       float g[9];
 #pragma unroll
@@ -209,12 +291,18 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
       }
     }
     __syncthreads();
-    // Fixed-order reduction over warps; one writer per entry.
+    // Fixed-order reduction over the warps that listed the entry; one writer per entry.
     for (int idx = threadIdx.x; idx < cnt * 9; idx += kBlend) {
       const int j = idx / 9, q = idx - j * 9;
-      float s = s_part[0][j][q];
+      const uint32_t m = s_mask[j];
+      const int64_t kk = static_cast<int64_t>(bstart) + j;
+      float s = 0.0f;
 #pragma unroll
-      for (int w = 1; w < NW; ++w) s += s_part[w][j][q];
+      for (int w = 0; w < kWarps; ++w) {
+        // listed by warp w iff its mask bit is set and the entry is below warp w's last
+        const bool listed = ((m >> w) & 1u) && kk < static_cast<int64_t>(s_wl[w]);
+        if (listed) s += s_part[w][j][q];
+      }
       a.partials[static_cast<size_t>(s_emit[j]) * 9 + q] = s;
     }
   }
@@ -223,7 +311,10 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
 }  // namespace
 
 int blend_forward(const BlendArgs& a, cudaStream_t st) {
-  blend_forward_kernel<<<a.tiles_x * a.tiles_y, kBlend, 0, st>>>(a);
+  if (a.counters)
+    blend_forward_kernel<true><<<a.tiles_x * a.tiles_y, kBlend, 0, st>>>(a);
+  else
+    blend_forward_kernel<false><<<a.tiles_x * a.tiles_y, kBlend, 0, st>>>(a);
   return 1;
 }
 
