@@ -1,10 +1,12 @@
-// binning.cu — K2: depth-rank scan, key duplication, onesweep LSD radix sort, tile ranges.
+// binning.cu — K2: compaction, depth-rank scan, key duplication, onesweep LSD radix sort,
+// tile ranges.
 //
 // Ordering contract (reference inc/splatting.hpp:192-249): the per-tile
 // lists are sorted by (tile id, depth key bits, source index). The reference duplicates keys
 // in source order and runs two stable LSD sorts (depth, then tile). Here the same order is
 // produced with less traffic:
-//   level 1: stable sort of the N Gaussians by depth key (ties keep source order);
+//   compact the Gaussians that touch >= 1 tile (source order kept);
+//   level 1: stable sort of those by depth key (ties keep source order);
 //   duplicate in depth-rank order (tiles ascending within a Gaussian);
 //   level 2: stable sort of the I intersections by tile id.
 // Stability of both levels gives exactly (tile, depth, source).
@@ -12,7 +14,9 @@
 // The radix sort is a single-pass-per-digit "onesweep" LSD sort: one histogram kernel for all
 // digit passes, then per pass one kernel whose CTAs take tiles in launch order from an atomic
 // counter, rank their keys with warp match-based multisplit, resolve global digit offsets by
-// decoupled look-back, and scatter through shared memory.
+// decoupled look-back (each digit's thread loads 4 predecessor statuses per step), and
+// scatter through shared memory. Element counts may live in device memory (written by the
+// previous kernel), so the grid is sized for the maximum and surplus CTAs exit.
 
 #include "fgs_kernels.h"
 
@@ -37,7 +41,11 @@ __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
   asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Block-wide exclusive scan of one value per thread (blockDim.x == 256 or 1024).
+__device__ __forceinline__ int load_n(const uint32_t* n_dev, int n_max) {
+  return n_dev ? static_cast<int>(min(*n_dev, static_cast<uint32_t>(n_max))) : n_max;
+}
+
+// Block-wide exclusive scan of one value per thread.
 template <int THREADS>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -65,10 +73,31 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   return warp_prefix + x - v;
 }
 
+// Decoupled look-back of one 30-bit value for tile `tile` (status words: value<<2 | flag).
+// Called by a single thread; loads 4 predecessors per step.
+__device__ __forceinline__ uint32_t look_back(const uint32_t* status, size_t stride, int tile) {
+  uint32_t prefix = 0;
+  int j = tile - 1;
+  while (true) {
+    uint32_t s[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[q] = j - q >= 0 ? ld_volatile(status + static_cast<size_t>(j - q) * stride) : 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t v = s[q];
+      while ((v & 3u) == 0u) v = ld_volatile(status + static_cast<size_t>(j - q) * stride);
+      prefix += v >> 2;
+      if ((v & 3u) == kFlagInc) return prefix;
+    }
+    j -= 4;
+  }
+}
+
 template <int PASSES>
-__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys, int n,
-                                                         uint32_t* __restrict__ hist) {
+__global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restrict__ keys, const uint32_t* n_dev,
+                                                         int n_max, uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[PASSES * 256];
+  const int n = load_n(n_dev, n_max);
   for (int j = threadIdx.x; j < PASSES * 256; j += 256) h[j] = 0;
   __syncthreads();
   const int n4 = n >> 2;
@@ -99,14 +128,14 @@ __global__ void __launch_bounds__(256) radix_hist_scan_kernel(uint32_t* hist) {
   __shared__ uint32_t s_warp[8];
   uint32_t* h = hist + blockIdx.x * 256;
   const uint32_t v = h[threadIdx.x];
-  const uint32_t ex = block_exclusive_scan<256>(v, s_warp, nullptr);
-  h[threadIdx.x] = ex;
+  h[threadIdx.x] = block_exclusive_scan<256>(v, s_warp, nullptr);
 }
 
 __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* __restrict__ keys_in,
                                                                 const uint32_t* __restrict__ vals_in,
                                                                 uint32_t* __restrict__ keys_out,
-                                                                uint32_t* __restrict__ vals_out, int n, int shift,
+                                                                uint32_t* __restrict__ vals_out,
+                                                                const uint32_t* n_dev, int n_max, int shift,
                                                                 const uint32_t* __restrict__ digit_offsets,
                                                                 uint32_t* __restrict__ lookback,
                                                                 uint32_t* __restrict__ tile_counter) {
@@ -120,11 +149,13 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* 
   __shared__ uint32_t s_vals[kSortTile];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = load_n(n_dev, n_max);
   if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
   for (int j = tid; j < W * 256; j += kSortThreads) (&s_warp_hist[0][0])[j] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
   const int base = static_cast<int>(tile) * kSortTile;
+  if (base >= n) return;  // surplus CTA (count known only on device)
   const int warp_base = base + warp * (32 * kSortItems);
 
   uint32_t k[kSortItems], v[kSortItems], rank[kSortItems];
@@ -154,39 +185,24 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* 
   __syncthreads();
   // Per digit (thread = digit): exclusive scan over warps, CTA total.
   uint32_t total = 0;
-  {
-    const int d = tid;
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-      const uint32_t c = s_warp_hist[w][d];
-      s_warp_hist[w][d] = total;
-      total += c;
-    }
+  for (int w = 0; w < W; ++w) {
+    const uint32_t c = s_warp_hist[w][tid];
+    s_warp_hist[w][tid] = total;
+    total += c;
   }
-  const uint32_t local_start = block_exclusive_scan<kSortThreads>(total, s_scan, nullptr);
-  s_local_start[tid] = local_start;
-  // Decoupled look-back for this digit.
-  {
-    const int d = tid;
-    uint32_t* mine = lookback + static_cast<size_t>(tile) * 256 + d;
-    uint32_t prefix = 0;
-    if (tile == 0) {
-      st_volatile(mine, (total << 2) | kFlagInc);
-    } else {
-      st_volatile(mine, (total << 2) | kFlagAgg);
-      int j = static_cast<int>(tile) - 1;
-      while (true) {
-        const uint32_t s = ld_volatile(lookback + static_cast<size_t>(j) * 256 + d);
-        const uint32_t flag = s & 3u;
-        if (flag == 0) continue;
-        prefix += s >> 2;
-        if (flag == kFlagInc) break;
-        --j;
-      }
-      st_volatile(mine, ((prefix + total) << 2) | kFlagInc);
-    }
-    s_global_start[d] = digit_offsets[d] + prefix;
+  // Publish this tile's aggregate for digit tid, then look back.
+  uint32_t* mine = lookback + static_cast<size_t>(tile) * 256 + tid;
+  uint32_t prefix = 0;
+  if (tile == 0) {
+    st_volatile(mine, (total << 2) | kFlagInc);
+  } else {
+    st_volatile(mine, (total << 2) | kFlagAgg);
+    prefix = look_back(lookback + tid, 256, static_cast<int>(tile));
+    st_volatile(mine, ((prefix + total) << 2) | kFlagInc);
   }
+  s_global_start[tid] = digit_offsets[tid] + prefix;
+  s_local_start[tid] = block_exclusive_scan<kSortThreads>(total, s_scan, nullptr);
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
@@ -209,66 +225,95 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* 
   }
 }
 
+// ---- single-pass scans (chained, decoupled look-back) ----
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 4;
-constexpr int kScanTile = kScanThreads * kScanItems;  // ranks per CTA
+constexpr int kScanTile = kScanThreads * kScanItems;
 
-__device__ __forceinline__ uint32_t touched_at(const uint32_t* perm, const uint32_t* touched, int r, int n) {
-  if (r >= n) return 0u;
-  const uint32_t g = perm ? __ldg(perm + r) : static_cast<uint32_t>(r);
-  return __ldg(touched + g);
-}
+enum ScanMode { kCompact = 0, kRank = 1, kPlain = 2 };
 
-__global__ void __launch_bounds__(kScanThreads) scan_block_sums_kernel(const uint32_t* __restrict__ perm,
-                                                                       const uint32_t* __restrict__ touched,
-                                                                       uint32_t* __restrict__ block_sums, int n) {
+struct ScanArgs {
+  const uint32_t* touched;
+  const uint32_t* perm;       // kRank
+  const uint32_t* depth_key;  // kCompact
+  uint32_t* keys_out;         // kCompact
+  uint32_t* vals_out;         // kCompact
+  uint32_t* offsets;          // kRank / kPlain
+  uint32_t* rank;             // kRank
+  const uint32_t* n_dev;
+  int n_max;
+  uint32_t* status;           // one word per tile, zeroed
+  uint32_t* counter;          // tile counter, zeroed
+  uint32_t* total_out;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
+  __shared__ uint32_t s_tile, s_prefix;
   __shared__ uint32_t s_warp[kScanThreads / 32];
-  const int r0 = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-  uint32_t s = 0;
+  const int n = load_n(a.n_dev, a.n_max);
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.counter, 1u);
+  __syncthreads();
+  const int tile = static_cast<int>(s_tile);
+  const int r0 = tile * kScanTile;
+  if (r0 >= n && !(tile == 0 && n == 0)) return;
+  uint32_t c[kScanItems], g[kScanItems];
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) s += touched_at(perm, touched, r0 + i, n);
-  uint32_t tot;
-  block_exclusive_scan<kScanThreads>(s, s_warp, &tot);
-  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* block_sums, int nb, uint32_t* total_out) {
-  __shared__ uint32_t s_warp[32];
-  uint32_t carry = 0;
-  for (int b0 = 0; b0 < nb; b0 += 1024) {
-    const int b = b0 + threadIdx.x;
-    const uint32_t v = b < nb ? block_sums[b] : 0u;
-    uint32_t tot;
-    const uint32_t ex = block_exclusive_scan<1024>(v, s_warp, &tot);
-    if (b < nb) block_sums[b] = carry + ex;
-    carry += tot;
+  for (int i = 0; i < kScanItems; ++i) {
+    const int r = r0 + i * kScanThreads + threadIdx.x;  // coalesced, i-major
+    g[i] = 0;
+    c[i] = 0;
+    if (r < n) {
+      if (MODE == kRank) {
+        g[i] = __ldg(a.perm + r);
+        c[i] = __ldg(a.touched + g[i]);
+      } else if (MODE == kCompact) {
+        c[i] = __ldg(a.touched + r) > 0 ? 1u : 0u;
+      } else {
+        c[i] = __ldg(a.touched + r);
+      }
+    }
+  }
+  // items are i-major across the CTA; scan chunk by chunk so positions follow r order
+  uint32_t run = 0;
+  uint32_t ex[kScanItems];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    uint32_t t_i;
+    const uint32_t e = block_exclusive_scan<kScanThreads>(c[i], s_warp, &t_i);
+    ex[i] = run + e;
+    run += t_i;
     __syncthreads();
   }
-  if (threadIdx.x == 0) *total_out = carry;
-}
-
-__global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(const uint32_t* __restrict__ perm,
-                                                                  const uint32_t* __restrict__ touched,
-                                                                  const uint32_t* __restrict__ block_sums,
-                                                                  uint32_t* __restrict__ offsets,
-                                                                  uint32_t* __restrict__ rank, int n) {
-  __shared__ uint32_t s_warp[kScanThreads / 32];
-  const int r0 = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
-  uint32_t c[kScanItems], s = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    c[i] = touched_at(perm, touched, r0 + i, n);
-    s += c[i];
-  }
-  uint32_t run = block_sums[blockIdx.x] + block_exclusive_scan<kScanThreads>(s, s_warp, nullptr);
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int r = r0 + i;
-    if (r < n) {
-      offsets[r] = run;
-      if (rank) rank[perm ? perm[r] : r] = static_cast<uint32_t>(r);
+  const uint32_t tot = run;
+  if (threadIdx.x == 0) {
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      st_volatile(a.status, (tot << 2) | kFlagInc);
+    } else {
+      st_volatile(a.status + tile, (tot << 2) | kFlagAgg);
+      prefix = look_back(a.status, 1, tile);
+      st_volatile(a.status + tile, ((prefix + tot) << 2) | kFlagInc);
     }
-    run += c[i];
+    s_prefix = prefix;
+    if (r0 + kScanTile >= n) *a.total_out = prefix + tot;
+  }
+  __syncthreads();
+  const uint32_t prefix = s_prefix;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int r = r0 + i * kScanThreads + threadIdx.x;
+    if (r >= n) continue;
+    const uint32_t pos = prefix + ex[i];
+    if (MODE == kCompact) {
+      if (c[i]) {
+        a.keys_out[pos] = __ldg(a.depth_key + r);
+        a.vals_out[pos] = static_cast<uint32_t>(r);
+      }
+    } else {
+      a.offsets[r] = pos;
+      if (MODE == kRank) a.rank[g[i]] = static_cast<uint32_t>(r);
+    }
   }
 }
 
@@ -278,7 +323,9 @@ __global__ void __launch_bounds__(256) duplicate_kernel(const uint32_t* __restri
                                                         const ushort4* __restrict__ rect, int tiles_x,
                                                         uint32_t* __restrict__ tile_keys,
                                                         uint32_t* __restrict__ emit_vals,
-                                                        uint32_t* __restrict__ emit_gauss, int n) {
+                                                        uint32_t* __restrict__ emit_gauss, const uint32_t* n_dev,
+                                                        int n_max) {
+  const int n = load_n(n_dev, n_max);
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const uint32_t g = __ldg(perm + r);
@@ -328,23 +375,35 @@ __global__ void __launch_bounds__(256) debug_keys_kernel(const uint32_t* __restr
     }
 }
 
+int launch_scan(int mode, ScanArgs a, cudaStream_t st) {
+  const int tiles = max(1, div_up(a.n_max, kScanTile));
+  cudaMemsetAsync(a.status, 0, sizeof(uint32_t) * (tiles + 1), st);
+  cudaMemsetAsync(a.counter, 0, sizeof(uint32_t), st);
+  if (mode == kCompact) scan_kernel<kCompact><<<tiles, kScanThreads, 0, st>>>(a);
+  else if (mode == kRank) scan_kernel<kRank><<<tiles, kScanThreads, 0, st>>>(a);
+  else scan_kernel<kPlain><<<tiles, kScanThreads, 0, st>>>(a);
+  return 1;
+}
+
 }  // namespace
 
+size_t scan_status_words(int n_max) { return static_cast<size_t>(max(1, div_up(n_max, kScanTile))) + 2; }
+
 SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_a, uint32_t* vals_a,
-                            uint32_t* keys_b, uint32_t* vals_b, int n, int passes, const SortScratch& s,
-                            cudaStream_t st) {
+                            uint32_t* keys_b, uint32_t* vals_b, const uint32_t* n_dev, int n_max, int passes,
+                            const SortScratch& s, cudaStream_t st) {
   SortResult r{const_cast<uint32_t*>(keys_in), const_cast<uint32_t*>(vals_in), 0};
-  if (n <= 0 || passes <= 0) return r;
-  const int tiles = div_up(n, kSortTile);
+  if (n_max <= 0 || passes <= 0) return r;
+  const int tiles = div_up(n_max, kSortTile);
   cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * 256 * passes, st);
   cudaMemsetAsync(s.lookback, 0, sizeof(uint32_t) * 256 * static_cast<size_t>(tiles) * passes, st);
   cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * passes, st);
-  const int hist_grid = max(1, min(div_up(n, 256 * 16), 148 * 4));
+  const int hist_grid = max(1, min(div_up(n_max, 256 * 16), 148 * 4));
   switch (passes) {
-    case 1: radix_hist_kernel<1><<<hist_grid, 256, 0, st>>>(keys_in, n, s.hist); break;
-    case 2: radix_hist_kernel<2><<<hist_grid, 256, 0, st>>>(keys_in, n, s.hist); break;
-    case 3: radix_hist_kernel<3><<<hist_grid, 256, 0, st>>>(keys_in, n, s.hist); break;
-    default: radix_hist_kernel<4><<<hist_grid, 256, 0, st>>>(keys_in, n, s.hist); break;
+    case 1: radix_hist_kernel<1><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
+    case 2: radix_hist_kernel<2><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
+    case 3: radix_hist_kernel<3><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
+    default: radix_hist_kernel<4><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
   }
   radix_hist_scan_kernel<<<passes, 256, 0, st>>>(s.hist);
   r.launches = 2 + passes;
@@ -352,7 +411,7 @@ SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, ui
   for (int p = 0; p < passes; ++p) {
     uint32_t* ko = (p & 1) ? keys_a : keys_b;
     uint32_t* vo = (p & 1) ? vals_a : vals_b;
-    onesweep_kernel<<<tiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n, 8 * p, s.hist + 256 * p,
+    onesweep_kernel<<<tiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, 8 * p, s.hist + 256 * p,
                                                    s.lookback + static_cast<size_t>(256) * tiles * p,
                                                    s.counters + p);
     ki = ko;
@@ -363,20 +422,43 @@ SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, ui
   return r;
 }
 
-int rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, uint32_t* rank, uint32_t* block_sums,
-              uint32_t* total_out, int n, cudaStream_t st) {
-  const int nb = max(1, div_up(n, kScanTile));
-  scan_block_sums_kernel<<<nb, kScanThreads, 0, st>>>(perm, touched, block_sums, n);
-  scan_top_kernel<<<1, 1024, 0, st>>>(block_sums, nb, total_out);
-  scan_apply_kernel<<<nb, kScanThreads, 0, st>>>(perm, touched, block_sums, offsets, rank, n);
-  return 3;
+int compact_visible(const uint32_t* touched, const uint32_t* depth_key, uint32_t* keys_out, uint32_t* vals_out,
+                    uint32_t* count_out, int n, uint32_t* status, uint32_t* counter, cudaStream_t st) {
+  ScanArgs a{};
+  a.touched = touched;
+  a.depth_key = depth_key;
+  a.keys_out = keys_out;
+  a.vals_out = vals_out;
+  a.n_dev = nullptr;
+  a.n_max = n;
+  a.status = status;
+  a.counter = counter;
+  a.total_out = count_out;
+  return launch_scan(kCompact, a, st);
+}
+
+int rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, uint32_t* rank,
+              const uint32_t* n_dev, int n_max, uint32_t* total_out, uint32_t* status, uint32_t* counter,
+              cudaStream_t st) {
+  ScanArgs a{};
+  a.touched = touched;
+  a.perm = perm;
+  a.offsets = offsets;
+  a.rank = rank;
+  a.n_dev = n_dev;
+  a.n_max = n_max;
+  a.status = status;
+  a.counter = counter;
+  a.total_out = total_out;
+  return launch_scan(kRank, a, st);
 }
 
 int duplicate(const uint32_t* perm, const uint32_t* offsets, const uint32_t* touched, const ushort4* rect, int tiles_x,
-              uint32_t* tile_keys, uint32_t* emit_vals, uint32_t* emit_gauss, int n, cudaStream_t st) {
-  if (n <= 0) return 0;
-  duplicate_kernel<<<div_up(n, 256), 256, 0, st>>>(perm, offsets, touched, rect, tiles_x, tile_keys, emit_vals,
-                                                   emit_gauss, n);
+              uint32_t* tile_keys, uint32_t* emit_vals, uint32_t* emit_gauss, const uint32_t* n_dev, int n_max,
+              cudaStream_t st) {
+  if (n_max <= 0) return 0;
+  duplicate_kernel<<<div_up(n_max, 256), 256, 0, st>>>(perm, offsets, touched, rect, tiles_x, tile_keys, emit_vals,
+                                                       emit_gauss, n_dev, n_max);
   return 1;
 }
 
@@ -392,10 +474,17 @@ int tile_ranges(const uint32_t* sorted_tiles, const uint32_t* sorted_emit, const
 }
 
 void debug_source_order_keys(const uint32_t* touched, const ushort4* rect, const uint32_t* depth_key, int tiles_x,
-                             int n, uint32_t* scratch_offsets, uint32_t* block_sums, uint32_t* total,
+                             int n, uint32_t* scratch_offsets, uint32_t* status, uint32_t* counter, uint32_t* total,
                              uint32_t* key_tile, uint32_t* key_depth, uint32_t* key_gauss, cudaStream_t st) {
   if (n <= 0) return;
-  rank_scan(nullptr, touched, scratch_offsets, nullptr, block_sums, total, n, st);
+  ScanArgs a{};
+  a.touched = touched;
+  a.offsets = scratch_offsets;
+  a.n_max = n;
+  a.status = status;
+  a.counter = counter;
+  a.total_out = total;
+  launch_scan(kPlain, a, st);
   debug_keys_kernel<<<div_up(n, 256), 256, 0, st>>>(scratch_offsets, touched, rect, depth_key, tiles_x, key_tile,
                                                     key_depth, key_gauss, n);
 }

@@ -54,7 +54,7 @@ struct fgs_context {
   DevBuf<float4> rec0, rec1;
   DevBuf<float> rec2;
   DevBuf<uint8_t> state;
-  DevBuf<uint32_t> dkey, dkey_a, dkey_b, iota, perm_a, perm_b, touched, rank, offsets, block_sums;
+  DevBuf<uint32_t> dkey, ckey, cval, dkey_a, dkey_b, perm_a, perm_b, touched, rank, offsets, scan_status;
   DevBuf<ushort4> rect;
   DevBuf<int32_t> radii;
   // per intersection
@@ -65,7 +65,8 @@ struct fgs_context {
   DevBuf<float> final_T;
   // sort scratch
   DevBuf<uint32_t> hist, lookback, sort_counters;
-  // misc device scalars: [0] total I, [1] error flag, [2..3] state counts
+  // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
+  // [5] scan tile counter
   DevBuf<uint32_t> scalars;
   DevBuf<unsigned long long> counters;
   uint32_t* h_scalars = nullptr;  // pinned
@@ -215,8 +216,8 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->rec0.release();
   ctx->rec1.release();
   ctx->state.release();
-  for (auto* b : {&ctx->dkey, &ctx->dkey_a, &ctx->dkey_b, &ctx->iota, &ctx->perm_a, &ctx->perm_b, &ctx->touched,
-                  &ctx->rank, &ctx->offsets, &ctx->block_sums, &ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b,
+  for (auto* b : {&ctx->dkey, &ctx->ckey, &ctx->cval, &ctx->dkey_a, &ctx->dkey_b, &ctx->perm_a, &ctx->perm_b,
+                  &ctx->touched, &ctx->rank, &ctx->offsets, &ctx->scan_status, &ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b,
                   &ctx->emit_a, &ctx->emit_b, &ctx->emit_gauss, &ctx->sorted_gauss, &ctx->tile_offsets, &ctx->last,
                   &ctx->hist, &ctx->lookback, &ctx->sort_counters, &ctx->scalars})
     b->release();
@@ -288,10 +289,10 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   FGS_CHECK(ctx->rec1.ensure(nn));
   FGS_CHECK(ctx->rec2.ensure(nn));
   FGS_CHECK(ctx->state.ensure(nn));
-  for (auto* b : {&ctx->dkey, &ctx->dkey_a, &ctx->dkey_b, &ctx->iota, &ctx->perm_a, &ctx->perm_b, &ctx->touched,
-                  &ctx->rank, &ctx->offsets})
+  for (auto* b : {&ctx->dkey, &ctx->ckey, &ctx->cval, &ctx->dkey_a, &ctx->dkey_b, &ctx->perm_a, &ctx->perm_b,
+                  &ctx->touched, &ctx->rank, &ctx->offsets})
     FGS_CHECK(b->ensure(nn));
-  FGS_CHECK(ctx->block_sums.ensure(nn / 1024 + 2));
+  FGS_CHECK(ctx->scan_status.ensure(fgs::scan_status_words(static_cast<int>(nn))));
   FGS_CHECK(ctx->rect.ensure(nn));
   FGS_CHECK(ctx->radii.ensure(nn));
   FGS_CHECK(ctx->tile_offsets.ensure(num_tiles + 1));
@@ -333,7 +334,6 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.rec2 = ctx->rec2.p;
     pa.state = ctx->state.p;
     pa.depth_key = ctx->dkey.p;
-    pa.gauss_iota = ctx->iota.p;
     pa.touched = ctx->touched.p;
     pa.rect = ctx->rect.p;
     pa.radii = ctx->radii.p;
@@ -343,19 +343,25 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     ++launches;
   }
   if (timing) cudaEventRecord(ev[1], st);
-  // level 1: Gaussians by depth key (stable; ties keep source order)
-  const fgs::SortResult l1 = fgs::radix_sort_pairs(ctx->dkey.p, ctx->iota.p, ctx->dkey_a.p, ctx->perm_a.p,
-                                                   ctx->dkey_b.p, ctx->perm_b.p, static_cast<int>(n), 4, ss, st);
-  ctx->perm = l1.vals;
-  launches += l1.launches;
-  if (n > 0)
-    launches += fgs::rank_scan(ctx->perm, ctx->touched.p, ctx->offsets.p, ctx->rank.p, ctx->block_sums.p, ctx->scalars.p,
-                   static_cast<int>(n), st);
-  FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, ctx->scalars.p, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  // compact the Gaussians that touch a tile, then level 1: sort them by depth key (stable;
+  // ties keep source order); then the exclusive scan of their tile counts in depth order
+  uint32_t* d_m = ctx->scalars.p + 4;
+  if (n > 0) {
+    launches += fgs::compact_visible(ctx->touched.p, ctx->dkey.p, ctx->ckey.p, ctx->cval.p, d_m, static_cast<int>(n),
+                                     ctx->scan_status.p, ctx->scalars.p + 5, st);
+    const fgs::SortResult l1 = fgs::radix_sort_pairs(ctx->ckey.p, ctx->cval.p, ctx->dkey_a.p, ctx->perm_a.p,
+                                                     ctx->dkey_b.p, ctx->perm_b.p, d_m, static_cast<int>(n), 4, ss, st);
+    ctx->perm = l1.vals;
+    launches += l1.launches;
+    launches += fgs::rank_scan(ctx->perm, ctx->touched.p, ctx->offsets.p, ctx->rank.p, d_m, static_cast<int>(n),
+                               ctx->scalars.p, ctx->scan_status.p, ctx->scalars.p + 5, st);
+  }
+  FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, ctx->scalars.p, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   FGS_CHECK(cudaStreamSynchronize(st));
   FGS_CHECK(cudaGetLastError());
   if (ctx->h_scalars[1]) return fail(ctx, FGS_EDEGENERATE_QUAT, "degenerate rotation: quaternion has zero norm");
   const int64_t I = ctx->h_scalars[0];
+  const int M = static_cast<int>(ctx->h_scalars[4]);
   ctx->num_isect = I;
   ctx->num_splats = ctx->h_scalars[2];
   ctx->num_degenerate = ctx->h_scalars[3];
@@ -368,13 +374,14 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     FGS_CHECK(b->ensure(ni));
   FGS_CHECK(ctx->lookback.ensure(static_cast<size_t>(4) * 256 * (ni / fgs::kSortTile + 1)));
   ss.lookback = ctx->lookback.p;
-  if (n > 0)
-    launches += fgs::duplicate(ctx->perm, ctx->offsets.p, ctx->touched.p, ctx->rect.p, tiles_x, ctx->tkey.p, ctx->emit.p,
-                   ctx->emit_gauss.p, static_cast<int>(n), st);
+  if (M > 0)
+    launches += fgs::duplicate(ctx->perm, ctx->offsets.p, ctx->touched.p, ctx->rect.p, tiles_x, ctx->tkey.p,
+                               ctx->emit.p, ctx->emit_gauss.p, nullptr, M, st);
   if (timing) cudaEventRecord(ev[2], st);
   const int passes2 = num_tiles <= 256 ? 1 : (num_tiles <= 65536 ? 2 : 3);
   const fgs::SortResult l2 = fgs::radix_sort_pairs(ctx->tkey.p, ctx->emit.p, ctx->tkey_a.p, ctx->emit_a.p,
-                                                   ctx->tkey_b.p, ctx->emit_b.p, static_cast<int>(I), passes2, ss, st);
+                                                   ctx->tkey_b.p, ctx->emit_b.p, nullptr, static_cast<int>(I), passes2,
+                                                   ss, st);
   ctx->sorted_tiles = l2.keys;
   ctx->sorted_emit = l2.vals;
   launches += l2.launches;
@@ -631,11 +638,11 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
     if (!dst) return static_cast<int64_t>(I * 4);
     // Recompute the reference's pre-sort emission order (source order) on demand.
     DevBuf<uint32_t> kt, kd, kg, off, bs, tot;
-    if (kt.ensure(I + 1) || kd.ensure(I + 1) || kg.ensure(I + 1) || off.ensure(n + 1) || bs.ensure(n / 1024 + 2) ||
-        tot.ensure(1))
+    if (kt.ensure(I + 1) || kd.ensure(I + 1) || kg.ensure(I + 1) || off.ensure(n + 1) ||
+        bs.ensure(fgs::scan_status_words(static_cast<int>(n))) || tot.ensure(2))
       return -1;
     fgs::debug_source_order_keys(ctx->touched.p, ctx->rect.p, ctx->dkey.p, ctx->tiles_x, static_cast<int>(n), off.p,
-                                 bs.p, tot.p, kt.p, kd.p, kg.p, st);
+                                 bs.p, tot.p + 1, tot.p, kt.p, kd.p, kg.p, st);
     const uint32_t* src = nm == "key_tile" ? kt.p : (nm == "key_depth" ? kd.p : kg.p);
     const int64_t r = copy(src, I * 4);
     for (auto* b : {&kt, &kd, &kg, &off, &bs, &tot}) b->release();

@@ -347,7 +347,6 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
   a.rec2[i] = r2v;
   a.state[i] = state;
   a.depth_key[i] = key;
-  a.gauss_iota[i] = static_cast<uint32_t>(i);
   a.touched[i] = touched;
   a.rect[i] = rect;
   a.radii[i] = state == 1 ? radius : 0;
