@@ -14,7 +14,7 @@
 // The radix sort is a single-pass-per-digit "onesweep" LSD sort: one histogram kernel for all
 // digit passes, then per pass one kernel whose CTAs take tiles in launch order from an atomic
 // counter, rank their keys with warp match-based multisplit, resolve global digit offsets by
-// decoupled look-back (each digit's thread loads 4 predecessor statuses per step), and
+// decoupled look-back (each digit's thread loads 16 predecessor statuses per step), and
 // scatter through shared memory. Element counts may live in device memory (written by the
 // previous kernel), so the grid is sized for the maximum and surplus CTAs exit.
 
@@ -73,23 +73,26 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   return warp_prefix + x - v;
 }
 
-// Decoupled look-back of one 30-bit value for tile `tile` (status words: value<<2 | flag).
-// Called by a single thread; loads 4 predecessors per step.
+// Decoupled look-back of one 30-bit value for tile `tile` (status words: value<<2 | flag),
+// predecessors at status[j * stride]. Called by a single thread; issues 16 independent loads
+// per step (nearest first) so that a tile whose predecessors all run concurrently walks
+// back 16 tiles per memory round trip.
 __device__ __forceinline__ uint32_t look_back(const uint32_t* status, size_t stride, int tile) {
+  constexpr int K = 16;
   uint32_t prefix = 0;
   int j = tile - 1;
   while (true) {
-    uint32_t s[4];
+    uint32_t s[K];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) s[q] = j - q >= 0 ? ld_volatile(status + static_cast<size_t>(j - q) * stride) : 0u;
+    for (int q = 0; q < K; ++q) s[q] = j - q >= 0 ? ld_volatile(status + static_cast<size_t>(j - q) * stride) : 0u;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < K; ++q) {
       uint32_t v = s[q];
       while ((v & 3u) == 0u) v = ld_volatile(status + static_cast<size_t>(j - q) * stride);
       prefix += v >> 2;
       if ((v & 3u) == kFlagInc) return prefix;
     }
-    j -= 4;
+    j -= K;
   }
 }
 
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* 
                                                                 uint32_t* __restrict__ vals_out,
                                                                 const uint32_t* n_dev, int n_max, int shift,
                                                                 const uint32_t* __restrict__ digit_offsets,
-                                                                uint32_t* __restrict__ lookback,
+                                                                uint32_t* __restrict__ lookback, int num_tiles,
                                                                 uint32_t* __restrict__ tile_counter) {
   constexpr int W = kSortThreads / 32;
   __shared__ uint32_t s_tile;
@@ -192,13 +195,15 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* 
     total += c;
   }
   // Publish this tile's aggregate for digit tid, then look back.
-  uint32_t* mine = lookback + static_cast<size_t>(tile) * 256 + tid;
+  // status layout [digit][tile]: a digit's predecessors are contiguous
+  uint32_t* row = lookback + static_cast<size_t>(tid) * num_tiles;
+  uint32_t* mine = row + tile;
   uint32_t prefix = 0;
   if (tile == 0) {
     st_volatile(mine, (total << 2) | kFlagInc);
   } else {
     st_volatile(mine, (total << 2) | kFlagAgg);
-    prefix = look_back(lookback + tid, 256, static_cast<int>(tile));
+    prefix = look_back(row, 1, static_cast<int>(tile));
     st_volatile(mine, ((prefix + total) << 2) | kFlagInc);
   }
   s_global_start[tid] = digit_offsets[tid] + prefix;
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* 
 
 // ---- single-pass scans (chained, decoupled look-back) ----
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 4;
+constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 enum ScanMode { kCompact = 0, kRank = 1, kPlain = 2 };
@@ -257,10 +262,12 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
   const int tile = static_cast<int>(s_tile);
   const int r0 = tile * kScanTile;
   if (r0 >= n && !(tile == 0 && n == 0)) return;
+  // thread-contiguous items: r = r0 + threadIdx.x * kScanItems + i
+  const int rt = r0 + threadIdx.x * kScanItems;
   uint32_t c[kScanItems], g[kScanItems];
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
-    const int r = r0 + i * kScanThreads + threadIdx.x;  // coalesced, i-major
+    const int r = rt + i;
     g[i] = 0;
     c[i] = 0;
     if (r < n) {
@@ -274,18 +281,11 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
       }
     }
   }
-  // items are i-major across the CTA; scan chunk by chunk so positions follow r order
-  uint32_t run = 0;
-  uint32_t ex[kScanItems];
+  uint32_t sum = 0;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    uint32_t t_i;
-    const uint32_t e = block_exclusive_scan<kScanThreads>(c[i], s_warp, &t_i);
-    ex[i] = run + e;
-    run += t_i;
-    __syncthreads();
-  }
-  const uint32_t tot = run;
+  for (int i = 0; i < kScanItems; ++i) sum += c[i];
+  uint32_t tot;
+  const uint32_t ex_t = block_exclusive_scan<kScanThreads>(sum, s_warp, &tot);
   if (threadIdx.x == 0) {
     uint32_t prefix = 0;
     if (tile == 0) {
@@ -299,21 +299,22 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
     if (r0 + kScanTile >= n) *a.total_out = prefix + tot;
   }
   __syncthreads();
-  const uint32_t prefix = s_prefix;
+  uint32_t pos = s_prefix + ex_t;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
-    const int r = r0 + i * kScanThreads + threadIdx.x;
-    if (r >= n) continue;
-    const uint32_t pos = prefix + ex[i];
-    if (MODE == kCompact) {
-      if (c[i]) {
-        a.keys_out[pos] = __ldg(a.depth_key + r);
-        a.vals_out[pos] = static_cast<uint32_t>(r);
+    const int r = rt + i;
+    if (r < n) {
+      if (MODE == kCompact) {
+        if (c[i]) {
+          a.keys_out[pos] = __ldg(a.depth_key + r);
+          a.vals_out[pos] = static_cast<uint32_t>(r);
+        }
+      } else {
+        a.offsets[r] = pos;
+        if (MODE == kRank) a.rank[g[i]] = static_cast<uint32_t>(r);
       }
-    } else {
-      a.offsets[r] = pos;
-      if (MODE == kRank) a.rank[g[i]] = static_cast<uint32_t>(r);
     }
+    pos += c[i];
   }
 }
 
@@ -412,7 +413,7 @@ SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, ui
     uint32_t* ko = (p & 1) ? keys_a : keys_b;
     uint32_t* vo = (p & 1) ? vals_a : vals_b;
     onesweep_kernel<<<tiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, 8 * p, s.hist + 256 * p,
-                                                   s.lookback + static_cast<size_t>(256) * tiles * p,
+                                                   s.lookback + static_cast<size_t>(256) * tiles * p, tiles,
                                                    s.counters + p);
     ki = ko;
     vi = vo;

@@ -82,8 +82,8 @@ struct SortScratch {
   int max_tiles;
 };
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 8;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 2048
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
 constexpr int kMaxPasses = 4;
 
 // Stable LSD radix sort of (u32 key, u32 value) over bits [0, 8*passes). The inputs are not
