@@ -11,8 +11,9 @@
 //   level 2: stable sort of the I intersections by tile id.
 // Stability of both levels gives exactly (tile, depth, source).
 //
-// The radix sort is a single-pass-per-digit "onesweep" LSD sort: one histogram kernel for all
-// digit passes, then per pass one kernel whose CTAs take tiles in launch order from an atomic
+// The radix sort is a single-pass-per-digit "onesweep" LSD sort: the digit histograms of all
+// passes are accumulated by the kernel that produces the keys (compaction / duplication),
+// then per pass one kernel whose CTAs take tiles in launch order from an atomic
 // counter, rank their keys with warp match-based multisplit, resolve global digit offsets by
 // decoupled look-back (each digit's thread loads 16 predecessor statuses per step), and
 // scatter through shared memory. Element counts may live in device memory (written by the
@@ -126,37 +127,35 @@ __global__ void __launch_bounds__(256) radix_hist_kernel(const uint32_t* __restr
     if (h[j]) atomicAdd(&hist[j], h[j]);
 }
 
-// One CTA per pass: exclusive scan of the 256 digit counts.
-__global__ void __launch_bounds__(256) radix_hist_scan_kernel(uint32_t* hist) {
-  __shared__ uint32_t s_warp[8];
-  uint32_t* h = hist + blockIdx.x * 256;
-  const uint32_t v = h[threadIdx.x];
-  h[threadIdx.x] = block_exclusive_scan<256>(v, s_warp, nullptr);
-}
+// Dynamic shared memory layout of onesweep_kernel.
+struct OnesweepSmem {
+  uint32_t keys[kSortTile];
+  uint32_t vals[kSortTile];
+  uint32_t warp_hist[kSortThreads / 32][256];
+  uint32_t local_start[256];
+  uint32_t global_start[256];
+  uint32_t scan[kSortThreads / 32];
+  uint32_t tile;
+};
 
 __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* __restrict__ keys_in,
                                                                 const uint32_t* __restrict__ vals_in,
                                                                 uint32_t* __restrict__ keys_out,
                                                                 uint32_t* __restrict__ vals_out,
                                                                 const uint32_t* n_dev, int n_max, int shift,
-                                                                const uint32_t* __restrict__ digit_offsets,
-                                                                uint32_t* __restrict__ lookback, int num_tiles,
+                                                                const uint32_t* __restrict__ digit_counts,
+                                                                uint32_t* __restrict__ lookback,
                                                                 uint32_t* __restrict__ tile_counter) {
   constexpr int W = kSortThreads / 32;
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_warp_hist[W][256];
-  __shared__ uint32_t s_local_start[256];
-  __shared__ uint32_t s_global_start[256];
-  __shared__ uint32_t s_scan[W];
-  __shared__ uint32_t s_keys[kSortTile];
-  __shared__ uint32_t s_vals[kSortTile];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  OnesweepSmem& sm = *reinterpret_cast<OnesweepSmem*>(smem_raw);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = load_n(n_dev, n_max);
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int j = tid; j < W * 256; j += kSortThreads) (&s_warp_hist[0][0])[j] = 0;
+  if (tid == 0) sm.tile = atomicAdd(tile_counter, 1u);
+  for (int j = tid; j < W * 256; j += kSortThreads) (&sm.warp_hist[0][0])[j] = 0;
   __syncthreads();
-  const uint32_t tile = s_tile;
+  const uint32_t tile = sm.tile;
   const int base = static_cast<int>(tile) * kSortTile;
   if (base >= n) return;  // surplus CTA (count known only on device)
   const int warp_base = base + warp * (32 * kSortItems);
@@ -169,7 +168,10 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* 
     k[i] = valid ? __ldg(keys_in + idx) : 0xFFFFFFFFu;
     v[i] = valid ? __ldg(vals_in + idx) : 0u;
   }
-  uint32_t* wh = s_warp_hist[warp];
+  // this pass's global digit offsets: exclusive scan of the pass histogram (every CTA
+  // computes it; 256 values)
+  const uint32_t dcount = tid < 256 ? __ldg(digit_counts + tid) : 0u;
+  uint32_t* wh = sm.warp_hist[warp];
   const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
@@ -188,51 +190,57 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const uint32_t* 
   __syncthreads();
   // Per digit (thread = digit): exclusive scan over warps, CTA total.
   uint32_t total = 0;
+  if (tid < 256) {
 #pragma unroll
-  for (int w = 0; w < W; ++w) {
-    const uint32_t c = s_warp_hist[w][tid];
-    s_warp_hist[w][tid] = total;
-    total += c;
+    for (int w = 0; w < W; ++w) {
+      const uint32_t c = sm.warp_hist[w][tid];
+      sm.warp_hist[w][tid] = total;
+      total += c;
+    }
   }
-  // Publish this tile's aggregate for digit tid, then look back.
-  // status layout [digit][tile]: a digit's predecessors are contiguous
-  uint32_t* row = lookback + static_cast<size_t>(tid) * num_tiles;
-  uint32_t* mine = row + tile;
+  // Publish this tile's aggregate for digit tid, then look back ([tile][digit] layout: a
+  // warp's 32 digits of one predecessor are one 128-byte line).
   uint32_t prefix = 0;
-  if (tile == 0) {
-    st_volatile(mine, (total << 2) | kFlagInc);
-  } else {
-    st_volatile(mine, (total << 2) | kFlagAgg);
-    prefix = look_back(row, 1, static_cast<int>(tile));
-    st_volatile(mine, ((prefix + total) << 2) | kFlagInc);
+  if (tid < 256) {
+    uint32_t* mine = lookback + static_cast<size_t>(tile) * 256 + tid;
+    if (tile == 0) {
+      st_volatile(mine, (total << 2) | kFlagInc);
+    } else {
+      st_volatile(mine, (total << 2) | kFlagAgg);
+      prefix = look_back(lookback + tid, 256, static_cast<int>(tile));
+      st_volatile(mine, ((prefix + total) << 2) | kFlagInc);
+    }
   }
-  s_global_start[tid] = digit_offsets[tid] + prefix;
-  s_local_start[tid] = block_exclusive_scan<kSortThreads>(total, s_scan, nullptr);
+  const uint32_t goff = block_exclusive_scan<kSortThreads>(dcount, sm.scan, nullptr);
+  if (tid < 256) sm.global_start[tid] = goff + prefix;
+  __syncthreads();
+  const uint32_t lstart = block_exclusive_scan<kSortThreads>(total, sm.scan, nullptr);
+  if (tid < 256) sm.local_start[tid] = lstart;
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const bool valid = (warp_base + i * 32 + lane) < n;
     if (valid) {
       const uint32_t d = (k[i] >> shift) & 255u;
-      const uint32_t pos = s_local_start[d] + s_warp_hist[warp][d] + rank[i];
-      s_keys[pos] = k[i];
-      s_vals[pos] = v[i];
+      const uint32_t pos = sm.local_start[d] + sm.warp_hist[warp][d] + rank[i];
+      sm.keys[pos] = k[i];
+      sm.vals[pos] = v[i];
     }
   }
   __syncthreads();
   const int n_tile = min(kSortTile, n - base);
   for (int p = tid; p < n_tile; p += kSortThreads) {
-    const uint32_t key = s_keys[p];
+    const uint32_t key = sm.keys[p];
     const uint32_t d = (key >> shift) & 255u;
-    const uint32_t gi = s_global_start[d] + (static_cast<uint32_t>(p) - s_local_start[d]);
+    const uint32_t gi = sm.global_start[d] + (static_cast<uint32_t>(p) - sm.local_start[d]);
     keys_out[gi] = key;
-    vals_out[gi] = s_vals[p];
+    vals_out[gi] = sm.vals[p];
   }
 }
 
 // ---- single-pass scans (chained, decoupled look-back) ----
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 enum ScanMode { kCompact = 0, kRank = 1, kPlain = 2 };
@@ -250,12 +258,16 @@ struct ScanArgs {
   uint32_t* status;           // one word per tile, zeroed
   uint32_t* counter;          // tile counter, zeroed
   uint32_t* total_out;
+  uint32_t* hist;             // kCompact: 4 x 256 digit counts of the compacted keys (zeroed)
 };
 
 template <int MODE>
 __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
   __shared__ uint32_t s_tile, s_prefix;
   __shared__ uint32_t s_warp[kScanThreads / 32];
+  __shared__ uint32_t s_hist[MODE == kCompact ? 4 * 256 : 1];
+  if (MODE == kCompact)
+    for (int j = threadIdx.x; j < 4 * 256; j += kScanThreads) s_hist[j] = 0;
   const int n = load_n(a.n_dev, a.n_max);
   if (threadIdx.x == 0) s_tile = atomicAdd(a.counter, 1u);
   __syncthreads();
@@ -306,8 +318,11 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
     if (r < n) {
       if (MODE == kCompact) {
         if (c[i]) {
-          a.keys_out[pos] = __ldg(a.depth_key + r);
+          const uint32_t key = __ldg(a.depth_key + r);
+          a.keys_out[pos] = key;
           a.vals_out[pos] = static_cast<uint32_t>(r);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) atomicAdd(&s_hist[p * 256 + ((key >> (8 * p)) & 255u)], 1u);
         }
       } else {
         a.offsets[r] = pos;
@@ -315,6 +330,11 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
       }
     }
     pos += c[i];
+  }
+  if (MODE == kCompact) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 4 * 256; j += kScanThreads)
+      if (s_hist[j]) atomicAdd(&a.hist[j], s_hist[j]);
   }
 }
 
@@ -325,21 +345,32 @@ __global__ void __launch_bounds__(256) duplicate_kernel(const uint32_t* __restri
                                                         uint32_t* __restrict__ tile_keys,
                                                         uint32_t* __restrict__ emit_vals,
                                                         uint32_t* __restrict__ emit_gauss, const uint32_t* n_dev,
-                                                        int n_max) {
+                                                        int n_max, uint32_t* __restrict__ hist, int passes) {
+  __shared__ uint32_t s_hist[2 * 256];
+  for (int j = threadIdx.x; j < 2 * 256; j += blockDim.x) s_hist[j] = 0;
+  __syncthreads();
   const int n = load_n(n_dev, n_max);
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const uint32_t g = __ldg(perm + r);
-  if (__ldg(touched + g) == 0) return;
-  const ushort4 b = rect[g];
-  uint32_t e = __ldg(offsets + r);
-  for (int ty = b.z; ty <= b.w; ++ty)
-    for (int tx = b.x; tx <= b.y; ++tx) {
-      tile_keys[e] = static_cast<uint32_t>(ty * tiles_x + tx);
-      emit_vals[e] = e;
-      emit_gauss[e] = g;
-      ++e;
+  if (r < n) {
+    const uint32_t g = __ldg(perm + r);
+    if (__ldg(touched + g) != 0) {
+      const ushort4 b = rect[g];
+      uint32_t e = __ldg(offsets + r);
+      for (int ty = b.z; ty <= b.w; ++ty)
+        for (int tx = b.x; tx <= b.y; ++tx) {
+          const uint32_t t = static_cast<uint32_t>(ty * tiles_x + tx);
+          tile_keys[e] = t;
+          emit_vals[e] = e;
+          emit_gauss[e] = g;
+          ++e;
+          atomicAdd(&s_hist[t & 255u], 1u);
+          if (passes > 1) atomicAdd(&s_hist[256 + ((t >> 8) & 255u)], 1u);
+        }
     }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < passes * 256; j += blockDim.x)
+    if (s_hist[j]) atomicAdd(&hist[j], s_hist[j]);
 }
 
 __global__ void __launch_bounds__(256) tile_ranges_kernel(const uint32_t* __restrict__ sorted_tiles,
@@ -392,29 +423,36 @@ size_t scan_status_words(int n_max) { return static_cast<size_t>(max(1, div_up(n
 
 SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_a, uint32_t* vals_a,
                             uint32_t* keys_b, uint32_t* vals_b, const uint32_t* n_dev, int n_max, int passes,
-                            const SortScratch& s, cudaStream_t st) {
+                            const SortScratch& s, bool hist_ready, cudaStream_t st) {
   SortResult r{const_cast<uint32_t*>(keys_in), const_cast<uint32_t*>(vals_in), 0};
   if (n_max <= 0 || passes <= 0) return r;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(OnesweepSmem));
+    configured = true;
+  }
   const int tiles = div_up(n_max, kSortTile);
-  cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * 256 * passes, st);
   cudaMemsetAsync(s.lookback, 0, sizeof(uint32_t) * 256 * static_cast<size_t>(tiles) * passes, st);
   cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * passes, st);
-  const int hist_grid = max(1, min(div_up(n_max, 256 * 16), 148 * 4));
-  switch (passes) {
-    case 1: radix_hist_kernel<1><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
-    case 2: radix_hist_kernel<2><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
-    case 3: radix_hist_kernel<3><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
-    default: radix_hist_kernel<4><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
+  if (!hist_ready) {
+    cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * 256 * passes, st);
+    const int hist_grid = max(1, min(div_up(n_max, 256 * 16), 148 * 4));
+    switch (passes) {
+      case 1: radix_hist_kernel<1><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
+      case 2: radix_hist_kernel<2><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
+      case 3: radix_hist_kernel<3><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
+      default: radix_hist_kernel<4><<<hist_grid, 256, 0, st>>>(keys_in, n_dev, n_max, s.hist); break;
+    }
+    r.launches += 1;
   }
-  radix_hist_scan_kernel<<<passes, 256, 0, st>>>(s.hist);
-  r.launches = 2 + passes;
+  r.launches += passes;
   const uint32_t *ki = keys_in, *vi = vals_in;
   for (int p = 0; p < passes; ++p) {
     uint32_t* ko = (p & 1) ? keys_a : keys_b;
     uint32_t* vo = (p & 1) ? vals_a : vals_b;
-    onesweep_kernel<<<tiles, kSortThreads, 0, st>>>(ki, vi, ko, vo, n_dev, n_max, 8 * p, s.hist + 256 * p,
-                                                   s.lookback + static_cast<size_t>(256) * tiles * p, tiles,
-                                                   s.counters + p);
+    onesweep_kernel<<<tiles, kSortThreads, sizeof(OnesweepSmem), st>>>(
+        ki, vi, ko, vo, n_dev, n_max, 8 * p, s.hist + 256 * p, s.lookback + static_cast<size_t>(256) * tiles * p,
+        s.counters + p);
     ki = ko;
     vi = vo;
     r.keys = ko;
@@ -424,8 +462,11 @@ SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, ui
 }
 
 int compact_visible(const uint32_t* touched, const uint32_t* depth_key, uint32_t* keys_out, uint32_t* vals_out,
-                    uint32_t* count_out, int n, uint32_t* status, uint32_t* counter, cudaStream_t st) {
+                    uint32_t* count_out, int n, uint32_t* status, uint32_t* counter, uint32_t* hist,
+                    cudaStream_t st) {
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * 4, st);
   ScanArgs a{};
+  a.hist = hist;
   a.touched = touched;
   a.depth_key = depth_key;
   a.keys_out = keys_out;
@@ -456,10 +497,11 @@ int rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, 
 
 int duplicate(const uint32_t* perm, const uint32_t* offsets, const uint32_t* touched, const ushort4* rect, int tiles_x,
               uint32_t* tile_keys, uint32_t* emit_vals, uint32_t* emit_gauss, const uint32_t* n_dev, int n_max,
-              cudaStream_t st) {
+              uint32_t* hist, int passes, cudaStream_t st) {
   if (n_max <= 0) return 0;
+  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 256 * passes, st);
   duplicate_kernel<<<div_up(n_max, 256), 256, 0, st>>>(perm, offsets, touched, rect, tiles_x, tile_keys, emit_vals,
-                                                       emit_gauss, n_dev, n_max);
+                                                       emit_gauss, n_dev, n_max, hist, passes);
   return 1;
 }
 

@@ -270,6 +270,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   if (camera->model != FGS_CAMERA_FISHEYE)
     return fail(ctx, FGS_EINVAL, "forward: only the equidistant fisheye camera is implemented on the GPU path");
   if (camera->width <= 0 || camera->height <= 0) return fail(ctx, FGS_EINVAL, "forward: empty image");
+  if ((static_cast<int64_t>(camera->width) + 15) / 16 * ((static_cast<int64_t>(camera->height) + 15) / 16) > 65536)
+    return fail(ctx, FGS_EINVAL, "forward: more than 65536 tiles");
   const int sh_degree = options ? options->sh_degree : 3;
   if (sh_degree < 0 || sh_degree > 3) return fail(ctx, FGS_EINVAL, "forward: sh_degree must be 0..3");
   const int64_t n = scene->n;
@@ -348,9 +350,10 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   uint32_t* d_m = ctx->scalars.p + 4;
   if (n > 0) {
     launches += fgs::compact_visible(ctx->touched.p, ctx->dkey.p, ctx->ckey.p, ctx->cval.p, d_m, static_cast<int>(n),
-                                     ctx->scan_status.p, ctx->scalars.p + 5, st);
+                                     ctx->scan_status.p, ctx->scalars.p + 5, ss.hist, st);
     const fgs::SortResult l1 = fgs::radix_sort_pairs(ctx->ckey.p, ctx->cval.p, ctx->dkey_a.p, ctx->perm_a.p,
-                                                     ctx->dkey_b.p, ctx->perm_b.p, d_m, static_cast<int>(n), 4, ss, st);
+                                                     ctx->dkey_b.p, ctx->perm_b.p, d_m, static_cast<int>(n), 4, ss,
+                                                     true, st);
     ctx->perm = l1.vals;
     launches += l1.launches;
     launches += fgs::rank_scan(ctx->perm, ctx->touched.p, ctx->offsets.p, ctx->rank.p, d_m, static_cast<int>(n),
@@ -374,14 +377,14 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     FGS_CHECK(b->ensure(ni));
   FGS_CHECK(ctx->lookback.ensure(static_cast<size_t>(4) * 256 * (ni / fgs::kSortTile + 1)));
   ss.lookback = ctx->lookback.p;
+  const int passes2 = num_tiles <= 256 ? 1 : 2;
   if (M > 0)
     launches += fgs::duplicate(ctx->perm, ctx->offsets.p, ctx->touched.p, ctx->rect.p, tiles_x, ctx->tkey.p,
-                               ctx->emit.p, ctx->emit_gauss.p, nullptr, M, st);
+                               ctx->emit.p, ctx->emit_gauss.p, nullptr, M, ss.hist, passes2, st);
   if (timing) cudaEventRecord(ev[2], st);
-  const int passes2 = num_tiles <= 256 ? 1 : (num_tiles <= 65536 ? 2 : 3);
   const fgs::SortResult l2 = fgs::radix_sort_pairs(ctx->tkey.p, ctx->emit.p, ctx->tkey_a.p, ctx->emit_a.p,
                                                    ctx->tkey_b.p, ctx->emit_b.p, nullptr, static_cast<int>(I), passes2,
-                                                   ss, st);
+                                                   ss, true, st);
   ctx->sorted_tiles = l2.keys;
   ctx->sorted_emit = l2.vals;
   launches += l2.launches;

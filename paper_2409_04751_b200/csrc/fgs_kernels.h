@@ -81,9 +81,9 @@ struct SortScratch {
   uint32_t* counters;    // passes tile counters
   int max_tiles;
 };
-constexpr int kSortThreads = 256;
+constexpr int kSortThreads = 512;
 constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
+constexpr int kSortTile = kSortThreads * kSortItems;  // 8192
 constexpr int kMaxPasses = 4;
 
 // Stable LSD radix sort of (u32 key, u32 value) over bits [0, 8*passes). The inputs are not
@@ -95,14 +95,16 @@ struct SortResult {
 };
 SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_a, uint32_t* vals_a,
                             uint32_t* keys_b, uint32_t* vals_b, const uint32_t* n_dev, int n_max, int passes,
-                            const SortScratch& s, cudaStream_t st);
+                            const SortScratch& s, bool hist_ready, cudaStream_t st);
 
 // Status words a single-pass scan over n_max items needs.
 size_t scan_status_words(int n_max);
 // Stream compaction (source order) of the Gaussians touching >= 1 tile: keys_out = depth keys,
-// vals_out = Gaussian indices, *count_out = their number (device).
+// vals_out = Gaussian indices, *count_out = their number (device); hist = the 4 digit
+// histograms of the compacted keys (level-1 sort input).
 int compact_visible(const uint32_t* touched, const uint32_t* depth_key, uint32_t* keys_out, uint32_t* vals_out,
-                    uint32_t* count_out, int n, uint32_t* status, uint32_t* counter, cudaStream_t st);
+                    uint32_t* count_out, int n, uint32_t* status, uint32_t* counter, uint32_t* hist,
+                    cudaStream_t st);
 // Exclusive scan of touched[perm[r]] over depth ranks r < *n_dev: offsets[r], rank[perm[r]] = r,
 // *total_out = I (device).
 int rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, uint32_t* rank,
@@ -111,7 +113,7 @@ int rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, 
 // Emit (tile key, emission slot, gaussian) per intersection in depth-rank order.
 int duplicate(const uint32_t* perm, const uint32_t* offsets, const uint32_t* touched, const ushort4* rect, int tiles_x,
               uint32_t* tile_keys, uint32_t* emit_vals, uint32_t* emit_gauss, const uint32_t* n_dev, int n_max,
-              cudaStream_t st);
+              uint32_t* hist, int passes, cudaStream_t st);
 // Per-tile ranges from sorted tile keys; sorted_gauss[k] = emit_gauss[sorted_emit[k]].
 int tile_ranges(const uint32_t* sorted_tiles, const uint32_t* sorted_emit, const uint32_t* emit_gauss,
                 uint32_t* tile_offsets, uint32_t* sorted_gauss, int num_isect, int num_tiles, cudaStream_t st);
