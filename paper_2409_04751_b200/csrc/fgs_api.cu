@@ -58,13 +58,11 @@ struct fgs_context {
   DevBuf<ushort4> rect;
   DevBuf<int32_t> radii;
   // per intersection
-  DevBuf<uint32_t> tkey, emit, tkey_a, tkey_b, emit_a, emit_b, emit_gauss, sorted_gauss;
+  DevBuf<uint32_t> tkey, emit, tkey_a, tkey_b, emit_a, emit_b, emit_gauss, sorted_gauss, sorted_emit_buf;
   DevBuf<float> partials;
   // per tile / pixel
   DevBuf<uint32_t> tile_offsets, last;
   DevBuf<float> final_T;
-  // sort scratch
-  DevBuf<uint32_t> hist, lookback, sort_counters;
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
   DevBuf<uint32_t> scalars;
@@ -98,6 +96,7 @@ struct fgs_context {
   uint32_t* sorted_tiles = nullptr;  // level-2 result keys
   uint32_t* sorted_emit = nullptr;   // level-2 result values
   size_t aux_bytes = 0;
+  fgs::BinArgs bin_args{};
 };
 
 namespace {
@@ -197,7 +196,7 @@ int fgs_create(int device, fgs_context** out) {
   }
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(4) != cudaSuccess ||
-      ctx->hist.ensure(4 * 256) != cudaSuccess || ctx->sort_counters.ensure(8) != cudaSuccess) {
+      false) {
     fgs_destroy(ctx);
     return FGS_ENOMEM;
   }
@@ -218,8 +217,9 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->state.release();
   for (auto* b : {&ctx->dkey, &ctx->ckey, &ctx->cval, &ctx->dkey_a, &ctx->dkey_b, &ctx->perm_a, &ctx->perm_b,
                   &ctx->touched, &ctx->rank, &ctx->offsets, &ctx->scan_status, &ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b,
-                  &ctx->emit_a, &ctx->emit_b, &ctx->emit_gauss, &ctx->sorted_gauss, &ctx->tile_offsets, &ctx->last,
-                  &ctx->hist, &ctx->lookback, &ctx->sort_counters, &ctx->scalars})
+                  &ctx->emit_a, &ctx->emit_b, &ctx->emit_gauss, &ctx->sorted_gauss, &ctx->sorted_emit_buf,
+                  &ctx->tile_offsets, &ctx->last,
+                  &ctx->scalars})
     b->release();
   ctx->rect.release();
   ctx->radii.release();
@@ -294,13 +294,12 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   for (auto* b : {&ctx->dkey, &ctx->ckey, &ctx->cval, &ctx->dkey_a, &ctx->dkey_b, &ctx->perm_a, &ctx->perm_b,
                   &ctx->touched, &ctx->rank, &ctx->offsets})
     FGS_CHECK(b->ensure(nn));
-  FGS_CHECK(ctx->scan_status.ensure(fgs::scan_status_words(static_cast<int>(nn))));
+  FGS_CHECK(ctx->scan_status.ensure(fgs::bin_part_words()));
   FGS_CHECK(ctx->rect.ensure(nn));
   FGS_CHECK(ctx->radii.ensure(nn));
   FGS_CHECK(ctx->tile_offsets.ensure(num_tiles + 1));
   FGS_CHECK(ctx->last.ensure(npix));
   FGS_CHECK(ctx->final_T.ensure(npix));
-  FGS_CHECK(ctx->lookback.ensure(static_cast<size_t>(4) * 256 * (nn / fgs::kSortTile + 1)));
 
   ctx->n = n;
   ctx->cam = *camera;
@@ -310,7 +309,6 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ctx->tiles_x = tiles_x;
   ctx->tiles_y = tiles_y;
 
-  fgs::SortScratch ss{ctx->hist.p, ctx->lookback.p, ctx->sort_counters.p, 0};
   const bool timing = stats != nullptr || (ctx->flags & FGS_FLAG_TIMING);
   if (ctx->pending.size() > 64) drain_sets(ctx, 8);
   cudaEvent_t* ev = timing ? take_set(ctx, 0)->e : ctx->ev;
@@ -345,51 +343,66 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     ++launches;
   }
   if (timing) cudaEventRecord(ev[1], st);
-  // compact the Gaussians that touch a tile, then level 1: sort them by depth key (stable;
-  // ties keep source order); then the exclusive scan of their tile counts in depth order
-  uint32_t* d_m = ctx->scalars.p + 4;
+  // K2 level 1 (one persistent kernel): compact the Gaussians that touch a tile, sort them
+  // by depth key (stable; ties keep source order), scan their tile counts in depth order
+  fgs::BinArgs bn{};
+  bn.n = static_cast<int>(n);
+  bn.tiles_x = tiles_x;
+  bn.num_tiles = num_tiles;
+  bn.passes2 = num_tiles <= 256 ? 1 : 2;
+  bn.touched = ctx->touched.p;
+  bn.depth_key_in = ctx->dkey.p;
+  bn.rect = ctx->rect.p;
+  bn.ckey = ctx->ckey.p;
+  bn.cval = ctx->cval.p;
+  bn.key_a = ctx->dkey_a.p;
+  bn.val_a = ctx->perm_a.p;
+  bn.key_b = ctx->dkey_b.p;
+  bn.val_b = ctx->perm_b.p;
+  bn.offsets = ctx->offsets.p;
+  bn.rank = ctx->rank.p;
+  bn.scalars = ctx->scalars.p;
+  bn.part_scan = ctx->scan_status.p;
+  bn.part_radix = ctx->scan_status.p + 256;
+  ctx->perm = ctx->perm_b.p;
   if (n > 0) {
-    launches += fgs::compact_visible(ctx->touched.p, ctx->dkey.p, ctx->ckey.p, ctx->cval.p, d_m, static_cast<int>(n),
-                                     ctx->scan_status.p, ctx->scalars.p + 5, ss.hist, st);
-    const fgs::SortResult l1 = fgs::radix_sort_pairs(ctx->ckey.p, ctx->cval.p, ctx->dkey_a.p, ctx->perm_a.p,
-                                                     ctx->dkey_b.p, ctx->perm_b.p, d_m, static_cast<int>(n), 4, ss,
-                                                     true, st);
-    ctx->perm = l1.vals;
-    launches += l1.launches;
-    launches += fgs::rank_scan(ctx->perm, ctx->touched.p, ctx->offsets.p, ctx->rank.p, d_m, static_cast<int>(n),
-                               ctx->scalars.p, ctx->scan_status.p, ctx->scalars.p + 5, st);
+    FGS_CHECK(fgs::bin_level1(bn, st));
+    ++launches;
   }
   FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, ctx->scalars.p, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   FGS_CHECK(cudaStreamSynchronize(st));
   FGS_CHECK(cudaGetLastError());
-  if (ctx->h_scalars[1]) return fail(ctx, FGS_EDEGENERATE_QUAT, "degenerate rotation: quaternion has zero norm");
-  const int64_t I = ctx->h_scalars[0];
-  const int M = static_cast<int>(ctx->h_scalars[4]);
+  if (ctx->h_scalars[fgs::kScalarErr]) return fail(ctx, FGS_EDEGENERATE_QUAT, "degenerate rotation: quaternion has zero norm");
+  const int64_t I = ctx->h_scalars[fgs::kScalarI];
   ctx->num_isect = I;
-  ctx->num_splats = ctx->h_scalars[2];
-  ctx->num_degenerate = ctx->h_scalars[3];
+  ctx->num_splats = ctx->h_scalars[fgs::kScalarKept];
+  ctx->num_degenerate = ctx->h_scalars[fgs::kScalarDegen];
   ctx->num_culled = static_cast<uint32_t>(n) - ctx->num_splats - ctx->num_degenerate;
   if (I >= (int64_t(1) << 30)) return fail(ctx, FGS_ENOMEM, "forward: intersection count exceeds 2^30");
+  if (timing) cudaEventRecord(ev[2], st);
 
+  // K2 level 2 (one persistent kernel): duplicate in depth-rank order, stable sort by tile,
+  // per-tile ranges
   const size_t ni = static_cast<size_t>(I > 0 ? I : 1);
   for (auto* b : {&ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b, &ctx->emit_a, &ctx->emit_b, &ctx->emit_gauss,
-                  &ctx->sorted_gauss})
+                  &ctx->sorted_gauss, &ctx->sorted_emit_buf})
     FGS_CHECK(b->ensure(ni));
-  FGS_CHECK(ctx->lookback.ensure(static_cast<size_t>(4) * 256 * (ni / fgs::kSortTile + 1)));
-  ss.lookback = ctx->lookback.p;
-  const int passes2 = num_tiles <= 256 ? 1 : 2;
-  if (M > 0)
-    launches += fgs::duplicate(ctx->perm, ctx->offsets.p, ctx->touched.p, ctx->rect.p, tiles_x, ctx->tkey.p,
-                               ctx->emit.p, ctx->emit_gauss.p, nullptr, M, ss.hist, passes2, st);
-  if (timing) cudaEventRecord(ev[2], st);
-  const fgs::SortResult l2 = fgs::radix_sort_pairs(ctx->tkey.p, ctx->emit.p, ctx->tkey_a.p, ctx->emit_a.p,
-                                                   ctx->tkey_b.p, ctx->emit_b.p, nullptr, static_cast<int>(I), passes2,
-                                                   ss, true, st);
-  ctx->sorted_tiles = l2.keys;
-  ctx->sorted_emit = l2.vals;
-  launches += l2.launches;
-  launches += fgs::tile_ranges(ctx->sorted_tiles, ctx->sorted_emit, ctx->emit_gauss.p, ctx->tile_offsets.p, ctx->sorted_gauss.p,
-                   static_cast<int>(I), num_tiles, st);
+  bn.num_isect = static_cast<int>(I);
+  bn.tkey = ctx->tkey.p;
+  bn.emit = ctx->emit.p;
+  bn.emit_gauss = ctx->emit_gauss.p;
+  bn.tkey_a = ctx->tkey_a.p;
+  bn.emit_a = ctx->emit_a.p;
+  bn.tkey_b = ctx->tkey_b.p;
+  bn.emit_b = ctx->emit_b.p;
+  bn.tile_offsets = ctx->tile_offsets.p;
+  bn.sorted_gauss = ctx->sorted_gauss.p;
+  bn.sorted_emit = ctx->sorted_emit_buf.p;
+  FGS_CHECK(fgs::bin_level2(bn, st));
+  if (I > 0) ++launches;
+  ctx->sorted_tiles = bn.passes2 == 1 ? ctx->tkey_a.p : ctx->tkey_b.p;
+  ctx->sorted_emit = ctx->sorted_emit_buf.p;
+  ctx->bin_args = bn;
   if (timing) cudaEventRecord(ev[3], st);
 
   fgs::BlendArgs ba{};
@@ -640,15 +653,13 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   if (nm == "key_tile" || nm == "key_depth" || nm == "key_gauss") {
     if (!dst) return static_cast<int64_t>(I * 4);
     // Recompute the reference's pre-sort emission order (source order) on demand.
-    DevBuf<uint32_t> kt, kd, kg, off, bs, tot;
-    if (kt.ensure(I + 1) || kd.ensure(I + 1) || kg.ensure(I + 1) || off.ensure(n + 1) ||
-        bs.ensure(fgs::scan_status_words(static_cast<int>(n))) || tot.ensure(2))
-      return -1;
-    fgs::debug_source_order_keys(ctx->touched.p, ctx->rect.p, ctx->dkey.p, ctx->tiles_x, static_cast<int>(n), off.p,
-                                 bs.p, tot.p + 1, tot.p, kt.p, kd.p, kg.p, st);
+    DevBuf<uint32_t> kt, kd, kg;
+    if (kt.ensure(I + 1) || kd.ensure(I + 1) || kg.ensure(I + 1)) return -1;
+    fgs::BinArgs a = ctx->bin_args;
+    if (fgs::debug_source_order_keys(a, kt.p, kd.p, kg.p, st) != cudaSuccess) return -1;
     const uint32_t* src = nm == "key_tile" ? kt.p : (nm == "key_depth" ? kd.p : kg.p);
     const int64_t r = copy(src, I * 4);
-    for (auto* b : {&kt, &kd, &kg, &off, &bs, &tot}) b->release();
+    for (auto* b : {&kt, &kd, &kg}) b->release();
     return r;
   }
   return -1;

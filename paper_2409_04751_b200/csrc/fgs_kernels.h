@@ -75,52 +75,49 @@ __global__ void preprocess_kernel(PreprocessArgs a);
 __global__ void preprocess_backward_kernel(PreprocessBackwardArgs a);
 
 // ---- binning / sorting (binning.cu) ----
-struct SortScratch {
-  uint32_t* hist;        // passes * 256 (exclusive offsets after scan)
-  uint32_t* lookback;    // passes * max_tiles * 256
-  uint32_t* counters;    // passes tile counters
-  int max_tiles;
-};
-constexpr int kSortThreads = 512;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 8192
-constexpr int kMaxPasses = 4;
+constexpr int kBinThreads = 1024;
+constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, kScalarM = 4;
 
-// Stable LSD radix sort of (u32 key, u32 value) over bits [0, 8*passes). The inputs are not
-// modified; passes alternate b, a, b, a. Returns where the sorted pairs are.
-struct SortResult {
-  uint32_t* keys;
-  uint32_t* vals;
-  int launches;
+struct BinArgs {
+  int n;                       // Gaussians
+  int tiles_x, num_tiles, passes2;
+  int num_isect;               // I (level 2 only; known on the host after level 1)
+  const uint32_t* touched;     // [n]
+  const uint32_t* depth_key_in;  // [n]
+  const ushort4* rect;         // [n]
+  uint32_t* ckey;              // compacted depth keys [n]
+  uint32_t* cval;              // compacted Gaussian ids [n]
+  uint32_t* key_a;             // ping-pong [n]
+  uint32_t* val_a;
+  uint32_t* key_b;
+  uint32_t* val_b;             // level-1 result: Gaussian ids by depth rank
+  uint32_t* offsets;           // [n] emission offset per depth rank
+  uint32_t* rank;              // [n] depth rank per Gaussian
+  uint32_t* scalars;           // device scalars (kScalar*)
+  uint32_t* part_scan;         // [grid]
+  uint32_t* part_radix;        // [grid * 256]
+  // level 2
+  uint32_t* tkey;              // [I] tile keys (emission order)
+  uint32_t* emit;              // [I] emission slots
+  uint32_t* emit_gauss;        // [I] Gaussian of each emission slot
+  uint32_t* tkey_a;
+  uint32_t* emit_a;
+  uint32_t* tkey_b;
+  uint32_t* emit_b;
+  uint32_t* tile_offsets;      // [num_tiles + 1]
+  uint32_t* sorted_gauss;      // [I]
+  uint32_t* sorted_emit;       // [I]
 };
-SortResult radix_sort_pairs(const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_a, uint32_t* vals_a,
-                            uint32_t* keys_b, uint32_t* vals_b, const uint32_t* n_dev, int n_max, int passes,
-                            const SortScratch& s, bool hist_ready, cudaStream_t st);
 
-// Status words a single-pass scan over n_max items needs.
-size_t scan_status_words(int n_max);
-// Stream compaction (source order) of the Gaussians touching >= 1 tile: keys_out = depth keys,
-// vals_out = Gaussian indices, *count_out = their number (device); hist = the 4 digit
-// histograms of the compacted keys (level-1 sort input).
-int compact_visible(const uint32_t* touched, const uint32_t* depth_key, uint32_t* keys_out, uint32_t* vals_out,
-                    uint32_t* count_out, int n, uint32_t* status, uint32_t* counter, uint32_t* hist,
-                    cudaStream_t st);
-// Exclusive scan of touched[perm[r]] over depth ranks r < *n_dev: offsets[r], rank[perm[r]] = r,
-// *total_out = I (device).
-int rank_scan(const uint32_t* perm, const uint32_t* touched, uint32_t* offsets, uint32_t* rank,
-              const uint32_t* n_dev, int n_max, uint32_t* total_out, uint32_t* status, uint32_t* counter,
-              cudaStream_t st);
-// Emit (tile key, emission slot, gaussian) per intersection in depth-rank order.
-int duplicate(const uint32_t* perm, const uint32_t* offsets, const uint32_t* touched, const ushort4* rect, int tiles_x,
-              uint32_t* tile_keys, uint32_t* emit_vals, uint32_t* emit_gauss, const uint32_t* n_dev, int n_max,
-              uint32_t* hist, int passes, cudaStream_t st);
-// Per-tile ranges from sorted tile keys; sorted_gauss[k] = emit_gauss[sorted_emit[k]].
-int tile_ranges(const uint32_t* sorted_tiles, const uint32_t* sorted_emit, const uint32_t* emit_gauss,
-                uint32_t* tile_offsets, uint32_t* sorted_gauss, int num_isect, int num_tiles, cudaStream_t st);
-// Debug: reference emission order keys (source order, ty-major, tx-minor).
-void debug_source_order_keys(const uint32_t* touched, const ushort4* rect, const uint32_t* depth_key, int tiles_x,
-                             int n, uint32_t* scratch_offsets, uint32_t* status, uint32_t* counter, uint32_t* total,
-                             uint32_t* key_tile, uint32_t* key_depth, uint32_t* key_gauss, cudaStream_t st);
+// Words of part_scan + part_radix scratch the persistent kernels need.
+size_t bin_part_words();
+// Compaction + level-1 sort + rank scan (writes scalars[kScalarM], scalars[kScalarI]).
+cudaError_t bin_level1(BinArgs& a, cudaStream_t st);
+// Duplication + level-2 sort + tile ranges (needs a.num_isect).
+cudaError_t bin_level2(BinArgs& a, cudaStream_t st);
+// Debug: the reference's pre-sort key list (source order).
+cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* key_depth, uint32_t* key_gauss,
+                                    cudaStream_t st);
 
 // ---- blend (raster.cu) ----
 int blend_forward(const BlendArgs& a, cudaStream_t st);
