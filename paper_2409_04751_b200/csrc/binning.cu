@@ -20,8 +20,9 @@
 //   [host reads I (8 bytes) to size the per-intersection buffers]
 //   bin_level2_kernel: duplication -> 1-2 radix passes -> tile ranges.
 // Each radix pass sweeps every CTA's contiguous chunk once for its digit histogram, resolves
-// the global digit offsets across CTAs with one grid barrier (reduce-then-scan over the 148
-// per-CTA histograms, no look-back chains), then ranks keys in 8192-key sub-tiles with a
+// the global digit offsets across CTAs with two grid barriers (reduce-then-scan over the 148
+// per-CTA histograms: each digit's column is scanned in parallel by one CTA, no look-back
+// chains), then ranks keys in 8192-key sub-tiles with a
 // ballot-based warp multisplit and scatters through shared memory (stable).
 
 #include <cooperative_groups.h>
@@ -119,15 +120,20 @@ __device__ void radix_pass(cg::grid_group& grid, BinSmem& sm, const uint32_t* __
   __syncthreads();
   if (tid < 256) part[blockIdx.x * 256 + tid] = sm.hist[tid];
   grid.sync();
-  // 2. global digit starts + this chunk's offset within each digit
-  uint32_t tot = 0, pre = 0;
-  if (tid < 256) {
-    for (int c = 0; c < static_cast<int>(gridDim.x); ++c) {
-      const uint32_t v = part[c * 256 + tid];
-      tot += v;
-      pre += c < static_cast<int>(blockIdx.x) ? v : 0u;
-    }
+  // 2. per digit, exclusive scan over CTAs: digit d is owned by CTA d mod grid, whose threads
+  //    (one per CTA c) load part[c][d] in one parallel burst, scan it in place and publish the
+  //    digit total. Then every CTA reads its own 256 offsets + the 256 totals (coalesced).
+  uint32_t* totals = part + gridDim.x * 256;
+  for (int d = blockIdx.x; d < 256; d += gridDim.x) {
+    const uint32_t v = tid < static_cast<int>(gridDim.x) ? part[tid * 256 + d] : 0u;
+    uint32_t t;
+    const uint32_t ex = block_exclusive_scan(v, sm.warp_tmp, &t);
+    if (tid < static_cast<int>(gridDim.x)) part[tid * 256 + d] = ex;
+    if (tid == 0) totals[d] = t;
   }
+  grid.sync();
+  const uint32_t tot = tid < 256 ? totals[tid] : 0u;
+  const uint32_t pre = tid < 256 ? part[blockIdx.x * 256 + tid] : 0u;
   const uint32_t dstart = block_exclusive_scan(tot, sm.warp_tmp, nullptr);
   if (tid < 256) sm.run[tid] = dstart + pre;
   __syncthreads();
@@ -422,7 +428,7 @@ cudaError_t launch_coop(const void* f, BinArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-size_t bin_part_words() { return static_cast<size_t>(grid_size() + 1) * 256 + 64; }
+size_t bin_part_words() { return static_cast<size_t>(grid_size() + 2) * 256 + 64; }
 
 cudaError_t bin_level1(BinArgs& a, cudaStream_t st) {
   return launch_coop(reinterpret_cast<const void*>(bin_level1_kernel), a, st);

@@ -27,6 +27,7 @@ namespace {
 constexpr int kBlend = 256;     // threads per tile CTA = pixels per tile
 constexpr int kBwdBatch = 128;  // splats per backward batch
 constexpr int kWarps = kBlend / 32;
+constexpr int kFwdThreads = 128;  // forward: 4 warps x 64 pixels
 
 // Warp w of a tile owns the 8x4 pixel block at (8*(w&1), 4*(w>>1)); lane l the pixel
 // (l&7, l>>3) inside it. Square-ish blocks make the per-warp culling below tight.
@@ -78,85 +79,133 @@ __device__ __forceinline__ int build_list(const uint8_t* s_mask, int cnt, int wa
   return n;
 }
 
+// Conservative test: can any pixel centre of the box [x0, x1] x [y0, y1] reach
+// alpha >= 1/255 for this splat? (same bound and margins as warp_mask)
+__device__ __forceinline__ bool box_may_hit(float4 r0, float4 r1, float x0, float x1, float y0, float y1) {
+  const float a = r0.z, b = r0.w, c = r1.x, amax = r1.y;
+  if (!(amax >= kAlphaSkip)) return false;
+  const float det = a * c - b * b;
+  if (!(det > 0.0f) || !(a > 0.0f) || !(c > 0.0f)) return true;
+  const float tau2 = 2.0f * __logf(255.0f * amax) * 1.002f + 1e-3f;
+  const float ex = sqrtf(fmaxf(tau2 * c / det, 0.0f)) * 1.001f + 1e-3f;
+  const float ey = sqrtf(fmaxf(tau2 * a / det, 0.0f)) * 1.001f + 1e-3f;
+  return r0.x + ex >= x0 && r0.x - ex <= x1 && r0.y + ey >= y0 && r0.y - ey <= y1;
+}
+
+struct PixelState {
+  float T, C0, C1, C2;
+  uint32_t last, stop, contrib;
+  bool done;
+};
+
+// One front-to-back step of the reference blend (inc/splatting.hpp:284-296) for one pixel.
+// t1 = (a*dx)*dx and bdx = b*dx are shared by the two pixels of a lane (same column).
 template <bool COUNTERS>
-__global__ void __launch_bounds__(kBlend) blend_forward_kernel(BlendArgs a) {
-  __shared__ float4 s0[kBlend];
-  __shared__ float4 s1[kBlend];
-  __shared__ float s2[kBlend];
-  __shared__ uint8_t s_mask[kBlend];
-  __shared__ uint8_t s_list[kWarps][kBlend];
+__device__ __forceinline__ void blend_step(PixelState& p, float fy, float4 r0, float4 r1, float r2, float t1,
+                                           float bdx, uint32_t k) {
+  if (p.done) return;
+  const float dy = __fsub_rn(fy, r0.y);
+  const float t2 = __fmul_rn(__fmul_rn(r1.x, dy), dy);
+  const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), __fmul_rn(bdx, dy));
+  if (power > 0.0f || power < kPowerFloor) return;
+  float e;
+  const float alpha = fminf(kAlphaClamp, alpha_raw(r1.y, power, &e));
+  if (alpha < kAlphaSkip) return;
+  const float Tn = __fmul_rn(p.T, __fsub_rn(1.0f, alpha));
+  if (Tn < kTransmittanceStop) {
+    p.done = true;
+    p.stop = k;
+    return;
+  }
+  const float w = __fmul_rn(alpha, p.T);
+  p.C0 = fmaf(r1.z, w, p.C0);
+  p.C1 = fmaf(r1.w, w, p.C1);
+  p.C2 = fmaf(r2, w, p.C2);
+  p.T = Tn;
+  p.last = k + 1;
+  if (COUNTERS) ++p.contrib;
+}
+
+// K3 forward blend. One 128-thread CTA per 16x16 tile; warp w owns the 8x8 block at
+// (8*(w&1), 8*(w>>1)) and lane l the two pixels (l&7, l>>3) and (l&7, (l>>3)+4), which share a
+// column (and so (a*dx)*dx and b*dx). Warps walk the tile's sorted list independently in
+// 32-splat chunks (no CTA barriers): each lane gathers one record, tests it against the warp's
+// 8x8 block (box_may_hit), the warp keeps the ballot of survivors and blends them in order
+// from warp-private shared memory while the next chunk's records are already being loaded.
+// A warp stops when all its 64 pixels have met the reference's termination rule.
+template <bool COUNTERS>
+__global__ void __launch_bounds__(kFwdThreads) blend_forward_kernel(BlendArgs a) {
+  constexpr int NW = kFwdThreads / 32;
+  __shared__ float4 s0[NW][32];
+  __shared__ float4 s1[NW][32];
+  __shared__ float s2[NW][32];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int lx, ly;
-  pixel_of(threadIdx.x, lx, ly);
-  const int px = tx * kTile + lx, py = ty * kTile + ly;
-  const bool inside = px < a.width && py < a.height;
+  const int bx = tx * kTile + ((warp & 1) << 3), by = ty * kTile + ((warp >> 1) << 3);
+  const int px = bx + (lane & 7), py0 = by + (lane >> 3), py1 = py0 + 4;
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
-  const float fx = static_cast<float>(px) + 0.5f, fy = static_cast<float>(py) + 0.5f;
-  const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
-  float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  uint32_t last = lo, stop_k = hi;
-  bool done = !inside;
-  uint32_t n_contrib = 0;
+  const float fx = static_cast<float>(px) + 0.5f;
+  const float fy0 = static_cast<float>(py0) + 0.5f, fy1 = static_cast<float>(py1) + 0.5f;
+  const float bx0 = static_cast<float>(bx) + 0.5f, by0 = static_cast<float>(by) + 0.5f;
+  PixelState p0{1.0f, 0.0f, 0.0f, 0.0f, lo, hi, 0u, !(px < a.width && py0 < a.height)};
+  PixelState p1{1.0f, 0.0f, 0.0f, 0.0f, lo, hi, 0u, !(px < a.width && py1 < a.height)};
 
-  for (uint32_t base = lo; base < hi; base += kBlend) {
-    if (__syncthreads_count(done) == kBlend) break;
-    const uint32_t k = base + threadIdx.x;
-    if (k < hi) {
-      const uint32_t g = __ldg(a.sorted_gauss + k);
-      const float4 r0 = __ldg(a.rec.rec0 + g);
-      const float4 r1 = __ldg(a.rec.rec1 + g);
-      s0[threadIdx.x] = r0;
-      s1[threadIdx.x] = r1;
-      s2[threadIdx.x] = __ldg(a.rec.rec2 + g);
-      s_mask[threadIdx.x] = static_cast<uint8_t>(warp_mask(r0, r1, tile_x0, tile_y0));
-    }
-    __syncthreads();
-    const int cnt = static_cast<int>(min(static_cast<uint32_t>(kBlend), hi - base));
-    if (__all_sync(0xffffffffu, done)) continue;
-    const int nl = build_list(s_mask, cnt, warp, lane, s_list[warp]);
-    for (int i = 0; i < nl; ++i) {
-      if (__all_sync(0xffffffffu, done)) break;
-      if (done) continue;
-      const int j = s_list[warp][i];
-      const float4 r0 = s0[j];
-      const float dx = __fsub_rn(fx, r0.x);
-      const float dy = __fsub_rn(fy, r0.y);
-      const float4 r1 = s1[j];
-      const float power = blend_power(r0.z, r0.w, r1.x, dx, dy);
-      if (power > 0.0f || power < kPowerFloor) continue;
-      float e;
-      const float alpha = fminf(kAlphaClamp, alpha_raw(r1.y, power, &e));
-      if (alpha < kAlphaSkip) continue;
-      const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-      if (Tn < kTransmittanceStop) {
-        done = true;
-        stop_k = base + j;
-        continue;
-      }
-      const float w = __fmul_rn(alpha, T);
-      C0 = fmaf(r1.z, w, C0);
-      C1 = fmaf(r1.w, w, C1);
-      C2 = fmaf(s2[j], w, C2);
-      T = Tn;
-      last = base + j + 1;
-      if (COUNTERS) ++n_contrib;
-    }
+  float4 n0 = make_float4(0.f, 0.f, 0.f, 0.f), n1 = n0;
+  float n2 = 0.0f;
+  if (lo + lane < hi) {
+    const uint32_t g = __ldg(a.sorted_gauss + lo + lane);
+    n0 = __ldg(a.rec.rec0 + g);
+    n1 = __ldg(a.rec.rec1 + g);
+    n2 = __ldg(a.rec.rec2 + g);
   }
-  if (inside) {
-    const size_t pix = static_cast<size_t>(py) * a.width + px;
-    a.image[pix * 3 + 0] = C0 + T * a.bg[0];
-    a.image[pix * 3 + 1] = C1 + T * a.bg[1];
-    a.image[pix * 3 + 2] = C2 + T * a.bg[2];
-    a.final_T[pix] = T;
-    a.last[pix] = last;
-    if (COUNTERS) {
-      // E_eval as the reference counts it: k-loop iterations entered, including the one
-      // that terminates (inc/splatting.hpp:282-292).
-      const unsigned long long n_eval = (stop_k < hi) ? (stop_k - lo + 1) : (hi - lo);
-      atomicAdd(a.counters + 0, n_eval);
-      atomicAdd(a.counters + 1, static_cast<unsigned long long>(n_contrib));
+  for (uint32_t base = lo; base < hi; base += 32) {
+    if (__all_sync(0xffffffffu, p0.done && p1.done)) break;
+    const bool pass = base + lane < hi && box_may_hit(n0, n1, bx0, bx0 + 7.0f, by0, by0 + 7.0f);
+    s0[warp][lane] = n0;
+    s1[warp][lane] = n1;
+    s2[warp][lane] = n2;
+    uint32_t mask = __ballot_sync(0xffffffffu, pass);
+    if (base + 32 + lane < hi) {  // prefetch the next chunk
+      const uint32_t g = __ldg(a.sorted_gauss + base + 32 + lane);
+      n0 = __ldg(a.rec.rec0 + g);
+      n1 = __ldg(a.rec.rec1 + g);
+      n2 = __ldg(a.rec.rec2 + g);
+    }
+    __syncwarp();
+    while (mask) {
+      const int j = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const float4 r0 = s0[warp][j];
+      const float4 r1 = s1[warp][j];
+      const float r2 = s2[warp][j];
+      const float dx = __fsub_rn(fx, r0.x);
+      const float t1 = __fmul_rn(__fmul_rn(r0.z, dx), dx);
+      const float bdx = __fmul_rn(r0.w, dx);
+      blend_step<COUNTERS>(p0, fy0, r0, r1, r2, t1, bdx, base + j);
+      blend_step<COUNTERS>(p1, fy1, r0, r1, r2, t1, bdx, base + j);
+    }
+    __syncwarp();
+  }
+  const PixelState* ps[2] = {&p0, &p1};
+  const int pys[2] = {py0, py1};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const PixelState& p = *ps[q];
+    if (px < a.width && pys[q] < a.height) {
+      const size_t pix = static_cast<size_t>(pys[q]) * a.width + px;
+      a.image[pix * 3 + 0] = p.C0 + p.T * a.bg[0];
+      a.image[pix * 3 + 1] = p.C1 + p.T * a.bg[1];
+      a.image[pix * 3 + 2] = p.C2 + p.T * a.bg[2];
+      a.final_T[pix] = p.T;
+      a.last[pix] = p.last;
+      if (COUNTERS) {
+        // E_eval as the reference counts it: k-loop iterations entered, including the one
+        // that terminates (inc/splatting.hpp:282-292).
+        const unsigned long long n_eval = (p.stop < hi) ? (p.stop - lo + 1) : (hi - lo);
+        atomicAdd(a.counters + 0, n_eval);
+        atomicAdd(a.counters + 1, static_cast<unsigned long long>(p.contrib));
+      }
     }
   }
 }
@@ -312,9 +361,9 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
 
 int blend_forward(const BlendArgs& a, cudaStream_t st) {
   if (a.counters)
-    blend_forward_kernel<true><<<a.tiles_x * a.tiles_y, kBlend, 0, st>>>(a);
+    blend_forward_kernel<true><<<a.tiles_x * a.tiles_y, kFwdThreads, 0, st>>>(a);
   else
-    blend_forward_kernel<false><<<a.tiles_x * a.tiles_y, kBlend, 0, st>>>(a);
+    blend_forward_kernel<false><<<a.tiles_x * a.tiles_y, kFwdThreads, 0, st>>>(a);
   return 1;
 }
 
