@@ -210,7 +210,8 @@ def run_ours(args, ws, rank, local):
     # work counters and stats of the measured view (instrumented run, outside the timed region)
     r.set_flags(_lib.FGS_FLAG_COUNTERS)
     _, st = r.forward(ds, cam, ropt, image=image, want_stats=True)
-    counters = r.debug("counters", np.uint64).tolist()
+    counters_all = r.debug("counters", np.uint64).tolist()
+    counters = counters_all[:2]
     r.set_flags(0)
     stn = {"num_splats": st.num_splats, "num_intersections": st.num_intersections}
     work = stage_work(cfg, scene, deg, stn, counters)
@@ -312,6 +313,7 @@ def run_ours(args, ws, rank, local):
         "num_splats": st.num_splats,
         "e_eval": int(counters[0]),
         "e_contrib": int(counters[1]),
+        "blend_pixel_evals_after_culling": int(counters_all[2]) * 64,
         "fp32_peak_tops": round(fp32_peak / 1e12, 2),
     }
     if rank == 0:

@@ -18,7 +18,8 @@
 // persistent kernels, one 1024-thread CTA per SM:
 //   bin_level1_kernel: compaction -> 4 radix passes (8-bit digits) -> rank scan (I);
 //   [host reads I (8 bytes) to size the per-intersection buffers]
-//   bin_level2_kernel: duplication -> 1-2 radix passes -> tile ranges.
+//   bin_level2_kernel: duplication -> 1-2 radix passes -> tile ranges + records gathered
+//   into sorted order (the blends then stream each tile's list contiguously).
 // Each radix pass sweeps every CTA's contiguous chunk once for its digit histogram, resolves
 // the global digit offsets across CTAs with two grid barriers (reduce-then-scan over the 148
 // per-CTA histograms: each digit's column is scanned in parallel by one CTA, no look-back
@@ -352,8 +353,14 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
     if (k == I - 1)
       for (int tt = t + 1; tt <= a.num_tiles; ++tt) a.tile_offsets[tt] = static_cast<uint32_t>(I);
     const uint32_t e = sv[k];
+    const uint32_t g = a.emit_gauss[e];
     a.sorted_emit[k] = e;
-    a.sorted_gauss[k] = a.emit_gauss[e];
+    a.sorted_gauss[k] = g;
+    SortedRec r;
+    r.a = __ldg(a.rec0 + g);
+    r.b = __ldg(a.rec1 + g);
+    r.c = make_float4(__ldg(a.rec2 + g), 0.0f, 0.0f, 0.0f);
+    a.sorted_rec[k] = r;
   }
 }
 

@@ -59,6 +59,7 @@ struct fgs_context {
   DevBuf<int32_t> radii;
   // per intersection
   DevBuf<uint32_t> tkey, emit, tkey_a, tkey_b, emit_a, emit_b, emit_gauss, sorted_gauss, sorted_emit_buf;
+  DevBuf<fgs::SortedRec> sorted_rec;
   DevBuf<float> partials;
   // per tile / pixel
   DevBuf<uint32_t> tile_offsets, last;
@@ -66,7 +67,7 @@ struct fgs_context {
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
   DevBuf<uint32_t> scalars;
-  DevBuf<unsigned long long> counters;
+  DevBuf<unsigned long long> counters, tile_cycles;
   uint32_t* h_scalars = nullptr;  // pinned
   // host-call staging
   DevBuf<float> h_means, h_rot, h_ls, h_op, h_sh, h_img, h_dl, h_grad;
@@ -223,8 +224,10 @@ int fgs_destroy(fgs_context* ctx) {
     b->release();
   ctx->rect.release();
   ctx->radii.release();
+  ctx->sorted_rec.release();
   ctx->h_radii.release();
   ctx->counters.release();
+  ctx->tile_cycles.release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   for (auto* v : {&ctx->pending, &ctx->spare})
@@ -398,6 +401,11 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.tile_offsets = ctx->tile_offsets.p;
   bn.sorted_gauss = ctx->sorted_gauss.p;
   bn.sorted_emit = ctx->sorted_emit_buf.p;
+  FGS_CHECK(ctx->sorted_rec.ensure(ni));
+  bn.rec0 = ctx->rec0.p;
+  bn.rec1 = ctx->rec1.p;
+  bn.rec2 = ctx->rec2.p;
+  bn.sorted_rec = ctx->sorted_rec.p;
   FGS_CHECK(fgs::bin_level2(bn, st));
   if (I > 0) ++launches;
   ctx->sorted_tiles = bn.passes2 == 1 ? ctx->tkey_a.p : ctx->tkey_b.p;
@@ -413,12 +421,17 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ba.tile_offsets = ctx->tile_offsets.p;
   ba.sorted_gauss = ctx->sorted_gauss.p;
   ba.sorted_emit = ctx->sorted_emit;
-  ba.rec = {ctx->rec0.p, ctx->rec1.p, ctx->rec2.p};
+  ba.srec = ctx->sorted_rec.p;
   for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
   ba.image = image;
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;
   ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
+  if (ba.counters) {
+    FGS_CHECK(ctx->tile_cycles.ensure(num_tiles));
+    FGS_CHECK(cudaMemsetAsync(ctx->tile_cycles.p, 0, num_tiles * sizeof(unsigned long long), st));
+    ba.tile_cycles = ctx->tile_cycles.p;
+  }
   launches += fgs::blend_forward(ba, st);
   if (timing) cudaEventRecord(ev[4], st);
   if (radii && n > 0) FGS_CHECK(cudaMemcpyAsync(radii, ctx->radii.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
@@ -470,7 +483,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   ba.tile_offsets = ctx->tile_offsets.p;
   ba.sorted_gauss = ctx->sorted_gauss.p;
   ba.sorted_emit = ctx->sorted_emit;
-  ba.rec = {ctx->rec0.p, ctx->rec1.p, ctx->rec2.p};
+  ba.srec = ctx->sorted_rec.p;
   for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;
@@ -649,7 +662,8 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   if (nm == "offsets") return copy(ctx->tile_offsets.p, (nt + 1) * 4);
   if (nm == "final_T") return copy(ctx->final_T.p, npix * 4);
   if (nm == "last") return copy(ctx->last.p, npix * 4);
-  if (nm == "counters") return copy(ctx->counters.p, 2 * sizeof(unsigned long long));
+  if (nm == "counters") return copy(ctx->counters.p, 4 * sizeof(unsigned long long));
+  if (nm == "tile_cycles") return copy(ctx->tile_cycles.p, nt * sizeof(unsigned long long));
   if (nm == "key_tile" || nm == "key_depth" || nm == "key_gauss") {
     if (!dst) return static_cast<int64_t>(I * 4);
     // Recompute the reference's pre-sort emission order (source order) on demand.

@@ -41,6 +41,14 @@ struct SplatRefs {
   const float* rec2;
 };
 
+// Splat record gathered into sorted (tile-list) order by the binning kernel, so the blends
+// read each tile's list as one contiguous, 16-byte aligned stream: 48 bytes per intersection.
+struct SortedRec {
+  float4 a;  // mean_px.x, mean_px.y, conic.a, conic.b
+  float4 b;  // conic.c, alpha_max, R, G
+  float4 c;  // B, unused x3
+};
+
 // Correctly rounded fp32 exp / atan2 (double evaluation, one rounding): the definition the
 // oracle's parity mode uses.
 __device__ __forceinline__ float cr_expf(float x) { return static_cast<float>(exp(static_cast<double>(x))); }

@@ -60,12 +60,13 @@ struct BlendArgs {
   const uint32_t* tile_offsets;  // T+1
   const uint32_t* sorted_gauss;  // I
   const uint32_t* sorted_emit;   // I (emission slot of each sorted entry; backward partials)
-  SplatRefs rec;
+  const SortedRec* srec;         // I records in sorted order
   float bg[3];
   float* image;                  // H*W*3
   float* final_T;                // H*W
   uint32_t* last;                // H*W: index one past the last contributing entry
-  unsigned long long* counters;  // optional: E_eval, E_contrib
+  unsigned long long* counters;  // optional: E_eval, E_contrib, culled evals, max CTA cycles
+  unsigned long long* tile_cycles;  // optional (with counters): per-tile CTA cycles
   // backward
   const float* dl_dimage;
   float* partials;               // I x 9
@@ -107,6 +108,10 @@ struct BinArgs {
   uint32_t* tile_offsets;      // [num_tiles + 1]
   uint32_t* sorted_gauss;      // [I]
   uint32_t* sorted_emit;       // [I]
+  const float4* rec0;          // per-Gaussian splat records (K1 output)
+  const float4* rec1;
+  const float* rec2;
+  SortedRec* sorted_rec;       // [I] records in sorted order
 };
 
 // Words of part_scan + part_radix scratch the persistent kernels need.

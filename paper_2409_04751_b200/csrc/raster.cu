@@ -28,6 +28,7 @@ constexpr int kBlend = 256;     // threads per tile CTA = pixels per tile
 constexpr int kBwdBatch = 128;  // splats per backward batch
 constexpr int kWarps = kBlend / 32;
 constexpr int kFwdThreads = 128;  // forward: 4 warps x 64 pixels
+constexpr int kGroup = 4;         // forward: splats whose alphas are computed together
 
 // Warp w of a tile owns the 8x4 pixel block at (8*(w&1), 4*(w>>1)); lane l the pixel
 // (l&7, l>>3) inside it. Square-ish blocks make the per-warp culling below tight.
@@ -80,15 +81,17 @@ __device__ __forceinline__ int build_list(const uint8_t* s_mask, int cnt, int wa
 }
 
 // Conservative test: can any pixel centre of the box [x0, x1] x [y0, y1] reach
-// alpha >= 1/255 for this splat? (same bound and margins as warp_mask)
+// alpha >= 1/255 for this splat? Same bound as warp_mask, evaluated with fast-math
+// (relative error ~1e-6, far inside the 0.1-0.2% margins).
 __device__ __forceinline__ bool box_may_hit(float4 r0, float4 r1, float x0, float x1, float y0, float y1) {
   const float a = r0.z, b = r0.w, c = r1.x, amax = r1.y;
   if (!(amax >= kAlphaSkip)) return false;
   const float det = a * c - b * b;
   if (!(det > 0.0f) || !(a > 0.0f) || !(c > 0.0f)) return true;
   const float tau2 = 2.0f * __logf(255.0f * amax) * 1.002f + 1e-3f;
-  const float ex = sqrtf(fmaxf(tau2 * c / det, 0.0f)) * 1.001f + 1e-3f;
-  const float ey = sqrtf(fmaxf(tau2 * a / det, 0.0f)) * 1.001f + 1e-3f;
+  const float k = __fdividef(tau2, det);
+  const float ex = __fsqrt_rn(fmaxf(k * c, 0.0f)) * 1.001f + 1e-3f;
+  const float ey = __fsqrt_rn(fmaxf(k * a, 0.0f)) * 1.001f + 1e-3f;
   return r0.x + ex >= x0 && r0.x - ex <= x1 && r0.y + ey >= y0 && r0.y - ey <= y1;
 }
 
@@ -98,19 +101,32 @@ struct PixelState {
   bool done;
 };
 
-// One front-to-back step of the reference blend (inc/splatting.hpp:284-296) for one pixel.
-// t1 = (a*dx)*dx and bdx = b*dx are shared by the two pixels of a lane (same column).
-template <bool COUNTERS>
-__device__ __forceinline__ void blend_step(PixelState& p, float fy, float4 r0, float4 r1, float r2, float t1,
-                                           float bdx, uint32_t k) {
-  if (p.done) return;
+// Power of one (pixel, splat) pair in the reference's exact op order (inc/splatting.hpp:
+// 284-287). t1 = (a*dx)*dx and bdx = b*dx are shared by the two pixels of a lane.
+__device__ __forceinline__ float blend_power_dy(float fy, float4 r0, float c, float t1, float bdx) {
   const float dy = __fsub_rn(fy, r0.y);
-  const float t2 = __fmul_rn(__fmul_rn(r1.x, dy), dy);
-  const float power = __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), __fmul_rn(bdx, dy));
-  if (power > 0.0f || power < kPowerFloor) return;
-  float e;
-  const float alpha = fminf(kAlphaClamp, alpha_raw(r1.y, power, &e));
-  if (alpha < kAlphaSkip) return;
+  const float t2 = __fmul_rn(__fmul_rn(c, dy), dy);
+  return __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), __fmul_rn(bdx, dy));
+}
+
+// alpha_max * exp(power) with the fast exp; *near = the product lies within the fast path's
+// error bound of the 1/255 skip threshold (the caller then recomputes it exactly).
+__device__ __forceinline__ float alpha_fast(float amax, float power, bool* near) {
+  const float ar = __fmul_rn(amax, __expf(power));
+  *near = power <= 0.0f && fabsf(ar - kAlphaSkip) <= kGuardRel * kAlphaSkip;
+  return ar;
+}
+
+// Final alpha of the reference step, or -1 when it skips (power > 0 or alpha < 1/255).
+__device__ __forceinline__ float alpha_final(float power, float ar) {
+  const float alpha = fminf(kAlphaClamp, ar);
+  return (power <= 0.0f && alpha >= kAlphaSkip) ? alpha : -1.0f;
+}
+
+// The transmittance-dependent half of one reference step (inc/splatting.hpp:291-296).
+template <bool COUNTERS>
+__device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr, float cg, float cb, uint32_t k) {
+  if (p.done || alpha < 0.0f) return;
   const float Tn = __fmul_rn(p.T, __fsub_rn(1.0f, alpha));
   if (Tn < kTransmittanceStop) {
     p.done = true;
@@ -118,9 +134,9 @@ __device__ __forceinline__ void blend_step(PixelState& p, float fy, float4 r0, f
     return;
   }
   const float w = __fmul_rn(alpha, p.T);
-  p.C0 = fmaf(r1.z, w, p.C0);
-  p.C1 = fmaf(r1.w, w, p.C1);
-  p.C2 = fmaf(r2, w, p.C2);
+  p.C0 = fmaf(cr, w, p.C0);
+  p.C1 = fmaf(cg, w, p.C1);
+  p.C2 = fmaf(cb, w, p.C2);
   p.T = Tn;
   p.last = k + 1;
   if (COUNTERS) ++p.contrib;
@@ -148,44 +164,107 @@ __global__ void __launch_bounds__(kFwdThreads) blend_forward_kernel(BlendArgs a)
   const float fx = static_cast<float>(px) + 0.5f;
   const float fy0 = static_cast<float>(py0) + 0.5f, fy1 = static_cast<float>(py1) + 0.5f;
   const float bx0 = static_cast<float>(bx) + 0.5f, by0 = static_cast<float>(by) + 0.5f;
+  const long long t_start = COUNTERS ? clock64() : 0;
+  unsigned long long warp_evals = 0;
   PixelState p0{1.0f, 0.0f, 0.0f, 0.0f, lo, hi, 0u, !(px < a.width && py0 < a.height)};
   PixelState p1{1.0f, 0.0f, 0.0f, 0.0f, lo, hi, 0u, !(px < a.width && py1 < a.height)};
 
-  float4 n0 = make_float4(0.f, 0.f, 0.f, 0.f), n1 = n0;
-  float n2 = 0.0f;
-  if (lo + lane < hi) {
-    const uint32_t g = __ldg(a.sorted_gauss + lo + lane);
-    n0 = __ldg(a.rec.rec0 + g);
-    n1 = __ldg(a.rec.rec1 + g);
-    n2 = __ldg(a.rec.rec2 + g);
-  }
+  // records of the tile's list are contiguous (sorted order): each chunk is one coalesced
+  // 1.5 KB read; two chunks are kept in flight ahead of the one being blended.
+  const SortedRec zero{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+  SortedRec cur = lo + lane < hi ? a.srec[lo + lane] : zero;
+  SortedRec nxt = lo + 32 + lane < hi ? a.srec[lo + 32 + lane] : zero;
   for (uint32_t base = lo; base < hi; base += 32) {
     if (__all_sync(0xffffffffu, p0.done && p1.done)) break;
-    const bool pass = base + lane < hi && box_may_hit(n0, n1, bx0, bx0 + 7.0f, by0, by0 + 7.0f);
-    s0[warp][lane] = n0;
-    s1[warp][lane] = n1;
-    s2[warp][lane] = n2;
+    const bool pass = base + lane < hi && box_may_hit(cur.a, cur.b, bx0, bx0 + 7.0f, by0, by0 + 7.0f);
+    s0[warp][lane] = cur.a;
+    s1[warp][lane] = cur.b;
+    s2[warp][lane] = cur.c.x;
     uint32_t mask = __ballot_sync(0xffffffffu, pass);
-    if (base + 32 + lane < hi) {  // prefetch the next chunk
-      const uint32_t g = __ldg(a.sorted_gauss + base + 32 + lane);
-      n0 = __ldg(a.rec.rec0 + g);
-      n1 = __ldg(a.rec.rec1 + g);
-      n2 = __ldg(a.rec.rec2 + g);
-    }
+    if (COUNTERS) warp_evals += __popc(mask);
+    cur = nxt;
+    if (base + 64 + lane < hi) nxt = a.srec[base + 64 + lane];
     __syncwarp();
+    // Groups of kGroup surviving splats: their alphas (independent of transmittance) are
+    // computed together for both pixels (8 independent power/exp chains), then applied in
+    // list order -- the same decisions as the sequential reference loop.
     while (mask) {
-      const int j = __ffs(mask) - 1;
-      mask &= mask - 1;
-      const float4 r0 = s0[warp][j];
-      const float4 r1 = s1[warp][j];
-      const float r2 = s2[warp][j];
-      const float dx = __fsub_rn(fx, r0.x);
-      const float t1 = __fmul_rn(__fmul_rn(r0.z, dx), dx);
-      const float bdx = __fmul_rn(r0.w, dx);
-      blend_step<COUNTERS>(p0, fy0, r0, r1, r2, t1, bdx, base + j);
-      blend_step<COUNTERS>(p1, fy1, r0, r1, r2, t1, bdx, base + j);
+      int js[kGroup];
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q) {
+        js[q] = mask ? __ffs(mask) - 1 : -1;
+        mask &= mask - 1;
+      }
+      float al0[kGroup], al1[kGroup], pw0[kGroup], pw1[kGroup], am[kGroup], cr[kGroup], cg_[kGroup], cb[kGroup];
+      bool any_near = false;
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q) {
+        const int jj = js[q] >= 0 ? js[q] : 0;
+        const float4 r0 = s0[warp][jj];
+        const float4 r1 = s1[warp][jj];
+        cr[q] = r1.z;
+        cg_[q] = r1.w;
+        cb[q] = s2[warp][jj];
+        am[q] = r1.y;
+        const float dx = __fsub_rn(fx, r0.x);
+        const float t1 = __fmul_rn(__fmul_rn(r0.z, dx), dx);
+        const float bdx = __fmul_rn(r0.w, dx);
+        pw0[q] = blend_power_dy(fy0, r0, r1.x, t1, bdx);
+        pw1[q] = blend_power_dy(fy1, r0, r1.x, t1, bdx);
+        bool n0, n1;
+        al0[q] = alpha_fast(r1.y, pw0[q], &n0);
+        al1[q] = alpha_fast(r1.y, pw1[q], &n1);
+        any_near |= (n0 && !p0.done) || (n1 && !p1.done);
+      }
+      if (__any_sync(0xffffffffu, any_near)) {  // rare: exact exp near the skip threshold
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) {
+          bool n;
+          alpha_fast(am[q], pw0[q], &n);
+          if (n) al0[q] = __fmul_rn(am[q], cr_expf(pw0[q]));
+          alpha_fast(am[q], pw1[q], &n);
+          if (n) al1[q] = __fmul_rn(am[q], cr_expf(pw1[q]));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q) {
+        al0[q] = alpha_final(pw0[q], al0[q]);
+        al1[q] = alpha_final(pw1[q], al1[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q) {
+        if (js[q] < 0) break;
+        blend_apply<COUNTERS>(p0, al0[q], cr[q], cg_[q], cb[q], base + js[q]);
+        blend_apply<COUNTERS>(p1, al1[q], cr[q], cg_[q], cb[q], base + js[q]);
+      }
     }
     __syncwarp();
+  }
+  if (COUNTERS) {
+    const long long t_cta = clock64() - t_start;
+    unsigned long long ev = 0, ec = 0;
+    const PixelState* pp[2] = {&p0, &p1};
+    const int yy[2] = {py0, py1};
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (px < a.width && yy[q] < a.height) {
+        // E_eval as the reference counts it: k-loop iterations entered, including the one
+        // that terminates (inc/splatting.hpp:282-292).
+        ev += (pp[q]->stop < hi) ? (pp[q]->stop - lo + 1) : (hi - lo);
+        ec += pp[q]->contrib;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ev += __shfl_xor_sync(0xffffffffu, ev, o);
+      ec += __shfl_xor_sync(0xffffffffu, ec, o);
+    }
+    if (lane == 0) {
+      atomicAdd(a.counters + 0, ev);
+      atomicAdd(a.counters + 1, ec);
+      atomicAdd(a.counters + 2, warp_evals);
+      atomicMax(a.counters + 3, static_cast<unsigned long long>(t_cta));
+      if (a.tile_cycles) atomicMax(a.tile_cycles + tile, static_cast<unsigned long long>(t_cta));
+    }
   }
   const PixelState* ps[2] = {&p0, &p1};
   const int pys[2] = {py0, py1};
@@ -199,13 +278,6 @@ __global__ void __launch_bounds__(kFwdThreads) blend_forward_kernel(BlendArgs a)
       a.image[pix * 3 + 2] = p.C2 + p.T * a.bg[2];
       a.final_T[pix] = p.T;
       a.last[pix] = p.last;
-      if (COUNTERS) {
-        // E_eval as the reference counts it: k-loop iterations entered, including the one
-        // that terminates (inc/splatting.hpp:282-292).
-        const unsigned long long n_eval = (p.stop < hi) ? (p.stop - lo + 1) : (hi - lo);
-        atomicAdd(a.counters + 0, n_eval);
-        atomicAdd(a.counters + 1, static_cast<unsigned long long>(p.contrib));
-      }
     }
   }
 }
@@ -272,12 +344,12 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     __syncthreads();
     if (threadIdx.x < cnt) {
       const uint32_t k = bstart + threadIdx.x;
-      const uint32_t g = __ldg(a.sorted_gauss + k);
-      const float4 r0 = __ldg(a.rec.rec0 + g);
-      const float4 r1 = __ldg(a.rec.rec1 + g);
+      const SortedRec rr = a.srec[k];
+      const float4 r0 = rr.a;
+      const float4 r1 = rr.b;
       s0[threadIdx.x] = r0;
       s1[threadIdx.x] = r1;
-      s2[threadIdx.x] = __ldg(a.rec.rec2 + g);
+      s2[threadIdx.x] = rr.c.x;
       s_emit[threadIdx.x] = __ldg(a.sorted_emit + k);
       s_mask[threadIdx.x] = static_cast<uint8_t>(warp_mask(r0, r1, tile_x0, tile_y0));
     }

@@ -173,9 +173,10 @@ def test_counters_match_oracle(rast, oracle_mod):
     rast.set_flags(_lib.FGS_FLAG_COUNTERS)
     try:
         fwd(rast, sc, cams[0], deg)
-        ev, ec = rast.debug("counters", np.uint64)
+        ev, ec, warp_iters, _ = rast.debug("counters", np.uint64)
     finally:
         rast.set_flags(0)
     st = oracle_mod.render(sc, cams[0], sh_degree=deg).stats()
     assert int(ec) == int(st["e_contrib"])
     assert int(ev) == int(st["e_eval"])
+    assert 0 < int(warp_iters) * 64 <= 2 * int(ev)  # culled warp-block evaluations actually done
