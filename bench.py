@@ -313,7 +313,7 @@ def run_ours(args, ws, rank, local):
         "num_splats": st.num_splats,
         "e_eval": int(counters[0]),
         "e_contrib": int(counters[1]),
-        "blend_pixel_evals_after_culling": int(counters_all[2]) * 64,
+        "blend_pixel_evals_after_culling": int(counters_all[2]),
         "fp32_peak_tops": round(fp32_peak / 1e12, 2),
     }
     if rank == 0:

@@ -362,6 +362,33 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
     r.c = make_float4(__ldg(a.rec2 + g), 0.0f, 0.0f, 0.0f);
     a.sorted_rec[k] = r;
   }
+  if (a.tile_order == nullptr) return;
+  grid.sync();
+  // ---- blend schedule: tiles by descending list length (log2 buckets), empty tiles last ----
+  if (blockIdx.x != 0) return;
+  constexpr int kB = 18;
+  if (tid < kB) sm.hist[tid] = 0;
+  __syncthreads();
+  for (int t = tid; t < a.num_tiles; t += kT) {
+    const uint32_t c = a.tile_offsets[t + 1] - a.tile_offsets[t];
+    const int b = c == 0 ? kB - 1 : 16 - min(16, 31 - __clz(c));
+    atomicAdd(&sm.hist[b], 1u);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t run = 0;
+    for (int b = 0; b < kB; ++b) {
+      const uint32_t c = sm.hist[b];
+      sm.run[b] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < a.num_tiles; t += kT) {
+    const uint32_t c = a.tile_offsets[t + 1] - a.tile_offsets[t];
+    const int b = c == 0 ? kB - 1 : 16 - min(16, 31 - __clz(c));
+    a.tile_order[atomicAdd(&sm.run[b], 1u)] = static_cast<uint32_t>(t);
+  }
 }
 
 // Debug export: the reference's pre-sort key list (source order, ty-major, tx-minor).

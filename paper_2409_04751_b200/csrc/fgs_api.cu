@@ -8,6 +8,7 @@
 //   K4a reverse blend (per-intersection partials) -> K4b preprocess backward.
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -62,7 +63,7 @@ struct fgs_context {
   DevBuf<fgs::SortedRec> sorted_rec;
   DevBuf<float> partials;
   // per tile / pixel
-  DevBuf<uint32_t> tile_offsets, last;
+  DevBuf<uint32_t> tile_offsets, last, tile_order;
   DevBuf<float> final_T;
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
@@ -97,6 +98,7 @@ struct fgs_context {
   uint32_t* sorted_tiles = nullptr;  // level-2 result keys
   uint32_t* sorted_emit = nullptr;   // level-2 result values
   size_t aux_bytes = 0;
+  int px_per_lane = 1;  // tuning knob: FGS_PX_PER_LANE env (1 or 2)
   fgs::BinArgs bin_args{};
 };
 
@@ -190,6 +192,7 @@ int fgs_create(int device, fgs_context** out) {
   if (e != cudaSuccess) return FGS_ECUDA;
   auto* ctx = new fgs_context();
   ctx->device = device;
+  if (const char* v = std::getenv("FGS_PX_PER_LANE")) ctx->px_per_lane = std::atoi(v) == 2 ? 2 : 1;
   e = cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   if (e != cudaSuccess) {
     delete ctx;
@@ -219,7 +222,7 @@ int fgs_destroy(fgs_context* ctx) {
   for (auto* b : {&ctx->dkey, &ctx->ckey, &ctx->cval, &ctx->dkey_a, &ctx->dkey_b, &ctx->perm_a, &ctx->perm_b,
                   &ctx->touched, &ctx->rank, &ctx->offsets, &ctx->scan_status, &ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b,
                   &ctx->emit_a, &ctx->emit_b, &ctx->emit_gauss, &ctx->sorted_gauss, &ctx->sorted_emit_buf,
-                  &ctx->tile_offsets, &ctx->last,
+                  &ctx->tile_offsets, &ctx->last, &ctx->tile_order,
                   &ctx->scalars})
     b->release();
   ctx->rect.release();
@@ -406,6 +409,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.rec1 = ctx->rec1.p;
   bn.rec2 = ctx->rec2.p;
   bn.sorted_rec = ctx->sorted_rec.p;
+  FGS_CHECK(ctx->tile_order.ensure(num_tiles));
+  bn.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
   FGS_CHECK(fgs::bin_level2(bn, st));
   if (I > 0) ++launches;
   ctx->sorted_tiles = bn.passes2 == 1 ? ctx->tkey_a.p : ctx->tkey_b.p;
@@ -427,6 +432,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;
   ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
+  ba.px_per_lane = ctx->px_per_lane;
+  ba.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
   if (ba.counters) {
     FGS_CHECK(ctx->tile_cycles.ensure(num_tiles));
     FGS_CHECK(cudaMemsetAsync(ctx->tile_cycles.p, 0, num_tiles * sizeof(unsigned long long), st));

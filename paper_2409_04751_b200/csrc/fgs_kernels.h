@@ -67,6 +67,8 @@ struct BlendArgs {
   uint32_t* last;                // H*W: index one past the last contributing entry
   unsigned long long* counters;  // optional: E_eval, E_contrib, culled evals, max CTA cycles
   unsigned long long* tile_cycles;  // optional (with counters): per-tile CTA cycles
+  const uint32_t* tile_order;    // optional: CTA -> tile (heaviest lists first)
+  int px_per_lane;               // forward blend: 1 or 2 pixels per lane
   // backward
   const float* dl_dimage;
   float* partials;               // I x 9
@@ -112,6 +114,7 @@ struct BinArgs {
   const float4* rec1;
   const float* rec2;
   SortedRec* sorted_rec;       // [I] records in sorted order
+  uint32_t* tile_order;        // [num_tiles] blend schedule (optional)
 };
 
 // Words of part_scan + part_radix scratch the persistent kernels need.

@@ -27,7 +27,6 @@ namespace {
 constexpr int kBlend = 256;     // threads per tile CTA = pixels per tile
 constexpr int kBwdBatch = 128;  // splats per backward batch
 constexpr int kWarps = kBlend / 32;
-constexpr int kFwdThreads = 128;  // forward: 4 warps x 64 pixels
 constexpr int kGroup = 4;         // forward: splats whose alphas are computed together
 
 // Warp w of a tile owns the 8x4 pixel block at (8*(w&1), 4*(w>>1)); lane l the pixel
@@ -142,41 +141,53 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr
   if (COUNTERS) ++p.contrib;
 }
 
-// K3 forward blend. One 128-thread CTA per 16x16 tile; warp w owns the 8x8 block at
-// (8*(w&1), 8*(w>>1)) and lane l the two pixels (l&7, l>>3) and (l&7, (l>>3)+4), which share a
-// column (and so (a*dx)*dx and b*dx). Warps walk the tile's sorted list independently in
-// 32-splat chunks (no CTA barriers): each lane gathers one record, tests it against the warp's
-// 8x8 block (box_may_hit), the warp keeps the ballot of survivors and blends them in order
-// from warp-private shared memory while the next chunk's records are already being loaded.
-// A warp stops when all its 64 pixels have met the reference's termination rule.
-template <bool COUNTERS>
-__global__ void __launch_bounds__(kFwdThreads) blend_forward_kernel(BlendArgs a) {
-  constexpr int NW = kFwdThreads / 32;
+// K3 forward blend. One CTA per 16x16 tile (scheduled heaviest list first when a tile order
+// is given). PX = pixels per lane: warp w owns an 8 x (4*PX) block at (8*(w&1), 4*PX*(w>>1));
+// lane l the pixel(s) (l&7, (l>>3) + 4*q), q < PX, which share a column (so (a*dx)*dx and
+// b*dx are computed once). Warps walk the tile's sorted list independently in 32-splat chunks
+// (no CTA barriers): each lane reads one record (the list is contiguous in sorted order, two
+// chunks stay in flight), tests it against the warp's block (box_may_hit), and the warp blends
+// the ballot of survivors in order from warp-private shared memory, kGroup splats at a time
+// (alphas first, independent of transmittance; then the sequential transmittance updates).
+// A warp stops when all its pixels have met the reference's termination rule.
+template <bool COUNTERS, int PX>
+__global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
+  constexpr int NW = 8 / PX;
   __shared__ float4 s0[NW][32];
   __shared__ float4 s1[NW][32];
   __shared__ float s2[NW][32];
-  const int tile = blockIdx.x;
+  const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bx = tx * kTile + ((warp & 1) << 3), by = ty * kTile + ((warp >> 1) << 3);
-  const int px = bx + (lane & 7), py0 = by + (lane >> 3), py1 = py0 + 4;
+  const int bx = tx * kTile + ((warp & 1) << 3), by = ty * kTile + (warp >> 1) * 4 * PX;
+  const int px = bx + (lane & 7);
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
   const float fx = static_cast<float>(px) + 0.5f;
-  const float fy0 = static_cast<float>(py0) + 0.5f, fy1 = static_cast<float>(py1) + 0.5f;
   const float bx0 = static_cast<float>(bx) + 0.5f, by0 = static_cast<float>(by) + 0.5f;
   const long long t_start = COUNTERS ? clock64() : 0;
   unsigned long long warp_evals = 0;
-  PixelState p0{1.0f, 0.0f, 0.0f, 0.0f, lo, hi, 0u, !(px < a.width && py0 < a.height)};
-  PixelState p1{1.0f, 0.0f, 0.0f, 0.0f, lo, hi, 0u, !(px < a.width && py1 < a.height)};
+  PixelState ps[PX];
+  int py[PX];
+  float fy[PX];
+#pragma unroll
+  for (int q = 0; q < PX; ++q) {
+    py[q] = by + (lane >> 3) + 4 * q;
+    fy[q] = static_cast<float>(py[q]) + 0.5f;
+    ps[q] = PixelState{1.0f, 0.0f, 0.0f, 0.0f, lo, hi, 0u, !(px < a.width && py[q] < a.height)};
+  }
+  auto all_done = [&]() {
+    bool d = true;
+#pragma unroll
+    for (int q = 0; q < PX; ++q) d = d && ps[q].done;
+    return d;
+  };
 
-  // records of the tile's list are contiguous (sorted order): each chunk is one coalesced
-  // 1.5 KB read; two chunks are kept in flight ahead of the one being blended.
   const SortedRec zero{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
   SortedRec cur = lo + lane < hi ? a.srec[lo + lane] : zero;
   SortedRec nxt = lo + 32 + lane < hi ? a.srec[lo + 32 + lane] : zero;
   for (uint32_t base = lo; base < hi; base += 32) {
-    if (__all_sync(0xffffffffu, p0.done && p1.done)) break;
-    const bool pass = base + lane < hi && box_may_hit(cur.a, cur.b, bx0, bx0 + 7.0f, by0, by0 + 7.0f);
+    if (__all_sync(0xffffffffu, all_done())) break;
+    const bool pass = base + lane < hi && box_may_hit(cur.a, cur.b, bx0, bx0 + 7.0f, by0, by0 + (4.0f * PX - 1.0f));
     s0[warp][lane] = cur.a;
     s1[warp][lane] = cur.b;
     s2[warp][lane] = cur.c.x;
@@ -185,9 +196,6 @@ __global__ void __launch_bounds__(kFwdThreads) blend_forward_kernel(BlendArgs a)
     cur = nxt;
     if (base + 64 + lane < hi) nxt = a.srec[base + 64 + lane];
     __syncwarp();
-    // Groups of kGroup surviving splats: their alphas (independent of transmittance) are
-    // computed together for both pixels (8 independent power/exp chains), then applied in
-    // list order -- the same decisions as the sequential reference loop.
     while (mask) {
       int js[kGroup];
 #pragma unroll
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(kFwdThreads) blend_forward_kernel(BlendArgs a)
         js[q] = mask ? __ffs(mask) - 1 : -1;
         mask &= mask - 1;
       }
-      float al0[kGroup], al1[kGroup], pw0[kGroup], pw1[kGroup], am[kGroup], cr[kGroup], cg_[kGroup], cb[kGroup];
+      float al[kGroup][PX], pw[kGroup][PX], am[kGroup], cr[kGroup], cg_[kGroup], cb[kGroup];
       bool any_near = false;
 #pragma unroll
       for (int q = 0; q < kGroup; ++q) {
@@ -209,33 +217,30 @@ __global__ void __launch_bounds__(kFwdThreads) blend_forward_kernel(BlendArgs a)
         const float dx = __fsub_rn(fx, r0.x);
         const float t1 = __fmul_rn(__fmul_rn(r0.z, dx), dx);
         const float bdx = __fmul_rn(r0.w, dx);
-        pw0[q] = blend_power_dy(fy0, r0, r1.x, t1, bdx);
-        pw1[q] = blend_power_dy(fy1, r0, r1.x, t1, bdx);
-        bool n0, n1;
-        al0[q] = alpha_fast(r1.y, pw0[q], &n0);
-        al1[q] = alpha_fast(r1.y, pw1[q], &n1);
-        any_near |= (n0 && !p0.done) || (n1 && !p1.done);
+#pragma unroll
+        for (int u = 0; u < PX; ++u) {
+          pw[q][u] = blend_power_dy(fy[u], r0, r1.x, t1, bdx);
+          bool nr;
+          al[q][u] = alpha_fast(r1.y, pw[q][u], &nr);
+          any_near |= nr && !ps[u].done;
+        }
       }
       if (__any_sync(0xffffffffu, any_near)) {  // rare: exact exp near the skip threshold
 #pragma unroll
-        for (int q = 0; q < kGroup; ++q) {
-          bool n;
-          alpha_fast(am[q], pw0[q], &n);
-          if (n) al0[q] = __fmul_rn(am[q], cr_expf(pw0[q]));
-          alpha_fast(am[q], pw1[q], &n);
-          if (n) al1[q] = __fmul_rn(am[q], cr_expf(pw1[q]));
-        }
-      }
+        for (int q = 0; q < kGroup; ++q)
 #pragma unroll
-      for (int q = 0; q < kGroup; ++q) {
-        al0[q] = alpha_final(pw0[q], al0[q]);
-        al1[q] = alpha_final(pw1[q], al1[q]);
+          for (int u = 0; u < PX; ++u) {
+            bool nr;
+            alpha_fast(am[q], pw[q][u], &nr);
+            if (nr) al[q][u] = __fmul_rn(am[q], cr_expf(pw[q][u]));
+          }
       }
 #pragma unroll
       for (int q = 0; q < kGroup; ++q) {
         if (js[q] < 0) break;
-        blend_apply<COUNTERS>(p0, al0[q], cr[q], cg_[q], cb[q], base + js[q]);
-        blend_apply<COUNTERS>(p1, al1[q], cr[q], cg_[q], cb[q], base + js[q]);
+#pragma unroll
+        for (int u = 0; u < PX; ++u)
+          blend_apply<COUNTERS>(ps[u], alpha_final(pw[q][u], al[q][u]), cr[q], cg_[q], cb[q], base + js[q]);
       }
     }
     __syncwarp();
@@ -243,15 +248,13 @@ __global__ void __launch_bounds__(kFwdThreads) blend_forward_kernel(BlendArgs a)
   if (COUNTERS) {
     const long long t_cta = clock64() - t_start;
     unsigned long long ev = 0, ec = 0;
-    const PixelState* pp[2] = {&p0, &p1};
-    const int yy[2] = {py0, py1};
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-      if (px < a.width && yy[q] < a.height) {
+    for (int q = 0; q < PX; ++q)
+      if (px < a.width && py[q] < a.height) {
         // E_eval as the reference counts it: k-loop iterations entered, including the one
         // that terminates (inc/splatting.hpp:282-292).
-        ev += (pp[q]->stop < hi) ? (pp[q]->stop - lo + 1) : (hi - lo);
-        ec += pp[q]->contrib;
+        ev += (ps[q].stop < hi) ? (ps[q].stop - lo + 1) : (hi - lo);
+        ec += ps[q].contrib;
       }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -261,18 +264,16 @@ __global__ void __launch_bounds__(kFwdThreads) blend_forward_kernel(BlendArgs a)
     if (lane == 0) {
       atomicAdd(a.counters + 0, ev);
       atomicAdd(a.counters + 1, ec);
-      atomicAdd(a.counters + 2, warp_evals);
+      atomicAdd(a.counters + 2, warp_evals * (32 * PX));
       atomicMax(a.counters + 3, static_cast<unsigned long long>(t_cta));
       if (a.tile_cycles) atomicMax(a.tile_cycles + tile, static_cast<unsigned long long>(t_cta));
     }
   }
-  const PixelState* ps[2] = {&p0, &p1};
-  const int pys[2] = {py0, py1};
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const PixelState& p = *ps[q];
-    if (px < a.width && pys[q] < a.height) {
-      const size_t pix = static_cast<size_t>(pys[q]) * a.width + px;
+  for (int q = 0; q < PX; ++q) {
+    const PixelState& p = ps[q];
+    if (px < a.width && py[q] < a.height) {
+      const size_t pix = static_cast<size_t>(py[q]) * a.width + px;
       a.image[pix * 3 + 0] = p.C0 + p.T * a.bg[0];
       a.image[pix * 3 + 1] = p.C1 + p.T * a.bg[1];
       a.image[pix * 3 + 2] = p.C2 + p.T * a.bg[2];
@@ -432,10 +433,15 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
 }  // namespace
 
 int blend_forward(const BlendArgs& a, cudaStream_t st) {
-  if (a.counters)
-    blend_forward_kernel<true><<<a.tiles_x * a.tiles_y, kFwdThreads, 0, st>>>(a);
-  else
-    blend_forward_kernel<false><<<a.tiles_x * a.tiles_y, kFwdThreads, 0, st>>>(a);
+  const int px = a.px_per_lane == 2 ? 2 : 1;
+  const int threads = 256 / px;
+  if (a.counters) {
+    if (px == 2) blend_forward_kernel<true, 2><<<a.tiles_x * a.tiles_y, threads, 0, st>>>(a);
+    else blend_forward_kernel<true, 1><<<a.tiles_x * a.tiles_y, threads, 0, st>>>(a);
+  } else {
+    if (px == 2) blend_forward_kernel<false, 2><<<a.tiles_x * a.tiles_y, threads, 0, st>>>(a);
+    else blend_forward_kernel<false, 1><<<a.tiles_x * a.tiles_y, threads, 0, st>>>(a);
+  }
   return 1;
 }
 

@@ -179,4 +179,4 @@ def test_counters_match_oracle(rast, oracle_mod):
     st = oracle_mod.render(sc, cams[0], sh_degree=deg).stats()
     assert int(ec) == int(st["e_contrib"])
     assert int(ev) == int(st["e_eval"])
-    assert 0 < int(warp_iters) * 64 <= 2 * int(ev)  # culled warp-block evaluations actually done
+    assert 0 < int(warp_iters) <= 2 * int(ev)  # pixel evaluations actually done after culling
