@@ -61,7 +61,7 @@ struct fgs_context {
   // per intersection
   DevBuf<uint32_t> tkey, emit, tkey_a, tkey_b, emit_a, emit_b, emit_gauss, sorted_gauss, sorted_emit_buf;
   DevBuf<fgs::SortedRec> sorted_rec;
-  DevBuf<float> partials;
+  DevBuf<float> partials, partial_tile;
   // per tile / pixel
   DevBuf<uint32_t> tile_offsets, last, tile_order;
   DevBuf<float> final_T;
@@ -213,7 +213,7 @@ int fgs_destroy(fgs_context* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   else cudaDeviceSynchronize();
-  for (auto* b : {&ctx->rec2, &ctx->final_T, &ctx->partials, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
+  for (auto* b : {&ctx->rec2, &ctx->final_T, &ctx->partials, &ctx->partial_tile, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
                   &ctx->h_sh, &ctx->h_img, &ctx->h_dl, &ctx->h_grad})
     b->release();
   ctx->rec0.release();
@@ -480,7 +480,8 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   cudaStream_t st = ctx->stream;
   const int64_t n = ctx->n, I = ctx->num_isect;
   if (n == 0) return FGS_OK;
-  FGS_CHECK(ctx->partials.ensure(static_cast<size_t>(I > 0 ? I : 1) * 9));
+  FGS_CHECK(ctx->partials.ensure(static_cast<size_t>(I > 0 ? I : 1) * fgs::kBwdWarps * 9));
+  FGS_CHECK(ctx->partial_tile.ensure(static_cast<size_t>(I > 0 ? I : 1) * 9));
 
   fgs::BlendArgs ba{};
   ba.width = ctx->cam.width;
@@ -496,11 +497,14 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   ba.last = ctx->last.p;
   ba.dl_dimage = dl_dimage;
   ba.partials = ctx->partials.p;
+  ba.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
   const bool timing = (ctx->flags & FGS_FLAG_TIMING) != 0;
   if (timing && ctx->pending.size() > 64) drain_sets(ctx, 8);
   cudaEvent_t* ev = timing ? take_set(ctx, 1)->e : nullptr;
   if (timing) cudaEventRecord(ev[0], st);
   if (I > 0) ctx->launches += fgs::blend_backward(ba, st);
+  ctx->launches += fgs::combine_partials(ctx->tkey.p, ctx->emit_gauss.p, ctx->rec0.p, ctx->rec1.p, ctx->partials.p,
+                                         ctx->partial_tile.p, ctx->tiles_x, static_cast<int>(I), st);
   if (timing) cudaEventRecord(ev[1], st);
 
   fgs::PreprocessBackwardArgs pb{};
@@ -520,7 +524,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.touched = ctx->touched.p;
   pb.rank = ctx->rank.p;
   pb.offsets = ctx->offsets.p;
-  pb.partials = ctx->partials.p;
+  pb.partials = ctx->partial_tile.p;
   pb.d_means = grads->d_means;
   pb.d_rotations = grads->d_rotations;
   pb.d_log_scales = grads->d_log_scales;

@@ -83,4 +83,50 @@ __device__ __forceinline__ float alpha_raw(float alpha_max, float power, float* 
 
 __host__ __device__ inline int div_up(int a, int b) { return (a + b - 1) / b; }
 
+// Conservative test: can any pixel centre of the box [x0, x1] x [y0, y1] reach
+// alpha >= 1/255 for this splat? alpha(d) = alpha_max * exp(-q(d)/2) with
+// q = a dx^2 + 2b dx dy + c dy^2, so alpha >= 1/255 needs q <= 2 ln(255 alpha_max), whose
+// bounding box has half-extents sqrt(2 tau Sigma_xx), sqrt(2 tau Sigma_yy) (Sigma = Q^-1).
+// The box is inflated (0.2% + 0.1% + 1e-3 px), far beyond the ~1e-6 relative error of the
+// fast-math evaluation and of the blend's fp32 power, so a culled (pixel, splat) pair is one the
+// reference would `continue` on. Every op is an explicit rounding intrinsic, so the result is
+// bit-identical in every translation unit (the backward writer and the K4b reader agree).
+// Half-extents (ex, ey) of the splat's alpha >= 1/255 region, inflated; returns 0 when the
+// splat can never reach 1/255 (alpha_max < 1/255), 2 when no finite bound applies (degenerate
+// conic: never cull), 1 otherwise.
+__device__ __forceinline__ int splat_extent(float4 r0, float4 r1, float& ex, float& ey) {
+  const float a = r0.z, b = r0.w, c = r1.x, amax = r1.y;
+  ex = ey = 0.0f;
+  if (!(amax >= kAlphaSkip)) return 0;
+  const float det = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, b));
+  if (!(det > 0.0f) || !(a > 0.0f) || !(c > 0.0f)) return 2;
+  const float tau2 = __fadd_rn(__fmul_rn(__fmul_rn(2.0f, __logf(__fmul_rn(255.0f, amax))), 1.002f), 1e-3f);
+  const float k = __fdividef(tau2, det);
+  ex = __fadd_rn(__fmul_rn(__fsqrt_rn(fmaxf(__fmul_rn(k, c), 0.0f)), 1.001f), 1e-3f);
+  ey = __fadd_rn(__fmul_rn(__fsqrt_rn(fmaxf(__fmul_rn(k, a), 0.0f)), 1.001f), 1e-3f);
+  return 1;
+}
+
+__device__ __forceinline__ bool extent_hits(int kind, float mx, float my, float ex, float ey, float x0, float x1,
+                                            float y0, float y1) {
+  if (kind != 1) return kind == 2;
+  return __fadd_rn(mx, ex) >= x0 && __fsub_rn(mx, ex) <= x1 && __fadd_rn(my, ey) >= y0 && __fsub_rn(my, ey) <= y1;
+}
+
+__device__ __forceinline__ bool box_may_hit(float4 r0, float4 r1, float x0, float x1, float y0, float y1) {
+  float ex, ey;
+  const int kind = splat_extent(r0, r1, ex, ey);
+  return extent_hits(kind, r0.x, r0.y, ex, ey, x0, x1, y0, y1);
+}
+
+// Backward blend geometry: 8 warps per 16x16 tile, warp w owns the 8x4 pixel block at
+// (8*(w&1), 4*(w>>1)); the box spans the block's pixel centres.
+constexpr int kBwdWarps = 8;
+__device__ __forceinline__ void bwd_block_box(int tx, int ty, int w, float& x0, float& x1, float& y0, float& y1) {
+  x0 = static_cast<float>(tx * kTile + ((w & 1) << 3)) + 0.5f;
+  x1 = x0 + 7.0f;
+  y0 = static_cast<float>(ty * kTile + ((w >> 1) << 2)) + 0.5f;
+  y1 = y0 + 3.0f;
+}
+
 }  // namespace fgs

@@ -47,7 +47,7 @@ struct PreprocessBackwardArgs {
   const uint32_t* touched;
   const uint32_t* rank;
   const uint32_t* offsets;   // per depth rank
-  const float* partials;     // I x 9
+  const float* partials;     // I x 9 per-intersection sums (K4c output)
   float* d_means;
   float* d_rotations;
   float* d_log_scales;
@@ -71,7 +71,7 @@ struct BlendArgs {
   int px_per_lane;               // forward blend: 1 or 2 pixels per lane
   // backward
   const float* dl_dimage;
-  float* partials;               // I x 9
+  float* partials;               // I x 8 x 9
 };
 
 __global__ void preprocess_kernel(PreprocessArgs a);
@@ -130,6 +130,9 @@ cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* ke
 // ---- blend (raster.cu) ----
 int blend_forward(const BlendArgs& a, cudaStream_t st);
 int blend_backward(const BlendArgs& a, cudaStream_t st);
+// K4c: per intersection, sum the per-block partials of the blocks passing the culling test.
+int combine_partials(const uint32_t* tile_keys, const uint32_t* emit_gauss, const float4* rec0, const float4* rec1,
+                     const float* partials, float* partial_tile, int tiles_x, int ni, cudaStream_t st);
 // FP32 pipe probe: returns achieved non-FMA fp32 op/s (FMUL + FADD, no contraction).
 double fp32_peak_probe(cudaStream_t st);
 

@@ -366,8 +366,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a) {
   if (threadIdx.x < 2 && s_counts[threadIdx.x]) atomicAdd(a.state_counts + threadIdx.x, s_counts[threadIdx.x]);
 }
 
-// K4b: per Gaussian, after the blend backward wrote per-intersection partials (9 floats) at
-// their emission slots [offset[rank[g]], +touched[g]) in ascending tile order.
+// K4b: per Gaussian, after K4a/K4c left one 9-float partial per intersection at the
+// Gaussian's emission slots [offset[rank[g]], +touched[g]) (ascending tile order; within a
+// tile the 8 pixel blocks were added in fixed order): deterministic, no atomics.
 __global__ void __launch_bounds__(128) preprocess_backward_kernel(PreprocessBackwardArgs a) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= a.n) return;

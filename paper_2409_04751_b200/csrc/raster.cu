@@ -25,74 +25,8 @@ namespace fgs {
 namespace {
 
 constexpr int kBlend = 256;     // threads per tile CTA = pixels per tile
-constexpr int kBwdBatch = 128;  // splats per backward batch
 constexpr int kWarps = kBlend / 32;
 constexpr int kGroup = 4;         // forward: splats whose alphas are computed together
-
-// Warp w of a tile owns the 8x4 pixel block at (8*(w&1), 4*(w>>1)); lane l the pixel
-// (l&7, l>>3) inside it. Square-ish blocks make the per-warp culling below tight.
-__device__ __forceinline__ void pixel_of(int tid, int& lx, int& ly) {
-  const int w = tid >> 5, l = tid & 31;
-  lx = ((w & 1) << 3) + (l & 7);
-  ly = ((w >> 1) << 2) + (l >> 3);
-}
-
-// Conservative per-warp visibility of one splat: bit w is set unless no pixel centre of warp
-// w's 8x4 block can reach alpha >= 1/255. alpha(d) = alpha_max * exp(-q(d)/2) with
-// q = a dx^2 + 2b dx dy + c dy^2, so alpha >= 1/255 needs q <= 2 ln(255 alpha_max), whose
-// bounding box has half-extents sqrt(2 tau Sigma_xx), sqrt(2 tau Sigma_yy) (Sigma = Q^-1).
-// The box is inflated (0.1% + 1e-3 px) far beyond fp32 rounding of the blend's power, so a
-// culled (pixel, splat) pair is exactly one the reference would `continue` on: the image and
-// every decision are unchanged; only evaluations that cannot contribute are skipped.
-__device__ __forceinline__ uint32_t warp_mask(float4 r0, float4 r1, float tile_x0, float tile_y0) {
-  const float a = r0.z, b = r0.w, c = r1.x, amax = r1.y;
-  if (!(amax >= kAlphaSkip)) return 0u;
-  const float det = a * c - b * b;
-  if (!(det > 0.0f) || !(a > 0.0f) || !(c > 0.0f)) return 0xFFu;
-  const float tau2 = 2.0f * __logf(255.0f * amax) * 1.002f + 1e-3f;
-  const float ex = sqrtf(fmaxf(tau2 * c / det, 0.0f)) * 1.001f + 1e-3f;
-  const float ey = sqrtf(fmaxf(tau2 * a / det, 0.0f)) * 1.001f + 1e-3f;
-  // box in tile-local pixel-centre coordinates
-  const float x0 = r0.x - ex - tile_x0, x1 = r0.x + ex - tile_x0;
-  const float y0 = r0.y - ey - tile_y0, y1 = r0.y + ey - tile_y0;
-  uint32_t m = 0;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    const float bx0 = ((w & 1) << 3) + 0.5f, bx1 = bx0 + 7.0f;
-    const float by0 = ((w >> 1) << 2) + 0.5f, by1 = by0 + 3.0f;
-    if (x1 >= bx0 && x0 <= bx1 && y1 >= by0 && y0 <= by1) m |= 1u << w;
-  }
-  return m;
-}
-
-// Each warp compacts the batch indices whose mask has its bit into s_list[warp][...].
-__device__ __forceinline__ int build_list(const uint8_t* s_mask, int cnt, int warp, int lane, uint8_t* list) {
-  int n = 0;
-  for (int c0 = 0; c0 < cnt; c0 += 32) {
-    const int j = c0 + lane;
-    const bool on = j < cnt && ((s_mask[j] >> warp) & 1u);
-    const uint32_t bal = __ballot_sync(0xffffffffu, on);
-    if (on) list[n + __popc(bal & ((1u << lane) - 1u))] = static_cast<uint8_t>(j);
-    n += __popc(bal);
-  }
-  __syncwarp();
-  return n;
-}
-
-// Conservative test: can any pixel centre of the box [x0, x1] x [y0, y1] reach
-// alpha >= 1/255 for this splat? Same bound as warp_mask, evaluated with fast-math
-// (relative error ~1e-6, far inside the 0.1-0.2% margins).
-__device__ __forceinline__ bool box_may_hit(float4 r0, float4 r1, float x0, float x1, float y0, float y1) {
-  const float a = r0.z, b = r0.w, c = r1.x, amax = r1.y;
-  if (!(amax >= kAlphaSkip)) return false;
-  const float det = a * c - b * b;
-  if (!(det > 0.0f) || !(a > 0.0f) || !(c > 0.0f)) return true;
-  const float tau2 = 2.0f * __logf(255.0f * amax) * 1.002f + 1e-3f;
-  const float k = __fdividef(tau2, det);
-  const float ex = __fsqrt_rn(fmaxf(k * c, 0.0f)) * 1.001f + 1e-3f;
-  const float ey = __fsqrt_rn(fmaxf(k * a, 0.0f)) * 1.001f + 1e-3f;
-  return r0.x + ex >= x0 && r0.x - ex <= x1 && r0.y + ey >= y0 && r0.y - ey <= y1;
-}
 
 struct PixelState {
   float T, C0, C1, C2;
@@ -289,29 +223,28 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// K4a backward blend (inc/gradients.hpp:69-175), barrier-free like the forward: 8 warps per
+// tile, warp w owns the 8x4 block of bwd_block_box, one pixel per lane. Each warp walks the
+// tile's list backwards from its last contributor (the max of its pixels' `last`) in 32-splat
+// chunks, culls them against its block (box_may_hit), and for each surviving splat recovers
+// T_before = T_after / (1 - alpha), accumulates the suffix colour and forms the 9 per-pixel
+// gradients (mean_px 2, conic 3, colour 3, alpha_max 1), summed over the warp's 32 pixels by
+// a shuffle tree. The warp sum goes to partials[emit][w] -- one slot per (intersection, block)
+// whose block passes the cull, zeros for passing splats past the warp's last contributor --
+// and K4b adds the passing slots in fixed (tile, block) order: deterministic, no atomics.
 __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
-  __shared__ float4 s0[kBwdBatch];
-  __shared__ float4 s1[kBwdBatch];
-  __shared__ float s2[kBwdBatch];
-  __shared__ uint32_t s_emit[kBwdBatch];
-  __shared__ uint8_t s_mask[kBwdBatch];
-  __shared__ uint8_t s_list[kWarps][kBwdBatch];
-  __shared__ float s_part[kWarps][kBwdBatch][9];
-  __shared__ uint32_t s_max_last;
-  __shared__ uint32_t s_wl[kWarps];
-
-  const int tile = blockIdx.x;
+  __shared__ float4 s0[kBwdWarps][32];
+  __shared__ float4 s1[kBwdWarps][32];
+  __shared__ float s2[kBwdWarps][32];
+  __shared__ uint32_t se[kBwdWarps][32];
+  const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int lx, ly;
-  pixel_of(threadIdx.x, lx, ly);
-  const int px = tx * kTile + lx, py = ty * kTile + ly;
+  float bx0, bx1, by0, by1;
+  bwd_block_box(tx, ty, warp, bx0, bx1, by0, by1);
+  const int px = static_cast<int>(bx0) + (lane & 7), py = static_cast<int>(by0) + (lane >> 3);
   const bool inside = px < a.width && py < a.height;
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
-  const float tile_x0 = static_cast<float>(tx * kTile), tile_y0 = static_cast<float>(ty * kTile);
-  if (threadIdx.x == 0) s_max_last = lo;
-  __syncthreads();
-
   const float fx = static_cast<float>(px) + 0.5f, fy = static_cast<float>(py) + 0.5f;
   float T = 1.0f, dl0 = 0.0f, dl1 = 0.0f, dl2 = 0.0f;
   uint32_t last = lo;
@@ -323,51 +256,48 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     dl1 = a.dl_dimage[pix * 3 + 1];
     dl2 = a.dl_dimage[pix * 3 + 2];
   }
-  const uint32_t warp_last = __reduce_max_sync(0xffffffffu, last);
-  if (lane == 0) {
-    atomicMax(&s_max_last, warp_last);
-    s_wl[warp] = warp_last;
-  }
+  const uint32_t wlast = __reduce_max_sync(0xffffffffu, last);
   float sf0 = T * a.bg[0], sf1 = T * a.bg[1], sf2 = T * a.bg[2];
-  __syncthreads();
-  const uint32_t end = s_max_last;
+  float* part = a.partials;
 
-  // Entries past every pixel's last contributor get zero partials.
-  for (uint32_t k = end + threadIdx.x; k < hi; k += kBlend) {
-    float* p = a.partials + static_cast<size_t>(a.sorted_emit[k]) * 9;
+  // passing splats past the warp's last contributor: zero slots
+  for (uint32_t base = wlast; base < hi; base += 32) {
+    const uint32_t k = base + lane;
+    if (k < hi) {
+      const SortedRec r = a.srec[k];
+      if (box_may_hit(r.a, r.b, bx0, bx1, by0, by1)) {
+        float* p = part + (static_cast<size_t>(a.sorted_emit[k]) * kBwdWarps + warp) * 9;
 #pragma unroll
-    for (int q = 0; q < 9; ++q) p[q] = 0.0f;
-  }
-
-  for (int64_t bend = end; bend > static_cast<int64_t>(lo); bend -= kBwdBatch) {
-    const uint32_t bstart = static_cast<uint32_t>(max(static_cast<int64_t>(lo), bend - kBwdBatch));
-    const int cnt = static_cast<int>(bend - bstart);
-    __syncthreads();
-    if (threadIdx.x < cnt) {
-      const uint32_t k = bstart + threadIdx.x;
-      const SortedRec rr = a.srec[k];
-      const float4 r0 = rr.a;
-      const float4 r1 = rr.b;
-      s0[threadIdx.x] = r0;
-      s1[threadIdx.x] = r1;
-      s2[threadIdx.x] = rr.c.x;
-      s_emit[threadIdx.x] = __ldg(a.sorted_emit + k);
-      s_mask[threadIdx.x] = static_cast<uint8_t>(warp_mask(r0, r1, tile_x0, tile_y0));
+        for (int q = 0; q < 9; ++q) p[q] = 0.0f;
+      }
     }
-    __syncthreads();
-    // a warp whose pixels all stopped before an entry cannot take a gradient from it
-    const int wcnt = static_cast<int>(min(static_cast<int64_t>(cnt), static_cast<int64_t>(warp_last) - bstart));
-    const int nl = wcnt > 0 ? build_list(s_mask, wcnt, warp, lane, s_list[warp]) : 0;
-    for (int i = nl - 1; i >= 0; --i) {
-      const int j = s_list[warp][i];
-      const uint32_t k = bstart + j;
+  }
+  // reverse walk over [lo, wlast)
+  for (int64_t end = wlast; end > static_cast<int64_t>(lo); end -= 32) {
+    const uint32_t cstart = static_cast<uint32_t>(max(static_cast<int64_t>(lo), end - 32));
+    const uint32_t k = cstart + lane;
+    bool pass = false;
+    if (k < end) {
+      const SortedRec r = a.srec[k];
+      pass = box_may_hit(r.a, r.b, bx0, bx1, by0, by1);
+      s0[warp][lane] = r.a;
+      s1[warp][lane] = r.b;
+      s2[warp][lane] = r.c.x;
+      se[warp][lane] = a.sorted_emit[k];
+    }
+    uint32_t mask = __ballot_sync(0xffffffffu, pass);
+    __syncwarp();
+    while (mask) {
+      const int j = 31 - __clz(mask);
+      mask &= ~(1u << j);
+      const uint32_t kk = cstart + j;
       float g[9];
 #pragma unroll
       for (int q = 0; q < 9; ++q) g[q] = 0.0f;
       bool contrib = false;
-      if (k < last) {
-        const float4 r0 = s0[j];
-        const float4 r1 = s1[j];
+      if (kk < last) {
+        const float4 r0 = s0[warp][j];
+        const float4 r1 = s1[warp][j];
         const float dx = __fsub_rn(fx, r0.x);
         const float dy = __fsub_rn(fy, r0.y);
         const float power = blend_power(r0.z, r0.w, r1.x, dx, dy);
@@ -380,7 +310,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
             const float one_m = 1.0f - alpha;
             const float Tb = T / one_m;
             const float w = alpha * Tb;
-            const float b2 = s2[j];
+            const float b2 = s2[warp][j];
             g[5] = dl0 * w;
             g[6] = dl1 * w;
             g[7] = dl2 * w;
@@ -407,30 +337,58 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
 #pragma unroll
         for (int q = 0; q < 9; ++q) g[q] = warp_sum(g[q]);
       }
-      if (lane == 0) {
+      if (lane < 9) {
+        float v = g[0];
 #pragma unroll
-        for (int q = 0; q < 9; ++q) s_part[warp][j][q] = g[q];
+        for (int q = 1; q < 9; ++q) v = lane == q ? g[q] : v;
+        part[(static_cast<size_t>(se[warp][j]) * kBwdWarps + warp) * 9 + lane] = v;
       }
     }
-    __syncthreads();
-    // Fixed-order reduction over the warps that listed the entry; one writer per entry.
-    for (int idx = threadIdx.x; idx < cnt * 9; idx += kBlend) {
-      const int j = idx / 9, q = idx - j * 9;
-      const uint32_t m = s_mask[j];
-      const int64_t kk = static_cast<int64_t>(bstart) + j;
-      float s = 0.0f;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        // listed by warp w iff its mask bit is set and the entry is below warp w's last
-        const bool listed = ((m >> w) & 1u) && kk < static_cast<int64_t>(s_wl[w]);
-        if (listed) s += s_part[w][j][q];
-      }
-      a.partials[static_cast<size_t>(s_emit[j]) * 9 + q] = s;
-    }
+    __syncwarp();
   }
 }
 
+// K4c: for every intersection (emission slot e), add the per-block partials of the blocks
+// that passed the backward's culling test, in block order: partial_tile[e] (9 floats).
+__global__ void __launch_bounds__(256) combine_partials_kernel(const uint32_t* __restrict__ tile_keys,
+                                                               const uint32_t* __restrict__ emit_gauss,
+                                                               const float4* __restrict__ rec0,
+                                                               const float4* __restrict__ rec1,
+                                                               const float* __restrict__ partials,
+                                                               float* __restrict__ partial_tile, int tiles_x, int ni) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ni) return;
+  const uint32_t t = __ldg(tile_keys + e), g = __ldg(emit_gauss + e);
+  const int tx = static_cast<int>(t) % tiles_x, ty = static_cast<int>(t) / tiles_x;
+  const float4 r0 = __ldg(rec0 + g), r1 = __ldg(rec1 + g);
+  float ex, ey;
+  const int kind = splat_extent(r0, r1, ex, ey);
+  float sg[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
+  const float* p = partials + static_cast<size_t>(e) * (kBwdWarps * 9);
+#pragma unroll
+  for (int w = 0; w < kBwdWarps; ++w) {
+    float x0, x1, y0, y1;
+    bwd_block_box(tx, ty, w, x0, x1, y0, y1);
+    if (!extent_hits(kind, r0.x, r0.y, ex, ey, x0, x1, y0, y1)) continue;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) sg[k] = sg[k] + p[w * 9 + k];
+  }
+  float* o = partial_tile + static_cast<size_t>(e) * 9;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) o[k] = sg[k];
+}
+
 }  // namespace
+
+int combine_partials(const uint32_t* tile_keys, const uint32_t* emit_gauss, const float4* rec0, const float4* rec1,
+                     const float* partials, float* partial_tile, int tiles_x, int ni, cudaStream_t st) {
+  if (ni <= 0) return 0;
+  combine_partials_kernel<<<div_up(ni, 256), 256, 0, st>>>(tile_keys, emit_gauss, rec0, rec1, partials,
+                                                            partial_tile, tiles_x, ni);
+  return 1;
+}
 
 int blend_forward(const BlendArgs& a, cudaStream_t st) {
   const int px = a.px_per_lane == 2 ? 2 : 1;
