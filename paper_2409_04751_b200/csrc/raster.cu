@@ -287,62 +287,85 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     }
     uint32_t mask = __ballot_sync(0xffffffffu, pass);
     __syncwarp();
+    // Groups of 3 surviving splats, latest first. Their alphas are independent of the
+    // transmittance and are computed together; the transmittance/suffix recurrence then runs
+    // in list order, leaving 3 x 9 per-lane gradients, which one butterfly reduce-scatter over
+    // the warp sums (31 shuffles instead of 3 x 45); lane l ends with value l.
     while (mask) {
-      const int j = 31 - __clz(mask);
-      mask &= ~(1u << j);
-      const uint32_t kk = cstart + j;
-      float g[9];
+      int js[3];
 #pragma unroll
-      for (int q = 0; q < 9; ++q) g[q] = 0.0f;
-      bool contrib = false;
-      if (kk < last) {
-        const float4 r0 = s0[warp][j];
-        const float4 r1 = s1[warp][j];
-        const float dx = __fsub_rn(fx, r0.x);
-        const float dy = __fsub_rn(fy, r0.y);
-        const float power = blend_power(r0.z, r0.w, r1.x, dx, dy);
-        if (power <= 0.0f && power >= kPowerFloor) {
-          float e;
-          const float ar = alpha_raw(r1.y, power, &e);
-          const float alpha = fminf(kAlphaClamp, ar);
-          if (alpha >= kAlphaSkip) {
-            contrib = true;
-            const float one_m = 1.0f - alpha;
-            const float Tb = T / one_m;
-            const float w = alpha * Tb;
-            const float b2 = s2[warp][j];
-            g[5] = dl0 * w;
-            g[6] = dl1 * w;
-            g[7] = dl2 * w;
-            const float dot_c = dl0 * r1.z + dl1 * r1.w + dl2 * b2;
-            const float dot_s = dl0 * sf0 + dl1 * sf1 + dl2 * sf2;
-            const float d_alpha = dot_c * Tb - dot_s / one_m;
-            sf0 = fmaf(r1.z, w, sf0);
-            sf1 = fmaf(r1.w, w, sf1);
-            sf2 = fmaf(b2, w, sf2);
-            T = Tb;
-            if (!(ar > kAlphaClamp)) {  // clamped contributions carry no geometric gradient
-              g[8] = d_alpha * e;
-              const float dp = d_alpha * alpha;
-              g[0] = dp * (r0.z * dx + r0.w * dy);
-              g[1] = dp * (r0.w * dx + r1.x * dy);
-              g[2] = dp * (-0.5f * dx * dx);
-              g[3] = dp * (-dx * dy);
-              g[4] = dp * (-0.5f * dy * dy);
-            }
+      for (int q = 0; q < 3; ++q) {
+        js[q] = mask ? 31 - __clz(mask) : -1;
+        if (mask) mask &= ~(1u << js[q]);
+      }
+      float pw[3], ex[3], ar[3], dxs[3], dys[3];
+      float4 r0s[3], r1s[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int jj = js[q] >= 0 ? js[q] : 0;
+        r0s[q] = s0[warp][jj];
+        r1s[q] = s1[warp][jj];
+        dxs[q] = __fsub_rn(fx, r0s[q].x);
+        dys[q] = __fsub_rn(fy, r0s[q].y);
+        pw[q] = blend_power(r0s[q].z, r0s[q].w, r1s[q].x, dxs[q], dys[q]);
+        ar[q] = alpha_raw(r1s[q].y, pw[q], &ex[q]);
+      }
+      float v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) v[q] = 0.0f;
+      bool contrib_any = false;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        if (js[q] < 0) break;
+        const uint32_t kk = cstart + js[q];
+        const float alpha = fminf(kAlphaClamp, ar[q]);
+        if (kk < last && pw[q] <= 0.0f && pw[q] >= kPowerFloor && alpha >= kAlphaSkip) {
+          contrib_any = true;
+          const float4 r0 = r0s[q], r1 = r1s[q];
+          const float dx = dxs[q], dy = dys[q];
+          const float one_m = 1.0f - alpha;
+          const float Tb = T / one_m;
+          const float w = alpha * Tb;
+          const float b2 = s2[warp][js[q]];
+          v[9 * q + 5] = dl0 * w;
+          v[9 * q + 6] = dl1 * w;
+          v[9 * q + 7] = dl2 * w;
+          const float dot_c = dl0 * r1.z + dl1 * r1.w + dl2 * b2;
+          const float dot_s = dl0 * sf0 + dl1 * sf1 + dl2 * sf2;
+          const float d_alpha = dot_c * Tb - dot_s / one_m;
+          sf0 = fmaf(r1.z, w, sf0);
+          sf1 = fmaf(r1.w, w, sf1);
+          sf2 = fmaf(b2, w, sf2);
+          T = Tb;
+          if (!(ar[q] > kAlphaClamp)) {  // clamped contributions carry no geometric gradient
+            v[9 * q + 8] = d_alpha * ex[q];
+            const float dp = d_alpha * alpha;
+            v[9 * q + 0] = dp * (r0.z * dx + r0.w * dy);
+            v[9 * q + 1] = dp * (r0.w * dx + r1.x * dy);
+            v[9 * q + 2] = dp * (-0.5f * dx * dx);
+            v[9 * q + 3] = dp * (-dx * dy);
+            v[9 * q + 4] = dp * (-0.5f * dy * dy);
           }
         }
       }
-      if (__any_sync(0xffffffffu, contrib)) {
+      if (__any_sync(0xffffffffu, contrib_any)) {
 #pragma unroll
-        for (int q = 0; q < 9; ++q) g[q] = warp_sum(g[q]);
-      }
-      if (lane < 9) {
-        float v = g[0];
+        for (int half = 16; half >= 1; half >>= 1) {
+          const bool up = (lane & half) != 0;
 #pragma unroll
-        for (int q = 1; q < 9; ++q) v = lane == q ? g[q] : v;
-        part[(static_cast<size_t>(se[warp][j]) * kBwdWarps + warp) * 9 + lane] = v;
+          for (int i = 0; i < half; ++i) {
+            const float send = up ? v[i] : v[i + half];
+            const float keep = up ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+          }
+        }
+      } else {
+        v[0] = 0.0f;
       }
+      // lane l now holds component l % 9 of splat l / 9 (l < 27)
+      const int q = lane / 9;
+      if (lane < 27 && js[q] >= 0)
+        part[(static_cast<size_t>(se[warp][js[q]]) * kBwdWarps + warp) * 9 + (lane - 9 * q)] = v[0];
     }
     __syncwarp();
   }
