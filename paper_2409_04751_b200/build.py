@@ -12,6 +12,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfgs.so")
 OBJ = os.path.join(HERE, "_obj")
+ROOT = os.path.dirname(HERE)
+EXAMPLE_SRC = os.path.join(ROOT, "tools", "fgs_render_example.cpp")
+EXAMPLE_BIN = os.path.join(ROOT, "tools", "fgs_render_example")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]
@@ -49,7 +52,20 @@ def build(verbose=False, force=False) -> str:
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
+    build_example(verbose)
     return OUT
+
+
+def build_example(verbose=False):
+    """C++ host example over include/fgs.hpp, linked against libfgs.so (rpath $ORIGIN/..)."""
+    if not os.path.exists(EXAMPLE_SRC):
+        return None
+    cmd = ["g++", "-O2", "-std=c++17", "-o", EXAMPLE_BIN, EXAMPLE_SRC, "-L" + HERE, "-lfgs",
+           "-Wl,-rpath,$ORIGIN/../paper_2409_04751_b200"]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return EXAMPLE_BIN
 
 
 if __name__ == "__main__":

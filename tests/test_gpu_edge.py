@@ -180,3 +180,23 @@ def test_counters_match_oracle(rast, oracle_mod):
     assert int(ec) == int(st["e_contrib"])
     assert int(ev) == int(st["e_eval"])
     assert 0 < int(warp_iters) <= 2 * int(ev)  # pixel evaluations actually done after culling
+
+
+def test_cpp_wrapper_example():
+    """The C++ host side over the C ABI (include/fgs.hpp) renders, back-propagates and maps the
+    reference's std::invalid_argument behaviour."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tools", "fgs_render_example")
+    if not os.path.exists(exe):
+        from paper_2409_04751_b200.build import build_example
+
+        build_example()
+    out = subprocess.run([exe, "20000", "512", "384"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    kv = dict(tok.split("=") for tok in out.stdout.split() if "=" in tok)
+    assert int(kv["intersections"]) > 0 and int(kv["splats"]) > 0
+    assert float(kv["image_mean"]) > 0 and float(kv["grad_mean_l1"]) > 0
+    assert kv["error_check"] == "ok"
