@@ -58,6 +58,15 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// Debug phase trace (FGS_FLAG_COUNTERS): CTA 0 records %globaltimer at phase boundaries.
+__device__ __forceinline__ void trace(unsigned long long* t, int slot) {
+  if (t && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    t[slot] = v;
+  }
+}
+
 __device__ __forceinline__ void chunk_of(int m, int& lo, int& hi) {
   lo = static_cast<int>(static_cast<int64_t>(m) * blockIdx.x / gridDim.x);
   hi = static_cast<int>(static_cast<int64_t>(m) * (blockIdx.x + 1) / gridDim.x);
@@ -110,7 +119,8 @@ __device__ __forceinline__ void cta_prefix(const uint32_t* part, uint32_t* s_war
 // One stable LSD radix pass of (kin, vin)[0, m) into (kout, vout) on digit (key >> shift) & 255.
 __device__ void radix_pass(cg::grid_group& grid, BinSmem& sm, const uint32_t* __restrict__ kin,
                            const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
-                           uint32_t* __restrict__ vout, int m, int shift, uint32_t* __restrict__ part) {
+                           uint32_t* __restrict__ vout, int m, int shift, uint32_t* __restrict__ part,
+                           unsigned long long* tr = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int lo, hi;
   chunk_of(m, lo, hi);
@@ -120,7 +130,9 @@ __device__ void radix_pass(cg::grid_group& grid, BinSmem& sm, const uint32_t* __
   for (int i = lo + tid; i < hi; i += kT) atomicAdd(&sm.hist[(kin[i] >> shift) & 255u], 1u);
   __syncthreads();
   if (tid < 256) part[blockIdx.x * 256 + tid] = sm.hist[tid];
+  trace(tr, 0);
   grid.sync();
+  trace(tr, 1);
   // 2. per digit, exclusive scan over CTAs: digit d is owned by CTA d mod grid, whose threads
   //    (one per CTA c) load part[c][d] in one parallel burst, scan it in place and publish the
   //    digit total. Then every CTA reads its own 256 offsets + the 256 totals (coalesced).
@@ -132,7 +144,9 @@ __device__ void radix_pass(cg::grid_group& grid, BinSmem& sm, const uint32_t* __
     if (tid < static_cast<int>(gridDim.x)) part[tid * 256 + d] = ex;
     if (tid == 0) totals[d] = t;
   }
+  trace(tr, 2);
   grid.sync();
+  trace(tr, 3);
   const uint32_t tot = tid < 256 ? totals[tid] : 0u;
   const uint32_t pre = tid < 256 ? part[blockIdx.x * 256 + tid] : 0u;
   const uint32_t dstart = block_exclusive_scan(tot, sm.warp_tmp, nullptr);
@@ -208,7 +222,9 @@ __device__ void radix_pass(cg::grid_group& grid, BinSmem& sm, const uint32_t* __
     if (tid < 256) sm.run[tid] += total;
     __syncthreads();
   }
+  trace(tr, 4);
   grid.sync();
+  trace(tr, 5);
 }
 
 __global__ void __launch_bounds__(kT, 1) bin_level1_kernel(BinArgs a) {
@@ -219,6 +235,7 @@ __global__ void __launch_bounds__(kT, 1) bin_level1_kernel(BinArgs a) {
   const int n = a.n;
   int lo, hi;
 
+  trace(a.trace, 0);
   // ---- compaction of Gaussians touching >= 1 tile (source order) ----
   chunk_of(n, lo, hi);
   {
@@ -258,12 +275,17 @@ __global__ void __launch_bounds__(kT, 1) bin_level1_kernel(BinArgs a) {
   }
   grid.sync();
   const int m = static_cast<int>(sm.scalar[0]);
+  trace(a.trace, 1);
 
   // ---- level 1: stable sort by depth key (4 x 8-bit digits): in -> a -> b -> a -> b ----
   radix_pass(grid, sm, a.ckey, a.cval, a.key_a, a.val_a, m, 0, a.part_radix);
-  radix_pass(grid, sm, a.key_a, a.val_a, a.key_b, a.val_b, m, 8, a.part_radix);
+  trace(a.trace, 2);
+  radix_pass(grid, sm, a.key_a, a.val_a, a.key_b, a.val_b, m, 8, a.part_radix, a.trace ? a.trace + 16 : nullptr);
+  trace(a.trace, 3);
   radix_pass(grid, sm, a.key_b, a.val_b, a.key_a, a.val_a, m, 16, a.part_radix);
+  trace(a.trace, 4);
   radix_pass(grid, sm, a.key_a, a.val_a, a.key_b, a.val_b, m, 24, a.part_radix);
+  trace(a.trace, 5);
   const uint32_t* perm = a.val_b;
 
   // ---- exclusive scan of tile counts in depth order: offsets[r], rank[perm[r]] = r, I ----
@@ -280,6 +302,7 @@ __global__ void __launch_bounds__(kT, 1) bin_level1_kernel(BinArgs a) {
     uint32_t prefix, total;
     cta_prefix(a.part_scan, sm.warp_tmp, prefix, total);
     if (blockIdx.x == 0 && tid == 0) a.scalars[kScalarI] = total;
+    trace(a.trace, 6);
     uint32_t run = prefix;
     for (int sb = lo; sb < hi; sb += kT * kItems) {
       const int r0 = sb + tid * kItems;
@@ -315,6 +338,7 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
   const uint32_t* perm = a.val_b;
   int lo, hi;
 
+  trace(a.trace, 8);
   // ---- duplication in depth-rank order (tiles ascending within a Gaussian) ----
   chunk_of(m, lo, hi);
   for (int r = lo + tid; r < hi; r += kT) {
@@ -330,6 +354,7 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
       }
   }
   grid.sync();
+  trace(a.trace, 9);
 
   // ---- level 2: stable sort by tile id ----
   const uint32_t *sk = a.tkey, *sv = a.emit;
@@ -344,6 +369,7 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
     sv = a.emit_b;
   }
 
+  trace(a.trace, 10);
   // ---- per-tile ranges, sorted Gaussian list ----
   chunk_of(I, lo, hi);
   for (int k = lo + tid; k < hi; k += kT) {
@@ -362,8 +388,10 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
     r.c = make_float4(__ldg(a.rec2 + g), 0.0f, 0.0f, 0.0f);
     a.sorted_rec[k] = r;
   }
+  trace(a.trace, 11);
   if (a.tile_order == nullptr) return;
   grid.sync();
+  trace(a.trace, 12);
   // ---- blend schedule: tiles by descending list length (log2 buckets), empty tiles last ----
   if (blockIdx.x != 0) return;
   constexpr int kB = 18;
@@ -389,6 +417,8 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
     const int b = c == 0 ? kB - 1 : 16 - min(16, 31 - __clz(c));
     a.tile_order[atomicAdd(&sm.run[b], 1u)] = static_cast<uint32_t>(t);
   }
+  __syncthreads();
+  trace(a.trace, 13);
 }
 
 // Debug export: the reference's pre-sort key list (source order, ty-major, tx-minor).

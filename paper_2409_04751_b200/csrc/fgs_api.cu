@@ -68,7 +68,7 @@ struct fgs_context {
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
   DevBuf<uint32_t> scalars;
-  DevBuf<unsigned long long> counters, tile_cycles;
+  DevBuf<unsigned long long> counters, tile_cycles, bin_trace;
   uint32_t* h_scalars = nullptr;  // pinned
   // host-call staging
   DevBuf<float> h_means, h_rot, h_ls, h_op, h_sh, h_img, h_dl, h_grad;
@@ -231,6 +231,7 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->h_radii.release();
   ctx->counters.release();
   ctx->tile_cycles.release();
+  ctx->bin_trace.release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   for (auto* v : {&ctx->pending, &ctx->spare})
@@ -371,6 +372,11 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.part_scan = ctx->scan_status.p;
   bn.part_radix = ctx->scan_status.p + 256;
   ctx->perm = ctx->perm_b.p;
+  if (ctx->flags & FGS_FLAG_COUNTERS) {
+    FGS_CHECK(ctx->bin_trace.ensure(32));
+    FGS_CHECK(cudaMemsetAsync(ctx->bin_trace.p, 0, 32 * sizeof(unsigned long long), st));
+    bn.trace = ctx->bin_trace.p;
+  }
   if (n > 0) {
     FGS_CHECK(fgs::bin_level1(bn, st));
     ++launches;
@@ -675,6 +681,7 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   if (nm == "last") return copy(ctx->last.p, npix * 4);
   if (nm == "counters") return copy(ctx->counters.p, 4 * sizeof(unsigned long long));
   if (nm == "tile_cycles") return copy(ctx->tile_cycles.p, nt * sizeof(unsigned long long));
+  if (nm == "bin_trace") return copy(ctx->bin_trace.p, 32 * sizeof(unsigned long long));
   if (nm == "key_tile" || nm == "key_depth" || nm == "key_gauss") {
     if (!dst) return static_cast<int64_t>(I * 4);
     // Recompute the reference's pre-sort emission order (source order) on demand.

@@ -115,6 +115,7 @@ struct BinArgs {
   const float* rec2;
   SortedRec* sorted_rec;       // [I] records in sorted order
   uint32_t* tile_order;        // [num_tiles] blend schedule (optional)
+  unsigned long long* trace;   // debug phase timestamps (optional)
 };
 
 // Words of part_scan + part_radix scratch the persistent kernels need.

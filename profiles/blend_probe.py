@@ -34,5 +34,32 @@ def main(cfg=2, reps=20):
     print("STAGES_US", {k: round(1000 * v / reps, 1) for k, v in t["ms"].items()})
 
 
+
+
+def bin_trace(cfg=2):
+    import torch
+
+    from paper_2409_04751_b200 import Rasterizer, RenderOptions, _lib, synthetic
+    from tests._helpers import to_device
+
+    sc, deg, cams, _ = synthetic.config(cfg)
+    ds = to_device(sc)
+    r = Rasterizer(0)
+    r.set_flags(_lib.FGS_FLAG_COUNTERS)
+    for _ in range(3):
+        r.forward(ds, cams[0], RenderOptions(sh_degree=deg))
+    torch.cuda.synchronize()
+    t = r.debug("bin_trace", np.uint64).astype(np.int64)
+    names = ["compact", "pass0", "pass1", "pass2", "pass3", "rankscan"]
+    l1 = [(names[i], (t[i + 1] - t[i]) / 1000.0) for i in range(6)]
+    l2n = ["duplicate", "tilesort", "ranges+gather", "sync", "order"]
+    l2 = [(l2n[i], (t[9 + i] - t[8 + i]) / 1000.0) for i in range(5)]
+    print("BIN_TRACE_US level1", l1, "level2", l2)
+    p = t[16:22]
+    print("PASS1_US", [("hist", (p[0] - t[2]) / 1e3), ("sync1", (p[1] - p[0]) / 1e3), ("colscan", (p[2] - p[1]) / 1e3),
+                       ("sync2", (p[3] - p[2]) / 1e3), ("rank+scatter", (p[4] - p[3]) / 1e3), ("sync3", (p[5] - p[4]) / 1e3)])
+
+
 if __name__ == "__main__":
     main(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
+    bin_trace(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
