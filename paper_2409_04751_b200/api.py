@@ -226,9 +226,8 @@ class Rasterizer:
     def splats(self) -> dict:
         """Per-Gaussian preprocess outputs of the last forward (reference Splat2D fields)."""
         state = self.debug("state_u8", np.uint8).astype(np.int32)
-        r0 = self.debug("rec0", np.float32).reshape(-1, 4)
-        r1 = self.debug("rec1", np.float32).reshape(-1, 4)
-        r2 = self.debug("rec2", np.float32)
+        rec = self.debug("rec", np.float32).reshape(-1, 12)
+        r0, r1, r2 = rec[:, 0:4], rec[:, 4:8], rec[:, 8].copy()
         dk = self.debug("depth_key", np.uint32)
         return {
             "state": state,

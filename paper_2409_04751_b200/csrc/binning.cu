@@ -328,6 +328,44 @@ __global__ void __launch_bounds__(kT, 1) bin_level1_kernel(BinArgs a) {
   }
 }
 
+// Largest rank r in [0, m) with offsets[r] <= v (offsets ascending, offsets[0] = 0):
+// two rounds of a 1024-ary search by the whole CTA.
+__device__ int cta_upper_rank(const uint32_t* offsets, int m, uint32_t v, BinSmem& sm) {
+  const int tid = threadIdx.x;
+  if (tid == 0) sm.scalar[1] = 0;
+  __syncthreads();
+  // round 1: sample every step-th rank
+  const int step = max(1, (m + kT - 1) / kT);
+  {
+    const int r = tid * step;
+    if (r < m && offsets[r] <= v) atomicMax(&sm.scalar[1], static_cast<uint32_t>(r));
+  }
+  __syncthreads();
+  const int base = static_cast<int>(sm.scalar[1]);
+  __syncthreads();
+  // round 2: scan [base, base + step) (step <= kT * ceil); loop for huge m
+  for (int r = base + tid; r < min(m, base + step); r += kT)
+    if (offsets[r] <= v) atomicMax(&sm.scalar[1], static_cast<uint32_t>(r));
+  __syncthreads();
+  const int res = static_cast<int>(sm.scalar[1]);
+  __syncthreads();
+  return res;
+}
+
+// Emit slots [e_b, e_e) of Gaussian g (slot off is its first tile; tiles ty-major, tx-minor),
+// lanes lane0, lane0 + stride, ...
+__device__ __forceinline__ void emit_slots(const BinArgs& a, uint32_t g, ushort4 rc, uint32_t off, uint32_t e_b,
+                                           uint32_t e_e, int lane0, int stride) {
+  const int wx = rc.y - rc.x + 1;
+  for (uint32_t e = e_b + lane0; e < e_e; e += stride) {
+    const int j = static_cast<int>(e - off);
+    const int ty = rc.z + j / wx, tx = rc.x + j % wx;
+    a.tkey[e] = static_cast<uint32_t>(ty * a.tiles_x + tx);
+    a.emit[e] = e;
+    a.emit_gauss[e] = g;
+  }
+}
+
 __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BinSmem& sm = *reinterpret_cast<BinSmem*>(smem_raw);
@@ -340,18 +378,45 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
 
   trace(a.trace, 8);
   // ---- duplication in depth-rank order (tiles ascending within a Gaussian) ----
-  chunk_of(m, lo, hi);
-  for (int r = lo + tid; r < hi; r += kT) {
-    const uint32_t g = perm[r];
-    const ushort4 b = a.rect[g];
-    uint32_t e = a.offsets[r];
-    for (int ty = b.z; ty <= b.w; ++ty)
-      for (int tx = b.x; tx <= b.y; ++tx) {
-        a.tkey[e] = static_cast<uint32_t>(ty * a.tiles_x + tx);
-        a.emit[e] = e;
-        a.emit_gauss[e] = g;
-        ++e;
+  // Balanced by intersections: CTA c emits slots [I*c/G, I*(c+1)/G). Its rank range comes
+  // from two 1024-ary searches over the depth-rank offsets; lanes emit their own Gaussian's
+  // slots when it has <= 32 of them in range, and whole warps share the big ones (a Gaussian
+  // near the camera can cover thousands of tiles).
+  chunk_of(I, lo, hi);
+  if (lo < hi) {
+    const int r_lo = cta_upper_rank(a.offsets, m, static_cast<uint32_t>(lo), sm);
+    const int r_hi = cta_upper_rank(a.offsets, m, static_cast<uint32_t>(hi - 1), sm);
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int rb = r_lo + warp * 32; rb <= r_hi; rb += kT) {
+      const int r = rb + lane;
+      uint32_t g = 0, e_b = 0, e_e = 0, off = 0;
+      ushort4 rc = make_ushort4(0, 0, 0, 0);
+      if (r <= r_hi) {
+        g = perm[r];
+        off = a.offsets[r];
+        rc = a.rect[g];
+        const uint32_t cnt = a.touched[g];
+        e_b = max(off, static_cast<uint32_t>(lo));
+        e_e = min(off + cnt, static_cast<uint32_t>(hi));
       }
+      const bool big = e_e > e_b + 32;
+      if (!big) emit_slots(a, g, rc, off, e_b, e_e, 0, 1);
+      uint32_t bigs = __ballot_sync(0xffffffffu, big);
+      while (bigs) {
+        const int j = __ffs(bigs) - 1;
+        bigs &= bigs - 1;
+        const uint32_t gj = __shfl_sync(0xffffffffu, g, j);
+        const uint32_t oj = __shfl_sync(0xffffffffu, off, j);
+        const uint32_t bj = __shfl_sync(0xffffffffu, e_b, j);
+        const uint32_t ej = __shfl_sync(0xffffffffu, e_e, j);
+        ushort4 rj;
+        rj.x = __shfl_sync(0xffffffffu, rc.x, j);
+        rj.y = __shfl_sync(0xffffffffu, rc.y, j);
+        rj.z = __shfl_sync(0xffffffffu, rc.z, j);
+        rj.w = __shfl_sync(0xffffffffu, rc.w, j);
+        emit_slots(a, gj, rj, oj, bj, ej, lane, 32);
+      }
+    }
   }
   grid.sync();
   trace(a.trace, 9);
@@ -370,23 +435,36 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
   }
 
   trace(a.trace, 10);
-  // ---- per-tile ranges, sorted Gaussian list ----
+  // ---- per-tile ranges, sorted Gaussian list, records gathered into sorted order ----
+  // 4 entries per thread per step so the dependent gathers (emission slot -> Gaussian ->
+  // 48-byte record) of several entries are in flight at once.
   chunk_of(I, lo, hi);
-  for (int k = lo + tid; k < hi; k += kT) {
-    const int t = static_cast<int>(sk[k]);
-    const int tp = k > 0 ? static_cast<int>(sk[k - 1]) : -1;
-    for (int tt = tp + 1; tt <= t; ++tt) a.tile_offsets[tt] = static_cast<uint32_t>(k);
-    if (k == I - 1)
-      for (int tt = t + 1; tt <= a.num_tiles; ++tt) a.tile_offsets[tt] = static_cast<uint32_t>(I);
-    const uint32_t e = sv[k];
-    const uint32_t g = a.emit_gauss[e];
-    a.sorted_emit[k] = e;
-    a.sorted_gauss[k] = g;
-    SortedRec r;
-    r.a = __ldg(a.rec0 + g);
-    r.b = __ldg(a.rec1 + g);
-    r.c = make_float4(__ldg(a.rec2 + g), 0.0f, 0.0f, 0.0f);
-    a.sorted_rec[k] = r;
+  for (int k0 = lo + tid; k0 < hi; k0 += 4 * kT) {
+    uint32_t e[4], g[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + u * kT;
+      e[u] = k < hi ? sv[k] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) g[u] = k0 + u * kT < hi ? a.emit_gauss[e[u]] : 0u;
+    SortedRec r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (k0 + u * kT < hi) r[u] = a.rec[g[u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + u * kT;
+      if (k >= hi) break;
+      const int t = static_cast<int>(sk[k]);
+      const int tp = k > 0 ? static_cast<int>(sk[k - 1]) : -1;
+      for (int tt = tp + 1; tt <= t; ++tt) a.tile_offsets[tt] = static_cast<uint32_t>(k);
+      if (k == I - 1)
+        for (int tt = t + 1; tt <= a.num_tiles; ++tt) a.tile_offsets[tt] = static_cast<uint32_t>(I);
+      a.sorted_emit[k] = e[u];
+      a.sorted_gauss[k] = g[u];
+      a.sorted_rec[k] = r[u];
+    }
   }
   trace(a.trace, 11);
   if (a.tile_order == nullptr) return;

@@ -52,8 +52,7 @@ struct fgs_context {
   std::string err;
 
   // per Gaussian
-  DevBuf<float4> rec0, rec1;
-  DevBuf<float> rec2;
+  DevBuf<fgs::SortedRec> rec;
   DevBuf<uint8_t> state;
   DevBuf<uint32_t> dkey, ckey, cval, dkey_a, dkey_b, perm_a, perm_b, touched, rank, offsets, scan_status;
   DevBuf<ushort4> rect;
@@ -213,11 +212,10 @@ int fgs_destroy(fgs_context* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   else cudaDeviceSynchronize();
-  for (auto* b : {&ctx->rec2, &ctx->final_T, &ctx->partials, &ctx->partial_tile, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
+  for (auto* b : {&ctx->final_T, &ctx->partials, &ctx->partial_tile, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
                   &ctx->h_sh, &ctx->h_img, &ctx->h_dl, &ctx->h_grad})
     b->release();
-  ctx->rec0.release();
-  ctx->rec1.release();
+  ctx->rec.release();
   ctx->state.release();
   for (auto* b : {&ctx->dkey, &ctx->ckey, &ctx->cval, &ctx->dkey_a, &ctx->dkey_b, &ctx->perm_a, &ctx->perm_b,
                   &ctx->touched, &ctx->rank, &ctx->offsets, &ctx->scan_status, &ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b,
@@ -294,9 +292,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   const int num_tiles = tiles_x * tiles_y;
   const size_t nn = static_cast<size_t>(n > 0 ? n : 1);
   const size_t npix = static_cast<size_t>(W) * H;
-  FGS_CHECK(ctx->rec0.ensure(nn));
-  FGS_CHECK(ctx->rec1.ensure(nn));
-  FGS_CHECK(ctx->rec2.ensure(nn));
+  FGS_CHECK(ctx->rec.ensure(nn));
   FGS_CHECK(ctx->state.ensure(nn));
   for (auto* b : {&ctx->dkey, &ctx->ckey, &ctx->cval, &ctx->dkey_a, &ctx->dkey_b, &ctx->perm_a, &ctx->perm_b,
                   &ctx->touched, &ctx->rank, &ctx->offsets})
@@ -336,9 +332,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.log_scales = scene->log_scales;
     pa.opacity = scene->opacity_logits;
     pa.sh = scene->sh;
-    pa.rec0 = ctx->rec0.p;
-    pa.rec1 = ctx->rec1.p;
-    pa.rec2 = ctx->rec2.p;
+    pa.rec = ctx->rec.p;
     pa.state = ctx->state.p;
     pa.depth_key = ctx->dkey.p;
     pa.touched = ctx->touched.p;
@@ -411,9 +405,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.sorted_gauss = ctx->sorted_gauss.p;
   bn.sorted_emit = ctx->sorted_emit_buf.p;
   FGS_CHECK(ctx->sorted_rec.ensure(ni));
-  bn.rec0 = ctx->rec0.p;
-  bn.rec1 = ctx->rec1.p;
-  bn.rec2 = ctx->rec2.p;
+  bn.rec = ctx->rec.p;
   bn.sorted_rec = ctx->sorted_rec.p;
   FGS_CHECK(ctx->tile_order.ensure(num_tiles));
   bn.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
@@ -509,7 +501,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   cudaEvent_t* ev = timing ? take_set(ctx, 1)->e : nullptr;
   if (timing) cudaEventRecord(ev[0], st);
   if (I > 0) ctx->launches += fgs::blend_backward(ba, st);
-  ctx->launches += fgs::combine_partials(ctx->tkey.p, ctx->emit_gauss.p, ctx->rec0.p, ctx->rec1.p, ctx->partials.p,
+  ctx->launches += fgs::combine_partials(ctx->tkey.p, ctx->emit_gauss.p, ctx->rec.p, ctx->partials.p,
                                          ctx->partial_tile.p, ctx->tiles_x, static_cast<int>(I), st);
   if (timing) cudaEventRecord(ev[1], st);
 
@@ -664,9 +656,7 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
     return static_cast<int64_t>(bytes);
   };
   if (nm == "state_u8") return copy(ctx->state.p, n);
-  if (nm == "rec0") return copy(ctx->rec0.p, n * 16);
-  if (nm == "rec1") return copy(ctx->rec1.p, n * 16);
-  if (nm == "rec2") return copy(ctx->rec2.p, n * 4);
+  if (nm == "rec") return copy(ctx->rec.p, n * sizeof(fgs::SortedRec));
   if (nm == "depth_key") return copy(ctx->dkey.p, n * 4);
   if (nm == "radius") return copy(ctx->radii.p, n * 4);
   if (nm == "touched") return copy(ctx->touched.p, n * 4);

@@ -33,16 +33,9 @@ struct DevCamera {
   float center[3];  // -W^T b (inc/cameras.hpp:60), precomputed on host in the same op order
 };
 
-// Splat record for the blend (per Gaussian):
-//   rec0 = (mean_px.x, mean_px.y, conic.a, conic.b), rec1 = (conic.c, alpha_max, R, G), rec2 = B
-struct SplatRefs {
-  const float4* rec0;
-  const float4* rec1;
-  const float* rec2;
-};
-
-// Splat record gathered into sorted (tile-list) order by the binning kernel, so the blends
-// read each tile's list as one contiguous, 16-byte aligned stream: 48 bytes per intersection.
+// Splat record (48 bytes, 16-byte aligned), written per Gaussian by K1 and gathered into
+// sorted (tile-list) order by the binning kernel, so the blends read each tile's list as one
+// contiguous stream.
 struct SortedRec {
   float4 a;  // mean_px.x, mean_px.y, conic.a, conic.b
   float4 b;  // conic.c, alpha_max, R, G

@@ -18,9 +18,7 @@ struct PreprocessArgs {
   const float* log_scales;
   const float* opacity;
   const float* sh;
-  float4* rec0;
-  float4* rec1;
-  float* rec2;
+  SortedRec* rec;        // per-Gaussian splat record
   uint8_t* state;
   uint32_t* depth_key;   // level-1 sort keys (0xFFFFFFFF for culled)
   uint32_t* touched;     // tiles touched
@@ -110,9 +108,7 @@ struct BinArgs {
   uint32_t* tile_offsets;      // [num_tiles + 1]
   uint32_t* sorted_gauss;      // [I]
   uint32_t* sorted_emit;       // [I]
-  const float4* rec0;          // per-Gaussian splat records (K1 output)
-  const float4* rec1;
-  const float* rec2;
+  const SortedRec* rec;        // per-Gaussian splat records (K1 output)
   SortedRec* sorted_rec;       // [I] records in sorted order
   uint32_t* tile_order;        // [num_tiles] blend schedule (optional)
   unsigned long long* trace;   // debug phase timestamps (optional)
@@ -132,7 +128,7 @@ cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* ke
 int blend_forward(const BlendArgs& a, cudaStream_t st);
 int blend_backward(const BlendArgs& a, cudaStream_t st);
 // K4c: per intersection, sum the per-block partials of the blocks passing the culling test.
-int combine_partials(const uint32_t* tile_keys, const uint32_t* emit_gauss, const float4* rec0, const float4* rec1,
+int combine_partials(const uint32_t* tile_keys, const uint32_t* emit_gauss, const SortedRec* rec,
                      const float* partials, float* partial_tile, int tiles_x, int ni, cudaStream_t st);
 // FP32 pipe probe: returns achieved non-FMA fp32 op/s (FMUL + FADD, no contraction).
 double fp32_peak_probe(cudaStream_t st);

@@ -342,9 +342,11 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
       }
     }
   }
-  a.rec0[i] = r0;
-  a.rec1[i] = r1;
-  a.rec2[i] = r2v;
+  SortedRec rr;
+  rr.a = r0;
+  rr.b = r1;
+  rr.c = make_float4(r2v, 0.0f, 0.0f, 0.0f);
+  a.rec[i] = rr;
   a.state[i] = state;
   a.depth_key[i] = key;
   a.touched[i] = touched;
@@ -370,26 +372,51 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a) {
 // Gaussian's emission slots [offset[rank[g]], +touched[g]) (ascending tile order; within a
 // tile the 8 pixel blocks were added in fixed order): deterministic, no atomics.
 __global__ void __launch_bounds__(128) preprocess_backward_kernel(PreprocessBackwardArgs a) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= a.n) return;
-  const uint8_t state = a.state[i];
+  const int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool valid = i0 < a.n;
+  const int64_t i = valid ? i0 : a.n - 1;
+  const uint8_t state = valid ? a.state[i] : 0;
+  const int lane = threadIdx.x & 31;
+  // gradients.hpp:161-173 -- per-splat sum over its intersections in ascending tile order.
+  // Gaussians with more than 32 tiles are summed by the whole warp (lane-strided, fixed
+  // shuffle tree): deterministic, and no lane walks thousands of tiles alone.
+  float sg[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
+  const uint32_t cnt = state == 1 ? a.touched[i] : 0u;
+  const uint32_t base = cnt ? a.offsets[a.rank[i]] : 0u;
+  const bool big = cnt > 32;
+  if (!big)
+    for (uint32_t e = base; e < base + cnt; ++e) {
+      const float* p = a.partials + int64_t(e) * 9;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) sg[k] = sg[k] + p[k];
+    }
+  uint32_t bigs = __ballot_sync(0xffffffffu, big);
+  while (bigs) {
+    const int j = __ffs(bigs) - 1;
+    bigs &= bigs - 1;
+    const uint32_t bj = __shfl_sync(0xffffffffu, base, j), cj = __shfl_sync(0xffffffffu, cnt, j);
+    float acc[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc[k] = 0.0f;
+    for (uint32_t e = bj + lane; e < bj + cj; e += 32) {
+      const float* p = a.partials + int64_t(e) * 9;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] = acc[k] + p[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[k] = acc[k] + __shfl_xor_sync(0xffffffffu, acc[k], o);
+      if (lane == j) sg[k] = acc[k];
+    }
+  }
+  if (!valid) return;
   float out[59];
 #pragma unroll
   for (int k = 0; k < 59; ++k) out[k] = 0.0f;
   if (state == 1) {
-    // gradients.hpp:161-173 — per-splat sum over tiles in ascending tile order
-    float sg[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
-    const uint32_t cnt = a.touched[i];
-    if (cnt) {
-      const uint32_t base = a.offsets[a.rank[i]];
-      for (uint32_t e = base; e < base + cnt; ++e) {
-        const float* p = a.partials + int64_t(e) * 9;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) sg[k] = sg[k] + p[k];
-      }
-    }
     const DevCamera& cam = a.cam;
     const float m[3] = {__ldg(a.means + 3 * i), __ldg(a.means + 3 * i + 1), __ldg(a.means + 3 * i + 2)};
     const float4 q = __ldg(reinterpret_cast<const float4*>(a.rotations) + i);

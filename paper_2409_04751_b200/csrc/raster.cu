@@ -375,15 +375,14 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
 // that passed the backward's culling test, in block order: partial_tile[e] (9 floats).
 __global__ void __launch_bounds__(256) combine_partials_kernel(const uint32_t* __restrict__ tile_keys,
                                                                const uint32_t* __restrict__ emit_gauss,
-                                                               const float4* __restrict__ rec0,
-                                                               const float4* __restrict__ rec1,
+                                                               const SortedRec* __restrict__ rec,
                                                                const float* __restrict__ partials,
                                                                float* __restrict__ partial_tile, int tiles_x, int ni) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= ni) return;
   const uint32_t t = __ldg(tile_keys + e), g = __ldg(emit_gauss + e);
   const int tx = static_cast<int>(t) % tiles_x, ty = static_cast<int>(t) / tiles_x;
-  const float4 r0 = __ldg(rec0 + g), r1 = __ldg(rec1 + g);
+  const float4 r0 = rec[g].a, r1 = rec[g].b;
   float ex, ey;
   const int kind = splat_extent(r0, r1, ex, ey);
   float sg[9];
@@ -405,10 +404,10 @@ __global__ void __launch_bounds__(256) combine_partials_kernel(const uint32_t* _
 
 }  // namespace
 
-int combine_partials(const uint32_t* tile_keys, const uint32_t* emit_gauss, const float4* rec0, const float4* rec1,
+int combine_partials(const uint32_t* tile_keys, const uint32_t* emit_gauss, const SortedRec* rec,
                      const float* partials, float* partial_tile, int tiles_x, int ni, cudaStream_t st) {
   if (ni <= 0) return 0;
-  combine_partials_kernel<<<div_up(ni, 256), 256, 0, st>>>(tile_keys, emit_gauss, rec0, rec1, partials,
+  combine_partials_kernel<<<div_up(ni, 256), 256, 0, st>>>(tile_keys, emit_gauss, rec, partials,
                                                             partial_tile, tiles_x, ni);
   return 1;
 }
