@@ -449,9 +449,10 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) g[u] = k0 + u * kT < hi ? a.emit_gauss[e[u]] : 0u;
     SortedRec r[4];
+    if (a.sorted_rec)
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (k0 + u * kT < hi) r[u] = a.rec[g[u]];
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u * kT < hi) r[u] = a.rec[g[u]];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int k = k0 + u * kT;
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(kT, 1) bin_level2_kernel(BinArgs a) {
         for (int tt = t + 1; tt <= a.num_tiles; ++tt) a.tile_offsets[tt] = static_cast<uint32_t>(I);
       a.sorted_emit[k] = e[u];
       a.sorted_gauss[k] = g[u];
-      a.sorted_rec[k] = r[u];
+      if (a.sorted_rec) a.sorted_rec[k] = r[u];
     }
   }
   trace(a.trace, 11);

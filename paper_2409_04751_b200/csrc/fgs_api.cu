@@ -98,6 +98,7 @@ struct fgs_context {
   uint32_t* sorted_emit = nullptr;   // level-2 result values
   size_t aux_bytes = 0;
   int px_per_lane = 1;  // tuning knob: FGS_PX_PER_LANE env (1 or 2)
+  int gather_records = 0;  // FGS_GATHER_RECORDS=1: binning gathers records into sorted order
   fgs::BinArgs bin_args{};
 };
 
@@ -192,6 +193,7 @@ int fgs_create(int device, fgs_context** out) {
   auto* ctx = new fgs_context();
   ctx->device = device;
   if (const char* v = std::getenv("FGS_PX_PER_LANE")) ctx->px_per_lane = std::atoi(v) == 2 ? 2 : 1;
+  if (const char* v = std::getenv("FGS_GATHER_RECORDS")) ctx->gather_records = std::atoi(v) != 0;
   e = cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   if (e != cudaSuccess) {
     delete ctx;
@@ -404,9 +406,9 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.tile_offsets = ctx->tile_offsets.p;
   bn.sorted_gauss = ctx->sorted_gauss.p;
   bn.sorted_emit = ctx->sorted_emit_buf.p;
-  FGS_CHECK(ctx->sorted_rec.ensure(ni));
+  if (ctx->gather_records) FGS_CHECK(ctx->sorted_rec.ensure(ni));
   bn.rec = ctx->rec.p;
-  bn.sorted_rec = ctx->sorted_rec.p;
+  bn.sorted_rec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
   FGS_CHECK(ctx->tile_order.ensure(num_tiles));
   bn.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
   FGS_CHECK(fgs::bin_level2(bn, st));
@@ -424,7 +426,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ba.tile_offsets = ctx->tile_offsets.p;
   ba.sorted_gauss = ctx->sorted_gauss.p;
   ba.sorted_emit = ctx->sorted_emit;
-  ba.srec = ctx->sorted_rec.p;
+  ba.srec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
+  ba.rec = ctx->rec.p;
   for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
   ba.image = image;
   ba.final_T = ctx->final_T.p;
@@ -489,7 +492,8 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   ba.tile_offsets = ctx->tile_offsets.p;
   ba.sorted_gauss = ctx->sorted_gauss.p;
   ba.sorted_emit = ctx->sorted_emit;
-  ba.srec = ctx->sorted_rec.p;
+  ba.srec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
+  ba.rec = ctx->rec.p;
   for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;

@@ -58,7 +58,8 @@ struct BlendArgs {
   const uint32_t* tile_offsets;  // T+1
   const uint32_t* sorted_gauss;  // I
   const uint32_t* sorted_emit;   // I (emission slot of each sorted entry; backward partials)
-  const SortedRec* srec;         // I records in sorted order
+  const SortedRec* srec;         // I records in sorted order (nullptr: read rec[sorted_gauss[k]])
+  const SortedRec* rec;          // per-Gaussian records
   float bg[3];
   float* image;                  // H*W*3
   float* final_T;                // H*W

@@ -28,6 +28,12 @@ constexpr int kBlend = 256;     // threads per tile CTA = pixels per tile
 constexpr int kWarps = kBlend / 32;
 constexpr int kGroup = 4;         // forward: splats whose alphas are computed together
 
+// Record of sorted entry k: from the gathered sorted stream when present, else through the
+// sorted Gaussian index.
+__device__ __forceinline__ SortedRec load_rec(const BlendArgs& a, uint32_t k) {
+  return a.srec ? a.srec[k] : a.rec[__ldg(a.sorted_gauss + k)];
+}
+
 struct PixelState {
   float T, C0, C1, C2;
   uint32_t last, stop, contrib;
@@ -117,8 +123,8 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   };
 
   const SortedRec zero{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-  SortedRec cur = lo + lane < hi ? a.srec[lo + lane] : zero;
-  SortedRec nxt = lo + 32 + lane < hi ? a.srec[lo + 32 + lane] : zero;
+  SortedRec cur = lo + lane < hi ? load_rec(a, lo + lane) : zero;
+  SortedRec nxt = lo + 32 + lane < hi ? load_rec(a, lo + 32 + lane) : zero;
   for (uint32_t base = lo; base < hi; base += 32) {
     if (__all_sync(0xffffffffu, all_done())) break;
     const bool pass = base + lane < hi && box_may_hit(cur.a, cur.b, bx0, bx0 + 7.0f, by0, by0 + (4.0f * PX - 1.0f));
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     uint32_t mask = __ballot_sync(0xffffffffu, pass);
     if (COUNTERS) warp_evals += __popc(mask);
     cur = nxt;
-    if (base + 64 + lane < hi) nxt = a.srec[base + 64 + lane];
+    if (base + 64 + lane < hi) nxt = load_rec(a, base + 64 + lane);
     __syncwarp();
     while (mask) {
       int js[kGroup];
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
   for (uint32_t base = wlast; base < hi; base += 32) {
     const uint32_t k = base + lane;
     if (k < hi) {
-      const SortedRec r = a.srec[k];
+      const SortedRec r = load_rec(a, k);
       if (box_may_hit(r.a, r.b, bx0, bx1, by0, by1)) {
         float* p = part + (static_cast<size_t>(a.sorted_emit[k]) * kBwdWarps + warp) * 9;
 #pragma unroll
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     const uint32_t k = cstart + lane;
     bool pass = false;
     if (k < end) {
-      const SortedRec r = a.srec[k];
+      const SortedRec r = load_rec(a, k);
       pass = box_may_hit(r.a, r.b, bx0, bx1, by0, by1);
       s0[warp][lane] = r.a;
       s1[warp][lane] = r.b;
