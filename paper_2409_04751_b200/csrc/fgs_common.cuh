@@ -39,7 +39,7 @@ struct DevCamera {
 struct SortedRec {
   float4 a;  // mean_px.x, mean_px.y, conic.a, conic.b
   float4 b;  // conic.c, alpha_max, R, G
-  float4 c;  // B, unused x3
+  float4 c;  // B, extent x, extent y (splat_extent_packed), unused
 };
 
 // Correctly rounded fp32 exp / atan2 (double evaluation, one rounding): the definition the
@@ -59,19 +59,19 @@ __device__ __forceinline__ float blend_power(float a, float b, float c, float dx
   return __fsub_rn(u, v);
 }
 
-// alpha_max * exp(power) with the fast MUFU exp, falling back to the correctly rounded exp
-// when the product lies within the fast path's error bound of a decision threshold.
-__device__ __forceinline__ float alpha_raw(float alpha_max, float power, float* expp) {
-  float e = __expf(power);
-  float ar = __fmul_rn(alpha_max, e);
-  const bool near_skip = fabsf(ar - kAlphaSkip) <= kGuardRel * kAlphaSkip;
-  const bool near_clamp = fabsf(ar - kAlphaClamp) <= kGuardRel * kAlphaClamp;
-  if (near_skip || near_clamp) {
-    e = cr_expf(power);
-    ar = __fmul_rn(alpha_max, e);
-  }
-  *expp = e;
-  return ar;
+// Fast exp: one MUFU.EX2 with flush-to-zero (no denormal fix-up; results below 2^-126 only
+// occur for power < -87, far past the skip threshold). Same value as __expf elsewhere.
+__device__ __forceinline__ float fast_exp(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__fmul_rn(x, 1.4426950408889634f)));
+  return y;
+}
+
+// Approximate reciprocal (MUFU.RCP, ftz) for arguments in [0.01, 1].
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 __host__ __device__ inline int div_up(int a, int b) { return (a + b - 1) / b; }
@@ -110,6 +110,22 @@ __device__ __forceinline__ bool box_may_hit(float4 r0, float4 r1, float x0, floa
   float ex, ey;
   const int kind = splat_extent(r0, r1, ex, ey);
   return extent_hits(kind, r0.x, r0.y, ex, ey, x0, x1, y0, y1);
+}
+
+// The extent as K1 stores it in the record (SortedRec.c.y/.z), computed once per Gaussian:
+// kind 0 -> -inf (the box test always fails), kind 2 -> +inf (it always passes).
+__device__ __forceinline__ float2 splat_extent_packed(float4 r0, float4 r1) {
+  float ex, ey;
+  const int kind = splat_extent(r0, r1, ex, ey);
+  if (kind == 0) return make_float2(-INFINITY, -INFINITY);
+  if (kind == 2) return make_float2(INFINITY, INFINITY);
+  return make_float2(ex, ey);
+}
+
+// box_may_hit from the stored extent: a = record .a (mean_px in .x/.y), c = record .c.
+__device__ __forceinline__ bool rec_hits(float4 a, float4 c, float x0, float x1, float y0, float y1) {
+  return __fadd_rn(a.x, c.y) >= x0 && __fsub_rn(a.x, c.y) <= x1 && __fadd_rn(a.y, c.z) >= y0 &&
+         __fsub_rn(a.y, c.z) <= y1;
 }
 
 // Backward blend geometry: 8 warps per 16x16 tile, warp w owns the 8x4 pixel block at

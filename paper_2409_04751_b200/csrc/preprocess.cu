@@ -345,7 +345,8 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
   SortedRec rr;
   rr.a = r0;
   rr.b = r1;
-  rr.c = make_float4(r2v, 0.0f, 0.0f, 0.0f);
+  const float2 ext = splat_extent_packed(r0, r1);
+  rr.c = make_float4(r2v, ext.x, ext.y, 0.0f);
   a.rec[i] = rr;
   a.state[i] = state;
   a.depth_key[i] = key;

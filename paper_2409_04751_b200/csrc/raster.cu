@@ -25,7 +25,6 @@ namespace fgs {
 namespace {
 
 constexpr int kBlend = 256;     // threads per tile CTA = pixels per tile
-constexpr int kWarps = kBlend / 32;
 constexpr int kGroup = 4;         // forward: splats whose alphas are computed together
 
 // Record of sorted entry k: from the gathered sorted stream when present, else through the
@@ -51,7 +50,7 @@ __device__ __forceinline__ float blend_power_dy(float fy, float4 r0, float c, fl
 // alpha_max * exp(power) with the fast exp; *near = the product lies within the fast path's
 // error bound of the 1/255 skip threshold (the caller then recomputes it exactly).
 __device__ __forceinline__ float alpha_fast(float amax, float power, bool* near) {
-  const float ar = __fmul_rn(amax, __expf(power));
+  const float ar = __fmul_rn(amax, fast_exp(power));
   *near = power <= 0.0f && fabsf(ar - kAlphaSkip) <= kGuardRel * kAlphaSkip;
   return ar;
 }
@@ -86,7 +85,7 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr
 // lane l the pixel(s) (l&7, (l>>3) + 4*q), q < PX, which share a column (so (a*dx)*dx and
 // b*dx are computed once). Warps walk the tile's sorted list independently in 32-splat chunks
 // (no CTA barriers): each lane reads one record (the list is contiguous in sorted order, two
-// chunks stay in flight), tests it against the warp's block (box_may_hit), and the warp blends
+// chunks stay in flight), tests it against the warp's block (rec_hits on the extent K1 stored), and the warp blends
 // the ballot of survivors in order from warp-private shared memory, kGroup splats at a time
 // (alphas first, independent of transmittance; then the sequential transmittance updates).
 // A warp stops when all its pixels have met the reference's termination rule.
@@ -127,7 +126,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   SortedRec nxt = lo + 32 + lane < hi ? load_rec(a, lo + 32 + lane) : zero;
   for (uint32_t base = lo; base < hi; base += 32) {
     if (__all_sync(0xffffffffu, all_done())) break;
-    const bool pass = base + lane < hi && box_may_hit(cur.a, cur.b, bx0, bx0 + 7.0f, by0, by0 + (4.0f * PX - 1.0f));
+    const bool pass = base + lane < hi && rec_hits(cur.a, cur.c, bx0, bx0 + 7.0f, by0, by0 + (4.0f * PX - 1.0f));
     s0[warp][lane] = cur.a;
     s1[warp][lane] = cur.b;
     s2[warp][lane] = cur.c.x;
@@ -223,16 +222,15 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   }
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+// alpha_raw's guard test: the fast-exp product lies within the error bound of a threshold.
+__device__ __forceinline__ bool near_threshold(float ar) {
+  return fabsf(ar - kAlphaSkip) <= kGuardRel * kAlphaSkip || fabsf(ar - kAlphaClamp) <= kGuardRel * kAlphaClamp;
 }
 
 // K4a backward blend (inc/gradients.hpp:69-175), barrier-free like the forward: 8 warps per
 // tile, warp w owns the 8x4 block of bwd_block_box, one pixel per lane. Each warp walks the
 // tile's list backwards from its last contributor (the max of its pixels' `last`) in 32-splat
-// chunks, culls them against its block (box_may_hit), and for each surviving splat recovers
+// chunks, culls them against its block (rec_hits on the extent K1 stored), and for each surviving splat recovers
 // T_before = T_after / (1 - alpha), accumulates the suffix colour and forms the 9 per-pixel
 // gradients (mean_px 2, conic 3, colour 3, alpha_max 1), summed over the warp's 32 pixels by
 // a shuffle tree. The warp sum goes to partials[emit][w] -- one slot per (intersection, block)
@@ -271,7 +269,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     const uint32_t k = base + lane;
     if (k < hi) {
       const SortedRec r = load_rec(a, k);
-      if (box_may_hit(r.a, r.b, bx0, bx1, by0, by1)) {
+      if (rec_hits(r.a, r.c, bx0, bx1, by0, by1)) {
         float* p = part + (static_cast<size_t>(a.sorted_emit[k]) * kBwdWarps + warp) * 9;
 #pragma unroll
         for (int q = 0; q < 9; ++q) p[q] = 0.0f;
@@ -285,7 +283,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     bool pass = false;
     if (k < end) {
       const SortedRec r = load_rec(a, k);
-      pass = box_may_hit(r.a, r.b, bx0, bx1, by0, by1);
+      pass = rec_hits(r.a, r.c, bx0, bx1, by0, by1);
       s0[warp][lane] = r.a;
       s1[warp][lane] = r.b;
       s2[warp][lane] = r.c.x;
@@ -306,6 +304,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
       }
       float pw[3], ex[3], ar[3], dxs[3], dys[3];
       float4 r0s[3], r1s[3];
+      bool any_near = false;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const int jj = js[q] >= 0 ? js[q] : 0;
@@ -314,46 +313,56 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
         dxs[q] = __fsub_rn(fx, r0s[q].x);
         dys[q] = __fsub_rn(fy, r0s[q].y);
         pw[q] = blend_power(r0s[q].z, r0s[q].w, r1s[q].x, dxs[q], dys[q]);
-        ar[q] = alpha_raw(r1s[q].y, pw[q], &ex[q]);
+        ex[q] = fast_exp(pw[q]);
+        ar[q] = __fmul_rn(r1s[q].y, ex[q]);
+        any_near |= near_threshold(ar[q]);
       }
-      float v[32];
+      if (__any_sync(0xffffffffu, any_near)) {  // rare: exact exp near the 1/255 or 0.99 threshold
 #pragma unroll
-      for (int q = 0; q < 32; ++q) v[q] = 0.0f;
+        for (int q = 0; q < 3; ++q)
+          if (near_threshold(ar[q])) {
+            ex[q] = cr_expf(pw[q]);
+            ar[q] = __fmul_rn(r1s[q].y, ex[q]);
+          }
+      }
+      // Branch-free: every lane evaluates all three steps and gates them (a non-contributing
+      // step leaves T and the suffix colour unchanged and gives zero gradients; all operands
+      // are finite: conic <= 1/0.3, one_m >= 0.01).
+      float v[32];
       bool contrib_any = false;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        if (js[q] < 0) break;
-        const uint32_t kk = cstart + js[q];
+        const uint32_t kk = cstart + static_cast<uint32_t>(js[q]);
         const float alpha = fminf(kAlphaClamp, ar[q]);
-        if (kk < last && pw[q] <= 0.0f && pw[q] >= kPowerFloor && alpha >= kAlphaSkip) {
-          contrib_any = true;
-          const float4 r0 = r0s[q], r1 = r1s[q];
-          const float dx = dxs[q], dy = dys[q];
-          const float one_m = 1.0f - alpha;
-          const float Tb = T / one_m;
-          const float w = alpha * Tb;
-          const float b2 = s2[warp][js[q]];
-          v[9 * q + 5] = dl0 * w;
-          v[9 * q + 6] = dl1 * w;
-          v[9 * q + 7] = dl2 * w;
-          const float dot_c = dl0 * r1.z + dl1 * r1.w + dl2 * b2;
-          const float dot_s = dl0 * sf0 + dl1 * sf1 + dl2 * sf2;
-          const float d_alpha = dot_c * Tb - dot_s / one_m;
-          sf0 = fmaf(r1.z, w, sf0);
-          sf1 = fmaf(r1.w, w, sf1);
-          sf2 = fmaf(b2, w, sf2);
-          T = Tb;
-          if (!(ar[q] > kAlphaClamp)) {  // clamped contributions carry no geometric gradient
-            v[9 * q + 8] = d_alpha * ex[q];
-            const float dp = d_alpha * alpha;
-            v[9 * q + 0] = dp * (r0.z * dx + r0.w * dy);
-            v[9 * q + 1] = dp * (r0.w * dx + r1.x * dy);
-            v[9 * q + 2] = dp * (-0.5f * dx * dx);
-            v[9 * q + 3] = dp * (-dx * dy);
-            v[9 * q + 4] = dp * (-0.5f * dy * dy);
-          }
-        }
+        const bool c = js[q] >= 0 && kk < last && pw[q] <= 0.0f && pw[q] >= kPowerFloor && alpha >= kAlphaSkip;
+        contrib_any |= c;
+        const float4 r0 = r0s[q], r1 = r1s[q];
+        const float dx = dxs[q], dy = dys[q];
+        const float inv = fast_rcp(1.0f - alpha);
+        const float Tb = T * inv;
+        const float w = c ? alpha * Tb : 0.0f;
+        const float b2 = s2[warp][js[q] >= 0 ? js[q] : 0];
+        v[9 * q + 5] = dl0 * w;
+        v[9 * q + 6] = dl1 * w;
+        v[9 * q + 7] = dl2 * w;
+        const float dot_c = dl0 * r1.z + dl1 * r1.w + dl2 * b2;
+        const float dot_s = dl0 * sf0 + dl1 * sf1 + dl2 * sf2;
+        // clamped contributions carry no geometric gradient
+        const float d_alpha = (c && !(ar[q] > kAlphaClamp)) ? dot_c * Tb - dot_s * inv : 0.0f;
+        sf0 = fmaf(r1.z, w, sf0);
+        sf1 = fmaf(r1.w, w, sf1);
+        sf2 = fmaf(b2, w, sf2);
+        T = c ? Tb : T;
+        v[9 * q + 8] = d_alpha * ex[q];
+        const float dp = d_alpha * alpha;
+        v[9 * q + 0] = dp * (r0.z * dx + r0.w * dy);
+        v[9 * q + 1] = dp * (r0.w * dx + r1.x * dy);
+        v[9 * q + 2] = dp * (-0.5f * dx * dx);
+        v[9 * q + 3] = dp * (-dx * dy);
+        v[9 * q + 4] = dp * (-0.5f * dy * dy);
       }
+#pragma unroll
+      for (int q = 27; q < 32; ++q) v[q] = 0.0f;
       if (__any_sync(0xffffffffu, contrib_any)) {
 #pragma unroll
         for (int half = 16; half >= 1; half >>= 1) {
@@ -388,9 +397,7 @@ __global__ void __launch_bounds__(256) combine_partials_kernel(const uint32_t* _
   if (e >= ni) return;
   const uint32_t t = __ldg(tile_keys + e), g = __ldg(emit_gauss + e);
   const int tx = static_cast<int>(t) % tiles_x, ty = static_cast<int>(t) / tiles_x;
-  const float4 r0 = rec[g].a, r1 = rec[g].b;
-  float ex, ey;
-  const int kind = splat_extent(r0, r1, ex, ey);
+  const float4 r0 = rec[g].a, r2 = rec[g].c;
   float sg[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
@@ -399,7 +406,7 @@ __global__ void __launch_bounds__(256) combine_partials_kernel(const uint32_t* _
   for (int w = 0; w < kBwdWarps; ++w) {
     float x0, x1, y0, y1;
     bwd_block_box(tx, ty, w, x0, x1, y0, y1);
-    if (!extent_hits(kind, r0.x, r0.y, ex, ey, x0, x1, y0, y1)) continue;
+    if (!rec_hits(r0, r2, x0, x1, y0, y1)) continue;
 #pragma unroll
     for (int k = 0; k < 9; ++k) sg[k] = sg[k] + p[w * 9 + k];
   }
