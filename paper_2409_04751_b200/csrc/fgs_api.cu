@@ -92,6 +92,7 @@ struct fgs_context {
   fgs::DevCamera dcam{};
   int tiles_x = 0, tiles_y = 0;
   int64_t num_isect = 0;
+  int64_t num_compact = 0;  // Gaussians touching >= 1 tile (rows the backward computes)
   uint32_t num_splats = 0, num_degenerate = 0, num_culled = 0;
   uint32_t* perm = nullptr;          // level-1 result values
   uint32_t* sorted_tiles = nullptr;  // level-2 result keys
@@ -383,6 +384,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   if (ctx->h_scalars[fgs::kScalarErr]) return fail(ctx, FGS_EDEGENERATE_QUAT, "degenerate rotation: quaternion has zero norm");
   const int64_t I = ctx->h_scalars[fgs::kScalarI];
   ctx->num_isect = I;
+  ctx->num_compact = ctx->h_scalars[fgs::kScalarM];
   ctx->num_splats = ctx->h_scalars[fgs::kScalarKept];
   ctx->num_degenerate = ctx->h_scalars[fgs::kScalarDegen];
   ctx->num_culled = static_cast<uint32_t>(n) - ctx->num_splats - ctx->num_degenerate;
@@ -532,8 +534,11 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.d_log_scales = grads->d_log_scales;
   pb.d_opacity = grads->d_opacity_logits;
   pb.d_sh = grads->d_sh;
-  fgs::preprocess_backward_kernel<<<fgs::div_up(static_cast<int>(n), 128), 128, 0, st>>>(pb);
-  ++ctx->launches;
+  pb.aligned16 = ((reinterpret_cast<uintptr_t>(grads->d_rotations) | reinterpret_cast<uintptr_t>(grads->d_sh)) & 15u) == 0;
+  if (n > 0) {
+    fgs::preprocess_backward_kernel<<<fgs::div_up(static_cast<int>(n), fgs::kPreprocessBackwardRange), 128, 0, st>>>(pb);
+    ++ctx->launches;
+  }
   if (timing) cudaEventRecord(ev[2], st);
   FGS_CHECK(cudaGetLastError());
   return FGS_OK;

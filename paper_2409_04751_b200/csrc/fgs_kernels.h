@@ -51,6 +51,7 @@ struct PreprocessBackwardArgs {
   float* d_log_scales;
   float* d_opacity;
   float* d_sh;
+  int aligned16;             // d_rotations and d_sh 16-byte aligned: float4 stores
 };
 
 struct BlendArgs {
@@ -75,6 +76,7 @@ struct BlendArgs {
 
 __global__ void preprocess_kernel(PreprocessArgs a);
 __global__ void preprocess_backward_kernel(PreprocessBackwardArgs a);
+constexpr int kPreprocessBackwardRange = 128;  // Gaussians (= threads) per K4b CTA
 
 // ---- binning / sorting (binning.cu) ----
 constexpr int kBinThreads = 1024;

@@ -369,55 +369,13 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a) {
   if (threadIdx.x < 2 && s_counts[threadIdx.x]) atomicAdd(a.state_counts + threadIdx.x, s_counts[threadIdx.x]);
 }
 
-// K4b: per Gaussian, after K4a/K4c left one 9-float partial per intersection at the
-// Gaussian's emission slots [offset[rank[g]], +touched[g]) (ascending tile order; within a
-// tile the 8 pixel blocks were added in fixed order): deterministic, no atomics.
-__global__ void __launch_bounds__(128) preprocess_backward_kernel(PreprocessBackwardArgs a) {
-  const int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool valid = i0 < a.n;
-  const int64_t i = valid ? i0 : a.n - 1;
-  const uint8_t state = valid ? a.state[i] : 0;
-  const int lane = threadIdx.x & 31;
-  // gradients.hpp:161-173 -- per-splat sum over its intersections in ascending tile order.
-  // Gaussians with more than 32 tiles are summed by the whole warp (lane-strided, fixed
-  // shuffle tree): deterministic, and no lane walks thousands of tiles alone.
-  float sg[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
-  const uint32_t cnt = state == 1 ? a.touched[i] : 0u;
-  const uint32_t base = cnt ? a.offsets[a.rank[i]] : 0u;
-  const bool big = cnt > 32;
-  if (!big)
-    for (uint32_t e = base; e < base + cnt; ++e) {
-      const float* p = a.partials + int64_t(e) * 9;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) sg[k] = sg[k] + p[k];
-    }
-  uint32_t bigs = __ballot_sync(0xffffffffu, big);
-  while (bigs) {
-    const int j = __ffs(bigs) - 1;
-    bigs &= bigs - 1;
-    const uint32_t bj = __shfl_sync(0xffffffffu, base, j), cj = __shfl_sync(0xffffffffu, cnt, j);
-    float acc[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) acc[k] = 0.0f;
-    for (uint32_t e = bj + lane; e < bj + cj; e += 32) {
-      const float* p = a.partials + int64_t(e) * 9;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) acc[k] = acc[k] + p[k];
-    }
-#pragma unroll
-    for (int k = 0; k < 9; ++k) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[k] = acc[k] + __shfl_xor_sync(0xffffffffu, acc[k], o);
-      if (lane == j) sg[k] = acc[k];
-    }
-  }
-  if (!valid) return;
+// K4b per-Gaussian chain rule for Gaussian i with its summed screen-space gradient sg[9]
+// (mean_px 2, conic 3, colour 3, alpha 1); writes (or adds) its 59 gradient values.
+__device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& a, int64_t i, const float sg[9]) {
   float out[59];
 #pragma unroll
   for (int k = 0; k < 59; ++k) out[k] = 0.0f;
-  if (state == 1) {
+  {
     const DevCamera& cam = a.cam;
     const float m[3] = {__ldg(a.means + 3 * i), __ldg(a.means + 3 * i + 1), __ldg(a.means + 3 * i + 2)};
     const float4 q = __ldg(reinterpret_cast<const float4*>(a.rotations) + i);
@@ -587,13 +545,119 @@ __global__ void __launch_bounds__(128) preprocess_backward_kernel(PreprocessBack
   } else {
 #pragma unroll
     for (int k = 0; k < 3; ++k) dm[k] = out[k];
-    reinterpret_cast<float4*>(drt)[0] = make_float4(out[3], out[4], out[5], out[6]);
 #pragma unroll
     for (int k = 0; k < 3; ++k) dls[k] = out[7 + k];
     a.d_opacity[i] = out[10];
+    if (a.aligned16) {
+      reinterpret_cast<float4*>(drt)[0] = make_float4(out[3], out[4], out[5], out[6]);
 #pragma unroll
-    for (int k = 0; k < 12; ++k)
-      reinterpret_cast<float4*>(dsh)[k] = make_float4(out[11 + 4 * k], out[12 + 4 * k], out[13 + 4 * k], out[14 + 4 * k]);
+      for (int k = 0; k < 12; ++k)
+        reinterpret_cast<float4*>(dsh)[k] = make_float4(out[11 + 4 * k], out[12 + 4 * k], out[13 + 4 * k], out[14 + 4 * k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) drt[k] = out[3 + k];
+#pragma unroll
+      for (int k = 0; k < 48; ++k) dsh[k] = out[11 + k];
+    }
+  }
+}
+
+// K4b: one CTA (one thread per Gaussian) per range of kBwdRange consecutive Gaussians.
+// K4a/K4c left one 9-float partial per intersection at the Gaussian's emission slots [offset[rank[g]], +touched[g])
+// (ascending tile order; within a tile the 8 pixel blocks were added in fixed order), summed
+// here in that order: deterministic, no atomics (gradients.hpp:161-173). Gaussians that
+// touched no tile have zero gradient. The CTA queues its touching Gaussians (so lanes are
+// not wasted on the others), runs the chain rule for them, and zero-fills the other rows of
+// its range with coalesced stores -- every sector of the range is written by one CTA in a
+// short window, so L2 merges partial-sector writes instead of read-modify-writing DRAM.
+constexpr int kBwdRange = kPreprocessBackwardRange;
+constexpr int kBwdThreads = kPreprocessBackwardRange;
+__global__ void __launch_bounds__(kBwdThreads) preprocess_backward_kernel(PreprocessBackwardArgs a) {
+  __shared__ uint16_t queue[kBwdRange];
+  __shared__ uint8_t vis[kBwdRange];
+  __shared__ int woff[kBwdThreads / 32 + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t g0 = int64_t(blockIdx.x) * kBwdRange;
+  const int nloc = static_cast<int>(a.n - g0 < kBwdRange ? a.n - g0 : kBwdRange);
+  // queue the touching Gaussians of the range in ascending order
+  const int j0 = tid;
+  const bool v0 = j0 < nloc && __ldg(a.touched + g0 + j0) > 0u;
+  vis[j0] = v0;
+  const uint32_t b0 = __ballot_sync(0xffffffffu, v0);
+  if (lane == 0) woff[warp + 1] = __popc(b0);
+  __syncthreads();
+  if (tid == 0) {
+    woff[0] = 0;
+    for (int w = 1; w <= kBwdThreads / 32; ++w) woff[w] += woff[w - 1];
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+  if (v0) queue[woff[warp] + __popc(b0 & lt)] = static_cast<uint16_t>(j0);
+  const int count = woff[kBwdThreads / 32];
+  __syncthreads();
+  if (!a.accumulate) {  // zero rows of the range's non-touching Gaussians, coalesced
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (a.aligned16) {
+      float4* sh4 = reinterpret_cast<float4*>(a.d_sh + 48 * g0);
+      for (int f = tid; f < nloc * 12; f += kBwdThreads)
+        if (!vis[f / 12]) sh4[f] = z;
+      float4* rt4 = reinterpret_cast<float4*>(a.d_rotations + 4 * g0);
+      for (int f = tid; f < nloc; f += kBwdThreads)
+        if (!vis[f]) rt4[f] = z;
+    } else {
+      for (int f = tid; f < nloc * 48; f += kBwdThreads)
+        if (!vis[f / 48]) a.d_sh[48 * g0 + f] = 0.f;
+      for (int f = tid; f < nloc * 4; f += kBwdThreads)
+        if (!vis[f / 4]) a.d_rotations[4 * g0 + f] = 0.f;
+    }
+    for (int f = tid; f < nloc; f += kBwdThreads)
+      if (!vis[f]) a.d_opacity[g0 + f] = 0.f;
+    for (int f = tid; f < nloc * 3; f += kBwdThreads)
+      if (!vis[f / 3]) {
+        a.d_means[3 * g0 + f] = 0.f;
+        a.d_log_scales[3 * g0 + f] = 0.f;
+      }
+  }
+  {
+    // warps past the queue's end have nothing left to do (their range rows are written)
+    if ((tid & ~31) >= count) return;
+    const bool valid = tid < count;
+    const int64_t i = g0 + (valid ? queue[tid] : queue[0]);
+    // Gaussians with more than 32 tiles are summed by the whole warp (lane-strided, fixed
+    // shuffle tree): deterministic, and no lane walks thousands of tiles alone.
+    float sg[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
+    const uint32_t cnt = valid ? a.touched[i] : 0u;
+    const uint32_t base = valid ? a.offsets[a.rank[i]] : 0u;
+    const bool big = cnt > 32;
+    if (!big)
+      for (uint32_t e = base; e < base + cnt; ++e) {
+        const float* p = a.partials + int64_t(e) * 9;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) sg[k] = sg[k] + p[k];
+      }
+    uint32_t bigs = __ballot_sync(0xffffffffu, big);
+    while (bigs) {
+      const int j = __ffs(bigs) - 1;
+      bigs &= bigs - 1;
+      const uint32_t bj = __shfl_sync(0xffffffffu, base, j), cj = __shfl_sync(0xffffffffu, cnt, j);
+      float acc[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) acc[k] = 0.0f;
+      for (uint32_t e = bj + lane; e < bj + cj; e += 32) {
+        const float* p = a.partials + int64_t(e) * 9;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) acc[k] = acc[k] + p[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[k] = acc[k] + __shfl_xor_sync(0xffffffffu, acc[k], o);
+        if (lane == j) sg[k] = acc[k];
+      }
+    }
+    if (valid) gaussian_backward(a, i, sg);
   }
 }
 

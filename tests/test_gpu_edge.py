@@ -200,3 +200,22 @@ def test_cpp_wrapper_example():
     assert int(kv["intersections"]) > 0 and int(kv["splats"]) > 0
     assert float(kv["image_mean"]) > 0 and float(kv["grad_mean_l1"]) > 0
     assert kv["error_check"] == "ok"
+
+
+def test_backward_unaligned_gradient_fields(rast, oracle_mod):
+    """N not a multiple of 4: the flat 59N gradient buffer's rotation and SH fields are not
+    16-byte aligned, so K4b takes its scalar-store path."""
+    import torch
+    from paper_2409_04751_b200 import BackwardOptions, RenderOptions, grads_as_rows
+
+    sc = spherical_scene(2999, 7)
+    cam = small_fisheye(256, 192)
+    rast.forward(to_device(sc), cam, RenderOptions(sh_degree=3, background=sc.background))
+    dl = np.random.default_rng(3).standard_normal((cam.height, cam.width, 3)).astype(np.float32)
+    g = rast.backward(to_device(sc), cam, torch.from_numpy(dl).cuda(), BackwardOptions())
+    torch.cuda.synchronize()
+    res = oracle_mod.render(sc, cam, sh_degree=3)
+    ref, _ = oracle_mod.backward(res, sc.n, dl)
+    got = grads_as_rows(g, sc.n)
+    for k in ("mean", "rotation", "log_scale", "opacity", "sh_dc", "sh_rest"):
+        assert rel_l2(got[:, GROUPS[k]], ref[:, GROUPS[k]]) <= 1e-3, k
