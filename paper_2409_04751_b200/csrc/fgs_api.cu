@@ -535,8 +535,12 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.d_opacity = grads->d_opacity_logits;
   pb.d_sh = grads->d_sh;
   pb.aligned16 = ((reinterpret_cast<uintptr_t>(grads->d_rotations) | reinterpret_cast<uintptr_t>(grads->d_sh)) & 15u) == 0;
-  if (n > 0) {
-    fgs::preprocess_backward_kernel<<<fgs::div_up(static_cast<int>(n), fgs::kPreprocessBackwardRange), 128, 0, st>>>(pb);
+  pb.m = ctx->num_compact;
+  pb.cval = ctx->cval.p;
+  pb.rec = ctx->rec.p;
+  if (n > 0 && (pb.m > 0 || !pb.accumulate)) {
+    const int blocks = pb.m > 0 ? fgs::div_up(static_cast<int>(pb.m), fgs::kPreprocessBackwardThreads) : 1;
+    fgs::preprocess_backward_kernel<<<blocks, fgs::kPreprocessBackwardThreads, 0, st>>>(pb);
     ++ctx->launches;
   }
   if (timing) cudaEventRecord(ev[2], st);

@@ -30,6 +30,9 @@ struct PreprocessArgs {
 
 struct PreprocessBackwardArgs {
   int64_t n;
+  int64_t m;                 // Gaussians that touched >= 1 tile (level-1 compaction count)
+  const uint32_t* cval;      // [m] their ids in source order
+  const SortedRec* rec;      // K1 per-Gaussian records (alpha, clamped colours)
   DevCamera cam;
   int sh_degree;
   int full_sh;
@@ -76,7 +79,7 @@ struct BlendArgs {
 
 __global__ void preprocess_kernel(PreprocessArgs a);
 __global__ void preprocess_backward_kernel(PreprocessBackwardArgs a);
-constexpr int kPreprocessBackwardRange = 128;  // Gaussians (= threads) per K4b CTA
+constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per K4b CTA
 
 // ---- binning / sorting (binning.cu) ----
 constexpr int kBinThreads = 1024;

@@ -222,6 +222,15 @@ __device__ __forceinline__ void load_sh(const float* __restrict__ sh, int64_t g,
   }
 }
 
+// The 16 coefficients of one colour channel (only the SH view-direction gradient needs them).
+__device__ __forceinline__ void load_sh_channel(const float* __restrict__ sh, int64_t g, int ch, int degree,
+                                                float k[16]) {
+  const float* p = sh + g * 48 + 16 * ch;
+  const int nb = (degree + 1) * (degree + 1);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) k[j] = j < nb ? __ldg(p + j) : 0.0f;
+}
+
 __device__ __forceinline__ void view_dir(const DevCamera& cam, const float m[3], float dir[3]) {
   const float v0 = m[0] - cam.center[0], v1 = m[1] - cam.center[1], v2 = m[2] - cam.center[2];
   const float n2 = v0 * v0 + v1 * v1 + v2 * v2;
@@ -372,9 +381,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a) {
 // K4b per-Gaussian chain rule for Gaussian i with its summed screen-space gradient sg[9]
 // (mean_px 2, conic 3, colour 3, alpha 1); writes (or adds) its 59 gradient values.
 __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& a, int64_t i, const float sg[9]) {
-  float out[59];
+  float out[11];  // mean 3, rotation 4, log-scale 3, opacity 1 (SH rows are stored as computed)
 #pragma unroll
-  for (int k = 0; k < 59; ++k) out[k] = 0.0f;
+  for (int k = 0; k < 11; ++k) out[k] = 0.0f;
   {
     const DevCamera& cam = a.cam;
     const float m[3] = {__ldg(a.means + 3 * i), __ldg(a.means + 3 * i + 1), __ldg(a.means + 3 * i + 2)};
@@ -494,27 +503,44 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
     const float v[3] = {direct[0] + cov[0], direct[1] + cov[1], direct[2] + cov[2]};
 #pragma unroll
     for (int r = 0; r < 3; ++r) out[r] = cam.W[0 * 3 + r] * v[0] + cam.W[1 * 3 + r] * v[1] + cam.W[2 * 3 + r] * v[2];
-    const float al = sigmoid(__ldg(a.opacity + i));
+    // K1's record holds sigmoid(opacity) and the clamped colours, computed by the same code
+    // in this translation unit: bit-identical to recomputing them, without the SH reads.
+    const float4 rb = a.rec[i].b;
+    const float colour[3] = {rb.z, rb.w, a.rec[i].c.x};
+    const float al = rb.y;
     out[10] = sg[8] * al * (1.0f - al);
     // SH: eval_sh_dc_backward (model.hpp:219-227) + higher bands (build extension)
     float dir[3];
     view_dir(cam, m, dir);
     float Y[16];
     sh_basis(dir, a.sh_degree, Y);
-    float k[48];
-    load_sh(a.sh, i, a.sh_degree, k);
     const int nb = a.full_sh ? (a.sh_degree + 1) * (a.sh_degree + 1) : 1;
     float ddir[3] = {0.0f, 0.0f, 0.0f};
+    float* dsh = a.d_sh + 48 * i;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      const float col = sh_channel(k + 16 * ch, Y, a.sh_degree);
-      if (!(col > 0.0f)) continue;
+      const bool live = colour[ch] > 0.0f;  // clamped channel: no gradient
       const float dc = sg[5 + ch];
-      out[11 + 16 * ch] = float(kC0) * dc;
+      float g[16];
 #pragma unroll
-      for (int jb = 1; jb < 16; ++jb)
-        if (jb < nb) out[11 + 16 * ch + jb] = Y[jb] * dc;
-      if (a.view_dir && a.sh_degree > 0) sh_dir_grad(dir, a.sh_degree, k + 16 * ch, dc, ddir);
+      for (int jb = 0; jb < 16; ++jb) g[jb] = (live && jb < nb) ? (jb == 0 ? float(kC0) : Y[jb]) * dc : 0.0f;
+      float* d = dsh + 16 * ch;
+      if (a.accumulate) {
+#pragma unroll
+        for (int jb = 0; jb < 16; ++jb) d[jb] += g[jb];
+      } else if (a.aligned16) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          reinterpret_cast<float4*>(d)[k] = make_float4(g[4 * k], g[4 * k + 1], g[4 * k + 2], g[4 * k + 3]);
+      } else {
+#pragma unroll
+        for (int jb = 0; jb < 16; ++jb) d[jb] = g[jb];
+      }
+      if (live && a.view_dir && a.sh_degree > 0) {
+        float k[16];
+        load_sh_channel(a.sh, i, ch, a.sh_degree, k);
+        sh_dir_grad(dir, a.sh_degree, k, dc, ddir);
+      }
     }
     if (a.view_dir && a.sh_degree > 0) {
       // colour -> view direction -> mean (not in the reference; opt-in)
@@ -531,7 +557,6 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
   float* dm = a.d_means + 3 * i;
   float* drt = a.d_rotations + 4 * i;
   float* dls = a.d_log_scales + 3 * i;
-  float* dsh = a.d_sh + 48 * i;
   if (a.accumulate) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) dm[k] += out[k];
@@ -540,8 +565,6 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
 #pragma unroll
     for (int k = 0; k < 3; ++k) dls[k] += out[7 + k];
     a.d_opacity[i] += out[10];
-#pragma unroll
-    for (int k = 0; k < 48; ++k) dsh[k] += out[11 + k];
   } else {
 #pragma unroll
     for (int k = 0; k < 3; ++k) dm[k] = out[k];
@@ -550,79 +573,59 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
     a.d_opacity[i] = out[10];
     if (a.aligned16) {
       reinterpret_cast<float4*>(drt)[0] = make_float4(out[3], out[4], out[5], out[6]);
-#pragma unroll
-      for (int k = 0; k < 12; ++k)
-        reinterpret_cast<float4*>(dsh)[k] = make_float4(out[11 + 4 * k], out[12 + 4 * k], out[13 + 4 * k], out[14 + 4 * k]);
     } else {
 #pragma unroll
       for (int k = 0; k < 4; ++k) drt[k] = out[3 + k];
-#pragma unroll
-      for (int k = 0; k < 48; ++k) dsh[k] = out[11 + k];
     }
   }
 }
 
-// K4b: one CTA (one thread per Gaussian) per range of kBwdRange consecutive Gaussians.
-// K4a/K4c left one 9-float partial per intersection at the Gaussian's emission slots [offset[rank[g]], +touched[g])
-// (ascending tile order; within a tile the 8 pixel blocks were added in fixed order), summed
-// here in that order: deterministic, no atomics (gradients.hpp:161-173). Gaussians that
-// touched no tile have zero gradient. The CTA queues its touching Gaussians (so lanes are
-// not wasted on the others), runs the chain rule for them, and zero-fills the other rows of
-// its range with coalesced stores -- every sector of the range is written by one CTA in a
-// short window, so L2 merges partial-sector writes instead of read-modify-writing DRAM.
-constexpr int kBwdRange = kPreprocessBackwardRange;
-constexpr int kBwdThreads = kPreprocessBackwardRange;
-__global__ void __launch_bounds__(kBwdThreads) preprocess_backward_kernel(PreprocessBackwardArgs a) {
-  __shared__ uint16_t queue[kBwdRange];
-  __shared__ uint8_t vis[kBwdRange];
-  __shared__ int woff[kBwdThreads / 32 + 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t g0 = int64_t(blockIdx.x) * kBwdRange;
-  const int nloc = static_cast<int>(a.n - g0 < kBwdRange ? a.n - g0 : kBwdRange);
-  // queue the touching Gaussians of the range in ascending order
-  const int j0 = tid;
-  const bool v0 = j0 < nloc && __ldg(a.touched + g0 + j0) > 0u;
-  vis[j0] = v0;
-  const uint32_t b0 = __ballot_sync(0xffffffffu, v0);
-  if (lane == 0) woff[warp + 1] = __popc(b0);
-  __syncthreads();
-  if (tid == 0) {
-    woff[0] = 0;
-    for (int w = 1; w <= kBwdThreads / 32; ++w) woff[w] += woff[w - 1];
-  }
-  __syncthreads();
-  const uint32_t lt = (1u << lane) - 1u;
-  if (v0) queue[woff[warp] + __popc(b0 & lt)] = static_cast<uint16_t>(j0);
-  const int count = woff[kBwdThreads / 32];
-  __syncthreads();
-  if (!a.accumulate) {  // zero rows of the range's non-touching Gaussians, coalesced
+// K4b: one thread per Gaussian that touched a tile, taken in source order from the level-1
+// compaction list (cval), 128 per CTA. K4a/K4c left one 9-float partial per intersection at
+// the Gaussian's emission slots [offset[rank[g]], +touched[g]) (ascending tile order; within
+// a tile the 8 pixel blocks were added in fixed order), summed here in that order:
+// deterministic, no atomics (gradients.hpp:161-173). Gaussians that touched no tile have zero
+// gradient; CTA b also zero-fills, with coalesced stores, the non-touching rows between its
+// predecessor's last Gaussian and its own last one -- so every sector of that source range
+// is written by one CTA in a short window and L2 merges the partial-sector writes.
+constexpr int kBwdThreads = kPreprocessBackwardThreads;
+__global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(PreprocessBackwardArgs a) {
+  __shared__ uint8_t vis[kBwdThreads];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t q0 = int64_t(blockIdx.x) * kBwdThreads;
+  const int64_t q1 = q0 + kBwdThreads < a.m ? q0 + kBwdThreads : a.m;  // this CTA's slice of cval
+  if (!a.accumulate) {
+    const int64_t start = q0 == 0 ? 0 : int64_t(a.cval[q0 - 1]) + 1;
+    const int64_t end = q1 >= a.m ? a.n : int64_t(a.cval[q1 - 1]) + 1;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (a.aligned16) {
-      float4* sh4 = reinterpret_cast<float4*>(a.d_sh + 48 * g0);
-      for (int f = tid; f < nloc * 12; f += kBwdThreads)
-        if (!vis[f / 12]) sh4[f] = z;
-      float4* rt4 = reinterpret_cast<float4*>(a.d_rotations + 4 * g0);
-      for (int f = tid; f < nloc; f += kBwdThreads)
-        if (!vis[f]) rt4[f] = z;
-    } else {
-      for (int f = tid; f < nloc * 48; f += kBwdThreads)
-        if (!vis[f / 48]) a.d_sh[48 * g0 + f] = 0.f;
-      for (int f = tid; f < nloc * 4; f += kBwdThreads)
-        if (!vis[f / 4]) a.d_rotations[4 * g0 + f] = 0.f;
-    }
-    for (int f = tid; f < nloc; f += kBwdThreads)
-      if (!vis[f]) a.d_opacity[g0 + f] = 0.f;
-    for (int f = tid; f < nloc * 3; f += kBwdThreads)
-      if (!vis[f / 3]) {
-        a.d_means[3 * g0 + f] = 0.f;
-        a.d_log_scales[3 * g0 + f] = 0.f;
+    for (int64_t c0 = start; c0 < end; c0 += kBwdThreads) {  // 128-row chunks
+      const int nloc = static_cast<int>(end - c0 < kBwdThreads ? end - c0 : kBwdThreads);
+      __syncthreads();
+      vis[tid] = tid < nloc && __ldg(a.touched + c0 + tid) > 0u;
+      __syncthreads();
+      if (a.aligned16) {
+        float4* sh4 = reinterpret_cast<float4*>(a.d_sh + 48 * c0);
+        for (int f = tid; f < nloc * 12; f += kBwdThreads)
+          if (!vis[f / 12]) sh4[f] = z;
+        if (tid < nloc && !vis[tid]) reinterpret_cast<float4*>(a.d_rotations + 4 * c0)[tid] = z;
+      } else {
+        for (int f = tid; f < nloc * 48; f += kBwdThreads)
+          if (!vis[f / 48]) a.d_sh[48 * c0 + f] = 0.f;
+        for (int f = tid; f < nloc * 4; f += kBwdThreads)
+          if (!vis[f / 4]) a.d_rotations[4 * c0 + f] = 0.f;
       }
+      if (tid < nloc && !vis[tid]) a.d_opacity[c0 + tid] = 0.f;
+      for (int f = tid; f < nloc * 3; f += kBwdThreads)
+        if (!vis[f / 3]) {
+          a.d_means[3 * c0 + f] = 0.f;
+          a.d_log_scales[3 * c0 + f] = 0.f;
+        }
+    }
   }
+  if (q0 + (tid & ~31) >= q1) return;  // warp past the end of the list
+  const bool valid = q0 + tid < q1;
   {
-    // warps past the queue's end have nothing left to do (their range rows are written)
-    if ((tid & ~31) >= count) return;
-    const bool valid = tid < count;
-    const int64_t i = g0 + (valid ? queue[tid] : queue[0]);
+    const int64_t i = a.cval[valid ? q0 + tid : q0];
     // Gaussians with more than 32 tiles are summed by the whole warp (lane-strided, fixed
     // shuffle tree): deterministic, and no lane walks thousands of tiles alone.
     float sg[9];
