@@ -16,7 +16,7 @@ METRICS = [
     ("gpu__time_duration.sum", "time"),
     ("dram__bytes_read.sum", "dram_read"),
     ("dram__bytes_write.sum", "dram_write"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_%peak"),
+    ("dram__bytes.sum.per_second", "dram_bw"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_%peak"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_%"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy_%"),
@@ -52,7 +52,9 @@ def load(rep):
     hdr, units, data = rows[0], rows[1], rows[2:]
     res = []
     for r in data:
-        d = {"kernel": r[hdr.index("Kernel Name")].split("(")[0].replace("fgs::", "").replace("<unnamed>::", "")}
+        name = r[hdr.index("Kernel Name")].split("(")[0]
+        d = {"kernel": name.replace("void ", "").replace("fgs::", "").replace("(anonymous namespace)::", "")
+             .replace("<unnamed>::", "").replace("unnamed>::", "")}
         for m, key in METRICS:
             if m not in hdr:
                 continue
@@ -60,8 +62,10 @@ def load(rep):
             v = r[i].replace(",", "")
             if key == "time":
                 d[key] = to_us(v, units[i])
-            elif key.startswith("dram_") and "%" not in key:
+            elif key in ("dram_read", "dram_write"):
                 d[key] = to_bytes(v, units[i])
+            elif key == "dram_bw":
+                d[key] = to_bytes(v, units[i].replace("/second", "").replace("/s", "")) / 1e9  # GB/s
             else:
                 try:
                     d[key] = float(v)
@@ -75,11 +79,11 @@ def main(rep, md_out):
     ks = load(rep)
     lines = [f"# ncu --set full summary ({os.path.basename(rep)})", "",
              "Cold-cache, serialised replay (ncu); use for traffic and the kernel mix, not absolute speed.", "",
-             "| kernel | us | DRAM read MB | DRAM write MB | DRAM %peak | SM %peak | issue % | occupancy % | regs | grid x block |",
+             "| kernel | us | DRAM read MB | DRAM write MB | DRAM GB/s | SM %peak | issue % | occupancy % | regs | grid x block |",
              "|---|---|---|---|---|---|---|---|---|---|"]
     for d in ks:
         lines.append(f"| {d['kernel']} | {d.get('time', 0):.1f} | {d.get('dram_read', 0) / 1e6:.1f} | "
-                     f"{d.get('dram_write', 0) / 1e6:.1f} | {d.get('dram_%peak', 0):.1f} | {d.get('sm_%peak', 0):.1f} | "
+                     f"{d.get('dram_write', 0) / 1e6:.1f} | {d.get('dram_bw', 0):.0f} | {d.get('sm_%peak', 0):.1f} | "
                      f"{d.get('issue_%', 0):.1f} | {d.get('occupancy_%', 0):.1f} | {d.get('regs', 0):.0f} | "
                      f"{d.get('grid', 0):.0f} x {d.get('block', 0):.0f} |")
     traffic = {}
