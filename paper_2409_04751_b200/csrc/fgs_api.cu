@@ -1,14 +1,15 @@
 // fgs_api.cu — the C ABI (include/fgs.h): context, device memory, stage orchestration.
 //
 // Forward (reference render, inc/splatting.hpp:330-374):
-//   K1 preprocess -> level-1 onesweep sort of Gaussians by depth key -> rank scan
-//   -> [one 8-byte D2H read of the intersection count + error flag]
-//   -> duplicate (depth-rank order) -> level-2 onesweep sort by tile -> tile ranges -> K3 blend.
+//   K1 preprocess (+ per-tile counts) -> K2a scan: emission offsets, I, tile ranges, schedule
+//   -> [one 32-byte D2H read of the intersection count + error flag]
+//   -> K2b key scatter into tile ranges -> K2c per-tile sort -> K3 blend.
 // Backward (reference backward, inc/gradients.hpp:207-267):
 //   K4a reverse blend (per-intersection partials) -> K4b preprocess backward.
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -54,20 +55,25 @@ struct fgs_context {
   // per Gaussian
   DevBuf<fgs::SortedRec> rec;
   DevBuf<uint8_t> state;
-  DevBuf<uint32_t> dkey, ckey, cval, dkey_a, dkey_b, perm_a, perm_b, touched, rank, offsets, scan_status;
+  DevBuf<uint32_t> dkey, cval, coff, touched, scan_status;
   DevBuf<ushort4> rect;
   DevBuf<int32_t> radii;
   // per intersection
-  DevBuf<uint32_t> tkey, emit, tkey_a, tkey_b, emit_a, emit_b, emit_gauss, sorted_gauss, sorted_emit_buf;
+  DevBuf<uint64_t> keys;
+  DevBuf<uint32_t> emit_gauss, sorted_gauss, emit_pos;
   DevBuf<fgs::SortedRec> sorted_rec;
-  DevBuf<float> partials, partial_tile;
+  DevBuf<float> partials;
   // per tile / pixel
-  DevBuf<uint32_t> tile_offsets, last, tile_order;
+  DevBuf<uint32_t> tile_offsets, fill, last, tile_order;
+  DevBuf<int32_t> rowdiff;  // zero between frames (K2a zeroes what K1 added)
+  size_t rowdiff_clean = 0; // entries known to be zero
+  int64_t isect_cap = 0;    // capacity of the per-intersection buffers
+  cudaEvent_t ev_scan = nullptr;  // after K2a's scalars reached the host
   DevBuf<float> final_T;
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
   DevBuf<uint32_t> scalars;
-  DevBuf<unsigned long long> counters, tile_cycles, bin_trace;
+  DevBuf<unsigned long long> counters, tile_cycles;
   uint32_t* h_scalars = nullptr;  // pinned
   // host-call staging
   DevBuf<float> h_means, h_rot, h_ls, h_op, h_sh, h_img, h_dl, h_grad;
@@ -94,9 +100,6 @@ struct fgs_context {
   int64_t num_isect = 0;
   int64_t num_compact = 0;  // Gaussians touching >= 1 tile (rows the backward computes)
   uint32_t num_splats = 0, num_degenerate = 0, num_culled = 0;
-  uint32_t* perm = nullptr;          // level-1 result values
-  uint32_t* sorted_tiles = nullptr;  // level-2 result keys
-  uint32_t* sorted_emit = nullptr;   // level-2 result values
   size_t aux_bytes = 0;
   int px_per_lane = 1;  // tuning knob: FGS_PX_PER_LANE env (1 or 2)
   int gather_records = 0;  // FGS_GATHER_RECORDS=1: binning gathers records into sorted order
@@ -201,6 +204,7 @@ int fgs_create(int device, fgs_context** out) {
     return FGS_ECUDA;
   }
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  cudaEventCreateWithFlags(&ctx->ev_scan, cudaEventDisableTiming);
   if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(4) != cudaSuccess ||
       false) {
     fgs_destroy(ctx);
@@ -215,26 +219,26 @@ int fgs_destroy(fgs_context* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   else cudaDeviceSynchronize();
-  for (auto* b : {&ctx->final_T, &ctx->partials, &ctx->partial_tile, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
+  for (auto* b : {&ctx->final_T, &ctx->partials, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
                   &ctx->h_sh, &ctx->h_img, &ctx->h_dl, &ctx->h_grad})
     b->release();
   ctx->rec.release();
   ctx->state.release();
-  for (auto* b : {&ctx->dkey, &ctx->ckey, &ctx->cval, &ctx->dkey_a, &ctx->dkey_b, &ctx->perm_a, &ctx->perm_b,
-                  &ctx->touched, &ctx->rank, &ctx->offsets, &ctx->scan_status, &ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b,
-                  &ctx->emit_a, &ctx->emit_b, &ctx->emit_gauss, &ctx->sorted_gauss, &ctx->sorted_emit_buf,
-                  &ctx->tile_offsets, &ctx->last, &ctx->tile_order,
+  for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->touched, &ctx->scan_status, &ctx->emit_gauss,
+                  &ctx->sorted_gauss, &ctx->emit_pos, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
                   &ctx->scalars})
     b->release();
+  ctx->keys.release();
+  ctx->rowdiff.release();
   ctx->rect.release();
   ctx->radii.release();
   ctx->sorted_rec.release();
   ctx->h_radii.release();
   ctx->counters.release();
   ctx->tile_cycles.release();
-  ctx->bin_trace.release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
+  if (ctx->ev_scan) cudaEventDestroy(ctx->ev_scan);
   for (auto* v : {&ctx->pending, &ctx->spare})
     for (auto& es : *v)
       for (auto& e : es.e) cudaEventDestroy(e);
@@ -297,13 +301,19 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   const size_t npix = static_cast<size_t>(W) * H;
   FGS_CHECK(ctx->rec.ensure(nn));
   FGS_CHECK(ctx->state.ensure(nn));
-  for (auto* b : {&ctx->dkey, &ctx->ckey, &ctx->cval, &ctx->dkey_a, &ctx->dkey_b, &ctx->perm_a, &ctx->perm_b,
-                  &ctx->touched, &ctx->rank, &ctx->offsets})
-    FGS_CHECK(b->ensure(nn));
+  for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->touched}) FGS_CHECK(b->ensure(nn));
   FGS_CHECK(ctx->scan_status.ensure(fgs::bin_part_words()));
   FGS_CHECK(ctx->rect.ensure(nn));
   FGS_CHECK(ctx->radii.ensure(nn));
   FGS_CHECK(ctx->tile_offsets.ensure(num_tiles + 1));
+  FGS_CHECK(ctx->fill.ensure(num_tiles));
+  FGS_CHECK(ctx->tile_order.ensure(num_tiles));
+  const size_t ndiff = static_cast<size_t>(tiles_x + 1) * tiles_y;
+  if (ctx->rowdiff.cap < ndiff || ctx->rowdiff_clean < ndiff) {
+    FGS_CHECK(ctx->rowdiff.ensure(ndiff));
+    FGS_CHECK(cudaMemsetAsync(ctx->rowdiff.p, 0, ctx->rowdiff.cap * sizeof(int32_t), ctx->stream));
+    ctx->rowdiff_clean = ctx->rowdiff.cap;
+  }
   FGS_CHECK(ctx->last.ensure(npix));
   FGS_CHECK(ctx->final_T.ensure(npix));
 
@@ -341,94 +351,54 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.touched = ctx->touched.p;
     pa.rect = ctx->rect.p;
     pa.radii = ctx->radii.p;
+    pa.rowdiff = ctx->rowdiff.p;
     pa.error_flag = reinterpret_cast<int*>(ctx->scalars.p + 1);
     pa.state_counts = ctx->scalars.p + 2;
     fgs::preprocess_kernel<<<fgs::div_up(static_cast<int>(n), 256), 256, 0, st>>>(pa);
     ++launches;
   }
   if (timing) cudaEventRecord(ev[1], st);
-  // K2 level 1 (one persistent kernel): compact the Gaussians that touch a tile, sort them
-  // by depth key (stable; ties keep source order), scan their tile counts in depth order
+  // K2a (one persistent kernel): emission offsets of the tile-touching Gaussians, I, tile
+  // ranges from K1's per-tile counts, blend schedule
   fgs::BinArgs bn{};
   bn.n = static_cast<int>(n);
   bn.tiles_x = tiles_x;
+  bn.tiles_y = tiles_y;
   bn.num_tiles = num_tiles;
-  bn.passes2 = num_tiles <= 256 ? 1 : 2;
   bn.touched = ctx->touched.p;
-  bn.depth_key_in = ctx->dkey.p;
+  bn.depth_key = ctx->dkey.p;
   bn.rect = ctx->rect.p;
-  bn.ckey = ctx->ckey.p;
+  bn.rowdiff = ctx->rowdiff.p;
   bn.cval = ctx->cval.p;
-  bn.key_a = ctx->dkey_a.p;
-  bn.val_a = ctx->perm_a.p;
-  bn.key_b = ctx->dkey_b.p;
-  bn.val_b = ctx->perm_b.p;
-  bn.offsets = ctx->offsets.p;
-  bn.rank = ctx->rank.p;
+  bn.coff = ctx->coff.p;
   bn.scalars = ctx->scalars.p;
   bn.part_scan = ctx->scan_status.p;
-  bn.part_radix = ctx->scan_status.p + 256;
-  ctx->perm = ctx->perm_b.p;
-  if (ctx->flags & FGS_FLAG_COUNTERS) {
-    FGS_CHECK(ctx->bin_trace.ensure(32));
-    FGS_CHECK(cudaMemsetAsync(ctx->bin_trace.p, 0, 32 * sizeof(unsigned long long), st));
-    bn.trace = ctx->bin_trace.p;
-  }
+  bn.tile_offsets = ctx->tile_offsets.p;
+  bn.fill = ctx->fill.p;
+  bn.tile_order = ctx->tile_order.p;
   if (n > 0) {
-    FGS_CHECK(fgs::bin_level1(bn, st));
+    ctx->rowdiff_clean = 0;  // dirty until K2a has consumed K1's counts
+    FGS_CHECK(fgs::bin_scan(bn, st));
+    ctx->rowdiff_clean = ndiff;
     ++launches;
+  } else {
+    FGS_CHECK(cudaMemsetAsync(ctx->tile_offsets.p, 0, sizeof(uint32_t) * (num_tiles + 1), st));
   }
   FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, ctx->scalars.p, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  FGS_CHECK(cudaStreamSynchronize(st));
-  FGS_CHECK(cudaGetLastError());
-  if (ctx->h_scalars[fgs::kScalarErr]) return fail(ctx, FGS_EDEGENERATE_QUAT, "degenerate rotation: quaternion has zero norm");
-  const int64_t I = ctx->h_scalars[fgs::kScalarI];
-  ctx->num_isect = I;
-  ctx->num_compact = ctx->h_scalars[fgs::kScalarM];
-  ctx->num_splats = ctx->h_scalars[fgs::kScalarKept];
-  ctx->num_degenerate = ctx->h_scalars[fgs::kScalarDegen];
-  ctx->num_culled = static_cast<uint32_t>(n) - ctx->num_splats - ctx->num_degenerate;
-  if (I >= (int64_t(1) << 30)) return fail(ctx, FGS_ENOMEM, "forward: intersection count exceeds 2^30");
+  FGS_CHECK(cudaEventRecord(ctx->ev_scan, st));
   if (timing) cudaEventRecord(ev[2], st);
 
-  // K2 level 2 (one persistent kernel): duplicate in depth-rank order, stable sort by tile,
-  // per-tile ranges
-  const size_t ni = static_cast<size_t>(I > 0 ? I : 1);
-  for (auto* b : {&ctx->tkey, &ctx->emit, &ctx->tkey_a, &ctx->tkey_b, &ctx->emit_a, &ctx->emit_b, &ctx->emit_gauss,
-                  &ctx->sorted_gauss, &ctx->sorted_emit_buf})
-    FGS_CHECK(b->ensure(ni));
-  bn.num_isect = static_cast<int>(I);
-  bn.tkey = ctx->tkey.p;
-  bn.emit = ctx->emit.p;
-  bn.emit_gauss = ctx->emit_gauss.p;
-  bn.tkey_a = ctx->tkey_a.p;
-  bn.emit_a = ctx->emit_a.p;
-  bn.tkey_b = ctx->tkey_b.p;
-  bn.emit_b = ctx->emit_b.p;
-  bn.tile_offsets = ctx->tile_offsets.p;
-  bn.sorted_gauss = ctx->sorted_gauss.p;
-  bn.sorted_emit = ctx->sorted_emit_buf.p;
-  if (ctx->gather_records) FGS_CHECK(ctx->sorted_rec.ensure(ni));
-  bn.rec = ctx->rec.p;
-  bn.sorted_rec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
-  FGS_CHECK(ctx->tile_order.ensure(num_tiles));
-  bn.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
-  FGS_CHECK(fgs::bin_level2(bn, st));
-  if (I > 0) ++launches;
-  ctx->sorted_tiles = bn.passes2 == 1 ? ctx->tkey_a.p : ctx->tkey_b.p;
-  ctx->sorted_emit = ctx->sorted_emit_buf.p;
-  ctx->bin_args = bn;
-  if (timing) cudaEventRecord(ev[3], st);
-
+  // K2b + K2c (scatter the (depth, emission slot) keys into their tile ranges, sort per tile)
+  // and K3 (blend). They are launched before the host knows I, against the capacity of the
+  // per-intersection buffers, so the GPU never waits for the host: every kernel reads I from
+  // the device and exits at once if it exceeds the capacity, in which case the host grows the
+  // buffers and launches them again (first frames, growing scenes).
   fgs::BlendArgs ba{};
   ba.width = W;
   ba.height = H;
   ba.tiles_x = tiles_x;
   ba.tiles_y = tiles_y;
   ba.tile_offsets = ctx->tile_offsets.p;
-  ba.sorted_gauss = ctx->sorted_gauss.p;
-  ba.sorted_emit = ctx->sorted_emit;
-  ba.srec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
   ba.rec = ctx->rec.p;
   for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
   ba.image = image;
@@ -436,19 +406,71 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ba.last = ctx->last.p;
   ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
   ba.px_per_lane = ctx->px_per_lane;
-  ba.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
+  ba.tile_order = n > 0 ? ctx->tile_order.p : nullptr;
+  ba.scalars = ctx->scalars.p;
   if (ba.counters) {
     FGS_CHECK(ctx->tile_cycles.ensure(num_tiles));
     FGS_CHECK(cudaMemsetAsync(ctx->tile_cycles.p, 0, num_tiles * sizeof(unsigned long long), st));
     ba.tile_cycles = ctx->tile_cycles.p;
   }
-  launches += fgs::blend_forward(ba, st);
-  if (timing) cudaEventRecord(ev[4], st);
+  auto launch_rest = [&](int n_big) -> int {
+    bn.isect_cap = ctx->isect_cap;
+    bn.keys = ctx->keys.p;
+    bn.emit_gauss = ctx->emit_gauss.p;
+    bn.sorted_gauss = ctx->sorted_gauss.p;
+    bn.emit_pos = ctx->emit_pos.p;
+    bn.rec = ctx->rec.p;
+    bn.sorted_rec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
+    int l = fgs::bin_sort(bn, n_big, st);
+    if (timing) cudaEventRecord(ev[3], st);
+    ba.isect_cap = ctx->isect_cap;
+    ba.sorted_gauss = ctx->sorted_gauss.p;
+    ba.srec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
+    l += fgs::blend_forward(ba, st);
+    if (timing) cudaEventRecord(ev[4], st);
+    return l;
+  };
+  const bool speculative = n > 0 && ctx->isect_cap > 0;
+  if (speculative) launches += launch_rest(-1);
+
+  FGS_CHECK(cudaEventSynchronize(ctx->ev_scan));
+  FGS_CHECK(cudaGetLastError());
+  if (ctx->h_scalars[fgs::kScalarErr]) return fail(ctx, FGS_EDEGENERATE_QUAT, "degenerate rotation: quaternion has zero norm");
+  const int64_t I = ctx->h_scalars[fgs::kScalarI];
+  if (n > 0 && ctx->h_scalars[fgs::kScalarI2] != ctx->h_scalars[fgs::kScalarI])
+    return fail(ctx, FGS_ECUDA, "forward: per-tile counts disagree with the intersection scan");
+  ctx->num_isect = I;
+  ctx->num_compact = ctx->h_scalars[fgs::kScalarM];
+  ctx->num_splats = ctx->h_scalars[fgs::kScalarKept];
+  ctx->num_degenerate = ctx->h_scalars[fgs::kScalarDegen];
+  ctx->num_culled = static_cast<uint32_t>(n) - ctx->num_splats - ctx->num_degenerate;
+  if (I >= (int64_t(1) << 30)) return fail(ctx, FGS_ENOMEM, "forward: intersection count exceeds 2^30");
+  if (!speculative || I > ctx->isect_cap) {
+    // (re)size the per-intersection buffers (cudaFree / cudaMalloc synchronise with the
+    // speculative kernels, which exited without work) and launch for real
+    const size_t ni = static_cast<size_t>(I > 0 ? I : 1);
+    FGS_CHECK(ctx->keys.ensure(ni));
+    for (auto* b : {&ctx->emit_gauss, &ctx->sorted_gauss, &ctx->emit_pos}) FGS_CHECK(b->ensure(ni));
+    size_t cap = ctx->keys.cap;
+    for (auto* b : {&ctx->emit_gauss, &ctx->sorted_gauss, &ctx->emit_pos}) cap = std::min(cap, b->cap);
+    if (ctx->gather_records) {
+      FGS_CHECK(ctx->sorted_rec.ensure(ni));
+      cap = std::min(cap, ctx->sorted_rec.cap);
+    }
+    ctx->isect_cap = static_cast<int64_t>(cap);
+    if (n > 0) launches += launch_rest(static_cast<int>(ctx->h_scalars[fgs::kScalarBig]));
+    else {
+      if (timing) cudaEventRecord(ev[3], st);
+      launches += fgs::blend_forward(ba, st);
+      if (timing) cudaEventRecord(ev[4], st);
+    }
+  }
+  ctx->bin_args = bn;
   if (radii && n > 0) FGS_CHECK(cudaMemcpyAsync(radii, ctx->radii.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
   FGS_CHECK(cudaGetLastError());
   ctx->launches += launches;
 
-  ctx->aux_bytes = nn * (16 + 16 + 4 + 1 + 4 * 9 + 8 + 4) + ni * 4 * 8 + (num_tiles + 1) * 4 + npix * 8;
+  ctx->aux_bytes = nn * (48 + 1 + 4 * 5 + 8) + static_cast<size_t>(std::max<int64_t>(ctx->isect_cap, 1)) * (8 + 4 * 3) + (num_tiles + 1) * 4 * 3 + ndiff * 4 + npix * 8;
   ctx->have_fwd = true;
   if (stats) {
     FGS_CHECK(cudaEventSynchronize(ev[4]));
@@ -484,7 +506,6 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   const int64_t n = ctx->n, I = ctx->num_isect;
   if (n == 0) return FGS_OK;
   FGS_CHECK(ctx->partials.ensure(static_cast<size_t>(I > 0 ? I : 1) * fgs::kBwdWarps * 9));
-  FGS_CHECK(ctx->partial_tile.ensure(static_cast<size_t>(I > 0 ? I : 1) * 9));
 
   fgs::BlendArgs ba{};
   ba.width = ctx->cam.width;
@@ -493,7 +514,6 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   ba.tiles_y = ctx->tiles_y;
   ba.tile_offsets = ctx->tile_offsets.p;
   ba.sorted_gauss = ctx->sorted_gauss.p;
-  ba.sorted_emit = ctx->sorted_emit;
   ba.srec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
   ba.rec = ctx->rec.p;
   for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
@@ -507,8 +527,6 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   cudaEvent_t* ev = timing ? take_set(ctx, 1)->e : nullptr;
   if (timing) cudaEventRecord(ev[0], st);
   if (I > 0) ctx->launches += fgs::blend_backward(ba, st);
-  ctx->launches += fgs::combine_partials(ctx->tkey.p, ctx->emit_gauss.p, ctx->rec.p, ctx->partials.p,
-                                         ctx->partial_tile.p, ctx->tiles_x, static_cast<int>(I), st);
   if (timing) cudaEventRecord(ev[1], st);
 
   fgs::PreprocessBackwardArgs pb{};
@@ -526,9 +544,10 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.sh = scene->sh;
   pb.state = ctx->state.p;
   pb.touched = ctx->touched.p;
-  pb.rank = ctx->rank.p;
-  pb.offsets = ctx->offsets.p;
-  pb.partials = ctx->partial_tile.p;
+  pb.coff = ctx->coff.p;
+  pb.rect = ctx->rect.p;
+  pb.emit_pos = ctx->emit_pos.p;
+  pb.partials = ctx->partials.p;
   pb.d_means = grads->d_means;
   pb.d_rotations = grads->d_rotations;
   pb.d_log_scales = grads->d_log_scales;
@@ -673,18 +692,27 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   if (nm == "depth_key") return copy(ctx->dkey.p, n * 4);
   if (nm == "radius") return copy(ctx->radii.p, n * 4);
   if (nm == "touched") return copy(ctx->touched.p, n * 4);
-  if (nm == "perm") return copy(ctx->perm, n * 4);
-  if (nm == "rank") return copy(ctx->rank.p, n * 4);
-  if (nm == "rank_offsets") return copy(ctx->offsets.p, n * 4);
   if (nm == "sorted_gauss") return copy(ctx->sorted_gauss.p, I * 4);
-  if (nm == "sorted_tile") return copy(ctx->sorted_tiles, I * 4);
-  if (nm == "sorted_emit") return copy(ctx->sorted_emit, I * 4);
+  if (nm == "emit_pos") return copy(ctx->emit_pos.p, I * 4);
+  if (nm == "compact_gauss") return copy(ctx->cval.p, static_cast<size_t>(ctx->num_compact) * 4);
+  if (nm == "compact_offsets") return copy(ctx->coff.p, static_cast<size_t>(ctx->num_compact) * 4);
+  if (nm == "sorted_tile") {
+    // tile id of every sorted entry, expanded from the tile ranges
+    if (!dst) return static_cast<int64_t>(I * 4);
+    if (static_cast<int64_t>(I * 4) > dst_bytes) return -1;
+    std::vector<uint32_t> off(nt + 1);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return -1;
+    if (cudaMemcpy(off.data(), ctx->tile_offsets.p, (nt + 1) * 4, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    auto* out = static_cast<uint32_t*>(dst);
+    for (size_t t = 0; t < nt; ++t)
+      for (uint32_t k = off[t]; k < off[t + 1] && k < I; ++k) out[k] = static_cast<uint32_t>(t);
+    return static_cast<int64_t>(I * 4);
+  }
   if (nm == "offsets") return copy(ctx->tile_offsets.p, (nt + 1) * 4);
   if (nm == "final_T") return copy(ctx->final_T.p, npix * 4);
   if (nm == "last") return copy(ctx->last.p, npix * 4);
   if (nm == "counters") return copy(ctx->counters.p, 4 * sizeof(unsigned long long));
   if (nm == "tile_cycles") return copy(ctx->tile_cycles.p, nt * sizeof(unsigned long long));
-  if (nm == "bin_trace") return copy(ctx->bin_trace.p, 32 * sizeof(unsigned long long));
   if (nm == "key_tile" || nm == "key_depth" || nm == "key_gauss") {
     if (!dst) return static_cast<int64_t>(I * 4);
     // Recompute the reference's pre-sort emission order (source order) on demand.

@@ -24,6 +24,7 @@ struct PreprocessArgs {
   uint32_t* touched;     // tiles touched
   ushort4* rect;         // tx0, tx1, ty0, ty1
   int32_t* radii;        // per Gaussian radius (0 = culled / degenerate)
+  int32_t* rowdiff;      // tiles_y x (tiles_x + 1) row-difference tile counts
   int* error_flag;
   uint32_t* state_counts;  // [kept, degenerate]
 };
@@ -46,9 +47,10 @@ struct PreprocessBackwardArgs {
   const float* sh;
   const uint8_t* state;
   const uint32_t* touched;
-  const uint32_t* rank;
-  const uint32_t* offsets;   // per depth rank
-  const float* partials;     // I x 9 per-intersection sums (K4c output)
+  const uint32_t* coff;      // [m] first emission slot of cval[q]
+  const ushort4* rect;       // [n] tile rectangles (K1)
+  const uint32_t* emit_pos;  // [I] sorted position of each emission slot
+  const float* partials;     // [I][8][9] K4a per-(intersection, block) sums, sorted order
   float* d_means;
   float* d_rotations;
   float* d_log_scales;
@@ -61,7 +63,6 @@ struct BlendArgs {
   int width, height, tiles_x, tiles_y;
   const uint32_t* tile_offsets;  // T+1
   const uint32_t* sorted_gauss;  // I
-  const uint32_t* sorted_emit;   // I (emission slot of each sorted entry; backward partials)
   const SortedRec* srec;         // I records in sorted order (nullptr: read rec[sorted_gauss[k]])
   const SortedRec* rec;          // per-Gaussian records
   float bg[3];
@@ -72,6 +73,8 @@ struct BlendArgs {
   unsigned long long* tile_cycles;  // optional (with counters): per-tile CTA cycles
   const uint32_t* tile_order;    // optional: CTA -> tile (heaviest lists first)
   int px_per_lane;               // forward blend: 1 or 2 pixels per lane
+  const uint32_t* scalars;       // forward: device scalars; exit if I > isect_cap (speculative launch)
+  int64_t isect_cap;
   // backward
   const float* dl_dimage;
   float* partials;               // I x 8 x 9
@@ -83,49 +86,40 @@ constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per 
 
 // ---- binning / sorting (binning.cu) ----
 constexpr int kBinThreads = 1024;
-constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, kScalarM = 4;
+constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, kScalarM = 4, kScalarI2 = 5, kScalarBig = 6;
 
 struct BinArgs {
   int n;                       // Gaussians
-  int tiles_x, num_tiles, passes2;
-  int num_isect;               // I (level 2 only; known on the host after level 1)
-  const uint32_t* touched;     // [n]
-  const uint32_t* depth_key_in;  // [n]
-  const ushort4* rect;         // [n]
-  uint32_t* ckey;              // compacted depth keys [n]
-  uint32_t* cval;              // compacted Gaussian ids [n]
-  uint32_t* key_a;             // ping-pong [n]
-  uint32_t* val_a;
-  uint32_t* key_b;
-  uint32_t* val_b;             // level-1 result: Gaussian ids by depth rank
-  uint32_t* offsets;           // [n] emission offset per depth rank
-  uint32_t* rank;              // [n] depth rank per Gaussian
+  int tiles_x, tiles_y, num_tiles;
+  int64_t isect_cap;           // capacity of the per-intersection buffers (scatter/sort exit if I exceeds it)
+  const uint32_t* touched;     // [n] tiles touched per Gaussian (K1)
+  const uint32_t* depth_key;   // [n] depth key bits (K1)
+  const ushort4* rect;         // [n] tile rectangle (K1)
+  int32_t* rowdiff;            // [tiles_y * (tiles_x + 1)] row-difference tile counts (K1 adds, bin_scan zeroes)
+  uint32_t* cval;              // [n] tile-touching Gaussians in source order (compacted)
+  uint32_t* coff;              // [n] their first emission slot
   uint32_t* scalars;           // device scalars (kScalar*)
-  uint32_t* part_scan;         // [grid]
-  uint32_t* part_radix;        // [grid * 256]
-  // level 2
-  uint32_t* tkey;              // [I] tile keys (emission order)
-  uint32_t* emit;              // [I] emission slots
-  uint32_t* emit_gauss;        // [I] Gaussian of each emission slot
-  uint32_t* tkey_a;
-  uint32_t* emit_a;
-  uint32_t* tkey_b;
-  uint32_t* emit_b;
+  uint32_t* part_scan;         // [2 * grid]
   uint32_t* tile_offsets;      // [num_tiles + 1]
-  uint32_t* sorted_gauss;      // [I]
-  uint32_t* sorted_emit;       // [I]
-  const SortedRec* rec;        // per-Gaussian splat records (K1 output)
-  SortedRec* sorted_rec;       // [I] records in sorted order
+  uint32_t* fill;              // [num_tiles] scatter cursors
   uint32_t* tile_order;        // [num_tiles] blend schedule (optional)
-  unsigned long long* trace;   // debug phase timestamps (optional)
+  // per intersection
+  uint64_t* keys;              // [I] (depth_key << 32 | emission slot), grouped by tile
+  uint32_t* emit_gauss;        // [I] Gaussian of each emission slot
+  uint32_t* sorted_gauss;      // [I]
+  uint32_t* emit_pos;          // [I] sorted position of each emission slot
+  const SortedRec* rec;        // per-Gaussian splat records (K1 output)
+  SortedRec* sorted_rec;       // [I] records in sorted order (optional)
 };
 
-// Words of part_scan + part_radix scratch the persistent kernels need.
+// Words of part_scan scratch bin_scan needs.
 size_t bin_part_words();
-// Compaction + level-1 sort + rank scan (writes scalars[kScalarM], scalars[kScalarI]).
-cudaError_t bin_level1(BinArgs& a, cudaStream_t st);
-// Duplication + level-2 sort + tile ranges (needs a.num_isect).
-cudaError_t bin_level2(BinArgs& a, cudaStream_t st);
+// K2a: compaction + emission offsets + I (scalars), tile ranges + blend schedule.
+cudaError_t bin_scan(BinArgs& a, cudaStream_t st);
+// K2b + K2c: key scatter into tile ranges, per-tile sort; returns launches. The kernels read
+// I and the big-tile count from the device scalars and do nothing if I > a.isect_cap; n_big
+// < 0 (unknown on the host) sizes the sort grid for the worst case.
+int bin_sort(BinArgs& a, int n_big, cudaStream_t st);
 // Debug: the reference's pre-sort key list (source order).
 cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* key_depth, uint32_t* key_gauss,
                                     cudaStream_t st);
@@ -133,9 +127,6 @@ cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* ke
 // ---- blend (raster.cu) ----
 int blend_forward(const BlendArgs& a, cudaStream_t st);
 int blend_backward(const BlendArgs& a, cudaStream_t st);
-// K4c: per intersection, sum the per-block partials of the blocks passing the culling test.
-int combine_partials(const uint32_t* tile_keys, const uint32_t* emit_gauss, const SortedRec* rec,
-                     const float* partials, float* partial_tile, int tiles_x, int ni, cudaStream_t st);
 // FP32 pipe probe: returns achieved non-FMA fp32 op/s (FMUL + FADD, no contraction).
 double fp32_peak_probe(cudaStream_t st);
 

@@ -348,6 +348,12 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
       if (tx1 >= tx0 && ty1 >= ty0) {
         touched = static_cast<uint32_t>((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
         rect = make_ushort4(tx0, tx1, ty0, ty1);
+        // per-tile counts for K2a: +1 / -1 at both ends of every covered row
+        const int rw = a.tiles_x + 1;
+        for (int ty = ty0; ty <= ty1; ++ty) {
+          atomicAdd(a.rowdiff + ty * rw + tx0, 1);
+          atomicAdd(a.rowdiff + ty * rw + tx1 + 1, -1);
+        }
       }
     }
   }
@@ -580,14 +586,38 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
   }
 }
 
-// K4b: one thread per Gaussian that touched a tile, taken in source order from the level-1
-// compaction list (cval), 128 per CTA. K4a/K4c left one 9-float partial per intersection at
-// the Gaussian's emission slots [offset[rank[g]], +touched[g]) (ascending tile order; within
-// a tile the 8 pixel blocks were added in fixed order), summed here in that order:
+// K4b: one thread per Gaussian that touched a tile, taken in source order from the K2a
+// compaction list (cval), 128 per CTA. K4a left 9-float partials per (intersection, pixel
+// block) at the intersection's sorted position; the Gaussian's emission slots
+// [coff[q], +touched[g]) (ascending tile order) map to those positions (emit_pos), and the
+// partials are summed here in (tile, block) order:
 // deterministic, no atomics (gradients.hpp:161-173). Gaussians that touched no tile have zero
 // gradient; CTA b also zero-fills, with coalesced stores, the non-touching rows between its
 // predecessor's last Gaussian and its own last one -- so every sector of that source range
 // is written by one CTA in a short window and L2 merges the partial-sector writes.
+// One intersection's screen-space gradient (K4a's per-block partials at its sorted position,
+// blocks passing the culling test added in block order) added into acc: emission slot e is
+// the Gaussian's j-th tile of rect rc (ty-major, tx-minor); r0/r2 = its K1 record .a/.c.
+__device__ __forceinline__ void intersection_sum(const PreprocessBackwardArgs& a, uint32_t e, uint32_t j, ushort4 rc,
+                                                 float4 r0, float4 r2, float* acc) {
+  const int wx = rc.y - rc.x + 1;
+  const int tx = rc.x + static_cast<int>(j) % wx, ty = rc.z + static_cast<int>(j) / wx;
+  const float* p = a.partials + static_cast<size_t>(__ldg(a.emit_pos + e)) * (kBwdWarps * 9);
+  float sg[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) sg[q] = 0.0f;
+#pragma unroll
+  for (int w = 0; w < kBwdWarps; ++w) {
+    float x0, x1, y0, y1;
+    bwd_block_box(tx, ty, w, x0, x1, y0, y1);
+    if (!rec_hits(r0, r2, x0, x1, y0, y1)) continue;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) sg[q] = sg[q] + p[w * 9 + q];
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) acc[q] = acc[q] + sg[q];
+}
+
 constexpr int kBwdThreads = kPreprocessBackwardThreads;
 __global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(PreprocessBackwardArgs a) {
   __shared__ uint8_t vis[kBwdThreads];
@@ -632,32 +662,41 @@ __global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(Pre
 #pragma unroll
     for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
     const uint32_t cnt = valid ? a.touched[i] : 0u;
-    const uint32_t base = valid ? a.offsets[a.rank[i]] : 0u;
+    const uint32_t base = valid ? a.coff[q0 + tid] : 0u;
+    ushort4 rc = make_ushort4(0, 0, 0, 0);
+    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r2 = r0;
+    if (valid) {
+      rc = a.rect[i];
+      r0 = a.rec[i].a;
+      r2 = a.rec[i].c;
+    }
     const bool big = cnt > 32;
     if (!big)
-      for (uint32_t e = base; e < base + cnt; ++e) {
-        const float* p = a.partials + int64_t(e) * 9;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) sg[k] = sg[k] + p[k];
-      }
+      for (uint32_t j = 0; j < cnt; ++j) intersection_sum(a, base + j, j, rc, r0, r2, sg);
     uint32_t bigs = __ballot_sync(0xffffffffu, big);
     while (bigs) {
-      const int j = __ffs(bigs) - 1;
+      const int jl = __ffs(bigs) - 1;
       bigs &= bigs - 1;
-      const uint32_t bj = __shfl_sync(0xffffffffu, base, j), cj = __shfl_sync(0xffffffffu, cnt, j);
+      const uint32_t bj = __shfl_sync(0xffffffffu, base, jl), cj = __shfl_sync(0xffffffffu, cnt, jl);
+      ushort4 rj;
+      rj.x = __shfl_sync(0xffffffffu, rc.x, jl);
+      rj.y = __shfl_sync(0xffffffffu, rc.y, jl);
+      rj.z = __shfl_sync(0xffffffffu, rc.z, jl);
+      rj.w = __shfl_sync(0xffffffffu, rc.w, jl);
+      float4 a0, a2;
+      a0.x = __shfl_sync(0xffffffffu, r0.x, jl);
+      a0.y = __shfl_sync(0xffffffffu, r0.y, jl);
+      a2.y = __shfl_sync(0xffffffffu, r2.y, jl);
+      a2.z = __shfl_sync(0xffffffffu, r2.z, jl);
       float acc[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) acc[k] = 0.0f;
-      for (uint32_t e = bj + lane; e < bj + cj; e += 32) {
-        const float* p = a.partials + int64_t(e) * 9;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) acc[k] = acc[k] + p[k];
-      }
+      for (uint32_t j = lane; j < cj; j += 32) intersection_sum(a, bj + j, j, rj, a0, a2, acc);
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[k] = acc[k] + __shfl_xor_sync(0xffffffffu, acc[k], o);
-        if (lane == j) sg[k] = acc[k];
+        if (lane == jl) sg[k] = acc[k];
       }
     }
     if (valid) gaussian_backward(a, i, sg);

@@ -14,7 +14,7 @@
 // from the forward's final transmittance and last-contributor index, accumulates the suffix
 // colour, and produces per-(pixel, splat) gradients (mean_px 2, conic 3, colour 3, alpha 1).
 // They are summed over the tile's pixels in a fixed order (warp shuffle tree, then warps in
-// order) and written to the intersection's emission slot: no atomics, deterministic.
+// order) and written to the intersection's sorted position: no atomics, deterministic.
 
 #include <algorithm>
 
@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   __shared__ float4 s0[NW][32];
   __shared__ float4 s1[NW][32];
   __shared__ float s2[NW][32];
+  if (a.scalars && a.scalars[kScalarI] > a.isect_cap) return;  // speculative launch, buffers too small
   const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -233,14 +234,13 @@ __device__ __forceinline__ bool near_threshold(float ar) {
 // chunks, culls them against its block (rec_hits on the extent K1 stored), and for each surviving splat recovers
 // T_before = T_after / (1 - alpha), accumulates the suffix colour and forms the 9 per-pixel
 // gradients (mean_px 2, conic 3, colour 3, alpha_max 1), summed over the warp's 32 pixels by
-// a shuffle tree. The warp sum goes to partials[emit][w] -- one slot per (intersection, block)
+// a shuffle tree. The warp sum goes to partials[k][w] -- one slot per (intersection, block)
 // whose block passes the cull, zeros for passing splats past the warp's last contributor --
 // and K4b adds the passing slots in fixed (tile, block) order: deterministic, no atomics.
 __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
   __shared__ float4 s0[kBwdWarps][32];
   __shared__ float4 s1[kBwdWarps][32];
   __shared__ float s2[kBwdWarps][32];
-  __shared__ uint32_t se[kBwdWarps][32];
   const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     if (k < hi) {
       const SortedRec r = load_rec(a, k);
       if (rec_hits(r.a, r.c, bx0, bx1, by0, by1)) {
-        float* p = part + (static_cast<size_t>(a.sorted_emit[k]) * kBwdWarps + warp) * 9;
+        float* p = part + (static_cast<size_t>(k) * kBwdWarps + warp) * 9;
 #pragma unroll
         for (int q = 0; q < 9; ++q) p[q] = 0.0f;
       }
@@ -287,7 +287,6 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
       s0[warp][lane] = r.a;
       s1[warp][lane] = r.b;
       s2[warp][lane] = r.c.x;
-      se[warp][lane] = a.sorted_emit[k];
     }
     uint32_t mask = __ballot_sync(0xffffffffu, pass);
     __syncwarp();
@@ -380,50 +379,13 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
       // lane l now holds component l % 9 of splat l / 9 (l < 27)
       const int q = lane / 9;
       if (lane < 27 && js[q] >= 0)
-        part[(static_cast<size_t>(se[warp][js[q]]) * kBwdWarps + warp) * 9 + (lane - 9 * q)] = v[0];
+        part[(static_cast<size_t>(cstart + js[q]) * kBwdWarps + warp) * 9 + (lane - 9 * q)] = v[0];
     }
     __syncwarp();
   }
 }
 
-// K4c: for every intersection (emission slot e), add the per-block partials of the blocks
-// that passed the backward's culling test, in block order: partial_tile[e] (9 floats).
-__global__ void __launch_bounds__(256) combine_partials_kernel(const uint32_t* __restrict__ tile_keys,
-                                                               const uint32_t* __restrict__ emit_gauss,
-                                                               const SortedRec* __restrict__ rec,
-                                                               const float* __restrict__ partials,
-                                                               float* __restrict__ partial_tile, int tiles_x, int ni) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= ni) return;
-  const uint32_t t = __ldg(tile_keys + e), g = __ldg(emit_gauss + e);
-  const int tx = static_cast<int>(t) % tiles_x, ty = static_cast<int>(t) / tiles_x;
-  const float4 r0 = rec[g].a, r2 = rec[g].c;
-  float sg[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
-  const float* p = partials + static_cast<size_t>(e) * (kBwdWarps * 9);
-#pragma unroll
-  for (int w = 0; w < kBwdWarps; ++w) {
-    float x0, x1, y0, y1;
-    bwd_block_box(tx, ty, w, x0, x1, y0, y1);
-    if (!rec_hits(r0, r2, x0, x1, y0, y1)) continue;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) sg[k] = sg[k] + p[w * 9 + k];
-  }
-  float* o = partial_tile + static_cast<size_t>(e) * 9;
-#pragma unroll
-  for (int k = 0; k < 9; ++k) o[k] = sg[k];
-}
-
 }  // namespace
-
-int combine_partials(const uint32_t* tile_keys, const uint32_t* emit_gauss, const SortedRec* rec,
-                     const float* partials, float* partial_tile, int tiles_x, int ni, cudaStream_t st) {
-  if (ni <= 0) return 0;
-  combine_partials_kernel<<<div_up(ni, 256), 256, 0, st>>>(tile_keys, emit_gauss, rec, partials,
-                                                            partial_tile, tiles_x, ni);
-  return 1;
-}
 
 int blend_forward(const BlendArgs& a, cudaStream_t st) {
   const int px = a.px_per_lane == 2 ? 2 : 1;
