@@ -1,9 +1,9 @@
 // fgs_api.cu — the C ABI (include/fgs.h): context, device memory, stage orchestration.
 //
 // Forward (reference render, inc/splatting.hpp:330-374):
-//   K1 preprocess (+ per-tile counts) -> K2a scan: emission offsets, I, tile ranges, schedule
-//   -> [one 32-byte D2H read of the intersection count + error flag]
-//   -> K2b key scatter into tile ranges -> K2c per-tile sort -> K3 blend.
+//   K1 preprocess (+ per-tile counts) -> K2 (cooperative): emission offsets, I, tile ranges,
+//   schedule, key scatter into the tile ranges -> K3 per-tile sort + blend. The host reads I
+//   (32 bytes) after K2 while K3 already runs against the buffers' capacity.
 // Backward (reference backward, inc/gradients.hpp:207-267):
 //   K4a reverse blend (per-intersection partials) -> K4b preprocess backward.
 
@@ -61,8 +61,7 @@ struct fgs_context {
   // per intersection
   DevBuf<uint64_t> keys;
   DevBuf<uint32_t> emit_gauss, sorted_gauss, emit_pos;
-  DevBuf<fgs::SortedRec> sorted_rec;
-  DevBuf<float> partials;
+  DevBuf<float> partials, partial_tile;
   // per tile / pixel
   DevBuf<uint32_t> tile_offsets, fill, last, tile_order;
   DevBuf<int32_t> rowdiff;  // zero between frames (K2a zeroes what K1 added)
@@ -101,8 +100,6 @@ struct fgs_context {
   int64_t num_compact = 0;  // Gaussians touching >= 1 tile (rows the backward computes)
   uint32_t num_splats = 0, num_degenerate = 0, num_culled = 0;
   size_t aux_bytes = 0;
-  int px_per_lane = 1;  // tuning knob: FGS_PX_PER_LANE env (1 or 2)
-  int gather_records = 0;  // FGS_GATHER_RECORDS=1: binning gathers records into sorted order
   fgs::BinArgs bin_args{};
 };
 
@@ -196,8 +193,6 @@ int fgs_create(int device, fgs_context** out) {
   if (e != cudaSuccess) return FGS_ECUDA;
   auto* ctx = new fgs_context();
   ctx->device = device;
-  if (const char* v = std::getenv("FGS_PX_PER_LANE")) ctx->px_per_lane = std::atoi(v) == 2 ? 2 : 1;
-  if (const char* v = std::getenv("FGS_GATHER_RECORDS")) ctx->gather_records = std::atoi(v) != 0;
   e = cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
   if (e != cudaSuccess) {
     delete ctx;
@@ -219,7 +214,7 @@ int fgs_destroy(fgs_context* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   else cudaDeviceSynchronize();
-  for (auto* b : {&ctx->final_T, &ctx->partials, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
+  for (auto* b : {&ctx->final_T, &ctx->partials, &ctx->partial_tile, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
                   &ctx->h_sh, &ctx->h_img, &ctx->h_dl, &ctx->h_grad})
     b->release();
   ctx->rec.release();
@@ -232,7 +227,6 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->rowdiff.release();
   ctx->rect.release();
   ctx->radii.release();
-  ctx->sorted_rec.release();
   ctx->h_radii.release();
   ctx->counters.release();
   ctx->tile_cycles.release();
@@ -358,8 +352,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     ++launches;
   }
   if (timing) cudaEventRecord(ev[1], st);
-  // K2a (one persistent kernel): emission offsets of the tile-touching Gaussians, I, tile
-  // ranges from K1's per-tile counts, blend schedule
+  // K2 (one persistent cooperative kernel): emission offsets of the tile-touching Gaussians,
+  // I, tile ranges from K1's per-tile counts, blend schedule, key scatter into the ranges
   fgs::BinArgs bn{};
   bn.n = static_cast<int>(n);
   bn.tiles_x = tiles_x;
@@ -376,9 +370,12 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.tile_offsets = ctx->tile_offsets.p;
   bn.fill = ctx->fill.p;
   bn.tile_order = ctx->tile_order.p;
+  bn.isect_cap = ctx->isect_cap;
+  bn.keys = ctx->keys.p;
+  bn.emit_gauss = ctx->emit_gauss.p;
   if (n > 0) {
-    ctx->rowdiff_clean = 0;  // dirty until K2a has consumed K1's counts
-    FGS_CHECK(fgs::bin_scan(bn, st));
+    ctx->rowdiff_clean = 0;  // dirty until K2 has consumed K1's counts
+    FGS_CHECK(fgs::bin_launch(bn, st));
     ctx->rowdiff_clean = ndiff;
     ++launches;
   } else {
@@ -387,12 +384,13 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, ctx->scalars.p, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   FGS_CHECK(cudaEventRecord(ctx->ev_scan, st));
   if (timing) cudaEventRecord(ev[2], st);
+  if (timing) cudaEventRecord(ev[3], st);
 
-  // K2b + K2c (scatter the (depth, emission slot) keys into their tile ranges, sort per tile)
-  // and K3 (blend). They are launched before the host knows I, against the capacity of the
-  // per-intersection buffers, so the GPU never waits for the host: every kernel reads I from
-  // the device and exits at once if it exceeds the capacity, in which case the host grows the
-  // buffers and launches them again (first frames, growing scenes).
+  // K3 (sort each tile's list + blend) is launched before the host knows I, against the
+  // capacity of the per-intersection buffers, so the GPU never waits for the host: K2's scatter
+  // and K3 read I from the device and do nothing if it exceeds the capacity, in which case
+  // the host grows the buffers and launches the scatter and K3 again (first frames, growing
+  // scenes).
   fgs::BlendArgs ba{};
   ba.width = W;
   ba.height = H;
@@ -405,7 +403,6 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;
   ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
-  ba.px_per_lane = ctx->px_per_lane;
   ba.tile_order = n > 0 ? ctx->tile_order.p : nullptr;
   ba.scalars = ctx->scalars.p;
   if (ba.counters) {
@@ -413,25 +410,18 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     FGS_CHECK(cudaMemsetAsync(ctx->tile_cycles.p, 0, num_tiles * sizeof(unsigned long long), st));
     ba.tile_cycles = ctx->tile_cycles.p;
   }
-  auto launch_rest = [&](int n_big) -> int {
-    bn.isect_cap = ctx->isect_cap;
-    bn.keys = ctx->keys.p;
-    bn.emit_gauss = ctx->emit_gauss.p;
-    bn.sorted_gauss = ctx->sorted_gauss.p;
-    bn.emit_pos = ctx->emit_pos.p;
-    bn.rec = ctx->rec.p;
-    bn.sorted_rec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
-    int l = fgs::bin_sort(bn, n_big, st);
-    if (timing) cudaEventRecord(ev[3], st);
+  auto launch_blend = [&]() -> int {
     ba.isect_cap = ctx->isect_cap;
+    ba.keys = ctx->keys.p;
+    ba.emit_gauss = ctx->emit_gauss.p;
+    ba.emit_pos = ctx->emit_pos.p;
     ba.sorted_gauss = ctx->sorted_gauss.p;
-    ba.srec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
-    l += fgs::blend_forward(ba, st);
+    const int l = fgs::blend_forward(ba, st);
     if (timing) cudaEventRecord(ev[4], st);
     return l;
   };
   const bool speculative = n > 0 && ctx->isect_cap > 0;
-  if (speculative) launches += launch_rest(-1);
+  if (speculative) launches += launch_blend();
 
   FGS_CHECK(cudaEventSynchronize(ctx->ev_scan));
   FGS_CHECK(cudaGetLastError());
@@ -453,17 +443,17 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     for (auto* b : {&ctx->emit_gauss, &ctx->sorted_gauss, &ctx->emit_pos}) FGS_CHECK(b->ensure(ni));
     size_t cap = ctx->keys.cap;
     for (auto* b : {&ctx->emit_gauss, &ctx->sorted_gauss, &ctx->emit_pos}) cap = std::min(cap, b->cap);
-    if (ctx->gather_records) {
-      FGS_CHECK(ctx->sorted_rec.ensure(ni));
-      cap = std::min(cap, ctx->sorted_rec.cap);
-    }
     ctx->isect_cap = static_cast<int64_t>(cap);
-    if (n > 0) launches += launch_rest(static_cast<int>(ctx->h_scalars[fgs::kScalarBig]));
-    else {
-      if (timing) cudaEventRecord(ev[3], st);
-      launches += fgs::blend_forward(ba, st);
-      if (timing) cudaEventRecord(ev[4], st);
+    if (n > 0 && I > 0) {
+      bn.isect_cap = ctx->isect_cap;
+      bn.keys = ctx->keys.p;
+      bn.emit_gauss = ctx->emit_gauss.p;
+      bn.scatter_only = 1;
+      FGS_CHECK(fgs::bin_launch(bn, st));
+      bn.scatter_only = 0;
+      ++launches;
     }
+    launches += launch_blend();
   }
   ctx->bin_args = bn;
   if (radii && n > 0) FGS_CHECK(cudaMemcpyAsync(radii, ctx->radii.p, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
@@ -506,6 +496,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   const int64_t n = ctx->n, I = ctx->num_isect;
   if (n == 0) return FGS_OK;
   FGS_CHECK(ctx->partials.ensure(static_cast<size_t>(I > 0 ? I : 1) * fgs::kBwdWarps * 9));
+  FGS_CHECK(ctx->partial_tile.ensure(static_cast<size_t>(I > 0 ? I : 1) * 9));
 
   fgs::BlendArgs ba{};
   ba.width = ctx->cam.width;
@@ -514,13 +505,13 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   ba.tiles_y = ctx->tiles_y;
   ba.tile_offsets = ctx->tile_offsets.p;
   ba.sorted_gauss = ctx->sorted_gauss.p;
-  ba.srec = ctx->gather_records ? ctx->sorted_rec.p : nullptr;
   ba.rec = ctx->rec.p;
   for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;
   ba.dl_dimage = dl_dimage;
   ba.partials = ctx->partials.p;
+  ba.partial_tile = ctx->partial_tile.p;
   ba.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
   const bool timing = (ctx->flags & FGS_FLAG_TIMING) != 0;
   if (timing && ctx->pending.size() > 64) drain_sets(ctx, 8);
@@ -545,9 +536,8 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.state = ctx->state.p;
   pb.touched = ctx->touched.p;
   pb.coff = ctx->coff.p;
-  pb.rect = ctx->rect.p;
   pb.emit_pos = ctx->emit_pos.p;
-  pb.partials = ctx->partials.p;
+  pb.partials = ctx->partial_tile.p;
   pb.d_means = grads->d_means;
   pb.d_rotations = grads->d_rotations;
   pb.d_log_scales = grads->d_log_scales;

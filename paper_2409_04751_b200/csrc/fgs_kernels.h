@@ -48,9 +48,8 @@ struct PreprocessBackwardArgs {
   const uint8_t* state;
   const uint32_t* touched;
   const uint32_t* coff;      // [m] first emission slot of cval[q]
-  const ushort4* rect;       // [n] tile rectangles (K1)
   const uint32_t* emit_pos;  // [I] sorted position of each emission slot
-  const float* partials;     // [I][8][9] K4a per-(intersection, block) sums, sorted order
+  const float* partials;     // [I][9] K4a per-intersection sums, sorted order
   float* d_means;
   float* d_rotations;
   float* d_log_scales;
@@ -62,8 +61,10 @@ struct PreprocessBackwardArgs {
 struct BlendArgs {
   int width, height, tiles_x, tiles_y;
   const uint32_t* tile_offsets;  // T+1
-  const uint32_t* sorted_gauss;  // I
-  const SortedRec* srec;         // I records in sorted order (nullptr: read rec[sorted_gauss[k]])
+  uint32_t* sorted_gauss;        // I (written by the forward's per-tile sort, read by the backward)
+  uint64_t* keys;                // forward: tile list keys (K2b), sorted in place per tile
+  const uint32_t* emit_gauss;    // forward: Gaussian of each emission slot
+  uint32_t* emit_pos;            // forward: sorted position of each emission slot
   const SortedRec* rec;          // per-Gaussian records
   float bg[3];
   float* image;                  // H*W*3
@@ -72,12 +73,12 @@ struct BlendArgs {
   unsigned long long* counters;  // optional: E_eval, E_contrib, culled evals, max CTA cycles
   unsigned long long* tile_cycles;  // optional (with counters): per-tile CTA cycles
   const uint32_t* tile_order;    // optional: CTA -> tile (heaviest lists first)
-  int px_per_lane;               // forward blend: 1 or 2 pixels per lane
   const uint32_t* scalars;       // forward: device scalars; exit if I > isect_cap (speculative launch)
   int64_t isect_cap;
   // backward
   const float* dl_dimage;
-  float* partials;               // I x 8 x 9
+  float* partials;               // I x 8 x 9 per-(entry, pixel block) sums
+  float* partial_tile;           // I x 9 per-entry sums (backward epilogue)
 };
 
 __global__ void preprocess_kernel(PreprocessArgs a);
@@ -91,7 +92,8 @@ constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, k
 struct BinArgs {
   int n;                       // Gaussians
   int tiles_x, tiles_y, num_tiles;
-  int64_t isect_cap;           // capacity of the per-intersection buffers (scatter/sort exit if I exceeds it)
+  int64_t isect_cap;           // capacity of the per-intersection buffers (the scatter is skipped if I exceeds it)
+  int scatter_only;            // relaunch: phases 1-2 already ran
   const uint32_t* touched;     // [n] tiles touched per Gaussian (K1)
   const uint32_t* depth_key;   // [n] depth key bits (K1)
   const ushort4* rect;         // [n] tile rectangle (K1)
@@ -106,20 +108,13 @@ struct BinArgs {
   // per intersection
   uint64_t* keys;              // [I] (depth_key << 32 | emission slot), grouped by tile
   uint32_t* emit_gauss;        // [I] Gaussian of each emission slot
-  uint32_t* sorted_gauss;      // [I]
-  uint32_t* emit_pos;          // [I] sorted position of each emission slot
-  const SortedRec* rec;        // per-Gaussian splat records (K1 output)
-  SortedRec* sorted_rec;       // [I] records in sorted order (optional)
 };
 
 // Words of part_scan scratch bin_scan needs.
 size_t bin_part_words();
-// K2a: compaction + emission offsets + I (scalars), tile ranges + blend schedule.
-cudaError_t bin_scan(BinArgs& a, cudaStream_t st);
-// K2b + K2c: key scatter into tile ranges, per-tile sort; returns launches. The kernels read
-// I and the big-tile count from the device scalars and do nothing if I > a.isect_cap; n_big
-// < 0 (unknown on the host) sizes the sort grid for the worst case.
-int bin_sort(BinArgs& a, int n_big, cudaStream_t st);
+// K2 (one cooperative kernel): compaction + emission offsets + I and M (device scalars),
+// tile ranges + blend schedule, key scatter into the tile ranges (skipped if I > isect_cap).
+cudaError_t bin_launch(BinArgs& a, cudaStream_t st);
 // Debug: the reference's pre-sort key list (source order).
 cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* key_depth, uint32_t* key_gauss,
                                     cudaStream_t st);

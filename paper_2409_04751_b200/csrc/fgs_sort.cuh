@@ -1,0 +1,279 @@
+// fgs_sort.cuh — per-tile bitonic sort of the (depth_key << 32 | emission slot) keys, run by
+// the forward blend's CTA on its own tile before blending (raster.cu).
+//
+// Ascending comparators only: stage (k, j) pairs index i with its mirror in the k-block
+// (i ^ (k - 1)) when j == k/2, else with i ^ j; the smaller key goes to the lower index. Pads
+// (index >= L) hold +inf and never move, so the global variant never materialises them.
+// Register form (one warp, 32*E keys, "striped": key i = r*32 + lane lives in register r of
+// lane `lane`): partners with j < 32 are in another lane (shuffles), partners with j >= 32 in
+// another register of the same lane. Lists of <= 256 keys are sorted by one warp in registers;
+// up to kSortCap keys by the CTA in shared memory (registers for the stages inside 256-key
+// chunks); longer lists by kSortCap-chunks in shared memory with the cross-chunk stages on
+// global memory.
+#pragma once
+
+#include <type_traits>
+
+#include "fgs_kernels.h"
+
+namespace fgs {
+namespace {
+
+constexpr int kSortThreads = 256;  // the blend CTA
+constexpr int kSortCap = 4096;     // keys sorted entirely in shared memory
+
+
+__device__ __forceinline__ uint64_t kmin(uint64_t x, uint64_t y) { return y < x ? y : x; }
+__device__ __forceinline__ uint64_t kmax(uint64_t x, uint64_t y) { return y < x ? x : y; }
+
+// Stage (k, j) with j < 32: partner in lane ^ mask, same register.
+template <int E>
+__device__ __forceinline__ void xlane_stage(uint64_t (&x)[E], int lane, int mask, int half) {
+  const bool lower = (lane & half) == 0;
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const uint64_t y = __shfl_xor_sync(0xffffffffu, x[r], mask);
+    x[r] = lower ? kmin(x[r], y) : kmax(x[r], y);
+  }
+}
+
+// Half-cleaner stage with j = 32 * RJ: partner register r | RJ of the same lane.
+template <int E, int RJ>
+__device__ __forceinline__ void inlane_pairs(uint64_t (&x)[E]) {
+#pragma unroll
+  for (int r = 0; r < E; ++r)
+    if ((r & RJ) == 0) {
+      const uint64_t l = kmin(x[r], x[r | RJ]), h = kmax(x[r], x[r | RJ]);
+      x[r] = l;
+      x[r | RJ] = h;
+    }
+}
+
+// Mirror stage of level k = 64 * RB (RM = (k - 1) >> 5): partner lane ^ 31, register r ^ RM;
+// the lower index is the one whose register has bit RB clear.
+template <int E, int RM, int RB>
+__device__ __forceinline__ void inlane_mirror(uint64_t (&x)[E]) {
+  // registers r and r ^ RM exchange with the partner lane as a pair (two live temporaries)
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    if (r < (r ^ RM)) {
+      const int q = r ^ RM;
+      const uint64_t ya = __shfl_xor_sync(0xffffffffu, x[q], 31);  // partner's x[q] pairs with x[r]
+      const uint64_t yb = __shfl_xor_sync(0xffffffffu, x[r], 31);  // partner's x[r] pairs with x[q]
+      x[r] = (r & RB) == 0 ? kmin(x[r], ya) : kmax(x[r], ya);
+      x[q] = (q & RB) == 0 ? kmin(x[q], yb) : kmax(x[q], yb);
+    }
+  }
+}
+
+// One stage (k, j) on a warp's 32*E striped keys (k = 0: a half-cleaner stage of a merge
+// level above 32E).
+template <int E>
+__device__ __forceinline__ void warp_stage(uint64_t (&x)[E], int lane, int k, int j) {
+  if (j < 32) {
+    const bool mir = j == (k >> 1);
+    xlane_stage<E>(x, lane, mir ? k - 1 : j, mir ? (k >> 1) : j);
+    return;
+  }
+  if constexpr (E >= 2) {
+    if (j == (k >> 1)) {
+      if (k == 64) inlane_mirror<E, 1, 1>(x);
+      if constexpr (E >= 4)
+        if (k == 128) inlane_mirror<E, 3, 2>(x);
+      if constexpr (E >= 8)
+        if (k == 256) inlane_mirror<E, 7, 4>(x);
+    } else {
+      if (j == 32) inlane_pairs<E, 1>(x);
+      if constexpr (E >= 4)
+        if (j == 64) inlane_pairs<E, 2>(x);
+      if constexpr (E >= 8)
+        if (j == 128) inlane_pairs<E, 4>(x);
+    }
+  }
+}
+
+// Full ascending sort of the warp's 32*E striped keys.
+template <int E>
+__device__ __forceinline__ void warp_sort(uint64_t (&x)[E], int lane) {
+#pragma unroll 1
+  for (int k = 2; k <= 32 * E; k <<= 1)
+#pragma unroll 1
+    for (int j = k >> 1; j >= 1; j >>= 1) warp_stage<E>(x, lane, k, j);
+}
+
+// The half-cleaner stages j = 16E .. 1 of a merge level k > 32E (no mirror stage).
+template <int E>
+__device__ __forceinline__ void warp_halfclean(uint64_t (&x)[E], int lane) {
+#pragma unroll 1
+  for (int j = 16 * E; j >= 1; j >>= 1) warp_stage<E>(x, lane, 0, j);
+}
+
+__device__ __forceinline__ void ce_index(int c, int k, int j, int& i, int& p) {
+  i = 2 * c - (c & (j - 1));
+  p = (j == (k >> 1)) ? (i ^ (k - 1)) : (i + j);
+}
+
+__device__ __forceinline__ void ce(uint64_t* s, int i, int p) {
+  const uint64_t x = s[i], y = s[p];
+  if (y < x) {
+    s[i] = y;
+    s[p] = x;
+  }
+}
+
+constexpr int kChunk = 256;  // keys per warp register chunk (E = 8)
+constexpr int kSortWarps = kSortThreads / 32;
+
+// Register phase over the shared array s[0, n) (n a multiple of kChunk): every warp loads its
+// 256-key chunks, runs a full sort (first) or the half-cleaner stages j < 256 of a merge level,
+// and stores them back. Callers barrier before and after.
+template <bool kFull>
+__device__ __forceinline__ void chunk_phase(uint64_t* s, int n) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = warp * kChunk; c < n; c += kSortWarps * kChunk) {
+    uint64_t x[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) x[r] = s[c + r * 32 + lane];
+    if (kFull) warp_sort<8>(x, lane);
+    else warp_halfclean<8>(x, lane);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) s[c + r * 32 + lane] = x[r];
+  }
+}
+
+// Ascending sort of s[0, n), n a power of two in [kChunk, kSortCap], by the whole CTA.
+__device__ void cta_sort(uint64_t* s, int n) {
+  __syncthreads();
+  chunk_phase<true>(s, n);
+  for (int k = 2 * kChunk; k <= n; k <<= 1) {
+    for (int j = k >> 1; j >= kChunk; j >>= 1) {
+      __syncthreads();
+      for (int c = threadIdx.x; c < (n >> 1); c += kSortThreads) {
+        int i, p;
+        ce_index(c, k, j, i, p);
+        ce(s, i, p);
+      }
+    }
+    __syncthreads();
+    chunk_phase<false>(s, n);
+  }
+  __syncthreads();
+}
+
+// Stages j = C/2 .. 1 of a merge level k > C on the shared chunk s[0, C) (C = kSortCap).
+__device__ void cta_halfclean(uint64_t* s) {
+  for (int j = kSortCap >> 1; j >= kChunk; j >>= 1) {
+    __syncthreads();
+    for (int c = threadIdx.x; c < (kSortCap >> 1); c += kSortThreads) {
+      const int i = 2 * c - (c & (j - 1));
+      ce(s, i, i + j);
+    }
+  }
+  __syncthreads();
+  chunk_phase<false>(s, kSortCap);
+  __syncthreads();
+}
+
+__device__ __forceinline__ int pow2_ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// Sort the tile list keys[lo, lo + L) (CTA-wide call, all kSortThreads threads). Writes the
+// sorted Gaussian ids (sorted_gauss[lo + k]) and the emission slot -> position map
+// (emit_pos[e] = lo + k). Returns true when the ids are also left in shared memory: g of
+// entry k at ((uint32_t*)s)[2k] (lists of <= kSortCap keys); else read sorted_gauss.
+__device__ bool sort_tile_list(uint64_t* keys, const uint32_t* __restrict__ emit_gauss, uint32_t* emit_pos,
+                               uint32_t* sorted_gauss, uint32_t lo, int L, uint64_t* s) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint32_t* s32 = reinterpret_cast<uint32_t*>(s);
+  uint64_t* g = keys + lo;
+  if (L <= 0) return true;
+  if (L <= kChunk) {
+    if (tid < 32) {
+      auto run = [&](auto e_tag) {
+        constexpr int E = decltype(e_tag)::value;
+        uint64_t x[E];
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int i = r * 32 + lane;
+          x[r] = i < L ? g[i] : ~0ull;
+        }
+        warp_sort<E>(x, lane);
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          const int i = r * 32 + lane;
+          if (i < L) {
+            const uint32_t e = static_cast<uint32_t>(x[r]);
+            const uint32_t gi = emit_gauss[e];
+            emit_pos[e] = lo + i;
+            sorted_gauss[lo + i] = gi;
+            s32[2 * i] = gi;
+          }
+        }
+      };
+      if (L <= 32) run(std::integral_constant<int, 1>{});
+      else if (L <= 64) run(std::integral_constant<int, 2>{});
+      else if (L <= 128) run(std::integral_constant<int, 4>{});
+      else run(std::integral_constant<int, 8>{});
+    }
+    __syncthreads();
+    return true;
+  }
+  const int P = pow2_ceil(L);
+  if (P <= kSortCap) {
+    for (int k = tid; k < P; k += kSortThreads) s[k] = k < L ? g[k] : ~0ull;
+    cta_sort(s, P);
+    for (int k = tid; k < L; k += kSortThreads) {
+      const uint32_t e = static_cast<uint32_t>(s[k]);
+      const uint32_t gi = emit_gauss[e];
+      emit_pos[e] = lo + k;
+      sorted_gauss[lo + k] = gi;
+      s32[2 * k] = gi;
+    }
+    __syncthreads();
+    return true;
+  }
+  constexpr int C = kSortCap;
+  for (int c0 = 0; c0 < L; c0 += C) {
+    __syncthreads();
+    for (int k = tid; k < C; k += kSortThreads) s[k] = c0 + k < L ? g[c0 + k] : ~0ull;
+    cta_sort(s, C);
+    for (int k = tid; k < C && c0 + k < L; k += kSortThreads) g[c0 + k] = s[k];
+  }
+  for (int k = 2 * C; k <= P; k <<= 1) {
+    for (int j = k >> 1; j >= C; j >>= 1) {
+      __syncthreads();
+      for (int c = tid; c < (P >> 1); c += kSortThreads) {
+        int i, p;
+        ce_index(c, k, j, i, p);
+        if (p < L) {
+          const uint64_t x = g[i], y = g[p];
+          if (y < x) {
+            g[i] = y;
+            g[p] = x;
+          }
+        }
+      }
+    }
+    for (int c0 = 0; c0 < L; c0 += C) {
+      __syncthreads();
+      for (int q = tid; q < C; q += kSortThreads) s[q] = c0 + q < L ? g[c0 + q] : ~0ull;
+      cta_halfclean(s);
+      for (int q = tid; q < C && c0 + q < L; q += kSortThreads) g[c0 + q] = s[q];
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < L; k += kSortThreads) {
+    const uint32_t e = static_cast<uint32_t>(g[k]);
+    const uint32_t gi = emit_gauss[e];
+    emit_pos[e] = lo + k;
+    sorted_gauss[lo + k] = gi;
+  }
+  __syncthreads();
+  return false;
+}
+
+}  // namespace
+}  // namespace fgs

@@ -587,35 +587,19 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
 }
 
 // K4b: one thread per Gaussian that touched a tile, taken in source order from the K2a
-// compaction list (cval), 128 per CTA. K4a left 9-float partials per (intersection, pixel
-// block) at the intersection's sorted position; the Gaussian's emission slots
-// [coff[q], +touched[g]) (ascending tile order) map to those positions (emit_pos), and the
-// partials are summed here in (tile, block) order:
+// compaction list (cval), 128 per CTA. K4a left one 9-float gradient sum per intersection at
+// its sorted position; the Gaussian's emission slots [coff[q], +touched[g]) (ascending tile
+// order) map to those positions (emit_pos), and they are summed here in tile order:
 // deterministic, no atomics (gradients.hpp:161-173). Gaussians that touched no tile have zero
 // gradient; CTA b also zero-fills, with coalesced stores, the non-touching rows between its
 // predecessor's last Gaussian and its own last one -- so every sector of that source range
 // is written by one CTA in a short window and L2 merges the partial-sector writes.
-// One intersection's screen-space gradient (K4a's per-block partials at its sorted position,
-// blocks passing the culling test added in block order) added into acc: emission slot e is
-// the Gaussian's j-th tile of rect rc (ty-major, tx-minor); r0/r2 = its K1 record .a/.c.
-__device__ __forceinline__ void intersection_sum(const PreprocessBackwardArgs& a, uint32_t e, uint32_t j, ushort4 rc,
-                                                 float4 r0, float4 r2, float* acc) {
-  const int wx = rc.y - rc.x + 1;
-  const int tx = rc.x + static_cast<int>(j) % wx, ty = rc.z + static_cast<int>(j) / wx;
-  const float* p = a.partials + static_cast<size_t>(__ldg(a.emit_pos + e)) * (kBwdWarps * 9);
-  float sg[9];
+// One intersection's screen-space gradient (the blend backward's per-entry sum at its sorted
+// position) added into acc.
+__device__ __forceinline__ void intersection_sum(const PreprocessBackwardArgs& a, uint32_t e, float* acc) {
+  const float* p = a.partials + static_cast<size_t>(__ldg(a.emit_pos + e)) * 9;
 #pragma unroll
-  for (int q = 0; q < 9; ++q) sg[q] = 0.0f;
-#pragma unroll
-  for (int w = 0; w < kBwdWarps; ++w) {
-    float x0, x1, y0, y1;
-    bwd_block_box(tx, ty, w, x0, x1, y0, y1);
-    if (!rec_hits(r0, r2, x0, x1, y0, y1)) continue;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) sg[q] = sg[q] + p[w * 9 + q];
-  }
-#pragma unroll
-  for (int q = 0; q < 9; ++q) acc[q] = acc[q] + sg[q];
+  for (int q = 0; q < 9; ++q) acc[q] = acc[q] + p[q];
 }
 
 constexpr int kBwdThreads = kPreprocessBackwardThreads;
@@ -663,35 +647,18 @@ __global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(Pre
     for (int k = 0; k < 9; ++k) sg[k] = 0.0f;
     const uint32_t cnt = valid ? a.touched[i] : 0u;
     const uint32_t base = valid ? a.coff[q0 + tid] : 0u;
-    ushort4 rc = make_ushort4(0, 0, 0, 0);
-    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r2 = r0;
-    if (valid) {
-      rc = a.rect[i];
-      r0 = a.rec[i].a;
-      r2 = a.rec[i].c;
-    }
     const bool big = cnt > 32;
     if (!big)
-      for (uint32_t j = 0; j < cnt; ++j) intersection_sum(a, base + j, j, rc, r0, r2, sg);
+      for (uint32_t e = base; e < base + cnt; ++e) intersection_sum(a, e, sg);
     uint32_t bigs = __ballot_sync(0xffffffffu, big);
     while (bigs) {
       const int jl = __ffs(bigs) - 1;
       bigs &= bigs - 1;
       const uint32_t bj = __shfl_sync(0xffffffffu, base, jl), cj = __shfl_sync(0xffffffffu, cnt, jl);
-      ushort4 rj;
-      rj.x = __shfl_sync(0xffffffffu, rc.x, jl);
-      rj.y = __shfl_sync(0xffffffffu, rc.y, jl);
-      rj.z = __shfl_sync(0xffffffffu, rc.z, jl);
-      rj.w = __shfl_sync(0xffffffffu, rc.w, jl);
-      float4 a0, a2;
-      a0.x = __shfl_sync(0xffffffffu, r0.x, jl);
-      a0.y = __shfl_sync(0xffffffffu, r0.y, jl);
-      a2.y = __shfl_sync(0xffffffffu, r2.y, jl);
-      a2.z = __shfl_sync(0xffffffffu, r2.z, jl);
       float acc[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) acc[k] = 0.0f;
-      for (uint32_t j = lane; j < cj; j += 32) intersection_sum(a, bj + j, j, rj, a0, a2, acc);
+      for (uint32_t e = bj + lane; e < bj + cj; e += 32) intersection_sum(a, e, acc);
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
 #pragma unroll

@@ -18,7 +18,7 @@
 
 #include <algorithm>
 
-#include "fgs_kernels.h"
+#include "fgs_sort.cuh"
 
 namespace fgs {
 
@@ -27,10 +27,9 @@ namespace {
 constexpr int kBlend = 256;     // threads per tile CTA = pixels per tile
 constexpr int kGroup = 4;         // forward: splats whose alphas are computed together
 
-// Record of sorted entry k: from the gathered sorted stream when present, else through the
-// sorted Gaussian index.
+// Record of sorted entry k, through the sorted Gaussian index.
 __device__ __forceinline__ SortedRec load_rec(const BlendArgs& a, uint32_t k) {
-  return a.srec ? a.srec[k] : a.rec[__ldg(a.sorted_gauss + k)];
+  return a.rec[__ldg(a.sorted_gauss + k)];
 }
 
 struct PixelState {
@@ -89,9 +88,10 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr
 // the ballot of survivors in order from warp-private shared memory, kGroup splats at a time
 // (alphas first, independent of transmittance; then the sequential transmittance updates).
 // A warp stops when all its pixels have met the reference's termination rule.
-template <bool COUNTERS, int PX>
-__global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
-  constexpr int NW = 8 / PX;
+template <bool COUNTERS>
+__global__ void __launch_bounds__(256) blend_forward_kernel(BlendArgs a) {
+  constexpr int PX = 1, NW = 8;
+  __shared__ uint64_t skeys[kSortCap];  // tile list sort; then the sorted Gaussian ids
   __shared__ float4 s0[NW][32];
   __shared__ float4 s1[NW][32];
   __shared__ float s2[NW][32];
@@ -102,9 +102,16 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   const int bx = tx * kTile + ((warp & 1) << 3), by = ty * kTile + (warp >> 1) * 4 * PX;
   const int px = bx + (lane & 7);
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
+  const long long t_start = COUNTERS ? clock64() : 0;
+  // sort the tile's (depth, emission slot) keys; the ids stay in shared memory when they fit
+  const bool ids_smem = sort_tile_list(a.keys, a.emit_gauss, a.emit_pos, a.sorted_gauss, lo,
+                                       static_cast<int>(hi - lo), skeys);
+  const uint32_t* sid = reinterpret_cast<const uint32_t*>(skeys);
+  auto rec_at = [&](uint32_t k) -> SortedRec {
+    return a.rec[ids_smem ? sid[2 * (k - lo)] : __ldg(a.sorted_gauss + k)];
+  };
   const float fx = static_cast<float>(px) + 0.5f;
   const float bx0 = static_cast<float>(bx) + 0.5f, by0 = static_cast<float>(by) + 0.5f;
-  const long long t_start = COUNTERS ? clock64() : 0;
   unsigned long long warp_evals = 0;
   PixelState ps[PX];
   int py[PX];
@@ -123,8 +130,8 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   };
 
   const SortedRec zero{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-  SortedRec cur = lo + lane < hi ? load_rec(a, lo + lane) : zero;
-  SortedRec nxt = lo + 32 + lane < hi ? load_rec(a, lo + 32 + lane) : zero;
+  SortedRec cur = lo + lane < hi ? rec_at(lo + lane) : zero;
+  SortedRec nxt = lo + 32 + lane < hi ? rec_at(lo + 32 + lane) : zero;
   for (uint32_t base = lo; base < hi; base += 32) {
     if (__all_sync(0xffffffffu, all_done())) break;
     const bool pass = base + lane < hi && rec_hits(cur.a, cur.c, bx0, bx0 + 7.0f, by0, by0 + (4.0f * PX - 1.0f));
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     uint32_t mask = __ballot_sync(0xffffffffu, pass);
     if (COUNTERS) warp_evals += __popc(mask);
     cur = nxt;
-    if (base + 64 + lane < hi) nxt = load_rec(a, base + 64 + lane);
+    if (base + 64 + lane < hi) nxt = rec_at(base + 64 + lane);
     __syncwarp();
     while (mask) {
       int js[kGroup];
@@ -236,7 +243,8 @@ __device__ __forceinline__ bool near_threshold(float ar) {
 // gradients (mean_px 2, conic 3, colour 3, alpha_max 1), summed over the warp's 32 pixels by
 // a shuffle tree. The warp sum goes to partials[k][w] -- one slot per (intersection, block)
 // whose block passes the cull, zeros for passing splats past the warp's last contributor --
-// and K4b adds the passing slots in fixed (tile, block) order: deterministic, no atomics.
+// and the CTA's epilogue adds the passing slots of every entry in block order into
+// partial_tile[k] (K4b then sums a Gaussian's entries in tile order): deterministic, no atomics.
 __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
   __shared__ float4 s0[kBwdWarps][32];
   __shared__ float4 s1[kBwdWarps][32];
@@ -383,20 +391,41 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     }
     __syncwarp();
   }
+  // Epilogue: per entry of the tile, the 9 gradients summed over the pixel blocks that passed
+  // the culling test, in block order (the partials are this CTA's own, L2-resident writes).
+  __syncthreads();
+  for (uint32_t k = lo + threadIdx.x; k < hi; k += kBlend) {
+    const SortedRec r = load_rec(a, k);
+    const float* p = part + static_cast<size_t>(k) * (kBwdWarps * 9);
+    float sg[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) sg[q] = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kBwdWarps; ++w) {
+      float x0, x1, y0, y1;
+      bwd_block_box(tx, ty, w, x0, x1, y0, y1);
+      if (!rec_hits(r.a, r.c, x0, x1, y0, y1)) continue;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) sg[q] = sg[q] + p[w * 9 + q];
+    }
+    float* o = a.partial_tile + static_cast<size_t>(k) * 9;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) o[q] = sg[q];
+  }
 }
 
 }  // namespace
 
 int blend_forward(const BlendArgs& a, cudaStream_t st) {
-  const int px = a.px_per_lane == 2 ? 2 : 1;
-  const int threads = 256 / px;
-  if (a.counters) {
-    if (px == 2) blend_forward_kernel<true, 2><<<a.tiles_x * a.tiles_y, threads, 0, st>>>(a);
-    else blend_forward_kernel<true, 1><<<a.tiles_x * a.tiles_y, threads, 0, st>>>(a);
-  } else {
-    if (px == 2) blend_forward_kernel<false, 2><<<a.tiles_x * a.tiles_y, threads, 0, st>>>(a);
-    else blend_forward_kernel<false, 1><<<a.tiles_x * a.tiles_y, threads, 0, st>>>(a);
+  static bool init = false;
+  if (!init) {
+    for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<true>),
+                          reinterpret_cast<const void*>(blend_forward_kernel<false>)})
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    init = true;
   }
+  if (a.counters) blend_forward_kernel<true><<<a.tiles_x * a.tiles_y, 256, 0, st>>>(a);
+  else blend_forward_kernel<false><<<a.tiles_x * a.tiles_y, 256, 0, st>>>(a);
   return 1;
 }
 
