@@ -45,7 +45,8 @@ enum {
 
 enum { FGS_CAMERA_PINHOLE = 0, FGS_CAMERA_FISHEYE = 1, FGS_CAMERA_PANORAMA = 2 };
 
-/* Camera (inc/cameras.hpp:29-74). Only FGS_CAMERA_FISHEYE is implemented on the GPU path. */
+/* Camera (inc/cameras.hpp:29-74): equidistant fisheye (the paper's model), pinhole, and
+ * equirectangular panorama (fx..cy unused). */
 typedef struct fgs_camera {
   int32_t model;
   int32_t width, height;

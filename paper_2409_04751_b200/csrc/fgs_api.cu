@@ -123,6 +123,7 @@ int cuda_fail(fgs_context* c, cudaError_t e, const char* where) {
 
 fgs::DevCamera make_dev_camera(const fgs_camera& c) {
   fgs::DevCamera d{};
+  d.model = c.model;
   d.width = c.width;
   d.height = c.height;
   d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy;
@@ -273,8 +274,9 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
                 const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
   if (!ctx) return FGS_EINVAL;
   if (!scene || !camera || !image) return fail(ctx, FGS_EINVAL, "forward: null argument");
-  if (camera->model != FGS_CAMERA_FISHEYE)
-    return fail(ctx, FGS_EINVAL, "forward: only the equidistant fisheye camera is implemented on the GPU path");
+  if (camera->model != FGS_CAMERA_FISHEYE && camera->model != FGS_CAMERA_PINHOLE &&
+      camera->model != FGS_CAMERA_PANORAMA)
+    return fail(ctx, FGS_EINVAL, "forward: unknown camera model");
   if (camera->width <= 0 || camera->height <= 0) return fail(ctx, FGS_EINVAL, "forward: empty image");
   if ((static_cast<int64_t>(camera->width) + 15) / 16 * ((static_cast<int64_t>(camera->height) + 15) / 16) > 65536)
     return fail(ctx, FGS_EINVAL, "forward: more than 65536 tiles");

@@ -24,7 +24,11 @@ constexpr float kPowerFloor = -5.6f;
 // fast exp is replaced by the correctly rounded one (SURVEY.md §7 hard part 2).
 constexpr float kGuardRel = 4.0e-6f;
 
+constexpr float kPinholeNearClip = 0.2f;  // core.hpp:52
+constexpr int kCamPinhole = 0, kCamFisheye = 1, kCamPanorama = 2;  // FGS_CAMERA_* (fgs.h)
+
 struct DevCamera {
+  int model;  // kCam*
   int width, height;
   float fx, fy, cx, cy;
   float W[9];   // rotation_wc row-major

@@ -1,4 +1,6 @@
-// preprocess.cu — K1 (fisheye preprocess) and K4b (preprocess backward), sm_100a.
+// preprocess.cu — K1 (preprocess) and K4b (preprocess backward), sm_100a. The camera model
+// (equidistant fisheye, pinhole, equirectangular panorama) only matters here: binning, sort
+// and blends are camera-agnostic (splatting.hpp:65-67).
 //
 // Compiled with --fmad=false: every expression below is evaluated in the reference's
 // operation order with IEEE-rounded fp32 ops (division and sqrt are IEEE by default), so the
@@ -8,7 +10,7 @@
 //
 // Reference: /root/reference/proj/include/omnisplat/
 //   preprocess            splatting.hpp:68-139
-//   project (fisheye)     cameras.hpp:139-177, fisheye_terms :99-128, jacobian :180-212
+//   project               cameras.hpp:139-177, fisheye_terms :99-128, jacobian :180-212
 //   build_covariance      model.hpp:95-140; eval_sh model.hpp:187-215; sigmoid core.hpp:30-36
 //   backward per splat    gradients.hpp:226-264, covariance_projection_backward :186-202,
 //                         projection_jacobian_grad cameras.hpp:217-271,
@@ -67,6 +69,61 @@ __device__ __forceinline__ void fisheye_jacobian(const float p[3], const DevCame
   j[1][0] = fy * x * y * t.u;
   j[1][1] = fy * (t.g + y * y * t.u);
   j[1][2] = -fy * y / r2;
+}
+
+constexpr float kPi = 3.14159265358979323846f;  // pi<float>() (core.hpp)
+
+// cameras.hpp:184-189
+__device__ __forceinline__ void pinhole_jacobian(const float p[3], const DevCamera& cam, float j[2][3]) {
+  const float x = p[0], y = p[1], z = p[2];
+  const float iz = 1.0f / z;
+  j[0][0] = cam.fx * iz; j[0][1] = 0.0f; j[0][2] = -cam.fx * x * iz * iz;
+  j[1][0] = 0.0f; j[1][1] = cam.fy * iz; j[1][2] = -cam.fy * y * iz * iz;
+}
+
+// cameras.hpp:200-208
+__device__ __forceinline__ void panorama_jacobian(const float p[3], const DevCamera& cam, float j[2][3]) {
+  const float x = p[0], y = p[1], z = p[2];
+  const float s = x * x + z * z;
+  const float rho = sqrtf(s);
+  const float r2 = s + y * y;
+  const float cw = static_cast<float>(cam.width) / (2.0f * kPi);
+  const float dh = static_cast<float>(cam.height) / kPi;
+  j[0][0] = cw * z / s; j[0][1] = 0.0f; j[0][2] = -cw * x / s;
+  j[1][0] = -dh * x * y / (rho * r2); j[1][1] = dh * rho / r2; j[1][2] = -dh * y * z / (rho * r2);
+}
+
+// cameras.hpp:223-230
+__device__ __forceinline__ void pinhole_jacobian_grad(const float p[3], const DevCamera& cam, float d[3][2][3]) {
+  const float x = p[0], y = p[1], z = p[2];
+  const float iz2 = 1.0f / (z * z);
+  const float fx = cam.fx, fy = cam.fy;
+  d[0][0][0] = 0.0f; d[0][0][1] = 0.0f; d[0][0][2] = -fx * iz2;
+  d[0][1][0] = 0.0f; d[0][1][1] = 0.0f; d[0][1][2] = 0.0f;
+  d[1][0][0] = 0.0f; d[1][0][1] = 0.0f; d[1][0][2] = 0.0f;
+  d[1][1][0] = 0.0f; d[1][1][1] = 0.0f; d[1][1][2] = -fy * iz2;
+  d[2][0][0] = -fx * iz2; d[2][0][1] = 0.0f; d[2][0][2] = 2.0f * fx * x * iz2 / z;
+  d[2][1][0] = 0.0f; d[2][1][1] = -fy * iz2; d[2][1][2] = 2.0f * fy * y * iz2 / z;
+}
+
+// cameras.hpp:249-268
+__device__ __forceinline__ void panorama_jacobian_grad(const float p[3], const DevCamera& cam, float d[3][2][3]) {
+  const float x = p[0], y = p[1], z = p[2];
+  const float s = x * x + z * z;
+  const float rho = sqrtf(s);
+  const float r2 = s + y * y;
+  const float cw = static_cast<float>(cam.width) / (2.0f * kPi);
+  const float dh = static_cast<float>(cam.height) / kPi;
+  const float is2 = 1.0f / (s * s);
+  const float e = 1.0f / (rho * r2);
+  const float f = (r2 + 2.0f * s) / (rho * s * r2 * r2);
+  const float ey = 2.0f * y / (rho * r2 * r2);
+  d[0][0][0] = -2.0f * cw * x * z * is2; d[0][0][1] = 0.0f; d[0][0][2] = cw * (x * x - z * z) * is2;
+  d[0][1][0] = -dh * y * (e - x * x * f); d[0][1][1] = dh * x * (y * y - s) / (rho * r2 * r2); d[0][1][2] = dh * x * y * z * f;
+  d[1][0][0] = 0.0f; d[1][0][1] = 0.0f; d[1][0][2] = 0.0f;
+  d[1][1][0] = -dh * x * (e - y * ey); d[1][1][1] = -2.0f * dh * rho * y / (r2 * r2); d[1][1][2] = -dh * z * (e - y * ey);
+  d[2][0][0] = cw * (x * x - z * z) * is2; d[2][0][1] = 0.0f; d[2][0][2] = 2.0f * cw * x * z * is2;
+  d[2][1][0] = dh * x * y * z * f; d[2][1][1] = dh * z * (y * y - s) / (rho * r2 * r2); d[2][1][2] = -dh * y * (e - z * z * f);
 }
 
 // cameras.hpp:232-247
@@ -264,14 +321,31 @@ __device__ __forceinline__ int project_covariance(const DevCamera& cam, const fl
   const float x = P.mu[0], y = P.mu[1], z = P.mu[2];
   const float r2 = x * x + y * y + z * z;
   if (r2 < 1e-24f) return -1;
-  const float lz2 = x * x + y * y;
-  if (z < 0.0f && lz2 < 1e-24f * z * z) return -1;
-  const float theta = cr_atan2f(sqrtf(lz2), z);
-  if (!(theta <= cam.fov_max + kFisheyeCullMargin)) return -1;
-  const float g = fisheye_terms(lz2, z).g;
-  P.pix[0] = cam.cx + cam.fx * g * x;
-  P.pix[1] = cam.cy + cam.fy * g * y;
-  fisheye_jacobian(P.mu, cam, P.j);
+  if (cam.model == kCamFisheye) {
+    const float lz2 = x * x + y * y;
+    if (z < 0.0f && lz2 < 1e-24f * z * z) return -1;
+    const float theta = cr_atan2f(sqrtf(lz2), z);
+    if (!(theta <= cam.fov_max + kFisheyeCullMargin)) return -1;
+    const float g = fisheye_terms(lz2, z).g;
+    P.pix[0] = cam.cx + cam.fx * g * x;
+    P.pix[1] = cam.cy + cam.fy * g * y;
+    fisheye_jacobian(P.mu, cam, P.j);
+  } else if (cam.model == kCamPinhole) {
+    if (fabsf(z) < 1e-12f) return -1;
+    P.pix[0] = cam.cx + cam.fx * x / z;
+    P.pix[1] = cam.cy + cam.fy * y / z;
+    if (!(z > kPinholeNearClip)) return -1;
+    pinhole_jacobian(P.mu, cam, P.j);
+  } else {
+    const float s = x * x + z * z;
+    if (s < 1e-24f * y * y) return -1;
+    const float w = static_cast<float>(cam.width), h = static_cast<float>(cam.height);
+    float xp = w * (cr_atan2f(x, z) + kPi) / (2.0f * kPi);
+    if (xp >= w) xp -= w;
+    P.pix[0] = xp;
+    P.pix[1] = h * (cr_atan2f(y, sqrtf(s)) + kPi / 2.0f) / kPi;
+    panorama_jacobian(P.mu, cam, P.j);
+  }
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -325,7 +399,9 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
           my - rf > static_cast<float>(cam.height))) {
       state = 1;
       const float ca = P.sp[1][1] / det, cb = -P.sp[0][1] / det, cc = P.sp[0][0] / det;
-      const float depth = sqrtf(P.mu[0] * P.mu[0] + P.mu[1] * P.mu[1] + P.mu[2] * P.mu[2]);
+      // splatting.hpp:114: z for the pinhole, the distance for fisheye / panorama
+      const float depth = cam.model == kCamPinhole ? P.mu[2]
+                                                   : sqrtf(P.mu[0] * P.mu[0] + P.mu[1] * P.mu[1] + P.mu[2] * P.mu[2]);
       float dir[3];
       view_dir(cam, m, dir);
       float Y[16];
@@ -441,7 +517,9 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
 #pragma unroll
       for (int c = 0; c < 3; ++c) dldj[r][c] = dldt[r][0] * cam.W[c * 3 + 0] + dldt[r][1] * cam.W[c * 3 + 1] + dldt[r][2] * cam.W[c * 3 + 2];
     float dj[3][2][3];
-    fisheye_jacobian_grad(P.mu, cam, dj);
+    if (cam.model == kCamFisheye) fisheye_jacobian_grad(P.mu, cam, dj);
+    else if (cam.model == kCamPinhole) pinhole_jacobian_grad(P.mu, cam, dj);
+    else panorama_jacobian_grad(P.mu, cam, dj);
     float cov[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {

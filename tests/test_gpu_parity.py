@@ -148,3 +148,30 @@ def test_reference_dc_only_grads(rast, oracle_mod):
     o = run_oracle(oracle_mod, scene, cams[0], deg, dls[0], full_sh=False)
     assert np.all(g["grads"][:, GROUPS["sh_rest"]] == 0)
     check_grads(g, o, ("mean", "rotation", "log_scale", "opacity", "sh_dc"))
+
+
+@pytest.mark.parametrize("model", ["pinhole", "panorama"])
+def test_other_camera_models_parity(rast, oracle_mod, model):
+    """the pinhole and equirectangular-panorama preprocess variants
+    (cameras.hpp:148-153, :163-173, :184-209, :223-268; depth = z for the pinhole,
+    splatting.hpp:114) -- only K1/K4b know the camera model. Same bars as the fisheye path:
+    keys / order / ranges bit-exact, image and gradients within tolerance."""
+    from paper_2409_04751_b200 import Camera, synthetic
+
+    scene, deg, cams, dls = synthetic.config(4, n=30000, views=1)
+    pose = cams[0]
+    if model == "pinhole":
+        cam = Camera.pinhole(640, 480, 500.0, 510.0, 320.0, 240.0)
+    else:
+        cam = Camera.panorama(1024, 512)
+    cam.rotation_wc = pose.rotation_wc
+    cam.translation_wc = pose.translation_wc
+    cam = cam.as_float32()
+    dl = np.random.default_rng(5).standard_normal((cam.height, cam.width, 3)).astype(np.float32)
+    g = run_gpu(rast, scene, cam, deg, dl)
+    o = run_oracle(oracle_mod, scene, cam, deg, dl)
+    assert o["res"].num_intersections > 1000
+    check_preprocess(g, o, scene)
+    check_keys(rast, o)
+    check_image(g, o)
+    check_grads(g, o)
