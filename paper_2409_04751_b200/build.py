@@ -15,6 +15,8 @@ OBJ = os.path.join(HERE, "_obj")
 ROOT = os.path.dirname(HERE)
 EXAMPLE_SRC = os.path.join(ROOT, "tools", "fgs_render_example.cpp")
 EXAMPLE_BIN = os.path.join(ROOT, "tools", "fgs_render_example")
+CLI_SRC = os.path.join(ROOT, "tools", "fgs_cli.cpp")
+CLI_BIN = os.path.join(ROOT, "tools", "fgs_cli")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]
@@ -36,6 +38,10 @@ def _nvcc():
 def build(verbose=False, force=False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "fgs.h")]
+    if not force and os.path.exists(OUT) and (not os.path.exists(CLI_BIN) or
+                                              os.path.getmtime(CLI_BIN) < max(os.path.getmtime(CLI_SRC),
+                                              os.path.getmtime(os.path.join(ROOT, "include", "fgs_io.hpp")))):
+        build_example(verbose)
     newest = max(os.path.getmtime(p) for p in deps)
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
         return OUT
@@ -57,14 +63,16 @@ def build(verbose=False, force=False) -> str:
 
 
 def build_example(verbose=False):
-    """C++ host example over include/fgs.hpp, linked against libfgs.so (rpath $ORIGIN/..)."""
-    if not os.path.exists(EXAMPLE_SRC):
-        return None
-    cmd = ["g++", "-O2", "-std=c++17", "-o", EXAMPLE_BIN, EXAMPLE_SRC, "-L" + HERE, "-lfgs",
-           "-Wl,-rpath,$ORIGIN/../paper_2409_04751_b200"]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+    """C++ host programs over include/fgs.hpp / fgs_io.hpp (the render example and the
+    reference-compatible CLI), linked against libfgs.so (rpath $ORIGIN/..)."""
+    for src, out in ((EXAMPLE_SRC, EXAMPLE_BIN), (CLI_SRC, CLI_BIN)):
+        if not os.path.exists(src):
+            continue
+        cmd = ["g++", "-O2", "-std=c++17", "-o", out, src, "-L" + HERE, "-lfgs",
+               "-Wl,-rpath,$ORIGIN/../paper_2409_04751_b200"]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
     return EXAMPLE_BIN
 
 

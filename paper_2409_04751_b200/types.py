@@ -36,8 +36,8 @@ GRAD_SLICES = {
 
 @dataclass
 class Camera:
-    """Equidistant-fisheye camera (cameras.hpp:29-74). Only the fisheye model is on the
-    B200 path; pinhole/panorama exist in the oracle for the ported reference tests."""
+    """Camera (cameras.hpp:29-74): equidistant fisheye (the paper's model), pinhole or
+    equirectangular panorama -- all three on the B200 path (only K1/K4b differ)."""
 
     width: int
     height: int
