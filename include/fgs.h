@@ -40,7 +40,8 @@ enum {
   FGS_EDEGENERATE_QUAT = 2,   /* zero-norm quaternion (inc/model.hpp:98, "degenerate rotation") */
   FGS_ECUDA = 3,              /* CUDA runtime error */
   FGS_ENOMEM = 4,             /* device allocation failed */
-  FGS_ESTATE = 5              /* backward without a matching forward */
+  FGS_ESTATE = 5,             /* backward without a matching forward */
+  FGS_ENONFINITE = 6          /* non-finite gradient in an Adam step (std::runtime_error) */
 };
 
 enum { FGS_CAMERA_PINHOLE = 0, FGS_CAMERA_FISHEYE = 1, FGS_CAMERA_PANORAMA = 2 };
@@ -144,6 +145,56 @@ int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s);
  *   "final_T" f32[H*W], "last" u32[H*W], "counters" u64[4] (E_eval, E_contrib, 0, 0).
  * Returns the number of bytes (dst may be NULL to query), or -1 for an unknown name. */
 int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst_bytes);
+
+/* ---- Training step: inc/metrics.hpp:86-195, inc/optimize.hpp:100-277 ---- */
+
+/* L = (1 - lambda) L1 + lambda (1 - SSIM) of `rendered` against `target` (device H*W*3 each,
+ * 11x11 Gaussian-window SSIM, zero padding); writes dL/drendered (device H*W*3) and
+ * out[3] = {total, l1, dssim} (host). Synchronises. */
+int fgs_l1_dssim_loss(fgs_context* ctx, const float* rendered, const float* target, int32_t width, int32_t height,
+                      float lambda, float* d_rendered, double out[3]);
+
+/* Mutable scene parameters (device arrays, the fgs_gaussians layout). */
+typedef struct fgs_params {
+  int64_t n;
+  float* means;
+  float* rotations;
+  float* log_scales;
+  float* opacity_logits;
+  float* sh;
+} fgs_params;
+
+/* AdamParams + GroupLearningRates (inc/optimize.hpp:72-97). lr_sh_rest (SH bands 1..3) is a
+ * build extension: the reference optimises the DC only; 0 reproduces that. */
+typedef struct fgs_adam_options {
+  float lr_mean, lr_rotation, lr_log_scale, lr_opacity, lr_sh_dc, lr_sh_rest;
+  float beta1, beta2, eps;  /* 0.9, 0.999, 1e-15 in the reference */
+} fgs_adam_options;
+
+/* AdamState (inc/optimize.hpp:78-90): step count and first/second moments, device arrays in
+ * the gradient layout (zero-initialised by the caller, step = 0). */
+typedef struct fgs_adam_state {
+  int64_t step;
+  fgs_gradients m, v;
+} fgs_adam_state;
+
+/* adam_step (inc/optimize.hpp:115-145) on device arrays. A non-finite gradient in an updated
+ * group returns FGS_ENONFINITE and changes nothing (the reference throws before updating). */
+int fgs_adam_step(fgs_context* ctx, fgs_params* params, const fgs_gradients* grads, fgs_adam_state* state,
+                  const fgs_adam_options* options);
+
+typedef struct fgs_train_options {
+  int32_t sh_degree;
+  float background[3];
+  float lambda;             /* loss_lambda, 0.2 in the reference */
+  fgs_adam_options adam;
+} fgs_train_options;
+
+/* One iteration of the reference's train loop body (inc/optimize.hpp:237-266): render the
+ * view, L1 + D-SSIM loss against `target` (device H*W*3), backward, Adam step -- all on the
+ * device, parameters updated in place. loss_out = {total, l1, dssim}. */
+int fgs_train_step(fgs_context* ctx, fgs_params* params, const fgs_camera* camera, const float* target,
+                   const fgs_train_options* options, fgs_adam_state* state, double loss_out[3]);
 
 /* Counters of the last forward: [n, num_splats, num_intersections, tiles_x, tiles_y, width, height,
  * num_culled, num_degenerate]. */

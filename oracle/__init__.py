@@ -334,3 +334,130 @@ def splats_backward(res: Result, dl_dimage, threads=0):
     if lib().orc_splats_backward_f64(res.handle, _p(dl, C.c_double), _p(out, C.c_double), threads) != 0:
         raise OracleError(lib().orc_last_error().decode())
     return out
+
+
+# ---------------------------------------------------------------------------------------
+# Training-step oracle: numpy restatements of the reference's loss and
+# optimizer, and wrappers around the reference's own code (oracle/_ref) that pin them.
+
+SSIM_WINDOW, SSIM_SIGMA, SSIM_C1, SSIM_C2 = 11, 1.5, 0.01 ** 2, 0.03 ** 2  # inc/metrics.hpp:18-21
+
+
+def _ssim_window():
+    """inc/metrics.hpp:23-34: normalised 11-tap Gaussian, sigma 1.5."""
+    d = np.arange(SSIM_WINDOW, dtype=np.float64) - SSIM_WINDOW // 2
+    w = np.exp(-d * d / (2.0 * SSIM_SIGMA * SSIM_SIGMA))
+    return w / w.sum()
+
+
+def _blur(plane):
+    """inc/metrics.hpp:37-61: separable zero-padded filter (rows, then columns)."""
+    w = _ssim_window()
+    r = SSIM_WINDOW // 2
+    h, wd = plane.shape
+    pad = np.zeros((h, wd + 2 * r))
+    pad[:, r:r + wd] = plane
+    tmp = sum(w[k] * pad[:, k:k + wd] for k in range(SSIM_WINDOW))
+    pad = np.zeros((h + 2 * r, wd))
+    pad[r:r + h, :] = tmp
+    return sum(w[k] * pad[k:k + h, :] for k in range(SSIM_WINDOW))
+
+
+def ssim(rendered, target, want_grad=False):
+    """inc/metrics.hpp:86-161: mean SSIM over the 11x11 Gaussian-window map per channel,
+    averaged; optionally d(mean SSIM)/d(rendered) in the difference-factored form."""
+    x_img = np.asarray(rendered, np.float64)
+    y_img = np.asarray(target, np.float64)
+    h, w, _ = x_img.shape
+    norm = 1.0 / (h * w * 3)
+    total = 0.0
+    grad = np.zeros_like(x_img) if want_grad else None
+    for ch in range(3):
+        x, y = x_img[:, :, ch], y_img[:, :, ch]
+        mx, my = _blur(x), _blur(y)
+        mxx, myy, mxy = _blur(x * x), _blur(y * y), _blur(x * y)
+        sx2, sy2, sxy = mxx - mx * mx, myy - my * my, mxy - mx * my
+        n1 = 2 * mx * my + SSIM_C1
+        n2 = 2 * sxy + SSIM_C2
+        d1 = mx * mx + my * my + SSIM_C1
+        d2 = sx2 + sy2 + SSIM_C2
+        s = (n1 * n2) / (d1 * d2)
+        total += s.sum()
+        if want_grad:
+            a = 2 * n2 * (my - mx) * (my * (mx + my) + SSIM_C1) / (d1 * d1 * d2)
+            b = -s / d2
+            e = 2 * n1 * (d2 - n2) / (d1 * d2 * d2)
+            ca, cb, cbdmu, ce, cemy = _blur(a), _blur(b), _blur(b * (mx - my)), _blur(e), _blur(e * my)
+            grad[:, :, ch] = norm * (ca + 2 * (x - y) * cb - 2 * cbdmu + y * ce - cemy)
+    return total * norm, grad
+
+
+def l1_dssim_loss(rendered, target, lam=0.2):
+    """inc/metrics.hpp:172-195: L = (1 - lam) L1 + lam (1 - SSIM) and dL/drendered.
+    Returns (total, l1, dssim, d_rendered)."""
+    x = np.asarray(rendered, np.float64)
+    y = np.asarray(target, np.float64)
+    norm = 1.0 / x.size
+    s, ds = ssim(x, y, want_grad=True)
+    diff = x - y
+    l1 = np.abs(diff).sum() * norm
+    d = (1.0 - lam) * np.sign(diff) * norm - lam * ds
+    return (1.0 - lam) * l1 + lam * (1.0 - s), l1, 1.0 - s, d
+
+
+ADAM_BETA1, ADAM_BETA2, ADAM_EPS = 0.9, 0.999, 1e-15  # inc/optimize.hpp:72-76
+PARAM_GROUPS = {"mean": slice(0, 3), "rotation": slice(3, 7), "log_scale": slice(7, 10), "opacity": slice(10, 11),
+                "sh_dc": [11, 27, 43], "sh_rest": [c * 16 + j + 11 for c in range(3) for j in range(1, 16)]}
+
+
+def adam_step(params, grads, m, v, step, lr):
+    """inc/optimize.hpp:100-145 on (N, 59) rows in place; lr maps PARAM_GROUPS names to rates
+    (the reference has no sh_rest group: rate 0 / absent leaves those rows untouched).
+    ``step`` is the state's step before the call; returns the new step."""
+    step += 1
+    bc1 = 1.0 - ADAM_BETA1 ** step
+    bc2 = 1.0 - ADAM_BETA2 ** step
+    for name, sl in PARAM_GROUPS.items():
+        rate = lr.get(name, 0.0)
+        if not rate:
+            continue
+        g = grads[:, sl]
+        m[:, sl] = ADAM_BETA1 * m[:, sl] + (1 - ADAM_BETA1) * g
+        v[:, sl] = ADAM_BETA2 * v[:, sl] + (1 - ADAM_BETA2) * g * g
+        params[:, sl] -= rate * (m[:, sl] / bc1) / (np.sqrt(v[:, sl] / bc2) + ADAM_EPS)
+    return step
+
+
+def ref_l1_dssim_loss(rendered, target, lam=0.2):
+    """The reference's own l1_dssim_loss (inc/metrics.hpp:172-195) via oracle/_ref."""
+    L = ref_lib()
+    x = np.ascontiguousarray(rendered, np.float64)
+    y = np.ascontiguousarray(target, np.float64)
+    h, w, _ = x.shape
+    d = np.zeros_like(x)
+    out = np.zeros(3)
+    dp = C.POINTER(C.c_double)
+    fn = L.ref_l1_dssim_loss_f64
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_int, C.c_int, dp, dp, C.c_double, dp, dp]
+    if fn(w, h, _p(x, C.c_double), _p(y, C.c_double), lam, _p(d, C.c_double), _p(out, C.c_double)) != 0:
+        raise OracleError(L.ref_last_error().decode())
+    return out[0], out[1], out[2], d
+
+
+def ref_adam_step(params, grads, m, v, step, lr):
+    """The reference's own adam_step (inc/optimize.hpp:115-145) via oracle/_ref, in place on
+    (N, 59) float64 rows (mean, rotation, log_scale, opacity, sh_dc updated)."""
+    L = ref_lib()
+    fn = L.ref_adam_step_f64
+    dp = C.POINTER(C.c_double)
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_int64, dp, dp, dp, dp, C.c_int64, dp]
+    rates = np.array([lr["mean"], lr["rotation"], lr["log_scale"], lr["opacity"], lr["sh_dc"]], np.float64)
+    for a in (params, m, v):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+    g = np.ascontiguousarray(grads, np.float64)
+    if fn(params.shape[0], _p(params, C.c_double), _p(g, C.c_double), _p(m, C.c_double), _p(v, C.c_double), step,
+          _p(rates, C.c_double)) != 0:
+        raise OracleError(L.ref_last_error().decode())
+    return step + 1

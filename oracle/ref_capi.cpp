@@ -16,6 +16,8 @@
 #include <type_traits>
 
 #include "omnisplat/gradients.hpp"
+#include "omnisplat/metrics.hpp"
+#include "omnisplat/optimize.hpp"
 #include "omnisplat/oracle.hpp"
 #include "omnisplat/splatting.hpp"
 
@@ -223,6 +225,82 @@ int ref_bruteforce_render_f64(int64_t n, const double* m, const double* r, const
     oo.max_gaussians = static_cast<size_t>(n) + 1;
     const ImageBuffer<double> img = bruteforce_render(s, c, oo);
     std::memcpy(image, img.pixels.data(), img.pixels.size() * sizeof(double));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+  return 0;
+}
+
+// L = (1 - lambda) L1 + lambda (1 - SSIM) and dL/drendered (double, as the reference trains).
+int ref_l1_dssim_loss_f64(int w, int h, const double* rendered, const double* target, double lambda,
+                          double* d_rendered, double* out3) {
+  try {
+    ImageBuffer<double> a(w, h), b(w, h);
+    std::memcpy(a.pixels.data(), rendered, a.pixels.size() * sizeof(double));
+    std::memcpy(b.pixels.data(), target, b.pixels.size() * sizeof(double));
+    const LossResult<double> r = l1_dssim_loss(a, b, lambda);
+    std::memcpy(d_rendered, r.d_rendered.pixels.data(), r.d_rendered.pixels.size() * sizeof(double));
+    out3[0] = r.total;
+    out3[1] = r.l1;
+    out3[2] = r.dssim;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+  return 0;
+}
+
+// One adam_step on n Gaussians (params/grads/m/v as 59-float rows: mean 3, rotation 4,
+// log_scale 3, opacity 1, sh 48 with DC at 11 + 16c; the reference updates the DC only).
+// lr = {mean, rotation, log_scale, opacity, sh_dc}; step = the state's step before the call.
+int ref_adam_step_f64(int64_t n, double* params, const double* grads, double* m, double* v, int64_t step,
+                      const double* lr) {
+  try {
+    Scene<double> s;
+    s.gaussians.resize(n);
+    GradientBuffer<double> g;
+    g.resize_zero(n);
+    AdamState<double> st;
+    st.init(n);
+    st.step = step;
+    auto load = [&](int64_t i, const double* row, auto& mean, auto& rot, auto& ls, double& op, auto& dc) {
+      for (int k = 0; k < 3; ++k) mean[k] = row[k];
+      for (int k = 0; k < 4; ++k) rot[k] = row[3 + k];
+      for (int k = 0; k < 3; ++k) ls[k] = row[7 + k];
+      op = row[10];
+      for (int c = 0; c < 3; ++c) dc[c] = row[11 + 16 * c];
+      (void)i;
+    };
+    for (int64_t i = 0; i < n; ++i) {
+      auto& q = s.gaussians[i];
+      Vec3<double> dc;
+      load(i, params + i * 59, q.mean, q.rotation, q.log_scale, q.opacity_logit, dc);
+      for (int c = 0; c < 3; ++c) q.sh(0, c) = dc[c];
+      load(i, grads + i * 59, g.d_mean[i], g.d_rotation[i], g.d_log_scale[i], g.d_opacity_logit[i], g.d_sh_dc[i]);
+      load(i, m + i * 59, st.m.d_mean[i], st.m.d_rotation[i], st.m.d_log_scale[i], st.m.d_opacity_logit[i],
+           st.m.d_sh_dc[i]);
+      load(i, v + i * 59, st.v.d_mean[i], st.v.d_rotation[i], st.v.d_log_scale[i], st.v.d_opacity_logit[i],
+           st.v.d_sh_dc[i]);
+    }
+    const GroupLearningRates<double> rates{lr[0], lr[1], lr[2], lr[3], lr[4]};
+    adam_step(s, g, st, rates);
+    auto store = [&](double* row, const auto& mean, const auto& rot, const auto& ls, double op, const auto& dc) {
+      for (int k = 0; k < 3; ++k) row[k] = mean[k];
+      for (int k = 0; k < 4; ++k) row[3 + k] = rot[k];
+      for (int k = 0; k < 3; ++k) row[7 + k] = ls[k];
+      row[10] = op;
+      for (int c = 0; c < 3; ++c) row[11 + 16 * c] = dc[c];
+    };
+    for (int64_t i = 0; i < n; ++i) {
+      const auto& q = s.gaussians[i];
+      const Vec3<double> dc(q.sh(0, 0), q.sh(0, 1), q.sh(0, 2));
+      store(params + i * 59, q.mean, q.rotation, q.log_scale, q.opacity_logit, dc);
+      store(m + i * 59, st.m.d_mean[i], st.m.d_rotation[i], st.m.d_log_scale[i], st.m.d_opacity_logit[i],
+            st.m.d_sh_dc[i]);
+      store(v + i * 59, st.v.d_mean[i], st.v.d_rotation[i], st.v.d_log_scale[i], st.v.d_opacity_logit[i],
+            st.v.d_sh_dc[i]);
+    }
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

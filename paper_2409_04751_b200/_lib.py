@@ -10,7 +10,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfgs.so")
 
-FGS_OK, FGS_EINVAL, FGS_EDEGENERATE_QUAT, FGS_ECUDA, FGS_ENOMEM, FGS_ESTATE = range(6)
+FGS_OK, FGS_EINVAL, FGS_EDEGENERATE_QUAT, FGS_ECUDA, FGS_ENOMEM, FGS_ESTATE, FGS_ENONFINITE = range(7)
 FGS_FLAG_COUNTERS, FGS_FLAG_KEEP_KEYS, FGS_FLAG_TIMING = 1, 2, 4
 
 
@@ -45,9 +45,28 @@ class fgs_stats(C.Structure):
                 ("sort_ms", C.c_double), ("raster_ms", C.c_double), ("peak_aux_bytes", C.c_uint64)]
 
 
+class fgs_params(C.Structure):
+    _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("rotations", C.c_void_p), ("log_scales", C.c_void_p),
+                ("opacity_logits", C.c_void_p), ("sh", C.c_void_p)]
+
+
+class fgs_adam_options(C.Structure):
+    _fields_ = [(k, C.c_float) for k in ("lr_mean", "lr_rotation", "lr_log_scale", "lr_opacity", "lr_sh_dc",
+                                         "lr_sh_rest", "beta1", "beta2", "eps")]
+
+
+class fgs_adam_state(C.Structure):
+    _fields_ = [("step", C.c_int64), ("m", fgs_gradients), ("v", fgs_gradients)]
+
+
+class fgs_train_options(C.Structure):
+    _fields_ = [("sh_degree", C.c_int32), ("background", C.c_float * 3), ("lam", C.c_float),
+                ("adam", fgs_adam_options)]
+
+
 EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs_forward", "fgs_backward",
            "fgs_render_host", "fgs_backward_host", "fgs_set_flags", "fgs_debug_get", "fgs_last_counts",
-           "fgs_timing", "fgs_measure_fp32_peak"]
+           "fgs_timing", "fgs_measure_fp32_peak", "fgs_l1_dssim_loss", "fgs_adam_step", "fgs_train_step"]
 
 _lib = None
 
@@ -87,5 +106,12 @@ def load(path: str = LIB_PATH):
     L.fgs_timing.restype = i32
     L.fgs_measure_fp32_peak.argtypes = [vp, P(C.c_double)]
     L.fgs_measure_fp32_peak.restype = i32
+    L.fgs_l1_dssim_loss.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_float, vp, P(C.c_double)]
+    L.fgs_l1_dssim_loss.restype = i32
+    L.fgs_adam_step.argtypes = [vp, P(fgs_params), P(fgs_gradients), P(fgs_adam_state), P(fgs_adam_options)]
+    L.fgs_adam_step.restype = i32
+    L.fgs_train_step.argtypes = [vp, P(fgs_params), P(fgs_camera), vp, P(fgs_train_options), P(fgs_adam_state),
+                                 P(C.c_double)]
+    L.fgs_train_step.restype = i32
     _lib = L
     return L

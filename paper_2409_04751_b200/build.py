@@ -25,6 +25,7 @@ SOURCES = {
     "preprocess.cu": ["--fmad=false"],
     "binning.cu": [],
     "raster.cu": [],
+    "train.cu": [],
     "fgs_api.cu": [],
 }
 

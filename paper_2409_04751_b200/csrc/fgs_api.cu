@@ -7,6 +7,7 @@
 // Backward (reference backward, inc/gradients.hpp:207-267):
 //   K4a reverse blend (per-intersection partials) -> K4b preprocess backward.
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -62,6 +63,10 @@ struct fgs_context {
   DevBuf<uint64_t> keys;
   DevBuf<uint32_t> emit_gauss, sorted_gauss, emit_pos;
   DevBuf<float> partials, partial_tile;
+  // training step
+  DevBuf<float> t_image, t_dimage, t_grads, t_maps;
+  DevBuf<double> t_part;
+  DevBuf<int> t_flag;
   // per tile / pixel
   DevBuf<uint32_t> tile_offsets, fill, last, tile_order;
   DevBuf<int32_t> rowdiff;  // zero between frames (K2a zeroes what K1 added)
@@ -215,7 +220,8 @@ int fgs_destroy(fgs_context* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   else cudaDeviceSynchronize();
-  for (auto* b : {&ctx->final_T, &ctx->partials, &ctx->partial_tile, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
+  for (auto* b : {&ctx->final_T, &ctx->partials, &ctx->partial_tile, &ctx->t_image, &ctx->t_dimage, &ctx->t_grads,
+                  &ctx->t_maps, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
                   &ctx->h_sh, &ctx->h_img, &ctx->h_dl, &ctx->h_grad})
     b->release();
   ctx->rec.release();
@@ -225,6 +231,8 @@ int fgs_destroy(fgs_context* ctx) {
                   &ctx->scalars})
     b->release();
   ctx->keys.release();
+  ctx->t_part.release();
+  ctx->t_flag.release();
   ctx->rowdiff.release();
   ctx->rect.release();
   ctx->radii.release();
@@ -635,6 +643,107 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
   }
   FGS_CHECK(cudaStreamSynchronize(st));
   return FGS_OK;
+}
+
+int fgs_l1_dssim_loss(fgs_context* ctx, const float* rendered, const float* target, int32_t width, int32_t height,
+                      float lambda, float* d_rendered, double out[3]) {
+  if (!ctx) return FGS_EINVAL;
+  if (!rendered || !target || !d_rendered || !out) return fail(ctx, FGS_EINVAL, "l1_dssim_loss: null argument");
+  if (width <= 0 || height <= 0) return fail(ctx, FGS_EINVAL, "l1_dssim_loss: image dimensions differ");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  FGS_CHECK(ctx->t_maps.ensure(fgs::loss_scratch_floats(width, height)));
+  const size_t nb = fgs::loss_partials(width, height);
+  FGS_CHECK(ctx->t_part.ensure(2 * nb + 2));
+  ctx->launches += fgs::l1_dssim_loss(rendered, target, width, height, lambda, d_rendered, ctx->t_maps.p,
+                                      ctx->t_part.p, st);
+  double sums[2];
+  FGS_CHECK(cudaMemcpyAsync(sums, ctx->t_part.p + 2 * nb, sizeof(sums), cudaMemcpyDeviceToHost, st));
+  FGS_CHECK(cudaStreamSynchronize(st));
+  FGS_CHECK(cudaGetLastError());
+  const double norm = 1.0 / (3.0 * static_cast<double>(width) * height);
+  const double l1 = sums[1] * norm, dssim = 1.0 - sums[0] * norm;
+  out[0] = (1.0 - lambda) * l1 + lambda * dssim;
+  out[1] = l1;
+  out[2] = dssim;
+  return FGS_OK;
+}
+
+int fgs_adam_step(fgs_context* ctx, fgs_params* params, const fgs_gradients* grads, fgs_adam_state* state,
+                  const fgs_adam_options* o) {
+  if (!ctx) return FGS_EINVAL;
+  if (!params || !grads || !state || !o) return fail(ctx, FGS_EINVAL, "adam_step: null argument");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int64_t n = params->n;
+  fgs::AdamArgs a{};
+  float* p[5] = {params->means, params->rotations, params->log_scales, params->opacity_logits, params->sh};
+  const float* g[5] = {grads->d_means, grads->d_rotations, grads->d_log_scales, grads->d_opacity_logits, grads->d_sh};
+  float* m[5] = {state->m.d_means, state->m.d_rotations, state->m.d_log_scales, state->m.d_opacity_logits,
+                 state->m.d_sh};
+  float* v[5] = {state->v.d_means, state->v.d_rotations, state->v.d_log_scales, state->v.d_opacity_logits,
+                 state->v.d_sh};
+  const int w[5] = {3, 4, 3, 1, 48};
+  for (int k = 0; k < 5; ++k) {
+    if (n > 0 && (!p[k] || !g[k] || !m[k] || !v[k])) return fail(ctx, FGS_EINVAL, "adam_step: null array");
+    a.p[k] = p[k];
+    a.g[k] = g[k];
+    a.m[k] = m[k];
+    a.v[k] = v[k];
+    a.len[k] = n * w[k];
+    a.width[k] = w[k];
+  }
+  const float lr[6] = {o->lr_mean, o->lr_rotation, o->lr_log_scale, o->lr_opacity, o->lr_sh_dc, o->lr_sh_rest};
+  for (int k = 0; k < 6; ++k) a.lr[k] = lr[k];
+  a.beta1 = o->beta1;
+  a.beta2 = o->beta2;
+  a.eps = o->eps;
+  FGS_CHECK(ctx->t_flag.ensure(1));
+  a.nonfinite = ctx->t_flag.p;
+  const int big = 0x7fffffff;
+  FGS_CHECK(cudaMemcpyAsync(ctx->t_flag.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  ctx->launches += fgs::adam_check(a, st);
+  int first_bad = big;
+  FGS_CHECK(cudaMemcpyAsync(&first_bad, ctx->t_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FGS_CHECK(cudaStreamSynchronize(st));
+  if (first_bad != big)
+    return fail(ctx, FGS_ENONFINITE, "adam_step: non-finite gradient for Gaussian " + std::to_string(first_bad));
+  // bias corrections in double, as the reference's std::pow on its double state
+  const int64_t step = state->step + 1;
+  a.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(o->beta1), static_cast<double>(step)));
+  a.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(o->beta2), static_cast<double>(step)));
+  ctx->launches += fgs::adam_step(a, st);
+  FGS_CHECK(cudaGetLastError());
+  state->step = step;
+  return FGS_OK;
+}
+
+int fgs_train_step(fgs_context* ctx, fgs_params* params, const fgs_camera* camera, const float* target,
+                   const fgs_train_options* opt, fgs_adam_state* state, double loss_out[3]) {
+  if (!ctx) return FGS_EINVAL;
+  if (!params || !camera || !target || !opt || !state || !loss_out)
+    return fail(ctx, FGS_EINVAL, "train_step: null argument");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  const int64_t n = params->n;
+  const size_t npix = static_cast<size_t>(camera->width) * camera->height;
+  FGS_CHECK(ctx->t_image.ensure(npix * 3));
+  FGS_CHECK(ctx->t_dimage.ensure(npix * 3));
+  FGS_CHECK(ctx->t_grads.ensure(static_cast<size_t>(n > 0 ? n : 1) * 59));
+  const fgs_gaussians scene{n, params->means, params->rotations, params->log_scales, params->opacity_logits, params->sh};
+  fgs_render_options ro{opt->sh_degree, 1, {opt->background[0], opt->background[1], opt->background[2]}};
+  int rc = fgs_forward(ctx, &scene, camera, &ro, ctx->t_image.p, nullptr, nullptr);
+  if (rc != FGS_OK) return rc;
+  rc = fgs_l1_dssim_loss(ctx, ctx->t_image.p, target, camera->width, camera->height, opt->lambda, ctx->t_dimage.p,
+                         loss_out);
+  if (rc != FGS_OK) return rc;
+  if (!std::isfinite(loss_out[0])) return fail(ctx, FGS_ENONFINITE, "train: loss diverged (non-finite)");
+  float* gb = ctx->t_grads.p;
+  const size_t nn = static_cast<size_t>(n);
+  fgs_gradients gr{gb, gb + 3 * nn, gb + 7 * nn, gb + 10 * nn, gb + 11 * nn};
+  fgs_backward_options bo{{1.f, 1.f, 1.f}, opt->adam.lr_sh_rest != 0.0f ? 1 : 0, 0, 0};
+  rc = fgs_backward(ctx, &scene, camera, ctx->t_dimage.p, &bo, &gr);
+  if (rc != FGS_OK) return rc;
+  return fgs_adam_step(ctx, params, &gr, state, &opt->adam);
 }
 
 int fgs_timing(fgs_context* ctx, double ms[6], uint64_t calls[2], uint64_t* launches, int reset) {

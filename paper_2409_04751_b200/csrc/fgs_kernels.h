@@ -122,6 +122,28 @@ cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* ke
 // ---- blend (raster.cu) ----
 int blend_forward(const BlendArgs& a, cudaStream_t st);
 int blend_backward(const BlendArgs& a, cudaStream_t st);
+// ---- training step (train.cu) ----
+// L1 + D-SSIM loss and dL/drendered (inc/metrics.hpp:86-195). maps: loss_scratch_floats();
+// partials: 2 * loss_partials() + 2 doubles, the last two = (sum of SSIM map, sum |x - y|).
+size_t loss_scratch_floats(int width, int height);
+size_t loss_partials(int width, int height);
+int l1_dssim_loss(const float* rendered, const float* target, int width, int height, float lambda, float* d_rendered,
+                  float* maps, double* partials, cudaStream_t st);
+
+struct AdamArgs {  // groups: means, rotations, log_scales, opacities, sh
+  float* p[5];
+  const float* g[5];
+  float* m[5];
+  float* v[5];
+  int64_t len[5];
+  int width[5];  // floats per Gaussian: 3, 4, 3, 1, 48
+  float lr[6];  // mean, rotation, log_scale, opacity, sh DC, sh higher bands
+  float beta1, beta2, eps, bc1, bc2;
+  int* nonfinite;  // min offending Gaussian index (INT_MAX = all finite)
+};
+int adam_check(AdamArgs& a, cudaStream_t st);
+int adam_step(AdamArgs& a, cudaStream_t st);
+
 // FP32 pipe probe: returns achieved non-FMA fp32 op/s (FMUL + FADD, no contraction).
 double fp32_peak_probe(cudaStream_t st);
 
