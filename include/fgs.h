@@ -196,6 +196,22 @@ typedef struct fgs_train_options {
 int fgs_train_step(fgs_context* ctx, fgs_params* params, const fgs_camera* camera, const float* target,
                    const fgs_train_options* options, fgs_adam_state* state, double loss_out[3]);
 
+/* ---- Validation ---- */
+
+/* The reference's brute-force renderer (inc/oracle.hpp:161-270) on the GPU in double: every
+ * splat in global (depth, source) order gated per 16x16 tile, with an independent projection /
+ * covariance / SH transcription (no code shared with the fast path). Scene: device fp32 arrays
+ * (cast to double); image: device double H*W*3; transmittance: device double H*W or NULL.
+ * Synchronises. For large-scene checks of fgs_forward and for finite-difference gradchecks. */
+int fgs_bruteforce_render(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, int32_t sh_degree,
+                          const double background[3], double* image, double* transmittance);
+/* Same with a double-precision scene (device arrays in the fgs_gaussians layout): the
+ * finite-difference gradcheck (inc/oracle.hpp:338-418) perturbs parameters in double. */
+int fgs_bruteforce_render_f64(fgs_context* ctx, int64_t n, const double* means, const double* rotations,
+                              const double* log_scales, const double* opacity_logits, const double* sh,
+                              const fgs_camera* camera, int32_t sh_degree, const double background[3], double* image,
+                              double* transmittance);
+
 /* Counters of the last forward: [n, num_splats, num_intersections, tiles_x, tiles_y, width, height,
  * num_culled, num_degenerate]. */
 int fgs_last_counts(const fgs_context* ctx, int64_t out[9]);

@@ -26,6 +26,7 @@ SOURCES = {
     "binning.cu": [],
     "raster.cu": [],
     "train.cu": [],
+    "bruteforce.cu": [],
     "fgs_api.cu": [],
 }
 

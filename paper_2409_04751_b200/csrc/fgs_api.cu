@@ -746,6 +746,37 @@ int fgs_train_step(fgs_context* ctx, fgs_params* params, const fgs_camera* camer
   return fgs_adam_step(ctx, params, &gr, state, &opt->adam);
 }
 
+int fgs_bruteforce_render(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, int32_t sh_degree,
+                          const double background[3], double* image, double* transmittance) {
+  if (!ctx) return FGS_EINVAL;
+  if (!scene || !camera || !image) return fail(ctx, FGS_EINVAL, "bruteforce_render: null argument");
+  if (sh_degree < 0 || sh_degree > 3) return fail(ctx, FGS_EINVAL, "bruteforce_render: sh_degree must be 0..3");
+  if (camera->width <= 0 || camera->height <= 0) return fail(ctx, FGS_EINVAL, "bruteforce_render: empty image");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  const double zero[3] = {0.0, 0.0, 0.0};
+  FGS_CHECK(fgs::bruteforce_render(*scene, *camera, sh_degree, background ? background : zero, image, transmittance,
+                                   ctx->stream));
+  ctx->launches += 2;
+  return FGS_OK;
+}
+
+int fgs_bruteforce_render_f64(fgs_context* ctx, int64_t n, const double* means, const double* rotations,
+                              const double* log_scales, const double* opacity_logits, const double* sh,
+                              const fgs_camera* camera, int32_t sh_degree, const double background[3], double* image,
+                              double* transmittance) {
+  if (!ctx) return FGS_EINVAL;
+  if (!camera || !image || (n > 0 && (!means || !rotations || !log_scales || !opacity_logits || !sh)))
+    return fail(ctx, FGS_EINVAL, "bruteforce_render: null argument");
+  if (sh_degree < 0 || sh_degree > 3) return fail(ctx, FGS_EINVAL, "bruteforce_render: sh_degree must be 0..3");
+  if (camera->width <= 0 || camera->height <= 0) return fail(ctx, FGS_EINVAL, "bruteforce_render: empty image");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  const double zero[3] = {0.0, 0.0, 0.0};
+  FGS_CHECK(fgs::bruteforce_render_f64(n, means, rotations, log_scales, opacity_logits, sh, *camera, sh_degree,
+                                       background ? background : zero, image, transmittance, ctx->stream));
+  ctx->launches += 2;
+  return FGS_OK;
+}
+
 int fgs_timing(fgs_context* ctx, double ms[6], uint64_t calls[2], uint64_t* launches, int reset) {
   if (!ctx) return FGS_EINVAL;
   FGS_CHECK(cudaSetDevice(ctx->device));

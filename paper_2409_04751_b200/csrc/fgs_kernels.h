@@ -144,6 +144,17 @@ struct AdamArgs {  // groups: means, rotations, log_scales, opacities, sh
 int adam_check(AdamArgs& a, cudaStream_t st);
 int adam_step(AdamArgs& a, cudaStream_t st);
 
+// ---- brute-force validation renderer (bruteforce.cu), double precision ----
+}  // namespace fgs
+struct fgs_gaussians;
+struct fgs_camera;
+namespace fgs {
+cudaError_t bruteforce_render(const ::fgs_gaussians& scene, const ::fgs_camera& cam, int sh_degree, const double bg[3],
+                              double* image, double* transmittance, cudaStream_t st);
+cudaError_t bruteforce_render_f64(int64_t n, const double* means, const double* rotations, const double* log_scales,
+                                  const double* opacity, const double* sh, const ::fgs_camera& cam, int sh_degree,
+                                  const double bg[3], double* image, double* transmittance, cudaStream_t st);
+
 // FP32 pipe probe: returns achieved non-FMA fp32 op/s (FMUL + FADD, no contraction).
 double fp32_peak_probe(cudaStream_t st);
 
