@@ -30,9 +30,9 @@ METRICS = [
 # bench.py stage -> kernels it times
 STAGES = {
     "preprocess": ["preprocess_kernel"],
-    "binning+sort": ["bin_level1_kernel", "bin_level2_kernel"],
+    "binning+sort": ["bin_kernel"],
     "raster": ["blend_forward_kernel"],
-    "raster_backward": ["blend_backward_kernel", "combine_partials_kernel"],
+    "raster_backward": ["blend_backward_kernel"],
     "preprocess_backward": ["preprocess_backward_kernel"],
 }
 
