@@ -12,15 +12,16 @@
 //      Gaussian (compacted list), the intersection count I; then CTA 0 turns the row-difference
 //      array into per-tile counts, the tile ranges (offsets[0..T]) and the blend schedule;
 //   [host reads I (16 bytes) to size the per-intersection buffers]
-//   K2b bin_scatter_kernel: each intersection (Gaussian g, tile t, emission slot e) claims a
-//      slot in tile t's range with one atomicAdd and writes the 64-bit key (depth_key << 32 | e);
+//   K2b: each intersection (Gaussian g, tile t) claims a position in tile t's range with
+//      one atomicAdd and writes the 64-bit key (depth_key << 32 | g);
 //   K2c tile_sort_kernel: one CTA per tile sorts its keys (bitonic, in shared memory up to 4096
 //      entries, a chunked global/shared hybrid beyond) and writes the sorted Gaussian list.
 //
-// Emission slots e are assigned in source order (Gaussian-major, tiles ascending within a
-// Gaussian), so among the entries of one tile e increases with the source index: sorting by
-// (depth_key, e) is sorting by (depth_key, source index) -- the reference's order, bit-exact,
-// whatever order the atomics handed out the slots in.
+// The key is the reference's own sort key within a tile, (depth key bits, source index), so
+// sorting a tile's keys gives the reference's order bit-exactly, whatever order the atomics
+// handed out the positions in. Emission slots (source order, tiles ascending within a
+// Gaussian) index the backward's per-intersection gradients: slot = src_off[g] + the tile's
+// index in g's rectangle.
 
 #include <cooperative_groups.h>
 
@@ -274,8 +275,7 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     if (ev[u] >= hi) continue;
-    a.keys[pv[u]] = (static_cast<uint64_t>(a.depth_key[gv[u]]) << 32) | ev[u];
-    a.emit_gauss[ev[u]] = gv[u];
+    a.keys[pv[u]] = (static_cast<uint64_t>(a.depth_key[gv[u]]) << 32) | gv[u];
   }
   __syncthreads();  // s_cnt / s_off reused by the next range
 }
@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
         if (c[i]) {
           a.cval[pos] = static_cast<uint32_t>(r0 + i);
           a.coff[pos] = off;
+          a.src_off[r0 + i] = off;
           ++pos;
           off += c[i];
         }

@@ -56,12 +56,12 @@ struct fgs_context {
   // per Gaussian
   DevBuf<fgs::SortedRec> rec;
   DevBuf<uint8_t> state;
-  DevBuf<uint32_t> dkey, cval, coff, touched, scan_status;
+  DevBuf<uint32_t> dkey, cval, coff, src_off, touched, scan_status;
   DevBuf<ushort4> rect;
   DevBuf<int32_t> radii;
   // per intersection
   DevBuf<uint64_t> keys;
-  DevBuf<uint32_t> emit_gauss, sorted_gauss, emit_pos;
+  DevBuf<uint32_t> sorted_gauss;
   DevBuf<float> partials, partial_tile;
   // training step
   DevBuf<float> t_image, t_dimage, t_grads, t_maps;
@@ -226,8 +226,8 @@ int fgs_destroy(fgs_context* ctx) {
     b->release();
   ctx->rec.release();
   ctx->state.release();
-  for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->touched, &ctx->scan_status, &ctx->emit_gauss,
-                  &ctx->sorted_gauss, &ctx->emit_pos, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
+  for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->src_off, &ctx->touched, &ctx->scan_status,
+                  &ctx->sorted_gauss, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
                   &ctx->scalars})
     b->release();
   ctx->keys.release();
@@ -305,7 +305,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   const size_t npix = static_cast<size_t>(W) * H;
   FGS_CHECK(ctx->rec.ensure(nn));
   FGS_CHECK(ctx->state.ensure(nn));
-  for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->touched}) FGS_CHECK(b->ensure(nn));
+  for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->src_off, &ctx->touched}) FGS_CHECK(b->ensure(nn));
   FGS_CHECK(ctx->scan_status.ensure(fgs::bin_part_words()));
   FGS_CHECK(ctx->rect.ensure(nn));
   FGS_CHECK(ctx->radii.ensure(nn));
@@ -382,7 +382,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.tile_order = ctx->tile_order.p;
   bn.isect_cap = ctx->isect_cap;
   bn.keys = ctx->keys.p;
-  bn.emit_gauss = ctx->emit_gauss.p;
+  bn.src_off = ctx->src_off.p;
   if (n > 0) {
     ctx->rowdiff_clean = 0;  // dirty until K2 has consumed K1's counts
     FGS_CHECK(fgs::bin_launch(bn, st));
@@ -423,8 +423,6 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   auto launch_blend = [&]() -> int {
     ba.isect_cap = ctx->isect_cap;
     ba.keys = ctx->keys.p;
-    ba.emit_gauss = ctx->emit_gauss.p;
-    ba.emit_pos = ctx->emit_pos.p;
     ba.sorted_gauss = ctx->sorted_gauss.p;
     const int l = fgs::blend_forward(ba, st);
     if (timing) cudaEventRecord(ev[4], st);
@@ -450,14 +448,13 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     // speculative kernels, which exited without work) and launch for real
     const size_t ni = static_cast<size_t>(I > 0 ? I : 1);
     FGS_CHECK(ctx->keys.ensure(ni));
-    for (auto* b : {&ctx->emit_gauss, &ctx->sorted_gauss, &ctx->emit_pos}) FGS_CHECK(b->ensure(ni));
+    FGS_CHECK(ctx->sorted_gauss.ensure(ni));
     size_t cap = ctx->keys.cap;
-    for (auto* b : {&ctx->emit_gauss, &ctx->sorted_gauss, &ctx->emit_pos}) cap = std::min(cap, b->cap);
+    cap = std::min(cap, ctx->sorted_gauss.cap);
     ctx->isect_cap = static_cast<int64_t>(cap);
     if (n > 0 && I > 0) {
       bn.isect_cap = ctx->isect_cap;
       bn.keys = ctx->keys.p;
-      bn.emit_gauss = ctx->emit_gauss.p;
       bn.scatter_only = 1;
       FGS_CHECK(fgs::bin_launch(bn, st));
       bn.scatter_only = 0;
@@ -470,7 +467,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   FGS_CHECK(cudaGetLastError());
   ctx->launches += launches;
 
-  ctx->aux_bytes = nn * (48 + 1 + 4 * 5 + 8) + static_cast<size_t>(std::max<int64_t>(ctx->isect_cap, 1)) * (8 + 4 * 3) + (num_tiles + 1) * 4 * 3 + ndiff * 4 + npix * 8;
+  ctx->aux_bytes = nn * (48 + 1 + 4 * 6 + 8) + static_cast<size_t>(std::max<int64_t>(ctx->isect_cap, 1)) * (8 + 4) + (num_tiles + 1) * 4 * 3 + ndiff * 4 + npix * 8;
   ctx->have_fwd = true;
   if (stats) {
     FGS_CHECK(cudaEventSynchronize(ev[4]));
@@ -522,6 +519,8 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   ba.dl_dimage = dl_dimage;
   ba.partials = ctx->partials.p;
   ba.partial_tile = ctx->partial_tile.p;
+  ba.src_off = ctx->src_off.p;
+  ba.rect = ctx->rect.p;
   ba.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
   const bool timing = (ctx->flags & FGS_FLAG_TIMING) != 0;
   if (timing && ctx->pending.size() > 64) drain_sets(ctx, 8);
@@ -546,7 +545,6 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.state = ctx->state.p;
   pb.touched = ctx->touched.p;
   pb.coff = ctx->coff.p;
-  pb.emit_pos = ctx->emit_pos.p;
   pb.partials = ctx->partial_tile.p;
   pb.d_means = grads->d_means;
   pb.d_rotations = grads->d_rotations;
@@ -825,7 +823,6 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   if (nm == "radius") return copy(ctx->radii.p, n * 4);
   if (nm == "touched") return copy(ctx->touched.p, n * 4);
   if (nm == "sorted_gauss") return copy(ctx->sorted_gauss.p, I * 4);
-  if (nm == "emit_pos") return copy(ctx->emit_pos.p, I * 4);
   if (nm == "compact_gauss") return copy(ctx->cval.p, static_cast<size_t>(ctx->num_compact) * 4);
   if (nm == "compact_offsets") return copy(ctx->coff.p, static_cast<size_t>(ctx->num_compact) * 4);
   if (nm == "sorted_tile") {

@@ -48,8 +48,7 @@ struct PreprocessBackwardArgs {
   const uint8_t* state;
   const uint32_t* touched;
   const uint32_t* coff;      // [m] first emission slot of cval[q]
-  const uint32_t* emit_pos;  // [I] sorted position of each emission slot
-  const float* partials;     // [I][9] K4a per-intersection sums, sorted order
+  const float* partials;     // [I][9] K4a per-intersection sums by emission slot
   float* d_means;
   float* d_rotations;
   float* d_log_scales;
@@ -62,9 +61,9 @@ struct BlendArgs {
   int width, height, tiles_x, tiles_y;
   const uint32_t* tile_offsets;  // T+1
   uint32_t* sorted_gauss;        // I (written by the forward's per-tile sort, read by the backward)
-  uint64_t* keys;                // forward: tile list keys (K2b), sorted in place per tile
-  const uint32_t* emit_gauss;    // forward: Gaussian of each emission slot
-  uint32_t* emit_pos;            // forward: sorted position of each emission slot
+  uint64_t* keys;                // forward: tile list keys (K2), sorted in place per tile
+  const uint32_t* src_off;       // backward: first emission slot of each tile-touching Gaussian
+  const ushort4* rect;           // backward: tile rectangle per Gaussian
   const SortedRec* rec;          // per-Gaussian records
   float bg[3];
   float* image;                  // H*W*3
@@ -78,7 +77,7 @@ struct BlendArgs {
   // backward
   const float* dl_dimage;
   float* partials;               // I x 8 x 9 per-(entry, pixel block) sums
-  float* partial_tile;           // I x 9 per-entry sums (backward epilogue)
+  float* partial_tile;           // I x 9 per-intersection sums by emission slot (backward epilogue)
 };
 
 __global__ void preprocess_kernel(PreprocessArgs a);
@@ -100,6 +99,7 @@ struct BinArgs {
   int32_t* rowdiff;            // [tiles_y * (tiles_x + 1)] row-difference tile counts (K1 adds, bin_scan zeroes)
   uint32_t* cval;              // [n] tile-touching Gaussians in source order (compacted)
   uint32_t* coff;              // [n] their first emission slot
+  uint32_t* src_off;           // [n] first emission slot by Gaussian id (tile-touching ones)
   uint32_t* scalars;           // device scalars (kScalar*)
   uint32_t* part_scan;         // [2 * grid]
   uint32_t* tile_offsets;      // [num_tiles + 1]
@@ -107,7 +107,6 @@ struct BinArgs {
   uint32_t* tile_order;        // [num_tiles] blend schedule (optional)
   // per intersection
   uint64_t* keys;              // [I] (depth_key << 32 | emission slot), grouped by tile
-  uint32_t* emit_gauss;        // [I] Gaussian of each emission slot
 };
 
 // Words of part_scan scratch bin_scan needs.

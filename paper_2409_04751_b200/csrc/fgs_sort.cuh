@@ -1,4 +1,4 @@
-// fgs_sort.cuh — per-tile bitonic sort of the (depth_key << 32 | emission slot) keys, run by
+// fgs_sort.cuh — per-tile bitonic sort of the (depth_key << 32 | Gaussian id) keys, run by
 // the forward blend's CTA on its own tile before blending (raster.cu).
 //
 // Ascending comparators only: stage (k, j) pairs index i with its mirror in the k-block
@@ -180,12 +180,10 @@ __device__ __forceinline__ int pow2_ceil(int x) {
   return p;
 }
 
-// Sort the tile list keys[lo, lo + L) (CTA-wide call, all kSortThreads threads). Writes the
-// sorted Gaussian ids (sorted_gauss[lo + k]) and the emission slot -> position map
-// (emit_pos[e] = lo + k). Returns true when the ids are also left in shared memory: g of
+// Sort the tile list keys[lo, lo + L) (CTA-wide call, all kSortThreads threads) by
+// (depth key, Gaussian id) and write the sorted Gaussian ids (sorted_gauss[lo + k]). Returns true when the ids are also left in shared memory: g of
 // entry k at ((uint32_t*)s)[2k] (lists of <= kSortCap keys); else read sorted_gauss.
-__device__ bool sort_tile_list(uint64_t* keys, const uint32_t* __restrict__ emit_gauss, uint32_t* emit_pos,
-                               uint32_t* sorted_gauss, uint32_t lo, int L, uint64_t* s) {
+__device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t lo, int L, uint64_t* s) {
   const int tid = threadIdx.x, lane = tid & 31;
   uint32_t* s32 = reinterpret_cast<uint32_t*>(s);
   uint64_t* g = keys + lo;
@@ -205,9 +203,7 @@ __device__ bool sort_tile_list(uint64_t* keys, const uint32_t* __restrict__ emit
         for (int r = 0; r < E; ++r) {
           const int i = r * 32 + lane;
           if (i < L) {
-            const uint32_t e = static_cast<uint32_t>(x[r]);
-            const uint32_t gi = emit_gauss[e];
-            emit_pos[e] = lo + i;
+            const uint32_t gi = static_cast<uint32_t>(x[r]);
             sorted_gauss[lo + i] = gi;
             s32[2 * i] = gi;
           }
@@ -226,9 +222,7 @@ __device__ bool sort_tile_list(uint64_t* keys, const uint32_t* __restrict__ emit
     for (int k = tid; k < P; k += kSortThreads) s[k] = k < L ? g[k] : ~0ull;
     cta_sort(s, P);
     for (int k = tid; k < L; k += kSortThreads) {
-      const uint32_t e = static_cast<uint32_t>(s[k]);
-      const uint32_t gi = emit_gauss[e];
-      emit_pos[e] = lo + k;
+      const uint32_t gi = static_cast<uint32_t>(s[k]);
       sorted_gauss[lo + k] = gi;
       s32[2 * k] = gi;
     }
@@ -266,10 +260,7 @@ __device__ bool sort_tile_list(uint64_t* keys, const uint32_t* __restrict__ emit
   }
   __syncthreads();
   for (int k = tid; k < L; k += kSortThreads) {
-    const uint32_t e = static_cast<uint32_t>(g[k]);
-    const uint32_t gi = emit_gauss[e];
-    emit_pos[e] = lo + k;
-    sorted_gauss[lo + k] = gi;
+    sorted_gauss[lo + k] = static_cast<uint32_t>(g[k]);
   }
   __syncthreads();
   return false;

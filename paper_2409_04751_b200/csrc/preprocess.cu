@@ -666,16 +666,16 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
 
 // K4b: one thread per Gaussian that touched a tile, taken in source order from the K2a
 // compaction list (cval), 128 per CTA. K4a left one 9-float gradient sum per intersection at
-// its sorted position; the Gaussian's emission slots [coff[q], +touched[g]) (ascending tile
-// order) map to those positions (emit_pos), and they are summed here in tile order:
+// its emission slot; the Gaussian's slots [coff[q], +touched[g]) are contiguous in ascending
+// tile order and are summed here in that order:
 // deterministic, no atomics (gradients.hpp:161-173). Gaussians that touched no tile have zero
 // gradient; CTA b also zero-fills, with coalesced stores, the non-touching rows between its
 // predecessor's last Gaussian and its own last one -- so every sector of that source range
 // is written by one CTA in a short window and L2 merges the partial-sector writes.
-// One intersection's screen-space gradient (the blend backward's per-entry sum at its sorted
-// position) added into acc.
+// One intersection's screen-space gradient (the blend backward's per-intersection sum at its
+// emission slot) added into acc.
 __device__ __forceinline__ void intersection_sum(const PreprocessBackwardArgs& a, uint32_t e, float* acc) {
-  const float* p = a.partials + static_cast<size_t>(__ldg(a.emit_pos + e)) * 9;
+  const float* p = a.partials + static_cast<size_t>(e) * 9;
 #pragma unroll
   for (int q = 0; q < 9; ++q) acc[q] = acc[q] + p[q];
 }

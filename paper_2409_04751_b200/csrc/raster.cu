@@ -104,8 +104,7 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(BlendArgs a) {
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
   const long long t_start = COUNTERS ? clock64() : 0;
   // sort the tile's (depth, emission slot) keys; the ids stay in shared memory when they fit
-  const bool ids_smem = sort_tile_list(a.keys, a.emit_gauss, a.emit_pos, a.sorted_gauss, lo,
-                                       static_cast<int>(hi - lo), skeys);
+  const bool ids_smem = sort_tile_list(a.keys, a.sorted_gauss, lo, static_cast<int>(hi - lo), skeys);
   const uint32_t* sid = reinterpret_cast<const uint32_t*>(skeys);
   auto rec_at = [&](uint32_t k) -> SortedRec {
     return a.rec[ids_smem ? sid[2 * (k - lo)] : __ldg(a.sorted_gauss + k)];
@@ -392,10 +391,15 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     __syncwarp();
   }
   // Epilogue: per entry of the tile, the 9 gradients summed over the pixel blocks that passed
-  // the culling test, in block order (the partials are this CTA's own, L2-resident writes).
+  // the culling test, in block order (the partials are this CTA's own, L2-resident writes),
+  // stored at the intersection's emission slot (K4b then reads each Gaussian's contiguously).
   __syncthreads();
   for (uint32_t k = lo + threadIdx.x; k < hi; k += kBlend) {
-    const SortedRec r = load_rec(a, k);
+    const uint32_t g = __ldg(a.sorted_gauss + k);
+    const SortedRec r = a.rec[g];
+    const ushort4 rc = a.rect[g];
+    // emission slot of (g, this tile): g's first slot + the tile's index in its rectangle
+    const uint32_t e = a.src_off[g] + static_cast<uint32_t>((ty - rc.z) * (rc.y - rc.x + 1) + (tx - rc.x));
     const float* p = part + static_cast<size_t>(k) * (kBwdWarps * 9);
     float sg[9];
 #pragma unroll
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
 #pragma unroll
       for (int q = 0; q < 9; ++q) sg[q] = sg[q] + p[w * 9 + q];
     }
-    float* o = a.partial_tile + static_cast<size_t>(k) * 9;
+    float* o = a.partial_tile + static_cast<size_t>(e) * 9;
 #pragma unroll
     for (int q = 0; q < 9; ++q) o[q] = sg[q];
   }
