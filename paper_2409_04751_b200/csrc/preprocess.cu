@@ -279,6 +279,23 @@ __device__ __forceinline__ void load_sh(const float* __restrict__ sh, int64_t g,
   }
 }
 
+// The 16 coefficients of one colour channel, vectorised (channel rows are 64-byte aligned).
+__device__ __forceinline__ void load_sh16(const float* __restrict__ sh, int64_t g, int ch, int degree, float k[16]) {
+  const float* p = sh + g * 48 + 16 * ch;
+  if (degree == 0) {
+    k[0] = __ldg(p);
+#pragma unroll
+    for (int j = 1; j < 16; ++j) k[j] = 0.0f;
+    return;
+  }
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 v = __ldg(p4 + q);
+    k[4 * q + 0] = v.x; k[4 * q + 1] = v.y; k[4 * q + 2] = v.z; k[4 * q + 3] = v.w;
+  }
+}
+
 // The 16 coefficients of one colour channel (only the SH view-direction gradient needs them).
 __device__ __forceinline__ void load_sh_channel(const float* __restrict__ sh, int64_t g, int ch, int degree,
                                                 float k[16]) {
@@ -406,11 +423,15 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
       view_dir(cam, m, dir);
       float Y[16];
       sh_basis(dir, a.sh_degree, Y);
-      float k[48];
-      load_sh(a.sh, i, a.sh_degree, k);
-      const float col0 = sh_channel(k, Y, a.sh_degree);
-      const float col1 = sh_channel(k + 16, Y, a.sh_degree);
-      const float col2 = sh_channel(k + 32, Y, a.sh_degree);
+      // one colour channel at a time (16 live coefficients instead of 48)
+      float col[3];
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        float k[16];
+        load_sh16(a.sh, i, ch, a.sh_degree, k);
+        col[ch] = sh_channel(k, Y, a.sh_degree);
+      }
+      const float col0 = col[0], col1 = col[1], col2 = col[2];
       const float alpha = sigmoid(__ldg(a.opacity + i));
       r0 = make_float4(mx, my, ca, cb);
       r1 = make_float4(cc, alpha, col0, col1);
@@ -450,7 +471,7 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
 
 
 // K1: one thread per Gaussian.
-__global__ void __launch_bounds__(256) preprocess_kernel(PreprocessArgs a) {
+__global__ void __launch_bounds__(256, 4) preprocess_kernel(PreprocessArgs a) {
   __shared__ unsigned s_counts[2];
   if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
   __syncthreads();
