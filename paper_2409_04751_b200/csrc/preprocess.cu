@@ -263,22 +263,6 @@ __device__ __forceinline__ void sh_dir_grad(const float d[3], int degree, const 
   ddir[2] += gz * dc;
 }
 
-__device__ __forceinline__ void load_sh(const float* __restrict__ sh, int64_t g, int degree, float k[48]) {
-  const float* p = sh + g * 48;
-  if (degree == 0) {
-    k[0] = __ldg(p);
-    k[16] = __ldg(p + 16);
-    k[32] = __ldg(p + 32);
-    return;
-  }
-  const float4* p4 = reinterpret_cast<const float4*>(p);
-#pragma unroll
-  for (int i = 0; i < 12; ++i) {
-    const float4 v = __ldg(p4 + i);
-    k[4 * i + 0] = v.x; k[4 * i + 1] = v.y; k[4 * i + 2] = v.z; k[4 * i + 3] = v.w;
-  }
-}
-
 // The 16 coefficients of one colour channel, vectorised (channel rows are 64-byte aligned).
 __device__ __forceinline__ void load_sh16(const float* __restrict__ sh, int64_t g, int ch, int degree, float k[16]) {
   const float* p = sh + g * 48 + 16 * ch;
