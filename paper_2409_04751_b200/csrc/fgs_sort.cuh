@@ -124,29 +124,35 @@ __device__ __forceinline__ void ce(uint64_t* s, int i, int p) {
 constexpr int kChunk = 256;  // keys per warp register chunk (E = 8)
 constexpr int kSortWarps = kSortThreads / 32;
 
-// Register phase over the shared array s[0, n) (n a multiple of kChunk): every warp loads its
-// 256-key chunks, runs a full sort (first) or the half-cleaner stages j < 256 of a merge level,
-// and stores them back. Callers barrier before and after.
-template <bool kFull>
+// Register phase over the shared array s[0, n) (n a multiple of the chunk 32*E): every warp
+// loads its chunks, runs a full sort (first) or the half-cleaner stages j < 32E of a merge
+// level, and stores them back. Callers barrier before and after.
+template <int E, bool kFull>
 __device__ __forceinline__ void chunk_phase(uint64_t* s, int n) {
+  constexpr int CH = 32 * E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = warp * kChunk; c < n; c += kSortWarps * kChunk) {
-    uint64_t x[8];
+  for (int c = warp * CH; c < n; c += kSortWarps * CH) {
+    uint64_t x[E];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) x[r] = s[c + r * 32 + lane];
-    if (kFull) warp_sort<8>(x, lane);
-    else warp_halfclean<8>(x, lane);
+    for (int r = 0; r < E; ++r) x[r] = s[c + r * 32 + lane];
+    if (kFull) warp_sort<E>(x, lane);
+    else warp_halfclean<E>(x, lane);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) s[c + r * 32 + lane] = x[r];
+    for (int r = 0; r < E; ++r) s[c + r * 32 + lane] = x[r];
   }
 }
 
-// Ascending sort of s[0, n), n a power of two in [kChunk, kSortCap], by the whole CTA.
-__device__ void cta_sort(uint64_t* s, int n) {
+// Ascending sort of s[0, n) (n a power of two, n >= 256 * E / 8... i.e. a multiple of 32E) by
+// the whole CTA: chunks of 32E keys sorted in registers, then every merge level's stages with
+// j >= 32E in shared memory and the rest in registers. E is chosen so that the first phase
+// keeps all warps busy (n / 32E >= kSortWarps where possible).
+template <int E>
+__device__ void cta_sort_e(uint64_t* s, int n) {
+  constexpr int CH = 32 * E;
   __syncthreads();
-  chunk_phase<true>(s, n);
-  for (int k = 2 * kChunk; k <= n; k <<= 1) {
-    for (int j = k >> 1; j >= kChunk; j >>= 1) {
+  chunk_phase<E, true>(s, n);
+  for (int k = 2 * CH; k <= n; k <<= 1) {
+    for (int j = k >> 1; j >= CH; j >>= 1) {
       __syncthreads();
       for (int c = threadIdx.x; c < (n >> 1); c += kSortThreads) {
         int i, p;
@@ -155,9 +161,15 @@ __device__ void cta_sort(uint64_t* s, int n) {
       }
     }
     __syncthreads();
-    chunk_phase<false>(s, n);
+    chunk_phase<E, false>(s, n);
   }
   __syncthreads();
+}
+
+__device__ void cta_sort(uint64_t* s, int n) {
+  if (n <= 512) cta_sort_e<2>(s, n);
+  else if (n <= 1024) cta_sort_e<4>(s, n);
+  else cta_sort_e<8>(s, n);
 }
 
 // Stages j = C/2 .. 1 of a merge level k > C on the shared chunk s[0, C) (C = kSortCap).
@@ -170,7 +182,7 @@ __device__ void cta_halfclean(uint64_t* s) {
     }
   }
   __syncthreads();
-  chunk_phase<false>(s, kSortCap);
+  chunk_phase<8, false>(s, kSortCap);
   __syncthreads();
 }
 

@@ -105,6 +105,14 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(BlendArgs a) {
   const long long t_start = COUNTERS ? clock64() : 0;
   // sort the tile's (depth, emission slot) keys; the ids stay in shared memory when they fit
   const bool ids_smem = sort_tile_list(a.keys, a.sorted_gauss, lo, static_cast<int>(hi - lo), skeys);
+  if (COUNTERS && threadIdx.x == 0) {
+    // sort-phase instrumentation: [4] sort cycles of small lists, [5] of long lists, [6] count long
+    const unsigned long long sc = static_cast<unsigned long long>(clock64() - t_start);
+    const bool big = hi - lo > 256;
+    atomicAdd(a.counters + (big ? 5 : 4), sc);
+    if (big) atomicAdd(a.counters + 6, 1ull);
+    atomicAdd(a.counters + 7, 1ull);
+  }
   const uint32_t* sid = reinterpret_cast<const uint32_t*>(skeys);
   auto rec_at = [&](uint32_t k) -> SortedRec {
     return a.rec[ids_smem ? sid[2 * (k - lo)] : __ldg(a.sorted_gauss + k)];
