@@ -206,7 +206,7 @@ int fgs_create(int device, fgs_context** out) {
   }
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   cudaEventCreateWithFlags(&ctx->ev_scan, cudaEventDisableTiming);
-  if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(8) != cudaSuccess ||
+  if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(16) != cudaSuccess ||
       false) {
     fgs_destroy(ctx);
     return FGS_ENOMEM;
@@ -336,7 +336,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   uint64_t launches = 0;
 
   FGS_CHECK(cudaMemsetAsync(ctx->scalars.p, 0, 16 * sizeof(uint32_t), st));
-  if (ctx->flags & FGS_FLAG_COUNTERS) FGS_CHECK(cudaMemsetAsync(ctx->counters.p, 0, 8 * sizeof(unsigned long long), st));
+  if (ctx->flags & FGS_FLAG_COUNTERS) FGS_CHECK(cudaMemsetAsync(ctx->counters.p, 0, 16 * sizeof(unsigned long long), st));
   if (n > 0) {
     fgs::PreprocessArgs pa{};
     pa.n = n;
@@ -518,6 +518,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   ba.last = ctx->last.p;
   ba.dl_dimage = dl_dimage;
   ba.partials = ctx->partials.p;
+  ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
   ba.partial_tile = ctx->partial_tile.p;
   ba.src_off = ctx->src_off.p;
   ba.rect = ctx->rect.p;
@@ -841,7 +842,7 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   if (nm == "final_T") return copy(ctx->final_T.p, npix * 4);
   if (nm == "last") return copy(ctx->last.p, npix * 4);
   if (nm == "counters") return copy(ctx->counters.p, 4 * sizeof(unsigned long long));
-  if (nm == "counters8") return copy(ctx->counters.p, 8 * sizeof(unsigned long long));
+  if (nm == "counters16") return copy(ctx->counters.p, 16 * sizeof(unsigned long long));
   if (nm == "tile_cycles") return copy(ctx->tile_cycles.p, nt * sizeof(unsigned long long));
   if (nm == "key_tile" || nm == "key_depth" || nm == "key_gauss") {
     if (!dst) return static_cast<int64_t>(I * 4);

@@ -8,7 +8,7 @@ for cfg in (2,3):
     for _ in range(3): r.forward(ds, cams[0], RenderOptions(sh_degree=deg))
     r.set_flags(_lib.FGS_FLAG_COUNTERS)
     r.forward(ds, cams[0], RenderOptions(sh_degree=deg)); torch.cuda.synchronize()
-    c = r.debug("counters8", np.uint64).astype(np.float64)
+    c = r.debug("counters16", np.uint64).astype(np.float64)
     tc = r.debug("tile_cycles", np.uint64).astype(np.float64)
     ntiles = c[7]; nbig = c[6]
     print(cfg, "tiles", ntiles, "big", nbig, "avg small sort cycles", c[4]/max(1,ntiles-nbig), "avg big sort cycles", c[5]/max(1,nbig),
