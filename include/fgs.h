@@ -116,11 +116,16 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
                  const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
 
 /* Host-buffer variants with the reference's calling convention: inputs and outputs in host
- * memory, host<->device copies included; blocking. */
+ * memory, host<->device transfers included; blocking. Scene arrays in page-locked (pinned)
+ * host memory are read in place over PCIe (zero copy: every Gaussian's geometry, the opacity
+ * and SH rows only of the splats that survive the culls); pageable ones are copied whole. */
 int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                     const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats);
 int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                       const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
+
+/* PCIe bytes moved by the last fgs_render_host / fgs_backward_host call: out = {h2d, d2h}. */
+int fgs_last_transfer(const fgs_context* ctx, uint64_t out[2]);
 
 /* Flags: FGS_FLAG_COUNTERS makes the forward blend count E_eval / E_contrib (atomics; slower);
  * FGS_FLAG_TIMING records CUDA events around every stage (read with fgs_timing). Default 0. */

@@ -67,7 +67,7 @@ class fgs_train_options(C.Structure):
 EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs_forward", "fgs_backward",
            "fgs_render_host", "fgs_backward_host", "fgs_set_flags", "fgs_debug_get", "fgs_last_counts",
            "fgs_timing", "fgs_measure_fp32_peak", "fgs_l1_dssim_loss", "fgs_adam_step", "fgs_train_step",
-           "fgs_bruteforce_render", "fgs_bruteforce_render_f64"]
+           "fgs_bruteforce_render", "fgs_bruteforce_render_f64", "fgs_last_transfer"]
 
 _lib = None
 
@@ -119,5 +119,7 @@ def load(path: str = LIB_PATH):
     L.fgs_bruteforce_render_f64.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, P(fgs_camera), C.c_int32,
                                             P(C.c_double), vp, vp]
     L.fgs_bruteforce_render_f64.restype = i32
+    L.fgs_last_transfer.argtypes = [vp, P(C.c_uint64)]
+    L.fgs_last_transfer.restype = i32
     _lib = L
     return L

@@ -190,6 +190,13 @@ class Rasterizer:
         self._check(rc)
         return grads
 
+    def last_transfer(self) -> dict:
+        """PCIe bytes moved by the last render_host / backward_host call (zero copy reads only
+        what the kernels touch when the scene arrays are pinned host memory)."""
+        out = (C.c_uint64 * 2)()
+        self._check(self._L.fgs_last_transfer(self._h, out))
+        return {"h2d": int(out[0]), "d2h": int(out[1])}
+
     # ---- parity / debug exports ----
     def debug(self, name: str, dtype=np.uint32):
         nbytes = self._L.fgs_debug_get(self._h, name.encode(), None, 0)

@@ -105,6 +105,7 @@ struct fgs_context {
   int64_t num_compact = 0;  // Gaussians touching >= 1 tile (rows the backward computes)
   uint32_t num_splats = 0, num_degenerate = 0, num_culled = 0;
   size_t aux_bytes = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;  // PCIe bytes of the last host-buffer call
   fgs::BinArgs bin_args{};
 };
 
@@ -566,6 +567,37 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   return FGS_OK;
 }
 
+namespace {
+// Device address of page-locked (pinned, mapped) host memory, or nullptr for pageable memory.
+const void* mapped_host(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
+// The scene's five arrays as device-accessible pointers when all of them are pinned host
+// memory: K1 then reads them over PCIe directly (zero copy), and only what it needs -- the
+// geometry of every Gaussian, the opacity and SH rows of the visible ones.
+bool mapped_scene(const fgs_gaussians* s, fgs_gaussians* out) {
+  *out = *s;
+  if (s->n <= 0) return false;
+  const void* p[5] = {mapped_host(s->means), mapped_host(s->rotations), mapped_host(s->log_scales),
+                      mapped_host(s->opacity_logits), mapped_host(s->sh)};
+  for (auto* q : p)
+    if (!q) return false;
+  out->means = static_cast<const float*>(p[0]);
+  out->rotations = static_cast<const float*>(p[1]);
+  out->log_scales = static_cast<const float*>(p[2]);
+  out->opacity_logits = static_cast<const float*>(p[3]);
+  out->sh = static_cast<const float*>(p[4]);
+  return true;
+}
+}  // namespace
+
 int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                     const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
   if (!ctx) return FGS_EINVAL;
@@ -581,19 +613,29 @@ int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_came
   FGS_CHECK(ctx->h_sh.ensure(nn * 48));
   FGS_CHECK(ctx->h_img.ensure(npix * 3));
   FGS_CHECK(ctx->h_radii.ensure(nn));
-  if (n) {
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_means.p, scene->means, n * 3 * 4, cudaMemcpyHostToDevice, st));
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_rot.p, scene->rotations, n * 4 * 4, cudaMemcpyHostToDevice, st));
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_ls.p, scene->log_scales, n * 3 * 4, cudaMemcpyHostToDevice, st));
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_op.p, scene->opacity_logits, n * 4, cudaMemcpyHostToDevice, st));
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_sh.p, scene->sh, n * 48 * 4, cudaMemcpyHostToDevice, st));
+  fgs_gaussians dev{};
+  const bool zero_copy = mapped_scene(scene, &dev);
+  if (!zero_copy) {  // pageable host memory: copy the whole scene
+    if (n) {
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_means.p, scene->means, n * 3 * 4, cudaMemcpyHostToDevice, st));
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_rot.p, scene->rotations, n * 4 * 4, cudaMemcpyHostToDevice, st));
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_ls.p, scene->log_scales, n * 3 * 4, cudaMemcpyHostToDevice, st));
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_op.p, scene->opacity_logits, n * 4, cudaMemcpyHostToDevice, st));
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_sh.p, scene->sh, n * 48 * 4, cudaMemcpyHostToDevice, st));
+    }
+    dev = fgs_gaussians{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
   }
-  fgs_gaussians dev{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
   int rc = fgs_forward(ctx, &dev, camera, options, ctx->h_img.p, radii ? ctx->h_radii.p : nullptr, stats);
   if (rc != FGS_OK) return rc;
   FGS_CHECK(cudaMemcpyAsync(image, ctx->h_img.p, npix * 3 * 4, cudaMemcpyDeviceToHost, st));
   if (radii && n) FGS_CHECK(cudaMemcpyAsync(radii, ctx->h_radii.p, n * 4, cudaMemcpyDeviceToHost, st));
   FGS_CHECK(cudaStreamSynchronize(st));
+  // bytes over PCIe: zero copy reads 40 B of geometry per Gaussian and, per splat that survives
+  // the culls, its opacity and the SH coefficients of the evaluated degree
+  const int deg = options ? options->sh_degree : 3;
+  const uint64_t sh_bytes = deg == 0 ? 3 * 4 : 48 * 4;
+  ctx->h2d_bytes = zero_copy ? n * 40 + static_cast<uint64_t>(ctx->num_splats) * (4 + sh_bytes) : n * 59 * 4;
+  ctx->d2h_bytes = npix * 3 * 4 + (radii ? n * 4 : 0);
   return FGS_OK;
 }
 
@@ -607,15 +649,19 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
   const size_t npix = static_cast<size_t>(camera->width) * camera->height;
   if (static_cast<int64_t>(n) != scene->n)
     return fail(ctx, FGS_EINVAL, "backward: forward context was built for a different scene");
-  // The scene arrays were uploaded by the matching fgs_render_host call; re-upload only if the
-  // caller's pointers differ is not knowable, so upload again (the reference takes the scene
-  // by value on every call).
-  if (n) {
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_means.p, scene->means, n * 3 * 4, cudaMemcpyHostToDevice, st));
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_rot.p, scene->rotations, n * 4 * 4, cudaMemcpyHostToDevice, st));
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_ls.p, scene->log_scales, n * 3 * 4, cudaMemcpyHostToDevice, st));
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_op.p, scene->opacity_logits, n * 4, cudaMemcpyHostToDevice, st));
-    FGS_CHECK(cudaMemcpyAsync(ctx->h_sh.p, scene->sh, n * 48 * 4, cudaMemcpyHostToDevice, st));
+  // The reference takes the scene by value on every call: pinned host arrays are read in place
+  // (zero copy, only the tile-touching Gaussians' parameters), pageable ones copied again.
+  fgs_gaussians dev{};
+  const bool zero_copy = mapped_scene(scene, &dev);
+  if (!zero_copy) {
+    if (n) {
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_means.p, scene->means, n * 3 * 4, cudaMemcpyHostToDevice, st));
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_rot.p, scene->rotations, n * 4 * 4, cudaMemcpyHostToDevice, st));
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_ls.p, scene->log_scales, n * 3 * 4, cudaMemcpyHostToDevice, st));
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_op.p, scene->opacity_logits, n * 4, cudaMemcpyHostToDevice, st));
+      FGS_CHECK(cudaMemcpyAsync(ctx->h_sh.p, scene->sh, n * 48 * 4, cudaMemcpyHostToDevice, st));
+    }
+    dev = fgs_gaussians{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
   }
   FGS_CHECK(ctx->h_dl.ensure(npix * 3));
   FGS_CHECK(ctx->h_grad.ensure(nn * 59));
@@ -630,7 +676,6 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
     FGS_CHECK(cudaMemcpyAsync(dg.d_opacity_logits, grads->d_opacity_logits, n * 4, cudaMemcpyHostToDevice, st));
     FGS_CHECK(cudaMemcpyAsync(dg.d_sh, grads->d_sh, n * 48 * 4, cudaMemcpyHostToDevice, st));
   }
-  fgs_gaussians dev{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
   int rc = fgs_backward(ctx, &dev, camera, ctx->h_dl.p, options, &dg);
   if (rc != FGS_OK) return rc;
   if (n) {
@@ -641,6 +686,16 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
     FGS_CHECK(cudaMemcpyAsync(grads->d_sh, dg.d_sh, n * 48 * 4, cudaMemcpyDeviceToHost, st));
   }
   FGS_CHECK(cudaStreamSynchronize(st));
+  ctx->h2d_bytes = npix * 3 * 4 + (zero_copy ? static_cast<uint64_t>(ctx->num_compact) * 44 : n * 59 * 4) +
+                   (acc ? n * 59 * 4 : 0);
+  ctx->d2h_bytes = n * 59 * 4;
+  return FGS_OK;
+}
+
+int fgs_last_transfer(const fgs_context* ctx, uint64_t out[2]) {
+  if (!ctx || !out) return FGS_EINVAL;
+  out[0] = ctx->h2d_bytes;
+  out[1] = ctx->d2h_bytes;
   return FGS_OK;
 }
 

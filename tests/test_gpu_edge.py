@@ -278,3 +278,30 @@ def test_capacity_growth_and_speculative_launch(rast, oracle_mod):
         np.testing.assert_array_equal(r.debug("offsets"), res.get("offsets"))
         np.testing.assert_array_equal(r.debug("sorted_gauss"), res.get("source")[res.get("refs")])
         assert np.abs(img.cpu().numpy().astype(np.float64) - res.image).max() <= 1e-3
+
+
+def test_zero_copy_host_path_equals_device_path(rast):
+    """Pinned host scene arrays are read in place over PCIe by K1 / K4b (fgs_render_host,
+    fgs_backward_host); results equal the device-resident path bit for bit, and the library
+    reports the bytes it moved."""
+    import torch
+    from paper_2409_04751_b200 import BackwardOptions, RenderOptions, Scene, grads_as_rows, synthetic
+
+    sc, deg, cams, dls = synthetic.config(1, n=30000)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).pin_memory().numpy()
+    hs = Scene(pin(sc.means), pin(sc.rotations), pin(sc.log_scales), pin(sc.opacity_logits), pin(sc.sh),
+               sc.background)
+    img_h, radii, st = rast.render_host(hs, cams[0], RenderOptions(sh_degree=deg))
+    t = rast.last_transfer()
+    assert t["h2d"] < sc.n * 59 * 4 and t["h2d"] >= sc.n * 40  # zero copy: not the whole scene
+    g_h = rast.backward_host(hs, cams[0], dls[0], BackwardOptions())
+    ds = to_device(sc)
+    img_d, _ = rast.forward(ds, cams[0], RenderOptions(sh_degree=deg))
+    g_d = rast.backward(ds, cams[0], torch.from_numpy(dls[0]).cuda(), BackwardOptions())
+    torch.cuda.synchronize()
+    assert img_h.tobytes() == img_d.cpu().numpy().tobytes()
+    assert g_h.tobytes() == g_d.cpu().numpy().tobytes()
+    # pageable arrays take the copy path and agree too
+    img_p, _, _ = rast.render_host(sc.astype(np.float32), cams[0], RenderOptions(sh_degree=deg))
+    assert rast.last_transfer()["h2d"] == sc.n * 59 * 4
+    assert img_p.tobytes() == img_h.tobytes()
