@@ -7,10 +7,10 @@
 //
 //   K1 (preprocess.cu) also adds each kept Gaussian's tile rectangle into a row-difference
 //      array over the tile grid (+1 at (ty, tx0), -1 at (ty, tx1 + 1) for each of its rows);
-//   K2a bin_scan_kernel (persistent cooperative, one grid barrier): exclusive scan of the
-//      per-Gaussian tile counts in source order -> emission offset of every tile-touching
-//      Gaussian (compacted list), the intersection count I; then CTA 0 turns the row-difference
-//      array into per-tile counts, the tile ranges (offsets[0..T]) and the blend schedule;
+//   K2 bin_kernel (persistent cooperative): exclusive scan of the per-Gaussian tile counts in
+//      source order -> emission offset of every tile-touching Gaussian (compacted list), the
+//      intersection count I; one warp per tile row turns the row-difference array into per-tile
+//      counts, the tile ranges (offsets[0..T]) and the blend schedule;
 //   [host reads I (16 bytes) to size the per-intersection buffers]
 //   K2b: each intersection (Gaussian g, tile t) claims a position in tile t's range with
 //      one atomicAdd and writes the 64-bit key (depth_key << 32 | g);
@@ -98,101 +98,120 @@ __device__ __forceinline__ void cta_prefix(const uint32_t* part, int stride, int
   total = tt;
 }
 
+// Debug phase trace (FGS_FLAG_COUNTERS): thread 0 of CTA `cta` records %globaltimer in slot.
+__device__ __forceinline__ void trace(unsigned long long* t, int cta, int slot) {
+  if (t && static_cast<int>(blockIdx.x) == cta && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    t[slot] = v;
+  }
+}
+
 __device__ __forceinline__ int sched_bucket(uint32_t c) {
   return c == 0 ? kSchedBuckets - 1 : 16 - min(16, 31 - __clz(c));
 }
 
-// Tile ranges (one CTA): the row-difference array K1 filled -> per-tile counts -> tile
-// offsets, scatter cursors, blend schedule, big-tile count.
-__device__ void tile_ranges(const BinArgs& a, ScanSmem& sm) {
-  const int tid = threadIdx.x;
-  // rowdiff is (tiles_y) x (tiles_x + 1), row-major; every +1 of a row has its -1 in the same
-  // row, so one running inclusive sum over the flattened array gives the count of every
-  // (row, column < tiles_x) cell. The array is zeroed as it is read (ready for the next frame).
-  const int rw = a.tiles_x + 1;
-  const int nd = rw * a.tiles_y;
-  const int lane = tid & 31;
+// ---- tile ranges, one warp per tile row (spread over the whole grid) ----
+// rowdiff is (tiles_y) x (tiles_x + 1), row-major: K1 added +1 at (ty, tx0) and -1 at
+// (ty, tx1 + 1) for every covered row, so a row's running sum gives its tiles' list lengths.
+// Rows are independent; the tile offsets need only the row totals' prefix on top.
+// Scratch (BinArgs::part_scan layout): hist[32] schedule buckets, cur[32] bucket cursors,
+// rowtot[tiles_y]; hist / cur are zero between frames (zeroed after their last use).
+constexpr int kRowItems = 8;
+
+// Phase 1: counts of row ty into fill[] (tile-major), its total into rowtot[ty], the schedule
+// histogram (warp-aggregated global atomics); rowdiff zeroed as read.
+__device__ void row_counts(const BinArgs& a, int ty, uint32_t* hist, uint32_t* rowtot) {
+  const int lane = threadIdx.x & 31, rw = a.tiles_x + 1;
   const uint32_t lt = lanemask_lt();
-  const bool single = nd <= kT * kItems;  // one pass: the counts stay in registers
-  if (tid < 32) sm.hist[tid] = 0;
-  uint32_t carry_d = 0, carry_o = 0;
-  uint32_t cnt[kItems];
-  int cell_tile[kItems];
-  for (int sb = 0; sb < nd; sb += kT * kItems) {
-    const int d0 = sb + tid * kItems;
-    int32_t v[kItems];
-    int32_t s = 0;
+  int32_t* rd = a.rowdiff + static_cast<size_t>(ty) * rw;
+  uint32_t carry = 0, tot = 0;
+  for (int c0 = 0; c0 < rw; c0 += 32 * kRowItems) {
+    int32_t v[kRowItems];
+    int32_t sum = 0;
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      v[i] = d0 + i < nd ? a.rowdiff[d0 + i] : 0;
-      s += v[i];
+    for (int i = 0; i < kRowItems; ++i) {
+      const int x = c0 + lane * kRowItems + i;
+      v[i] = x < rw ? rd[x] : 0;
+      sum += v[i];
+      if (x < rw && v[i]) rd[x] = 0;
     }
+    uint32_t incl = static_cast<uint32_t>(sum);
 #pragma unroll
-    for (int i = 0; i < kItems; ++i)
-      if (d0 + i < nd && v[i]) a.rowdiff[d0 + i] = 0;
-    uint32_t td;
-    uint32_t run = carry_d + block_exclusive_scan(static_cast<uint32_t>(s), sm.warp_tmp, &td);
-    uint32_t cs = 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t run = carry + incl - static_cast<uint32_t>(sum);
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const int d = d0 + i;
+    for (int i = 0; i < kRowItems; ++i) {
+      const int x = c0 + lane * kRowItems + i;
       run += static_cast<uint32_t>(v[i]);
-      const bool cell = d < nd && d % rw < a.tiles_x;
-      cnt[i] = cell ? run : 0u;
-      cell_tile[i] = cell ? (d / rw) * a.tiles_x + d % rw : -1;
-      cs += cnt[i];
+      const bool cell = x < a.tiles_x;
+      if (cell) {
+        a.fill[static_cast<size_t>(ty) * a.tiles_x + x] = run;
+        tot += run;
+      }
+      const int bk = cell ? sched_bucket(run) : 31;
+      const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+      if (bk != 31 && (peers & lt) == 0) atomicAdd(hist + bk, __popc(peers));
     }
-    uint32_t to;
-    uint32_t off = carry_o + block_exclusive_scan(cs, sm.warp_tmp2, &to);
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const int t = cell_tile[i];
-      if (t >= 0) {
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if (lane == 0) rowtot[ty] = tot;
+}
+
+// Phase 2: tile offsets and scatter cursors of row ty (row prefix + in-row exclusive scan),
+// blend schedule slots (tiles by descending list length: log2 buckets, empty tiles last).
+__device__ void row_offsets(const BinArgs& a, int ty, const uint32_t* rowtot, const uint32_t* hist, uint32_t* cur,
+                            uint32_t bprefix_lane) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  uint32_t pre = 0;
+  for (int r = lane; r < ty; r += 32) pre += rowtot[r];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  uint32_t carry = pre;
+  for (int c0 = 0; c0 < a.tiles_x; c0 += 32 * kRowItems) {
+    uint32_t c[kRowItems], sum = 0;
+#pragma unroll
+    for (int i = 0; i < kRowItems; ++i) {
+      const int x = c0 + lane * kRowItems + i;
+      c[i] = x < a.tiles_x ? a.fill[static_cast<size_t>(ty) * a.tiles_x + x] : 0u;
+      sum += c[i];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t off = carry + incl - sum;
+#pragma unroll
+    for (int i = 0; i < kRowItems; ++i) {
+      const int x = c0 + lane * kRowItems + i;
+      const bool cell = x < a.tiles_x;
+      const int t = ty * a.tiles_x + x;
+      if (cell) {
         a.tile_offsets[t] = off;
         a.fill[t] = off;
-        off += cnt[i];
       }
-      // schedule histogram, warp-aggregated (bucket 31 = no cell)
-      const int b = t >= 0 ? sched_bucket(cnt[i]) : 31;
-      const uint32_t peers = __match_any_sync(0xffffffffu, b);
-      if (b != 31 && (peers & lt) == 0) atomicAdd(&sm.hist[b], __popc(peers));
-    }
-    carry_d += td;
-    carry_o += to;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    a.tile_offsets[a.num_tiles] = carry_o;
-    a.scalars[kScalarI2] = carry_o;
-    // blend schedule: tiles by descending list length (log2 buckets), empty tiles last.
-    // The first `big` entries (lists of >= 256 keys) are CTA-sorted by K2c.
-    uint32_t r = 0, big = 0;
-    for (int b = 0; b < kSchedBuckets; ++b) {
-      const uint32_t c = sm.hist[b];
-      if (16 - b >= 8) big += c;
-      sm.run[b] = r;
-      r += c;
-    }
-    a.scalars[kScalarBig] = big;
-  }
-  __syncthreads();
-  if (single) {
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const int t = cell_tile[i];
-      const int b = t >= 0 ? sched_bucket(cnt[i]) : 31;
-      const uint32_t peers = __match_any_sync(0xffffffffu, b);
+      off += c[i];
+      const int bk = cell ? sched_bucket(c[i]) : 31;
+      const uint32_t peers = __match_any_sync(0xffffffffu, bk);
       const int leader = __ffs(peers) - 1;
       uint32_t base = 0;
-      if (b != 31 && lane == leader) base = atomicAdd(&sm.run[b], __popc(peers));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (t >= 0) a.tile_order[base + __popc(peers & lt)] = static_cast<uint32_t>(t);
+      if (bk != 31 && lane == leader) base = atomicAdd(cur + bk, __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader) + __shfl_sync(0xffffffffu, bprefix_lane, bk & 31);
+      if (cell) a.tile_order[base + __popc(peers & lt)] = static_cast<uint32_t>(t);
     }
-  } else {
-    for (int t = tid; t < a.num_tiles; t += kT) {
-      const uint32_t c = a.tile_offsets[t + 1] - a.tile_offsets[t];
-      a.tile_order[atomicAdd(&sm.run[sched_bucket(c)], 1u)] = static_cast<uint32_t>(t);
-    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (ty == a.tiles_y - 1 && lane == 0) {
+    a.tile_offsets[a.num_tiles] = carry;
+    a.scalars[kScalarI2] = carry;
   }
 }
 
@@ -281,10 +300,12 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
 }
 
 // K2: one persistent cooperative kernel, two grid barriers.
-//   phase 1: CTAs 0..G-2 count their chunk's tile-touching Gaussians and intersections;
-//            CTA G-1 builds the tile ranges (tile_ranges) at the same time;
-//   phase 2: CTAs 0..G-2 compact the tile-touching Gaussians (source order) with their
-//            emission offsets (cval, coff); M and I to the device scalars;
+//   phase 1: every CTA counts its chunk's tile-touching Gaussians and intersections; one warp
+//            per tile row turns K1's row-difference array into per-tile list lengths (fill[]),
+//            row totals and the schedule histogram;
+//   phase 2: compaction of the tile-touching Gaussians (source order) with their emission
+//            offsets (cval, coff, src_off); M and I to the device scalars; the row warps write
+//            the tile offsets, scatter cursors and blend schedule (descending list length);
 //   phase 3: all CTAs scatter the I emission slots (balanced by intersections) into the tile
 //            ranges -- unless I exceeds the buffers' capacity (speculative launch: the host
 //            grows them and launches again).
@@ -296,15 +317,17 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
   __shared__ uint32_t s_res;
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x;
-  const int G = static_cast<int>(gridDim.x) - 1;  // scan CTAs
+  const int G = static_cast<int>(gridDim.x);
   const int b = static_cast<int>(blockIdx.x);
-  const bool tiler = b == G;
+  const int lane = tid & 31, nw = G * kW;
+  uint32_t* hist = a.part_scan + 2 * G;
+  uint32_t* cur = hist + 32;
+  uint32_t* rowtot = cur + 32;
   int lo = static_cast<int>(static_cast<int64_t>(a.n) * b / G);
   int hi = static_cast<int>(static_cast<int64_t>(a.n) * (b + 1) / G);
   if (a.scatter_only) goto scatter;  // relaunch after the buffers grew: phases 1-2 are done
-  if (tiler) {
-    tile_ranges(a, sm);
-  } else {
+  trace(a.trace, 0, 0);
+  {
     uint32_t c1 = 0, c2 = 0;
     for (int i = lo + tid; i < hi; i += kT) {
       const uint32_t t = a.touched[i];
@@ -319,15 +342,36 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
       a.part_scan[2 * b + 1] = t2;
     }
   }
+  // rows spread over CTAs first (row ty -> CTA ty mod G), so no CTA gets two
+  for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw) row_counts(a, ty, hist, rowtot);
+  trace(a.trace, 0, 3);
   grid.sync();
-  if (!tiler) {
+  trace(a.trace, 0, 4);
+  {
     uint32_t p1, tot1, p2, tot2;
     cta_prefix(a.part_scan, 2, G, sm.warp_tmp, p1, tot1);
     cta_prefix(a.part_scan + 1, 2, G, sm.warp_tmp, p2, tot2);
+    // schedule bucket prefix (lane k holds bucket k's start) and the long-list count
+    const uint32_t hk = lane < kSchedBuckets ? hist[lane] : 0u;
+    uint32_t incl = hk;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const uint32_t bprefix = incl - hk;
     if (b == 0 && tid == 0) {
       a.scalars[kScalarM] = tot1;
       a.scalars[kScalarI] = tot2;
     }
+    if (b == 0 && tid < 32) {
+      // the first n_big schedule slots hold the lists of >= 256 keys (log2 buckets 0..8)
+      uint32_t big = lane < kSchedBuckets && 16 - lane >= 8 ? hk : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) big += __shfl_xor_sync(0xffffffffu, big, o);
+      if (lane == 0) a.scalars[kScalarBig] = big;
+    }
+    for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw) row_offsets(a, ty, rowtot, hist, cur, bprefix);
     uint32_t run1 = p1, run2 = p2;
     for (int sb = lo; sb < hi; sb += kT * kItems) {
       const int r0 = sb + tid * kItems;
@@ -355,7 +399,10 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
       run2 += t2;
     }
   }
+  trace(a.trace, 0, 5);
   grid.sync();
+  trace(a.trace, 0, 6);
+  if (b == 0 && tid < 64) hist[tid] = 0;  // hist + cur: last read before this barrier
 scatter:
   const uint32_t I = a.scalars[kScalarI];
   if (I > a.isect_cap || I == 0) return;
@@ -363,6 +410,7 @@ scatter:
   const uint32_t s_lo = static_cast<uint32_t>(static_cast<uint64_t>(I) * b / gridDim.x);
   const uint32_t s_hi = static_cast<uint32_t>(static_cast<uint64_t>(I) * (b + 1) / gridDim.x);
   for (uint32_t x = s_lo; x < s_hi; x += kSub) scatter_range<PRIV>(a, m, x, min(s_hi, x + kSub), s_cnt, s_off, &s_res);
+  trace(a.trace, 0, 7);
 }
 
 // Debug export: the reference's pre-sort key list (source order, ty-major, tx-minor).
@@ -402,13 +450,17 @@ int grid_size() {
 
 }  // namespace
 
-size_t bin_part_words() { return static_cast<size_t>(grid_size()) * 2 + 64; }
+size_t bin_part_words(int tiles_y) { return static_cast<size_t>(grid_size()) * 2 + 64 + tiles_y; }
 
 cudaError_t bin_launch(BinArgs& a, cudaStream_t st) {
   const int g = grid_size();
   if (g < 2) return cudaErrorCooperativeLaunchTooLarge;
   void* args[] = {&a};
-  if (a.num_tiles <= kPrivTiles)
+  static const int priv_env = [] {
+    const char* v = std::getenv("FGS_SCATTER_PRIV");
+    return v ? std::atoi(v) : -1;
+  }();
+  if (a.num_tiles <= kPrivTiles && priv_env != 0)
     return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bin_kernel<true>), g, kT, args,
                                        a.num_tiles * 4, st);
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bin_kernel<false>), g, kT, args, 0, st);

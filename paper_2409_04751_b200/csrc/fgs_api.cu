@@ -207,7 +207,7 @@ int fgs_create(int device, fgs_context** out) {
   }
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
   cudaEventCreateWithFlags(&ctx->ev_scan, cudaEventDisableTiming);
-  if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(16) != cudaSuccess ||
+  if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(24) != cudaSuccess ||
       false) {
     fgs_destroy(ctx);
     return FGS_ENOMEM;
@@ -307,7 +307,11 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   FGS_CHECK(ctx->rec.ensure(nn));
   FGS_CHECK(ctx->state.ensure(nn));
   for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->src_off, &ctx->touched}) FGS_CHECK(b->ensure(nn));
-  FGS_CHECK(ctx->scan_status.ensure(fgs::bin_part_words()));
+  const size_t part_words = fgs::bin_part_words(tiles_y);
+  if (ctx->scan_status.cap < part_words) {
+    FGS_CHECK(ctx->scan_status.ensure(part_words));
+    ctx->rowdiff_clean = 0;  // forces the scratch memsets below
+  }
   FGS_CHECK(ctx->rect.ensure(nn));
   FGS_CHECK(ctx->radii.ensure(nn));
   FGS_CHECK(ctx->tile_offsets.ensure(num_tiles + 1));
@@ -317,6 +321,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   if (ctx->rowdiff.cap < ndiff || ctx->rowdiff_clean < ndiff) {
     FGS_CHECK(ctx->rowdiff.ensure(ndiff));
     FGS_CHECK(cudaMemsetAsync(ctx->rowdiff.p, 0, ctx->rowdiff.cap * sizeof(int32_t), ctx->stream));
+    FGS_CHECK(cudaMemsetAsync(ctx->scan_status.p, 0, ctx->scan_status.cap * sizeof(uint32_t), ctx->stream));
     ctx->rowdiff_clean = ctx->rowdiff.cap;
   }
   FGS_CHECK(ctx->last.ensure(npix));
@@ -337,7 +342,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   uint64_t launches = 0;
 
   FGS_CHECK(cudaMemsetAsync(ctx->scalars.p, 0, 16 * sizeof(uint32_t), st));
-  if (ctx->flags & FGS_FLAG_COUNTERS) FGS_CHECK(cudaMemsetAsync(ctx->counters.p, 0, 16 * sizeof(unsigned long long), st));
+  if (ctx->flags & FGS_FLAG_COUNTERS) FGS_CHECK(cudaMemsetAsync(ctx->counters.p, 0, 24 * sizeof(unsigned long long), st));
   if (n > 0) {
     fgs::PreprocessArgs pa{};
     pa.n = n;
@@ -384,6 +389,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.isect_cap = ctx->isect_cap;
   bn.keys = ctx->keys.p;
   bn.src_off = ctx->src_off.p;
+  bn.trace = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p + 16 : nullptr;
   if (n > 0) {
     ctx->rowdiff_clean = 0;  // dirty until K2 has consumed K1's counts
     FGS_CHECK(fgs::bin_launch(bn, st));
@@ -898,6 +904,7 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   if (nm == "last") return copy(ctx->last.p, npix * 4);
   if (nm == "counters") return copy(ctx->counters.p, 4 * sizeof(unsigned long long));
   if (nm == "counters16") return copy(ctx->counters.p, 16 * sizeof(unsigned long long));
+  if (nm == "bin_trace") return copy(ctx->counters.p + 16, 8 * sizeof(unsigned long long));
   if (nm == "tile_cycles") return copy(ctx->tile_cycles.p, nt * sizeof(unsigned long long));
   if (nm == "key_tile" || nm == "key_depth" || nm == "key_gauss") {
     if (!dst) return static_cast<int64_t>(I * 4);

@@ -93,6 +93,7 @@ struct BinArgs {
   int tiles_x, tiles_y, num_tiles;
   int64_t isect_cap;           // capacity of the per-intersection buffers (the scatter is skipped if I exceeds it)
   int scatter_only;            // relaunch: phases 1-2 already ran
+  unsigned long long* trace;   // debug phase timestamps (FGS_FLAG_COUNTERS), 8 slots
   const uint32_t* touched;     // [n] tiles touched per Gaussian (K1)
   const uint32_t* depth_key;   // [n] depth key bits (K1)
   const ushort4* rect;         // [n] tile rectangle (K1)
@@ -101,7 +102,7 @@ struct BinArgs {
   uint32_t* coff;              // [n] their first emission slot
   uint32_t* src_off;           // [n] first emission slot by Gaussian id (tile-touching ones)
   uint32_t* scalars;           // device scalars (kScalar*)
-  uint32_t* part_scan;         // [2 * grid]
+  uint32_t* part_scan;         // [2 * grid] CTA partials, [64] schedule histogram + cursors, [tiles_y] row totals
   uint32_t* tile_offsets;      // [num_tiles + 1]
   uint32_t* fill;              // [num_tiles] scatter cursors
   uint32_t* tile_order;        // [num_tiles] blend schedule (optional)
@@ -110,7 +111,7 @@ struct BinArgs {
 };
 
 // Words of part_scan scratch bin_scan needs.
-size_t bin_part_words();
+size_t bin_part_words(int tiles_y);
 // K2 (one cooperative kernel): compaction + emission offsets + I and M (device scalars),
 // tile ranges + blend schedule, key scatter into the tile ranges (skipped if I > isect_cap).
 cudaError_t bin_launch(BinArgs& a, cudaStream_t st);
