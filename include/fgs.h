@@ -127,8 +127,9 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
 /* PCIe bytes moved by the last fgs_render_host / fgs_backward_host call: out = {h2d, d2h}. */
 int fgs_last_transfer(const fgs_context* ctx, uint64_t out[2]);
 
-/* Flags: FGS_FLAG_COUNTERS makes the forward blend count E_eval / E_contrib (atomics; slower);
- * FGS_FLAG_TIMING records CUDA events around every stage (read with fgs_timing). Default 0. */
+/* Flags: FGS_FLAG_COUNTERS makes the forward blend count E_eval / E_contrib (atomics; slower)
+ * and records the binning phase trace; FGS_FLAG_TIMING records CUDA events around every stage
+ * (read with fgs_timing). FGS_FLAG_KEEP_KEYS is reserved (no effect). Default 0. */
 enum { FGS_FLAG_COUNTERS = 1, FGS_FLAG_KEEP_KEYS = 2, FGS_FLAG_TIMING = 4 };
 int fgs_set_flags(fgs_context* ctx, uint32_t flags);
 
@@ -143,11 +144,13 @@ int fgs_timing(fgs_context* ctx, double ms[6], uint64_t calls[2], uint64_t* laun
 int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s);
 
 /* Parity/debug export of the last forward's state into host memory. Names:
- *   "state" int32[N] (0 culled, 1 kept, 2 degenerate), "mean_px" f32[N*2], "conic" f32[N*3],
- *   "depth" f32[N], "radius" int32[N], "color" f32[N*3], "alpha" f32[N],
- *   "key_tile"/"key_depth"/"key_gauss" u32[I] (pre-sort keys, reference emission order),
- *   "sorted_gauss" u32[I], "sorted_tile" u32[I], "sorted_depth" u32[I], "offsets" u32[T+1],
- *   "final_T" f32[H*W], "last" u32[H*W], "counters" u64[4] (E_eval, E_contrib, 0, 0).
+ *   "state_u8" u8[N] (0 culled, 1 kept, 2 degenerate), "rec" f32[N*12] (splat records: mean_px,
+ *   conic, alpha_max, colour, extent), "depth_key" u32[N], "radius" int32[N], "touched" u32[N],
+ *   "key_tile"/"key_depth"/"key_gauss" u32[I] (pre-sort keys in the reference's emission order),
+ *   "sorted_gauss" u32[I], "sorted_tile" u32[I], "offsets" u32[T+1] (tile ranges),
+ *   "compact_gauss"/"compact_offsets" u32[M], "final_T" f32[H*W], "last" u32[H*W],
+ *   "counters" u64[4] (E_eval, E_contrib, culled evaluations, max CTA cycles; with
+ *   FGS_FLAG_COUNTERS), "counters16" u64[16], "bin_trace" u64[8], "tile_cycles" u64[T].
  * Returns the number of bytes (dst may be NULL to query), or -1 for an unknown name. */
 int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst_bytes);
 

@@ -21,9 +21,13 @@
 namespace {
 
 template <typename T>
-struct DevBuf {
+struct DevBuf {  // owning device allocation that only grows (freed on destruction)
   T* p = nullptr;
   size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
   cudaError_t ensure(size_t n) {
     if (n <= cap && p) return cudaSuccess;
     if (p) cudaFree(p);
