@@ -538,7 +538,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   if (timing && ctx->pending.size() > 64) drain_sets(ctx, 8);
   cudaEvent_t* ev = timing ? take_set(ctx, 1)->e : nullptr;
   if (timing) cudaEventRecord(ev[0], st);
-  if (I > 0) ctx->launches += fgs::blend_backward(ba, st);
+  if (I > 0) ctx->launches += fgs::blend_backward(ba, I, st);
   if (timing) cudaEventRecord(ev[1], st);
 
   fgs::PreprocessBackwardArgs pb{};

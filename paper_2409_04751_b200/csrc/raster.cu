@@ -17,6 +17,7 @@
 // order) and written to the intersection's sorted position: no atomics, deterministic.
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fgs_sort.cuh"
 
@@ -242,41 +243,63 @@ __device__ __forceinline__ bool near_threshold(float ar) {
   return fabsf(ar - kAlphaSkip) <= kGuardRel * kAlphaSkip || fabsf(ar - kAlphaClamp) <= kGuardRel * kAlphaClamp;
 }
 
-// K4a backward blend (inc/gradients.hpp:69-175), barrier-free like the forward: 8 warps per
-// tile, warp w owns the 8x4 block of bwd_block_box, one pixel per lane. Each warp walks the
-// tile's list backwards from its last contributor (the max of its pixels' `last`) in 32-splat
-// chunks, culls them against its block (rec_hits on the extent K1 stored), and for each surviving splat recovers
-// T_before = T_after / (1 - alpha), accumulates the suffix colour and forms the 9 per-pixel
-// gradients (mean_px 2, conic 3, colour 3, alpha_max 1), summed over the warp's 32 pixels by
-// a shuffle tree. The warp sum goes to partials[k][w] -- one slot per (intersection, block)
-// whose block passes the cull, zeros for passing splats past the warp's last contributor --
-// and the CTA's epilogue adds the passing slots of every entry in block order into
-// partial_tile[k] (K4b then sums a Gaussian's entries in tile order): deterministic, no atomics.
-__global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
-  __shared__ float4 s0[kBwdWarps][32];
-  __shared__ float4 s1[kBwdWarps][32];
-  __shared__ float s2[kBwdWarps][32];
+// K4a backward blend (inc/gradients.hpp:69-175), barrier-free like the forward. PX pixels per
+// lane: 8/PX warps per tile, warp w owns the 8 x 4PX block of bwd_block_box<PX>, lane l the
+// pixels (l&7, (l>>3) + 4u), u < PX (one column, so dx and its products are shared). Each warp
+// walks the tile's list backwards from its last contributor (the max of its pixels' `last`) in
+// 32-splat chunks, culls them against its block (rec_hits on the extent K1 stored), and for
+// each surviving splat recovers T_before = T_after / (1 - alpha), accumulates the suffix colour
+// and forms the 9 per-pixel gradients (mean_px 2, conic 3, colour 3, alpha_max 1), summed over
+// the lane's pixels and then the warp by a shuffle tree. The warp sum goes to partials[k][w] --
+// one slot per (intersection, block) whose block passes the cull, zeros for passing splats past
+// the warp's last contributor -- and the CTA's epilogue adds the passing slots of every entry
+// in block order into partial_tile[emission slot]: deterministic, no atomics.
+template <int PX>
+__device__ __forceinline__ void bwd_box(int tx, int ty, int w, float& x0, float& x1, float& y0, float& y1) {
+  x0 = static_cast<float>(tx * kTile + ((w & 1) << 3)) + 0.5f;
+  x1 = x0 + 7.0f;
+  y0 = static_cast<float>(ty * kTile + (w >> 1) * 4 * PX) + 0.5f;
+  y1 = y0 + (4.0f * PX - 1.0f);
+}
+
+template <int PX>
+__global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
+  constexpr int NW = 8 / PX;
+  __shared__ float4 s0[NW][32];
+  __shared__ float4 s1[NW][32];
+  __shared__ float s2[NW][32];
   const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float bx0, bx1, by0, by1;
-  bwd_block_box(tx, ty, warp, bx0, bx1, by0, by1);
-  const int px = static_cast<int>(bx0) + (lane & 7), py = static_cast<int>(by0) + (lane >> 3);
-  const bool inside = px < a.width && py < a.height;
+  bwd_box<PX>(tx, ty, warp, bx0, bx1, by0, by1);
+  const int px = static_cast<int>(bx0) + (lane & 7);
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
-  const float fx = static_cast<float>(px) + 0.5f, fy = static_cast<float>(py) + 0.5f;
-  float T = 1.0f, dl0 = 0.0f, dl1 = 0.0f, dl2 = 0.0f;
-  uint32_t last = lo;
-  if (inside) {
-    const size_t pix = static_cast<size_t>(py) * a.width + px;
-    T = a.final_T[pix];
-    last = a.last[pix];
-    dl0 = a.dl_dimage[pix * 3 + 0];
-    dl1 = a.dl_dimage[pix * 3 + 1];
-    dl2 = a.dl_dimage[pix * 3 + 2];
+  const float fx = static_cast<float>(px) + 0.5f;
+  float T[PX], dl[PX][3], sf[PX][3], fy[PX];
+  uint32_t last[PX];
+  uint32_t mylast = lo;
+#pragma unroll
+  for (int u = 0; u < PX; ++u) {
+    const int py = static_cast<int>(by0) + (lane >> 3) + 4 * u;
+    fy[u] = static_cast<float>(py) + 0.5f;
+    T[u] = 1.0f;
+    dl[u][0] = dl[u][1] = dl[u][2] = 0.0f;
+    last[u] = lo;
+    if (px < a.width && py < a.height) {
+      const size_t pix = static_cast<size_t>(py) * a.width + px;
+      T[u] = a.final_T[pix];
+      last[u] = a.last[pix];
+      dl[u][0] = a.dl_dimage[pix * 3 + 0];
+      dl[u][1] = a.dl_dimage[pix * 3 + 1];
+      dl[u][2] = a.dl_dimage[pix * 3 + 2];
+    }
+    sf[u][0] = T[u] * a.bg[0];
+    sf[u][1] = T[u] * a.bg[1];
+    sf[u][2] = T[u] * a.bg[2];
+    mylast = max(mylast, last[u]);
   }
-  const uint32_t wlast = __reduce_max_sync(0xffffffffu, last);
-  float sf0 = T * a.bg[0], sf1 = T * a.bg[1], sf2 = T * a.bg[2];
+  const uint32_t wlast = __reduce_max_sync(0xffffffffu, mylast);
   float* part = a.partials;
 
   // passing splats past the warp's last contributor: zero slots
@@ -285,7 +308,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     if (k < hi) {
       const SortedRec r = load_rec(a, k);
       if (rec_hits(r.a, r.c, bx0, bx1, by0, by1)) {
-        float* p = part + (static_cast<size_t>(k) * kBwdWarps + warp) * 9;
+        float* p = part + (static_cast<size_t>(k) * NW + warp) * 9;
 #pragma unroll
         for (int q = 0; q < 9; ++q) p[q] = 0.0f;
       }
@@ -307,8 +330,8 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
     __syncwarp();
     // Groups of 3 surviving splats, latest first. Their alphas are independent of the
     // transmittance and are computed together; the transmittance/suffix recurrence then runs
-    // in list order, leaving 3 x 9 per-lane gradients, which one butterfly reduce-scatter over
-    // the warp sums (31 shuffles instead of 3 x 45); lane l ends with value l.
+    // in list order, leaving 3 x 9 per-lane gradients (summed over the lane's pixels), which one
+    // butterfly reduce-scatter over the warp sums (31 shuffles); lane l ends with value l.
     while (mask) {
       int js[3];
 #pragma unroll
@@ -316,7 +339,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
         js[q] = mask ? 31 - __clz(mask) : -1;
         if (mask) mask &= ~(1u << js[q]);
       }
-      float pw[3], ex[3], ar[3], dxs[3], dys[3];
+      float pw[3][PX], ex[3][PX], ar[3][PX], dxs[3], dys[3][PX];
       float4 r0s[3], r1s[3];
       bool any_near = false;
 #pragma unroll
@@ -325,19 +348,24 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
         r0s[q] = s0[warp][jj];
         r1s[q] = s1[warp][jj];
         dxs[q] = __fsub_rn(fx, r0s[q].x);
-        dys[q] = __fsub_rn(fy, r0s[q].y);
-        pw[q] = blend_power(r0s[q].z, r0s[q].w, r1s[q].x, dxs[q], dys[q]);
-        ex[q] = fast_exp(pw[q]);
-        ar[q] = __fmul_rn(r1s[q].y, ex[q]);
-        any_near |= near_threshold(ar[q]);
+#pragma unroll
+        for (int u = 0; u < PX; ++u) {
+          dys[q][u] = __fsub_rn(fy[u], r0s[q].y);
+          pw[q][u] = blend_power(r0s[q].z, r0s[q].w, r1s[q].x, dxs[q], dys[q][u]);
+          ex[q][u] = fast_exp(pw[q][u]);
+          ar[q][u] = __fmul_rn(r1s[q].y, ex[q][u]);
+          any_near |= near_threshold(ar[q][u]);
+        }
       }
       if (__any_sync(0xffffffffu, any_near)) {  // rare: exact exp near the 1/255 or 0.99 threshold
 #pragma unroll
         for (int q = 0; q < 3; ++q)
-          if (near_threshold(ar[q])) {
-            ex[q] = cr_expf(pw[q]);
-            ar[q] = __fmul_rn(r1s[q].y, ex[q]);
-          }
+#pragma unroll
+          for (int u = 0; u < PX; ++u)
+            if (near_threshold(ar[q][u])) {
+              ex[q][u] = cr_expf(pw[q][u]);
+              ar[q][u] = __fmul_rn(r1s[q].y, ex[q][u]);
+            }
       }
       // Branch-free: every lane evaluates all three steps and gates them (a non-contributing
       // step leaves T and the suffix colour unchanged and gives zero gradients; all operands
@@ -347,33 +375,40 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const uint32_t kk = cstart + static_cast<uint32_t>(js[q]);
-        const float alpha = fminf(kAlphaClamp, ar[q]);
-        const bool c = js[q] >= 0 && kk < last && pw[q] <= 0.0f && pw[q] >= kPowerFloor && alpha >= kAlphaSkip;
-        contrib_any |= c;
         const float4 r0 = r0s[q], r1 = r1s[q];
-        const float dx = dxs[q], dy = dys[q];
-        const float inv = fast_rcp(1.0f - alpha);
-        const float Tb = T * inv;
-        const float w = c ? alpha * Tb : 0.0f;
         const float b2 = s2[warp][js[q] >= 0 ? js[q] : 0];
-        v[9 * q + 5] = dl0 * w;
-        v[9 * q + 6] = dl1 * w;
-        v[9 * q + 7] = dl2 * w;
-        const float dot_c = dl0 * r1.z + dl1 * r1.w + dl2 * b2;
-        const float dot_s = dl0 * sf0 + dl1 * sf1 + dl2 * sf2;
-        // clamped contributions carry no geometric gradient
-        const float d_alpha = (c && !(ar[q] > kAlphaClamp)) ? dot_c * Tb - dot_s * inv : 0.0f;
-        sf0 = fmaf(r1.z, w, sf0);
-        sf1 = fmaf(r1.w, w, sf1);
-        sf2 = fmaf(b2, w, sf2);
-        T = c ? Tb : T;
-        v[9 * q + 8] = d_alpha * ex[q];
-        const float dp = d_alpha * alpha;
-        v[9 * q + 0] = dp * (r0.z * dx + r0.w * dy);
-        v[9 * q + 1] = dp * (r0.w * dx + r1.x * dy);
-        v[9 * q + 2] = dp * (-0.5f * dx * dx);
-        v[9 * q + 3] = dp * (-dx * dy);
-        v[9 * q + 4] = dp * (-0.5f * dy * dy);
+        const float dx = dxs[q];
+#pragma unroll
+        for (int c9 = 0; c9 < 9; ++c9) v[9 * q + c9] = 0.0f;
+#pragma unroll
+        for (int u = 0; u < PX; ++u) {
+          const float alpha = fminf(kAlphaClamp, ar[q][u]);
+          const bool c = js[q] >= 0 && kk < last[u] && pw[q][u] <= 0.0f && pw[q][u] >= kPowerFloor &&
+                         alpha >= kAlphaSkip;
+          contrib_any |= c;
+          const float dy = dys[q][u];
+          const float inv = fast_rcp(1.0f - alpha);
+          const float Tb = T[u] * inv;
+          const float w = c ? alpha * Tb : 0.0f;
+          v[9 * q + 5] += dl[u][0] * w;
+          v[9 * q + 6] += dl[u][1] * w;
+          v[9 * q + 7] += dl[u][2] * w;
+          const float dot_c = dl[u][0] * r1.z + dl[u][1] * r1.w + dl[u][2] * b2;
+          const float dot_s = dl[u][0] * sf[u][0] + dl[u][1] * sf[u][1] + dl[u][2] * sf[u][2];
+          // clamped contributions carry no geometric gradient
+          const float d_alpha = (c && !(ar[q][u] > kAlphaClamp)) ? dot_c * Tb - dot_s * inv : 0.0f;
+          sf[u][0] = fmaf(r1.z, w, sf[u][0]);
+          sf[u][1] = fmaf(r1.w, w, sf[u][1]);
+          sf[u][2] = fmaf(b2, w, sf[u][2]);
+          T[u] = c ? Tb : T[u];
+          v[9 * q + 8] += d_alpha * ex[q][u];
+          const float dp = d_alpha * alpha;
+          v[9 * q + 0] += dp * (r0.z * dx + r0.w * dy);
+          v[9 * q + 1] += dp * (r0.w * dx + r1.x * dy);
+          v[9 * q + 2] += dp * (-0.5f * dx * dx);
+          v[9 * q + 3] += dp * (-dx * dy);
+          v[9 * q + 4] += dp * (-0.5f * dy * dy);
+        }
       }
 #pragma unroll
       for (int q = 27; q < 32; ++q) v[q] = 0.0f;
@@ -394,7 +429,7 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
       // lane l now holds component l % 9 of splat l / 9 (l < 27)
       const int q = lane / 9;
       if (lane < 27 && js[q] >= 0)
-        part[(static_cast<size_t>(cstart + js[q]) * kBwdWarps + warp) * 9 + (lane - 9 * q)] = v[0];
+        part[(static_cast<size_t>(cstart + js[q]) * NW + warp) * 9 + (lane - 9 * q)] = v[0];
     }
     __syncwarp();
   }
@@ -402,20 +437,20 @@ __global__ void __launch_bounds__(kBlend) blend_backward_kernel(BlendArgs a) {
   // the culling test, in block order (the partials are this CTA's own, L2-resident writes),
   // stored at the intersection's emission slot (K4b then reads each Gaussian's contiguously).
   __syncthreads();
-  for (uint32_t k = lo + threadIdx.x; k < hi; k += kBlend) {
+  for (uint32_t k = lo + threadIdx.x; k < hi; k += 256 / PX) {
     const uint32_t g = __ldg(a.sorted_gauss + k);
     const SortedRec r = a.rec[g];
     const ushort4 rc = a.rect[g];
     // emission slot of (g, this tile): g's first slot + the tile's index in its rectangle
     const uint32_t e = a.src_off[g] + static_cast<uint32_t>((ty - rc.z) * (rc.y - rc.x + 1) + (tx - rc.x));
-    const float* p = part + static_cast<size_t>(k) * (kBwdWarps * 9);
+    const float* p = part + static_cast<size_t>(k) * (NW * 9);
     float sg[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) sg[q] = 0.0f;
 #pragma unroll
-    for (int w = 0; w < kBwdWarps; ++w) {
+    for (int w = 0; w < NW; ++w) {
       float x0, x1, y0, y1;
-      bwd_block_box(tx, ty, w, x0, x1, y0, y1);
+      bwd_box<PX>(tx, ty, w, x0, x1, y0, y1);
       if (!rec_hits(r.a, r.c, x0, x1, y0, y1)) continue;
 #pragma unroll
       for (int q = 0; q < 9; ++q) sg[q] = sg[q] + p[w * 9 + q];
@@ -441,8 +476,19 @@ int blend_forward(const BlendArgs& a, cudaStream_t st) {
   return 1;
 }
 
-int blend_backward(const BlendArgs& a, cudaStream_t st) {
-  blend_backward_kernel<<<a.tiles_x * a.tiles_y, kBlend, 0, st>>>(a);
+int blend_backward(const BlendArgs& a, int64_t num_isect, cudaStream_t st) {
+  // Dense tile lists (measured: config 4, ~545 entries per tile) amortise the per-splat
+  // overhead (chunk staging, culling, group selection, the 27-value warp reduction) better over
+  // 8x8 warp blocks with 2 pixels per lane; sparser ones (config 2, ~104) cull better with
+  // 8x4 blocks. FGS_BWD_PX=1|2 overrides.
+  static const int env = [] {
+    const char* v = std::getenv("FGS_BWD_PX");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int tiles = a.tiles_x * a.tiles_y;
+  const int px = env == 1 || env == 2 ? env : (num_isect >= 256 * static_cast<int64_t>(tiles) ? 2 : 1);
+  if (px == 1) blend_backward_kernel<1><<<tiles, 256, 0, st>>>(a);
+  else blend_backward_kernel<2><<<tiles, 128, 0, st>>>(a);
   return 1;
 }
 
