@@ -435,7 +435,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     ba.isect_cap = ctx->isect_cap;
     ba.keys = ctx->keys.p;
     ba.sorted_gauss = ctx->sorted_gauss.p;
-    const int l = fgs::blend_forward(ba, st);
+    // density hint for the work decomposition: this frame's I once known, else the last frame's
+    const int l = fgs::blend_forward(ba, ctx->num_isect, st);
     if (timing) cudaEventRecord(ev[4], st);
     return l;
   };

@@ -19,7 +19,6 @@
 namespace fgs {
 namespace {
 
-constexpr int kSortThreads = 256;  // the blend CTA
 constexpr int kSortCap = 4096;     // keys sorted entirely in shared memory
 
 
@@ -122,16 +121,15 @@ __device__ __forceinline__ void ce(uint64_t* s, int i, int p) {
 }
 
 constexpr int kChunk = 256;  // keys per warp register chunk (E = 8)
-constexpr int kSortWarps = kSortThreads / 32;
 
 // Register phase over the shared array s[0, n) (n a multiple of the chunk 32*E): every warp
 // loads its chunks, runs a full sort (first) or the half-cleaner stages j < 32E of a merge
 // level, and stores them back. Callers barrier before and after.
-template <int E, bool kFull>
+template <int NT, int E, bool kFull>
 __device__ __forceinline__ void chunk_phase(uint64_t* s, int n) {
   constexpr int CH = 32 * E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = warp * CH; c < n; c += kSortWarps * CH) {
+  for (int c = warp * CH; c < n; c += (NT / 32) * CH) {
     uint64_t x[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) x[r] = s[c + r * 32 + lane];
@@ -146,43 +144,47 @@ __device__ __forceinline__ void chunk_phase(uint64_t* s, int n) {
 // the whole CTA: chunks of 32E keys sorted in registers, then every merge level's stages with
 // j >= 32E in shared memory and the rest in registers. E is chosen so that the first phase
 // keeps all warps busy (n / 32E >= kSortWarps where possible).
-template <int E>
+template <int NT, int E>
 __device__ void cta_sort_e(uint64_t* s, int n) {
   constexpr int CH = 32 * E;
   __syncthreads();
-  chunk_phase<E, true>(s, n);
+  chunk_phase<NT, E, true>(s, n);
   for (int k = 2 * CH; k <= n; k <<= 1) {
     for (int j = k >> 1; j >= CH; j >>= 1) {
       __syncthreads();
-      for (int c = threadIdx.x; c < (n >> 1); c += kSortThreads) {
+      for (int c = threadIdx.x; c < (n >> 1); c += NT) {
         int i, p;
         ce_index(c, k, j, i, p);
         ce(s, i, p);
       }
     }
     __syncthreads();
-    chunk_phase<E, false>(s, n);
+    chunk_phase<NT, E, false>(s, n);
   }
   __syncthreads();
 }
 
+// E = n / (32 * warps) where possible, so the first (register) phase keeps every warp busy.
+template <int NT>
 __device__ void cta_sort(uint64_t* s, int n) {
-  if (n <= 512) cta_sort_e<2>(s, n);
-  else if (n <= 1024) cta_sort_e<4>(s, n);
-  else cta_sort_e<8>(s, n);
+  constexpr int W = NT / 32;
+  if (n <= 64 * W) cta_sort_e<NT, 2>(s, n);
+  else if (n <= 128 * W) cta_sort_e<NT, 4>(s, n);
+  else cta_sort_e<NT, 8>(s, n);
 }
 
 // Stages j = C/2 .. 1 of a merge level k > C on the shared chunk s[0, C) (C = kSortCap).
+template <int NT>
 __device__ void cta_halfclean(uint64_t* s) {
   for (int j = kSortCap >> 1; j >= kChunk; j >>= 1) {
     __syncthreads();
-    for (int c = threadIdx.x; c < (kSortCap >> 1); c += kSortThreads) {
+    for (int c = threadIdx.x; c < (kSortCap >> 1); c += NT) {
       const int i = 2 * c - (c & (j - 1));
       ce(s, i, i + j);
     }
   }
   __syncthreads();
-  chunk_phase<8, false>(s, kSortCap);
+  chunk_phase<NT, 8, false>(s, kSortCap);
   __syncthreads();
 }
 
@@ -192,9 +194,10 @@ __device__ __forceinline__ int pow2_ceil(int x) {
   return p;
 }
 
-// Sort the tile list keys[lo, lo + L) (CTA-wide call, all kSortThreads threads) by
+// Sort the tile list keys[lo, lo + L) (CTA-wide call, all NT threads) by
 // (depth key, Gaussian id) and write the sorted Gaussian ids (sorted_gauss[lo + k]). Returns true when the ids are also left in shared memory: g of
 // entry k at ((uint32_t*)s)[2k] (lists of <= kSortCap keys); else read sorted_gauss.
+template <int NT>
 __device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t lo, int L, uint64_t* s) {
   const int tid = threadIdx.x, lane = tid & 31;
   uint32_t* s32 = reinterpret_cast<uint32_t*>(s);
@@ -231,9 +234,9 @@ __device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t 
   }
   const int P = pow2_ceil(L);
   if (P <= kSortCap) {
-    for (int k = tid; k < P; k += kSortThreads) s[k] = k < L ? g[k] : ~0ull;
-    cta_sort(s, P);
-    for (int k = tid; k < L; k += kSortThreads) {
+    for (int k = tid; k < P; k += NT) s[k] = k < L ? g[k] : ~0ull;
+    cta_sort<NT>(s, P);
+    for (int k = tid; k < L; k += NT) {
       const uint32_t gi = static_cast<uint32_t>(s[k]);
       sorted_gauss[lo + k] = gi;
       s32[2 * k] = gi;
@@ -244,14 +247,14 @@ __device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t 
   constexpr int C = kSortCap;
   for (int c0 = 0; c0 < L; c0 += C) {
     __syncthreads();
-    for (int k = tid; k < C; k += kSortThreads) s[k] = c0 + k < L ? g[c0 + k] : ~0ull;
-    cta_sort(s, C);
-    for (int k = tid; k < C && c0 + k < L; k += kSortThreads) g[c0 + k] = s[k];
+    for (int k = tid; k < C; k += NT) s[k] = c0 + k < L ? g[c0 + k] : ~0ull;
+    cta_sort<NT>(s, C);
+    for (int k = tid; k < C && c0 + k < L; k += NT) g[c0 + k] = s[k];
   }
   for (int k = 2 * C; k <= P; k <<= 1) {
     for (int j = k >> 1; j >= C; j >>= 1) {
       __syncthreads();
-      for (int c = tid; c < (P >> 1); c += kSortThreads) {
+      for (int c = tid; c < (P >> 1); c += NT) {
         int i, p;
         ce_index(c, k, j, i, p);
         if (p < L) {
@@ -265,13 +268,13 @@ __device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t 
     }
     for (int c0 = 0; c0 < L; c0 += C) {
       __syncthreads();
-      for (int q = tid; q < C; q += kSortThreads) s[q] = c0 + q < L ? g[c0 + q] : ~0ull;
-      cta_halfclean(s);
-      for (int q = tid; q < C && c0 + q < L; q += kSortThreads) g[c0 + q] = s[q];
+      for (int q = tid; q < C; q += NT) s[q] = c0 + q < L ? g[c0 + q] : ~0ull;
+      cta_halfclean<NT>(s);
+      for (int q = tid; q < C && c0 + q < L; q += NT) g[c0 + q] = s[q];
     }
   }
   __syncthreads();
-  for (int k = tid; k < L; k += kSortThreads) {
+  for (int k = tid; k < L; k += NT) {
     sorted_gauss[lo + k] = static_cast<uint32_t>(g[k]);
   }
   __syncthreads();

@@ -89,9 +89,9 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr
 // the ballot of survivors in order from warp-private shared memory, kGroup splats at a time
 // (alphas first, independent of transmittance; then the sequential transmittance updates).
 // A warp stops when all its pixels have met the reference's termination rule.
-template <bool COUNTERS>
-__global__ void __launch_bounds__(256) blend_forward_kernel(BlendArgs a) {
-  constexpr int PX = 1, NW = 8;
+template <bool COUNTERS, int PX>
+__global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
+  constexpr int NW = 8 / PX;
   __shared__ uint64_t skeys[kSortCap];  // tile list sort; then the sorted Gaussian ids
   __shared__ float4 s0[NW][32];
   __shared__ float4 s1[NW][32];
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) blend_forward_kernel(BlendArgs a) {
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
   const long long t_start = COUNTERS ? clock64() : 0;
   // sort the tile's (depth, emission slot) keys; the ids stay in shared memory when they fit
-  const bool ids_smem = sort_tile_list(a.keys, a.sorted_gauss, lo, static_cast<int>(hi - lo), skeys);
+  const bool ids_smem = sort_tile_list<256 / PX>(a.keys, a.sorted_gauss, lo, static_cast<int>(hi - lo), skeys);
   if (COUNTERS && threadIdx.x == 0) {
     // sort-phase instrumentation: [4] sort cycles of small lists, [5] of long lists, [6] count long
     const unsigned long long sc = static_cast<unsigned long long>(clock64() - t_start);
@@ -463,16 +463,32 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
 
 }  // namespace
 
-int blend_forward(const BlendArgs& a, cudaStream_t st) {
+int blend_forward(const BlendArgs& a, int64_t num_isect, cudaStream_t st) {
   static bool init = false;
   if (!init) {
-    for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<true>),
-                          reinterpret_cast<const void*>(blend_forward_kernel<false>)})
+    for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<true, 1>),
+                          reinterpret_cast<const void*>(blend_forward_kernel<false, 1>),
+                          reinterpret_cast<const void*>(blend_forward_kernel<true, 2>),
+                          reinterpret_cast<const void*>(blend_forward_kernel<false, 2>)})
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     init = true;
   }
-  if (a.counters) blend_forward_kernel<true><<<a.tiles_x * a.tiles_y, 256, 0, st>>>(a);
-  else blend_forward_kernel<false><<<a.tiles_x * a.tiles_y, 256, 0, st>>>(a);
+  // Dense tile lists: 2 pixels per lane (4 warps of 8x8 blocks) amortise the per-splat work and
+  // idle fewer warps while a CTA sorts its list; sparse lists: 1 pixel per lane (8x4 blocks).
+  // The choice only changes the work decomposition, never the result. FGS_FWD_PX overrides.
+  static const int env = [] {
+    const char* v = std::getenv("FGS_FWD_PX");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int tiles = a.tiles_x * a.tiles_y;
+  const int px = env == 1 || env == 2 ? env : (num_isect >= 256 * static_cast<int64_t>(tiles) ? 2 : 1);
+  if (px == 1) {
+    if (a.counters) blend_forward_kernel<true, 1><<<tiles, 256, 0, st>>>(a);
+    else blend_forward_kernel<false, 1><<<tiles, 256, 0, st>>>(a);
+  } else {
+    if (a.counters) blend_forward_kernel<true, 2><<<tiles, 128, 0, st>>>(a);
+    else blend_forward_kernel<false, 2><<<tiles, 128, 0, st>>>(a);
+  }
   return 1;
 }
 
