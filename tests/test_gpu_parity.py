@@ -175,3 +175,26 @@ def test_other_camera_models_parity(rast, oracle_mod, model):
     check_keys(rast, o)
     check_image(g, o)
     check_grads(g, o)
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_full_scale_config_parity(rast, oracle_mod, cfg):
+    """The BASELINE configs at full scale (1M clustered / 3M uniform Gaussians, 1752x1168): keys,
+    sorted order and tile ranges bit-exact, image and (configs 2, 4) gradients within tolerance.
+    Config 2 has lists of up to ~2600 keys (the CTA sort's long path); configs 3 and 4 are dense
+    enough (>= 256 keys per tile on average) that forward and backward run with 2 pixels per
+    lane."""
+    from paper_2409_04751_b200 import synthetic
+
+    scene, deg, cams, dls = synthetic.config(cfg, **({"views": 1} if cfg >= 3 else {}))
+    dl = dls[0] if dls else None
+    g = run_gpu(rast, scene, cams[0], deg, dl)
+    o = run_oracle(oracle_mod, scene, cams[0], deg, dl)
+    if cfg >= 3:
+        assert o["res"].num_intersections >= 256 * cams[0].tiles_x * cams[0].tiles_y
+    check_preprocess(g, o, scene)
+    np.testing.assert_array_equal(rast.debug("offsets"), o["res"].get("offsets"))
+    np.testing.assert_array_equal(rast.debug("sorted_gauss"), o["res"].get("source")[o["res"].get("refs")])
+    check_image(g, o)
+    if dl is not None:
+        check_grads(g, o)
