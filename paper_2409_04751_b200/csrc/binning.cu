@@ -432,8 +432,8 @@ __global__ void __launch_bounds__(kT, 1) debug_keys_kernel(BinArgs a, uint32_t* 
 }
 
 int grid_size() {
-  static int g = 0;
-  if (!g) {
+  static PerDevice cache;
+  return cache.get([] {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -443,14 +443,13 @@ int grid_size() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin_kernel<true>, kT, kPrivTiles * 4);
     int per_sm2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, bin_kernel<false>, kT, 0);
-    g = (per_sm > 0 && per_sm2 > 0) ? sms : 0;
-  }
-  return g;
+    return (per_sm > 0 && per_sm2 > 0) ? sms : -1;  // -1: cooperative launch impossible
+  });
 }
 
 }  // namespace
 
-size_t bin_part_words(int tiles_y) { return static_cast<size_t>(grid_size()) * 2 + 64 + tiles_y; }
+size_t bin_part_words(int tiles_y) { return static_cast<size_t>(std::max(grid_size(), 0)) * 2 + 64 + tiles_y; }
 
 cudaError_t bin_launch(BinArgs& a, cudaStream_t st) {
   const int g = grid_size();

@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
+
 #include <cuda_runtime.h>
 
 namespace fgs {
@@ -79,6 +81,23 @@ __device__ __forceinline__ float fast_rcp(float x) {
 }
 
 __host__ __device__ inline int div_up(int a, int b) { return (a + b - 1) / b; }
+
+// Host-side one-time setup that is per device (function attributes, __constant__ data,
+// occupancy): `get(f)` runs f() once for the current device, under a lock, and caches its
+// non-zero result.
+struct PerDevice {
+  std::mutex m;
+  int v[64] = {};
+  template <typename F>
+  int get(F f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(m);
+    if (dev < 0 || dev >= 64) return f();
+    if (!v[dev]) v[dev] = f();
+    return v[dev];
+  }
+};
 
 // Conservative test: can any pixel centre of the box [x0, x1] x [y0, y1] reach
 // alpha >= 1/255 for this splat? alpha(d) = alpha_max * exp(-q(d)/2) with

@@ -464,15 +464,15 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
 }  // namespace
 
 int blend_forward(const BlendArgs& a, int64_t num_isect, cudaStream_t st) {
-  static bool init = false;
-  if (!init) {
+  static PerDevice attrs;
+  attrs.get([] {
     for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<true, 1>),
                           reinterpret_cast<const void*>(blend_forward_kernel<false, 1>),
                           reinterpret_cast<const void*>(blend_forward_kernel<true, 2>),
                           reinterpret_cast<const void*>(blend_forward_kernel<false, 2>)})
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    init = true;
-  }
+    return 1;
+  });
   // Dense tile lists: 2 pixels per lane (4 warps of 8x8 blocks) amortise the per-splat work and
   // idle fewer warps while a CTA sorts its list; sparse lists: 1 pixel per lane (8x4 blocks).
   // The choice only changes the work decomposition, never the result. FGS_FWD_PX overrides.

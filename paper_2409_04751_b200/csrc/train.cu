@@ -32,19 +32,20 @@ constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 __constant__ float c_win[kWin];
 
 // inc/metrics.hpp:23-34, evaluated in double on the host and rounded once.
-void upload_window() {
-  static bool done = false;
-  if (done) return;
-  double w[kWin], sum = 0.0;
-  for (int i = 0; i < kWin; ++i) {
-    const double d = i - kWin / 2;
-    w[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
-    sum += w[i];
-  }
-  float wf[kWin];
-  for (int i = 0; i < kWin; ++i) wf[i] = static_cast<float>(w[i] / sum);
-  cudaMemcpyToSymbol(c_win, wf, sizeof(wf));
-  done = true;
+void upload_window() {  // __constant__ memory is per device
+  static PerDevice done;
+  done.get([] {
+    double w[kWin], sum = 0.0;
+    for (int i = 0; i < kWin; ++i) {
+      const double d = i - kWin / 2;
+      w[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+      sum += w[i];
+    }
+    float wf[kWin];
+    for (int i = 0; i < kWin; ++i) wf[i] = static_cast<float>(w[i] / sum);
+    cudaMemcpyToSymbol(c_win, wf, sizeof(wf));
+    return 1;
+  });
 }
 
 // Block sum of one double per thread (kLossThreads threads); thread 0 gets the result.
