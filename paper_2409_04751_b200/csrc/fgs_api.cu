@@ -110,6 +110,7 @@ struct fgs_context {
   uint32_t num_splats = 0, num_degenerate = 0, num_culled = 0;
   size_t aux_bytes = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;  // PCIe bytes of the last host-buffer call
+  bool scene_on_host = false;  // the scene arrays of the current call are pinned host memory
   fgs::BinArgs bin_args{};
 };
 
@@ -368,7 +369,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.rowdiff = ctx->rowdiff.p;
     pa.error_flag = reinterpret_cast<int*>(ctx->scalars.p + 1);
     pa.state_counts = ctx->scalars.p + 2;
-    fgs::preprocess_kernel<<<fgs::div_up(static_cast<int>(n), 256), 256, 0, st>>>(pa);
+    if (ctx->scene_on_host) fgs::preprocess_kernel<true><<<fgs::div_up(static_cast<int>(n), 256), 256, 0, st>>>(pa);
+    else fgs::preprocess_kernel<false><<<fgs::div_up(static_cast<int>(n), 256), 256, 0, st>>>(pa);
     ++launches;
   }
   if (timing) cudaEventRecord(ev[1], st);
@@ -570,7 +572,8 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.rec = ctx->rec.p;
   if (n > 0 && (pb.m > 0 || !pb.accumulate)) {
     const int blocks = pb.m > 0 ? fgs::div_up(static_cast<int>(pb.m), fgs::kPreprocessBackwardThreads) : 1;
-    fgs::preprocess_backward_kernel<<<blocks, fgs::kPreprocessBackwardThreads, 0, st>>>(pb);
+    if (ctx->scene_on_host) fgs::preprocess_backward_kernel<true><<<blocks, fgs::kPreprocessBackwardThreads, 0, st>>>(pb);
+    else fgs::preprocess_backward_kernel<false><<<blocks, fgs::kPreprocessBackwardThreads, 0, st>>>(pb);
     ++ctx->launches;
   }
   if (timing) cudaEventRecord(ev[2], st);
@@ -636,7 +639,9 @@ int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_came
     }
     dev = fgs_gaussians{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
   }
+  ctx->scene_on_host = zero_copy;
   int rc = fgs_forward(ctx, &dev, camera, options, ctx->h_img.p, radii ? ctx->h_radii.p : nullptr, stats);
+  ctx->scene_on_host = false;
   if (rc != FGS_OK) return rc;
   FGS_CHECK(cudaMemcpyAsync(image, ctx->h_img.p, npix * 3 * 4, cudaMemcpyDeviceToHost, st));
   if (radii && n) FGS_CHECK(cudaMemcpyAsync(radii, ctx->h_radii.p, n * 4, cudaMemcpyDeviceToHost, st));
@@ -687,7 +692,9 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
     FGS_CHECK(cudaMemcpyAsync(dg.d_opacity_logits, grads->d_opacity_logits, n * 4, cudaMemcpyHostToDevice, st));
     FGS_CHECK(cudaMemcpyAsync(dg.d_sh, grads->d_sh, n * 48 * 4, cudaMemcpyHostToDevice, st));
   }
+  ctx->scene_on_host = zero_copy;
   int rc = fgs_backward(ctx, &dev, camera, ctx->h_dl.p, options, &dg);
+  ctx->scene_on_host = false;
   if (rc != FGS_OK) return rc;
   if (n) {
     FGS_CHECK(cudaMemcpyAsync(grads->d_means, dg.d_means, n * 3 * 4, cudaMemcpyDeviceToHost, st));

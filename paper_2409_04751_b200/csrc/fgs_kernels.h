@@ -80,7 +80,9 @@ struct BlendArgs {
   float* partial_tile;           // I x 9 per-intersection sums by emission slot (backward epilogue)
 };
 
+template <bool HOST_SCENE>
 __global__ void preprocess_kernel(PreprocessArgs a);
+template <bool HOST_SCENE>
 __global__ void preprocess_backward_kernel(PreprocessBackwardArgs a);
 constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per K4b CTA
 

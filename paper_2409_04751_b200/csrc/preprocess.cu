@@ -455,6 +455,9 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
 
 
 // K1: one thread per Gaussian.
+// HOST_SCENE: the scene arrays are pinned host memory read in place over PCIe (the host-buffer
+// calls); the same code, instantiated separately so profiles tell the two apart.
+template <bool HOST_SCENE>
 __global__ void __launch_bounds__(256, 4) preprocess_kernel(PreprocessArgs a) {
   __shared__ unsigned s_counts[2];
   if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
@@ -686,6 +689,7 @@ __device__ __forceinline__ void intersection_sum(const PreprocessBackwardArgs& a
 }
 
 constexpr int kBwdThreads = kPreprocessBackwardThreads;
+template <bool HOST_SCENE>
 __global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(PreprocessBackwardArgs a) {
   __shared__ uint8_t vis[kBwdThreads];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -752,5 +756,10 @@ __global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(Pre
     if (valid) gaussian_backward(a, i, sg);
   }
 }
+
+template __global__ void preprocess_kernel<false>(PreprocessArgs);
+template __global__ void preprocess_kernel<true>(PreprocessArgs);
+template __global__ void preprocess_backward_kernel<false>(PreprocessBackwardArgs);
+template __global__ void preprocess_backward_kernel<true>(PreprocessBackwardArgs);
 
 }  // namespace fgs
