@@ -369,7 +369,15 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.rowdiff = ctx->rowdiff.p;
     pa.error_flag = reinterpret_cast<int*>(ctx->scalars.p + 1);
     pa.state_counts = ctx->scalars.p + 2;
-    if (ctx->scene_on_host) fgs::preprocess_kernel<true><<<fgs::div_up(static_cast<int>(n), 256), 256, 0, st>>>(pa);
+    if (ctx->scene_on_host) {
+      static fgs::PerDevice attr;
+      attr.get([] {
+        cudaFuncSetAttribute(fgs::preprocess_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(fgs::preprocess_host_smem()));
+        return 1;
+      });
+      fgs::preprocess_kernel<true><<<fgs::div_up(static_cast<int>(n), 256), 256, fgs::preprocess_host_smem(), st>>>(pa);
+    }
     else fgs::preprocess_kernel<false><<<fgs::div_up(static_cast<int>(n), 256), 256, 0, st>>>(pa);
     ++launches;
   }
@@ -649,7 +657,7 @@ int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_came
   // bytes over PCIe: zero copy reads 40 B of geometry per Gaussian and, per splat that survives
   // the culls, its opacity and the SH coefficients of the evaluated degree
   const int deg = options ? options->sh_degree : 3;
-  const uint64_t sh_bytes = deg == 0 ? 3 * 4 : 48 * 4;
+  const uint64_t sh_bytes = deg == 0 ? 3 * 4 : (deg == 1 ? 3 * 16 : (deg == 2 ? 3 * 48 : 3 * 64));
   ctx->h2d_bytes = zero_copy ? n * 40 + static_cast<uint64_t>(ctx->num_splats) * (4 + sh_bytes) : n * 59 * 4;
   ctx->d2h_bytes = npix * 3 * 4 + (radii ? n * 4 : 0);
   return FGS_OK;

@@ -82,6 +82,7 @@ struct BlendArgs {
 
 template <bool HOST_SCENE>
 __global__ void preprocess_kernel(PreprocessArgs a);
+size_t preprocess_host_smem();  // dynamic shared memory of preprocess_kernel<true>
 template <bool HOST_SCENE>
 __global__ void preprocess_backward_kernel(PreprocessBackwardArgs a);
 constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per K4b CTA

@@ -370,12 +370,39 @@ __device__ __forceinline__ int project_covariance(const DevCamera& cam, const fl
 
 }  // namespace
 
-// K1 body for one Gaussian.
-__device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t i, unsigned* s_counts) {
+// Host-scene SH rows: float4s of one colour channel row that the degree evaluates (the
+// device path loads all four).
+__device__ __forceinline__ int sh_row_f4(int degree) { return degree == 1 ? 1 : (degree == 2 ? 3 : 4); }
+constexpr int kStageRow = 13;  // float4 per staged row: 12 + 1 pad (conflict-free LDS.128)
+// dynamic shared memory of preprocess_kernel<true>
+size_t preprocess_host_smem() { return sizeof(float4) * 8 * 32 * kStageRow; }
+
+// Warp-collective (host scene): the SH rows of the warp's lanes with `need` set, read over PCIe
+// as contiguous runs by the whole warp (a lane reading its own 192-byte row issues 16-byte
+// pieces 192 bytes apart, which PCIe serves at a third of the rate) into stage[lane][...].
+__device__ __forceinline__ void stage_sh_rows(const float* __restrict__ sh, int64_t warp_g0, bool need, int degree,
+                                              float4* stage) {
+  const int lane = threadIdx.x & 31;
+  const unsigned mask = __ballot_sync(0xffffffffu, need);
+  const int nq = sh_row_f4(degree), per_row = 3 * nq;
+  const int total = __popc(mask) * per_row;
+  for (int it = lane; it < total; it += 32) {
+    const int r = it / per_row, t = it - r * per_row;
+    const int src_lane = __fns(mask, 0, r + 1);  // the r-th needing lane
+    const int ch = t / nq, q = t - ch * nq;
+    const float4* row = reinterpret_cast<const float4*>(sh + (warp_g0 + src_lane) * 48);
+    stage[src_lane * kStageRow + ch * 4 + q] = __ldg(row + ch * 4 + q);
+  }
+  __syncwarp();
+}
+
+// K1 body for one Gaussian (every lane of the warp calls it: the host-scene variant has
+// warp-collective loads). m / ls: the mean and log-scales, read by the caller.
+template <bool HOST_SCENE>
+__device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t i, bool valid, const float m[3],
+                                               const float ls[3], unsigned* s_counts, float4* stage) {
   const DevCamera& cam = a.cam;
-  const float m[3] = {__ldg(a.means + 3 * i), __ldg(a.means + 3 * i + 1), __ldg(a.means + 3 * i + 2)};
-  const float4 q = __ldg(reinterpret_cast<const float4*>(a.rotations) + i);
-  const float ls[3] = {__ldg(a.log_scales + 3 * i), __ldg(a.log_scales + 3 * i + 1), __ldg(a.log_scales + 3 * i + 2)};
+  const float4 q = valid ? __ldg(reinterpret_cast<const float4*>(a.rotations) + i) : make_float4(1.f, 0.f, 0.f, 0.f);
 
   uint8_t state = 0;
   uint32_t key = 0xFFFFFFFFu, touched = 0;
@@ -385,7 +412,9 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
   float r2v = 0.f;
 
   Proj P;
-  const int pc = project_covariance(cam, m, q, ls, P);
+  const int pc = valid ? project_covariance(cam, m, q, ls, P) : -1;
+  bool keep = false;
+  float mx = 0.f, my = 0.f, rf = 0.f;
   if (pc == 3) {
     *a.error_flag = 1;
   } else if (pc == 2) {
@@ -395,49 +424,65 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
     const float mid = (P.sp[0][0] + P.sp[1][1]) / 2.0f;
     const float lambda_max = mid + sqrtf(fmaxf(mid * mid - det, 0.0f));
     radius = static_cast<int>(ceilf(kRadiusSigma * sqrtf(lambda_max)));
-    const float mx = P.pix[0], my = P.pix[1], rf = static_cast<float>(radius);
-    if (!(mx + rf < 0.0f || mx - rf > static_cast<float>(cam.width) || my + rf < 0.0f ||
-          my - rf > static_cast<float>(cam.height))) {
-      state = 1;
-      const float ca = P.sp[1][1] / det, cb = -P.sp[0][1] / det, cc = P.sp[0][0] / det;
-      // splatting.hpp:114: z for the pinhole, the distance for fisheye / panorama
-      const float depth = cam.model == kCamPinhole ? P.mu[2]
-                                                   : sqrtf(P.mu[0] * P.mu[0] + P.mu[1] * P.mu[1] + P.mu[2] * P.mu[2]);
-      float dir[3];
-      view_dir(cam, m, dir);
-      float Y[16];
-      sh_basis(dir, a.sh_degree, Y);
-      // one colour channel at a time (16 live coefficients instead of 48)
-      float col[3];
+    mx = P.pix[0], my = P.pix[1], rf = static_cast<float>(radius);
+    keep = !(mx + rf < 0.0f || mx - rf > static_cast<float>(cam.width) || my + rf < 0.0f ||
+             my - rf > static_cast<float>(cam.height));
+  }
+  if constexpr (HOST_SCENE) {
+    if (a.sh_degree > 0) stage_sh_rows(a.sh, i - (threadIdx.x & 31), keep, a.sh_degree, stage);
+  }
+  if (keep) {
+    state = 1;
+    const float det = P.det;
+    const float ca = P.sp[1][1] / det, cb = -P.sp[0][1] / det, cc = P.sp[0][0] / det;
+    // splatting.hpp:114: z for the pinhole, the distance for fisheye / panorama
+    const float depth = cam.model == kCamPinhole ? P.mu[2]
+                                                 : sqrtf(P.mu[0] * P.mu[0] + P.mu[1] * P.mu[1] + P.mu[2] * P.mu[2]);
+    float dir[3];
+    view_dir(cam, m, dir);
+    float Y[16];
+    sh_basis(dir, a.sh_degree, Y);
+    // one colour channel at a time (16 live coefficients instead of 48)
+    float col[3];
 #pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        float k[16];
-        load_sh16(a.sh, i, ch, a.sh_degree, k);
-        col[ch] = sh_channel(k, Y, a.sh_degree);
-      }
-      const float col0 = col[0], col1 = col[1], col2 = col[2];
-      const float alpha = sigmoid(__ldg(a.opacity + i));
-      r0 = make_float4(mx, my, ca, cb);
-      r1 = make_float4(cc, alpha, col0, col1);
-      r2v = col2;
-      key = depth_key_bits(depth);
-      // splatting.hpp:211-214 — inclusive, floor, clamped
-      const int tx0 = max(0, static_cast<int>(floorf((mx - rf) / 16.0f)));
-      const int tx1 = min(a.tiles_x - 1, static_cast<int>(floorf((mx + rf) / 16.0f)));
-      const int ty0 = max(0, static_cast<int>(floorf((my - rf) / 16.0f)));
-      const int ty1 = min(a.tiles_y - 1, static_cast<int>(floorf((my + rf) / 16.0f)));
-      if (tx1 >= tx0 && ty1 >= ty0) {
-        touched = static_cast<uint32_t>((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
-        rect = make_ushort4(tx0, tx1, ty0, ty1);
-        // per-tile counts for K2a: +1 / -1 at both ends of every covered row
-        const int rw = a.tiles_x + 1;
-        for (int ty = ty0; ty <= ty1; ++ty) {
-          atomicAdd(a.rowdiff + ty * rw + tx0, 1);
-          atomicAdd(a.rowdiff + ty * rw + tx1 + 1, -1);
+    for (int ch = 0; ch < 3; ++ch) {
+      float k[16];
+      if (HOST_SCENE && a.sh_degree > 0) {
+        const int nq = sh_row_f4(a.sh_degree);
+        const float4* st = stage + (threadIdx.x & 31) * kStageRow + ch * 4;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          const float4 v = qq < nq ? st[qq] : make_float4(0.f, 0.f, 0.f, 0.f);
+          k[4 * qq + 0] = v.x; k[4 * qq + 1] = v.y; k[4 * qq + 2] = v.z; k[4 * qq + 3] = v.w;
         }
+      } else {
+        load_sh16(a.sh, i, ch, a.sh_degree, k);
+      }
+      col[ch] = sh_channel(k, Y, a.sh_degree);
+    }
+    const float col0 = col[0], col1 = col[1], col2 = col[2];
+    const float alpha = sigmoid(__ldg(a.opacity + i));
+    r0 = make_float4(mx, my, ca, cb);
+    r1 = make_float4(cc, alpha, col0, col1);
+    r2v = col2;
+    key = depth_key_bits(depth);
+    // splatting.hpp:211-214 — inclusive, floor, clamped
+    const int tx0 = max(0, static_cast<int>(floorf((mx - rf) / 16.0f)));
+    const int tx1 = min(a.tiles_x - 1, static_cast<int>(floorf((mx + rf) / 16.0f)));
+    const int ty0 = max(0, static_cast<int>(floorf((my - rf) / 16.0f)));
+    const int ty1 = min(a.tiles_y - 1, static_cast<int>(floorf((my + rf) / 16.0f)));
+    if (tx1 >= tx0 && ty1 >= ty0) {
+      touched = static_cast<uint32_t>((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+      rect = make_ushort4(tx0, tx1, ty0, ty1);
+      // per-tile counts for K2a: +1 / -1 at both ends of every covered row
+      const int rw = a.tiles_x + 1;
+      for (int ty = ty0; ty <= ty1; ++ty) {
+        atomicAdd(a.rowdiff + ty * rw + tx0, 1);
+        atomicAdd(a.rowdiff + ty * rw + tx1 + 1, -1);
       }
     }
   }
+  if (!valid) return;
   SortedRec rr;
   rr.a = r0;
   rr.b = r1;
@@ -456,14 +501,52 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
 
 // K1: one thread per Gaussian.
 // HOST_SCENE: the scene arrays are pinned host memory read in place over PCIe (the host-buffer
-// calls); the same code, instantiated separately so profiles tell the two apart.
+// calls). Reads are then shaped for PCIe: the CTA's means and log-scales (3 KB runs each) are
+// copied through shared memory with 16-byte loads, and SH rows are fetched warp-cooperatively.
 template <bool HOST_SCENE>
 __global__ void __launch_bounds__(256, 4) preprocess_kernel(PreprocessArgs a) {
   __shared__ unsigned s_counts[2];
-  if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < a.n) preprocess_one(a, i, s_counts);
+  const int64_t i0 = int64_t(blockIdx.x) * blockDim.x;
+  const int64_t i = i0 + threadIdx.x;
+  const bool valid = i < a.n;
+  float m[3] = {0.f, 0.f, 0.f}, ls[3] = {0.f, 0.f, 0.f};
+  float4* stage = nullptr;
+  if constexpr (HOST_SCENE) {
+    __shared__ float4 s_geo[2][192];                       // means, log-scales of 256 Gaussians
+    extern __shared__ float4 s_stage[];                   // SH rows: [8 warps][32][kStageRow]
+    const int64_t nrem = a.n - i0;
+    const int nf = static_cast<int>((nrem < 256 ? nrem : 256) * 3);  // floats of this CTA
+    const float* src[2] = {a.means + i0 * 3, a.log_scales + i0 * 3};
+    // 3 * 256 floats per array; i0 * 3 * 4 bytes is 16-byte aligned (i0 is a multiple of 256)
+    for (int t = threadIdx.x; t < 2 * 192; t += blockDim.x) {
+      const int arr = t / 192, j = t - arr * 192;
+      if (4 * j + 3 < nf) s_geo[arr][j] = __ldg(reinterpret_cast<const float4*>(src[arr]) + j);
+      else {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int e = 0; e < 4; ++e) if (4 * j + e < nf) v[e] = __ldg(src[arr] + 4 * j + e);
+        s_geo[arr][j] = make_float4(v[0], v[1], v[2], v[3]);
+      }
+    }
+    if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
+    __syncthreads();
+    const float* gm = reinterpret_cast<const float*>(s_geo[0]);
+    const float* gl = reinterpret_cast<const float*>(s_geo[1]);
+    for (int c = 0; c < 3; ++c) {
+      m[c] = gm[3 * threadIdx.x + c];
+      ls[c] = gl[3 * threadIdx.x + c];
+    }
+    stage = s_stage + (threadIdx.x >> 5) * (32 * kStageRow);
+  } else {
+    if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
+    __syncthreads();
+    if (valid) {
+      for (int c = 0; c < 3; ++c) {
+        m[c] = __ldg(a.means + 3 * i + c);
+        ls[c] = __ldg(a.log_scales + 3 * i + c);
+      }
+    }
+  }
+  preprocess_one<HOST_SCENE>(a, i, valid, m, ls, s_counts, stage);
   __syncthreads();
   if (threadIdx.x < 2 && s_counts[threadIdx.x]) atomicAdd(a.state_counts + threadIdx.x, s_counts[threadIdx.x]);
 }
