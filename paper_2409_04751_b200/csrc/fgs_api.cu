@@ -284,6 +284,15 @@ int fgs_last_counts(const fgs_context* ctx, int64_t out[9]) {
   return FGS_OK;
 }
 
+// Exact ellipse culling in the blends (FGS_ELLIPSE=0 turns it off; profiling switch).
+static int blend_ellipse() {
+  static const int v = [] {
+    const char* e = std::getenv("FGS_ELLIPSE");
+    return e && *e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                 const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
   if (!ctx) return FGS_EINVAL;
@@ -423,6 +432,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   // the host grows the buffers and launches the scatter and K3 again (first frames, growing
   // scenes).
   fgs::BlendArgs ba{};
+  ba.ellipse = blend_ellipse();
   ba.width = W;
   ba.height = H;
   ba.tiles_x = tiles_x;
@@ -528,6 +538,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   FGS_CHECK(ctx->partial_tile.ensure(static_cast<size_t>(I > 0 ? I : 1) * 9));
 
   fgs::BlendArgs ba{};
+  ba.ellipse = blend_ellipse();
   ba.width = ctx->cam.width;
   ba.height = ctx->cam.height;
   ba.tiles_x = ctx->tiles_x;

@@ -45,7 +45,7 @@ struct DevCamera {
 struct SortedRec {
   float4 a;  // mean_px.x, mean_px.y, conic.a, conic.b
   float4 b;  // conic.c, alpha_max, R, G
-  float4 c;  // B, extent x, extent y (splat_extent_packed), unused
+  float4 c;  // B, extent x, extent y, tau (splat_cull_params)
 };
 
 // Correctly rounded fp32 exp / atan2 (double evaluation, one rounding): the definition the
@@ -135,20 +135,53 @@ __device__ __forceinline__ bool box_may_hit(float4 r0, float4 r1, float x0, floa
   return extent_hits(kind, r0.x, r0.y, ex, ey, x0, x1, y0, y1);
 }
 
-// The extent as K1 stores it in the record (SortedRec.c.y/.z), computed once per Gaussian:
-// kind 0 -> -inf (the box test always fails), kind 2 -> +inf (it always passes).
-__device__ __forceinline__ float2 splat_extent_packed(float4 r0, float4 r1) {
+// The culling parameters as K1 stores them in the record (SortedRec.c.y/.z/.w), computed once
+// per Gaussian: the inflated half-extents and tau2, the inflated bound on the quadratic form
+// (alpha >= 1/255 needs q <= 2 ln(255 alpha_max)). kind 0 -> -inf (every test fails), kind 2
+// -> +inf (every test passes).
+__device__ __forceinline__ float3 splat_cull_params(float4 r0, float4 r1) {
   float ex, ey;
   const int kind = splat_extent(r0, r1, ex, ey);
-  if (kind == 0) return make_float2(-INFINITY, -INFINITY);
-  if (kind == 2) return make_float2(INFINITY, INFINITY);
-  return make_float2(ex, ey);
+  if (kind == 0) return make_float3(-INFINITY, -INFINITY, -INFINITY);
+  if (kind == 2) return make_float3(INFINITY, INFINITY, INFINITY);
+  const float tau2 = __fadd_rn(__fmul_rn(__fmul_rn(2.0f, __logf(__fmul_rn(255.0f, r1.y))), 1.002f), 1e-3f);
+  return make_float3(ex, ey, tau2);
 }
 
 // box_may_hit from the stored extent: a = record .a (mean_px in .x/.y), c = record .c.
 __device__ __forceinline__ bool rec_hits(float4 a, float4 c, float x0, float x1, float y0, float y1) {
   return __fadd_rn(a.x, c.y) >= x0 && __fsub_rn(a.x, c.y) <= x1 && __fadd_rn(a.y, c.z) >= y0 &&
          __fsub_rn(a.y, c.z) <= y1;
+}
+
+// Exact form of the test above: min over the box of q(p - mean) = a dx^2 + 2b dx dy + c dy^2
+// against the record's tau2. q is convex, so the minimum is 0 when the mean lies in the box and
+// otherwise lies on an edge, where it is a clamped 1D minimum. The comparison carries a slack of
+// 1e-5 of the terms' magnitudes (far above the fp32 rounding of q) on top of tau2's own
+// inflation, so it stays conservative: a culled pair is one the reference skips. Culls ~13-19%
+// of the (block, splat) pairs the box test keeps at configs 1-2. Every op is an explicit
+// rounding intrinsic, so the backward's warps and its epilogue take identical decisions.
+__device__ __forceinline__ bool rec_hits_ellipse(float4 ra, float4 rb, float4 rc, float x0, float x1, float y0,
+                                                 float y1) {
+  const float tau = rc.w;
+  if (!(tau < INFINITY)) return tau > 0.0f;
+  const float lx = __fsub_rn(x0, ra.x), hx = __fsub_rn(x1, ra.x);
+  const float ly = __fsub_rn(y0, ra.y), hy = __fsub_rn(y1, ra.y);
+  if (lx <= 0.0f && hx >= 0.0f && ly <= 0.0f && hy >= 0.0f) return true;
+  const float a = ra.z, b = ra.w, c = rb.x;
+  const float nbc = __fdiv_rn(-b, c), nba = __fdiv_rn(-b, a);
+  auto q = [&](float dx, float dy) {
+    const float t1 = __fmul_rn(__fmul_rn(a, dx), dx);
+    const float t2 = __fmul_rn(__fmul_rn(__fmul_rn(2.0f, b), dx), dy);
+    const float t3 = __fmul_rn(__fmul_rn(c, dy), dy);
+    const float v = __fadd_rn(__fadd_rn(t1, t2), t3);
+    return __fsub_rn(v, __fmul_rn(1e-5f, __fadd_rn(__fadd_rn(t1, fabsf(t2)), t3)));
+  };
+  float best = q(lx, fminf(fmaxf(__fmul_rn(nbc, lx), ly), hy));
+  best = fminf(best, q(hx, fminf(fmaxf(__fmul_rn(nbc, hx), ly), hy)));
+  best = fminf(best, q(fminf(fmaxf(__fmul_rn(nba, ly), lx), hx), ly));
+  best = fminf(best, q(fminf(fmaxf(__fmul_rn(nba, hy), lx), hx), hy));
+  return best <= tau;
 }
 
 // Backward blend geometry: 8 warps per 16x16 tile, warp w owns the 8x4 pixel block at

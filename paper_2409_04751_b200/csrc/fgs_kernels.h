@@ -59,6 +59,7 @@ struct PreprocessBackwardArgs {
 
 struct BlendArgs {
   int width, height, tiles_x, tiles_y;
+  int ellipse;                   // backward: exact ellipse-vs-block culling on top of the box test
   const uint32_t* tile_offsets;  // T+1
   uint32_t* sorted_gauss;        // I (written by the forward's per-tile sort, read by the backward)
   uint64_t* keys;                // forward: tile list keys (K2), sorted in place per tile

@@ -486,8 +486,8 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
   SortedRec rr;
   rr.a = r0;
   rr.b = r1;
-  const float2 ext = splat_extent_packed(r0, r1);
-  rr.c = make_float4(r2v, ext.x, ext.y, 0.0f);
+  const float3 cull = splat_cull_params(r0, r1);
+  rr.c = make_float4(r2v, cull.x, cull.y, cull.z);
   a.rec[i] = rr;
   a.state[i] = state;
   a.depth_key[i] = key;

@@ -142,6 +142,8 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   SortedRec nxt = lo + 32 + lane < hi ? rec_at(lo + 32 + lane) : zero;
   for (uint32_t base = lo; base < hi; base += 32) {
     if (__all_sync(0xffffffffu, all_done())) break;
+    // (the exact ellipse test, which the backward uses, costs the forward more than the ~13%
+    // of pairs it removes at config 2)
     const bool pass = base + lane < hi && rec_hits(cur.a, cur.c, bx0, bx0 + 7.0f, by0, by0 + (4.0f * PX - 1.0f));
     s0[warp][lane] = cur.a;
     s1[warp][lane] = cur.b;
@@ -262,9 +264,12 @@ __device__ __forceinline__ void bwd_box(int tx, int ty, int w, float& x0, float&
   y1 = y0 + (4.0f * PX - 1.0f);
 }
 
+constexpr uint32_t kPassCap = 4096;  // list entries whose per-block pass bits live in shared memory
+
 template <int PX>
 __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
   constexpr int NW = 8 / PX;
+  __shared__ uint32_t s_pass[kPassCap / 4];  // 8 bits (one per warp block) per list entry
   __shared__ float4 s0[NW][32];
   __shared__ float4 s1[NW][32];
   __shared__ float s2[NW][32];
@@ -275,6 +280,8 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
   bwd_box<PX>(tx, ty, warp, bx0, bx1, by0, by1);
   const int px = static_cast<int>(bx0) + (lane & 7);
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
+  for (uint32_t j = threadIdx.x; j < min(hi - lo, kPassCap) / 4 + 1; j += blockDim.x) s_pass[j] = 0u;
+  __syncthreads();
   const float fx = static_cast<float>(px) + 0.5f;
   float T[PX], dl[PX][3], sf[PX][3], fy[PX];
   uint32_t last[PX];
@@ -307,7 +314,9 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
     const uint32_t k = base + lane;
     if (k < hi) {
       const SortedRec r = load_rec(a, k);
-      if (rec_hits(r.a, r.c, bx0, bx1, by0, by1)) {
+      if (rec_hits(r.a, r.c, bx0, bx1, by0, by1) &&
+          (!a.ellipse || rec_hits_ellipse(r.a, r.b, r.c, bx0, bx1, by0, by1))) {
+        if (k - lo < kPassCap) atomicOr(s_pass + ((k - lo) >> 2), 1u << (8 * ((k - lo) & 3) + warp));
         float* p = part + (static_cast<size_t>(k) * NW + warp) * 9;
 #pragma unroll
         for (int q = 0; q < 9; ++q) p[q] = 0.0f;
@@ -321,7 +330,9 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
     bool pass = false;
     if (k < end) {
       const SortedRec r = load_rec(a, k);
-      pass = rec_hits(r.a, r.c, bx0, bx1, by0, by1);
+      pass = rec_hits(r.a, r.c, bx0, bx1, by0, by1) &&
+             (!a.ellipse || rec_hits_ellipse(r.a, r.b, r.c, bx0, bx1, by0, by1));
+      if (pass && k - lo < kPassCap) atomicOr(s_pass + ((k - lo) >> 2), 1u << (8 * ((k - lo) & 3) + warp));
       s0[warp][lane] = r.a;
       s1[warp][lane] = r.b;
       s2[warp][lane] = r.c.x;
@@ -439,7 +450,6 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
   __syncthreads();
   for (uint32_t k = lo + threadIdx.x; k < hi; k += 256 / PX) {
     const uint32_t g = __ldg(a.sorted_gauss + k);
-    const SortedRec r = a.rec[g];
     const ushort4 rc = a.rect[g];
     // emission slot of (g, this tile): g's first slot + the tile's index in its rectangle
     const uint32_t e = a.src_off[g] + static_cast<uint32_t>((ty - rc.z) * (rc.y - rc.x + 1) + (tx - rc.x));
@@ -447,11 +457,24 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
     float sg[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) sg[q] = 0.0f;
+    // blocks whose warp wrote a slot: the pass bits the warps left, or (lists past the bit
+    // capacity) the same tests again
+    uint32_t bits = 0;
+    if (k - lo < kPassCap) {
+      bits = (s_pass[(k - lo) >> 2] >> (8 * ((k - lo) & 3))) & 0xffu;
+    } else {
+      const SortedRec r = a.rec[g];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        float x0, x1, y0, y1;
+        bwd_box<PX>(tx, ty, w, x0, x1, y0, y1);
+        if (rec_hits(r.a, r.c, x0, x1, y0, y1) && (!a.ellipse || rec_hits_ellipse(r.a, r.b, r.c, x0, x1, y0, y1)))
+          bits |= 1u << w;
+      }
+    }
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
-      float x0, x1, y0, y1;
-      bwd_box<PX>(tx, ty, w, x0, x1, y0, y1);
-      if (!rec_hits(r.a, r.c, x0, x1, y0, y1)) continue;
+      if (!(bits & (1u << w))) continue;
 #pragma unroll
       for (int q = 0; q < 9; ++q) sg[q] = sg[q] + p[w * 9 + q];
     }
