@@ -188,6 +188,134 @@ __device__ void cta_halfclean(uint64_t* s) {
   __syncthreads();
 }
 
+// CTA radix sort of L <= kRadixCap tile-list keys by depth key, then Gaussian id.
+// Stable LSD radix over the 32-bit depth key (4 passes of 8 bits, ping-pong between the two
+// halves of the shared key buffer, the last pass writing the sorted 64-bit keys) with the id
+// as payload; keys tied in depth (rare) are then
+// put in id order by one thread per run. Every warp owns a contiguous segment of the list and
+// walks it in order, so ranks follow list order: per-warp digit counts (peers by eight
+// ballots), one CTA scan over (digit, warp), then the scatter. 4 passes x 3 barriers
+// replace the bitonic network's O(log^2 L) stages.
+constexpr int kRadixCap = 2048;
+
+// Lanes holding the same 8-bit digit as this lane (among the lanes with `ok`): eight ballots.
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, bool ok) {
+  unsigned peers = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const unsigned bit = (d >> b) & 1u;
+    const unsigned bb = __ballot_sync(0xffffffffu, bit);
+    peers &= bb ^ (bit - 1u);  // bit set: bb; clear: ~bb
+  }
+  return peers;
+}
+
+template <int NT>
+__device__ void cta_radix_sort(uint32_t* s32, int L, uint32_t (*hist)[256]) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int seg = ((L + NW - 1) / NW + 31) & ~31;  // keys per warp, whole rows
+  const int b0 = warp * seg, b1 = min(L, b0 + seg);
+  uint32_t* ka = s32;                 // buffer A: keys [0, kRadixCap), ids [kRadixCap, 2 kRadixCap)
+  uint32_t* kb = s32 + 2 * kRadixCap;  // buffer B; the last pass writes (id, key) pairs over A
+#pragma unroll 1
+  for (int pass = 0; pass < 4; ++pass) {
+    const int sh = 8 * pass;
+    uint32_t* src = (pass & 1) ? kb : ka;
+    uint32_t* dst = (pass & 1) ? ka : kb;
+    for (int d = lane; d < 256; d += 32) hist[warp][d] = 0;
+    __syncwarp();
+    for (int r = b0; r < b1; r += 32) {
+      const int i = r + lane;
+      const uint32_t d = i < b1 ? (src[i] >> sh) & 0xffu : 0u;
+      const unsigned peers = digit_peers(d, i < b1);
+      if (i < b1 && (peers & lt) == 0) hist[warp][d] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // exclusive offsets in (digit, warp) order
+    for (int d = tid; d < 256; d += NT) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) t += hist[w][d];
+      hist[0][d] = hist[0][d] | (t << 16);  // stash the digit total in the high half (L < 65536)
+    }
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t run = 0;
+#pragma unroll 1
+      for (int c = 0; c < 256; c += 32) {
+        const uint32_t t = hist[0][c + lane] >> 16;
+        uint32_t x = t;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const uint32_t excl = run + x - t;
+        run += __shfl_sync(0xffffffffu, x, 31);
+        // per-warp offsets of digit c + lane
+        uint32_t acc = excl;
+        const uint32_t h0 = hist[0][c + lane] & 0xffffu;
+        hist[0][c + lane] = acc;
+        acc += h0;
+#pragma unroll
+        for (int w = 1; w < NW; ++w) {
+          const uint32_t hw = hist[w][c + lane];
+          hist[w][c + lane] = acc;
+          acc += hw;
+        }
+      }
+    }
+    __syncthreads();
+    for (int r = b0; r < b1; r += 32) {
+      const int i = r + lane;
+      const bool ok = i < b1;
+      const uint32_t key = ok ? src[i] : 0u;
+      const uint32_t id = ok ? src[kRadixCap + i] : 0u;
+      const uint32_t d = (key >> sh) & 0xffu;
+      const unsigned peers = digit_peers(d, ok);
+      if (ok) {
+        const uint32_t pos = hist[warp][d] + __popc(peers & lt);
+        if (pass == 3) {  // last pass: (id, key) pairs, i.e. the 64-bit keys, into buffer A's space
+          s32[2 * pos] = id;
+          s32[2 * pos + 1] = key;
+        } else {
+          dst[pos] = key;
+          dst[kRadixCap + pos] = id;
+        }
+      }
+      __syncwarp();
+      if (ok && (peers & lt) == 0) hist[warp][d] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  // ties in depth: ids ascending within each run of equal keys (runs are rare and short)
+  auto key_at = [&](int k) { return s32[2 * k + 1]; };
+  bool tie = false;
+  for (int i = tid + 1; i < L; i += NT) tie |= key_at(i) == key_at(i - 1);
+  if (__syncthreads_or(tie)) {
+    for (int i = tid; i < L - 1; i += NT) {
+      if (key_at(i) == key_at(i + 1) && (i == 0 || key_at(i - 1) != key_at(i))) {
+        int e = i + 1;
+        while (e + 1 < L && key_at(e + 1) == key_at(i)) ++e;
+        for (int x = i + 1; x <= e; ++x) {
+          const uint32_t t = s32[2 * x];
+          int y = x - 1;
+          while (y >= i && s32[2 * y] > t) {
+            s32[2 * (y + 1)] = s32[2 * y];
+            --y;
+          }
+          s32[2 * (y + 1)] = t;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ int pow2_ceil(int x) {
   int p = 1;
   while (p < x) p <<= 1;
@@ -197,8 +325,10 @@ __device__ __forceinline__ int pow2_ceil(int x) {
 // Sort the tile list keys[lo, lo + L) (CTA-wide call, all NT threads) by
 // (depth key, Gaussian id) and write the sorted Gaussian ids (sorted_gauss[lo + k]). Returns true when the ids are also left in shared memory: g of
 // entry k at ((uint32_t*)s)[2k] (lists of <= kSortCap keys); else read sorted_gauss.
+// hist (NT/32 x 256 counters): enables the radix path for 256 < L <= kRadixCap.
 template <int NT>
-__device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t lo, int L, uint64_t* s) {
+__device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t lo, int L, uint64_t* s,
+                               uint32_t (*hist)[256] = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31;
   uint32_t* s32 = reinterpret_cast<uint32_t*>(s);
   uint64_t* g = keys + lo;
@@ -230,6 +360,17 @@ __device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t 
       else run(std::integral_constant<int, 8>{});
     }
     __syncthreads();
+    return true;
+  }
+  if (L <= kRadixCap && hist) {
+    for (int k = tid; k < L; k += NT) {
+      const uint64_t v = g[k];
+      s32[k] = static_cast<uint32_t>(v >> 32);
+      s32[kRadixCap + k] = static_cast<uint32_t>(v);
+    }
+    __syncthreads();
+    cta_radix_sort<NT>(s32, L, hist);  // leaves the sorted 64-bit keys in s[0, L)
+    for (int k = tid; k < L; k += NT) sorted_gauss[lo + k] = s32[2 * k];
     return true;
   }
   const int P = pow2_ceil(L);

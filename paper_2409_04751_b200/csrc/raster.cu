@@ -93,9 +93,10 @@ template <bool COUNTERS, int PX>
 __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   constexpr int NW = 8 / PX;
   __shared__ uint64_t skeys[kSortCap];  // tile list sort; then the sorted Gaussian ids
-  __shared__ float4 s0[NW][32];
-  __shared__ float4 s1[NW][32];
+  __shared__ float4 s01[2][NW][32];  // record staging (s0, s1); the radix sort's digit counters before
   __shared__ float s2[NW][32];
+  float4 (*s0)[32] = s01[0];
+  float4 (*s1)[32] = s01[1];
   if (a.scalars && a.scalars[kScalarI] > a.isect_cap) return;  // speculative launch, buffers too small
   const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -105,7 +106,9 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
   const long long t_start = COUNTERS ? clock64() : 0;
   // sort the tile's (depth, emission slot) keys; the ids stay in shared memory when they fit
-  const bool ids_smem = sort_tile_list<256 / PX>(a.keys, a.sorted_gauss, lo, static_cast<int>(hi - lo), skeys);
+  static_assert(sizeof(s01) == NW * 256 * sizeof(uint32_t), "digit counters overlay the staging");
+  const bool ids_smem = sort_tile_list<256 / PX>(a.keys, a.sorted_gauss, lo, static_cast<int>(hi - lo), skeys,
+                                                 reinterpret_cast<uint32_t(*)[256]>(&s01[0][0][0]));
   if (COUNTERS && threadIdx.x == 0) {
     // sort-phase instrumentation: [4] sort cycles of small lists, [5] of long lists, [6] count long
     const unsigned long long sc = static_cast<unsigned long long>(clock64() - t_start);
