@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import subprocess
+import sys
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,7 +32,8 @@ _ref = None
 
 def build(quiet=True):
     """Build the oracle (and, when /root/reference is mounted, the reference) via make."""
-    subprocess.run(["make", "-C", HERE] + (["-s"] if quiet else []), check=True)
+    # make's messages go to stderr: callers such as bench.py print one JSON line on stdout
+    subprocess.run(["make", "-C", HERE] + (["-s"] if quiet else []), check=True, stdout=sys.stderr)
 
 
 def _p(a, ct):
