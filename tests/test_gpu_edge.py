@@ -221,15 +221,17 @@ def test_backward_unaligned_gradient_fields(rast, oracle_mod):
         assert rel_l2(got[:, GROUPS[k]], ref[:, GROUPS[k]]) <= 1e-3, k
 
 
-def test_dense_tile_long_lists_and_depth_ties(rast, oracle_mod):
-    """Per-tile lists far beyond the 4096-entry shared-memory sort (chunked global/shared
-    bitonic path), with exact depth-key ties (duplicated means) that only the source index
-    breaks: sorted order, ranges, image and gradients vs the oracle."""
+@pytest.mark.parametrize("n_distinct,min_len,max_len", [(6000, 2 * 4096, None), (1500, 2049, 4096),
+                                                        (500, 257, 2048)])
+def test_dense_tile_long_lists_and_depth_ties(rast, oracle_mod, n_distinct, min_len, max_len):
+    """Per-tile lists in each sort regime -- beyond the 4096-entry shared-memory sort (chunked
+    global/shared bitonic path), the shared-memory bitonic range and the radix range -- with
+    exact depth-key ties (duplicated means) that only the source index breaks
+    (SPEC.md:270-271): sorted order, ranges, image and gradients vs the oracle."""
     import torch
     from paper_2409_04751_b200 import BackwardOptions, RenderOptions, Scene, grads_as_rows
 
     rng = np.random.default_rng(11)
-    n_distinct = 6000
     d = np.array([0.2, 0.1, 1.0]) / np.linalg.norm([0.2, 0.1, 1.0])
     base = d * rng.uniform(3.0, 6.0, size=(n_distinct, 1)) + rng.normal(0, 0.02, size=(n_distinct, 3))
     means = np.repeat(base, 2, axis=0).astype(np.float32)  # every depth key appears twice
@@ -245,7 +247,8 @@ def test_dense_tile_long_lists_and_depth_ties(rast, oracle_mod):
     img, st = rast.forward(ds, cam, RenderOptions(sh_degree=0), want_stats=True)
     res = oracle_mod.render(sc, cam, sh_degree=0)
     off = res.get("offsets")
-    assert np.diff(off).max() > 2 * 4096, np.diff(off).max()
+    longest = int(np.diff(off).max())
+    assert longest >= min_len and (max_len is None or longest <= max_len), longest
     np.testing.assert_array_equal(rast.debug("offsets"), off)
     np.testing.assert_array_equal(rast.debug("sorted_gauss"), res.get("source")[res.get("refs")])
     torch.cuda.synchronize()
@@ -280,14 +283,16 @@ def test_capacity_growth_and_speculative_launch(rast, oracle_mod):
         assert np.abs(img.cpu().numpy().astype(np.float64) - res.image).max() <= 1e-3
 
 
-def test_zero_copy_host_path_equals_device_path(rast):
+@pytest.mark.parametrize("deg", [3, 2, 1, 0])
+def test_zero_copy_host_path_equals_device_path(rast, deg):
     """Pinned host scene arrays are read in place over PCIe by K1 / K4b (fgs_render_host,
-    fgs_backward_host); results equal the device-resident path bit for bit, and the library
-    reports the bytes it moved."""
+    fgs_backward_host): K1 stages geometry per CTA and fetches each SH degree's rows
+    warp-cooperatively; results equal the device-resident path bit for bit at every degree and
+    at scene sizes that end mid-CTA, and the library reports the bytes it moved."""
     import torch
     from paper_2409_04751_b200 import BackwardOptions, RenderOptions, Scene, grads_as_rows, synthetic
 
-    sc, deg, cams, dls = synthetic.config(1, n=30000)
+    sc, _, cams, dls = synthetic.config(1, n=30000 + 7 * deg)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).pin_memory().numpy()
     hs = Scene(pin(sc.means), pin(sc.rotations), pin(sc.log_scales), pin(sc.opacity_logits), pin(sc.sh),
                sc.background)
