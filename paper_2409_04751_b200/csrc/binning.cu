@@ -253,20 +253,30 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
   const int nr = r_hi - r_lo + 1;  // <= kSub: every Gaussian here owns >= 1 slot
   for (int i = tid; i < nr; i += kT) s_off[i] = a.coff[r_lo + i];
   __syncthreads();
+  trace(a.trace, 0, 1);
   uint32_t ev[U], gv[U], tv[U], pv[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) {
-    ev[u] = lo + u * kT + tid;
+  // each thread owns U consecutive slots: one binary search for the first, then a forward walk
+  // (a Gaussian owns ~3 slots on average, so the walk advances a step or two)
+  {
+    const uint32_t e0 = lo + static_cast<uint32_t>(tid) * U;
     int l = 0, h = nr - 1;
     while (l < h) {
       const int mid = (l + h + 1) >> 1;
-      if (s_off[mid] <= ev[u]) l = mid;
+      if (s_off[mid] <= e0) l = mid;
       else h = mid - 1;
     }
-    tv[u] = static_cast<uint32_t>(l);  // local rank for now
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      ev[u] = e0 + u;
+      while (l + 1 < nr && s_off[l + 1] <= ev[u]) ++l;
+      tv[u] = static_cast<uint32_t>(l);  // local rank for now
+    }
   }
 #pragma unroll
   for (int u = 0; u < U; ++u) gv[u] = ev[u] < hi ? a.cval[r_lo + tv[u]] : 0u;
+  uint32_t dk[U];  // depth keys, in flight across the atomics
+#pragma unroll
+  for (int u = 0; u < U; ++u) dk[u] = a.depth_key[gv[u]];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     if (ev[u] >= hi) continue;
@@ -275,15 +285,18 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
     const int j = static_cast<int>(ev[u] - s_off[tv[u]]);
     tv[u] = static_cast<uint32_t>((rc.z + j / wx) * a.tiles_x + rc.x + j % wx);
   }
+  if (a.trace) { __syncthreads(); trace(a.trace, 0, 3); }
   if (PRIV) {
 #pragma unroll
     for (int u = 0; u < U; ++u) pv[u] = ev[u] < hi ? atomicAdd(s_cnt + tv[u], 1u) : 1u;
     __syncthreads();
+    trace(a.trace, 0, 4);
     // the slot that took local position 0 reserves the CTA's block of tile tv[u]
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (pv[u] == 0) s_cnt[tv[u]] = atomicAdd(a.fill + tv[u], s_cnt[tv[u]]);
     __syncthreads();
+    trace(a.trace, 0, 2);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (ev[u] < hi) pv[u] += s_cnt[tv[u]];
@@ -294,7 +307,7 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     if (ev[u] >= hi) continue;
-    a.keys[pv[u]] = (static_cast<uint64_t>(a.depth_key[gv[u]]) << 32) | gv[u];
+    a.keys[pv[u]] = (static_cast<uint64_t>(dk[u]) << 32) | gv[u];
   }
   __syncthreads();  // s_cnt / s_off reused by the next range
 }
@@ -344,9 +357,7 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
   }
   // rows spread over CTAs first (row ty -> CTA ty mod G), so no CTA gets two
   for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw) row_counts(a, ty, hist, rowtot);
-  trace(a.trace, 0, 3);
   grid.sync();
-  trace(a.trace, 0, 4);
   {
     uint32_t p1, tot1, p2, tot2;
     cta_prefix(a.part_scan, 2, G, sm.warp_tmp, p1, tot1);

@@ -22,6 +22,6 @@ for _ in range(3):
     torch.cuda.synchronize()
     t = r.debug("bin_trace", np.uint64).astype(np.int64)
     t0 = t[0]
-    names = ["start(cta0)", "start(tiler)", "tiler done", "phase1 done(cta0)", "sync1", "phase2 done", "sync2",
+    names = ["start(cta0)", "scatter: ranks+offs", "scatter: global atomics", "scatter: gathers", "scatter: smem atomics", "phase2 done", "sync2",
              "scatter done"]
     print("  ".join(f"{n}={(v - t0) / 1000:.1f}us" for n, v in zip(names, t)))
