@@ -255,10 +255,12 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
   __syncthreads();
   trace(a.trace, 0, 1);
   uint32_t ev[U], gv[U], tv[U], pv[U];
-  // each thread owns U consecutive slots: one binary search for the first, then a forward walk
-  // (a Gaussian owns ~3 slots on average, so the walk advances a step or two)
+  // each thread owns un <= U consecutive slots (every thread busy when the range is short): one
+  // binary search for the first, then a forward walk (a Gaussian owns ~3 slots on average, so
+  // the walk advances a step or two)
   {
-    const uint32_t e0 = lo + static_cast<uint32_t>(tid) * U;
+    const uint32_t un = (hi - lo + kT - 1) / kT;
+    const uint32_t e0 = lo + static_cast<uint32_t>(tid) * un;
     int l = 0, h = nr - 1;
     while (l < h) {
       const int mid = (l + h + 1) >> 1;
@@ -267,8 +269,9 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      ev[u] = e0 + u;
-      while (l + 1 < nr && s_off[l + 1] <= ev[u]) ++l;
+      ev[u] = u < static_cast<int>(un) ? e0 + u : hi;  // hi: no slot
+      if (ev[u] < hi)
+        while (l + 1 < nr && s_off[l + 1] <= ev[u]) ++l;
       tv[u] = static_cast<uint32_t>(l);  // local rank for now
     }
   }
