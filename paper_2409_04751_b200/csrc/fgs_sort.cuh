@@ -323,16 +323,18 @@ __device__ __forceinline__ int pow2_ceil(int x) {
 }
 
 // Sort the tile list keys[lo, lo + L) (CTA-wide call, all NT threads) by
-// (depth key, Gaussian id) and write the sorted Gaussian ids (sorted_gauss[lo + k]). Returns true when the ids are also left in shared memory: g of
-// entry k at ((uint32_t*)s)[2k] (lists of <= kSortCap keys); else read sorted_gauss.
+// (depth key, Gaussian id) and write the sorted Gaussian ids (sorted_gauss[lo + k]). Returns the
+// word offset in s at which the ids are also left in shared memory (g of entry k at
+// ((uint32_t*)s)[offset + k]: 0 for lists of <= 256, 2 kRadixCap for the radix range), or -1
+// (read sorted_gauss).
 // hist (NT/32 x 256 counters): enables the radix path for 256 < L <= kRadixCap.
 template <int NT>
-__device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t lo, int L, uint64_t* s,
-                               uint32_t (*hist)[256] = nullptr) {
+__device__ int sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t lo, int L, uint64_t* s,
+                              uint32_t (*hist)[256] = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31;
   uint32_t* s32 = reinterpret_cast<uint32_t*>(s);
   uint64_t* g = keys + lo;
-  if (L <= 0) return true;
+  if (L <= 0) return 0;
   if (L <= kChunk) {
     if (tid < 32) {
       auto run = [&](auto e_tag) {
@@ -350,7 +352,7 @@ __device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t 
           if (i < L) {
             const uint32_t gi = static_cast<uint32_t>(x[r]);
             sorted_gauss[lo + i] = gi;
-            s32[2 * i] = gi;
+            s32[i] = gi;
           }
         }
       };
@@ -360,7 +362,7 @@ __device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t 
       else run(std::integral_constant<int, 8>{});
     }
     __syncthreads();
-    return true;
+    return 0;
   }
   if (L <= kRadixCap && hist) {
     for (int k = tid; k < L; k += NT) {
@@ -370,20 +372,21 @@ __device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t 
     }
     __syncthreads();
     cta_radix_sort<NT>(s32, L, hist);  // leaves the sorted 64-bit keys in s[0, L)
-    for (int k = tid; k < L; k += NT) sorted_gauss[lo + k] = s32[2 * k];
-    return true;
+    for (int k = tid; k < L; k += NT) {
+      const uint32_t gi = s32[2 * k];
+      sorted_gauss[lo + k] = gi;
+      s32[2 * kRadixCap + k] = gi;
+    }
+    __syncthreads();
+    return 2 * kRadixCap;
   }
   const int P = pow2_ceil(L);
   if (P <= kSortCap) {
     for (int k = tid; k < P; k += NT) s[k] = k < L ? g[k] : ~0ull;
     cta_sort<NT>(s, P);
-    for (int k = tid; k < L; k += NT) {
-      const uint32_t gi = static_cast<uint32_t>(s[k]);
-      sorted_gauss[lo + k] = gi;
-      s32[2 * k] = gi;
-    }
+    for (int k = tid; k < L; k += NT) sorted_gauss[lo + k] = static_cast<uint32_t>(s[k]);
     __syncthreads();
-    return true;
+    return -1;
   }
   constexpr int C = kSortCap;
   for (int c0 = 0; c0 < L; c0 += C) {
@@ -419,7 +422,7 @@ __device__ bool sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t 
     sorted_gauss[lo + k] = static_cast<uint32_t>(g[k]);
   }
   __syncthreads();
-  return false;
+  return -1;
 }
 
 }  // namespace

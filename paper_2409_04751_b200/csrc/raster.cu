@@ -92,9 +92,10 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr
 template <bool COUNTERS, int PX>
 __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   constexpr int NW = 8 / PX;
-  __shared__ uint64_t skeys[kSortCap];  // tile list sort; then the sorted Gaussian ids
+  __shared__ __align__(16) uint64_t skeys[kSortCap];  // tile list sort; then the sorted ids and the raw records
   __shared__ float4 s01[2][NW][32];  // record staging (s0, s1); the radix sort's digit counters before
   __shared__ float s2[NW][32];
+  __shared__ uint32_t sk[NW][32];    // list index of each staged record
   float4 (*s0)[32] = s01[0];
   float4 (*s1)[32] = s01[1];
   if (a.scalars && a.scalars[kScalarI] > a.isect_cap) return;  // speculative launch, buffers too small
@@ -107,8 +108,8 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   const long long t_start = COUNTERS ? clock64() : 0;
   // sort the tile's (depth, emission slot) keys; the ids stay in shared memory when they fit
   static_assert(sizeof(s01) == NW * 256 * sizeof(uint32_t), "digit counters overlay the staging");
-  const bool ids_smem = sort_tile_list<256 / PX>(a.keys, a.sorted_gauss, lo, static_cast<int>(hi - lo), skeys,
-                                                 reinterpret_cast<uint32_t(*)[256]>(&s01[0][0][0]));
+  const int id_off = sort_tile_list<256 / PX>(a.keys, a.sorted_gauss, lo, static_cast<int>(hi - lo), skeys,
+                                              reinterpret_cast<uint32_t(*)[256]>(&s01[0][0][0]));
   if (COUNTERS && threadIdx.x == 0) {
     // sort-phase instrumentation: [4] sort cycles of small lists, [5] of long lists, [6] count long
     const unsigned long long sc = static_cast<unsigned long long>(clock64() - t_start);
@@ -117,10 +118,12 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     if (big) atomicAdd(a.counters + 6, 1ull);
     atomicAdd(a.counters + 7, 1ull);
   }
-  const uint32_t* sid = reinterpret_cast<const uint32_t*>(skeys);
-  auto rec_at = [&](uint32_t k) -> SortedRec {
-    return a.rec[ids_smem ? sid[2 * (k - lo)] : __ldg(a.sorted_gauss + k)];
-  };
+  uint32_t* s32 = reinterpret_cast<uint32_t*>(skeys);
+  // raw records of the warp's next chunk (32 x 48 bytes), filled by cp.async; they sit in the
+  // part of the sort buffer the ids do not use (ids at word 0 for short lists, at 2 kRadixCap
+  // for the radix range, in global memory otherwise)
+  float4* raw = reinterpret_cast<float4*>(s32 + (id_off == 0 ? 2 * kRadixCap : 0)) + warp * 96;
+  static_assert(sizeof(skeys) >= (2 * kRadixCap + NW * 96 * 4) * 4, "raw record buffers fit the sort buffer");
   const float fx = static_cast<float>(px) + 0.5f;
   const float bx0 = static_cast<float>(bx) + 0.5f, by0 = static_cast<float>(by) + 0.5f;
   unsigned long long warp_evals = 0;
@@ -139,35 +142,48 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     for (int q = 0; q < PX; ++q) d = d && ps[q].done;
     return d;
   };
-
-  const SortedRec zero{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-  SortedRec cur = lo + lane < hi ? rec_at(lo + lane) : zero;
-  SortedRec nxt = lo + 32 + lane < hi ? rec_at(lo + 32 + lane) : zero;
+  // issue the copies of chunk [base, base + 32)'s records into raw (one record per lane)
+  auto prefetch = [&](uint32_t base) {
+    const uint32_t k = base + lane;
+    if (k < hi) {
+      const uint32_t g = id_off >= 0 ? s32[id_off + (k - lo)] : __ldg(a.sorted_gauss + k);
+      const float4* src = reinterpret_cast<const float4*>(a.rec + g);
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(raw + lane * 3));
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + q) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const unsigned lt = (1u << lane) - 1u;
+  prefetch(lo);
   for (uint32_t base = lo; base < hi; base += 32) {
     if (__all_sync(0xffffffffu, all_done())) break;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
     // (the exact ellipse test, which the backward uses, costs the forward more than the ~13%
     // of pairs it removes at config 2)
-    const bool pass = base + lane < hi && rec_hits(cur.a, cur.c, bx0, bx0 + 7.0f, by0, by0 + (4.0f * PX - 1.0f));
-    s0[warp][lane] = cur.a;
-    s1[warp][lane] = cur.b;
-    s2[warp][lane] = cur.c.x;
-    uint32_t mask = __ballot_sync(0xffffffffu, pass);
-    if (COUNTERS) warp_evals += __popc(mask);
-    cur = nxt;
-    if (base + 64 + lane < hi) nxt = rec_at(base + 64 + lane);
+    const float4 ra = raw[lane * 3], rc = raw[lane * 3 + 2];
+    const bool pass = base + lane < hi && rec_hits(ra, rc, bx0, bx0 + 7.0f, by0, by0 + (4.0f * PX - 1.0f));
+    // survivors compacted, in list order, into the warp's staging slots
+    const uint32_t mask = __ballot_sync(0xffffffffu, pass);
+    const int nsurv = __popc(mask);
+    if (COUNTERS) warp_evals += nsurv;
+    if (pass) {
+      const int pos = __popc(mask & lt);
+      s0[warp][pos] = ra;
+      s1[warp][pos] = raw[lane * 3 + 1];
+      s2[warp][pos] = rc.x;
+      sk[warp][pos] = base + lane;
+    }
     __syncwarp();
-    while (mask) {
-      int js[kGroup];
-#pragma unroll
-      for (int q = 0; q < kGroup; ++q) {
-        js[q] = mask ? __ffs(mask) - 1 : -1;
-        mask &= mask - 1;
-      }
+    if (base + 32 < hi) prefetch(base + 32);
+    for (int j0 = 0; j0 < nsurv; j0 += kGroup) {
       float al[kGroup][PX], pw[kGroup][PX], am[kGroup], cr[kGroup], cg_[kGroup], cb[kGroup];
       bool any_near = false;
 #pragma unroll
       for (int q = 0; q < kGroup; ++q) {
-        const int jj = js[q] >= 0 ? js[q] : 0;
+        const int jj = j0 + q < nsurv ? j0 + q : j0;
         const float4 r0 = s0[warp][jj];
         const float4 r1 = s1[warp][jj];
         cr[q] = r1.z;
@@ -197,14 +213,16 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
       }
 #pragma unroll
       for (int q = 0; q < kGroup; ++q) {
-        if (js[q] < 0) break;
+        if (j0 + q >= nsurv) break;
+        const uint32_t k = sk[warp][j0 + q];
 #pragma unroll
         for (int u = 0; u < PX; ++u)
-          blend_apply<COUNTERS>(ps[u], alpha_final(pw[q][u], al[q][u]), cr[q], cg_[q], cb[q], base + js[q]);
+          blend_apply<COUNTERS>(ps[u], alpha_final(pw[q][u], al[q][u]), cr[q], cg_[q], cb[q], k);
       }
     }
     __syncwarp();
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   if (COUNTERS) {
     const long long t_cta = clock64() - t_start;
     unsigned long long ev = 0, ec = 0;
