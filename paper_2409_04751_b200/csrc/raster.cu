@@ -294,6 +294,8 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
   __shared__ float4 s0[NW][32];
   __shared__ float4 s1[NW][32];
   __shared__ float s2[NW][32];
+  __shared__ uint32_t sk[NW][32];            // list index of each staged record
+  __shared__ float4 s_raw[NW][96];           // the next chunk's records (cp.async)
   const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -344,39 +346,56 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
       }
     }
   }
-  // reverse walk over [lo, wlast)
+  // reverse walk over [lo, wlast) in 32-entry chunks: the chunk's records arrive by cp.async
+  // one chunk ahead into the warp's raw buffer; survivors are compacted latest first into the
+  // staging slots
+  float4* raw = s_raw[warp];
+  auto prefetch = [&](int64_t end) {  // chunk [max(lo, end - 32), end)
+    const int64_t k = max(static_cast<int64_t>(lo), end - 32) + lane;
+    if (k < end) {
+      const float4* src = reinterpret_cast<const float4*>(a.rec + __ldg(a.sorted_gauss + k));
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(raw + lane * 3));
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + q) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const unsigned gt = ~((2u << lane) - 1u);  // lanes above this one
+  if (wlast > lo) prefetch(wlast);
   for (int64_t end = wlast; end > static_cast<int64_t>(lo); end -= 32) {
     const uint32_t cstart = static_cast<uint32_t>(max(static_cast<int64_t>(lo), end - 32));
     const uint32_t k = cstart + lane;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    const float4 ra = raw[lane * 3], rb = raw[lane * 3 + 1], rc = raw[lane * 3 + 2];
     bool pass = false;
     if (k < end) {
-      const SortedRec r = load_rec(a, k);
-      pass = rec_hits(r.a, r.c, bx0, bx1, by0, by1) &&
-             (!a.ellipse || rec_hits_ellipse(r.a, r.b, r.c, bx0, bx1, by0, by1));
+      pass = rec_hits(ra, rc, bx0, bx1, by0, by1) && (!a.ellipse || rec_hits_ellipse(ra, rb, rc, bx0, bx1, by0, by1));
       if (pass && k - lo < kPassCap) atomicOr(s_pass + ((k - lo) >> 2), 1u << (8 * ((k - lo) & 3) + warp));
-      s0[warp][lane] = r.a;
-      s1[warp][lane] = r.b;
-      s2[warp][lane] = r.c.x;
     }
-    uint32_t mask = __ballot_sync(0xffffffffu, pass);
+    const uint32_t mask = __ballot_sync(0xffffffffu, pass);
+    const int nsurv = __popc(mask);
+    if (pass) {
+      const int pos = __popc(mask & gt);
+      s0[warp][pos] = ra;
+      s1[warp][pos] = rb;
+      s2[warp][pos] = rc.x;
+      sk[warp][pos] = k;
+    }
     __syncwarp();
+    if (end - 32 > static_cast<int64_t>(lo)) prefetch(end - 32);
     // Groups of 3 surviving splats, latest first. Their alphas are independent of the
     // transmittance and are computed together; the transmittance/suffix recurrence then runs
     // in list order, leaving 3 x 9 per-lane gradients (summed over the lane's pixels), which one
     // butterfly reduce-scatter over the warp sums (31 shuffles); lane l ends with value l.
-    while (mask) {
-      int js[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        js[q] = mask ? 31 - __clz(mask) : -1;
-        if (mask) mask &= ~(1u << js[q]);
-      }
+    for (int j0 = 0; j0 < nsurv; j0 += 3) {
       float pw[3][PX], ex[3][PX], ar[3][PX], dxs[3], dys[3][PX];
       float4 r0s[3], r1s[3];
       bool any_near = false;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const int jj = js[q] >= 0 ? js[q] : 0;
+        const int jj = j0 + q < nsurv ? j0 + q : j0;
         r0s[q] = s0[warp][jj];
         r1s[q] = s1[warp][jj];
         dxs[q] = __fsub_rn(fx, r0s[q].x);
@@ -406,16 +425,18 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
       bool contrib_any = false;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const uint32_t kk = cstart + static_cast<uint32_t>(js[q]);
+        const bool valid = j0 + q < nsurv;
+        const int jj = valid ? j0 + q : j0;
+        const uint32_t kk = sk[warp][jj];
         const float4 r0 = r0s[q], r1 = r1s[q];
-        const float b2 = s2[warp][js[q] >= 0 ? js[q] : 0];
+        const float b2 = s2[warp][jj];
         const float dx = dxs[q];
 #pragma unroll
         for (int c9 = 0; c9 < 9; ++c9) v[9 * q + c9] = 0.0f;
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
           const float alpha = fminf(kAlphaClamp, ar[q][u]);
-          const bool c = js[q] >= 0 && kk < last[u] && pw[q][u] <= 0.0f && pw[q][u] >= kPowerFloor &&
+          const bool c = valid && kk < last[u] && pw[q][u] <= 0.0f && pw[q][u] >= kPowerFloor &&
                          alpha >= kAlphaSkip;
           contrib_any |= c;
           const float dy = dys[q][u];
@@ -460,11 +481,12 @@ __global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
       }
       // lane l now holds component l % 9 of splat l / 9 (l < 27)
       const int q = lane / 9;
-      if (lane < 27 && js[q] >= 0)
-        part[(static_cast<size_t>(cstart + js[q]) * NW + warp) * 9 + (lane - 9 * q)] = v[0];
+      if (lane < 27 && j0 + q < nsurv)
+        part[(static_cast<size_t>(sk[warp][j0 + q]) * NW + warp) * 9 + (lane - 9 * q)] = v[0];
     }
     __syncwarp();
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   // Epilogue: per entry of the tile, the 9 gradients summed over the pixel blocks that passed
   // the culling test, in block order (the partials are this CTA's own, L2-resident writes),
   // stored at the intersection's emission slot (K4b then reads each Gaussian's contiguously).
