@@ -288,7 +288,7 @@ __device__ __forceinline__ void bwd_box(int tx, int ty, int w, float& x0, float&
 constexpr uint32_t kPassCap = 4096;  // list entries whose per-block pass bits live in shared memory
 
 template <int PX>
-__global__ void __launch_bounds__(256 / PX) blend_backward_kernel(BlendArgs a) {
+__global__ void __launch_bounds__(256 / PX, PX == 1 ? 4 : 1) blend_backward_kernel(BlendArgs a) {
   constexpr int NW = 8 / PX;
   __shared__ uint32_t s_pass[kPassCap / 4];  // 8 bits (one per warp block) per list entry
   __shared__ float4 s0[NW][32];
