@@ -559,16 +559,17 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, cudaStream_t st) {
 }
 
 int blend_backward(const BlendArgs& a, int64_t num_isect, cudaStream_t st) {
-  // Dense tile lists (measured: config 4, ~545 entries per tile) amortise the per-splat
-  // overhead (chunk staging, culling, group selection, the 27-value warp reduction) better over
-  // 8x8 warp blocks with 2 pixels per lane; sparser ones (config 2, ~104) cull better with
-  // 8x4 blocks. FGS_BWD_PX=1|2 overrides.
+  // 8x8 warp blocks with 2 pixels per lane amortise the per-splat overhead (chunk staging,
+  // culling, the 27-value warp reduction) over twice the pixels; with the exact ellipse culling
+  // that wins from ~30 entries per tile up (measured: config 1 0.19 -> 0.16 ms, config 2
+  // 0.345 -> 0.313 ms, config 4), while the sparse config 0 keeps 8x4 blocks.
+  // FGS_BWD_PX=1|2 overrides.
   static const int env = [] {
     const char* v = std::getenv("FGS_BWD_PX");
     return v ? std::atoi(v) : 0;
   }();
   const int tiles = a.tiles_x * a.tiles_y;
-  const int px = env == 1 || env == 2 ? env : (num_isect >= 256 * static_cast<int64_t>(tiles) ? 2 : 1);
+  const int px = env == 1 || env == 2 ? env : (num_isect >= 32 * static_cast<int64_t>(tiles) ? 2 : 1);
   if (px == 1) blend_backward_kernel<1><<<tiles, 256, 0, st>>>(a);
   else blend_backward_kernel<2><<<tiles, 128, 0, st>>>(a);
   return 1;
