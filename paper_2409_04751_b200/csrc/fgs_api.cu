@@ -51,6 +51,78 @@ struct DevBuf {  // owning device allocation that only grows (freed on destructi
 
 }  // namespace
 
+// Forward-blend pixels-per-lane autotuning: the first frames of a context time both work
+// decompositions (CUDA events around the launch, read back without blocking on a later frame,
+// normalised by the frame's intersection count since views differ in cost) and keep the
+// faster; a >2x change in the intersection count starts over. Results do not depend
+// on the choice (each pixel's blend is the same sequence of operations).
+struct PxTuner {
+  cudaEvent_t a[3] = {}, b[3] = {};  // per pixels-per-lane value (1, 2)
+  bool pending[3] = {false, false, false};
+  int64_t work[3] = {0, 0, 0};        // intersections of the timed frame (views differ in cost)
+  float best[3] = {0.0f, 0.0f, 0.0f};
+  int samples[3] = {0, 0, 0};
+  int choice = 0;
+  int64_t ref = 0;
+  int timing = 0;  // px of the launch being issued (between pick and done)
+  static constexpr int kSamples = 3;
+  void create() {
+    for (int p = 1; p <= 2; ++p) {
+      cudaEventCreate(&a[p]);
+      cudaEventCreate(&b[p]);
+    }
+  }
+  void destroy() {
+    for (int p = 1; p <= 2; ++p) {
+      if (a[p]) cudaEventDestroy(a[p]);
+      if (b[p]) cudaEventDestroy(b[p]);
+    }
+  }
+  void reset() {
+    pending[1] = pending[2] = false;
+    samples[1] = samples[2] = 0;
+    choice = 0;
+  }
+  void collect(int64_t isect) {
+    for (int p = 1; p <= 2; ++p) {
+      if (!pending[p] || cudaEventQuery(b[p]) != cudaSuccess) continue;
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, a[p], b[p]) == cudaSuccess && work[p] > 0) {
+        const float per = ms / static_cast<float>(work[p]);  // time per intersection
+        best[p] = samples[p] ? std::min(best[p], per) : per;
+        ++samples[p];
+      }
+      pending[p] = false;
+    }
+    if (!choice && samples[1] >= kSamples && samples[2] >= kSamples) {
+      choice = best[1] <= best[2] ? 1 : 2;
+      ref = isect;
+    }
+  }
+  // pixels per lane for this launch (0: the kernel's own rule); records the start event when timed
+  int pick(int64_t isect, cudaStream_t st) {
+    timing = 0;
+    if (!a[1] || isect <= 0) return 0;
+    if (choice && (isect > 2 * ref || 2 * isect < ref)) reset();
+    collect(isect);
+    if (choice) return choice;
+    int p = samples[1] <= samples[2] ? 1 : 2;
+    if (pending[p]) p = 3 - p;
+    if (pending[p]) return 0;
+    cudaEventRecord(a[p], st);
+    work[p] = isect;
+    timing = p;
+    return p;
+  }
+  void done(cudaStream_t st) {
+    if (!timing) return;
+    cudaEventRecord(b[timing], st);
+    pending[timing] = true;
+    timing = 0;
+  }
+  void drop() { pending[1] = pending[2] = false; }
+};
+
 struct fgs_context {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -79,6 +151,7 @@ struct fgs_context {
   cudaEvent_t ev_scan = nullptr;  // after K2a's scalars reached the host
   cudaEvent_t ev_k2 = nullptr;    // K2 done on the caller's stream
   cudaStream_t aux = nullptr;     // the scalars' readback, off the caller's stream so K3 follows K2 directly
+  PxTuner fwd_px;
   DevBuf<float> final_T;
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
@@ -216,6 +289,7 @@ int fgs_create(int device, fgs_context** out) {
   cudaEventCreateWithFlags(&ctx->ev_scan, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_k2, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
+  ctx->fwd_px.create();
   if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(24) != cudaSuccess ||
       false) {
     fgs_destroy(ctx);
@@ -253,6 +327,7 @@ int fgs_destroy(fgs_context* ctx) {
     if (ev) cudaEventDestroy(ev);
   if (ctx->ev_scan) cudaEventDestroy(ctx->ev_scan);
   if (ctx->ev_k2) cudaEventDestroy(ctx->ev_k2);
+  ctx->fwd_px.destroy();
   if (ctx->aux) {
     cudaStreamSynchronize(ctx->aux);
     cudaStreamDestroy(ctx->aux);
@@ -473,7 +548,9 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     ba.keys = ctx->keys.p;
     ba.sorted_gauss = ctx->sorted_gauss.p;
     // density hint for the work decomposition: this frame's I once known, else the last frame's
-    const int l = fgs::blend_forward(ba, ctx->num_isect, st);
+    const int px = (ctx->flags & FGS_FLAG_COUNTERS) ? 0 : ctx->fwd_px.pick(ctx->num_isect, st);
+    const int l = fgs::blend_forward(ba, ctx->num_isect, px, st);
+    ctx->fwd_px.done(st);
     if (timing) cudaEventRecord(ev[4], st);
     return l;
   };
@@ -493,6 +570,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ctx->num_culled = static_cast<uint32_t>(n) - ctx->num_splats - ctx->num_degenerate;
   if (I >= (int64_t(1) << 30)) return fail(ctx, FGS_ENOMEM, "forward: intersection count exceeds 2^30");
   if (!speculative || I > ctx->isect_cap) {
+    ctx->fwd_px.drop();  // the timed launch (if any) exited without work
     // (re)size the per-intersection buffers (cudaFree / cudaMalloc synchronise with the
     // speculative kernels, which exited without work) and launch for real
     const size_t ni = static_cast<size_t>(I > 0 ? I : 1);

@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(256 / PX, PX == 1 ? 4 : 1) blend_backward_kern
 
 }  // namespace
 
-int blend_forward(const BlendArgs& a, int64_t num_isect, cudaStream_t st) {
+int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStream_t st) {
   static PerDevice attrs;
   attrs.get([] {
     for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<true, 1>),
@@ -539,15 +539,21 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, cudaStream_t st) {
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return 1;
   });
-  // Dense tile lists: 2 pixels per lane (4 warps of 8x8 blocks) amortise the per-splat work and
-  // idle fewer warps while a CTA sorts its list; sparse lists: 1 pixel per lane (8x4 blocks).
-  // The choice only changes the work decomposition, never the result. FGS_FWD_PX overrides.
+  // 2 pixels per lane (4 warps of 8x8 blocks) amortise the per-splat work and idle fewer warps
+  // while a CTA sorts its list; 1 pixel per lane (8x4 blocks) culls and terminates finer. Which
+  // wins depends on the scene, not only on the list lengths (config 1: 2 by 18%; the
+  // heavy-tailed config 2: 1 by 22%), so the caller times both (px_request); without a request
+  // dense lists take 2. The choice only changes the work decomposition, never a pixel's value.
+  // FGS_FWD_PX overrides.
   static const int env = [] {
     const char* v = std::getenv("FGS_FWD_PX");
     return v ? std::atoi(v) : 0;
   }();
   const int tiles = a.tiles_x * a.tiles_y;
-  const int px = env == 1 || env == 2 ? env : (num_isect >= 256 * static_cast<int64_t>(tiles) ? 2 : 1);
+  const int px = env == 1 || env == 2 ? env
+                 : px_request == 1 || px_request == 2
+                     ? px_request
+                     : (num_isect >= 256 * static_cast<int64_t>(tiles) ? 2 : 1);
   if (px == 1) {
     if (a.counters) blend_forward_kernel<true, 1><<<tiles, 256, 0, st>>>(a);
     else blend_forward_kernel<false, 1><<<tiles, 256, 0, st>>>(a);

@@ -113,6 +113,23 @@ def test_forward_and_backward_are_deterministic(rast):
     assert outs[0] == outs[1] == outs[2]
 
 
+def test_forward_independent_of_pixels_per_lane(rast):
+    """The first frames of a context time both forward work decompositions (1 and 2 pixels per
+    lane) and keep the faster; every frame's image must be the same bits either way."""
+    import torch
+    from paper_2409_04751_b200 import Rasterizer, RenderOptions, synthetic
+
+    r = Rasterizer(0)  # fresh context: starts tuning
+    sc, deg, cams, _ = synthetic.config(1, n=40000)
+    ds = to_device(sc)
+    imgs = set()
+    for _ in range(16):
+        img, _ = r.forward(ds, cams[0], RenderOptions(sh_degree=deg))
+        torch.cuda.synchronize()
+        imgs.add(img.cpu().numpy().tobytes())
+    assert len(imgs) == 1
+
+
 def test_multiview_accumulate_equals_sum(rast):
     import torch
     from paper_2409_04751_b200 import BackwardOptions, RenderOptions, synthetic
