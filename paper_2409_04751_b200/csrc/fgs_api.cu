@@ -51,7 +51,8 @@ struct DevBuf {  // owning device allocation that only grows (freed on destructi
 
 }  // namespace
 
-// Forward-blend pixels-per-lane autotuning: the first frames of a context time both work
+// Autotuning between two launch variants with identical results (forward: pixels per lane;
+// backward: register / occupancy variant): the first frames of a context time both work
 // decompositions (CUDA events around the launch, read back without blocking on a later frame,
 // normalised by the frame's intersection count since views differ in cost) and keep the
 // faster; a >2x change in the intersection count starts over. Results do not depend
@@ -152,6 +153,7 @@ struct fgs_context {
   cudaEvent_t ev_k2 = nullptr;    // K2 done on the caller's stream
   cudaStream_t aux = nullptr;     // the scalars' readback, off the caller's stream so K3 follows K2 directly
   PxTuner fwd_px;
+  PxTuner bwd_var;  // backward blend occupancy variant (same results)
   DevBuf<float> final_T;
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
@@ -290,6 +292,7 @@ int fgs_create(int device, fgs_context** out) {
   cudaEventCreateWithFlags(&ctx->ev_k2, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   ctx->fwd_px.create();
+  ctx->bwd_var.create();
   if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(24) != cudaSuccess ||
       false) {
     fgs_destroy(ctx);
@@ -328,6 +331,7 @@ int fgs_destroy(fgs_context* ctx) {
   if (ctx->ev_scan) cudaEventDestroy(ctx->ev_scan);
   if (ctx->ev_k2) cudaEventDestroy(ctx->ev_k2);
   ctx->fwd_px.destroy();
+  ctx->bwd_var.destroy();
   if (ctx->aux) {
     cudaStreamSynchronize(ctx->aux);
     cudaStreamDestroy(ctx->aux);
@@ -655,7 +659,11 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   if (timing && ctx->pending.size() > 64) drain_sets(ctx, 8);
   cudaEvent_t* ev = timing ? take_set(ctx, 1)->e : nullptr;
   if (timing) cudaEventRecord(ev[0], st);
-  if (I > 0) ctx->launches += fgs::blend_backward(ba, I, st);
+  if (I > 0) {
+    const int var = ctx->bwd_var.pick(I, st);
+    ctx->launches += fgs::blend_backward(ba, I, var, st);
+    ctx->bwd_var.done(st);
+  }
   if (timing) cudaEventRecord(ev[1], st);
 
   fgs::PreprocessBackwardArgs pb{};

@@ -125,7 +125,7 @@ cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* ke
 
 // ---- blend (raster.cu) ----
 int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStream_t st);
-int blend_backward(const BlendArgs& a, int64_t num_isect, cudaStream_t st);
+int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStream_t st);
 // ---- training step (train.cu) ----
 // L1 + D-SSIM loss and dL/drendered (inc/metrics.hpp:86-195). maps: loss_scratch_floats();
 // partials: 2 * loss_partials() + 2 doubles, the last two = (sum of SSIM map, sum |x - y|).

@@ -287,8 +287,10 @@ __device__ __forceinline__ void bwd_box(int tx, int ty, int w, float& x0, float&
 
 constexpr uint32_t kPassCap = 4096;  // list entries whose per-block pass bits live in shared memory
 
-template <int PX>
-__global__ void __launch_bounds__(256 / PX, PX == 1 ? 4 : 1) blend_backward_kernel(BlendArgs a) {
+// MINB: CTAs per SM the register allocation is fitted to (a launch-bounds variant: same code,
+// same results, different occupancy; which is faster depends on the scene).
+template <int PX, int MINB>
+__global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArgs a) {
   constexpr int NW = 8 / PX;
   __shared__ uint32_t s_pass[kPassCap / 4];  // 8 bits (one per warp block) per list entry
   __shared__ float4 s0[NW][32];
@@ -564,7 +566,7 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStr
   return 1;
 }
 
-int blend_backward(const BlendArgs& a, int64_t num_isect, cudaStream_t st) {
+int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStream_t st) {
   // 8x8 warp blocks with 2 pixels per lane amortise the per-splat overhead (chunk staging,
   // culling, the 27-value warp reduction) over twice the pixels; with the exact ellipse culling
   // that wins from ~30 entries per tile up (measured: config 1 0.19 -> 0.16 ms, config 2
@@ -576,8 +578,12 @@ int blend_backward(const BlendArgs& a, int64_t num_isect, cudaStream_t st) {
   }();
   const int tiles = a.tiles_x * a.tiles_y;
   const int px = env == 1 || env == 2 ? env : (num_isect >= 32 * static_cast<int64_t>(tiles) ? 2 : 1);
-  if (px == 1) blend_backward_kernel<1><<<tiles, 256, 0, st>>>(a);
-  else blend_backward_kernel<2><<<tiles, 128, 0, st>>>(a);
+  // 2 pixels per lane: variant 1 at ~116 registers (4 CTAs per SM), variant 2 fitted to 6 CTAs
+  // per SM (config 2: 0.313 vs 0.350 ms; configs 1 and 4 the other way round) -- the caller
+  // times both; identical results.
+  if (px == 1) blend_backward_kernel<1, 4><<<tiles, 256, 0, st>>>(a);
+  else if (variant == 2) blend_backward_kernel<2, 6><<<tiles, 128, 0, st>>>(a);
+  else blend_backward_kernel<2, 1><<<tiles, 128, 0, st>>>(a);
   return 1;
 }
 
