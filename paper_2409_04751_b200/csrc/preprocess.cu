@@ -553,7 +553,11 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(PreprocessArgs a) {
 
 // K4b per-Gaussian chain rule for Gaussian i with its summed screen-space gradient sg[9]
 // (mean_px 2, conic 3, colour 3, alpha 1); writes (or adds) its 59 gradient values.
-__device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& a, int64_t i, const float sg[9]) {
+// shstage: this lane's 20-float slot -- the SH gradient rows are Y (x) dcolour, so the lane leaves
+// Y[16] (band-masked), dcolour[3] (clamp-masked) and i there and the warp writes the rows as
+// contiguous 192-byte runs afterwards (sh_rows_store).
+__device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& a, int64_t i, const float sg[9],
+                                                  float* shstage) {
   float out[11];  // mean 3, rotation 4, log-scale 3, opacity 1 (SH rows are stored as computed)
 #pragma unroll
   for (int k = 0; k < 11; ++k) out[k] = 0.0f;
@@ -691,26 +695,14 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
     sh_basis(dir, a.sh_degree, Y);
     const int nb = a.full_sh ? (a.sh_degree + 1) * (a.sh_degree + 1) : 1;
     float ddir[3] = {0.0f, 0.0f, 0.0f};
-    float* dsh = a.d_sh + 48 * i;
+#pragma unroll
+    for (int jb = 0; jb < 16; ++jb) shstage[jb] = jb < nb ? (jb == 0 ? float(kC0) : Y[jb]) : 0.0f;
+    shstage[19] = __int_as_float(static_cast<int>(i));
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
       const bool live = colour[ch] > 0.0f;  // clamped channel: no gradient
       const float dc = sg[5 + ch];
-      float g[16];
-#pragma unroll
-      for (int jb = 0; jb < 16; ++jb) g[jb] = (live && jb < nb) ? (jb == 0 ? float(kC0) : Y[jb]) * dc : 0.0f;
-      float* d = dsh + 16 * ch;
-      if (a.accumulate) {
-#pragma unroll
-        for (int jb = 0; jb < 16; ++jb) d[jb] += g[jb];
-      } else if (a.aligned16) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          reinterpret_cast<float4*>(d)[k] = make_float4(g[4 * k], g[4 * k + 1], g[4 * k + 2], g[4 * k + 3]);
-      } else {
-#pragma unroll
-        for (int jb = 0; jb < 16; ++jb) d[jb] = g[jb];
-      }
+      shstage[16 + ch] = live ? dc : 0.0f;
       if (live && a.view_dir && a.sh_degree > 0) {
         float k[16];
         load_sh_channel(a.sh, i, ch, a.sh_degree, k);
@@ -772,9 +764,39 @@ __device__ __forceinline__ void intersection_sum(const PreprocessBackwardArgs& a
 }
 
 constexpr int kBwdThreads = kPreprocessBackwardThreads;
+
+// The warp's SH gradient rows (one per lane with `has`), from the lanes' slots: row r's float4 c
+// is Y[4 (c % 4) ..] * dcolour[c / 4]; 12 lanes cover a row with contiguous 16-byte accesses
+// (a lane writing its own row issues 16-byte pieces 192 bytes apart). The products are the
+// same single-rounded multiplications as per lane.
+__device__ __forceinline__ void sh_rows_store(const PreprocessBackwardArgs& a, const float* stage, bool has) {
+  const int lane = threadIdx.x & 31;
+  const unsigned mask = __ballot_sync(0xffffffffu, has);
+  const int total = __popc(mask) * 12;
+  __syncwarp();
+  for (int it = lane; it < total; it += 32) {
+    const int r = it / 12, c = it - 12 * r;
+    const int src = __fns(mask, 0, r + 1);
+    const float* st = stage + src * 20;
+    const int64_t i = __float_as_int(st[19]);
+    const float dc = st[16 + c / 4];
+    const float4 y = *reinterpret_cast<const float4*>(st + 4 * (c & 3));
+    // (+ 0.0f: masked entries are +0 whatever the signs of the factors)
+    const float4 g = make_float4(y.x * dc + 0.0f, y.y * dc + 0.0f, y.z * dc + 0.0f, y.w * dc + 0.0f);
+    float* d = a.d_sh + 48 * i + 4 * c;
+    if (a.accumulate) {
+      d[0] += g.x; d[1] += g.y; d[2] += g.z; d[3] += g.w;
+    } else if (a.aligned16) {
+      *reinterpret_cast<float4*>(d) = g;
+    } else {
+      d[0] = g.x; d[1] = g.y; d[2] = g.z; d[3] = g.w;
+    }
+  }
+}
 template <bool HOST_SCENE>
 __global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(PreprocessBackwardArgs a) {
   __shared__ uint8_t vis[kBwdThreads];
+  __shared__ __align__(16) float s_shstage[kBwdThreads * 20];  // per-lane SH gradient factors
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t q0 = int64_t(blockIdx.x) * kBwdThreads;
   const int64_t q1 = q0 + kBwdThreads < a.m ? q0 + kBwdThreads : a.m;  // this CTA's slice of cval
@@ -836,7 +858,9 @@ __global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(Pre
         if (lane == jl) sg[k] = acc[k];
       }
     }
-    if (valid) gaussian_backward(a, i, sg);
+    float* slot = s_shstage + tid * 20;
+    if (valid) gaussian_backward(a, i, sg, slot);
+    sh_rows_store(a, s_shstage + (tid & ~31) * 20, valid);
   }
 }
 
