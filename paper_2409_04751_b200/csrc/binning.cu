@@ -166,9 +166,8 @@ __device__ void row_counts(const BinArgs& a, int ty, uint32_t* hist, uint32_t* r
 // Phase 2: tile offsets and scatter cursors of row ty (row prefix + in-row exclusive scan),
 // blend schedule slots (tiles by descending list length: log2 buckets, empty tiles last).
 __device__ void row_offsets(const BinArgs& a, int ty, const uint32_t* rowtot, const uint32_t* hist, uint32_t* cur,
-                            uint32_t bprefix_lane) {
+                            uint32_t bprefix_lane, uint32_t* wsm) {
   const int lane = threadIdx.x & 31;
-  const uint32_t lt = lanemask_lt();
   uint32_t pre = 0;
   for (int r = lane; r < ty; r += 32) pre += rowtot[r];
 #pragma unroll
@@ -189,6 +188,11 @@ __device__ void row_offsets(const BinArgs& a, int ty, const uint32_t* rowtot, co
       if (lane >= o) incl += y;
     }
     uint32_t off = carry + incl - sum;
+    // schedule slots: ranks within the row's bucket counts (warp-private shared counters), then
+    // one global reservation per bucket for the whole row
+    wsm[lane] = 0u;
+    __syncwarp();
+    uint32_t rk[kRowItems];
 #pragma unroll
     for (int i = 0; i < kRowItems; ++i) {
       const int x = c0 + lane * kRowItems + i;
@@ -197,16 +201,20 @@ __device__ void row_offsets(const BinArgs& a, int ty, const uint32_t* rowtot, co
       if (cell) {
         a.tile_offsets[t] = off;
         a.fill[t] = off;
+        rk[i] = atomicAdd(wsm + sched_bucket(c[i]), 1u);
       }
       off += c[i];
-      const int bk = cell ? sched_bucket(c[i]) : 31;
-      const uint32_t peers = __match_any_sync(0xffffffffu, bk);
-      const int leader = __ffs(peers) - 1;
-      uint32_t base = 0;
-      if (bk != 31 && lane == leader) base = atomicAdd(cur + bk, __popc(peers));
-      base = __shfl_sync(0xffffffffu, base, leader) + __shfl_sync(0xffffffffu, bprefix_lane, bk & 31);
-      if (cell) a.tile_order[base + __popc(peers & lt)] = static_cast<uint32_t>(t);
     }
+    __syncwarp();
+    if (lane < kSchedBuckets && wsm[lane]) wsm[32 + lane] = atomicAdd(cur + lane, wsm[lane]) + bprefix_lane;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < kRowItems; ++i) {
+      const int x = c0 + lane * kRowItems + i;
+      if (x < a.tiles_x)
+        a.tile_order[wsm[32 + sched_bucket(c[i])] + rk[i]] = static_cast<uint32_t>(ty * a.tiles_x + x);
+    }
+    __syncwarp();
     carry += __shfl_sync(0xffffffffu, incl, 31);
   }
   if (ty == a.tiles_y - 1 && lane == 0) {
@@ -385,7 +393,8 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
       for (int o = 16; o > 0; o >>= 1) big += __shfl_xor_sync(0xffffffffu, big, o);
       if (lane == 0) a.scalars[kScalarBig] = big;
     }
-    for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw) row_offsets(a, ty, rowtot, hist, cur, bprefix);
+    for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw)
+      row_offsets(a, ty, rowtot, hist, cur, bprefix, s_off + 64 * (tid >> 5));  // s_off: free until the scatter
     uint32_t run1 = p1, run2 = p2;
     for (int sb = lo; sb < hi; sb += kT * kItems) {
       const int r0 = sb + tid * kItems;
