@@ -466,16 +466,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.rowdiff = ctx->rowdiff.p;
     pa.error_flag = reinterpret_cast<int*>(ctx->scalars.p + 1);
     pa.state_counts = ctx->scalars.p + 2;
-    if (ctx->scene_on_host) {
-      static fgs::PerDevice attr;
-      attr.get([] {
-        cudaFuncSetAttribute(fgs::preprocess_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(fgs::preprocess_host_smem()));
-        return 1;
-      });
-      fgs::preprocess_kernel<true><<<fgs::div_up(static_cast<int>(n), 256), 256, fgs::preprocess_host_smem(), st>>>(pa);
-    }
-    else fgs::preprocess_kernel<false><<<fgs::div_up(static_cast<int>(n), 256), 256, 0, st>>>(pa);
+    fgs::preprocess_launch(pa, ctx->scene_on_host, st);
     ++launches;
   }
   if (timing) cudaEventRecord(ev[1], st);
@@ -693,9 +684,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.cval = ctx->cval.p;
   pb.rec = ctx->rec.p;
   if (n > 0 && (pb.m > 0 || !pb.accumulate)) {
-    const int blocks = pb.m > 0 ? fgs::div_up(static_cast<int>(pb.m), fgs::kPreprocessBackwardThreads) : 1;
-    if (ctx->scene_on_host) fgs::preprocess_backward_kernel<true><<<blocks, fgs::kPreprocessBackwardThreads, 0, st>>>(pb);
-    else fgs::preprocess_backward_kernel<false><<<blocks, fgs::kPreprocessBackwardThreads, 0, st>>>(pb);
+    fgs::preprocess_backward_launch(pb, ctx->scene_on_host, st);
     ++ctx->launches;
   }
   if (timing) cudaEventRecord(ev[2], st);

@@ -81,11 +81,10 @@ struct BlendArgs {
   float* partial_tile;           // I x 9 per-intersection sums by emission slot (backward epilogue)
 };
 
-template <bool HOST_SCENE>
-__global__ void preprocess_kernel(PreprocessArgs a);
-size_t preprocess_host_smem();  // dynamic shared memory of preprocess_kernel<true>
-template <bool HOST_SCENE>
-__global__ void preprocess_backward_kernel(PreprocessBackwardArgs a);
+// K1 / K4b launches (preprocess.cu); host_scene: the scene arrays are pinned host memory read in
+// place over PCIe (separate instantiations, so profiles tell the two apart).
+void preprocess_launch(const PreprocessArgs& a, bool host_scene, cudaStream_t st);
+void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene, cudaStream_t st);
 constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per K4b CTA
 
 // ---- binning / sorting (binning.cu) ----

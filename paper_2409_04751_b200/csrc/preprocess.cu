@@ -375,7 +375,7 @@ __device__ __forceinline__ int project_covariance(const DevCamera& cam, const fl
 __device__ __forceinline__ int sh_row_f4(int degree) { return degree == 1 ? 1 : (degree == 2 ? 3 : 4); }
 constexpr int kStageRow = 13;  // float4 per staged row: 12 + 1 pad (conflict-free LDS.128)
 // dynamic shared memory of preprocess_kernel<true>
-size_t preprocess_host_smem() { return sizeof(float4) * 8 * 32 * kStageRow; }
+static size_t preprocess_host_smem() { return sizeof(float4) * 8 * 32 * kStageRow; }
 
 // Warp-collective (host scene): the SH rows of the warp's lanes with `need` set, read over PCIe
 // as contiguous runs by the whole warp (a lane reading its own 192-byte row issues 16-byte
@@ -864,9 +864,25 @@ __global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(Pre
   }
 }
 
-template __global__ void preprocess_kernel<false>(PreprocessArgs);
-template __global__ void preprocess_kernel<true>(PreprocessArgs);
-template __global__ void preprocess_backward_kernel<false>(PreprocessBackwardArgs);
-template __global__ void preprocess_backward_kernel<true>(PreprocessBackwardArgs);
+void preprocess_launch(const PreprocessArgs& a, bool host_scene, cudaStream_t st) {
+  const int blocks = div_up(static_cast<int>(a.n), 256);
+  if (host_scene) {
+    static PerDevice attr;
+    attr.get([] {
+      cudaFuncSetAttribute(preprocess_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(preprocess_host_smem()));
+      return 1;
+    });
+    preprocess_kernel<true><<<blocks, 256, preprocess_host_smem(), st>>>(a);
+  } else {
+    preprocess_kernel<false><<<blocks, 256, 0, st>>>(a);
+  }
+}
+
+void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene, cudaStream_t st) {
+  const int blocks = a.m > 0 ? div_up(static_cast<int>(a.m), kBwdThreads) : 1;
+  if (host_scene) preprocess_backward_kernel<true><<<blocks, kBwdThreads, 0, st>>>(a);
+  else preprocess_backward_kernel<false><<<blocks, kBwdThreads, 0, st>>>(a);
+}
 
 }  // namespace fgs

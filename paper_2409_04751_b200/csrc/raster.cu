@@ -25,7 +25,6 @@ namespace fgs {
 
 namespace {
 
-constexpr int kBlend = 256;     // threads per tile CTA = pixels per tile
 constexpr int kGroup = 4;         // forward: splats whose alphas are computed together
 
 // Record of sorted entry k, through the sorted Gaussian index.
