@@ -757,11 +757,11 @@ int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_came
   FGS_CHECK(cudaMemcpyAsync(image, ctx->h_img.p, npix * 3 * 4, cudaMemcpyDeviceToHost, st));
   if (radii && n) FGS_CHECK(cudaMemcpyAsync(radii, ctx->h_radii.p, n * 4, cudaMemcpyDeviceToHost, st));
   FGS_CHECK(cudaStreamSynchronize(st));
-  // bytes over PCIe: zero copy reads 40 B of geometry per Gaussian and, per splat that survives
-  // the culls, its opacity and the SH coefficients of the evaluated degree
+  // bytes over PCIe: zero copy reads 40 B of geometry and the opacity of every Gaussian and,
+  // per splat that survives the culls, the SH coefficients of the evaluated degree
   const int deg = options ? options->sh_degree : 3;
   const uint64_t sh_bytes = deg == 0 ? 3 * 4 : (deg == 1 ? 3 * 16 : (deg == 2 ? 3 * 48 : 3 * 64));
-  ctx->h2d_bytes = zero_copy ? n * 40 + static_cast<uint64_t>(ctx->num_splats) * (4 + sh_bytes) : n * 59 * 4;
+  ctx->h2d_bytes = zero_copy ? n * 44 + static_cast<uint64_t>(ctx->num_splats) * sh_bytes : n * 59 * 4;
   ctx->d2h_bytes = npix * 3 * 4 + (radii ? n * 4 : 0);
   return FGS_OK;
 }

@@ -403,6 +403,9 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
                                                const float ls[3], unsigned* s_counts, float4* stage) {
   const DevCamera& cam = a.cam;
   const float4 q = valid ? __ldg(reinterpret_cast<const float4*>(a.rotations) + i) : make_float4(1.f, 0.f, 0.f, 0.f);
+  // host scene: every lane reads its opacity (one coalesced 128-byte run per warp over PCIe
+  // instead of scattered 4-byte reads by the kept lanes)
+  const float op_host = HOST_SCENE && valid ? __ldg(a.opacity + i) : 0.0f;
 
   uint8_t state = 0;
   uint32_t key = 0xFFFFFFFFu, touched = 0;
@@ -461,7 +464,7 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
       col[ch] = sh_channel(k, Y, a.sh_degree);
     }
     const float col0 = col[0], col1 = col[1], col2 = col[2];
-    const float alpha = sigmoid(__ldg(a.opacity + i));
+    const float alpha = sigmoid(HOST_SCENE ? op_host : __ldg(a.opacity + i));
     r0 = make_float4(mx, my, ca, cb);
     r1 = make_float4(cc, alpha, col0, col1);
     r2v = col2;
