@@ -90,7 +90,8 @@ typedef struct fgs_backward_options {
                                    inc/gradients.hpp:255-262); 0 (default) = reference parity */
 } fgs_backward_options;
 
-/* RenderStats (inc/splatting.hpp:41-48); stage times from CUDA events. */
+/* RenderStats (inc/splatting.hpp:41-48); stage times from CUDA events. The per-tile sort runs
+   inside the blend kernel: its time is part of raster_ms and sort_ms is 0. */
 typedef struct fgs_stats {
   uint64_t num_intersections;
   uint32_t num_splats, num_culled, num_degenerate;

@@ -251,7 +251,8 @@ void drain_sets(fgs_context* ctx, size_t keep) {
     cudaEventSynchronize(es.e[nint]);
     for (int k = 0; k < nint; ++k) {
       float ms = 0.0f;
-      cudaEventElapsedTime(&ms, es.e[k], es.e[k + 1]);
+      if (es.kind == 0 && k == 2) continue;  // forward: the sort runs inside K3 (no event 3)
+      cudaEventElapsedTime(&ms, es.e[es.kind == 0 && k == 3 ? 2 : k], es.e[k + 1]);
       ctx->acc_ms[(es.kind == 0 ? 0 : 4) + k] += ms;
     }
     ctx->acc_calls[es.kind] += 1;
@@ -510,8 +511,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   }
   FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, ctx->scalars.p, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, rb));
   FGS_CHECK(cudaEventRecord(ctx->ev_scan, rb));
-  if (timing) cudaEventRecord(ev[2], st);
-  if (timing) cudaEventRecord(ev[3], st);
+  if (timing) cudaEventRecord(ev[2], st);  // (no separate sort stage: K3 sorts each tile's list)
 
   // K3 (sort each tile's list + blend) is launched before the host knows I, against the
   // capacity of the per-intersection buffers, so the GPU never waits for the host: K2's scatter
@@ -593,8 +593,10 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ctx->have_fwd = true;
   if (stats) {
     FGS_CHECK(cudaEventSynchronize(ev[4]));
-    float ms[4];
-    for (int s = 0; s < 4; ++s) cudaEventElapsedTime(&ms[s], ev[s], ev[s + 1]);
+    float ms[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    cudaEventElapsedTime(&ms[0], ev[0], ev[1]);
+    cudaEventElapsedTime(&ms[1], ev[1], ev[2]);
+    cudaEventElapsedTime(&ms[3], ev[2], ev[4]);  // sort_ms stays 0: K3 sorts each tile's list
     if (!(ctx->flags & FGS_FLAG_TIMING)) {  // stats-only timing: recycle the set now
       ctx->spare.push_back(ctx->pending.back());
       ctx->pending.pop_back();
