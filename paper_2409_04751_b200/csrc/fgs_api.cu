@@ -153,6 +153,11 @@ struct fgs_context {
   cudaEvent_t ev_k2 = nullptr;    // K2 done on the caller's stream
   cudaStream_t aux = nullptr;     // the scalars' readback, off the caller's stream so K3 follows K2 directly
   PxTuner fwd_px;
+  // The device scalars alternate between two 16-word halves by frame parity; a frame's K3 zeroes
+  // the other half for the next frame (whose previous readback finished before this frame began),
+  // so no memset precedes K1. scalars_clean[h]: half h is known to be zero.
+  int64_t frame = 0;
+  bool scalars_clean[2] = {true, true};
   PxTuner bwd_var;  // backward blend occupancy variant (same results)
   DevBuf<float> final_T;
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
@@ -294,7 +299,7 @@ int fgs_create(int device, fgs_context** out) {
   cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   ctx->fwd_px.create();
   ctx->bwd_var.create();
-  if (ctx->scalars.ensure(16) != cudaSuccess || ctx->counters.ensure(24) != cudaSuccess ||
+  if (ctx->scalars.ensure(32) != cudaSuccess || cudaMemset(ctx->scalars.p, 0, 32 * sizeof(uint32_t)) != cudaSuccess || ctx->counters.ensure(24) != cudaSuccess ||
       false) {
     fgs_destroy(ctx);
     return FGS_ENOMEM;
@@ -444,7 +449,10 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   if (timing) cudaEventRecord(ev[0], st);
   uint64_t launches = 0;
 
-  FGS_CHECK(cudaMemsetAsync(ctx->scalars.p, 0, 16 * sizeof(uint32_t), st));
+  const int half = static_cast<int>(ctx->frame++ & 1);
+  uint32_t* scalars = ctx->scalars.p + 16 * half;
+  if (!ctx->scalars_clean[half]) FGS_CHECK(cudaMemsetAsync(scalars, 0, 16 * sizeof(uint32_t), st));
+  ctx->scalars_clean[half] = false;
   if (ctx->flags & FGS_FLAG_COUNTERS) FGS_CHECK(cudaMemsetAsync(ctx->counters.p, 0, 24 * sizeof(unsigned long long), st));
   if (n > 0) {
     fgs::PreprocessArgs pa{};
@@ -465,8 +473,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.rect = ctx->rect.p;
     pa.radii = ctx->radii.p;
     pa.rowdiff = ctx->rowdiff.p;
-    pa.error_flag = reinterpret_cast<int*>(ctx->scalars.p + 1);
-    pa.state_counts = ctx->scalars.p + 2;
+    pa.error_flag = reinterpret_cast<int*>(scalars + 1);
+    pa.state_counts = scalars + 2;
     fgs::preprocess_launch(pa, ctx->scene_on_host, st);
     ++launches;
   }
@@ -484,7 +492,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.rowdiff = ctx->rowdiff.p;
   bn.cval = ctx->cval.p;
   bn.coff = ctx->coff.p;
-  bn.scalars = ctx->scalars.p;
+  bn.scalars = scalars;
   bn.part_scan = ctx->scan_status.p;
   bn.tile_offsets = ctx->tile_offsets.p;
   bn.fill = ctx->fill.p;
@@ -509,7 +517,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     FGS_CHECK(cudaEventRecord(ctx->ev_k2, st));
     FGS_CHECK(cudaStreamWaitEvent(rb, ctx->ev_k2, 0));
   }
-  FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, ctx->scalars.p, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, rb));
+  FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, scalars, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, rb));
   FGS_CHECK(cudaEventRecord(ctx->ev_scan, rb));
   if (timing) cudaEventRecord(ev[2], st);  // (no separate sort stage: K3 sorts each tile's list)
 
@@ -532,7 +540,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ba.last = ctx->last.p;
   ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
   ba.tile_order = n > 0 ? ctx->tile_order.p : nullptr;
-  ba.scalars = ctx->scalars.p;
+  ba.scalars = scalars;
+  ba.zero_next = ctx->scalars.p + 16 * (1 - half);
   if (ba.counters) {
     FGS_CHECK(ctx->tile_cycles.ensure(num_tiles));
     FGS_CHECK(cudaMemsetAsync(ctx->tile_cycles.p, 0, num_tiles * sizeof(unsigned long long), st));
@@ -546,6 +555,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     const int px = (ctx->flags & FGS_FLAG_COUNTERS) ? 0 : ctx->fwd_px.pick(ctx->num_isect, st);
     const int l = fgs::blend_forward(ba, ctx->num_isect, px, st);
     ctx->fwd_px.done(st);
+    ctx->scalars_clean[1 - half] = true;  // K3 zeroes the other half
     if (timing) cudaEventRecord(ev[4], st);
     return l;
   };

@@ -74,6 +74,7 @@ struct BlendArgs {
   unsigned long long* tile_cycles;  // optional (with counters): per-tile CTA cycles
   const uint32_t* tile_order;    // optional: CTA -> tile (heaviest lists first)
   const uint32_t* scalars;       // forward: device scalars; exit if I > isect_cap (speculative launch)
+  uint32_t* zero_next;           // forward: 16 scalars of the next frame, zeroed by CTA 0
   int64_t isect_cap;
   // backward
   const float* dl_dimage;

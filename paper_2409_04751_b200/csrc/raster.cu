@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   __shared__ uint32_t sk[NW][32];    // list index of each staged record
   float4 (*s0)[32] = s01[0];
   float4 (*s1)[32] = s01[1];
+  if (a.zero_next && blockIdx.x == 0 && threadIdx.x < 16) a.zero_next[threadIdx.x] = 0u;
   if (a.scalars && a.scalars[kScalarI] > a.isect_cap) return;  // speculative launch, buffers too small
   const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
