@@ -25,7 +25,9 @@ namespace fgs {
 
 namespace {
 
-constexpr int kGroup = 4;         // forward: splats whose alphas are computed together
+// forward: splats whose alphas are computed together (measured: 4 for 1 pixel per lane, 3 for 2)
+template <int PX>
+constexpr int kGroup = PX == 1 ? 4 : 3;
 
 // Record of sorted entry k, through the sorted Gaussian index.
 __device__ __forceinline__ SortedRec load_rec(const BlendArgs& a, uint32_t k) {
@@ -85,7 +87,7 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr
 // b*dx are computed once). Warps walk the tile's sorted list independently in 32-splat chunks
 // (no CTA barriers): each lane reads one record (the list is contiguous in sorted order, two
 // chunks stay in flight), tests it against the warp's block (rec_hits on the extent K1 stored), and the warp blends
-// the ballot of survivors in order from warp-private shared memory, kGroup splats at a time
+// the ballot of survivors in order from warp-private shared memory, kGroup<PX> splats at a time
 // (alphas first, independent of transmittance; then the sequential transmittance updates).
 // A warp stops when all its pixels have met the reference's termination rule.
 template <bool COUNTERS, int PX>
@@ -178,11 +180,12 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     }
     __syncwarp();
     if (base + 32 < hi) prefetch(base + 32);
-    for (int j0 = 0; j0 < nsurv; j0 += kGroup) {
-      float al[kGroup][PX], pw[kGroup][PX], am[kGroup], cr[kGroup], cg_[kGroup], cb[kGroup];
+    constexpr int G = kGroup<PX>;
+    for (int j0 = 0; j0 < nsurv; j0 += G) {
+      float al[G][PX], pw[G][PX], am[G], cr[G], cg_[G], cb[G];
       bool any_near = false;
 #pragma unroll
-      for (int q = 0; q < kGroup; ++q) {
+      for (int q = 0; q < G; ++q) {
         const int jj = j0 + q < nsurv ? j0 + q : j0;
         const float4 r0 = s0[warp][jj];
         const float4 r1 = s1[warp][jj];
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
       }
       if (__any_sync(0xffffffffu, any_near)) {  // rare: exact exp near the skip threshold
 #pragma unroll
-        for (int q = 0; q < kGroup; ++q)
+        for (int q = 0; q < G; ++q)
 #pragma unroll
           for (int u = 0; u < PX; ++u) {
             bool nr;
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
           }
       }
 #pragma unroll
-      for (int q = 0; q < kGroup; ++q) {
+      for (int q = 0; q < G; ++q) {
         if (j0 + q >= nsurv) break;
         const uint32_t k = sk[warp][j0 + q];
 #pragma unroll
