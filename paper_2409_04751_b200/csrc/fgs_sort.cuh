@@ -197,6 +197,7 @@ __device__ void cta_halfclean(uint64_t* s) {
 // ballots), one CTA scan over (digit, warp), then the scatter. 4 passes x 3 barriers
 // replace the bitonic network's O(log^2 L) stages.
 constexpr int kRadixCap = 2048;
+constexpr int kRadixMin = 512;  // shorter lists: the bitonic network is faster (measured)
 
 // Lanes holding the same 8-bit digit as this lane (among the lanes with `ok`): eight ballots.
 __device__ __forceinline__ unsigned digit_peers(uint32_t d, bool ok) {
@@ -327,7 +328,7 @@ __device__ __forceinline__ int pow2_ceil(int x) {
 // word offset in s at which the ids are also left in shared memory (g of entry k at
 // ((uint32_t*)s)[offset + k]: 0 for lists of <= 256, 2 kRadixCap for the radix range), or -1
 // (read sorted_gauss).
-// hist (NT/32 x 256 counters): enables the radix path for 256 < L <= kRadixCap.
+// hist (NT/32 x 256 counters): enables the radix path for kRadixMin < L <= kRadixCap.
 template <int NT>
 __device__ int sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t lo, int L, uint64_t* s,
                               uint32_t (*hist)[256] = nullptr) {
@@ -364,7 +365,7 @@ __device__ int sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t l
     __syncthreads();
     return 0;
   }
-  if (L <= kRadixCap && hist) {
+  if (L <= kRadixCap && L > kRadixMin && hist) {
     for (int k = tid; k < L; k += NT) {
       const uint64_t v = g[k];
       s32[k] = static_cast<uint32_t>(v >> 32);

@@ -239,7 +239,7 @@ def test_backward_unaligned_gradient_fields(rast, oracle_mod):
 
 
 @pytest.mark.parametrize("n_distinct,min_len,max_len", [(6000, 2 * 4096, None), (1500, 2049, 4096),
-                                                        (500, 257, 2048)])
+                                                        (500, 513, 2048)])
 def test_dense_tile_long_lists_and_depth_ties(rast, oracle_mod, n_distinct, min_len, max_len):
     """Per-tile lists in each sort regime -- beyond the 4096-entry shared-memory sort (chunked
     global/shared bitonic path), the shared-memory bitonic range and the radix range -- with
