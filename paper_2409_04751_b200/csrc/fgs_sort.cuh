@@ -385,9 +385,16 @@ __device__ int sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t l
   if (P <= kSortCap) {
     for (int k = tid; k < P; k += NT) s[k] = k < L ? g[k] : ~0ull;
     cta_sort<NT>(s, P);
-    for (int k = tid; k < L; k += NT) sorted_gauss[lo + k] = static_cast<uint32_t>(s[k]);
+    // lists up to 2048 keys: the ids also go to the upper half of the buffer (free: the keys
+    // used s[0, P) = words [0, 2P)), as for the radix range
+    const bool keep = P <= kRadixCap;
+    for (int k = tid; k < L; k += NT) {
+      const uint32_t gi = static_cast<uint32_t>(s[k]);
+      sorted_gauss[lo + k] = gi;
+      if (keep) s32[2 * kRadixCap + k] = gi;
+    }
     __syncthreads();
-    return -1;
+    return keep ? 2 * kRadixCap : -1;
   }
   constexpr int C = kSortCap;
   for (int c0 = 0; c0 < L; c0 += C) {
