@@ -223,23 +223,37 @@ __device__ void row_offsets(const BinArgs& a, int ty, const uint32_t* rowtot, co
   }
 }
 
-// Largest r in [0, m) with offs[r] <= v (offs ascending, offs[0] = 0): repeated
+// Largest r in [0, m) with offs[r] <= v (offs ascending, offs[0] = 0), for two values: repeated
 // blockDim-ary search by the whole CTA.
-__device__ int cta_upper_rank(const uint32_t* offs, int m, uint32_t v, uint32_t* s_res) {
+__device__ void cta_upper_rank2(const uint32_t* offs, int m, uint32_t v0, uint32_t v1, uint32_t* s_res, int& r0,
+                                int& r1) {
+  // the two searches share their rounds (and barriers)
   const int tid = threadIdx.x, nt = blockDim.x;
-  int base = 0, range = m;
+  int base[2] = {0, 0}, range[2] = {m, m};
+  const uint32_t v[2] = {v0, v1};
   while (true) {
-    const int step = (range + nt - 1) / nt;
-    if (tid == 0) *s_res = static_cast<uint32_t>(base);
+    int step[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) step[q] = (range[q] + nt - 1) / nt;
+    if (tid < 2) s_res[tid] = static_cast<uint32_t>(base[tid]);
     __syncthreads();
-    const int r = base + tid * step;
-    if (tid * step < range && offs[r] <= v) atomicMax(s_res, static_cast<uint32_t>(r));
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int r = base[q] + tid * step[q];
+      if (tid * step[q] < range[q] && offs[r] <= v[q]) atomicMax(s_res + q, static_cast<uint32_t>(r));
+    }
     __syncthreads();
-    const int nb = static_cast<int>(*s_res);
+    const int nb0 = static_cast<int>(s_res[0]), nb1 = static_cast<int>(s_res[1]);
     __syncthreads();
-    if (step == 1) return nb;
-    base = nb;
-    range = min(step, m - nb);
+    if (step[0] <= 1 && step[1] <= 1) {
+      r0 = nb0;
+      r1 = nb1;
+      return;
+    }
+    base[0] = nb0;
+    base[1] = nb1;
+    range[0] = step[0] <= 1 ? 1 : min(step[0], m - nb0);
+    range[1] = step[1] <= 1 ? 1 : min(step[1], m - nb1);
   }
 }
 
@@ -256,8 +270,8 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
   const int tid = threadIdx.x;
   if (PRIV)
     for (int t = tid; t < a.num_tiles; t += kT) s_cnt[t] = 0;
-  const int r_lo = cta_upper_rank(a.coff, m, lo, s_res);
-  const int r_hi = cta_upper_rank(a.coff, m, hi - 1, s_res);
+  int r_lo, r_hi;
+  cta_upper_rank2(a.coff, m, lo, hi - 1, s_res, r_lo, r_hi);
   const int nr = r_hi - r_lo + 1;  // <= kSub: every Gaussian here owns >= 1 slot
   for (int i = tid; i < nr; i += kT) s_off[i] = a.coff[r_lo + i];
   __syncthreads();
@@ -338,7 +352,7 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
   extern __shared__ uint32_t s_cnt[];  // [num_tiles] (PRIV)
   __shared__ ScanSmem sm;
   __shared__ uint32_t s_off[kSub];
-  __shared__ uint32_t s_res;
+  __shared__ uint32_t s_res[2];
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x;
   const int G = static_cast<int>(gridDim.x);
@@ -432,7 +446,7 @@ scatter:
   const int m = static_cast<int>(a.scalars[kScalarM]);
   const uint32_t s_lo = static_cast<uint32_t>(static_cast<uint64_t>(I) * b / gridDim.x);
   const uint32_t s_hi = static_cast<uint32_t>(static_cast<uint64_t>(I) * (b + 1) / gridDim.x);
-  for (uint32_t x = s_lo; x < s_hi; x += kSub) scatter_range<PRIV>(a, m, x, min(s_hi, x + kSub), s_cnt, s_off, &s_res);
+  for (uint32_t x = s_lo; x < s_hi; x += kSub) scatter_range<PRIV>(a, m, x, min(s_hi, x + kSub), s_cnt, s_off, s_res);
   trace(a.trace, 0, 7);
 }
 
