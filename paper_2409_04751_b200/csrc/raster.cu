@@ -437,7 +437,8 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
         const float b2 = s2[warp][jj];
         const float dx = dxs[q];
 #pragma unroll
-        for (int c9 = 0; c9 < 9; ++c9) v[9 * q + c9] = 0.0f;
+        for (int c9 = 5; c9 < 9; ++c9) v[9 * q + c9] = 0.0f;
+        float p0 = 0.0f, p1 = 0.0f, p2 = 0.0f;
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
           const float alpha = fminf(kAlphaClamp, ar[q][u]);
@@ -460,13 +461,18 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
           sf[u][2] = fmaf(b2, w, sf[u][2]);
           T[u] = c ? Tb : T[u];
           v[9 * q + 8] += d_alpha * ex[q][u];
+          // the mean / conic terms through the lane's moments of dpower (its pixels share dx)
           const float dp = d_alpha * alpha;
-          v[9 * q + 0] += dp * (r0.z * dx + r0.w * dy);
-          v[9 * q + 1] += dp * (r0.w * dx + r1.x * dy);
-          v[9 * q + 2] += dp * (-0.5f * dx * dx);
-          v[9 * q + 3] += dp * (-dx * dy);
-          v[9 * q + 4] += dp * (-0.5f * dy * dy);
+          p0 += dp;
+          p1 = fmaf(dp, dy, p1);
+          p2 = fmaf(dp * dy, dy, p2);
         }
+        // sum_u dp (a dx + b dy), sum_u dp (b dx + c dy), -1/2 sum dp dx^2, -sum dp dx dy, -1/2 sum dp dy^2
+        v[9 * q + 0] = fmaf(r0.z * dx, p0, r0.w * p1);
+        v[9 * q + 1] = fmaf(r0.w * dx, p0, r1.x * p1);
+        v[9 * q + 2] = (-0.5f * dx * dx) * p0;
+        v[9 * q + 3] = -dx * p1;
+        v[9 * q + 4] = -0.5f * p2;
       }
 #pragma unroll
       for (int q = 27; q < 32; ++q) v[q] = 0.0f;
