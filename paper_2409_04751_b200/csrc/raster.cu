@@ -311,7 +311,9 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   for (uint32_t j = threadIdx.x; j < min(hi - lo, kPassCap) / 4 + 1; j += blockDim.x) s_pass[j] = 0u;
   __syncthreads();
   const float fx = static_cast<float>(px) + 0.5f;
-  float T[PX], dl[PX][3], sf[PX][3], fy[PX];
+  // ds: dL/dpixel . (suffix colour), the suffix colour T_final * bg + sum_{j later} c_j w_j
+  // (gradients.hpp:132, :143) kept only through its dot product with dL/dpixel
+  float T[PX], dl[PX][3], ds[PX], fy[PX];
   uint32_t last[PX];
   uint32_t mylast = lo;
 #pragma unroll
@@ -329,9 +331,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
       dl[u][1] = a.dl_dimage[pix * 3 + 1];
       dl[u][2] = a.dl_dimage[pix * 3 + 2];
     }
-    sf[u][0] = T[u] * a.bg[0];
-    sf[u][1] = T[u] * a.bg[1];
-    sf[u][2] = T[u] * a.bg[2];
+    ds[u] = dl[u][0] * (T[u] * a.bg[0]) + dl[u][1] * (T[u] * a.bg[1]) + dl[u][2] * (T[u] * a.bg[2]);
     mylast = max(mylast, last[u]);
   }
   const uint32_t wlast = __reduce_max_sync(0xffffffffu, mylast);
@@ -453,12 +453,9 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
           v[9 * q + 6] += dl[u][1] * w;
           v[9 * q + 7] += dl[u][2] * w;
           const float dot_c = dl[u][0] * r1.z + dl[u][1] * r1.w + dl[u][2] * b2;
-          const float dot_s = dl[u][0] * sf[u][0] + dl[u][1] * sf[u][1] + dl[u][2] * sf[u][2];
           // clamped contributions carry no geometric gradient
-          const float d_alpha = (c && !(ar[q][u] > kAlphaClamp)) ? dot_c * Tb - dot_s * inv : 0.0f;
-          sf[u][0] = fmaf(r1.z, w, sf[u][0]);
-          sf[u][1] = fmaf(r1.w, w, sf[u][1]);
-          sf[u][2] = fmaf(b2, w, sf[u][2]);
+          const float d_alpha = (c && !(ar[q][u] > kAlphaClamp)) ? dot_c * Tb - ds[u] * inv : 0.0f;
+          ds[u] = fmaf(dot_c, w, ds[u]);
           T[u] = c ? Tb : T[u];
           v[9 * q + 8] += d_alpha * ex[q][u];
           // the mean / conic terms through the lane's moments of dpower (its pixels share dx)
