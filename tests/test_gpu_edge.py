@@ -81,10 +81,12 @@ def test_backward_rejects_mismatched_context(rast):  # test_gradients.cpp:287-29
         rast.backward(to_device(sc), cam, torch.zeros((2, 2, 3), device="cuda"))
 
 
-@pytest.mark.parametrize("wh", [(256, 256), (100, 37), (17, 16), (1752, 1168)])
+@pytest.mark.parametrize("wh", [(256, 256), (100, 37), (17, 16), (1752, 1168), (2600, 2100)])
 def test_ragged_sizes_and_tile_edges(rast, oracle_mod, wh):
     """W, H multiples of 16 exercise the zero-tile splat (mx - r == W passes the cull,
     splatting.hpp:107-108 / 211-214); odd sizes exercise partial edge tiles."""
+    # (2600 x 2100: 163 x 132 = 21516 tiles, past the binning scatter's 16384-tile shared
+    # counters, takes the global-atomic scatter)
     w, h = wh
     sc = spherical_scene(3000, 5)
     cam = small_fisheye(w, h)
@@ -92,6 +94,7 @@ def test_ragged_sizes_and_tile_edges(rast, oracle_mod, wh):
     res = oracle_mod.render(sc, cam, sh_degree=3)
     assert st.num_intersections == res.num_intersections and st.num_splats == res.num_splats
     np.testing.assert_array_equal(rast.debug("offsets"), res.get("offsets"))
+    np.testing.assert_array_equal(rast.debug("sorted_gauss"), res.get("source")[res.get("refs")])
     assert np.abs(img.astype(np.float64) - res.image).max() <= 1e-3
 
 
