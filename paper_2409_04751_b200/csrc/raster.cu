@@ -1,8 +1,9 @@
 // raster.cu — K3 forward tile blend and K4a reverse blend backward, sm_100a.
 //
-// One CTA of 256 threads per 16x16 tile, one pixel per thread. Splat records of a tile's
-// sorted list are staged in shared memory in batches; a pixel stops at the reference's
-// termination rule and the CTA exits when every pixel has stopped (__syncthreads_count).
+// One CTA per 16x16 tile; it first sorts the tile's list (fgs_sort.cuh), then each warp walks
+// the sorted list independently for its pixel block, the next chunk's records arriving in
+// shared memory by cp.async; a pixel stops at the reference's termination rule and a warp when
+// all its pixels have stopped.
 //
 // Exactness: the decision chain (dx, dy, power, alpha thresholds, transmittance stop) is
 // evaluated FMA-free in the reference's op order (inc/splatting.hpp:284-292); the exp uses
@@ -12,9 +13,10 @@
 //
 // Backward (inc/gradients.hpp:69-175): the reverse walk recovers T_before = T_after/(1-alpha)
 // from the forward's final transmittance and last-contributor index, accumulates the suffix
-// colour, and produces per-(pixel, splat) gradients (mean_px 2, conic 3, colour 3, alpha 1).
-// They are summed over the tile's pixels in a fixed order (warp shuffle tree, then warps in
-// order) and written to the intersection's sorted position: no atomics, deterministic.
+// colour (as its dot product with dL/dpixel), and produces per-(pixel, splat) gradients
+// (mean_px 2, conic 3, colour 3, alpha 1). They are summed over the tile's pixels in a fixed
+// order (warp shuffle tree, then warp blocks in order) and written to the intersection's
+// emission slot: no atomics, deterministic.
 
 #include <algorithm>
 #include <cstdlib>
@@ -85,10 +87,11 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr
 // is given). PX = pixels per lane: warp w owns an 8 x (4*PX) block at (8*(w&1), 4*PX*(w>>1));
 // lane l the pixel(s) (l&7, (l>>3) + 4*q), q < PX, which share a column (so (a*dx)*dx and
 // b*dx are computed once). Warps walk the tile's sorted list independently in 32-splat chunks
-// (no CTA barriers): each lane reads one record (the list is contiguous in sorted order, two
-// chunks stay in flight), tests it against the warp's block (rec_hits on the extent K1 stored), and the warp blends
-// the ballot of survivors in order from warp-private shared memory, kGroup<PX> splats at a time
-// (alphas first, independent of transmittance; then the sequential transmittance updates).
+// (no CTA barriers): each lane takes one record of the chunk (fetched by cp.async one chunk
+// ahead), tests it against the warp's block (rec_hits on the extent K1 stored), the survivors
+// are compacted in list order into warp-private staging slots, and the warp blends them
+// kGroup<PX> splats at a time (alphas first, independent of transmittance; then the sequential
+// transmittance updates).
 // A warp stops when all its pixels have met the reference's termination rule.
 template <bool COUNTERS, int PX>
 __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
