@@ -103,7 +103,9 @@ typedef struct fgs_context fgs_context;
 
 int fgs_create(int device, fgs_context** out);
 int fgs_destroy(fgs_context* ctx);
-/* Stream for all subsequent work (cudaStream_t; NULL = legacy default stream). */
+/* Stream for all subsequent work (cudaStream_t; NULL = legacy default stream). Switching
+   streams first waits for the work queued on the previous one (the context's buffers are
+   reused by the next call). */
 int fgs_set_stream(fgs_context* ctx, void* stream);
 const char* fgs_last_error(const fgs_context* ctx);
 

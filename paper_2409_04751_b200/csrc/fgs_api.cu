@@ -352,7 +352,14 @@ int fgs_destroy(fgs_context* ctx) {
 
 int fgs_set_stream(fgs_context* ctx, void* stream) {
   if (!ctx) return FGS_EINVAL;
-  ctx->stream = static_cast<cudaStream_t>(stream);
+  const cudaStream_t next = static_cast<cudaStream_t>(stream);
+  if (next != ctx->stream) {
+    // the context's buffers (records, keys, scalars, ...) are reused by the next call: work
+    // still queued on the old stream must finish before the new stream may touch them
+    FGS_CHECK(cudaSetDevice(ctx->device));
+    FGS_CHECK(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = next;
+  }
   return FGS_OK;
 }
 
