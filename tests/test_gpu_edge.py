@@ -63,6 +63,37 @@ def test_degenerate_quaternion_raises(rast):  # model.hpp:98
         fwd(rast, sc, cam)
 
 
+def test_context_recovers_after_errors_and_empty_frames(oracle_mod):
+    """A context's per-frame device state (the double-buffered scalars, the speculative launch
+    against last frame's capacity, the launch-variant timing) survives a failed frame and an
+    empty scene: every later frame matches the oracle."""
+    import torch
+    from paper_2409_04751_b200 import InvalidArgument, Rasterizer, RenderOptions, Scene
+
+    r = Rasterizer(0)
+    good = spherical_scene(2500, 7)
+    bad = spherical_scene(2500, 7)
+    bad.rotations[3] = 0
+    empty = Scene(good.means[:0], good.rotations[:0], good.log_scales[:0], good.opacity_logits[:0], good.sh[:0],
+                  good.background)
+    cam = small_fisheye(320, 240)
+    ref = oracle_mod.render(good, cam, sh_degree=3)
+    for sc in (good, bad, good, empty, good, bad, bad, good, good):
+        if sc is bad:
+            with pytest.raises(InvalidArgument):
+                r.forward(to_device(sc), cam, RenderOptions(sh_degree=3, background=sc.background))
+            continue
+        img, st = r.forward(to_device(sc), cam, RenderOptions(sh_degree=3, background=sc.background),
+                            want_stats=True)
+        torch.cuda.synchronize()
+        if sc is empty:
+            assert st.num_intersections == 0
+            continue
+        assert st.num_intersections == ref.num_intersections
+        np.testing.assert_array_equal(r.debug("offsets"), ref.get("offsets"))
+        assert np.abs(img.cpu().numpy().astype(np.float64) - ref.image).max() <= 1e-3
+
+
 def test_backward_rejects_mismatched_context(rast):  # test_gradients.cpp:287-299
     import torch
     from paper_2409_04751_b200 import InvalidArgument
