@@ -52,7 +52,7 @@ struct DevBuf {  // owning device allocation that only grows (freed on destructi
 }  // namespace
 
 // Autotuning between two launch variants with identical results (forward: pixels per lane;
-// backward: register / occupancy variant): the first frames of a context time both work
+// backward blend and K4b: register / occupancy variants): the first frames of a context time both work
 // decompositions (CUDA events around the launch, read back without blocking on a later frame,
 // normalised by the frame's intersection count since views differ in cost) and keep the
 // faster; a >2x change in the intersection count starts over. Results do not depend
@@ -159,6 +159,7 @@ struct fgs_context {
   int64_t frame = 0;
   bool scalars_clean[2] = {true, true};
   PxTuner bwd_var;  // backward blend occupancy variant (same results)
+  PxTuner k4b_var;  // K4b register-fit variant (same results)
   DevBuf<float> final_T;
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
@@ -299,6 +300,7 @@ int fgs_create(int device, fgs_context** out) {
   cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   ctx->fwd_px.create();
   ctx->bwd_var.create();
+  ctx->k4b_var.create();
   if (ctx->scalars.ensure(32) != cudaSuccess || cudaMemset(ctx->scalars.p, 0, 32 * sizeof(uint32_t)) != cudaSuccess || ctx->counters.ensure(24) != cudaSuccess ||
       false) {
     fgs_destroy(ctx);
@@ -338,6 +340,7 @@ int fgs_destroy(fgs_context* ctx) {
   if (ctx->ev_k2) cudaEventDestroy(ctx->ev_k2);
   ctx->fwd_px.destroy();
   ctx->bwd_var.destroy();
+  ctx->k4b_var.destroy();
   if (ctx->aux) {
     cudaStreamSynchronize(ctx->aux);
     cudaStreamDestroy(ctx->aux);
@@ -703,7 +706,9 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.cval = ctx->cval.p;
   pb.rec = ctx->rec.p;
   if (n > 0 && (pb.m > 0 || !pb.accumulate)) {
-    fgs::preprocess_backward_launch(pb, ctx->scene_on_host, st);
+    const int var = ctx->scene_on_host ? 0 : ctx->k4b_var.pick(ctx->num_isect, st);
+    fgs::preprocess_backward_launch(pb, ctx->scene_on_host, var, st);
+    if (!ctx->scene_on_host) ctx->k4b_var.done(st);
     ++ctx->launches;
   }
   if (timing) cudaEventRecord(ev[2], st);

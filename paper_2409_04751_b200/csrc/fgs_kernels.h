@@ -85,7 +85,7 @@ struct BlendArgs {
 // K1 / K4b launches (preprocess.cu); host_scene: the scene arrays are pinned host memory read in
 // place over PCIe (separate instantiations, so profiles tell the two apart).
 void preprocess_launch(const PreprocessArgs& a, bool host_scene, cudaStream_t st);
-void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene, cudaStream_t st);
+void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene, int variant, cudaStream_t st);
 constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per K4b CTA
 
 // ---- binning / sorting (binning.cu) ----

@@ -796,8 +796,11 @@ __device__ __forceinline__ void sh_rows_store(const PreprocessBackwardArgs& a, c
     }
   }
 }
-template <bool HOST_SCENE>
-__global__ void __launch_bounds__(kBwdThreads, 6) preprocess_backward_kernel(PreprocessBackwardArgs a) {
+// MINB: the register fit (6 CTAs per SM: 80 registers with a few spills; 4: 85, none) -- same
+// code and results, scene-dependent speed (config 2 0.107 vs 0.099 ms, config 4 0.289 vs
+// 0.305): the caller times both per context.
+template <bool HOST_SCENE, int MINB>
+__global__ void __launch_bounds__(kBwdThreads, MINB) preprocess_backward_kernel(PreprocessBackwardArgs a) {
   __shared__ uint8_t vis[kBwdThreads];
   __shared__ __align__(16) float s_shstage[kBwdThreads * 20];  // per-lane SH gradient factors
   const int tid = threadIdx.x, lane = tid & 31;
@@ -882,10 +885,11 @@ void preprocess_launch(const PreprocessArgs& a, bool host_scene, cudaStream_t st
   }
 }
 
-void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene, cudaStream_t st) {
+void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene, int variant, cudaStream_t st) {
   const int blocks = a.m > 0 ? div_up(static_cast<int>(a.m), kBwdThreads) : 1;
-  if (host_scene) preprocess_backward_kernel<true><<<blocks, kBwdThreads, 0, st>>>(a);
-  else preprocess_backward_kernel<false><<<blocks, kBwdThreads, 0, st>>>(a);
+  if (host_scene) preprocess_backward_kernel<true, 6><<<blocks, kBwdThreads, 0, st>>>(a);
+  else if (variant == 2) preprocess_backward_kernel<false, 4><<<blocks, kBwdThreads, 0, st>>>(a);
+  else preprocess_backward_kernel<false, 6><<<blocks, kBwdThreads, 0, st>>>(a);
 }
 
 }  // namespace fgs
