@@ -48,7 +48,7 @@ if __name__ == "__main__" and len(sys.argv) > 1:
     res, _ = summarise(sys.argv[1])
     for title, names in (("forward step (device-resident)", ["void preprocess_kernel<0>", "void bin_kernel",
                                                             "void blend_forward_kernel<0"]),
-                         ("backward step", ["void blend_backward_kernel", "void preprocess_backward_kernel<0>"])):
+                         ("backward step", ["void blend_backward_kernel", "void preprocess_backward_kernel<0"])):
         sh, tot = step_share(res, names)
         print(f"{title}: {tot:.1f} us = " + ", ".join(f"{k.replace('void ', '')} {v:.1f} us ({p:.0f}%)"
                                                         for k, (v, p) in sh.items()))
