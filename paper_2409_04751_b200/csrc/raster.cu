@@ -340,17 +340,19 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   const uint32_t wlast = __reduce_max_sync(0xffffffffu, mylast);
   float* part = a.partials;
 
-  // passing splats past the warp's last contributor: zero slots
-  for (uint32_t base = wlast; base < hi; base += 32) {
-    const uint32_t k = base + lane;
-    if (k < hi) {
-      const SortedRec r = load_rec(a, k);
-      if (rec_hits(r.a, r.c, bx0, bx1, by0, by1) &&
-          (!a.ellipse || rec_hits_ellipse(r.a, r.b, r.c, bx0, bx1, by0, by1))) {
-        if (k - lo < kPassCap) atomicOr(s_pass + ((k - lo) >> 2), 1u << (8 * ((k - lo) & 3) + warp));
-        float* p = part + (static_cast<size_t>(k) * NW + warp) * 9;
+  // Splats past the warp's last contributor add nothing: with pass bits (lists up to kPassCap)
+  // their bits simply stay clear; longer lists, whose epilogue re-tests the blocks, get zero slots
+  if (hi - lo > kPassCap) {
+    for (uint32_t base = wlast; base < hi; base += 32) {
+      const uint32_t k = base + lane;
+      if (k < hi) {
+        const SortedRec r = load_rec(a, k);
+        if (rec_hits(r.a, r.c, bx0, bx1, by0, by1) &&
+            (!a.ellipse || rec_hits_ellipse(r.a, r.b, r.c, bx0, bx1, by0, by1))) {
+          float* p = part + (static_cast<size_t>(k) * NW + warp) * 9;
 #pragma unroll
-        for (int q = 0; q < 9; ++q) p[q] = 0.0f;
+          for (int q = 0; q < 9; ++q) p[q] = 0.0f;
+        }
       }
     }
   }
