@@ -151,9 +151,13 @@ int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s);
  *   conic, alpha_max, colour, extent), "depth_key" u32[N], "radius" int32[N], "touched" u32[N],
  *   "key_tile"/"key_depth"/"key_gauss" u32[I] (pre-sort keys in the reference's emission order),
  *   "sorted_gauss" u32[I], "sorted_tile" u32[I], "offsets" u32[T+1] (tile ranges),
+ *   "keys" u64[I] (depth key << 32 | Gaussian id, as the binning scatter wrote them into each tile's
+ *   range), "rect" u16[N*4] (tile rectangle tx0, tx1, ty0, ty1 per Gaussian),
  *   "compact_gauss"/"compact_offsets" u32[M], "final_T" f32[H*W], "last" u32[H*W],
  *   "counters" u64[4] (E_eval, E_contrib, culled evaluations, max CTA cycles; with
- *   FGS_FLAG_COUNTERS), "counters16" u64[16], "bin_trace" u64[8], "tile_cycles" u64[T].
+ *   FGS_FLAG_COUNTERS), "counters16" u64[16], "bin_trace" u64[8], "tile_cycles" u64[T],
+ *   "tile_span" / "tile_span_bwd" u64[2T] (per tile CTA start / end %globaltimer ns of the last forward
+ *   / backward blend; with FGS_FLAG_COUNTERS).
  * Returns the number of bytes (dst may be NULL to query), or -1 for an unknown name. */
 int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst_bytes);
 

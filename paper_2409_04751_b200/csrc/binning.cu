@@ -125,7 +125,7 @@ __device__ void row_counts(const BinArgs& a, int ty, uint32_t* hist, uint32_t* r
   const int lane = threadIdx.x & 31, rw = a.tiles_x + 1;
   const uint32_t lt = lanemask_lt();
   int32_t* rd = a.rowdiff + static_cast<size_t>(ty) * rw;
-  uint32_t carry = 0, tot = 0;
+  uint32_t carry = 0, tot = 0, segs = 0;
   for (int c0 = 0; c0 < rw; c0 += 32 * kRowItems) {
     int32_t v[kRowItems];
     int32_t sum = 0;
@@ -151,6 +151,7 @@ __device__ void row_counts(const BinArgs& a, int ty, uint32_t* hist, uint32_t* r
       if (cell) {
         a.fill[static_cast<size_t>(ty) * a.tiles_x + x] = run;
         tot += run;
+        if (run > kSeg) segs += (run + kSeg - 1) / kSeg;  // the backward's segments of a long list
       }
       const int bk = cell ? sched_bucket(run) : 31;
       const uint32_t peers = __match_any_sync(0xffffffffu, bk);
@@ -159,8 +160,14 @@ __device__ void row_counts(const BinArgs& a, int ty, uint32_t* hist, uint32_t* r
     carry += __shfl_sync(0xffffffffu, incl, 31);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-  if (lane == 0) rowtot[ty] = tot;
+  for (int o = 16; o > 0; o >>= 1) {
+    tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    segs += __shfl_xor_sync(0xffffffffu, segs, o);
+  }
+  if (lane == 0) {
+    rowtot[ty] = tot;
+    if (segs) atomicAdd(a.scalars + kScalarSegs, segs);
+  }
 }
 
 // Phase 2: tile offsets and scatter cursors of row ty (row prefix + in-row exclusive scan),

@@ -139,7 +139,12 @@ struct fgs_context {
   // per intersection
   DevBuf<uint64_t> keys;
   DevBuf<uint32_t> sorted_gauss;
-  DevBuf<float> partials, partial_tile;
+  DevBuf<uint32_t> sorted_slot;  // backward: emission slot per sorted entry
+  DevBuf<float> ckpt;             // backward segments: forward checkpoints [slot][4][256]
+  DevBuf<uint32_t> seg_items, tile_ckpt;
+  int64_t ckpt_cap = 0;           // slots of ckpt / seg_items
+  int64_t num_segs = 0;           // slots of the last forward
+  DevBuf<float> partial_tile;     // backward: 9 screen-space gradient sums per intersection
   // training step
   DevBuf<float> t_image, t_dimage, t_grads, t_maps;
   DevBuf<double> t_part;
@@ -164,7 +169,7 @@ struct fgs_context {
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
   DevBuf<uint32_t> scalars;
-  DevBuf<unsigned long long> counters, tile_cycles;
+  DevBuf<unsigned long long> counters, tile_cycles, tile_span, tile_span_bwd;
   uint32_t* h_scalars = nullptr;  // pinned
   // host-call staging
   DevBuf<float> h_means, h_rot, h_ls, h_op, h_sh, h_img, h_dl, h_grad;
@@ -249,6 +254,42 @@ fgs_context::EventSet* take_set(fgs_context* ctx, int kind) {
   return &ctx->pending.back();
 }
 
+// Device bytes the render/backward path holds (RenderStats::peak_aux_bytes): per-Gaussian and
+// per-intersection state, tile and pixel arrays, and the backward's scratch once allocated.
+template <typename T>
+size_t cap_bytes(const DevBuf<T>& b) { return b.p ? b.cap * sizeof(T) : 0; }
+size_t path_bytes(const fgs_context* c) {
+  return cap_bytes(c->rec) + cap_bytes(c->state) + cap_bytes(c->dkey) + cap_bytes(c->cval) + cap_bytes(c->coff) +
+         cap_bytes(c->src_off) + cap_bytes(c->touched) + cap_bytes(c->scan_status) + cap_bytes(c->rect) +
+         cap_bytes(c->radii) + cap_bytes(c->keys) + cap_bytes(c->sorted_gauss) + cap_bytes(c->sorted_slot) + cap_bytes(c->ckpt) + cap_bytes(c->seg_items) + cap_bytes(c->tile_ckpt) +
+         cap_bytes(c->partial_tile) + cap_bytes(c->tile_offsets) + cap_bytes(c->fill) + cap_bytes(c->last) +
+         cap_bytes(c->tile_order) + cap_bytes(c->rowdiff) + cap_bytes(c->final_T);
+}
+
+// Checkpoint slots for X backward segments (grows only).
+cudaError_t ensure_ckpt(fgs_context* c, int64_t X) {
+  if (X <= c->ckpt_cap && c->ckpt.p) return cudaSuccess;
+  const size_t slots = static_cast<size_t>(std::max<int64_t>(X, 1));
+  cudaError_t e = c->ckpt.ensure(slots * 4 * fgs::kTile * fgs::kTile);
+  if (e == cudaSuccess) e = c->seg_items.ensure(slots);
+  if (e != cudaSuccess) return e;
+  c->ckpt_cap = static_cast<int64_t>(std::min(c->ckpt.cap / (4 * fgs::kTile * fgs::kTile), c->seg_items.cap));
+  return cudaSuccess;
+}
+
+// An event set taken by a call that then fails returns to the spare pool unread (its later events
+// were never recorded): error paths leave no pending interval behind.
+struct SetGuard {
+  fgs_context* ctx;
+  bool armed;
+  ~SetGuard() {
+    if (armed && !ctx->pending.empty()) {
+      ctx->spare.push_back(ctx->pending.back());
+      ctx->pending.pop_back();
+    }
+  }
+};
+
 void drain_sets(fgs_context* ctx, size_t keep) {
   while (ctx->pending.size() > keep) {
     fgs_context::EventSet es = ctx->pending.front();
@@ -258,13 +299,18 @@ void drain_sets(fgs_context* ctx, size_t keep) {
     for (int k = 0; k < nint; ++k) {
       float ms = 0.0f;
       if (es.kind == 0 && k == 2) continue;  // forward: the sort runs inside K3 (no event 3)
-      cudaEventElapsedTime(&ms, es.e[es.kind == 0 && k == 3 ? 2 : k], es.e[k + 1]);
+      if (cudaEventElapsedTime(&ms, es.e[es.kind == 0 && k == 3 ? 2 : k], es.e[k + 1]) != cudaSuccess) {
+        cudaGetLastError();  // an interval of a failed call: not counted, and no sticky error left
+        continue;
+      }
       ctx->acc_ms[(es.kind == 0 ? 0 : 4) + k] += ms;
     }
     ctx->acc_calls[es.kind] += 1;
     ctx->spare.push_back(es);
   }
 }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 bool same_camera(const fgs_camera& a, const fgs_camera& b) {
   // the fields the reference compares (inc/gradients.hpp:213-217)
@@ -315,14 +361,14 @@ int fgs_destroy(fgs_context* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   else cudaDeviceSynchronize();
-  for (auto* b : {&ctx->final_T, &ctx->partials, &ctx->partial_tile, &ctx->t_image, &ctx->t_dimage, &ctx->t_grads,
+  for (auto* b : {&ctx->final_T, &ctx->partial_tile, &ctx->ckpt, &ctx->t_image, &ctx->t_dimage, &ctx->t_grads,
                   &ctx->t_maps, &ctx->h_means, &ctx->h_rot, &ctx->h_ls, &ctx->h_op,
                   &ctx->h_sh, &ctx->h_img, &ctx->h_dl, &ctx->h_grad})
     b->release();
   ctx->rec.release();
   ctx->state.release();
   for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->src_off, &ctx->touched, &ctx->scan_status,
-                  &ctx->sorted_gauss, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
+                  &ctx->sorted_gauss, &ctx->sorted_slot, &ctx->seg_items, &ctx->tile_ckpt, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
                   &ctx->scalars})
     b->release();
   ctx->keys.release();
@@ -334,6 +380,8 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->h_radii.release();
   ctx->counters.release();
   ctx->tile_cycles.release();
+  ctx->tile_span.release();
+  ctx->tile_span_bwd.release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->ev_scan) cudaEventDestroy(ctx->ev_scan);
@@ -435,6 +483,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   FGS_CHECK(ctx->tile_offsets.ensure(num_tiles + 1));
   FGS_CHECK(ctx->fill.ensure(num_tiles));
   FGS_CHECK(ctx->tile_order.ensure(num_tiles));
+  FGS_CHECK(ctx->tile_ckpt.ensure(num_tiles));
   const size_t ndiff = static_cast<size_t>(tiles_x + 1) * tiles_y;
   if (ctx->rowdiff.cap < ndiff || ctx->rowdiff_clean < ndiff) {
     FGS_CHECK(ctx->rowdiff.ensure(ndiff));
@@ -456,6 +505,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   const bool timing = stats != nullptr || (ctx->flags & FGS_FLAG_TIMING);
   if (ctx->pending.size() > 64) drain_sets(ctx, 8);
   cudaEvent_t* ev = timing ? take_set(ctx, 0)->e : ctx->ev;
+  SetGuard guard{ctx, timing};
   if (timing) cudaEventRecord(ev[0], st);
   uint64_t launches = 0;
 
@@ -483,6 +533,9 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.rect = ctx->rect.p;
     pa.radii = ctx->radii.p;
     pa.rowdiff = ctx->rowdiff.p;
+    pa.vec_rot = aligned16(scene->rotations);
+    pa.vec_sh = aligned16(scene->sh);
+    pa.vec_geo = aligned16(scene->means) && aligned16(scene->log_scales);
     pa.error_flag = reinterpret_cast<int*>(scalars + 1);
     pa.state_counts = scalars + 2;
     fgs::preprocess_launch(pa, ctx->scene_on_host, st);
@@ -556,9 +609,17 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     FGS_CHECK(ctx->tile_cycles.ensure(num_tiles));
     FGS_CHECK(cudaMemsetAsync(ctx->tile_cycles.p, 0, num_tiles * sizeof(unsigned long long), st));
     ba.tile_cycles = ctx->tile_cycles.p;
+    FGS_CHECK(ctx->tile_span.ensure(2 * num_tiles));
+    FGS_CHECK(cudaMemsetAsync(ctx->tile_span.p, 0, 2 * num_tiles * sizeof(unsigned long long), st));
+    ba.tile_span = ctx->tile_span.p;
   }
+  ba.seg_cursor = scalars + fgs::kScalarSegPos;
+  ba.tile_ckpt = ctx->tile_ckpt.p;
   auto launch_blend = [&]() -> int {
     ba.isect_cap = ctx->isect_cap;
+    ba.ckpt = ctx->ckpt.p;
+    ba.seg_items = ctx->seg_items.p;
+    ba.ckpt_cap = ctx->ckpt_cap;
     ba.keys = ctx->keys.p;
     ba.sorted_gauss = ctx->sorted_gauss.p;
     // density hint for the work decomposition: this frame's I once known, else the last frame's
@@ -584,7 +645,17 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ctx->num_degenerate = ctx->h_scalars[fgs::kScalarDegen];
   ctx->num_culled = static_cast<uint32_t>(n) - ctx->num_splats - ctx->num_degenerate;
   if (I >= (int64_t(1) << 30)) return fail(ctx, FGS_ENOMEM, "forward: intersection count exceeds 2^30");
-  if (!speculative || I > ctx->isect_cap) {
+  const int64_t X = ctx->h_scalars[fgs::kScalarSegs];
+  ctx->num_segs = X;
+  if (speculative && I <= ctx->isect_cap && X > ctx->ckpt_cap) {
+    // only the checkpoint slots ran short: the speculative K3 exited; grow them and blend again
+    ctx->fwd_px.drop();
+    FGS_CHECK(ensure_ckpt(ctx, X));
+    FGS_CHECK(cudaMemsetAsync(scalars + fgs::kScalarSegPos, 0, sizeof(uint32_t), st));
+    launches += launch_blend();
+  } else if (!speculative || I > ctx->isect_cap) {
+    FGS_CHECK(ensure_ckpt(ctx, X));
+    FGS_CHECK(cudaMemsetAsync(scalars + fgs::kScalarSegPos, 0, sizeof(uint32_t), st));
     ctx->fwd_px.drop();  // the timed launch (if any) exited without work
     // (re)size the per-intersection buffers (cudaFree / cudaMalloc synchronise with the
     // speculative kernels, which exited without work) and launch for real
@@ -609,8 +680,9 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   FGS_CHECK(cudaGetLastError());
   ctx->launches += launches;
 
-  ctx->aux_bytes = nn * (48 + 1 + 4 * 6 + 8) + static_cast<size_t>(std::max<int64_t>(ctx->isect_cap, 1)) * (8 + 4) + (num_tiles + 1) * 4 * 3 + ndiff * 4 + npix * 8;
+  ctx->aux_bytes = path_bytes(ctx);
   ctx->have_fwd = true;
+  guard.armed = false;
   if (stats) {
     FGS_CHECK(cudaEventSynchronize(ev[4]));
     float ms[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -646,8 +718,9 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   cudaStream_t st = ctx->stream;
   const int64_t n = ctx->n, I = ctx->num_isect;
   if (n == 0) return FGS_OK;
-  FGS_CHECK(ctx->partials.ensure(static_cast<size_t>(I > 0 ? I : 1) * fgs::kBwdWarps * 9));
+  FGS_CHECK(ctx->sorted_slot.ensure(static_cast<size_t>(I > 0 ? I : 1)));
   FGS_CHECK(ctx->partial_tile.ensure(static_cast<size_t>(I > 0 ? I : 1) * 9));
+  ctx->aux_bytes = path_bytes(ctx);
 
   fgs::BlendArgs ba{};
   ba.ellipse = blend_ellipse();
@@ -662,15 +735,26 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;
   ba.dl_dimage = dl_dimage;
-  ba.partials = ctx->partials.p;
+  ba.sorted_slot = ctx->sorted_slot.p;
+  ba.ckpt = ctx->ckpt.p;
+  ba.seg_items = ctx->seg_items.p;
+  ba.tile_ckpt = ctx->tile_ckpt.p;
+  ba.num_seg_items = ctx->num_segs;
   ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
   ba.partial_tile = ctx->partial_tile.p;
   ba.src_off = ctx->src_off.p;
   ba.rect = ctx->rect.p;
   ba.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
+  if (ba.counters) {
+    const size_t nt = static_cast<size_t>(ctx->tiles_x) * ctx->tiles_y;
+    FGS_CHECK(ctx->tile_span_bwd.ensure(2 * nt));
+    FGS_CHECK(cudaMemsetAsync(ctx->tile_span_bwd.p, 0, 2 * nt * sizeof(unsigned long long), st));
+    ba.tile_span = ctx->tile_span_bwd.p;
+  }
   const bool timing = (ctx->flags & FGS_FLAG_TIMING) != 0;
   if (timing && ctx->pending.size() > 64) drain_sets(ctx, 8);
   cudaEvent_t* ev = timing ? take_set(ctx, 1)->e : nullptr;
+  SetGuard guard{ctx, timing};
   if (timing) cudaEventRecord(ev[0], st);
   if (I > 0) {
     const int var = ctx->bwd_var.pick(I, st);
@@ -692,6 +776,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.log_scales = scene->log_scales;
   pb.opacity = scene->opacity_logits;
   pb.sh = scene->sh;
+  pb.vec_rot = aligned16(scene->rotations);
   pb.state = ctx->state.p;
   pb.touched = ctx->touched.p;
   pb.coff = ctx->coff.p;
@@ -713,6 +798,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   }
   if (timing) cudaEventRecord(ev[2], st);
   FGS_CHECK(cudaGetLastError());
+  guard.armed = false;
   return FGS_OK;
 }
 
@@ -1032,6 +1118,10 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   if (nm == "radius") return copy(ctx->radii.p, n * 4);
   if (nm == "touched") return copy(ctx->touched.p, n * 4);
   if (nm == "sorted_gauss") return copy(ctx->sorted_gauss.p, I * 4);
+  // hot-path state: the 64-bit (depth key << 32 | Gaussian id) keys as K2's scatter left them in
+  // each tile's range (K3 sorts lists of <= 4096 keys in shared memory, longer ones in place)
+  if (nm == "keys") return copy(ctx->keys.p, I * 8);
+  if (nm == "rect") return copy(ctx->rect.p, n * sizeof(ushort4));
   if (nm == "compact_gauss") return copy(ctx->cval.p, static_cast<size_t>(ctx->num_compact) * 4);
   if (nm == "compact_offsets") return copy(ctx->coff.p, static_cast<size_t>(ctx->num_compact) * 4);
   if (nm == "sorted_tile") {
@@ -1053,6 +1143,8 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   if (nm == "counters16") return copy(ctx->counters.p, 16 * sizeof(unsigned long long));
   if (nm == "bin_trace") return copy(ctx->counters.p + 16, 8 * sizeof(unsigned long long));
   if (nm == "tile_cycles") return copy(ctx->tile_cycles.p, nt * sizeof(unsigned long long));
+  if (nm == "tile_span") return copy(ctx->tile_span.p, 2 * nt * sizeof(unsigned long long));
+  if (nm == "tile_span_bwd") return copy(ctx->tile_span_bwd.p, 2 * nt * sizeof(unsigned long long));
   if (nm == "key_tile" || nm == "key_depth" || nm == "key_gauss") {
     if (!dst) return static_cast<int64_t>(I * 4);
     // Recompute the reference's pre-sort emission order (source order) on demand.

@@ -80,6 +80,20 @@ __device__ __forceinline__ float fast_rcp(float x) {
   return y;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+
+// Instrumentation (FGS_FLAG_COUNTERS): a CTA's [start, end] in span[2 tile], span[2 tile + 1].
+__device__ __forceinline__ void span_start(unsigned long long* span, int tile) {
+  if (span && threadIdx.x == 0) span[2 * tile] = global_ns();
+}
+__device__ __forceinline__ void span_end(unsigned long long* span, int tile) {
+  if (span && (threadIdx.x & 31) == 0) atomicMax(span + 2 * tile + 1, global_ns());
+}
+
 __host__ __device__ inline int div_up(int a, int b) { return (a + b - 1) / b; }
 
 // Host-side one-time setup that is per device (function attributes, __constant__ data,
@@ -182,16 +196,6 @@ __device__ __forceinline__ bool rec_hits_ellipse(float4 ra, float4 rb, float4 rc
   best = fminf(best, q(fminf(fmaxf(__fmul_rn(nba, ly), lx), hx), ly));
   best = fminf(best, q(fminf(fmaxf(__fmul_rn(nba, hy), lx), hx), hy));
   return best <= tau;
-}
-
-// Backward blend geometry: 8 warps per 16x16 tile, warp w owns the 8x4 pixel block at
-// (8*(w&1), 4*(w>>1)); the box spans the block's pixel centres.
-constexpr int kBwdWarps = 8;
-__device__ __forceinline__ void bwd_block_box(int tx, int ty, int w, float& x0, float& x1, float& y0, float& y1) {
-  x0 = static_cast<float>(tx * kTile + ((w & 1) << 3)) + 0.5f;
-  x1 = x0 + 7.0f;
-  y0 = static_cast<float>(ty * kTile + ((w >> 1) << 2)) + 0.5f;
-  y1 = y0 + 3.0f;
 }
 
 }  // namespace fgs

@@ -24,6 +24,7 @@ struct PreprocessArgs {
   uint32_t* touched;     // tiles touched
   ushort4* rect;         // tx0, tx1, ty0, ty1
   int32_t* radii;        // per Gaussian radius (0 = culled / degenerate)
+  int vec_rot, vec_sh, vec_geo;  // rotations / sh / means+log_scales 16-byte aligned: LDG.128
   int32_t* rowdiff;      // tiles_y x (tiles_x + 1) row-difference tile counts
   int* error_flag;
   uint32_t* state_counts;  // [kept, degenerate]
@@ -45,6 +46,7 @@ struct PreprocessBackwardArgs {
   const float* log_scales;
   const float* opacity;
   const float* sh;
+  int vec_rot;               // rotations 16-byte aligned: LDG.128
   const uint8_t* state;
   const uint32_t* touched;
   const uint32_t* coff;      // [m] first emission slot of cval[q]
@@ -72,14 +74,21 @@ struct BlendArgs {
   uint32_t* last;                // H*W: index one past the last contributing entry
   unsigned long long* counters;  // optional: E_eval, E_contrib, culled evals, max CTA cycles
   unsigned long long* tile_cycles;  // optional (with counters): per-tile CTA cycles
+  unsigned long long* tile_span;    // optional (with counters): per tile [start, end] %globaltimer (ns)
   const uint32_t* tile_order;    // optional: CTA -> tile (heaviest lists first)
   const uint32_t* scalars;       // forward: device scalars; exit if I > isect_cap (speculative launch)
+  uint32_t* seg_cursor;          // forward: slot allocation cursor (scalars[kScalarSegPos])
+  float* ckpt;                   // segment checkpoints [slot][4][256] (T, C0, C1, C2 per tile pixel)
+  uint32_t* seg_items;           // [slot] tile | k << 16 (segment k >= 1 of tile), k = kSegFinal: final state
+  uint32_t* tile_ckpt;           // [tile] first slot of a long list's checkpoints
+  int64_t ckpt_cap;              // slots the checkpoint buffers hold
+  int64_t num_seg_items;         // backward: slots of the frame (the first CTAs take the segments k >= 1)
   uint32_t* zero_next;           // forward: 16 scalars of the next frame, zeroed by CTA 0
   int64_t isect_cap;
   // backward
   const float* dl_dimage;
-  float* partials;               // I x 8 x 9 per-(entry, pixel block) sums
-  float* partial_tile;           // I x 9 per-intersection sums by emission slot (backward epilogue)
+  uint32_t* sorted_slot;          // I: emission slot of each sorted entry (backward scratch)
+  float* partial_tile;           // I x 9 per-intersection sums by emission slot (K4a -> K4b)
 };
 
 // K1 / K4b launches (preprocess.cu); host_scene: the scene arrays are pinned host memory read in
@@ -90,7 +99,16 @@ constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per 
 
 // ---- binning / sorting (binning.cu) ----
 constexpr int kBinThreads = 1024;
-constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, kScalarM = 4, kScalarI2 = 5, kScalarBig = 6;
+constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, kScalarM = 4, kScalarI2 = 5, kScalarBig = 6,
+              kScalarSegs = 7,    // backward segment slots of the frame (K2: sum over long lists of ceil(L / kSeg))
+              kScalarSegPos = 8;  // K3's slot allocation cursor
+
+// Backward segments: a tile list longer than kSeg entries is split into ceil(L / kSeg) segments
+// that the blend backward processes as independent CTAs; the forward leaves each pixel's state
+// (T and accumulated colour) at every segment boundary, plus its final (T, colour), in one
+// checkpoint slot per segment (4 x 256 floats, SoA over the tile's pixels).
+constexpr int kSeg = 256;
+constexpr uint32_t kSegFinal = 0xFFFFu;  // item marker of a tile's final-state slot
 
 struct BinArgs {
   int n;                       // Gaussians

@@ -263,8 +263,17 @@ __device__ __forceinline__ void sh_dir_grad(const float d[3], int degree, const 
   ddir[2] += gz * dc;
 }
 
-// The 16 coefficients of one colour channel, vectorised (channel rows are 64-byte aligned).
-__device__ __forceinline__ void load_sh16(const float* __restrict__ sh, int64_t g, int ch, int degree, float k[16]) {
+// 16-byte load of p[0..3]: one LDG.128 when the array base is 16-byte aligned (vec), else four
+// scalar loads (a caller's arrays may start anywhere, e.g. field blocks of a flat 59*N buffer).
+__device__ __forceinline__ float4 ld4(const float* __restrict__ p, bool vec) {
+  if (vec) return __ldg(reinterpret_cast<const float4*>(p));
+  return make_float4(__ldg(p), __ldg(p + 1), __ldg(p + 2), __ldg(p + 3));
+}
+
+// The 16 coefficients of one colour channel, vectorised when the SH array is 16-byte aligned
+// (channel rows are then 64-byte aligned).
+__device__ __forceinline__ void load_sh16(const float* __restrict__ sh, int64_t g, int ch, int degree, bool vec,
+                                          float k[16]) {
   const float* p = sh + g * 48 + 16 * ch;
   if (degree == 0) {
     k[0] = __ldg(p);
@@ -272,10 +281,9 @@ __device__ __forceinline__ void load_sh16(const float* __restrict__ sh, int64_t 
     for (int j = 1; j < 16; ++j) k[j] = 0.0f;
     return;
   }
-  const float4* p4 = reinterpret_cast<const float4*>(p);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const float4 v = __ldg(p4 + q);
+    const float4 v = ld4(p + 4 * q, vec);
     k[4 * q + 0] = v.x; k[4 * q + 1] = v.y; k[4 * q + 2] = v.z; k[4 * q + 3] = v.w;
   }
 }
@@ -381,7 +389,7 @@ static size_t preprocess_host_smem() { return sizeof(float4) * 8 * 32 * kStageRo
 // as contiguous runs by the whole warp (a lane reading its own 192-byte row issues 16-byte
 // pieces 192 bytes apart, which PCIe serves at a third of the rate) into stage[lane][...].
 __device__ __forceinline__ void stage_sh_rows(const float* __restrict__ sh, int64_t warp_g0, bool need, int degree,
-                                              float4* stage) {
+                                              bool vec, float4* stage) {
   const int lane = threadIdx.x & 31;
   const unsigned mask = __ballot_sync(0xffffffffu, need);
   const int nq = sh_row_f4(degree), per_row = 3 * nq;
@@ -390,8 +398,8 @@ __device__ __forceinline__ void stage_sh_rows(const float* __restrict__ sh, int6
     const int r = it / per_row, t = it - r * per_row;
     const int src_lane = __fns(mask, 0, r + 1);  // the r-th needing lane
     const int ch = t / nq, q = t - ch * nq;
-    const float4* row = reinterpret_cast<const float4*>(sh + (warp_g0 + src_lane) * 48);
-    stage[src_lane * kStageRow + ch * 4 + q] = __ldg(row + ch * 4 + q);
+    const float* row = sh + (warp_g0 + src_lane) * 48;
+    stage[src_lane * kStageRow + ch * 4 + q] = ld4(row + 4 * (ch * 4 + q), vec);
   }
   __syncwarp();
 }
@@ -402,7 +410,7 @@ template <bool HOST_SCENE>
 __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t i, bool valid, const float m[3],
                                                const float ls[3], unsigned* s_counts, float4* stage) {
   const DevCamera& cam = a.cam;
-  const float4 q = valid ? __ldg(reinterpret_cast<const float4*>(a.rotations) + i) : make_float4(1.f, 0.f, 0.f, 0.f);
+  const float4 q = valid ? ld4(a.rotations + 4 * i, a.vec_rot) : make_float4(1.f, 0.f, 0.f, 0.f);
   // host scene: every lane reads its opacity (one coalesced 128-byte run per warp over PCIe
   // instead of scattered 4-byte reads by the kept lanes)
   const float op_host = HOST_SCENE && valid ? __ldg(a.opacity + i) : 0.0f;
@@ -432,7 +440,7 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
              my - rf > static_cast<float>(cam.height));
   }
   if constexpr (HOST_SCENE) {
-    if (a.sh_degree > 0) stage_sh_rows(a.sh, i - (threadIdx.x & 31), keep, a.sh_degree, stage);
+    if (a.sh_degree > 0) stage_sh_rows(a.sh, i - (threadIdx.x & 31), keep, a.sh_degree, a.vec_sh, stage);
   }
   if (keep) {
     state = 1;
@@ -459,7 +467,7 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
           k[4 * qq + 0] = v.x; k[4 * qq + 1] = v.y; k[4 * qq + 2] = v.z; k[4 * qq + 3] = v.w;
         }
       } else {
-        load_sh16(a.sh, i, ch, a.sh_degree, k);
+        load_sh16(a.sh, i, ch, a.sh_degree, a.vec_sh, k);
       }
       col[ch] = sh_channel(k, Y, a.sh_degree);
     }
@@ -520,10 +528,10 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(PreprocessArgs a) {
     const int64_t nrem = a.n - i0;
     const int nf = static_cast<int>((nrem < 256 ? nrem : 256) * 3);  // floats of this CTA
     const float* src[2] = {a.means + i0 * 3, a.log_scales + i0 * 3};
-    // 3 * 256 floats per array; i0 * 3 * 4 bytes is 16-byte aligned (i0 is a multiple of 256)
+    // 3 * 256 floats per array; i0 * 3 * 4 bytes is a multiple of 16 (i0 is a multiple of 256)
     for (int t = threadIdx.x; t < 2 * 192; t += blockDim.x) {
       const int arr = t / 192, j = t - arr * 192;
-      if (4 * j + 3 < nf) s_geo[arr][j] = __ldg(reinterpret_cast<const float4*>(src[arr]) + j);
+      if (4 * j + 3 < nf) s_geo[arr][j] = ld4(src[arr] + 4 * j, a.vec_geo);
       else {
         float v[4] = {0.f, 0.f, 0.f, 0.f};
         for (int e = 0; e < 4; ++e) if (4 * j + e < nf) v[e] = __ldg(src[arr] + 4 * j + e);
@@ -567,7 +575,7 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
   {
     const DevCamera& cam = a.cam;
     const float m[3] = {__ldg(a.means + 3 * i), __ldg(a.means + 3 * i + 1), __ldg(a.means + 3 * i + 2)};
-    const float4 q = __ldg(reinterpret_cast<const float4*>(a.rotations) + i);
+    const float4 q = ld4(a.rotations + 4 * i, a.vec_rot);
     const float ls[3] = {__ldg(a.log_scales + 3 * i), __ldg(a.log_scales + 3 * i + 1), __ldg(a.log_scales + 3 * i + 2)};
     Proj P;
     project_covariance(cam, m, q, ls, P);

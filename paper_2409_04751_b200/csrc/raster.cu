@@ -31,11 +31,6 @@ namespace {
 template <int PX>
 constexpr int kGroup = PX == 1 ? 4 : 3;
 
-// Record of sorted entry k, through the sorted Gaussian index.
-__device__ __forceinline__ SortedRec load_rec(const BlendArgs& a, uint32_t k) {
-  return a.rec[__ldg(a.sorted_gauss + k)];
-}
-
 struct PixelState {
   float T, C0, C1, C2;
   uint32_t last, stop, contrib;
@@ -103,7 +98,9 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   float4 (*s0)[32] = s01[0];
   float4 (*s1)[32] = s01[1];
   if (a.zero_next && blockIdx.x == 0 && threadIdx.x < 16) a.zero_next[threadIdx.x] = 0u;
-  if (a.scalars && a.scalars[kScalarI] > a.isect_cap) return;  // speculative launch, buffers too small
+  // speculative launch with buffers too small: the host grows them and launches again
+  if (a.scalars && (a.scalars[kScalarI] > a.isect_cap || a.scalars[kScalarSegs] > a.ckpt_cap)) return;
+  __shared__ int s_slot0;  // first checkpoint slot of this tile (long lists), or -1
   const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -111,6 +108,22 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   const int px = bx + (lane & 7);
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
   const long long t_start = COUNTERS ? clock64() : 0;
+  if (COUNTERS) span_start(a.tile_span, tile);
+  // long list: reserve its segments' checkpoint slots (segments k = 1.. of the backward, then
+  // the final state); visible to all threads after the sort's barriers
+  const int nseg = static_cast<int>((hi - lo + kSeg - 1) / kSeg);
+  if (threadIdx.x == 0) {
+    s_slot0 = -1;
+    if (nseg > 1 && a.ckpt) {
+      const uint32_t pos = atomicAdd(a.seg_cursor, static_cast<uint32_t>(nseg));
+      if (pos + nseg <= a.ckpt_cap) {
+        s_slot0 = static_cast<int>(pos);
+        a.tile_ckpt[tile] = pos;
+        for (int k = 1; k < nseg; ++k) a.seg_items[pos + k - 1] = static_cast<uint32_t>(tile) | (static_cast<uint32_t>(k) << 16);
+        a.seg_items[pos + nseg - 1] = static_cast<uint32_t>(tile) | (kSegFinal << 16);
+      }
+    }
+  }
   // sort the tile's (depth, emission slot) keys; the ids stay in shared memory when they fit
   static_assert(sizeof(s01) == NW * 256 * sizeof(uint32_t), "digit counters overlay the staging");
   const int id_off = sort_tile_list<256 / PX>(a.keys, a.sorted_gauss, lo, static_cast<int>(hi - lo), skeys,
@@ -162,8 +175,24 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   };
   const unsigned lt = (1u << lane) - 1u;
   prefetch(lo);
+  const int slot0 = nseg > 1 ? s_slot0 : -1;  // (short lists: no barrier since thread 0 wrote it)
+  const int lpix = (py[0] - ty * kTile) * kTile + (px - tx * kTile);  // pixel q at lpix + 64 q
+  // one checkpoint: (T, C) of the lane's pixels before entries >= the boundary (or final)
+  auto checkpoint = [&](int slot, bool fin) {
+    float* c = a.ckpt + static_cast<size_t>(slot) * (4 * kTile * kTile);
+#pragma unroll
+    for (int q = 0; q < PX; ++q) {
+      const PixelState& p = ps[q];
+      const int l = lpix + 64 * q;
+      c[l] = p.T;
+      c[256 + l] = fin ? p.C0 + p.T * a.bg[0] : p.C0;
+      c[512 + l] = fin ? p.C1 + p.T * a.bg[1] : p.C1;
+      c[768 + l] = fin ? p.C2 + p.T * a.bg[2] : p.C2;
+    }
+  };
   for (uint32_t base = lo; base < hi; base += 32) {
     if (__all_sync(0xffffffffu, all_done())) break;
+    if (slot0 >= 0 && base > lo && (base - lo) % kSeg == 0) checkpoint(slot0 + static_cast<int>((base - lo) / kSeg) - 1, false);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
     // (the exact ellipse test, which the backward uses, costs the forward more than the ~13%
@@ -229,6 +258,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     __syncwarp();
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  if (slot0 >= 0) checkpoint(slot0 + nseg - 1, true);  // final state: T and the pixel's image value
   if (COUNTERS) {
     const long long t_cta = clock64() - t_start;
     unsigned long long ev = 0, ec = 0;
@@ -252,6 +282,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
       atomicMax(a.counters + 3, static_cast<unsigned long long>(t_cta));
       if (a.tile_cycles) atomicMax(a.tile_cycles + tile, static_cast<unsigned long long>(t_cta));
     }
+    span_end(a.tile_span, tile);
   }
 #pragma unroll
   for (int q = 0; q < PX; ++q) {
@@ -272,17 +303,24 @@ __device__ __forceinline__ bool near_threshold(float ar) {
   return fabsf(ar - kAlphaSkip) <= kGuardRel * kAlphaSkip || fabsf(ar - kAlphaClamp) <= kGuardRel * kAlphaClamp;
 }
 
-// K4a backward blend (inc/gradients.hpp:69-175), barrier-free like the forward. PX pixels per
-// lane: 8/PX warps per tile, warp w owns the 8 x 4PX block of bwd_block_box<PX>, lane l the
-// pixels (l&7, (l>>3) + 4u), u < PX (one column, so dx and its products are shared). Each warp
-// walks the tile's list backwards from its last contributor (the max of its pixels' `last`) in
-// 32-splat chunks, culls them against its block (rec_hits on the extent K1 stored), and for
-// each surviving splat recovers T_before = T_after / (1 - alpha), accumulates the suffix colour
-// and forms the 9 per-pixel gradients (mean_px 2, conic 3, colour 3, alpha_max 1), summed over
-// the lane's pixels and then the warp by a shuffle tree. The warp sum goes to partials[k][w] --
-// one slot per (intersection, block) whose block passes the cull, zeros for passing splats past
-// the warp's last contributor -- and the CTA's epilogue adds the passing slots of every entry
-// in block order into partial_tile[emission slot]: deterministic, no atomics.
+// K4a backward blend (inc/gradients.hpp:69-175). One CTA per tile, PX pixels per lane: 8/PX
+// warps, warp w owns the 8 x 4PX block of bwd_box<PX>, lane l the pixels (l&7, (l>>3) + 4u),
+// u < PX (one column, so dx and its products are shared).
+//
+// The CTA walks the tile's list backwards in 32-entry chunks, from the last contributor of any
+// of its pixels, all warps on the same chunk:
+//   * the chunk's 48-byte records (and each entry's emission slot) are staged in shared memory
+//     once per CTA by cp.async, two chunks ahead;
+//   * each warp culls the chunk against its block (box test on K1's extent, then the exact
+//     ellipse test), and for every surviving splat, latest first, recovers T_before =
+//     T_after / (1 - alpha), accumulates the suffix colour and forms the 9 per-pixel gradients
+//     (mean_px 2, conic 3, colour 3, alpha_max 1), summed over the lane's pixels and then the warp
+//     by a butterfly reduce-scatter; the warp's 9 sums per surviving entry and its survivor mask
+//     go to shared memory;
+//   * after one CTA barrier per chunk, the CTA adds, per entry, the sums of the warps whose mask
+//     has it, in warp order, and stores the 9 values at the intersection's emission slot (K4b
+//     then reads each Gaussian's intersections contiguously).
+// Per-entry sums never leave the SM; deterministic (fixed summation order, no atomics).
 template <int PX>
 __device__ __forceinline__ void bwd_box(int tx, int ty, int w, float& x0, float& x1, float& y0, float& y1) {
   x0 = static_cast<float>(tx * kTile + ((w & 1) << 3)) + 0.5f;
@@ -291,31 +329,58 @@ __device__ __forceinline__ void bwd_box(int tx, int ty, int w, float& x0, float&
   y1 = y0 + (4.0f * PX - 1.0f);
 }
 
-constexpr uint32_t kPassCap = 4096;  // list entries whose per-block pass bits live in shared memory
+// emission slot of tile (tx, ty) in Gaussian g's intersection list: g's first slot + the tile's
+// index in its rectangle (ty-major, tx-minor; splatting.hpp:216-221)
+__device__ __forceinline__ uint32_t emission_slot(const BlendArgs& a, uint32_t g, int tx, int ty) {
+  const ushort4 rc = a.rect[g];
+  return a.src_off[g] + static_cast<uint32_t>((ty - rc.z) * (rc.y - rc.x + 1) + (tx - rc.x));
+}
 
 // MINB: CTAs per SM the register allocation is fitted to (a launch-bounds variant: same code,
-// same results, different occupancy; which is faster depends on the scene).
+// same results, different occupancy).
 template <int PX, int MINB>
 __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArgs a) {
-  constexpr int NW = 8 / PX;
-  __shared__ uint32_t s_pass[kPassCap / 4];  // 8 bits (one per warp block) per list entry
-  __shared__ float4 s0[NW][32];
-  __shared__ float4 s1[NW][32];
-  __shared__ float s2[NW][32];
-  __shared__ uint32_t sk[NW][32];            // list index of each staged record
-  __shared__ float4 s_raw[NW][96];           // the next chunk's records (cp.async)
-  const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
+  constexpr int NT = 256 / PX, NW = 8 / PX;
+  __shared__ float4 s_rec[2][96];          // chunk records, double buffered
+  __shared__ uint32_t s_slot[3][32];       // chunk entries' emission slots (read by the reduction)
+  __shared__ float s_part[2][NW][32 * 9];  // per-warp sums of the chunk's entries
+  __shared__ uint32_t s_mask[2][NW];       // per-warp survivor masks (bit j: entry cs + j)
+  __shared__ uint32_t s_top[NW];
+  // work item: segment `seg` of a tile's list (the first num_seg_items CTAs take the segments
+  // k >= 1 of long lists, the rest segment 0 of every tile, heaviest lists first)
+  int tile, seg = 0;
+  if (static_cast<int64_t>(blockIdx.x) < a.num_seg_items) {
+    const uint32_t item = a.seg_items[blockIdx.x];
+    seg = static_cast<int>(item >> 16);
+    if (seg == static_cast<int>(kSegFinal)) return;  // a final-state slot: no work item
+    tile = static_cast<int>(item & 0xFFFFu);
+  } else {
+    const uint32_t b = blockIdx.x - static_cast<uint32_t>(a.num_seg_items);
+    tile = a.tile_order ? static_cast<int>(a.tile_order[b]) : static_cast<int>(b);
+  }
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (seg == 0) span_start(a.tile_span, tile);
   float bx0, bx1, by0, by1;
   bwd_box<PX>(tx, ty, warp, bx0, bx1, by0, by1);
   const int px = static_cast<int>(bx0) + (lane & 7);
-  const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
-  for (uint32_t j = threadIdx.x; j < min(hi - lo, kPassCap) / 4 + 1; j += blockDim.x) s_pass[j] = 0u;
-  __syncthreads();
+  const uint32_t tlo = a.tile_offsets[tile], thi = a.tile_offsets[tile + 1];
+  // this item's entries [lo, hi)
+  const uint32_t lo = tlo + static_cast<uint32_t>(seg) * kSeg;
+  const uint32_t hi = min(thi, lo + static_cast<uint32_t>(kSeg));
+  const int nseg = static_cast<int>((thi - tlo + kSeg - 1) / kSeg);
+  const float* ck = nullptr;   // checkpoint at hi (state before entries >= hi), for hi < thi
+  const float* fin = nullptr;  // the tile's final state (T, image value)
+  if (nseg > 1) {
+    const uint32_t slot0 = a.tile_ckpt[tile];
+    fin = a.ckpt + static_cast<size_t>(slot0 + nseg - 1) * (4 * kTile * kTile);
+    if (seg + 1 < nseg) ck = a.ckpt + static_cast<size_t>(slot0 + seg) * (4 * kTile * kTile);
+  }
   const float fx = static_cast<float>(px) + 0.5f;
   // ds: dL/dpixel . (suffix colour), the suffix colour T_final * bg + sum_{j later} c_j w_j
-  // (gradients.hpp:132, :143) kept only through its dot product with dL/dpixel
+  // (gradients.hpp:132, :143) kept only through its dot product with dL/dpixel. A pixel whose last
+  // contributor lies past this segment starts from the forward's checkpoint at hi: T there, and
+  // the suffix colour = (image value) - (colour accumulated before hi).
   float T[PX], dl[PX][3], ds[PX], fy[PX];
   uint32_t last[PX];
   uint32_t mylast = lo;
@@ -326,95 +391,123 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
     T[u] = 1.0f;
     dl[u][0] = dl[u][1] = dl[u][2] = 0.0f;
     last[u] = lo;
+    float suf[3] = {0.0f, 0.0f, 0.0f};
     if (px < a.width && py < a.height) {
       const size_t pix = static_cast<size_t>(py) * a.width + px;
-      T[u] = a.final_T[pix];
-      last[u] = a.last[pix];
+      const uint32_t lp = a.last[pix];
       dl[u][0] = a.dl_dimage[pix * 3 + 0];
       dl[u][1] = a.dl_dimage[pix * 3 + 1];
       dl[u][2] = a.dl_dimage[pix * 3 + 2];
+      if (lp > hi) {
+        const int l = (py - ty * kTile) * kTile + (px - tx * kTile);
+        T[u] = ck[l];
+#pragma unroll
+        for (int c3 = 0; c3 < 3; ++c3) suf[c3] = fin[256 * (c3 + 1) + l] - ck[256 * (c3 + 1) + l];
+        last[u] = hi;
+      } else {
+        T[u] = a.final_T[pix];
+#pragma unroll
+        for (int c3 = 0; c3 < 3; ++c3) suf[c3] = T[u] * a.bg[c3];
+        last[u] = max(lp, lo);
+      }
     }
-    ds[u] = dl[u][0] * (T[u] * a.bg[0]) + dl[u][1] * (T[u] * a.bg[1]) + dl[u][2] * (T[u] * a.bg[2]);
+    ds[u] = dl[u][0] * suf[0] + dl[u][1] * suf[1] + dl[u][2] * suf[2];
     mylast = max(mylast, last[u]);
   }
   const uint32_t wlast = __reduce_max_sync(0xffffffffu, mylast);
-  float* part = a.partials;
-
-  // Splats past the warp's last contributor add nothing: with pass bits (lists up to kPassCap)
-  // their bits simply stay clear; longer lists, whose epilogue re-tests the blocks, get zero slots
-  if (hi - lo > kPassCap) {
-    for (uint32_t base = wlast; base < hi; base += 32) {
-      const uint32_t k = base + lane;
-      if (k < hi) {
-        const SortedRec r = load_rec(a, k);
-        if (rec_hits(r.a, r.c, bx0, bx1, by0, by1) &&
-            (!a.ellipse || rec_hits_ellipse(r.a, r.b, r.c, bx0, bx1, by0, by1))) {
-          float* p = part + (static_cast<size_t>(k) * NW + warp) * 9;
+  if (lane == 0) s_top[warp] = wlast;
+  __syncthreads();
+  uint32_t top = lo;
 #pragma unroll
-          for (int q = 0; q < 9; ++q) p[q] = 0.0f;
+  for (int w = 0; w < NW; ++w) top = max(top, s_top[w]);
+  // every entry's emission slot, computed up front (two dependent loads each, all in flight at
+  // once) so the chunk loop fetches slots with plain asynchronous copies; entries past every
+  // pixel's last contributor add nothing: zero sums at their slots
+  for (uint32_t k = lo + tid; k < hi; k += NT) {
+    const uint32_t e = emission_slot(a, __ldg(a.sorted_gauss + k), tx, ty);
+    if (k < top) {
+      a.sorted_slot[k] = e;
+    } else {
+      float* o = a.partial_tile + static_cast<size_t>(e) * 9;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) o[q] = 0.0f;
+    }
+  }
+  __syncthreads();  // sorted_slot written by this CTA is read back by its cp.async below
+  const int nch = static_cast<int>((top - lo + 31) / 32);
+  // chunk c covers [max(lo, top - 32 (c + 1)), top - 32 c)
+  auto chunk_lo = [&](int c) {
+    return static_cast<uint32_t>(max(static_cast<int64_t>(lo), static_cast<int64_t>(top) - 32 * (c + 1)));
+  };
+  auto prefetch = [&](int c) {  // records of chunk c into s_rec[c & 1], its slots into s_slot[c % 3]
+    if (c < nch) {
+      const uint32_t cs = chunk_lo(c), n = top - 32 * c - cs;
+      if (tid < 96) {
+        const uint32_t j = tid / 3, q = tid - 3 * j;
+        if (j < n) {
+          const float4* src = reinterpret_cast<const float4*>(a.rec + __ldg(a.sorted_gauss + cs + j)) + q;
+          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_rec[c & 1][tid]));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+        }
+      } else if (tid < 128) {
+        const uint32_t j = tid - 96;
+        if (j < n) {
+          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_slot[c % 3][j]));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(a.sorted_slot + cs + j) : "memory");
         }
       }
     }
-  }
-  // reverse walk over [lo, wlast) in 32-entry chunks: the chunk's records arrive by cp.async
-  // one chunk ahead into the warp's raw buffer; survivors are compacted latest first into the
-  // staging slots
-  float4* raw = s_raw[warp];
-  auto prefetch = [&](int64_t end) {  // chunk [max(lo, end - 32), end)
-    const int64_t k = max(static_cast<int64_t>(lo), end - 32) + lane;
-    if (k < end) {
-      const float4* src = reinterpret_cast<const float4*>(a.rec + __ldg(a.sorted_gauss + k));
-      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(raw + lane * 3));
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + q) : "memory");
-    }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  const unsigned gt = ~((2u << lane) - 1u);  // lanes above this one
-  if (wlast > lo) prefetch(wlast);
-  for (int64_t end = wlast; end > static_cast<int64_t>(lo); end -= 32) {
-    const uint32_t cstart = static_cast<uint32_t>(max(static_cast<int64_t>(lo), end - 32));
-    const uint32_t k = cstart + lane;
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncwarp();
-    const float4 ra = raw[lane * 3], rb = raw[lane * 3 + 1], rc = raw[lane * 3 + 2];
-    bool pass = false;
-    if (k < end) {
-      pass = rec_hits(ra, rc, bx0, bx1, by0, by1) && (!a.ellipse || rec_hits_ellipse(ra, rb, rc, bx0, bx1, by0, by1));
-      if (pass && k - lo < kPassCap) atomicOr(s_pass + ((k - lo) >> 2), 1u << (8 * ((k - lo) & 3) + warp));
+  prefetch(0);
+  prefetch(1);
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int b = c & 1;
+    const uint32_t cs = chunk_lo(c), ce = top - 32 * c;
+    const float4* rec = s_rec[b];
+    // ---- this warp's gradients of the chunk ----
+    uint32_t mask = 0;
+    if (cs < wlast) {  // warp-uniform
+      const uint32_t k = cs + lane;
+      if (k < ce && k < wlast) {
+        const float4 ra = rec[3 * lane], rb = rec[3 * lane + 1], rc = rec[3 * lane + 2];
+        if (rec_hits(ra, rc, bx0, bx1, by0, by1) && (!a.ellipse || rec_hits_ellipse(ra, rb, rc, bx0, bx1, by0, by1)))
+          mask = 1u;
+      }
+      mask = __ballot_sync(0xffffffffu, mask != 0);
     }
-    const uint32_t mask = __ballot_sync(0xffffffffu, pass);
-    const int nsurv = __popc(mask);
-    if (pass) {
-      const int pos = __popc(mask & gt);
-      s0[warp][pos] = ra;
-      s1[warp][pos] = rb;
-      s2[warp][pos] = rc.x;
-      sk[warp][pos] = k;
-    }
-    __syncwarp();
-    if (end - 32 > static_cast<int64_t>(lo)) prefetch(end - 32);
+    if (lane == 0) s_mask[b][warp] = mask;
+    float* part = s_part[b][warp];
     // Groups of 3 surviving splats, latest first. Their alphas are independent of the
     // transmittance and are computed together; the transmittance/suffix recurrence then runs
     // in list order, leaving 3 x 9 per-lane gradients (summed over the lane's pixels), which one
     // butterfly reduce-scatter over the warp sums (31 shuffles); lane l ends with value l.
-    for (int j0 = 0; j0 < nsurv; j0 += 3) {
-      float pw[3][PX], ex[3][PX], ar[3][PX], dxs[3], dys[3][PX];
-      float4 r0s[3], r1s[3];
+    for (uint32_t m = mask; m;) {
+      int js[3];
+      int nv = 0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        js[q] = m ? 31 - __clz(m) : js[0];
+        if (m) {
+          m &= ~(1u << js[q]);
+          ++nv;
+        }
+      }
+      float pw[3][PX], ex[3][PX], ar[3][PX], dys[3][PX];
       bool any_near = false;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const int jj = j0 + q < nsurv ? j0 + q : j0;
-        r0s[q] = s0[warp][jj];
-        r1s[q] = s1[warp][jj];
-        dxs[q] = __fsub_rn(fx, r0s[q].x);
+        const float4 r0 = rec[3 * js[q]];
+        const float amax = rec[3 * js[q] + 1].y;
+        const float dx = __fsub_rn(fx, r0.x);
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
-          dys[q][u] = __fsub_rn(fy[u], r0s[q].y);
-          pw[q][u] = blend_power(r0s[q].z, r0s[q].w, r1s[q].x, dxs[q], dys[q][u]);
+          dys[q][u] = __fsub_rn(fy[u], r0.y);
+          pw[q][u] = blend_power(r0.z, r0.w, rec[3 * js[q] + 1].x, dx, dys[q][u]);
           ex[q][u] = fast_exp(pw[q][u]);
-          ar[q][u] = __fmul_rn(r1s[q].y, ex[q][u]);
+          ar[q][u] = __fmul_rn(amax, ex[q][u]);
           any_near |= near_threshold(ar[q][u]);
         }
       }
@@ -425,7 +518,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
           for (int u = 0; u < PX; ++u)
             if (near_threshold(ar[q][u])) {
               ex[q][u] = cr_expf(pw[q][u]);
-              ar[q][u] = __fmul_rn(r1s[q].y, ex[q][u]);
+              ar[q][u] = __fmul_rn(rec[3 * js[q] + 1].y, ex[q][u]);
             }
       }
       // Branch-free: every lane evaluates all three steps and gates them (a non-contributing
@@ -435,33 +528,31 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
       bool contrib_any = false;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const bool valid = j0 + q < nsurv;
-        const int jj = valid ? j0 + q : j0;
-        const uint32_t kk = sk[warp][jj];
-        const float4 r0 = r0s[q], r1 = r1s[q];
-        const float b2 = s2[warp][jj];
-        const float dx = dxs[q];
+        const bool valid = q < nv;
+        const uint32_t kk = cs + js[q];
+        const float4 r0 = rec[3 * js[q]], r1 = rec[3 * js[q] + 1];
+        const float b2 = rec[3 * js[q] + 2].x;
+        const float dx = __fsub_rn(fx, r0.x);
 #pragma unroll
         for (int c9 = 5; c9 < 9; ++c9) v[9 * q + c9] = 0.0f;
         float p0 = 0.0f, p1 = 0.0f, p2 = 0.0f;
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
           const float alpha = fminf(kAlphaClamp, ar[q][u]);
-          const bool c = valid && kk < last[u] && pw[q][u] <= 0.0f && pw[q][u] >= kPowerFloor &&
-                         alpha >= kAlphaSkip;
-          contrib_any |= c;
+          const bool cc = valid && kk < last[u] && pw[q][u] <= 0.0f && pw[q][u] >= kPowerFloor && alpha >= kAlphaSkip;
+          contrib_any |= cc;
           const float dy = dys[q][u];
           const float inv = fast_rcp(1.0f - alpha);
           const float Tb = T[u] * inv;
-          const float w = c ? alpha * Tb : 0.0f;
+          const float w = cc ? alpha * Tb : 0.0f;
           v[9 * q + 5] += dl[u][0] * w;
           v[9 * q + 6] += dl[u][1] * w;
           v[9 * q + 7] += dl[u][2] * w;
           const float dot_c = dl[u][0] * r1.z + dl[u][1] * r1.w + dl[u][2] * b2;
           // clamped contributions carry no geometric gradient
-          const float d_alpha = (c && !(ar[q][u] > kAlphaClamp)) ? dot_c * Tb - ds[u] * inv : 0.0f;
+          const float d_alpha = (cc && !(ar[q][u] > kAlphaClamp)) ? dot_c * Tb - ds[u] * inv : 0.0f;
           ds[u] = fmaf(dot_c, w, ds[u]);
-          T[u] = c ? Tb : T[u];
+          T[u] = cc ? Tb : T[u];
           v[9 * q + 8] += d_alpha * ex[q][u];
           // the mean / conic terms through the lane's moments of dpower (its pixels share dx)
           const float dp = d_alpha * alpha;
@@ -494,52 +585,26 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
       }
       // lane l now holds component l % 9 of splat l / 9 (l < 27)
       const int q = lane / 9;
-      if (lane < 27 && j0 + q < nsurv)
-        part[(static_cast<size_t>(sk[warp][j0 + q]) * NW + warp) * 9 + (lane - 9 * q)] = v[0];
+      const int jq = q == 0 ? js[0] : (q == 1 ? js[1] : js[2]);  // (no dynamic register indexing)
+      if (lane < 27 && q < nv) part[jq * 9 + (lane - 9 * q)] = v[0];
     }
-    __syncwarp();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    // ---- per entry of the chunk: the passing warps' sums in warp order, at the emission slot ----
+    const uint32_t n = ce - cs;
+    for (uint32_t idx = tid; idx < n * 9; idx += NT) {
+      const uint32_t j = idx / 9, q = idx - 9 * j;
+      float sg = 0.0f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+        if ((s_mask[b][w] >> j) & 1u) sg = sg + s_part[b][w][idx];
+      a.partial_tile[static_cast<size_t>(s_slot[c % 3][j]) * 9 + q] = sg;
+    }
+    prefetch(c + 2);
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-  // Epilogue: per entry of the tile, the 9 gradients summed over the pixel blocks that passed
-  // the culling test, in block order (the partials are this CTA's own, L2-resident writes),
-  // stored at the intersection's emission slot (K4b then reads each Gaussian's contiguously).
-  __syncthreads();
-  for (uint32_t k = lo + threadIdx.x; k < hi; k += 256 / PX) {
-    const uint32_t g = __ldg(a.sorted_gauss + k);
-    const ushort4 rc = a.rect[g];
-    // emission slot of (g, this tile): g's first slot + the tile's index in its rectangle
-    const uint32_t e = a.src_off[g] + static_cast<uint32_t>((ty - rc.z) * (rc.y - rc.x + 1) + (tx - rc.x));
-    const float* p = part + static_cast<size_t>(k) * (NW * 9);
-    float sg[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) sg[q] = 0.0f;
-    // blocks whose warp wrote a slot: the pass bits the warps left, or (lists past the bit
-    // capacity) the same tests again
-    uint32_t bits = 0;
-    if (k - lo < kPassCap) {
-      bits = (s_pass[(k - lo) >> 2] >> (8 * ((k - lo) & 3))) & 0xffu;
-    } else {
-      const SortedRec r = a.rec[g];
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        float x0, x1, y0, y1;
-        bwd_box<PX>(tx, ty, w, x0, x1, y0, y1);
-        if (rec_hits(r.a, r.c, x0, x1, y0, y1) && (!a.ellipse || rec_hits_ellipse(r.a, r.b, r.c, x0, x1, y0, y1)))
-          bits |= 1u << w;
-      }
-    }
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      if (!(bits & (1u << w))) continue;
-#pragma unroll
-      for (int q = 0; q < 9; ++q) sg[q] = sg[q] + p[w * 9 + q];
-    }
-    float* o = a.partial_tile + static_cast<size_t>(e) * 9;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) o[q] = sg[q];
-  }
+  if (seg == 0) span_end(a.tile_span, tile);
 }
-
 }  // namespace
 
 int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStream_t st) {
@@ -593,12 +658,18 @@ int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStrea
   }();
   const int tiles = a.tiles_x * a.tiles_y;
   const int px = env == 1 || env == 2 ? env : (num_isect >= 32 * static_cast<int64_t>(tiles) ? 2 : 1);
-  // 2 pixels per lane: variant 1 at ~116 registers (4 CTAs per SM), variant 2 fitted to 6 CTAs
-  // per SM (config 2: 0.313 vs 0.350 ms; configs 1 and 4 the other way round) -- the caller
-  // times both; identical results.
-  if (px == 1) blend_backward_kernel<1, 4><<<tiles, 256, 0, st>>>(a);
-  else if (variant == 2) blend_backward_kernel<2, 6><<<tiles, 128, 0, st>>>(a);
-  else blend_backward_kernel<2, 1><<<tiles, 128, 0, st>>>(a);
+  // 2 pixels per lane: fitted to 6 CTAs per SM (72 registers, no spills) or 8 (64); identical
+  // results. FGS_BWD_MINB=6|8 overrides the variant.
+  static const int env_minb = [] {
+    const char* v = std::getenv("FGS_BWD_MINB");
+    return v ? std::atoi(v) : 0;
+  }();
+  const int minb = env_minb == 6 || env_minb == 8 ? env_minb : (variant == 2 ? 8 : 6);
+  // one CTA per (tile, segment): the long lists' segments k >= 1 first, then every tile's first
+  const int grid = tiles + static_cast<int>(a.num_seg_items);
+  if (px == 1) blend_backward_kernel<1, 4><<<grid, 256, 0, st>>>(a);
+  else if (minb == 8) blend_backward_kernel<2, 8><<<grid, 128, 0, st>>>(a);
+  else blend_backward_kernel<2, 6><<<grid, 128, 0, st>>>(a);
   return 1;
 }
 
