@@ -100,7 +100,6 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   if (a.zero_next && blockIdx.x == 0 && threadIdx.x < 16) a.zero_next[threadIdx.x] = 0u;
   // speculative launch with buffers too small: the host grows them and launches again
   if (a.scalars && (a.scalars[kScalarI] > a.isect_cap || a.scalars[kScalarSegs] > a.ckpt_cap)) return;
-  __shared__ int s_slot0;  // first checkpoint slot of this tile (long lists), or -1
   const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -110,14 +109,14 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   const long long t_start = COUNTERS ? clock64() : 0;
   if (COUNTERS) span_start(a.tile_span, tile);
   // long list: reserve its segments' checkpoint slots (segments k = 1.. of the backward, then
-  // the final state); visible to all threads after the sort's barriers
+  // the final state) in tile_ckpt[tile] (0xFFFFFFFF: none), which the CTA's other threads read
+  // after the sort's barriers (a shared word would cost the 2-pixel kernel its 6th CTA per SM)
   const int nseg = static_cast<int>((hi - lo + kSeg - 1) / kSeg);
-  if (threadIdx.x == 0) {
-    s_slot0 = -1;
-    if (nseg > 1 && a.ckpt) {
+  if (threadIdx.x == 0 && nseg > 1) {
+    a.tile_ckpt[tile] = 0xFFFFFFFFu;
+    if (a.ckpt) {
       const uint32_t pos = atomicAdd(a.seg_cursor, static_cast<uint32_t>(nseg));
       if (pos + nseg <= a.ckpt_cap) {
-        s_slot0 = static_cast<int>(pos);
         a.tile_ckpt[tile] = pos;
         for (int k = 1; k < nseg; ++k) a.seg_items[pos + k - 1] = static_cast<uint32_t>(tile) | (static_cast<uint32_t>(k) << 16);
         a.seg_items[pos + nseg - 1] = static_cast<uint32_t>(tile) | (kSegFinal << 16);
@@ -175,11 +174,15 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   };
   const unsigned lt = (1u << lane) - 1u;
   prefetch(lo);
-  const int slot0 = nseg > 1 ? s_slot0 : -1;  // (short lists: no barrier since thread 0 wrote it)
-  const int lpix = (py[0] - ty * kTile) * kTile + (px - tx * kTile);  // pixel q at lpix + 64 q
-  // one checkpoint: (T, C) of the lane's pixels before entries >= the boundary (or final)
-  auto checkpoint = [&](int slot, bool fin) {
-    float* c = a.ckpt + static_cast<size_t>(slot) * (4 * kTile * kTile);
+  // one checkpoint: (T, C) of the lane's pixels before entries >= the boundary (or final). The
+  // slot and pixel index are re-derived here (shared memory / thread index) to keep the hot
+  // loop's registers free. tile_ckpt is only read for lists longer than kSeg, whose sort has
+  // barriers after thread 0 wrote it.
+  auto checkpoint = [&](int k, bool fin) {
+    const uint32_t slot0 = *reinterpret_cast<volatile const uint32_t*>(a.tile_ckpt + tile);
+    if (slot0 == 0xFFFFFFFFu) return;
+    float* c = a.ckpt + static_cast<size_t>(slot0 + k) * (4 * kTile * kTile);
+    const int lpix = ((warp >> 1) * 4 * PX + (lane >> 3)) * kTile + ((warp & 1) << 3) + (lane & 7);
 #pragma unroll
     for (int q = 0; q < PX; ++q) {
       const PixelState& p = ps[q];
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   };
   for (uint32_t base = lo; base < hi; base += 32) {
     if (__all_sync(0xffffffffu, all_done())) break;
-    if (slot0 >= 0 && base > lo && (base - lo) % kSeg == 0) checkpoint(slot0 + static_cast<int>((base - lo) / kSeg) - 1, false);
+    if (base > lo && (base - lo) % kSeg == 0) checkpoint(static_cast<int>((base - lo) / kSeg) - 1, false);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
     // (the exact ellipse test, which the backward uses, costs the forward more than the ~13%
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     __syncwarp();
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
-  if (slot0 >= 0) checkpoint(slot0 + nseg - 1, true);  // final state: T and the pixel's image value
+  if (hi - lo > kSeg) checkpoint(static_cast<int>((hi - lo + kSeg - 1) / kSeg) - 1, true);  // final: T, image value
   if (COUNTERS) {
     const long long t_cta = clock64() - t_start;
     unsigned long long ev = 0, ec = 0;
