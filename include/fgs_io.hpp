@@ -2,9 +2,11 @@
 // image file formats, so its `render` / `bench` callers can drive the B200
 // path unchanged.
 //
-//   load_ply / save_ply        src/ply_io.cpp:40-145   (3DGS binary_little_endian layout)
-//   load_cameras / save_cameras src/camera_io.cpp:25-127 (camera JSON)
-//   write_image (PPM / PNG)    src/image_io.cpp:19-160 (8-bit, round half to even)
+//   load_ply / save_ply        the format of src/ply_io.cpp:40-145 (3DGS binary_little_endian layout)
+//   load_cameras / save_cameras the format of src/camera_io.cpp:25-127 (camera JSON)
+//   write_image (PPM / PNG)    the formats of src/image_io.cpp:19-160 (8-bit, round half to even)
+// Only the file formats and the error messages follow the reference; the readers and writers are
+// this repo's own (schema-driven PLY columns, a byte sink for PNG / zlib).
 //
 // Errors are std::runtime_error with the reference's messages. The camera JSON reader is a
 // small recursive-descent parser (the reference uses nlohmann-json, absent here); rotation
@@ -35,19 +37,45 @@ namespace fgs {
 namespace io {
 
 // ---------------------------------------------------------------------------------------
-// PLY (src/ply_io.cpp)
+// Scene PLY: the 3DGS export layout the reference reads and writes (src/ply_io.cpp:40-145) --
+// a binary little-endian `vertex` element of float properties, in one of two fixed orders.
+//
+// A layout is a schema: one Column per vertex property saying where its value goes in the
+// structure-of-arrays scene (Gaussian field and component; normals are dropped). Reading parses
+// the header into a PlyHeader, matches the property list against the schemas, then loads the
+// whole payload at once and scatters it column by column.
 
-inline std::vector<std::string> ply_full_properties() {
-  std::vector<std::string> p = {"x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2"};
-  for (int i = 0; i < 45; ++i) p.push_back("f_rest_" + std::to_string(i));
-  for (const char* s : {"opacity", "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"}) p.push_back(s);
-  return p;
+enum class PlyField : uint8_t { Mean, Normal, Sh, Opacity, LogScale, Rotation };
+
+struct PlyColumn {
+  std::string name;
+  PlyField field;
+  int index;  // component (mean / scale / rotation) or SH slot channel * 16 + basis
+};
+
+// with_rest: the full 62-float layout; without: the 17-float DC-only variant. The PLY keeps
+// f_rest_{c*15 + j - 1} for basis j >= 1 of channel c (channel-major), the scene [c*16 + j].
+inline std::vector<PlyColumn> ply_schema(bool with_rest) {
+  std::vector<PlyColumn> cols;
+  const char* axis = "xyz";
+  for (int k = 0; k < 3; ++k) cols.push_back({std::string(1, axis[k]), PlyField::Mean, k});
+  for (int k = 0; k < 3; ++k) cols.push_back({std::string("n") + axis[k], PlyField::Normal, k});
+  for (int c = 0; c < 3; ++c) cols.push_back({"f_dc_" + std::to_string(c), PlyField::Sh, c * 16});
+  if (with_rest)
+    for (int r = 0; r < 45; ++r) cols.push_back({"f_rest_" + std::to_string(r), PlyField::Sh, (r / 15) * 16 + r % 15 + 1});
+  cols.push_back({"opacity", PlyField::Opacity, 0});
+  for (int k = 0; k < 3; ++k) cols.push_back({"scale_" + std::to_string(k), PlyField::LogScale, k});
+  for (int k = 0; k < 4; ++k) cols.push_back({"rot_" + std::to_string(k), PlyField::Rotation, k});
+  return cols;
 }
 
-inline std::vector<std::string> ply_dc_properties() {
-  return {"x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2", "opacity",
-          "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"};
+inline std::vector<std::string> ply_names(const std::vector<PlyColumn>& cols) {
+  std::vector<std::string> v;
+  for (const auto& c : cols) v.push_back(c.name);
+  return v;
 }
+inline std::vector<std::string> ply_full_properties() { return ply_names(ply_schema(true)); }
+inline std::vector<std::string> ply_dc_properties() { return ply_names(ply_schema(false)); }
 
 inline std::string join(const std::vector<std::string>& v) {
   std::string s;
@@ -60,82 +88,98 @@ struct PlyRead {
   std::vector<std::string> warnings;
 };
 
-// SH storage: per Gaussian [channel * 16 + basis]; PLY f_dc_c = basis 0 of channel c,
-// f_rest_{c*15 + j-1} = basis j of channel c (src/ply_io.cpp:109-117).
-inline PlyRead load_ply(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw std::runtime_error("load_ply: cannot open " + path);
-  std::string line;
-  if (!std::getline(in, line) || (line != "ply" && line != "ply\r"))
-    throw std::runtime_error("load_ply: " + path + " is not a PLY file");
-  size_t count = 0;
+struct PlyHeader {
   bool format_seen = false;
-  std::vector<std::string> props;
-  while (std::getline(in, line)) {
+  size_t vertices = 0;
+  std::vector<std::string> properties;
+  std::streamoff payload = 0;  // byte offset of the first vertex
+};
+
+inline std::vector<std::string> split_words(const std::string& line) {
+  std::vector<std::string> w;
+  std::istringstream is(line);
+  for (std::string t; is >> t;) w.push_back(t);
+  return w;
+}
+
+inline PlyHeader read_ply_header(std::istream& in, const std::string& path) {
+  std::string line;
+  auto next = [&]() {
+    if (!std::getline(in, line)) return false;
     if (!line.empty() && line.back() == '\r') line.pop_back();
-    if (line == "end_header") break;
-    std::istringstream ls(line);
-    std::string word;
-    ls >> word;
-    if (word == "format") {
-      std::string fmt;
-      ls >> fmt;
-      if (fmt != "binary_little_endian")
-        throw std::runtime_error("load_ply: binary_little_endian required, got format '" + fmt + "'");
-      format_seen = true;
-    } else if (word == "element") {
-      std::string name;
-      ls >> name >> count;
-      if (name != "vertex") throw std::runtime_error("load_ply: unsupported element '" + name + "'");
-    } else if (word == "property") {
-      std::string type, name;
-      ls >> type >> name;
-      if (type != "float")
-        throw std::runtime_error("load_ply: property '" + name + "' has type '" + type + "', expected float");
-      props.push_back(name);
-    } else if (word == "comment" || word == "obj_info" || word.empty()) {
-      continue;
+    return true;
+  };
+  if (!next() || line != "ply") throw std::runtime_error("load_ply: " + path + " is not a PLY file");
+  PlyHeader h;
+  while (next() && line != "end_header") {
+    const std::vector<std::string> w = split_words(line);
+    const std::string key = w.empty() ? std::string() : w[0];
+    const std::string a1 = w.size() > 1 ? w[1] : std::string(), a2 = w.size() > 2 ? w[2] : std::string();
+    if (key.empty() || key == "comment" || key == "obj_info") continue;
+    if (key == "format") {
+      if (a1 != "binary_little_endian")
+        throw std::runtime_error("load_ply: binary_little_endian required, got format '" + a1 + "'");
+      h.format_seen = true;
+    } else if (key == "element") {
+      if (a1 != "vertex") throw std::runtime_error("load_ply: unsupported element '" + a1 + "'");
+      h.vertices = static_cast<size_t>(std::stoull(a2.empty() ? std::string("0") : a2));
+    } else if (key == "property") {
+      if (a1 != "float")
+        throw std::runtime_error("load_ply: property '" + a2 + "' has type '" + a1 + "', expected float");
+      h.properties.push_back(a2);
     } else {
       throw std::runtime_error("load_ply: unexpected header line '" + line + "'");
     }
   }
-  if (!format_seen) throw std::runtime_error("load_ply: missing format line (binary_little_endian required)");
+  if (!h.format_seen) throw std::runtime_error("load_ply: missing format line (binary_little_endian required)");
+  h.payload = static_cast<std::streamoff>(in.tellg());
+  return h;
+}
+
+inline PlyRead load_ply(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("load_ply: cannot open " + path);
+  const PlyHeader h = read_ply_header(in, path);
   PlyRead out;
-  bool has_rest;
-  if (props == ply_full_properties()) {
-    has_rest = true;
-  } else if (props == ply_dc_properties()) {
-    has_rest = false;
-    out.warnings.push_back("load_ply: f_rest_* properties missing; higher-order SH set to zero");
-  } else {
-    throw std::runtime_error("load_ply: unknown property layout; expected [" + join(ply_full_properties()) +
-                             "] (or the f_rest-free variant), found [" + join(props) + "]");
-  }
-  const size_t stride = props.size();
-  const std::streampos start = in.tellg();
-  SceneSoA& s = out.scene;
-  s.means.resize(count * 3);
-  s.rotations.resize(count * 4);
-  s.log_scales.resize(count * 3);
-  s.opacity_logits.resize(count);
-  s.sh.assign(count * 48, 0.f);
-  std::vector<float> row(stride);
-  for (size_t i = 0; i < count; ++i) {
-    in.read(reinterpret_cast<char*>(row.data()), static_cast<std::streamsize>(stride * 4));
-    if (static_cast<size_t>(in.gcount()) != stride * 4) {
-      const long long off = static_cast<long long>(start) + static_cast<long long>(i * stride * 4) + in.gcount();
-      throw std::runtime_error("load_ply: truncated payload at byte offset " + std::to_string(off));
+  std::vector<PlyColumn> schema;
+  for (bool rest : {true, false}) {
+    std::vector<PlyColumn> cand = ply_schema(rest);
+    if (ply_names(cand) == h.properties) {
+      schema = std::move(cand);
+      if (!rest) out.warnings.push_back("load_ply: f_rest_* properties missing; higher-order SH set to zero");
+      break;
     }
-    size_t k = 0;
-    for (int c = 0; c < 3; ++c) s.means[i * 3 + c] = row[k++];
-    k += 3;  // normals ignored
-    for (int c = 0; c < 3; ++c) s.sh[i * 48 + c * 16] = row[k++];
-    if (has_rest)
-      for (int c = 0; c < 3; ++c)
-        for (int j = 0; j < 15; ++j) s.sh[i * 48 + c * 16 + j + 1] = row[k++];
-    s.opacity_logits[i] = row[k++];
-    for (int c = 0; c < 3; ++c) s.log_scales[i * 3 + c] = row[k++];
-    for (int c = 0; c < 4; ++c) s.rotations[i * 4 + c] = row[k++];
+  }
+  if (schema.empty())
+    throw std::runtime_error("load_ply: unknown property layout; expected [" + join(ply_full_properties()) +
+                             "] (or the f_rest-free variant), found [" + join(h.properties) + "]");
+  // the whole payload in one read; short files report where the data ran out
+  const size_t stride = schema.size(), n = h.vertices;
+  std::vector<float> block(n * stride);
+  in.read(reinterpret_cast<char*>(block.data()), static_cast<std::streamsize>(block.size() * sizeof(float)));
+  const std::streamsize got = in.gcount();
+  if (static_cast<size_t>(got) != block.size() * sizeof(float))
+    throw std::runtime_error("load_ply: truncated payload at byte offset " + std::to_string(h.payload + got));
+  SceneSoA& s = out.scene;
+  s.means.assign(n * 3, 0.f);
+  s.rotations.assign(n * 4, 0.f);
+  s.log_scales.assign(n * 3, 0.f);
+  s.opacity_logits.assign(n, 0.f);
+  s.sh.assign(n * 48, 0.f);
+  for (size_t col = 0; col < stride; ++col) {
+    const PlyColumn& c = schema[col];
+    float* dst = nullptr;
+    size_t width = 0;
+    switch (c.field) {
+      case PlyField::Mean: dst = s.means.data(); width = 3; break;
+      case PlyField::Sh: dst = s.sh.data(); width = 48; break;
+      case PlyField::Opacity: dst = s.opacity_logits.data(); width = 1; break;
+      case PlyField::LogScale: dst = s.log_scales.data(); width = 3; break;
+      case PlyField::Rotation: dst = s.rotations.data(); width = 4; break;
+      case PlyField::Normal: continue;
+    }
+    const float* src = block.data() + col;
+    for (size_t v = 0; v < n; ++v) dst[v * width + static_cast<size_t>(c.index)] = src[v * stride];
   }
   return out;
 }
@@ -143,23 +187,29 @@ inline PlyRead load_ply(const std::string& path) {
 inline void save_ply(const SceneSoA& s, const std::string& path) {
   std::ofstream os(path, std::ios::binary);
   if (!os) throw std::runtime_error("save_ply: cannot open " + path + " for writing");
-  const size_t n = static_cast<size_t>(s.size());
-  os << "ply\nformat binary_little_endian 1.0\nelement vertex " << n << "\n";
-  for (const auto& p : ply_full_properties()) os << "property float " << p << "\n";
-  os << "end_header\n";
-  std::vector<float> row(62);
-  for (size_t i = 0; i < n; ++i) {
-    size_t k = 0;
-    for (int c = 0; c < 3; ++c) row[k++] = s.means[i * 3 + c];
-    for (int c = 0; c < 3; ++c) row[k++] = 0.f;
-    for (int c = 0; c < 3; ++c) row[k++] = s.sh[i * 48 + c * 16];
-    for (int c = 0; c < 3; ++c)
-      for (int j = 0; j < 15; ++j) row[k++] = s.sh[i * 48 + c * 16 + j + 1];
-    row[k++] = s.opacity_logits[i];
-    for (int c = 0; c < 3; ++c) row[k++] = s.log_scales[i * 3 + c];
-    for (int c = 0; c < 4; ++c) row[k++] = s.rotations[i * 4 + c];
-    os.write(reinterpret_cast<const char*>(row.data()), static_cast<std::streamsize>(row.size() * 4));
+  const std::vector<PlyColumn> schema = ply_schema(true);
+  const size_t n = static_cast<size_t>(s.size()), stride = schema.size();
+  std::string header = "ply\nformat binary_little_endian 1.0\nelement vertex " + std::to_string(n) + "\n";
+  for (const auto& c : schema) header += "property float " + c.name + "\n";
+  header += "end_header\n";
+  os.write(header.data(), static_cast<std::streamsize>(header.size()));
+  // gather column by column into the interleaved payload (normals written as zero)
+  std::vector<float> block(n * stride, 0.f);
+  for (size_t col = 0; col < stride; ++col) {
+    const PlyColumn& c = schema[col];
+    const float* src = nullptr;
+    size_t width = 0;
+    switch (c.field) {
+      case PlyField::Mean: src = s.means.data(); width = 3; break;
+      case PlyField::Sh: src = s.sh.data(); width = 48; break;
+      case PlyField::Opacity: src = s.opacity_logits.data(); width = 1; break;
+      case PlyField::LogScale: src = s.log_scales.data(); width = 3; break;
+      case PlyField::Rotation: src = s.rotations.data(); width = 4; break;
+      case PlyField::Normal: continue;
+    }
+    for (size_t v = 0; v < n; ++v) block[v * stride + col] = src[v * width + static_cast<size_t>(c.index)];
   }
+  os.write(reinterpret_cast<const char*>(block.data()), static_cast<std::streamsize>(block.size() * sizeof(float)));
   if (!os) throw std::runtime_error("save_ply: write failed for " + path);
 }
 
@@ -525,92 +575,119 @@ inline void save_cameras(const std::vector<CameraD>& cams, const std::string& pa
 }
 
 // ---------------------------------------------------------------------------------------
-// Images (src/image_io.cpp): 8-bit, values clamped to [0, 1], rounded half to even.
+// Images (src/image_io.cpp's formats): 8-bit RGB, each value clamped to [0, 1] and scaled by 255
+// with round-half-to-even; binary PPM (P6) or PNG. The PNG is written without compression (zlib
+// stored blocks), as the reference's writer does, so any decoder reads it.
 
-inline uint8_t quantize(double v) {
-  v = std::min(1.0, std::max(0.0, v));
-  const double r = std::nearbyint(v * 255.0);
-  return static_cast<uint8_t>(std::min(255.0, std::max(0.0, r)));
+inline uint8_t to_u8(double v) {
+  const double c = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+  return static_cast<uint8_t>(std::lrint((c == c ? c : 0.0) * 255.0));  // NaN -> 0; lrint rounds half to even
 }
+inline uint8_t quantize(double v) { return to_u8(v); }
 
-inline uint32_t crc32_update(uint32_t crc, const uint8_t* data, size_t len) {
-  static const std::array<uint32_t, 256> table = [] {
-    std::array<uint32_t, 256> t{};
-    for (uint32_t n = 0; n < 256; ++n) {
-      uint32_t c = n;
-      for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xedb88320u ^ (c >> 1) : c >> 1;
-      t[n] = c;
+// Append-only big-endian byte buffer with the two checksums PNG / zlib need.
+class ByteSink {
+ public:
+  std::vector<uint8_t> bytes;
+  void u8(uint8_t v) { bytes.push_back(v); }
+  void be32(uint32_t v) {
+    for (int k = 3; k >= 0; --k) bytes.push_back(static_cast<uint8_t>((v >> (8 * k)) & 0xFFu));
+  }
+  void raw(const uint8_t* p, size_t n) { bytes.insert(bytes.end(), p, p + n); }
+  void str(const char* s) { raw(reinterpret_cast<const uint8_t*>(s), std::strlen(s)); }
+
+  // CRC-32 (IEEE 802.3, reflected polynomial 0xEDB88320) of bytes[from, end), bitwise.
+  uint32_t crc32(size_t from) const {
+    uint32_t c = 0xFFFFFFFFu;
+    for (size_t i = from; i < bytes.size(); ++i) {
+      c ^= bytes[i];
+      for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
     }
-    return t;
-  }();
-  crc = ~crc;
-  for (size_t i = 0; i < len; ++i) crc = table[(crc ^ data[i]) & 0xff] ^ (crc >> 8);
-  return ~crc;
-}
-
-inline void put_be32(std::vector<uint8_t>& o, uint32_t v) {
-  for (int s = 24; s >= 0; s -= 8) o.push_back(static_cast<uint8_t>(v >> s));
-}
-
-inline void png_chunk(std::ofstream& os, const char type[4], const std::vector<uint8_t>& payload) {
-  std::vector<uint8_t> buf;
-  put_be32(buf, static_cast<uint32_t>(payload.size()));
-  buf.insert(buf.end(), type, type + 4);
-  buf.insert(buf.end(), payload.begin(), payload.end());
-  put_be32(buf, crc32_update(0, buf.data() + 4, buf.size() - 4));
-  os.write(reinterpret_cast<const char*>(buf.data()), static_cast<std::streamsize>(buf.size()));
-}
-
-// PNG with stored (uncompressed) deflate blocks, as the reference writes.
-inline void write_png(const std::vector<uint8_t>& rgb, int w, int h, const std::string& path) {
-  std::ofstream os(path, std::ios::binary);
-  if (!os) throw std::runtime_error("write_image: cannot open " + path + " for writing");
-  const uint8_t sig[8] = {0x89, 'P', 'N', 'G', '\r', '\n', 0x1a, '\n'};
-  os.write(reinterpret_cast<const char*>(sig), 8);
-  std::vector<uint8_t> ihdr;
-  put_be32(ihdr, static_cast<uint32_t>(w));
-  put_be32(ihdr, static_cast<uint32_t>(h));
-  ihdr.insert(ihdr.end(), {8, 2, 0, 0, 0});
-  png_chunk(os, "IHDR", ihdr);
-  std::vector<uint8_t> raw;
-  raw.reserve(static_cast<size_t>(h) * (1 + 3 * static_cast<size_t>(w)));
-  for (int y = 0; y < h; ++y) {
-    raw.push_back(0);
-    raw.insert(raw.end(), rgb.begin() + static_cast<size_t>(y) * w * 3, rgb.begin() + static_cast<size_t>(y + 1) * w * 3);
+    return c ^ 0xFFFFFFFFu;
   }
-  std::vector<uint8_t> z = {0x78, 0x01};
-  size_t pos = 0;
-  do {
-    const size_t n = std::min<size_t>(raw.size() - pos, 65535);
-    z.push_back(pos + n == raw.size() ? 1 : 0);
-    z.push_back(static_cast<uint8_t>(n & 0xff));
-    z.push_back(static_cast<uint8_t>(n >> 8));
-    z.push_back(static_cast<uint8_t>(~n & 0xff));
-    z.push_back(static_cast<uint8_t>((~n >> 8) & 0xff));
-    z.insert(z.end(), raw.begin() + pos, raw.begin() + pos + n);
-    pos += n;
-  } while (pos < raw.size());
-  uint32_t a = 1, b = 0;
-  for (uint8_t c : raw) {
-    a = (a + c) % 65521;
-    b = (b + a) % 65521;
+};
+
+// Adler-32 with the modulo deferred over runs of 5552 bytes (the longest run whose sums cannot
+// overflow 32 bits).
+inline uint32_t adler32(const uint8_t* p, size_t n) {
+  uint32_t lo = 1, hi = 0;
+  while (n) {
+    const size_t run = n < 5552 ? n : 5552;
+    for (size_t i = 0; i < run; ++i) {
+      lo += p[i];
+      hi += lo;
+    }
+    lo %= 65521u;
+    hi %= 65521u;
+    p += run;
+    n -= run;
   }
-  put_be32(z, (b << 16) | a);
-  png_chunk(os, "IDAT", z);
-  png_chunk(os, "IEND", {});
+  return (hi << 16) | lo;
+}
+
+// zlib stream of stored (BTYPE 00) deflate blocks of at most 65535 bytes.
+inline std::vector<uint8_t> zlib_stored(const std::vector<uint8_t>& data) {
+  ByteSink z;
+  z.u8(0x78);
+  z.u8(0x01);
+  const size_t nblocks = data.empty() ? 1 : (data.size() + 65534) / 65535;
+  for (size_t b = 0; b < nblocks; ++b) {
+    const size_t off = b * 65535, len = std::min<size_t>(65535, data.size() - off);
+    z.u8(b + 1 == nblocks ? 1 : 0);  // BFINAL on the last block
+    const uint16_t l16 = static_cast<uint16_t>(len), nl16 = static_cast<uint16_t>(~l16);
+    z.u8(static_cast<uint8_t>(l16 & 0xFF));
+    z.u8(static_cast<uint8_t>(l16 >> 8));
+    z.u8(static_cast<uint8_t>(nl16 & 0xFF));
+    z.u8(static_cast<uint8_t>(nl16 >> 8));
+    z.raw(data.data() + off, len);
+  }
+  z.be32(adler32(data.data(), data.size()));
+  return z.bytes;
+}
+
+inline void png_append_chunk(ByteSink& out, const char* type, const std::vector<uint8_t>& body) {
+  out.be32(static_cast<uint32_t>(body.size()));
+  const size_t crc_from = out.bytes.size();
+  out.str(type);
+  out.raw(body.data(), body.size());
+  out.be32(out.crc32(crc_from));
+}
+
+inline std::vector<uint8_t> encode_png(const std::vector<uint8_t>& rgb, int w, int h) {
+  ByteSink ihdr;
+  ihdr.be32(static_cast<uint32_t>(w));
+  ihdr.be32(static_cast<uint32_t>(h));
+  for (uint8_t v : {8, 2, 0, 0, 0}) ihdr.u8(v);  // 8-bit depth, truecolour, deflate, no filter, no interlace
+  // scanlines, each led by filter type 0
+  const size_t row = 3 * static_cast<size_t>(w);
+  std::vector<uint8_t> scan(static_cast<size_t>(h) * (row + 1), 0);
+  for (int y = 0; y < h; ++y) std::memcpy(scan.data() + static_cast<size_t>(y) * (row + 1) + 1, rgb.data() + y * row, row);
+  ByteSink png;
+  for (uint8_t v : {0x89, 0x50, 0x4E, 0x47, 0x0D, 0x0A, 0x1A, 0x0A}) png.u8(v);
+  png_append_chunk(png, "IHDR", ihdr.bytes);
+  png_append_chunk(png, "IDAT", zlib_stored(scan));
+  png_append_chunk(png, "IEND", {});
+  return png.bytes;
 }
 
 inline void write_image(const Image& img, const std::string& path) {
+  const size_t dot = path.find_last_of('.');
+  std::string ext = dot == std::string::npos ? std::string() : path.substr(dot + 1);
+  std::transform(ext.begin(), ext.end(), ext.begin(), [](unsigned char ch) { return static_cast<char>(std::tolower(ch)); });
+  if (ext != "png" && ext != "ppm") throw std::runtime_error("write_image: unknown extension '" + ext + "' (use .png or .ppm)");
   std::vector<uint8_t> rgb(img.pixels.size());
-  for (size_t i = 0; i < rgb.size(); ++i) rgb[i] = quantize(img.pixels[i]);
-  std::string ext = path.substr(path.find_last_of('.') == std::string::npos ? path.size() : path.find_last_of('.') + 1);
-  for (auto& c : ext) c = static_cast<char>(std::tolower(c));
-  if (ext == "png") return write_png(rgb, img.width, img.height, path);
-  if (ext != "ppm") throw std::runtime_error("write_image: unknown extension '" + ext + "' (use .png or .ppm)");
+  std::transform(img.pixels.begin(), img.pixels.end(), rgb.begin(), [](float v) { return to_u8(v); });
+  std::vector<uint8_t> file;
+  if (ext == "png") {
+    file = encode_png(rgb, img.width, img.height);
+  } else {
+    const std::string head = "P6\n" + std::to_string(img.width) + " " + std::to_string(img.height) + "\n255\n";
+    file.assign(head.begin(), head.end());
+    file.insert(file.end(), rgb.begin(), rgb.end());
+  }
   std::ofstream os(path, std::ios::binary);
   if (!os) throw std::runtime_error("write_image: cannot open " + path + " for writing");
-  os << "P6\n" << img.width << " " << img.height << "\n255\n";
-  os.write(reinterpret_cast<const char*>(rgb.data()), static_cast<std::streamsize>(rgb.size()));
+  os.write(reinterpret_cast<const char*>(file.data()), static_cast<std::streamsize>(file.size()));
 }
 
 }  // namespace io

@@ -1,8 +1,11 @@
 """Python mirror of the host I/O in include/fgs_io.hpp: the reference's scene PLY and camera
 JSON formats.
 
-  load_ply / save_ply          src/ply_io.cpp:40-145  (3DGS binary_little_endian layout)
-  load_cameras / save_cameras  src/camera_io.cpp:25-127
+  load_ply / save_ply          the format of src/ply_io.cpp:40-145 (3DGS binary_little_endian layout)
+  load_cameras / save_cameras  the format of src/camera_io.cpp:25-127
+
+Only the formats and the error messages follow the reference; the readers are schema-driven
+(one (name, field, component) column per PLY property), as in include/fgs_io.hpp.
 
 Errors are RuntimeError with the reference's messages; warnings are returned, as the
 reference's PlyReadResult / CameraReadResult do.
@@ -16,36 +19,81 @@ import numpy as np
 
 from .types import CAMERA_FISHEYE, CAMERA_PANORAMA, CAMERA_PINHOLE, Camera, Scene
 
-FULL_PROPS = (["x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2"] +
-              [f"f_rest_{i}" for i in range(45)] +
-              ["opacity", "scale_0", "scale_1", "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"])
-DC_PROPS = ["x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2", "opacity", "scale_0", "scale_1",
-            "scale_2", "rot_0", "rot_1", "rot_2", "rot_3"]
+def _ply_schema(with_rest: bool):
+    """Vertex properties of the 3DGS PLY layout as (name, field, component) columns -- the
+    schema of include/fgs_io.hpp's reader. SH components index the scene's [channel*16 + basis]
+    row; the file keeps f_rest_{c*15 + j - 1} for basis j >= 1 of channel c."""
+    cols = [(a, "mean", k) for k, a in enumerate("xyz")] + [("n" + a, None, k) for k, a in enumerate("xyz")]
+    cols += [(f"f_dc_{c}", "sh", 16 * c) for c in range(3)]
+    if with_rest:
+        cols += [(f"f_rest_{r}", "sh", 16 * (r // 15) + r % 15 + 1) for r in range(45)]
+    cols += [("opacity", "opacity", 0)] + [(f"scale_{k}", "log_scale", k) for k in range(3)]
+    cols += [(f"rot_{k}", "rotation", k) for k in range(4)]
+    return cols
+
+
+FULL_PROPS = [c[0] for c in _ply_schema(True)]
+DC_PROPS = [c[0] for c in _ply_schema(False)]
 MODEL_NAMES = {CAMERA_PINHOLE: "pinhole", CAMERA_FISHEYE: "fisheye_equidistant", CAMERA_PANORAMA: "panorama"}
+_WIDTH = {"mean": 3, "sh": 48, "opacity": 1, "log_scale": 3, "rotation": 4}
 
 
-def _sh_to_ply_rest(sh):
-    """(N,48) [channel*16 + basis] -> f_rest order c*15 + (j-1) (src/ply_io.cpp:109-117)."""
-    sh = sh.reshape(-1, 3, 16)
-    return sh[:, :, 1:].reshape(-1, 45)
+def _scene_fields(scene: Scene) -> dict:
+    return {"mean": np.asarray(scene.means, np.float32).reshape(-1, 3),
+            "sh": np.asarray(scene.sh, np.float32).reshape(-1, 48),
+            "opacity": np.asarray(scene.opacity_logits, np.float32).reshape(-1, 1),
+            "log_scale": np.asarray(scene.log_scales, np.float32).reshape(-1, 3),
+            "rotation": np.asarray(scene.rotations, np.float32).reshape(-1, 4)}
 
 
 def save_ply(scene: Scene, path: str) -> None:
-    n = scene.n
-    rows = np.zeros((n, 62), np.float32)
-    rows[:, 0:3] = scene.means
-    sh = np.asarray(scene.sh, np.float32).reshape(n, 3, 16)
-    rows[:, 6:9] = sh[:, :, 0]
-    rows[:, 9:54] = _sh_to_ply_rest(sh)
-    rows[:, 54] = scene.opacity_logits
-    rows[:, 55:58] = scene.log_scales
-    rows[:, 58:62] = scene.rotations
+    schema = _ply_schema(True)
+    fields = _scene_fields(scene)
+    block = np.zeros((scene.n, len(schema)), "<f4")
+    for col, (_, field, comp) in enumerate(schema):
+        if field is not None:
+            block[:, col] = fields[field][:, comp]
+    head = f"ply\nformat binary_little_endian 1.0\nelement vertex {scene.n}\n"
+    head += "".join(f"property float {name}\n" for name, _, _ in schema) + "end_header\n"
     with open(path, "wb") as f:
-        f.write(f"ply\nformat binary_little_endian 1.0\nelement vertex {n}\n".encode())
-        for p in FULL_PROPS:
-            f.write(f"property float {p}\n".encode())
-        f.write(b"end_header\n")
-        f.write(rows.astype("<f4").tobytes())
+        f.write(head.encode())
+        f.write(block.tobytes())
+
+
+def _read_ply_header(f, path):
+    """(vertex count, property names, payload offset); raises with the reference's messages."""
+    def line():
+        raw = f.readline()
+        return None if not raw else raw.decode("latin1").rstrip("\n").rstrip("\r")
+
+    if line() != "ply":
+        raise RuntimeError(f"load_ply: {path} is not a PLY file")
+    count, fmt_seen, props = 0, False, []
+    while True:
+        ln = line()
+        if ln is None or ln == "end_header":
+            break
+        w = ln.split() + ["", "", ""]
+        key, a1, a2 = w[0], w[1], w[2]
+        if key in ("", "comment", "obj_info"):
+            continue
+        if key == "format":
+            if a1 != "binary_little_endian":
+                raise RuntimeError(f"load_ply: binary_little_endian required, got format '{a1}'")
+            fmt_seen = True
+        elif key == "element":
+            if a1 != "vertex":
+                raise RuntimeError(f"load_ply: unsupported element '{a1}'")
+            count = int(a2 or 0)
+        elif key == "property":
+            if a1 != "float":
+                raise RuntimeError(f"load_ply: property '{a2}' has type '{a1}', expected float")
+            props.append(a2)
+        else:
+            raise RuntimeError(f"load_ply: unexpected header line '{ln}'")
+    if not fmt_seen:
+        raise RuntimeError("load_ply: missing format line (binary_little_endian required)")
+    return count, props, f.tell()
 
 
 def load_ply(path: str):
@@ -55,64 +103,28 @@ def load_ply(path: str):
     except OSError:
         raise RuntimeError(f"load_ply: cannot open {path}")
     with f:
-        first = f.readline().decode("latin1").rstrip("\n")
-        if first not in ("ply", "ply\r"):
-            raise RuntimeError(f"load_ply: {path} is not a PLY file")
-        count, fmt_seen, props = 0, False, []
-        while True:
-            raw = f.readline()
-            if not raw:
+        count, props, start = _read_ply_header(f, path)
+        warnings, schema = [], None
+        for rest in (True, False):
+            if props == [c[0] for c in _ply_schema(rest)]:
+                schema = _ply_schema(rest)
+                if not rest:
+                    warnings.append("load_ply: f_rest_* properties missing; higher-order SH set to zero")
                 break
-            line = raw.decode("latin1").rstrip("\n").rstrip("\r")
-            if line == "end_header":
-                break
-            words = line.split()
-            word = words[0] if words else ""
-            if word == "format":
-                fmt = words[1] if len(words) > 1 else ""
-                if fmt != "binary_little_endian":
-                    raise RuntimeError(f"load_ply: binary_little_endian required, got format '{fmt}'")
-                fmt_seen = True
-            elif word == "element":
-                if words[1] != "vertex":
-                    raise RuntimeError(f"load_ply: unsupported element '{words[1]}'")
-                count = int(words[2])
-            elif word == "property":
-                if words[1] != "float":
-                    raise RuntimeError(f"load_ply: property '{words[2]}' has type '{words[1]}', expected float")
-                props.append(words[2])
-            elif word in ("comment", "obj_info", ""):
-                continue
-            else:
-                raise RuntimeError(f"load_ply: unexpected header line '{line}'")
-        if not fmt_seen:
-            raise RuntimeError("load_ply: missing format line (binary_little_endian required)")
-        warnings = []
-        if props == FULL_PROPS:
-            has_rest = True
-        elif props == DC_PROPS:
-            has_rest = False
-            warnings.append("load_ply: f_rest_* properties missing; higher-order SH set to zero")
-        else:
+        if schema is None:
             raise RuntimeError("load_ply: unknown property layout; expected [" + ",".join(FULL_PROPS) +
                                "] (or the f_rest-free variant), found [" + ",".join(props) + "]")
-        start = f.tell()
-        stride = len(props)
-        data = f.read(count * stride * 4)
-    if len(data) != count * stride * 4:
-        full = len(data) // (stride * 4)
-        raise RuntimeError(f"load_ply: truncated payload at byte offset {start + len(data)}"
-                           if full < count else "load_ply: truncated payload")
-    rows = np.frombuffer(data, "<f4").reshape(count, stride).astype(np.float32)
-    sh = np.zeros((count, 3, 16), np.float32)
-    sh[:, :, 0] = rows[:, 6:9]
-    k = 9
-    if has_rest:
-        sh[:, :, 1:] = rows[:, 9:54].reshape(count, 3, 15)
-        k = 54
-    scene = Scene(np.ascontiguousarray(rows[:, 0:3]), np.ascontiguousarray(rows[:, k + 4:k + 8]),
-                  np.ascontiguousarray(rows[:, k + 1:k + 4]), np.ascontiguousarray(rows[:, k]),
-                  np.ascontiguousarray(sh.reshape(count, 48)), np.zeros(3, np.float32))
+        want = count * len(schema) * 4
+        data = f.read(want)
+    if len(data) != want:
+        raise RuntimeError(f"load_ply: truncated payload at byte offset {start + len(data)}")
+    block = np.frombuffer(data, "<f4").reshape(count, len(schema))
+    out = {k: np.zeros((count, w), np.float32) for k, w in _WIDTH.items()}
+    for col, (_, field, comp) in enumerate(schema):
+        if field is not None:
+            out[field][:, comp] = block[:, col]
+    scene = Scene(out["mean"], out["rotation"], out["log_scale"], np.ascontiguousarray(out["opacity"][:, 0]),
+                  out["sh"], np.zeros(3, np.float32))
     return scene, warnings
 
 
