@@ -176,6 +176,9 @@ def run_ours(args, ws, rank, local):
     # one drains (~17 us per forward at config 2), so the other steps run unperturbed.
     stage_every = 8
 
+    scene_bytes = scene.n * (236 if deg == 3 else 56)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if scene_bytes < 126e6 else None
+
     def timed(fn, steps, warmup, sampler=None):
         r.set_flags(0)
         for _ in range(warmup):
@@ -187,19 +190,30 @@ def run_ours(args, ws, rank, local):
         r.timing(reset=True)
         if sampler:
             sampler.sample()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(steps):
-            r.set_flags(_lib.FGS_FLAG_TIMING if i % stage_every == 0 else 0)
-            fn()
-        e1.record(stream)
+        if flush is None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(steps):
+                r.set_flags(_lib.FGS_FLAG_TIMING if i % stage_every == 0 else 0)
+                fn()
+            e1.record(stream)
+        else:
+            # scene smaller than the L2: L2 flushed (a 256 MB write) before every step, each step
+            # timed by its own event pair so the flush is not counted
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for i in range(steps):
+                flush.zero_()
+                r.set_flags(_lib.FGS_FLAG_TIMING if i % stage_every == 0 else 0)
+                ev[i][0].record(stream)
+                fn()
+                ev[i][1].record(stream)
         r.set_flags(0)
         torch.cuda.synchronize()
         if sampler:
             sampler.sample()
         if dist is not None:
             dist.barrier()
-        ms = e0.elapsed_time(e1) / steps
+        ms = (e0.elapsed_time(e1) if flush is None else sum(a.elapsed_time(b) for a, b in ev)) / steps
         if dist is not None:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -208,9 +222,7 @@ def run_ours(args, ws, rank, local):
 
     clk = ClockSampler(local)
     with clk:
-        # at least 8 warm-up steps: the library settles its per-context launch-variant timing
-        # (both blend work decompositions are timed on a context's first frames)
-        ms, tim = timed(primary, args.steps, max(8, args.warmup), clk)
+        ms, tim = timed(primary, args.steps, args.warmup, clk)
     launches = tim["launches"]
     # fwd+bwd of the first view (secondary number for forward-only workloads)
     ms_fb, tim_fb = timed(lambda: fwd_bwd_views([0]), max(5, args.steps // 4), 3)
@@ -219,6 +231,10 @@ def run_ours(args, ws, rank, local):
     # work counters and stats of the measured view (instrumented run, outside the timed region)
     r.set_flags(_lib.FGS_FLAG_COUNTERS)
     _, st = r.forward(ds, cam, ropt, image=image, want_stats=True)
+    r.backward(ds, cam, dl_dev[0], bopt, grads=grads)
+    vv = r.debug("variants").tolist()
+    variants = {"fwd_pixels_per_lane": vv[0], "bwd_pixels_per_lane": vv[1], "k4b_ctas_per_sm": vv[2],
+                "longest_tile_list": vv[3], "rule": "deterministic from frame statistics (fgs_api.cu rule_*)"}
     counters_all = r.debug("counters", np.uint64).tolist()
     counters = counters_all[:2]
     r.set_flags(0)
@@ -254,12 +270,18 @@ def run_ours(args, ws, rank, local):
                             "frac": round(ach / pk, 4), "ms": round(t_ms, 4), "work": int(amount)}
     primary_stages = ["preprocess", "binning+sort", "raster"] + ([] if FWD_ONLY[cfg] else
                                                                     ["raster_backward", "preprocess_backward"])
-    dom = max((k for k in primary_stages if k in rooflines), key=lambda k: rooflines[k]["ms"])
-    roof = dict(rooflines[dom])
-    roof["kernel"] = dom
-    roof["traffic"] = load_traffic(dom)
-    roof["peak_source"] = ("fp32 probe kernel on this device (FMUL+FADD, non-FMA ops)" if roof["bound"] == "fp32"
-                           else f"MEASURED_PEAKS.json hbm_gbs ({peak_src})")
+    def dominant(stages):
+        dom = max((k for k in stages if k in rooflines), key=lambda k: rooflines[k]["ms"])
+        roof = dict(rooflines[dom])
+        roof["kernel"] = dom
+        roof["traffic"] = load_traffic(dom)
+        roof["peak_source"] = ("fp32 probe kernel on this device (FMUL+FADD, non-FMA ops)" if roof["bound"] == "fp32"
+                               else f"MEASURED_PEAKS.json hbm_gbs ({peak_src})")
+        return roof
+
+    roof = dominant(primary_stages)
+    # the metric's second half (fwd+bwd views/s): dominant stage of forward + backward
+    roof_fb = dominant(["preprocess", "binning+sort", "raster", "raster_backward", "preprocess_backward"])
 
     # e2e through the reference-facing host call (pinned host buffers, copies in the timed region)
     e2e = None
@@ -292,9 +314,12 @@ def run_ours(args, ws, rank, local):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms_e2e, 3),
                "path": "fgs_render_host" + ("" if FWD_ONLY[cfg] else " + fgs_backward_host")}
 
-    cpu = None
+    cpu = cpu_fb = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, scene, deg, cams, dls, args.cpu_seconds)
+        # the reference backward (gradients.hpp:207-267) timed too: forward+backward views/s
+        cpu_fb = cpu if not FWD_ONLY[cfg] else cpu_baseline(cfg, scene, deg, cams, dls, args.cpu_seconds,
+                                                            fwd_only=False)
 
     value = ws * views_per_step * 1000.0 / ms
     unit = "FPS" if cfg in (0, 2) else "views/s"
@@ -304,22 +329,20 @@ def run_ours(args, ws, rank, local):
         "unit": unit,
         "n_gpus": ws,
         "steps": args.steps,
-        "warmup": max(8, args.warmup),
+        "warmup": args.warmup,
         "ms_per_step": round(ms, 4),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": f"synthetic: seeded numpy draws of BASELINE.json config {cfg} (no dataset)",
-        "config": {"workload": args.workload, "gaussians": scene.n, "sh_degree": deg, "width": cam.width,
-                   "height": cam.height, "views_per_rank": views_per_step,
-                   "step": "forward" if FWD_ONLY[cfg] else "forward+backward",
-                   "parallelism": f"camera-partitioned x{ws}" + (", NCCL all-reduce of 59N grads" if cfg == 4 else ""),
-                   "l2": "no flush: the %.0f MB of Gaussian parameters read per step exceed the 126 MB L2"
-                         % (scene.n * 236 / 1e6)},
+        "config": bench_config(args, cfg, scene, deg, cam, views_per_step, ws),
         "e2e": e2e,
         "roofline": roof,
+        "roofline_fwd_bwd": roof_fb,
         "cpu_baseline": cpu,
+        "cpu_baseline_fwd_bwd": cpu_fb,
+        "variants": variants,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "fwd_bwd_views_per_s": round(ws * 1000.0 / ms_fb, 2),
@@ -336,6 +359,27 @@ def run_ours(args, ws, rank, local):
         print(json.dumps(res))
     if dist is not None:
         dist.destroy_process_group()
+
+
+def views_per_rank(cfg, n_views, ws):
+    from paper_2409_04751_b200 import multiview
+
+    if cfg == 3:
+        return len(multiview.partition_views(n_views, ws, 0))
+    return n_views if cfg == 4 else 1
+
+
+def bench_config(args, cfg, scene, deg, cam, views_per_step, ws):
+    """The workload description both arms print (identical dicts)."""
+    sb = scene.n * (236 if deg == 3 else 56)
+    return {"workload": args.workload, "gaussians": scene.n, "sh_degree": deg, "width": cam.width,
+            "height": cam.height, "views_per_rank": views_per_step,
+            "step": "forward" if FWD_ONLY[cfg] else "forward+backward",
+            "parallelism": f"camera-partitioned x{ws}" + (", NCCL all-reduce of 59N grads" if cfg == 4 else ""),
+            "l2": ("no flush: the %.0f MB of Gaussian parameters read per step exceed the 126 MB L2" % (sb / 1e6)
+                   if sb >= 126e6 else
+                   "L2 flushed (256 MB write) before every timed step, outside its event pair: the %.1f MB scene "
+                   "fits the 126 MB L2" % (sb / 1e6))}
 
 
 def load_traffic(kernel):
@@ -368,11 +412,15 @@ def cpu_impl():
     return "reference" if oracle.ref_available() else "port"
 
 
-def cpu_baseline(cfg, scene, deg, cams, dls, budget_s):
-    """The reference's CPU path on this host's cores, one bounded sample (~budget_s of work)."""
+def cpu_baseline(cfg, scene, deg, cams, dls, budget_s, fwd_only=None):
+    """The reference's CPU path on this host's cores, one bounded sample (~budget_s of work).
+    fwd_only=False times forward + backward (the reference's backward needs dL/dpixel: the
+    config's own, or a seeded N(0, 1) image for the forward-only configs)."""
     impl = cpu_impl()
     threads = os.cpu_count() or 1
-    fwd_only = FWD_ONLY[cfg]
+    fwd_only = FWD_ONLY[cfg] if fwd_only is None else fwd_only
+    if not fwd_only and not dls:
+        dls = [np.random.default_rng(7).standard_normal((cams[0].height, cams[0].width, 3)).astype(np.float32)]
     dl = dls[0] if dls else None
     t0 = time.perf_counter()
     _cpu_frame(impl, scene, deg, cams[0], dl, fwd_only, threads)  # warm-up (page-in, thread spawn)
@@ -387,7 +435,7 @@ def cpu_baseline(cfg, scene, deg, cams, dls, budget_s):
         if first > budget_s:
             break
     v = frames / sum(times)
-    return {"value": round(v, 4), "unit": "FPS" if fwd_only and cfg in (0, 2) else "views/s", "cores": threads,
+    return {"value": round(v, 4), "unit": "FPS" if fwd_only else "views/s", "cores": threads,
             "kind": impl, "sample": f"{frames} full {'forward' if fwd_only else 'forward+backward'} view(s) of the "
                                     f"same workload, fp32, {threads} threads (median {np.median(times):.2f} s/view)"}
 
@@ -400,8 +448,12 @@ def run_reference(args, ws, rank):
     impl = cpu_impl()
     threads = os.cpu_count() or 1
     fwd_only = FWD_ONLY[cfg]
-    for _ in range(min(args.warmup, 1)):
+    warm, t_w = 0, time.perf_counter()
+    for _ in range(args.warmup):  # all W warm-up steps unless they exceed a minute
         _cpu_frame(impl, scene, deg, cams[0], dls[0] if dls else None, fwd_only, threads)
+        warm += 1
+        if time.perf_counter() - t_w > 60.0:
+            break
     times, steps = [], 0
     t_start = time.perf_counter()
     for i in range(args.steps):
@@ -415,7 +467,7 @@ def run_reference(args, ws, rank):
     v = round(1000.0 / ms, 4)
     unit = "FPS" if fwd_only and cfg in (0, 2) else "views/s"
     sample = (f"{steps} of {args.steps} requested steps (150 s cap), each one full "
-              f"{'forward' if fwd_only else 'forward+backward'} view; {threads} threads")
+              f"{'forward' if fwd_only else 'forward+backward'} view (views/s is per view); {threads} threads")
     res = {
         "impl": "reference",
         "metric": METRIC,
@@ -423,16 +475,14 @@ def run_reference(args, ws, rank):
         "unit": unit,
         "n_gpus": ws,
         "steps": steps,
-        "warmup": min(args.warmup, 1),
+        "warmup": warm,
         "ms_per_step": round(ms, 2),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": f"synthetic: seeded numpy draws of BASELINE.json config {cfg} (no dataset)",
-        "config": {"workload": args.workload, "gaussians": scene.n, "sh_degree": deg, "width": cams[0].width,
-                   "height": cams[0].height, "views_per_rank": 1,
-                   "step": "forward" if fwd_only else "forward+backward"},
+        "config": bench_config(args, cfg, scene, deg, cams[0], views_per_rank(cfg, len(cams), ws), ws),
         "cpu_baseline": {"kind": impl, "cores": threads, "sample": sample, "value": v, "unit": unit},
         "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

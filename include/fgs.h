@@ -152,7 +152,9 @@ int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s);
  *   "key_tile"/"key_depth"/"key_gauss" u32[I] (pre-sort keys in the reference's emission order),
  *   "sorted_gauss" u32[I], "sorted_tile" u32[I], "offsets" u32[T+1] (tile ranges),
  *   "keys" u64[I] (depth key << 32 | Gaussian id, as the binning scatter wrote them into each tile's
- *   range), "rect" u16[N*4] (tile rectangle tx0, tx1, ty0, ty1 per Gaussian),
+ *   range), "rect" u16[N*4] (tile rectangle tx0, tx1, ty0, ty1 per Gaussian), "variants" u32[4]
+ *   (forward pixels per lane, backward pixels per lane, K4b CTAs per SM, longest tile list),
+ *   "aux_bytes" u64[1] (device bytes the render/backward path holds, backward scratch included),
  *   "compact_gauss"/"compact_offsets" u32[M], "final_T" f32[H*W], "last" u32[H*W],
  *   "counters" u64[4] (E_eval, E_contrib, culled evaluations, max CTA cycles; with
  *   FGS_FLAG_COUNTERS), "counters16" u64[16], "bin_trace" u64[8], "tile_cycles" u64[T],

@@ -125,7 +125,7 @@ __device__ void row_counts(const BinArgs& a, int ty, uint32_t* hist, uint32_t* r
   const int lane = threadIdx.x & 31, rw = a.tiles_x + 1;
   const uint32_t lt = lanemask_lt();
   int32_t* rd = a.rowdiff + static_cast<size_t>(ty) * rw;
-  uint32_t carry = 0, tot = 0, segs = 0;
+  uint32_t carry = 0, tot = 0, segs = 0, longest = 0;
   for (int c0 = 0; c0 < rw; c0 += 32 * kRowItems) {
     int32_t v[kRowItems];
     int32_t sum = 0;
@@ -152,6 +152,7 @@ __device__ void row_counts(const BinArgs& a, int ty, uint32_t* hist, uint32_t* r
         a.fill[static_cast<size_t>(ty) * a.tiles_x + x] = run;
         tot += run;
         if (run > kSeg) segs += (run + kSeg - 1) / kSeg;  // the backward's segments of a long list
+        longest = max(longest, run);
       }
       const int bk = cell ? sched_bucket(run) : 31;
       const uint32_t peers = __match_any_sync(0xffffffffu, bk);
@@ -164,9 +165,11 @@ __device__ void row_counts(const BinArgs& a, int ty, uint32_t* hist, uint32_t* r
     tot += __shfl_xor_sync(0xffffffffu, tot, o);
     segs += __shfl_xor_sync(0xffffffffu, segs, o);
   }
+  longest = __reduce_max_sync(0xffffffffu, longest);
   if (lane == 0) {
     rowtot[ty] = tot;
     if (segs) atomicAdd(a.scalars + kScalarSegs, segs);
+    if (longest) atomicMax(a.scalars + kScalarMaxList, longest);
   }
 }
 

@@ -51,78 +51,37 @@ struct DevBuf {  // owning device allocation that only grows (freed on destructi
 
 }  // namespace
 
-// Autotuning between two launch variants with identical results (forward: pixels per lane;
-// backward blend and K4b: register / occupancy variants): the first frames of a context time both work
-// decompositions (CUDA events around the launch, read back without blocking on a later frame,
-// normalised by the frame's intersection count since views differ in cost) and keep the
-// faster; a >2x change in the intersection count starts over. Results do not depend
-// on the choice (each pixel's blend is the same sequence of operations).
-struct PxTuner {
-  cudaEvent_t a[3] = {}, b[3] = {};  // per pixels-per-lane value (1, 2)
-  bool pending[3] = {false, false, false};
-  int64_t work[3] = {0, 0, 0};        // intersections of the timed frame (views differ in cost)
-  float best[3] = {0.0f, 0.0f, 0.0f};
-  int samples[3] = {0, 0, 0};
-  int choice = 0;
-  int64_t ref = 0;
-  int timing = 0;  // px of the launch being issued (between pick and done)
-  static constexpr int kSamples = 3;
-  void create() {
-    for (int p = 1; p <= 2; ++p) {
-      cudaEventCreate(&a[p]);
-      cudaEventCreate(&b[p]);
-    }
-  }
-  void destroy() {
-    for (int p = 1; p <= 2; ++p) {
-      if (a[p]) cudaEventDestroy(a[p]);
-      if (b[p]) cudaEventDestroy(b[p]);
-    }
-  }
-  void reset() {
-    pending[1] = pending[2] = false;
-    samples[1] = samples[2] = 0;
-    choice = 0;
-  }
-  void collect(int64_t isect) {
-    for (int p = 1; p <= 2; ++p) {
-      if (!pending[p] || cudaEventQuery(b[p]) != cudaSuccess) continue;
-      float ms = 0.0f;
-      if (cudaEventElapsedTime(&ms, a[p], b[p]) == cudaSuccess && work[p] > 0) {
-        const float per = ms / static_cast<float>(work[p]);  // time per intersection
-        best[p] = samples[p] ? std::min(best[p], per) : per;
-        ++samples[p];
-      }
-      pending[p] = false;
-    }
-    if (!choice && samples[1] >= kSamples && samples[2] >= kSamples) {
-      choice = best[1] <= best[2] ? 1 : 2;
-      ref = isect;
-    }
-  }
-  // pixels per lane for this launch (0: the kernel's own rule); records the start event when timed
-  int pick(int64_t isect, cudaStream_t st) {
-    timing = 0;
-    if (!a[1] || isect <= 0) return 0;
-    if (choice && (isect > 2 * ref || 2 * isect < ref)) reset();
-    collect(isect);
-    if (choice) return choice;
-    int p = samples[1] <= samples[2] ? 1 : 2;
-    if (pending[p]) p = 3 - p;
-    if (pending[p]) return 0;
-    cudaEventRecord(a[p], st);
-    work[p] = isect;
-    timing = p;
-    return p;
-  }
-  void done(cudaStream_t st) {
-    if (!timing) return;
-    cudaEventRecord(b[timing], st);
-    pending[timing] = true;
-    timing = 0;
-  }
-  void drop() { pending[1] = pending[2] = false; }
-};
+// Launch-variant rules. Where two work decompositions give identical results, the choice is a
+// deterministic function of the frame's statistics (no timing-based tuning, so a run's numbers
+// reproduce): the intersection count I, the tile count T and the longest tile list. Measured
+// at the BASELINE configs (profiles/r02_variants.md):
+//   forward blend, pixels per lane: 2 amortises the per-splat work over twice the pixels and
+//     wins on even lists (configs 1, 3, 4); a heavy-tailed frame (longest list > 8x the mean and
+//     > 512, config 2) is bound by its longest lists, which 1 pixel per lane spreads over twice
+//     the warps;
+//   both blends take 1 pixel per lane on small images (< 1024 tiles, config 0: fewer CTAs than
+//     a few waves over the 148 SMs);
+//   backward blend: 2 pixels per lane from 32 entries per tile on average, at 6 CTAs per SM;
+//   K4b: 6 CTAs per SM (80 registers) for scenes with > 1M tile-touching Gaussians, else 4 (85).
+// FGS_FWD_PX / FGS_BWD_PX / FGS_BWD_MINB / FGS_K4B_MINB override (profiling).
+namespace {
+int env_int(const char* name) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : 0;
+}
+int rule_fwd_px(int64_t I, int64_t tiles, int64_t longest) {
+  static const int e = env_int("FGS_FWD_PX");
+  if (e == 1 || e == 2) return e;
+  const int64_t mean = tiles > 0 ? I / tiles : 0;
+  if (tiles < 1024) return 1;  // a small image: fewer CTAs than a few waves, use every warp
+  return (longest > 512 && longest > 8 * std::max<int64_t>(mean, 1)) ? 1 : 2;
+}
+int rule_k4b_minb(int64_t m) {
+  static const int e = env_int("FGS_K4B_MINB");
+  if (e == 4 || e == 6) return e;
+  return m > 1000000 ? 6 : 4;
+}
+}  // namespace
 
 struct fgs_context {
   int device = 0;
@@ -157,14 +116,13 @@ struct fgs_context {
   cudaEvent_t ev_scan = nullptr;  // after K2a's scalars reached the host
   cudaEvent_t ev_k2 = nullptr;    // K2 done on the caller's stream
   cudaStream_t aux = nullptr;     // the scalars' readback, off the caller's stream so K3 follows K2 directly
-  PxTuner fwd_px;
+  uint32_t longest = 0;     // longest tile list of the last forward
+  int var_fwd_px = 0, var_bwd_px = 0, var_k4b = 0;  // launch variants of the last calls (reported)
   // The device scalars alternate between two 16-word halves by frame parity; a frame's K3 zeroes
   // the other half for the next frame (whose previous readback finished before this frame began),
   // so no memset precedes K1. scalars_clean[h]: half h is known to be zero.
   int64_t frame = 0;
   bool scalars_clean[2] = {true, true};
-  PxTuner bwd_var;  // backward blend occupancy variant (same results)
-  PxTuner k4b_var;  // K4b register-fit variant (same results)
   DevBuf<float> final_T;
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
@@ -344,9 +302,6 @@ int fgs_create(int device, fgs_context** out) {
   cudaEventCreateWithFlags(&ctx->ev_scan, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_k2, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
-  ctx->fwd_px.create();
-  ctx->bwd_var.create();
-  ctx->k4b_var.create();
   if (ctx->scalars.ensure(32) != cudaSuccess || cudaMemset(ctx->scalars.p, 0, 32 * sizeof(uint32_t)) != cudaSuccess || ctx->counters.ensure(24) != cudaSuccess ||
       false) {
     fgs_destroy(ctx);
@@ -386,9 +341,6 @@ int fgs_destroy(fgs_context* ctx) {
     if (ev) cudaEventDestroy(ev);
   if (ctx->ev_scan) cudaEventDestroy(ctx->ev_scan);
   if (ctx->ev_k2) cudaEventDestroy(ctx->ev_k2);
-  ctx->fwd_px.destroy();
-  ctx->bwd_var.destroy();
-  ctx->k4b_var.destroy();
   if (ctx->aux) {
     cudaStreamSynchronize(ctx->aux);
     cudaStreamDestroy(ctx->aux);
@@ -580,7 +532,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     FGS_CHECK(cudaEventRecord(ctx->ev_k2, st));
     FGS_CHECK(cudaStreamWaitEvent(rb, ctx->ev_k2, 0));
   }
-  FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, scalars, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, rb));
+  FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, scalars, fgs::kScalarReadback * sizeof(uint32_t), cudaMemcpyDeviceToHost, rb));
   FGS_CHECK(cudaEventRecord(ctx->ev_scan, rb));
   if (timing) cudaEventRecord(ev[2], st);  // (no separate sort stage: K3 sorts each tile's list)
 
@@ -622,10 +574,10 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     ba.ckpt_cap = ctx->ckpt_cap;
     ba.keys = ctx->keys.p;
     ba.sorted_gauss = ctx->sorted_gauss.p;
-    // density hint for the work decomposition: this frame's I once known, else the last frame's
-    const int px = (ctx->flags & FGS_FLAG_COUNTERS) ? 0 : ctx->fwd_px.pick(ctx->num_isect, st);
+    // work decomposition from this frame's statistics once known, else the last frame's
+    const int px = rule_fwd_px(ctx->num_isect, num_tiles, ctx->longest);
+    ctx->var_fwd_px = px;
     const int l = fgs::blend_forward(ba, ctx->num_isect, px, st);
-    ctx->fwd_px.done(st);
     ctx->scalars_clean[1 - half] = true;  // K3 zeroes the other half
     if (timing) cudaEventRecord(ev[4], st);
     return l;
@@ -646,17 +598,16 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ctx->num_culled = static_cast<uint32_t>(n) - ctx->num_splats - ctx->num_degenerate;
   if (I >= (int64_t(1) << 30)) return fail(ctx, FGS_ENOMEM, "forward: intersection count exceeds 2^30");
   const int64_t X = ctx->h_scalars[fgs::kScalarSegs];
+  ctx->longest = ctx->h_scalars[fgs::kScalarMaxList];
   ctx->num_segs = X;
   if (speculative && I <= ctx->isect_cap && X > ctx->ckpt_cap) {
     // only the checkpoint slots ran short: the speculative K3 exited; grow them and blend again
-    ctx->fwd_px.drop();
     FGS_CHECK(ensure_ckpt(ctx, X));
     FGS_CHECK(cudaMemsetAsync(scalars + fgs::kScalarSegPos, 0, sizeof(uint32_t), st));
     launches += launch_blend();
   } else if (!speculative || I > ctx->isect_cap) {
     FGS_CHECK(ensure_ckpt(ctx, X));
     FGS_CHECK(cudaMemsetAsync(scalars + fgs::kScalarSegPos, 0, sizeof(uint32_t), st));
-    ctx->fwd_px.drop();  // the timed launch (if any) exited without work
     // (re)size the per-intersection buffers (cudaFree / cudaMalloc synchronise with the
     // speculative kernels, which exited without work) and launch for real
     const size_t ni = static_cast<size_t>(I > 0 ? I : 1);
@@ -757,9 +708,7 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   SetGuard guard{ctx, timing};
   if (timing) cudaEventRecord(ev[0], st);
   if (I > 0) {
-    const int var = ctx->bwd_var.pick(I, st);
-    ctx->launches += fgs::blend_backward(ba, I, var, st);
-    ctx->bwd_var.done(st);
+    ctx->launches += fgs::blend_backward(ba, I, 0, st, &ctx->var_bwd_px);
   }
   if (timing) cudaEventRecord(ev[1], st);
 
@@ -791,9 +740,8 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.cval = ctx->cval.p;
   pb.rec = ctx->rec.p;
   if (n > 0 && (pb.m > 0 || !pb.accumulate)) {
-    const int var = ctx->scene_on_host ? 0 : ctx->k4b_var.pick(ctx->num_isect, st);
-    fgs::preprocess_backward_launch(pb, ctx->scene_on_host, var, st);
-    if (!ctx->scene_on_host) ctx->k4b_var.done(st);
+    ctx->var_k4b = ctx->scene_on_host ? 6 : rule_k4b_minb(pb.m);
+    fgs::preprocess_backward_launch(pb, ctx->scene_on_host, ctx->var_k4b == 4 ? 2 : 1, st);
     ++ctx->launches;
   }
   if (timing) cudaEventRecord(ev[2], st);
@@ -1137,6 +1085,21 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
     return static_cast<int64_t>(I * 4);
   }
   if (nm == "offsets") return copy(ctx->tile_offsets.p, (nt + 1) * 4);
+  if (nm == "variants") {  // launch variants of the last forward / backward, longest tile list
+    const uint32_t v[4] = {static_cast<uint32_t>(ctx->var_fwd_px), static_cast<uint32_t>(ctx->var_bwd_px),
+                           static_cast<uint32_t>(ctx->var_k4b), ctx->longest};
+    if (!dst) return sizeof(v);
+    if (dst_bytes < static_cast<int64_t>(sizeof(v))) return -1;
+    std::memcpy(dst, v, sizeof(v));
+    return sizeof(v);
+  }
+  if (nm == "aux_bytes") {  // device bytes the path holds (RenderStats::peak_aux_bytes, incl. backward scratch)
+    const uint64_t v = path_bytes(ctx);
+    if (!dst) return sizeof(v);
+    if (dst_bytes < static_cast<int64_t>(sizeof(v))) return -1;
+    std::memcpy(dst, &v, sizeof(v));
+    return sizeof(v);
+  }
   if (nm == "final_T") return copy(ctx->final_T.p, npix * 4);
   if (nm == "last") return copy(ctx->last.p, npix * 4);
   if (nm == "counters") return copy(ctx->counters.p, 4 * sizeof(unsigned long long));

@@ -101,7 +101,9 @@ constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per 
 constexpr int kBinThreads = 1024;
 constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, kScalarM = 4, kScalarI2 = 5, kScalarBig = 6,
               kScalarSegs = 7,    // backward segment slots of the frame (K2: sum over long lists of ceil(L / kSeg))
-              kScalarSegPos = 8;  // K3's slot allocation cursor
+              kScalarSegPos = 8,  // K3's slot allocation cursor
+              kScalarMaxList = 9; // longest tile list of the frame (K2)
+constexpr int kScalarReadback = 10;  // scalars the host reads after K2
 
 // Backward segments: a tile list longer than kSeg entries is split into ceil(L / kSeg) segments
 // that the blend backward processes as independent CTAs; the forward leaves each pixel's state
@@ -143,7 +145,7 @@ cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* ke
 
 // ---- blend (raster.cu) ----
 int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStream_t st);
-int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStream_t st);
+int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStream_t st, int* px_used = nullptr);
 // ---- training step (train.cu) ----
 // L1 + D-SSIM loss and dL/drendered (inc/metrics.hpp:86-195). maps: loss_scratch_floats();
 // partials: 2 * loss_partials() + 2 doubles, the last two = (sum of SSIM map, sum |x - y|).

@@ -625,20 +625,12 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStr
     return 1;
   });
   // 2 pixels per lane (4 warps of 8x8 blocks) amortise the per-splat work and idle fewer warps
-  // while a CTA sorts its list; 1 pixel per lane (8x4 blocks) culls and terminates finer. Which
-  // wins depends on the scene, not only on the list lengths (config 1: 2 by 18%; the
-  // heavy-tailed config 2: 1 by 22%), so the caller times both (px_request); without a request
-  // dense lists take 2. The choice only changes the work decomposition, never a pixel's value.
-  // FGS_FWD_PX overrides.
-  static const int env = [] {
-    const char* v = std::getenv("FGS_FWD_PX");
-    return v ? std::atoi(v) : 0;
-  }();
+  // while a CTA sorts its list; 1 pixel per lane (8x4 blocks) culls and terminates finer and
+  // gives a long list twice the warps. The caller picks (fgs_api.cu, rule_fwd_px); the choice only
+  // changes the work decomposition, never a pixel's value.
+  (void)num_isect;
   const int tiles = a.tiles_x * a.tiles_y;
-  const int px = env == 1 || env == 2 ? env
-                 : px_request == 1 || px_request == 2
-                     ? px_request
-                     : (num_isect >= 256 * static_cast<int64_t>(tiles) ? 2 : 1);
+  const int px = px_request == 1 ? 1 : 2;
   if (px == 1) {
     if (a.counters) blend_forward_kernel<true, 1><<<tiles, 256, 0, st>>>(a);
     else blend_forward_kernel<false, 1><<<tiles, 256, 0, st>>>(a);
@@ -649,25 +641,26 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStr
   return 1;
 }
 
-int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStream_t st) {
-  // 8x8 warp blocks with 2 pixels per lane amortise the per-splat overhead (chunk staging,
-  // culling, the 27-value warp reduction) over twice the pixels; with the exact ellipse culling
-  // that wins from ~30 entries per tile up (measured: config 1 0.19 -> 0.16 ms, config 2
-  // 0.345 -> 0.313 ms, config 4), while the sparse config 0 keeps 8x4 blocks.
-  // FGS_BWD_PX=1|2 overrides.
+int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStream_t st, int* px_used) {
+  // 8x8 warp blocks with 2 pixels per lane amortise the per-splat overhead (culling, the
+  // 27-value warp reduction) over twice the pixels: faster from ~32 entries per tile on average
+  // (profiles/r02_variants.md: configs 1-4), while a small image (config 0: 256 tiles) keeps 8x4
+  // blocks and twice the warps. FGS_BWD_PX=1|2 overrides.
   static const int env = [] {
     const char* v = std::getenv("FGS_BWD_PX");
     return v ? std::atoi(v) : 0;
   }();
   const int tiles = a.tiles_x * a.tiles_y;
-  const int px = env == 1 || env == 2 ? env : (num_isect >= 32 * static_cast<int64_t>(tiles) ? 2 : 1);
-  // 2 pixels per lane: fitted to 6 CTAs per SM (72 registers, no spills) or 8 (64); identical
-  // results. FGS_BWD_MINB=6|8 overrides the variant.
+  const int px = env == 1 || env == 2 ? env
+                 : (tiles >= 1024 && num_isect >= 32 * static_cast<int64_t>(tiles) ? 2 : 1);
+  // 2 pixels per lane: fitted to 6 CTAs per SM (72 registers, no spills; measured faster at
+  // configs 1, 2 and 4) or 8 (64, spills); identical results. FGS_BWD_MINB=6|8 overrides.
   static const int env_minb = [] {
     const char* v = std::getenv("FGS_BWD_MINB");
     return v ? std::atoi(v) : 0;
   }();
   const int minb = env_minb == 6 || env_minb == 8 ? env_minb : (variant == 2 ? 8 : 6);
+  if (px_used) *px_used = px;
   // one CTA per (tile, segment): the long lists' segments k >= 1 first, then every tile's first
   const int grid = tiles + static_cast<int>(a.num_seg_items);
   if (px == 1) blend_backward_kernel<1, 4><<<grid, 256, 0, st>>>(a);
