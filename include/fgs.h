@@ -127,13 +127,34 @@ int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_came
 int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                       const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
 
+/* A scene in array-of-structures form: n records of `stride` bytes in host memory, each holding
+ * the float fields at the given byte offsets -- e.g. the reference's std::vector<Gaussian3D<float>>
+ * (inc/model.hpp:18-36: mean 3, rotation 4 (w,x,y,z), log_scale 3, opacity_logit 1, sh 48 =
+ * ShCoeffs column-major [channel*16 + basis]), described with offsetof() (include/fgs_omnisplat.hpp). */
+typedef struct fgs_gaussians_aos {
+  int64_t n;
+  const void* data;
+  int64_t stride;
+  int64_t off_mean, off_rotation, off_log_scale, off_opacity_logit, off_sh;
+} fgs_gaussians_aos;
+
+/* fgs_render_host / fgs_backward_host for an AoS scene: the records go to the device in one
+ * transfer and a gather kernel splits them into the structure-of-arrays layout. */
+int fgs_render_host_aos(fgs_context* ctx, const fgs_gaussians_aos* scene, const fgs_camera* camera,
+                        const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats);
+int fgs_backward_host_aos(fgs_context* ctx, const fgs_gaussians_aos* scene, const fgs_camera* camera,
+                          const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
+
 /* PCIe bytes moved by the last fgs_render_host / fgs_backward_host call: out = {h2d, d2h}. */
 int fgs_last_transfer(const fgs_context* ctx, uint64_t out[2]);
 
 /* Flags: FGS_FLAG_COUNTERS makes the forward blend count E_eval / E_contrib (atomics; slower)
  * and records the binning phase trace; FGS_FLAG_TIMING records CUDA events around every stage
- * (read with fgs_timing). FGS_FLAG_KEEP_KEYS is reserved (no effect). Default 0. */
-enum { FGS_FLAG_COUNTERS = 1, FGS_FLAG_KEEP_KEYS = 2, FGS_FLAG_TIMING = 4 };
+ * (read with fgs_timing). FGS_FLAG_BLEND_COUNT makes the forward also write the per-pixel
+ * contribution count (ForwardContext::blend_count, inc/splatting.hpp:299-301; debug name
+ * "blend_count", u16[H*W]; also written with FGS_FLAG_COUNTERS). FGS_FLAG_KEEP_KEYS is reserved
+ * (no effect). Default 0. */
+enum { FGS_FLAG_COUNTERS = 1, FGS_FLAG_KEEP_KEYS = 2, FGS_FLAG_TIMING = 4, FGS_FLAG_BLEND_COUNT = 8 };
 int fgs_set_flags(fgs_context* ctx, uint32_t flags);
 
 /* Device time per stage accumulated from CUDA events while FGS_FLAG_TIMING is set, and the

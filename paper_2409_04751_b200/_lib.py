@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfgs.so")
 
 FGS_OK, FGS_EINVAL, FGS_EDEGENERATE_QUAT, FGS_ECUDA, FGS_ENOMEM, FGS_ESTATE, FGS_ENONFINITE = range(7)
-FGS_FLAG_COUNTERS, FGS_FLAG_KEEP_KEYS, FGS_FLAG_TIMING = 1, 2, 4
+FGS_FLAG_COUNTERS, FGS_FLAG_KEEP_KEYS, FGS_FLAG_TIMING, FGS_FLAG_BLEND_COUNT = 1, 2, 4, 8
 
 
 class fgs_camera(C.Structure):
@@ -59,6 +59,12 @@ class fgs_adam_state(C.Structure):
     _fields_ = [("step", C.c_int64), ("m", fgs_gradients), ("v", fgs_gradients)]
 
 
+class fgs_gaussians_aos(C.Structure):
+    _fields_ = [("n", C.c_int64), ("data", C.c_void_p), ("stride", C.c_int64), ("off_mean", C.c_int64),
+                ("off_rotation", C.c_int64), ("off_log_scale", C.c_int64), ("off_opacity_logit", C.c_int64),
+                ("off_sh", C.c_int64)]
+
+
 class fgs_train_options(C.Structure):
     _fields_ = [("sh_degree", C.c_int32), ("background", C.c_float * 3), ("lam", C.c_float),
                 ("adam", fgs_adam_options)]
@@ -67,7 +73,8 @@ class fgs_train_options(C.Structure):
 EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs_forward", "fgs_backward",
            "fgs_render_host", "fgs_backward_host", "fgs_set_flags", "fgs_debug_get", "fgs_last_counts",
            "fgs_timing", "fgs_measure_fp32_peak", "fgs_l1_dssim_loss", "fgs_adam_step", "fgs_train_step",
-           "fgs_bruteforce_render", "fgs_bruteforce_render_f64", "fgs_last_transfer"]
+           "fgs_bruteforce_render", "fgs_bruteforce_render_f64", "fgs_last_transfer", "fgs_render_host_aos",
+           "fgs_backward_host_aos"]
 
 _lib = None
 
@@ -119,6 +126,12 @@ def load(path: str = LIB_PATH):
     L.fgs_bruteforce_render_f64.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, P(fgs_camera), C.c_int32,
                                             P(C.c_double), vp, vp]
     L.fgs_bruteforce_render_f64.restype = i32
+    L.fgs_render_host_aos.argtypes = [vp, P(fgs_gaussians_aos), P(fgs_camera), P(fgs_render_options), vp, vp,
+                                      P(fgs_stats)]
+    L.fgs_render_host_aos.restype = i32
+    L.fgs_backward_host_aos.argtypes = [vp, P(fgs_gaussians_aos), P(fgs_camera), vp, P(fgs_backward_options),
+                                        P(fgs_gradients)]
+    L.fgs_backward_host_aos.restype = i32
     L.fgs_last_transfer.argtypes = [vp, P(C.c_uint64)]
     L.fgs_last_transfer.restype = i32
     _lib = L

@@ -37,12 +37,21 @@ def _nvcc():
             return c
 
 
+def _programs_stale() -> bool:
+    inputs = [CLI_SRC, EXAMPLE_SRC, OUT] + [os.path.join(ROOT, "include", h) for h in
+                                            ("fgs.h", "fgs.hpp", "fgs_io.hpp", "fgs_omnisplat.hpp")]
+    newest = max(os.path.getmtime(p) for p in inputs if os.path.exists(p))
+    outs = [CLI_BIN, EXAMPLE_BIN]
+    if os.path.exists(os.path.join(REF_INC, "omnisplat", "splatting.hpp")):
+        outs += [o for _, o, _ in OMNI_PROGRAMS]
+        newest = max([newest] + [os.path.getmtime(s) for s, _, _ in OMNI_PROGRAMS])
+    return any(not os.path.exists(o) or os.path.getmtime(o) < newest for o in outs)
+
+
 def build(verbose=False, force=False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "fgs.h")]
-    if not force and os.path.exists(OUT) and (not os.path.exists(CLI_BIN) or
-                                              os.path.getmtime(CLI_BIN) < max(os.path.getmtime(CLI_SRC),
-                                              os.path.getmtime(os.path.join(ROOT, "include", "fgs_io.hpp")))):
+    if not force and os.path.exists(OUT) and _programs_stale():
         build_example(verbose)
     newest = max(os.path.getmtime(p) for p in deps)
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
@@ -64,9 +73,21 @@ def build(verbose=False, force=False) -> str:
     return OUT
 
 
+REF_INC = "/root/reference/proj/include"
+SHIM = os.path.join(ROOT, "oracle", "eigen_shim")
+# Programs written against the reference's own types (omnisplat::Scene / Camera / RenderResult)
+# through include/fgs_omnisplat.hpp: compiled only where the reference headers are mounted (this
+# container), against the repo's Eigen-subset shim; the binaries travel to the GPU box.
+OMNI_PROGRAMS = [(os.path.join(ROOT, "tools", "omnisplat_bench.cpp"), os.path.join(ROOT, "tools", "omnisplat_bench"),
+                  "$ORIGIN/../paper_2409_04751_b200"),
+                 (os.path.join(ROOT, "tests", "cpp", "omni_dropin_check.cpp"),
+                  os.path.join(ROOT, "tests", "cpp", "omni_dropin_check"), "$ORIGIN/../../paper_2409_04751_b200")]
+
+
 def build_example(verbose=False):
     """C++ host programs over include/fgs.hpp / fgs_io.hpp (the render example and the
-    reference-compatible CLI), linked against libfgs.so (rpath $ORIGIN/..)."""
+    reference-compatible CLI), linked against libfgs.so (rpath $ORIGIN/..); and, with the
+    reference headers mounted, the omnisplat-typed drop-in programs."""
     for src, out in ((EXAMPLE_SRC, EXAMPLE_BIN), (CLI_SRC, CLI_BIN)):
         if not os.path.exists(src):
             continue
@@ -75,6 +96,13 @@ def build_example(verbose=False):
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
+    if os.path.exists(os.path.join(REF_INC, "omnisplat", "splatting.hpp")):
+        for src, out, rpath in OMNI_PROGRAMS:
+            cmd = ["g++", "-O2", "-std=c++20", "-ffp-contract=off", "-isystem", SHIM, "-I" + REF_INC, "-o", out, src,
+                   "-L" + HERE, "-lfgs", "-Wl,-rpath," + rpath, "-lpthread"]
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.run(cmd, check=True)
     return EXAMPLE_BIN
 
 

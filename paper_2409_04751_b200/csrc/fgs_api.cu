@@ -124,6 +124,8 @@ struct fgs_context {
   int64_t frame = 0;
   bool scalars_clean[2] = {true, true};
   DevBuf<float> final_T;
+  DevBuf<uint16_t> blend_count;  // per pixel (FGS_FLAG_BLEND_COUNT)
+  bool have_blend_count = false;
   // misc device scalars: [0] total I, [1] error flag, [2..3] state counts, [4] compacted count M,
   // [5] scan tile counter
   DevBuf<uint32_t> scalars;
@@ -131,6 +133,7 @@ struct fgs_context {
   uint32_t* h_scalars = nullptr;  // pinned
   // host-call staging
   DevBuf<float> h_means, h_rot, h_ls, h_op, h_sh, h_img, h_dl, h_grad;
+  DevBuf<uint8_t> h_aos;  // AoS scene upload (fgs_*_host_aos)
   DevBuf<int32_t> h_radii;
   cudaEvent_t ev[5] = {};
   // stage timing (FGS_FLAG_TIMING): event sets pending accumulation
@@ -335,6 +338,8 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->h_radii.release();
   ctx->counters.release();
   ctx->tile_cycles.release();
+  ctx->blend_count.release();
+  ctx->h_aos.release();
   ctx->tile_span.release();
   ctx->tile_span_bwd.release();
   for (auto& ev : ctx->ev)
@@ -554,6 +559,13 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;
   ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
+  if (ctx->flags & (FGS_FLAG_COUNTERS | FGS_FLAG_BLEND_COUNT)) {
+    FGS_CHECK(ctx->blend_count.ensure(npix));
+    ba.blend_count = ctx->blend_count.p;
+    ctx->have_blend_count = true;
+  } else {
+    ctx->have_blend_count = false;
+  }
   ba.tile_order = n > 0 ? ctx->tile_order.p : nullptr;
   ba.scalars = scalars;
   ba.zero_next = ctx->scalars.p + 16 * (1 - half);
@@ -824,6 +836,12 @@ int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_came
   return FGS_OK;
 }
 
+namespace {
+// Host-buffer backward with the scene already on the device (dev) or mapped (zero_copy).
+int backward_host_dev(fgs_context* ctx, const fgs_gaussians& dev, bool zero_copy, const fgs_camera* camera,
+                      const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
+}  // namespace
+
 int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, const float* dl_dimage,
                       const fgs_backward_options* options, fgs_gradients* grads) {
   if (!ctx) return FGS_EINVAL;
@@ -831,7 +849,6 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
   FGS_CHECK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
   const size_t n = static_cast<size_t>(ctx->n), nn = n ? n : 1;
-  const size_t npix = static_cast<size_t>(camera->width) * camera->height;
   if (static_cast<int64_t>(n) != scene->n)
     return fail(ctx, FGS_EINVAL, "backward: forward context was built for a different scene");
   // The reference takes the scene by value on every call: pinned host arrays are read in place
@@ -839,6 +856,11 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
   fgs_gaussians dev{};
   const bool zero_copy = mapped_scene(scene, &dev);
   if (!zero_copy) {
+    FGS_CHECK(ctx->h_means.ensure(nn * 3));
+    FGS_CHECK(ctx->h_rot.ensure(nn * 4));
+    FGS_CHECK(ctx->h_ls.ensure(nn * 3));
+    FGS_CHECK(ctx->h_op.ensure(nn));
+    FGS_CHECK(ctx->h_sh.ensure(nn * 48));
     if (n) {
       FGS_CHECK(cudaMemcpyAsync(ctx->h_means.p, scene->means, n * 3 * 4, cudaMemcpyHostToDevice, st));
       FGS_CHECK(cudaMemcpyAsync(ctx->h_rot.p, scene->rotations, n * 4 * 4, cudaMemcpyHostToDevice, st));
@@ -848,6 +870,17 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
     }
     dev = fgs_gaussians{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
   }
+  const int rc = backward_host_dev(ctx, dev, zero_copy, camera, dl_dimage, options, grads);
+  if (rc == FGS_OK && !zero_copy) ctx->h2d_bytes += n * 59 * 4;
+  return rc;
+}
+
+namespace {
+int backward_host_dev(fgs_context* ctx, const fgs_gaussians& dev, bool zero_copy, const fgs_camera* camera,
+                      const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads) {
+  cudaStream_t st = ctx->stream;
+  const size_t n = static_cast<size_t>(ctx->n), nn = n ? n : 1;
+  const size_t npix = static_cast<size_t>(camera->width) * camera->height;
   FGS_CHECK(ctx->h_dl.ensure(npix * 3));
   FGS_CHECK(ctx->h_grad.ensure(nn * 59));
   FGS_CHECK(cudaMemcpyAsync(ctx->h_dl.p, dl_dimage, npix * 3 * 4, cudaMemcpyHostToDevice, st));
@@ -873,10 +906,110 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
     FGS_CHECK(cudaMemcpyAsync(grads->d_sh, dg.d_sh, n * 48 * 4, cudaMemcpyDeviceToHost, st));
   }
   FGS_CHECK(cudaStreamSynchronize(st));
-  ctx->h2d_bytes = npix * 3 * 4 + (zero_copy ? static_cast<uint64_t>(ctx->num_compact) * 44 : n * 59 * 4) +
+  ctx->h2d_bytes = npix * 3 * 4 + (zero_copy ? static_cast<uint64_t>(ctx->num_compact) * 44 : 0) +
                    (acc ? n * 59 * 4 : 0);
   ctx->d2h_bytes = n * 59 * 4;
   return FGS_OK;
+}
+}  // namespace
+
+namespace {
+// AoS -> SoA on the device: one thread per (Gaussian, float field component); consecutive threads
+// read consecutive floats of a record and write consecutive entries of each field array.
+__global__ void aos_to_soa_kernel(const uint8_t* __restrict__ raw, int64_t n, int64_t stride, int64_t o_mean,
+                                  int64_t o_rot, int64_t o_ls, int64_t o_op, int64_t o_sh, float* means, float* rot,
+                                  float* ls, float* op, float* sh) {
+  const int64_t total = n * 59;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = i / 59;
+    const int f = static_cast<int>(i - g * 59);
+    const uint8_t* rec = raw + g * stride;
+    float v;
+    if (f < 3) {
+      memcpy(&v, rec + o_mean + 4 * f, 4);
+      means[g * 3 + f] = v;
+    } else if (f < 7) {
+      memcpy(&v, rec + o_rot + 4 * (f - 3), 4);
+      rot[g * 4 + f - 3] = v;
+    } else if (f < 10) {
+      memcpy(&v, rec + o_ls + 4 * (f - 7), 4);
+      ls[g * 3 + f - 7] = v;
+    } else if (f == 10) {
+      memcpy(&v, rec + o_op, 4);
+      op[g] = v;
+    } else {
+      memcpy(&v, rec + o_sh + 4 * (f - 11), 4);
+      sh[g * 48 + f - 11] = v;
+    }
+  }
+}
+
+// Uploads an AoS host scene in one transfer and splits it into the context's device SoA arrays.
+int upload_aos(fgs_context* ctx, const fgs_gaussians_aos* s, fgs_gaussians* dev) {
+  if (s->n < 0 || (s->n > 0 && (!s->data || s->stride < 59 * 4))) return fail(ctx, FGS_EINVAL, "scene: bad AoS layout");
+  const int64_t offs[5] = {s->off_mean, s->off_rotation, s->off_log_scale, s->off_opacity_logit, s->off_sh};
+  const int64_t widths[5] = {3, 4, 3, 1, 48};
+  for (int k = 0; k < 5; ++k)
+    if (offs[k] < 0 || offs[k] + 4 * widths[k] > s->stride) return fail(ctx, FGS_EINVAL, "scene: AoS field outside the record");
+  cudaStream_t st = ctx->stream;
+  const size_t n = static_cast<size_t>(s->n), nn = n ? n : 1;
+  FGS_CHECK(ctx->h_means.ensure(nn * 3));
+  FGS_CHECK(ctx->h_rot.ensure(nn * 4));
+  FGS_CHECK(ctx->h_ls.ensure(nn * 3));
+  FGS_CHECK(ctx->h_op.ensure(nn));
+  FGS_CHECK(ctx->h_sh.ensure(nn * 48));
+  FGS_CHECK(ctx->h_aos.ensure(nn * static_cast<size_t>(s->stride)));
+  if (n) {
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_aos.p, s->data, n * s->stride, cudaMemcpyHostToDevice, st));
+    const int64_t total = static_cast<int64_t>(n) * 59;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    aos_to_soa_kernel<<<blocks, 256, 0, st>>>(ctx->h_aos.p, s->n, s->stride, s->off_mean, s->off_rotation,
+                                              s->off_log_scale, s->off_opacity_logit, s->off_sh, ctx->h_means.p,
+                                              ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p);
+    ++ctx->launches;
+    FGS_CHECK(cudaGetLastError());
+  }
+  *dev = fgs_gaussians{s->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
+  return FGS_OK;
+}
+}  // namespace
+
+int fgs_render_host_aos(fgs_context* ctx, const fgs_gaussians_aos* scene, const fgs_camera* camera,
+                        const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
+  if (!ctx) return FGS_EINVAL;
+  if (!scene || !camera || !image) return fail(ctx, FGS_EINVAL, "render: null argument");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  fgs_gaussians dev{};
+  int rc = upload_aos(ctx, scene, &dev);
+  if (rc != FGS_OK) return rc;
+  const size_t n = static_cast<size_t>(scene->n), nn = n ? n : 1;
+  const size_t npix = static_cast<size_t>(camera->width) * camera->height;
+  FGS_CHECK(ctx->h_img.ensure(npix * 3));
+  FGS_CHECK(ctx->h_radii.ensure(nn));
+  rc = fgs_forward(ctx, &dev, camera, options, ctx->h_img.p, radii ? ctx->h_radii.p : nullptr, stats);
+  if (rc != FGS_OK) return rc;
+  FGS_CHECK(cudaMemcpyAsync(image, ctx->h_img.p, npix * 3 * 4, cudaMemcpyDeviceToHost, st));
+  if (radii && n) FGS_CHECK(cudaMemcpyAsync(radii, ctx->h_radii.p, n * 4, cudaMemcpyDeviceToHost, st));
+  FGS_CHECK(cudaStreamSynchronize(st));
+  ctx->h2d_bytes = n * static_cast<uint64_t>(scene->stride);
+  ctx->d2h_bytes = npix * 3 * 4 + (radii ? n * 4 : 0);
+  return FGS_OK;
+}
+
+int fgs_backward_host_aos(fgs_context* ctx, const fgs_gaussians_aos* scene, const fgs_camera* camera,
+                          const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads) {
+  if (!ctx) return FGS_EINVAL;
+  if (!scene || !camera || !dl_dimage || !grads) return fail(ctx, FGS_EINVAL, "backward: null argument");
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  if (scene->n != ctx->n) return fail(ctx, FGS_EINVAL, "backward: forward context was built for a different scene");
+  fgs_gaussians dev{};
+  int rc = upload_aos(ctx, scene, &dev);
+  if (rc != FGS_OK) return rc;
+  rc = backward_host_dev(ctx, dev, false, camera, dl_dimage, options, grads);
+  if (rc == FGS_OK) ctx->h2d_bytes += static_cast<uint64_t>(scene->n) * static_cast<uint64_t>(scene->stride);
+  return rc;
 }
 
 int fgs_last_transfer(const fgs_context* ctx, uint64_t out[2]) {
@@ -1101,6 +1234,7 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
     return sizeof(v);
   }
   if (nm == "final_T") return copy(ctx->final_T.p, npix * 4);
+  if (nm == "blend_count") return ctx->have_blend_count ? copy(ctx->blend_count.p, npix * 2) : -1;
   if (nm == "last") return copy(ctx->last.p, npix * 4);
   if (nm == "counters") return copy(ctx->counters.p, 4 * sizeof(unsigned long long));
   if (nm == "counters16") return copy(ctx->counters.p, 16 * sizeof(unsigned long long));

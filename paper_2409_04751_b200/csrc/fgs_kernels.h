@@ -72,6 +72,7 @@ struct BlendArgs {
   float* image;                  // H*W*3
   float* final_T;                // H*W
   uint32_t* last;                // H*W: index one past the last contributing entry
+  uint16_t* blend_count;         // optional H*W: contributions per pixel (FGS_FLAG_BLEND_COUNT / counters)
   unsigned long long* counters;  // optional: E_eval, E_contrib, culled evals, max CTA cycles
   unsigned long long* tile_cycles;  // optional (with counters): per-tile CTA cycles
   unsigned long long* tile_span;    // optional (with counters): per tile [start, end] %globaltimer (ns)

@@ -60,7 +60,7 @@ __device__ __forceinline__ float alpha_final(float power, float ar) {
 }
 
 // The transmittance-dependent half of one reference step (inc/splatting.hpp:291-296).
-template <bool COUNTERS>
+template <bool CONTRIB>
 __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr, float cg, float cb, uint32_t k) {
   if (p.done || alpha < 0.0f) return;
   const float Tn = __fmul_rn(p.T, __fsub_rn(1.0f, alpha));
@@ -75,7 +75,7 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr
   p.C2 = fmaf(cb, w, p.C2);
   p.T = Tn;
   p.last = k + 1;
-  if (COUNTERS) ++p.contrib;
+  if (CONTRIB) ++p.contrib;
 }
 
 // K3 forward blend. One CTA per 16x16 tile (scheduled heaviest list first when a tile order
@@ -88,8 +88,14 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr
 // kGroup<PX> splats at a time (alphas first, independent of transmittance; then the sequential
 // transmittance updates).
 // A warp stops when all its pixels have met the reference's termination rule.
-template <bool COUNTERS, int PX>
+// MODE: 0 the product kernel; kModeCounters: work counters + timing instrumentation (global
+// atomics) and the per-pixel blend count; kModeBlendCount: the per-pixel blend count only (the
+// reference's ForwardContext::blend_count, inc/splatting.hpp:299-301).
+constexpr int kModeCounters = 1, kModeBlendCount = 2;
+template <int MODE, int PX>
 __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
+  constexpr bool COUNTERS = MODE == kModeCounters;
+  constexpr bool CONTRIB = MODE != 0;
   constexpr int NW = 8 / PX;
   __shared__ __align__(16) uint64_t skeys[kSortCap];  // tile list sort; then the sorted ids and the raw records
   __shared__ float4 s01[2][NW][32];  // record staging (s0, s1); the radix sort's digit counters before
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
         const uint32_t k = sk[warp][j0 + q];
 #pragma unroll
         for (int u = 0; u < PX; ++u)
-          blend_apply<COUNTERS>(ps[u], alpha_final(pw[q][u], al[q][u]), cr[q], cg_[q], cb[q], k);
+          blend_apply<CONTRIB>(ps[u], alpha_final(pw[q][u], al[q][u]), cr[q], cg_[q], cb[q], k);
       }
     }
     __syncwarp();
@@ -297,6 +303,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
       a.image[pix * 3 + 2] = p.C2 + p.T * a.bg[2];
       a.final_T[pix] = p.T;
       a.last[pix] = p.last;
+      if (CONTRIB && a.blend_count) a.blend_count[pix] = static_cast<uint16_t>(min(p.contrib, 65535u));
     }
   }
 }
@@ -616,11 +623,13 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStr
     // Shared-memory carveout: the 2-pixel kernel fits 6 CTAs per SM only with the largest
     // carveout; the 1-pixel kernel (4 CTAs, register-bound) needs ~78% and gets the rest as L1,
     // where the 8 warps of a tile re-read each chunk's records (config 2 blend 0.177 -> 0.172 ms).
-    for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<true, 1>),
-                          reinterpret_cast<const void*>(blend_forward_kernel<false, 1>)})
+    for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<kModeCounters, 1>),
+                          reinterpret_cast<const void*>(blend_forward_kernel<kModeBlendCount, 1>),
+                          reinterpret_cast<const void*>(blend_forward_kernel<0, 1>)})
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 78);
-    for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<true, 2>),
-                          reinterpret_cast<const void*>(blend_forward_kernel<false, 2>)})
+    for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<kModeCounters, 2>),
+                          reinterpret_cast<const void*>(blend_forward_kernel<kModeBlendCount, 2>),
+                          reinterpret_cast<const void*>(blend_forward_kernel<0, 2>)})
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return 1;
   });
@@ -632,11 +641,13 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStr
   const int tiles = a.tiles_x * a.tiles_y;
   const int px = px_request == 1 ? 1 : 2;
   if (px == 1) {
-    if (a.counters) blend_forward_kernel<true, 1><<<tiles, 256, 0, st>>>(a);
-    else blend_forward_kernel<false, 1><<<tiles, 256, 0, st>>>(a);
+    if (a.counters) blend_forward_kernel<kModeCounters, 1><<<tiles, 256, 0, st>>>(a);
+    else if (a.blend_count) blend_forward_kernel<kModeBlendCount, 1><<<tiles, 256, 0, st>>>(a);
+    else blend_forward_kernel<0, 1><<<tiles, 256, 0, st>>>(a);
   } else {
-    if (a.counters) blend_forward_kernel<true, 2><<<tiles, 128, 0, st>>>(a);
-    else blend_forward_kernel<false, 2><<<tiles, 128, 0, st>>>(a);
+    if (a.counters) blend_forward_kernel<kModeCounters, 2><<<tiles, 128, 0, st>>>(a);
+    else if (a.blend_count) blend_forward_kernel<kModeBlendCount, 2><<<tiles, 128, 0, st>>>(a);
+    else blend_forward_kernel<0, 2><<<tiles, 128, 0, st>>>(a);
   }
   return 1;
 }
