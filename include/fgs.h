@@ -250,6 +250,33 @@ int fgs_bruteforce_render_f64(fgs_context* ctx, int64_t n, const double* means, 
                               const fgs_camera* camera, int32_t sh_degree, const double background[3], double* image,
                               double* transmittance);
 
+/* ---- Multi-GPU: views partitioned by camera, Gaussians replicated, the
+ * per-Gaussian gradients summed over the GPUs with one NCCL all-reduce (NCCL is loaded at first
+ * use; libfgs.so itself does not depend on it). ---- */
+typedef struct fgs_comm fgs_comm;
+
+/* One rank per process: rank 0 creates the 128-byte id and shares it out of band (MPI,
+ * torch.distributed, a file); every rank then joins with its context (device and stream). */
+int fgs_comm_get_unique_id(uint8_t id[128]);
+int fgs_comm_init(fgs_context* ctx, const uint8_t id[128], int nranks, int rank, fgs_comm** out);
+/* One process driving ndev devices (ncclCommInitAll): one communicator per context. */
+int fgs_comm_init_all(fgs_context* const* ctxs, int ndev, fgs_comm** comms);
+int fgs_comm_destroy(fgs_comm* comm);
+
+/* In-place sum over the ranks of the five gradient arrays of n Gaussians (device memory), ordered
+ * on the context's stream. */
+int fgs_allreduce_gradients(fgs_comm* comm, fgs_gradients* grads, int64_t n);
+
+/* The multi-view step of one rank: forward + backward of its `nviews` cameras (dl_dimages[v] and
+ * images[v], device H*W*3 each; images may be NULL), the gradients accumulated into `grads` (the
+ * first view overwrites unless options->accumulate), then -- with a communicator -- summed over
+ * the ranks: the last view's preprocess backward runs in 4 Gaussian-id ranges and each range's
+ * all-reduce starts on a communication stream as soon as the range is written, overlapping the
+ * next range. comm = NULL: single GPU, no collective. Asynchronous on the context's stream. */
+int fgs_fwd_bwd_views(fgs_context* ctx, fgs_comm* comm, const fgs_gaussians* scene, const fgs_camera* cameras,
+                      int nviews, const float* const* dl_dimages, const fgs_render_options* render_options,
+                      const fgs_backward_options* backward_options, fgs_gradients* grads, float* const* images);
+
 /* Counters of the last forward: [n, num_splats, num_intersections, tiles_x, tiles_y, width, height,
  * num_culled, num_degenerate]. */
 int fgs_last_counts(const fgs_context* ctx, int64_t out[9]);

@@ -74,7 +74,8 @@ EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs
            "fgs_render_host", "fgs_backward_host", "fgs_set_flags", "fgs_debug_get", "fgs_last_counts",
            "fgs_timing", "fgs_measure_fp32_peak", "fgs_l1_dssim_loss", "fgs_adam_step", "fgs_train_step",
            "fgs_bruteforce_render", "fgs_bruteforce_render_f64", "fgs_last_transfer", "fgs_render_host_aos",
-           "fgs_backward_host_aos"]
+           "fgs_backward_host_aos", "fgs_comm_get_unique_id", "fgs_comm_init", "fgs_comm_init_all",
+           "fgs_comm_destroy", "fgs_allreduce_gradients", "fgs_fwd_bwd_views"]
 
 _lib = None
 
@@ -132,6 +133,19 @@ def load(path: str = LIB_PATH):
     L.fgs_backward_host_aos.argtypes = [vp, P(fgs_gaussians_aos), P(fgs_camera), vp, P(fgs_backward_options),
                                         P(fgs_gradients)]
     L.fgs_backward_host_aos.restype = i32
+    L.fgs_comm_get_unique_id.argtypes = [P(C.c_uint8)]
+    L.fgs_comm_get_unique_id.restype = i32
+    L.fgs_comm_init.argtypes = [vp, P(C.c_uint8), i32, i32, P(vp)]
+    L.fgs_comm_init.restype = i32
+    L.fgs_comm_init_all.argtypes = [P(vp), i32, P(vp)]
+    L.fgs_comm_init_all.restype = i32
+    L.fgs_comm_destroy.argtypes = [vp]
+    L.fgs_comm_destroy.restype = i32
+    L.fgs_allreduce_gradients.argtypes = [vp, P(fgs_gradients), C.c_int64]
+    L.fgs_allreduce_gradients.restype = i32
+    L.fgs_fwd_bwd_views.argtypes = [vp, vp, P(fgs_gaussians), P(fgs_camera), i32, P(vp), P(fgs_render_options),
+                                    P(fgs_backward_options), P(fgs_gradients), P(vp)]
+    L.fgs_fwd_bwd_views.restype = i32
     L.fgs_last_transfer.argtypes = [vp, P(C.c_uint64)]
     L.fgs_last_transfer.restype = i32
     _lib = L

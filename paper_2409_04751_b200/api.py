@@ -158,6 +158,34 @@ class Rasterizer:
         self._check(rc)
         return grads
 
+    def fwd_bwd_views(self, scene: Scene, cameras, dl_dimages, render_options: Optional[RenderOptions] = None,
+                      backward_options: Optional[BackwardOptions] = None, grads=None, comm=None, images=None,
+                      accumulate: bool = False):
+        """This rank's multi-view step through the C ABI (fgs_fwd_bwd_views): forward + backward of
+        every camera, the gradients accumulated into one 59*N buffer and, with a ``Communicator``,
+        summed over the ranks by NCCL (the last view's gradient ranges all-reduced while the next
+        range is computed). Returns the gradient buffer."""
+        import torch
+
+        n = scene.n
+        if grads is None:
+            grads = torch.zeros(59 * n, dtype=torch.float32, device=scene.means.device)
+        nv = len(cameras)
+        cams = (_lib.fgs_camera * max(nv, 1))(*[_camera_struct(c) for c in cameras])
+        for c, d in zip(cameras, dl_dimages):
+            if tuple(d.shape) != (c.height, c.width, 3):
+                raise InvalidArgument("rasterize_backward: image gradient shape does not match context")
+        dls = (C.c_void_p * max(nv, 1))(*[_ptr(d) for d in dl_dimages])
+        imgs = (C.c_void_p * max(nv, 1))(*[(_ptr(images[i]) if images is not None else None) for i in range(nv)])
+        ro = _render_options(render_options, getattr(scene, "background", None))
+        bo = _backward_options(backward_options, accumulate)
+        gs = _grad_struct(grads, n)
+        rc = self._L.fgs_fwd_bwd_views(self._h, comm._h if comm is not None else None, C.byref(self._gaussians(scene)),
+                                       cams, nv, dls, C.byref(ro), C.byref(bo), C.byref(gs),
+                                       imgs if images is not None else None)
+        self._check(rc)
+        return grads
+
     # ---- host path (numpy), the reference's calling convention ----
     def render_host(self, scene: Scene, camera: Camera, options: Optional[RenderOptions] = None, radii=True,
                     image=None, want_stats=True):

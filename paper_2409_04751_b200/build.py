@@ -28,6 +28,7 @@ SOURCES = {
     "train.cu": [],
     "bruteforce.cu": [],
     "fgs_api.cu": [],
+    "comm.cu": [],
 }
 
 
@@ -65,7 +66,7 @@ def build(verbose=False, force=False) -> str:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs]
+    cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs, "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

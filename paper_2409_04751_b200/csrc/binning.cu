@@ -420,6 +420,9 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
     for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw)
       row_offsets(a, ty, rowtot, hist, cur, bprefix, s_off + 64 * (tid >> 5));  // s_off: free until the scatter
     uint32_t run1 = p1, run2 = p2;
+    int gchunk[kGradChunks];
+#pragma unroll
+    for (int cb = 0; cb < kGradChunks; ++cb) gchunk[cb] = static_cast<int>(static_cast<int64_t>(a.n) * cb / kGradChunks);
     for (int sb = lo; sb < hi; sb += kT * kItems) {
       const int r0 = sb + tid * kItems;
       uint32_t c[kItems], s1 = 0, s2 = 0;
@@ -434,6 +437,10 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
       uint32_t off = run2 + block_exclusive_scan(s2, sm.warp_tmp2, &t2);
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
+        // a gradient-chunk boundary c N / C at this id: the compacted position there
+#pragma unroll
+        for (int cb = 1; cb < kGradChunks; ++cb)
+          if (r0 + i == gchunk[cb]) a.scalars[kScalarChunkQ + cb - 1] = pos;
         if (c[i]) {
           a.cval[pos] = static_cast<uint32_t>(r0 + i);
           a.coff[pos] = off;

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -156,6 +157,7 @@ struct fgs_context {
   int tiles_x = 0, tiles_y = 0;
   int64_t num_isect = 0;
   int64_t num_compact = 0;  // Gaussians touching >= 1 tile (rows the backward computes)
+  int64_t chunk_q[fgs::kGradChunks + 1] = {};  // compacted-list position of each gradient-chunk boundary
   uint32_t num_splats = 0, num_degenerate = 0, num_culled = 0;
   size_t aux_bytes = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;  // PCIe bytes of the last host-buffer call
@@ -605,6 +607,9 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     return fail(ctx, FGS_ECUDA, "forward: per-tile counts disagree with the intersection scan");
   ctx->num_isect = I;
   ctx->num_compact = ctx->h_scalars[fgs::kScalarM];
+  ctx->chunk_q[0] = 0;
+  for (int c = 1; c < fgs::kGradChunks; ++c) ctx->chunk_q[c] = n > 0 ? ctx->h_scalars[fgs::kScalarChunkQ + c - 1] : 0;
+  ctx->chunk_q[fgs::kGradChunks] = ctx->num_compact;
   ctx->num_splats = ctx->h_scalars[fgs::kScalarKept];
   ctx->num_degenerate = ctx->h_scalars[fgs::kScalarDegen];
   ctx->num_culled = static_cast<uint32_t>(n) - ctx->num_splats - ctx->num_degenerate;
@@ -669,8 +674,13 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   return FGS_OK;
 }
 
-int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, const float* dl_dimage,
-                 const fgs_backward_options* options, fgs_gradients* grads) {
+// The backward of the last forward. K4b runs as one launch, or (chunk_done set) as kGradChunks
+// launches over the Gaussian-id ranges [c n / C, (c + 1) n / C) with chunk_done(c, id0, id1)
+// called after each: the multi-GPU step enqueues that range's all-reduce there
+// (fgs_fwd_bwd_views), overlapping it with the next range's K4b.
+int backward_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, const float* dl_dimage,
+                  const fgs_backward_options* options, fgs_gradients* grads,
+                  const std::function<int(int, int64_t, int64_t)>& chunk_done) {
   if (!ctx) return FGS_EINVAL;
   if (!scene || !camera || !dl_dimage || !grads) return fail(ctx, FGS_EINVAL, "backward: null argument");
   if (!ctx->have_fwd) return fail(ctx, FGS_ESTATE, "backward: no forward context");
@@ -751,16 +761,56 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
   pb.m = ctx->num_compact;
   pb.cval = ctx->cval.p;
   pb.rec = ctx->rec.p;
-  if (n > 0 && (pb.m > 0 || !pb.accumulate)) {
-    ctx->var_k4b = ctx->scene_on_host ? 6 : rule_k4b_minb(pb.m);
-    fgs::preprocess_backward_launch(pb, ctx->scene_on_host, ctx->var_k4b == 4 ? 2 : 1, st);
-    ++ctx->launches;
+  ctx->var_k4b = ctx->scene_on_host ? 6 : rule_k4b_minb(pb.m);
+  const int variant = ctx->var_k4b == 4 ? 2 : 1;
+  if (!chunk_done) {
+    pb.q_begin = 0;
+    pb.q_end = pb.m;
+    pb.id_begin = 0;
+    pb.id_end = n;
+    if (n > 0 && (pb.m > 0 || !pb.accumulate)) {
+      fgs::preprocess_backward_launch(pb, ctx->scene_on_host, variant, st);
+      ++ctx->launches;
+    }
+  } else {
+    for (int c = 0; c < fgs::kGradChunks; ++c) {
+      pb.q_begin = ctx->chunk_q[c];
+      pb.q_end = ctx->chunk_q[c + 1];
+      pb.id_begin = n * c / fgs::kGradChunks;
+      pb.id_end = n * (c + 1) / fgs::kGradChunks;
+      if (pb.id_end > pb.id_begin && (pb.q_end > pb.q_begin || !pb.accumulate)) {
+        fgs::preprocess_backward_launch(pb, ctx->scene_on_host, variant, st);
+        ++ctx->launches;
+      }
+      FGS_CHECK(cudaGetLastError());
+      const int rc = chunk_done(c, pb.id_begin, pb.id_end);
+      if (rc != FGS_OK) return rc;
+    }
   }
   if (timing) cudaEventRecord(ev[2], st);
   FGS_CHECK(cudaGetLastError());
   guard.armed = false;
   return FGS_OK;
 }
+
+int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, const float* dl_dimage,
+                 const fgs_backward_options* options, fgs_gradients* grads) {
+  return backward_impl(ctx, scene, camera, dl_dimage, options, grads, nullptr);
+}
+
+}  // extern "C"
+
+// Internal entry points for comm.cu (not part of the C ABI).
+int fgs_internal_fail(fgs_context* ctx, int code, const char* msg) { return fail(ctx, code, msg); }
+cudaStream_t fgs_internal_stream(fgs_context* ctx) { return ctx->stream; }
+int fgs_internal_device(fgs_context* ctx) { return ctx->device; }
+int fgs_internal_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                          const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads,
+                          const std::function<int(int, int64_t, int64_t)>& chunk_done) {
+  return backward_impl(ctx, scene, camera, dl_dimage, options, grads, chunk_done);
+}
+
+extern "C" {
 
 namespace {
 // Device address of page-locked (pinned, mapped) host memory, or nullptr for pageable memory.

@@ -33,6 +33,8 @@ struct PreprocessArgs {
 struct PreprocessBackwardArgs {
   int64_t n;
   int64_t m;                 // Gaussians that touched >= 1 tile (level-1 compaction count)
+  int64_t q_begin, q_end;    // this launch's slice of the compacted list (all: 0, m)
+  int64_t id_begin, id_end;  // and the Gaussian-id range it writes (all: 0, n)
   const uint32_t* cval;      // [m] their ids in source order
   const SortedRec* rec;      // K1 per-Gaussian records (alpha, clamped colours)
   DevCamera cam;
@@ -103,8 +105,13 @@ constexpr int kBinThreads = 1024;
 constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, kScalarM = 4, kScalarI2 = 5, kScalarBig = 6,
               kScalarSegs = 7,    // backward segment slots of the frame (K2: sum over long lists of ceil(L / kSeg))
               kScalarSegPos = 8,  // K3's slot allocation cursor
-              kScalarMaxList = 9; // longest tile list of the frame (K2)
-constexpr int kScalarReadback = 10;  // scalars the host reads after K2
+              kScalarMaxList = 9, // longest tile list of the frame (K2)
+              kScalarChunkQ = 10; // [kGradChunks - 1]: tile-touching Gaussians with id < c N / kGradChunks
+// The backward's K4b can run as kGradChunks launches over Gaussian-id ranges [c N / C, (c+1) N / C)
+// so that a multi-GPU step all-reduces each range's gradients while the next range is computed
+// (fgs_fwd_bwd_views); K2 records where each range starts in the compacted list.
+constexpr int kGradChunks = 4;
+constexpr int kScalarReadback = kScalarChunkQ + kGradChunks - 1;  // scalars the host reads after K2
 
 // Backward segments: a tile list longer than kSeg entries is split into ceil(L / kSeg) segments
 // that the blend backward processes as independent CTAs; the forward leaves each pixel's state

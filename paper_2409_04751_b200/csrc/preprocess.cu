@@ -812,11 +812,12 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) preprocess_backward_kernel(
   __shared__ uint8_t vis[kBwdThreads];
   __shared__ __align__(16) float s_shstage[kBwdThreads * 20];  // per-lane SH gradient factors
   const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t q0 = int64_t(blockIdx.x) * kBwdThreads;
-  const int64_t q1 = q0 + kBwdThreads < a.m ? q0 + kBwdThreads : a.m;  // this CTA's slice of cval
+  const int64_t q0 = a.q_begin + int64_t(blockIdx.x) * kBwdThreads;
+  const int64_t q1 = q0 + kBwdThreads < a.q_end ? q0 + kBwdThreads : a.q_end;  // this CTA's slice of cval
   if (!a.accumulate) {
-    const int64_t start = q0 == 0 ? 0 : int64_t(a.cval[q0 - 1]) + 1;
-    const int64_t end = q1 >= a.m ? a.n : int64_t(a.cval[q1 - 1]) + 1;
+    // rows of this CTA's id span: from its predecessor's last Gaussian (or the launch's first id)
+    const int64_t start = q0 <= a.q_begin ? a.id_begin : int64_t(a.cval[q0 - 1]) + 1;
+    const int64_t end = q1 >= a.q_end ? a.id_end : int64_t(a.cval[q1 - 1]) + 1;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int64_t c0 = start; c0 < end; c0 += kBwdThreads) {  // 128-row chunks
       const int nloc = static_cast<int>(end - c0 < kBwdThreads ? end - c0 : kBwdThreads);
@@ -894,7 +895,8 @@ void preprocess_launch(const PreprocessArgs& a, bool host_scene, cudaStream_t st
 }
 
 void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene, int variant, cudaStream_t st) {
-  const int blocks = a.m > 0 ? div_up(static_cast<int>(a.m), kBwdThreads) : 1;
+  const int64_t mq = a.q_end - a.q_begin;
+  const int blocks = mq > 0 ? div_up(static_cast<int>(mq), kBwdThreads) : 1;
   if (host_scene) preprocess_backward_kernel<true, 6><<<blocks, kBwdThreads, 0, st>>>(a);
   else if (variant == 2) preprocess_backward_kernel<false, 4><<<blocks, kBwdThreads, 0, st>>>(a);
   else preprocess_backward_kernel<false, 6><<<blocks, kBwdThreads, 0, st>>>(a);
