@@ -159,13 +159,14 @@ def run_ours(args, ws, rank, local):
     def fwd_views():
         multiview.forward_views(cams, lambda c: r.forward(ds, c, ropt, image=image))
 
-    def fwd_bwd_views(views):
-        def rb(i, buf, acc):
-            r.forward(ds, cams[i], ropt, image=image)
-            r.backward(ds, cams[i], dl_dev[i % len(dl_dev)], bopt, grads=buf, accumulate=acc)
+    # config 4 over several GPUs: the library's own NCCL communicator (csrc/comm.cu), the id shared
+    # over the torch.distributed group; the all-reduce overlaps the last view's preprocess backward
+    comm = multiview.Communicator.from_process_group(r) if (dist is not None and cfg == 4) else None
 
-        multiview.fwd_bwd_views(views, rb, grads, process_group=dist.group.WORLD if dist else None,
-                                all_reduce=cfg == 4)
+    def fwd_bwd_views(views):
+        # the native rank step: forward + accumulating backward of every view (+ the all-reduce)
+        r.fwd_bwd_views(ds, [cams[i] for i in views], [dl_dev[i % len(dl_dev)] for i in views], ropt, bopt,
+                        grads=grads, comm=comm)
 
     views = list(range(len(cams)))
     primary = fwd_views if FWD_ONLY[cfg] else (lambda: fwd_bwd_views(views))
@@ -357,6 +358,8 @@ def run_ours(args, ws, rank, local):
     }
     if rank == 0:
         print(json.dumps(res))
+    if comm is not None:
+        comm.close()
     if dist is not None:
         dist.destroy_process_group()
 

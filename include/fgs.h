@@ -169,7 +169,7 @@ int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s);
 
 /* Parity/debug export of the last forward's state into host memory. Names:
  *   "state_u8" u8[N] (0 culled, 1 kept, 2 degenerate), "rec" f32[N*12] (splat records: mean_px,
- *   conic, alpha_max, colour, extent), "depth_key" u32[N], "radius" int32[N], "touched" u32[N],
+ *   -conic.a/2, conic.b, -conic.c/2, alpha_max, colour, extent), "depth_key" u32[N], "radius" int32[N], "touched" u32[N],
  *   "key_tile"/"key_depth"/"key_gauss" u32[I] (pre-sort keys in the reference's emission order),
  *   "sorted_gauss" u32[I], "sorted_tile" u32[I], "offsets" u32[T+1] (tile ranges),
  *   "keys" u64[I] (depth key << 32 | Gaussian id, as the binning scatter wrote them into each tile's

@@ -207,7 +207,7 @@ class Renderer {
       const float* r = rec.data() + 12 * i;
       omnisplat::Splat2D<float> sp;
       sp.mean_px = omnisplat::Vec2<float>(r[0], r[1]);
-      sp.conic = omnisplat::Vec3<float>(r[2], r[3], r[4]);
+      sp.conic = omnisplat::Vec3<float>(-2.0f * r[2], r[3], -2.0f * r[4]);  // the record holds -a/2, -c/2
       const uint32_t bits = dkey[i] & 0x7FFFFFFFu;  // positive depth: the key is the bits | 0x80000000
       std::memcpy(&sp.depth, &bits, 4);
       sp.radius_px = radius[i];

@@ -267,7 +267,7 @@ class Rasterizer:
         return {
             "state": state,
             "mean_px": r0[:, 0:2].copy(),
-            "conic": np.stack([r0[:, 2], r0[:, 3], r1[:, 0]], 1),
+            "conic": np.stack([-2.0 * r0[:, 2], r0[:, 3], -2.0 * r1[:, 0]], 1).astype(np.float32),  # record: -a/2, -c/2
             "color": np.stack([r1[:, 2], r1[:, 3], r2], 1),
             "alpha": r1[:, 1].copy(),
             "depth": (dk & np.uint32(0x7FFFFFFF)).view(np.float32),

@@ -43,10 +43,12 @@ struct DevCamera {
 // sorted (tile-list) order by the binning kernel, so the blends read each tile's list as one
 // contiguous stream.
 struct SortedRec {
-  float4 a;  // mean_px.x, mean_px.y, conic.a, conic.b
-  float4 b;  // conic.c, alpha_max, R, G
+  float4 a;  // mean_px.x, mean_px.y, -conic.a / 2, conic.b
+  float4 b;  // -conic.c / 2, alpha_max, R, G
   float4 c;  // B, extent x, extent y, tau (splat_cull_params)
 };
+// (-a/2) dx dx + (-c/2) dy dy = -((a dx dx + c dy dy) / 2) exactly: scaling by -1/2 commutes with
+// every rounding (short of subnormal results, where |power| < 1e-37 leaves alpha unchanged).
 
 // Correctly rounded fp32 exp / atan2 (double evaluation, one rounding): the definition the
 // oracle's parity mode uses.
@@ -56,13 +58,13 @@ __device__ __forceinline__ float cr_atan2f(float y, float x) {
 }
 
 // The blend's decision chain in the reference's exact op order, FMA-free
-// (inc/splatting.hpp:284-287): power = -0.5*((a*dx)*dx + (c*dy)*dy) - (b*dx)*dy.
-__device__ __forceinline__ float blend_power(float a, float b, float c, float dx, float dy) {
-  const float t1 = __fmul_rn(__fmul_rn(a, dx), dx);
-  const float t2 = __fmul_rn(__fmul_rn(c, dy), dy);
-  const float u = __fmul_rn(-0.5f, __fadd_rn(t1, t2));
+// (inc/splatting.hpp:284-287): power = -0.5*((a*dx)*dx + (c*dy)*dy) - (b*dx)*dy, from the record's
+// na = -a/2, nc = -c/2: ((na*dx)*dx + (nc*dy)*dy) - (b*dx)*dy, the same value.
+__device__ __forceinline__ float blend_power(float na, float b, float nc, float dx, float dy) {
+  const float t1 = __fmul_rn(__fmul_rn(na, dx), dx);
+  const float t2 = __fmul_rn(__fmul_rn(nc, dy), dy);
   const float v = __fmul_rn(__fmul_rn(b, dx), dy);
-  return __fsub_rn(u, v);
+  return __fsub_rn(__fadd_rn(t1, t2), v);
 }
 
 // Fast exp: one MUFU.EX2 with flush-to-zero (no denormal fix-up; results below 2^-126 only
@@ -182,7 +184,7 @@ __device__ __forceinline__ bool rec_hits_ellipse(float4 ra, float4 rb, float4 rc
   const float lx = __fsub_rn(x0, ra.x), hx = __fsub_rn(x1, ra.x);
   const float ly = __fsub_rn(y0, ra.y), hy = __fsub_rn(y1, ra.y);
   if (lx <= 0.0f && hx >= 0.0f && ly <= 0.0f && hy >= 0.0f) return true;
-  const float a = ra.z, b = ra.w, c = rb.x;
+  const float a = -2.0f * ra.z, b = ra.w, c = -2.0f * rb.x;  // the record's -a/2, -c/2
   const float nbc = __fdiv_rn(-b, c), nba = __fdiv_rn(-b, a);
   auto q = [&](float dx, float dy) {
     const float t1 = __fmul_rn(__fmul_rn(a, dx), dx);

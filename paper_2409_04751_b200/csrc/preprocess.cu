@@ -35,8 +35,10 @@ struct Terms {
   float g, u, U;
 };
 
-// cameras.hpp:107-128 (AxisMode::Auto)
-__device__ __forceinline__ Terms fisheye_terms(float lz2, float z) {
+// cameras.hpp:107-128 (AxisMode::Auto). theta = atan2(sqrt(lz2), z): the reference evaluates it
+// again in every call (visibility, pixel, Jacobian, Jacobian gradient); the value is the same, so
+// it is computed once per Gaussian and passed in.
+__device__ __forceinline__ Terms fisheye_terms(float lz2, float z, float theta) {
   const float z2 = z * z;
   Terms t;
   if (z > 0.0f && lz2 < kFisheyeSeriesW2 * z2) {
@@ -48,7 +50,6 @@ __device__ __forceinline__ Terms fisheye_terms(float lz2, float z) {
   } else {
     const float lz = sqrtf(lz2);
     const float r2 = lz2 + z2;
-    const float theta = cr_atan2f(lz, z);
     t.g = theta / lz;
     t.u = z / (lz2 * r2) - theta / (lz2 * lz);
     t.U = 3.0f * theta / (lz2 * lz2 * lz) - z / (r2 * lz2 * lz2) - 2.0f * z * (r2 + lz2) / (lz2 * lz2 * r2 * r2);
@@ -57,11 +58,11 @@ __device__ __forceinline__ Terms fisheye_terms(float lz2, float z) {
 }
 
 // cameras.hpp:191-198
-__device__ __forceinline__ void fisheye_jacobian(const float p[3], const DevCamera& cam, float j[2][3]) {
+__device__ __forceinline__ void fisheye_jacobian(const float p[3], const DevCamera& cam, const Terms& t,
+                                                 float j[2][3]) {
   const float x = p[0], y = p[1], z = p[2];
   const float lz2 = x * x + y * y;
   const float r2 = lz2 + z * z;
-  const Terms t = fisheye_terms(lz2, z);
   const float fx = cam.fx, fy = cam.fy;
   j[0][0] = fx * (t.g + x * x * t.u);
   j[0][1] = fx * x * y * t.u;
@@ -127,12 +128,12 @@ __device__ __forceinline__ void panorama_jacobian_grad(const float p[3], const D
 }
 
 // cameras.hpp:232-247
-__device__ __forceinline__ void fisheye_jacobian_grad(const float p[3], const DevCamera& cam, float d[3][2][3]) {
+__device__ __forceinline__ void fisheye_jacobian_grad(const float p[3], const DevCamera& cam, const Terms& t,
+                                                      float d[3][2][3]) {
   const float x = p[0], y = p[1], z = p[2];
   const float lz2 = x * x + y * y;
   const float r2 = lz2 + z * z;
   const float ir4 = 1.0f / (r2 * r2);
-  const Terms t = fisheye_terms(lz2, z);
   const float fx = cam.fx, fy = cam.fy;
   const float x2 = x * x, y2 = y * y;
   const float ux = t.u + x2 * t.U;
@@ -314,6 +315,7 @@ __device__ __forceinline__ uint32_t depth_key_bits(float d) {
 
 // Projected covariance + conic for a visible Gaussian: returns 0 kept-candidate, 2 degenerate.
 struct Proj {
+  Terms ft;  // fisheye terms (g, u, U) at mu (fisheye camera only)
   float mu[3];
   float pix[2];
   float j[2][3];
@@ -335,10 +337,11 @@ __device__ __forceinline__ int project_covariance(const DevCamera& cam, const fl
     if (z < 0.0f && lz2 < 1e-24f * z * z) return -1;
     const float theta = cr_atan2f(sqrtf(lz2), z);
     if (!(theta <= cam.fov_max + kFisheyeCullMargin)) return -1;
-    const float g = fisheye_terms(lz2, z).g;
+    P.ft = fisheye_terms(lz2, z, theta);
+    const float g = P.ft.g;
     P.pix[0] = cam.cx + cam.fx * g * x;
     P.pix[1] = cam.cy + cam.fy * g * y;
-    fisheye_jacobian(P.mu, cam, P.j);
+    fisheye_jacobian(P.mu, cam, P.ft, P.j);
   } else if (cam.model == kCamPinhole) {
     if (fabsf(z) < 1e-12f) return -1;
     P.pix[0] = cam.cx + cam.fx * x / z;
@@ -495,9 +498,12 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
   }
   if (!valid) return;
   SortedRec rr;
-  rr.a = r0;
-  rr.b = r1;
   const float3 cull = splat_cull_params(r0, r1);
+  // the record keeps -a/2 and -c/2 (exact power-of-two scalings): the blends' power is then
+  // (a' dx) dx + (c' dy) dy - (b dx) dy, one multiplication less per (pixel, splat) pair, with
+  // the reference's value bit for bit (SortedRec, fgs_common.cuh)
+  rr.a = make_float4(r0.x, r0.y, -0.5f * r0.z, r0.w);
+  rr.b = make_float4(-0.5f * r1.x, r1.y, r1.z, r1.w);
   rr.c = make_float4(r2v, cull.x, cull.y, cull.z);
   a.rec[i] = rr;
   a.state[i] = state;
@@ -623,7 +629,7 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
 #pragma unroll
       for (int c = 0; c < 3; ++c) dldj[r][c] = dldt[r][0] * cam.W[c * 3 + 0] + dldt[r][1] * cam.W[c * 3 + 1] + dldt[r][2] * cam.W[c * 3 + 2];
     float dj[3][2][3];
-    if (cam.model == kCamFisheye) fisheye_jacobian_grad(P.mu, cam, dj);
+    if (cam.model == kCamFisheye) fisheye_jacobian_grad(P.mu, cam, P.ft, dj);
     else if (cam.model == kCamPinhole) pinhole_jacobian_grad(P.mu, cam, dj);
     else panorama_jacobian_grad(P.mu, cam, dj);
     float cov[3];

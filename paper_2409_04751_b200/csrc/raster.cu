@@ -37,12 +37,12 @@ struct PixelState {
   bool done;
 };
 
-// Power of one (pixel, splat) pair in the reference's exact op order (inc/splatting.hpp:
-// 284-287). t1 = (a*dx)*dx and bdx = b*dx are shared by the two pixels of a lane.
-__device__ __forceinline__ float blend_power_dy(float fy, float4 r0, float c, float t1, float bdx) {
+// Power of one (pixel, splat) pair with the reference's value (inc/splatting.hpp:284-287; see
+// blend_power): t1 = (na*dx)*dx and bdx = b*dx are shared by the two pixels of a lane, nc = -c/2.
+__device__ __forceinline__ float blend_power_dy(float fy, float4 r0, float nc, float t1, float bdx) {
   const float dy = __fsub_rn(fy, r0.y);
-  const float t2 = __fmul_rn(__fmul_rn(c, dy), dy);
-  return __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), __fmul_rn(bdx, dy));
+  const float t2 = __fmul_rn(__fmul_rn(nc, dy), dy);
+  return __fsub_rn(__fadd_rn(t1, t2), __fmul_rn(bdx, dy));
 }
 
 // alpha_max * exp(power) with the fast exp; *near = the product lies within the fast path's
@@ -571,8 +571,8 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
           p2 = fmaf(dp * dy, dy, p2);
         }
         // sum_u dp (a dx + b dy), sum_u dp (b dx + c dy), -1/2 sum dp dx^2, -sum dp dx dy, -1/2 sum dp dy^2
-        v[9 * q + 0] = fmaf(r0.z * dx, p0, r0.w * p1);
-        v[9 * q + 1] = fmaf(r0.w * dx, p0, r1.x * p1);
+        v[9 * q + 0] = fmaf((-2.0f * r0.z) * dx, p0, r0.w * p1);  // conic a = -2 (record's -a/2)
+        v[9 * q + 1] = fmaf(r0.w * dx, p0, (-2.0f * r1.x) * p1);
         v[9 * q + 2] = (-0.5f * dx * dx) * p0;
         v[9 * q + 3] = -dx * p1;
         v[9 * q + 4] = -0.5f * p2;
