@@ -53,29 +53,26 @@ __device__ __forceinline__ float alpha_fast(float amax, float power, bool* near)
   return ar;
 }
 
-// Final alpha of the reference step, or -1 when it skips (power > 0 or alpha < 1/255).
-__device__ __forceinline__ float alpha_final(float power, float ar) {
-  const float alpha = fminf(kAlphaClamp, ar);
-  return (power <= 0.0f && alpha >= kAlphaSkip) ? alpha : -1.0f;
-}
-
-// The transmittance-dependent half of one reference step (inc/splatting.hpp:291-296).
+// The transmittance-dependent half of one reference step (inc/splatting.hpp:288-296), branch-free:
+// skip (power > 0 or alpha < 1/255), stop (T' < 1e-4: the pixel is done before accumulating) or
+// accumulate. A skipped or stopped step adds cr * 0 = +0 to the (non-negative) colours.
 template <bool CONTRIB>
-__device__ __forceinline__ void blend_apply(PixelState& p, float alpha, float cr, float cg, float cb, uint32_t k) {
-  if (p.done || alpha < 0.0f) return;
+__device__ __forceinline__ void blend_apply(PixelState& p, float power, float ar, float cr, float cg, float cb,
+                                            uint32_t k) {
+  const float alpha = fminf(kAlphaClamp, ar);
+  const bool live = !p.done && power <= 0.0f && alpha >= kAlphaSkip;
   const float Tn = __fmul_rn(p.T, __fsub_rn(1.0f, alpha));
-  if (Tn < kTransmittanceStop) {
-    p.done = true;
-    p.stop = k;
-    return;
-  }
-  const float w = __fmul_rn(alpha, p.T);
+  const bool stop = live && Tn < kTransmittanceStop;
+  const bool add = live && !stop;
+  const float w = add ? __fmul_rn(alpha, p.T) : 0.0f;
   p.C0 = fmaf(cr, w, p.C0);
   p.C1 = fmaf(cg, w, p.C1);
   p.C2 = fmaf(cb, w, p.C2);
-  p.T = Tn;
-  p.last = k + 1;
-  if (CONTRIB) ++p.contrib;
+  p.T = add ? Tn : p.T;
+  p.last = add ? k + 1 : p.last;
+  p.stop = stop ? k : p.stop;
+  p.done = p.done || stop;
+  if (CONTRIB) p.contrib += add ? 1u : 0u;
 }
 
 // K3 forward blend. One CTA per 16x16 tile (scheduled heaviest list first when a tile order
@@ -227,7 +224,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
       bool any_near = false;
 #pragma unroll
       for (int q = 0; q < G; ++q) {
-        const int jj = j0 + q < nsurv ? j0 + q : j0;
+        const int jj = min(j0 + q, nsurv - 1);
         const float4 r0 = s0[warp][jj];
         const float4 r1 = s1[warp][jj];
         cr[q] = r1.z;
@@ -261,7 +258,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
         const uint32_t k = sk[warp][j0 + q];
 #pragma unroll
         for (int u = 0; u < PX; ++u)
-          blend_apply<CONTRIB>(ps[u], alpha_final(pw[q][u], al[q][u]), cr[q], cg_[q], cb[q], k);
+          blend_apply<CONTRIB>(ps[u], pw[q][u], al[q][u], cr[q], cg_[q], cb[q], k);
       }
     }
     __syncwarp();
