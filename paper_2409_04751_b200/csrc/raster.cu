@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "fgs_sort.cuh"
 
@@ -218,18 +219,20 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     }
     __syncwarp();
     if (base + 32 < hi) prefetch(base + 32);
-    constexpr int G = kGroup<PX>;
-    for (int j0 = 0; j0 < nsurv; j0 += G) {
-      float al[G][PX], pw[G][PX], am[G], cr[G], cg_[G], cb[G];
+    // survivors [j0, j0 + NG): alphas first (independent of the transmittance), then the
+    // sequential steps; full groups of kGroup<PX>, the chunk's remainder as one smaller group
+    // (no padded slots)
+    auto group = [&](int j0, auto ng_tag) {
+      constexpr int NG = decltype(ng_tag)::value;
+      float al[NG][PX], pw[NG][PX], am[NG], cr[NG], cg_[NG], cb[NG];
       bool any_near = false;
 #pragma unroll
-      for (int q = 0; q < G; ++q) {
-        const int jj = min(j0 + q, nsurv - 1);
-        const float4 r0 = s0[warp][jj];
-        const float4 r1 = s1[warp][jj];
+      for (int q = 0; q < NG; ++q) {
+        const float4 r0 = s0[warp][j0 + q];
+        const float4 r1 = s1[warp][j0 + q];
         cr[q] = r1.z;
         cg_[q] = r1.w;
-        cb[q] = s2[warp][jj];
+        cb[q] = s2[warp][j0 + q];
         am[q] = r1.y;
         const float dx = __fsub_rn(fx, r0.x);
         const float t1 = __fmul_rn(__fmul_rn(r0.z, dx), dx);
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
       }
       if (__any_sync(0xffffffffu, any_near)) {  // rare: exact exp near the skip threshold
 #pragma unroll
-        for (int q = 0; q < G; ++q)
+        for (int q = 0; q < NG; ++q)
 #pragma unroll
           for (int u = 0; u < PX; ++u) {
             bool nr;
@@ -253,14 +256,20 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
           }
       }
 #pragma unroll
-      for (int q = 0; q < G; ++q) {
-        if (j0 + q >= nsurv) break;
+      for (int q = 0; q < NG; ++q) {
         const uint32_t k = sk[warp][j0 + q];
 #pragma unroll
         for (int u = 0; u < PX; ++u)
           blend_apply<CONTRIB>(ps[u], pw[q][u], al[q][u], cr[q], cg_[q], cb[q], k);
       }
-    }
+    };
+    constexpr int G = kGroup<PX>;
+    int j0 = 0;
+    for (; j0 + G <= nsurv; j0 += G) group(j0, std::integral_constant<int, G>{});
+    const int rem = nsurv - j0;  // warp-uniform
+    if (rem == 1) group(j0, std::integral_constant<int, 1>{});
+    else if (rem == 2) group(j0, std::integral_constant<int, 2>{});
+    else if (G == 4 && rem == 3) group(j0, std::integral_constant<int, G == 4 ? 3 : 1>{});
     __syncwarp();
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
