@@ -34,6 +34,7 @@
 int fgs_internal_fail(fgs_context* ctx, int code, const char* msg);
 cudaStream_t fgs_internal_stream(fgs_context* ctx);
 int fgs_internal_device(fgs_context* ctx);
+float* fgs_internal_scratch_image(fgs_context* ctx, size_t floats);  // context-owned, grows only
 int fgs_internal_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                           const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads,
                           const std::function<int(int, int64_t, int64_t)>& chunk_done);
@@ -234,7 +235,7 @@ int fgs_fwd_bwd_views(fgs_context* ctx, fgs_comm* comm, const fgs_gaussians* sce
   size_t scratch_px = 0;
   for (int v = 0; v < nviews; ++v)
     if (!images || !images[v]) scratch_px = std::max(scratch_px, static_cast<size_t>(cameras[v].width) * cameras[v].height);
-  if (scratch_px && cudaMallocAsync(reinterpret_cast<void**>(&scratch), scratch_px * 3 * sizeof(float), st) != cudaSuccess)
+  if (scratch_px && !(scratch = fgs_internal_scratch_image(ctx, scratch_px * 3)))
     return fgs_internal_fail(ctx, FGS_ENOMEM, "fwd_bwd_views: image scratch");
   int rc = FGS_OK;
   for (int v = 0; v < nviews && rc == FGS_OK; ++v) {
@@ -268,7 +269,6 @@ int fgs_fwd_bwd_views(fgs_context* ctx, fgs_comm* comm, const fgs_gaussians* sce
         rc = fgs_internal_fail(ctx, FGS_ECUDA, "fwd_bwd_views: zero gradients");
   }
   if (rc == FGS_OK && comm && nviews == 0) rc = fgs_allreduce_gradients(comm, grads, n);
-  if (scratch) cudaFreeAsync(scratch, st);
   return rc;
 }
 

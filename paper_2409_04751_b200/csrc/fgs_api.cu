@@ -804,6 +804,9 @@ int fgs_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera*
 int fgs_internal_fail(fgs_context* ctx, int code, const char* msg) { return fail(ctx, code, msg); }
 cudaStream_t fgs_internal_stream(fgs_context* ctx) { return ctx->stream; }
 int fgs_internal_device(fgs_context* ctx) { return ctx->device; }
+float* fgs_internal_scratch_image(fgs_context* ctx, size_t floats) {
+  return ctx->t_image.ensure(floats) == cudaSuccess ? ctx->t_image.p : nullptr;
+}
 int fgs_internal_backward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                           const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads,
                           const std::function<int(int, int64_t, int64_t)>& chunk_done) {

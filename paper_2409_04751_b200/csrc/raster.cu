@@ -496,25 +496,24 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
     }
     if (lane == 0) s_mask[b][warp] = mask;
     float* part = s_part[b][warp];
-    // Groups of 3 surviving splats, latest first. Their alphas are independent of the
-    // transmittance and are computed together; the transmittance/suffix recurrence then runs
-    // in list order, leaving 3 x 9 per-lane gradients (summed over the lane's pixels), which one
-    // butterfly reduce-scatter over the warp sums (31 shuffles); lane l ends with value l.
-    for (uint32_t m = mask; m;) {
-      int js[3];
-      int nv = 0;
+    // Groups of 3 surviving splats, latest first (the chunk's remainder as one smaller group).
+    // Their alphas are independent of the transmittance and are computed together; the
+    // transmittance/suffix recurrence then runs in list order, leaving NG x 9 per-lane gradients
+    // (summed over the lane's pixels), which one butterfly reduce-scatter over the warp sums (31
+    // shuffles); lane l ends with value l.
+    uint32_t m = mask;
+    auto group = [&](auto ng_tag) {
+      constexpr int NG = decltype(ng_tag)::value;
+      int js[NG];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        js[q] = m ? 31 - __clz(m) : js[0];
-        if (m) {
-          m &= ~(1u << js[q]);
-          ++nv;
-        }
+      for (int q = 0; q < NG; ++q) {
+        js[q] = 31 - __clz(m);
+        m &= ~(1u << js[q]);
       }
-      float pw[3][PX], ex[3][PX], ar[3][PX], dys[3][PX];
+      float pw[NG][PX], ex[NG][PX], ar[NG][PX], dys[NG][PX];
       bool any_near = false;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
+      for (int q = 0; q < NG; ++q) {
         const float4 r0 = rec[3 * js[q]];
         const float amax = rec[3 * js[q] + 1].y;
         const float dx = __fsub_rn(fx, r0.x);
@@ -529,7 +528,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
       }
       if (__any_sync(0xffffffffu, any_near)) {  // rare: exact exp near the 1/255 or 0.99 threshold
 #pragma unroll
-        for (int q = 0; q < 3; ++q)
+        for (int q = 0; q < NG; ++q)
 #pragma unroll
           for (int u = 0; u < PX; ++u)
             if (near_threshold(ar[q][u])) {
@@ -537,14 +536,13 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
               ar[q][u] = __fmul_rn(rec[3 * js[q] + 1].y, ex[q][u]);
             }
       }
-      // Branch-free: every lane evaluates all three steps and gates them (a non-contributing
-      // step leaves T and the suffix colour unchanged and gives zero gradients; all operands
-      // are finite: conic <= 1/0.3, one_m >= 0.01).
+      // Branch-free: every lane evaluates all steps and gates them (a non-contributing step
+      // leaves T and the suffix colour unchanged and gives zero gradients; all operands are
+      // finite: conic <= 1/0.3, one_m >= 0.01).
       float v[32];
       bool contrib_any = false;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const bool valid = q < nv;
+      for (int q = 0; q < NG; ++q) {
         const uint32_t kk = cs + js[q];
         const float4 r0 = rec[3 * js[q]], r1 = rec[3 * js[q] + 1];
         const float b2 = rec[3 * js[q] + 2].x;
@@ -555,7 +553,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
           const float alpha = fminf(kAlphaClamp, ar[q][u]);
-          const bool cc = valid && kk < last[u] && pw[q][u] <= 0.0f && pw[q][u] >= kPowerFloor && alpha >= kAlphaSkip;
+          const bool cc = kk < last[u] && pw[q][u] <= 0.0f && pw[q][u] >= kPowerFloor && alpha >= kAlphaSkip;
           contrib_any |= cc;
           const float dy = dys[q][u];
           const float inv = fast_rcp(1.0f - alpha);
@@ -584,7 +582,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
         v[9 * q + 4] = -0.5f * p2;
       }
 #pragma unroll
-      for (int q = 27; q < 32; ++q) v[q] = 0.0f;
+      for (int q = 9 * NG; q < 32; ++q) v[q] = 0.0f;
       if (__any_sync(0xffffffffu, contrib_any)) {
 #pragma unroll
         for (int half = 16; half >= 1; half >>= 1) {
@@ -599,11 +597,17 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
       } else {
         v[0] = 0.0f;
       }
-      // lane l now holds component l % 9 of splat l / 9 (l < 27)
+      // lane l now holds component l % 9 of splat l / 9 (l < 9 NG)
       const int q = lane / 9;
-      const int jq = q == 0 ? js[0] : (q == 1 ? js[1] : js[2]);  // (no dynamic register indexing)
-      if (lane < 27 && q < nv) part[jq * 9 + (lane - 9 * q)] = v[0];
-    }
+      int jq = js[0];  // (no dynamic register indexing)
+#pragma unroll
+      for (int t = 1; t < NG; ++t) jq = q == t ? js[t] : jq;
+      if (lane < 9 * NG) part[jq * 9 + (lane - 9 * q)] = v[0];
+    };
+    const int nsurv = __popc(mask);
+    for (int t = 0; t + 3 <= nsurv; t += 3) group(std::integral_constant<int, 3>{});
+    if (nsurv % 3 == 1) group(std::integral_constant<int, 1>{});
+    else if (nsurv % 3 == 2) group(std::integral_constant<int, 2>{});
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     // ---- per entry of the chunk: the passing warps' sums in warp order, at the emission slot ----
