@@ -98,12 +98,17 @@ __device__ __forceinline__ void cta_prefix(const uint32_t* part, int stride, int
   total = tt;
 }
 
-// Debug phase trace (FGS_FLAG_COUNTERS): thread 0 of CTA `cta` records %globaltimer in slot.
+// Debug phase profile (FGS_FLAG_COUNTERS): thread 0 of CTA `cta` adds the %globaltimer time since
+// its previous call to slot (ns, accumulated over the kernel's loops). Slots: 0 counts + row counts,
+// 1 compaction + tile offsets, 2 the two grid barriers, 3 scatter: rank search + offset staging,
+// 4 slot search + gathers, 5 shared-memory atomics, 6 global atomics, 7 key writes.
 __device__ __forceinline__ void trace(unsigned long long* t, int cta, int slot) {
   if (t && static_cast<int>(blockIdx.x) == cta && threadIdx.x == 0) {
+    static __shared__ unsigned long long prev;
     unsigned long long v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
-    t[slot] = v;
+    if (slot >= 0) t[slot] += v - prev;
+    prev = v;
   }
 }
 
@@ -285,7 +290,7 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
   const int nr = r_hi - r_lo + 1;  // <= kSub: every Gaussian here owns >= 1 slot
   for (int i = tid; i < nr; i += kT) s_off[i] = a.coff[r_lo + i];
   __syncthreads();
-  trace(a.trace, 0, 1);
+  trace(a.trace, 0, 3);
   uint32_t ev[U], gv[U], tv[U], pv[U];
   // each thread owns un <= U consecutive slots (every thread busy when the range is short): one
   // binary search for the first, then a forward walk (a Gaussian owns ~3 slots on average, so
@@ -320,18 +325,18 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
     const int j = static_cast<int>(ev[u] - s_off[tv[u]]);
     tv[u] = static_cast<uint32_t>((rc.z + j / wx) * a.tiles_x + rc.x + j % wx);
   }
-  if (a.trace) { __syncthreads(); trace(a.trace, 0, 3); }
+  if (a.trace) { __syncthreads(); trace(a.trace, 0, 4); }
   if (PRIV) {
 #pragma unroll
     for (int u = 0; u < U; ++u) pv[u] = ev[u] < hi ? atomicAdd(s_cnt + tv[u], 1u) : 1u;
     __syncthreads();
-    trace(a.trace, 0, 4);
+    trace(a.trace, 0, 5);
     // the slot that took local position 0 reserves the CTA's block of tile tv[u]
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (pv[u] == 0) s_cnt[tv[u]] = atomicAdd(a.fill + tv[u], s_cnt[tv[u]]);
     __syncthreads();
-    trace(a.trace, 0, 2);
+    trace(a.trace, 0, 6);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (ev[u] < hi) pv[u] += s_cnt[tv[u]];
@@ -345,6 +350,7 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
     a.keys[pv[u]] = (static_cast<uint64_t>(dk[u]) << 32) | gv[u];
   }
   __syncthreads();  // s_cnt / s_off reused by the next range
+  trace(a.trace, 0, 7);
 }
 
 // K2: one persistent cooperative kernel, two grid barriers.
@@ -373,8 +379,8 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
   uint32_t* rowtot = cur + 32;
   int lo = static_cast<int>(static_cast<int64_t>(a.n) * b / G);
   int hi = static_cast<int>(static_cast<int64_t>(a.n) * (b + 1) / G);
+  trace(a.trace, 0, -1);
   if (a.scatter_only) goto scatter;  // relaunch after the buffers grew: phases 1-2 are done
-  trace(a.trace, 0, 0);
   {
     uint32_t c1 = 0, c2 = 0;
     for (int i = lo + tid; i < hi; i += kT) {
@@ -392,7 +398,9 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
   }
   // rows spread over CTAs first (row ty -> CTA ty mod G), so no CTA gets two
   for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw) row_counts(a, ty, hist, rowtot);
+  trace(a.trace, 0, 0);
   grid.sync();
+  trace(a.trace, 0, 2);
   {
     uint32_t p1, tot1, p2, tot2;
     cta_prefix(a.part_scan, 2, G, sm.warp_tmp, p1, tot1);
@@ -453,9 +461,9 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
       run2 += t2;
     }
   }
-  trace(a.trace, 0, 5);
+  trace(a.trace, 0, 1);
   grid.sync();
-  trace(a.trace, 0, 6);
+  trace(a.trace, 0, 2);
   if (b == 0 && tid < 64) hist[tid] = 0;  // hist + cur: last read before this barrier
 scatter:
   const uint32_t I = a.scalars[kScalarI];
@@ -464,7 +472,6 @@ scatter:
   const uint32_t s_lo = static_cast<uint32_t>(static_cast<uint64_t>(I) * b / gridDim.x);
   const uint32_t s_hi = static_cast<uint32_t>(static_cast<uint64_t>(I) * (b + 1) / gridDim.x);
   for (uint32_t x = s_lo; x < s_hi; x += kSub) scatter_range<PRIV>(a, m, x, min(s_hi, x + kSub), s_cnt, s_off, s_res);
-  trace(a.trace, 0, 7);
 }
 
 // Debug export: the reference's pre-sort key list (source order, ty-major, tx-minor).

@@ -1,5 +1,5 @@
-"""K2 (bin_kernel) phase timeline from %globaltimer stamps (FGS_FLAG_COUNTERS): CTA 0 and the
-tiler CTA. Run on the GPU box: python profiles/bin_trace.py [cfg]"""
+"""K2 (bin_kernel) phase profile of CTA 0 from %globaltimer (FGS_FLAG_COUNTERS): microseconds spent
+per phase, summed over the scatter's sub-ranges. Run on the GPU box: python profiles/bin_trace.py [cfg]"""
 import os
 import sys
 
@@ -9,6 +9,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2409_04751_b200 import Rasterizer, RenderOptions, _lib, synthetic  # noqa: E402
 from tests._helpers import to_device  # noqa: E402
+
+NAMES = ["counts+rows", "compaction+offsets", "grid barriers", "scatter: rank search+staging",
+         "scatter: slot search+gathers", "scatter: smem atomics", "scatter: global atomics", "scatter: key writes"]
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 sc, deg, cams, _ = synthetic.config(cfg, **({"views": 1} if cfg >= 3 else {}))
@@ -21,7 +24,5 @@ for _ in range(3):
     r.forward(ds, cams[0], RenderOptions(sh_degree=deg))
     torch.cuda.synchronize()
     t = r.debug("bin_trace", np.uint64).astype(np.int64)
-    t0 = t[0]
-    names = ["start(cta0)", "scatter: ranks+offs", "scatter: global atomics", "scatter: gathers", "scatter: smem atomics", "phase2 done", "sync2",
-             "scatter done"]
-    print("  ".join(f"{n}={(v - t0) / 1000:.1f}us" for n, v in zip(names, t)))
+    print(f"cfg{cfg} I={r.counts()['num_intersections']} " + "  ".join(f"{n}={v / 1000:.1f}us" for n, v in zip(NAMES, t)),
+          f" total={t.sum() / 1000:.1f}us")
