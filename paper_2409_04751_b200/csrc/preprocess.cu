@@ -325,9 +325,18 @@ struct Proj {
   float det;
 };
 
-// splatting.hpp:83-97. Returns -1 invisible, 2 degenerate, 1 ok, 3 zero quaternion.
+// splatting.hpp:83-97. Returns -1 invisible, 2 degenerate, 1 ok, 3 zero quaternion. prefetch: the
+// Gaussian's SH row, requested into L1 as soon as the Gaussian is known to be in the field of
+// view, so its load after the projection finds it there.
+__device__ __forceinline__ void prefetch_row(const float* p) {
+  if (!p) return;
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 32));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 47));
+}
+
 __device__ __forceinline__ int project_covariance(const DevCamera& cam, const float m[3], const float4 q,
-                                                  const float ls[3], Proj& P) {
+                                                  const float ls[3], Proj& P, const float* prefetch = nullptr) {
   world_to_camera(cam, m, P.mu);
   const float x = P.mu[0], y = P.mu[1], z = P.mu[2];
   const float r2 = x * x + y * y + z * z;
@@ -337,6 +346,7 @@ __device__ __forceinline__ int project_covariance(const DevCamera& cam, const fl
     if (z < 0.0f && lz2 < 1e-24f * z * z) return -1;
     const float theta = cr_atan2f(sqrtf(lz2), z);
     if (!(theta <= cam.fov_max + kFisheyeCullMargin)) return -1;
+    prefetch_row(prefetch);
     P.ft = fisheye_terms(lz2, z, theta);
     const float g = P.ft.g;
     P.pix[0] = cam.cx + cam.fx * g * x;
@@ -347,6 +357,7 @@ __device__ __forceinline__ int project_covariance(const DevCamera& cam, const fl
     P.pix[0] = cam.cx + cam.fx * x / z;
     P.pix[1] = cam.cy + cam.fy * y / z;
     if (!(z > kPinholeNearClip)) return -1;
+    prefetch_row(prefetch);
     pinhole_jacobian(P.mu, cam, P.j);
   } else {
     const float s = x * x + z * z;
@@ -356,6 +367,7 @@ __device__ __forceinline__ int project_covariance(const DevCamera& cam, const fl
     if (xp >= w) xp -= w;
     P.pix[0] = xp;
     P.pix[1] = h * (cr_atan2f(y, sqrtf(s)) + kPi / 2.0f) / kPi;
+    prefetch_row(prefetch);
     panorama_jacobian(P.mu, cam, P.j);
   }
 #pragma unroll
@@ -416,7 +428,8 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
   const float4 q = valid ? ld4(a.rotations + 4 * i, a.vec_rot) : make_float4(1.f, 0.f, 0.f, 0.f);
   // host scene: every lane reads its opacity (one coalesced 128-byte run per warp over PCIe
   // instead of scattered 4-byte reads by the kept lanes)
-  const float op_host = HOST_SCENE && valid ? __ldg(a.opacity + i) : 0.0f;
+  const float op = valid ? __ldg(a.opacity + i) : 0.0f;  // issued early (coalesced; the host scene reads
+                                                        // it as one 128-byte run per warp over PCIe)
 
   uint8_t state = 0;
   uint32_t key = 0xFFFFFFFFu, touched = 0;
@@ -426,7 +439,8 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
   float r2v = 0.f;
 
   Proj P;
-  const int pc = valid ? project_covariance(cam, m, q, ls, P) : -1;
+  const int pc = valid ? project_covariance(cam, m, q, ls, P, (!HOST_SCENE && a.sh_degree > 0) ? a.sh + 48 * i : nullptr)
+                       : -1;
   bool keep = false;
   float mx = 0.f, my = 0.f, rf = 0.f;
   if (pc == 3) {
@@ -475,7 +489,7 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
       col[ch] = sh_channel(k, Y, a.sh_degree);
     }
     const float col0 = col[0], col1 = col[1], col2 = col[2];
-    const float alpha = sigmoid(HOST_SCENE ? op_host : __ldg(a.opacity + i));
+    const float alpha = sigmoid(op);
     r0 = make_float4(mx, my, ca, cb);
     r1 = make_float4(cc, alpha, col0, col1);
     r2v = col2;
