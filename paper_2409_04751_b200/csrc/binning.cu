@@ -1,4 +1,4 @@
-// binning.cu — K2: intersection scan, tile ranges, key duplication and per-tile sort.
+// binning.cu — K2: intersection scan, tile ranges and key scatter (one cooperative kernel).
 //
 // Ordering contract (reference inc/splatting.hpp:192-249): the per-tile
 // lists are sorted by (tile id, depth key bits, source index). The reference duplicates keys
@@ -7,15 +7,18 @@
 //
 //   K1 (preprocess.cu) also adds each kept Gaussian's tile rectangle into a row-difference
 //      array over the tile grid (+1 at (ty, tx0), -1 at (ty, tx1 + 1) for each of its rows);
-//   K2 bin_kernel (persistent cooperative): exclusive scan of the per-Gaussian tile counts in
-//      source order -> emission offset of every tile-touching Gaussian (compacted list), the
-//      intersection count I; one warp per tile row turns the row-difference array into per-tile
-//      counts, the tile ranges (offsets[0..T]) and the blend schedule;
-//   [host reads I (16 bytes) to size the per-intersection buffers]
-//   K2b: each intersection (Gaussian g, tile t) claims a position in tile t's range with
-//      one atomicAdd and writes the 64-bit key (depth_key << 32 | g);
-//   K2c tile_sort_kernel: one CTA per tile sorts its keys (bitonic, in shared memory up to 4096
-//      entries, a chunked global/shared hybrid beyond) and writes the sorted Gaussian list.
+//   K2 bin_kernel (persistent cooperative, two grid barriers):
+//      phase 1: per-CTA counts of tile-touching Gaussians / intersections; one warp per tile
+//               row turns the row-difference array into per-tile counts, row totals, the
+//               schedule histogram, the longest list and the backward's segment count;
+//      phase 2: exclusive scan in source order -> emission offset of every tile-touching
+//               Gaussian (compacted list), I, the gradient-chunk boundaries; the tile ranges
+//               (offsets[0..T]), scatter cursors and the blend schedule;
+//      phase 3: each intersection (Gaussian g, tile t) claims a position in tile t's range
+//               (per-CTA shared-memory counts, one global atomicAdd per (CTA, tile)) and its
+//               64-bit key (depth_key << 32 | g) is written there;
+//   [host reads I and the frame's scalars, off the critical path; K3 is already queued]
+//   K3 (raster.cu) sorts each tile's keys at the start of its CTA (fgs_sort.cuh).
 //
 // The key is the reference's own sort key within a tile, (depth key bits, source index), so
 // sorting a tile's keys gives the reference's order bit-exactly, whatever order the atomics

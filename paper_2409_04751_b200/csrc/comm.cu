@@ -20,6 +20,7 @@
 
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstring>
 #include <functional>
@@ -127,6 +128,12 @@ ncclResult_t allreduce_range(fgs_comm* c, fgs_gradients* g, int64_t id0, int64_t
 
 }  // namespace
 
+namespace {
+int fwd_bwd_views_impl(fgs_context* ctx, fgs_comm* comm, const fgs_gaussians* scene, const fgs_camera* cameras,
+                       int nviews, const float* const* dl_dimages, const fgs_render_options* ropt,
+                       const fgs_backward_options* bopt, fgs_gradients* grads, float* const* images);
+}  // namespace
+
 extern "C" {
 
 int fgs_comm_get_unique_id(uint8_t id[128]) {
@@ -222,6 +229,18 @@ int fgs_fwd_bwd_views(fgs_context* ctx, fgs_comm* comm, const fgs_gaussians* sce
                       int nviews, const float* const* dl_dimages, const fgs_render_options* ropt,
                       const fgs_backward_options* bopt, fgs_gradients* grads, float* const* images) {
   if (!ctx) return FGS_EINVAL;
+  nvtxRangePushA("fgs.fwd_bwd_views");
+  const int rc = fwd_bwd_views_impl(ctx, comm, scene, cameras, nviews, dl_dimages, ropt, bopt, grads, images);
+  nvtxRangePop();
+  return rc;
+}
+
+}  // extern "C"
+
+namespace {
+int fwd_bwd_views_impl(fgs_context* ctx, fgs_comm* comm, const fgs_gaussians* scene, const fgs_camera* cameras,
+                       int nviews, const float* const* dl_dimages, const fgs_render_options* ropt,
+                       const fgs_backward_options* bopt, fgs_gradients* grads, float* const* images) {
   if (!scene || (nviews > 0 && (!cameras || !dl_dimages)) || !grads || nviews < 0)
     return fgs_internal_fail(ctx, FGS_EINVAL, "fwd_bwd_views: null argument");
   if (comm && comm->ctx != ctx) return fgs_internal_fail(ctx, FGS_EINVAL, "fwd_bwd_views: communicator of another context");
@@ -271,5 +290,4 @@ int fgs_fwd_bwd_views(fgs_context* ctx, fgs_comm* comm, const fgs_gaussians* sce
   if (rc == FGS_OK && comm && nviews == 0) rc = fgs_allreduce_gradients(comm, grads, n);
   return rc;
 }
-
-}  // extern "C"
+}  // namespace

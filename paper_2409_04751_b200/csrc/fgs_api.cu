@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fgs.h"
 #include "fgs_kernels.h"
 
@@ -166,6 +168,13 @@ struct fgs_context {
 };
 
 namespace {
+
+// NVTX ranges around the public calls and markers at each stage launch (header-only NVTX 3: a
+// few nanoseconds when no tool is attached), so an nsys / ncu timeline shows the path's stages.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail(fgs_context* c, int code, const std::string& msg) {
   if (c) c->err = msg;
@@ -407,6 +416,7 @@ static int blend_ellipse() {
 int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                 const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
   if (!ctx) return FGS_EINVAL;
+  NvtxRange nvtx("fgs.forward");
   if (!scene || !camera || !image) return fail(ctx, FGS_EINVAL, "forward: null argument");
   if (camera->model != FGS_CAMERA_FISHEYE && camera->model != FGS_CAMERA_PINHOLE &&
       camera->model != FGS_CAMERA_PANORAMA)
@@ -497,6 +507,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     pa.vec_geo = aligned16(scene->means) && aligned16(scene->log_scales);
     pa.error_flag = reinterpret_cast<int*>(scalars + 1);
     pa.state_counts = scalars + 2;
+    nvtxMarkA("K1 preprocess");
     fgs::preprocess_launch(pa, ctx->scene_on_host, st);
     ++launches;
   }
@@ -525,6 +536,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.trace = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p + 16 : nullptr;
   if (n > 0) {
     ctx->rowdiff_clean = 0;  // dirty until K2 has consumed K1's counts
+    nvtxMarkA("K2 binning");
     FGS_CHECK(fgs::bin_launch(bn, st));
     ctx->rowdiff_clean = ndiff;
     ++launches;
@@ -589,6 +601,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     ba.keys = ctx->keys.p;
     ba.sorted_gauss = ctx->sorted_gauss.p;
     // work decomposition from this frame's statistics once known, else the last frame's
+    nvtxMarkA("K3 sort + blend");
     const int px = rule_fwd_px(ctx->num_isect, num_tiles, ctx->longest);
     ctx->var_fwd_px = px;
     const int l = fgs::blend_forward(ba, ctx->num_isect, px, st);
@@ -682,6 +695,7 @@ int backward_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera
                   const fgs_backward_options* options, fgs_gradients* grads,
                   const std::function<int(int, int64_t, int64_t)>& chunk_done) {
   if (!ctx) return FGS_EINVAL;
+  NvtxRange nvtx("fgs.backward");
   if (!scene || !camera || !dl_dimage || !grads) return fail(ctx, FGS_EINVAL, "backward: null argument");
   if (!ctx->have_fwd) return fail(ctx, FGS_ESTATE, "backward: no forward context");
   if (scene->n != ctx->n) return fail(ctx, FGS_EINVAL, "backward: forward context was built for a different scene");
@@ -730,6 +744,7 @@ int backward_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera
   SetGuard guard{ctx, timing};
   if (timing) cudaEventRecord(ev[0], st);
   if (I > 0) {
+    nvtxMarkA("K4a blend backward");
     ctx->launches += fgs::blend_backward(ba, I, 0, st, &ctx->var_bwd_px);
   }
   if (timing) cudaEventRecord(ev[1], st);
