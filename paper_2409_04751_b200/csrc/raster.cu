@@ -458,18 +458,21 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   auto prefetch = [&](int c) {  // records of chunk c into s_rec[c & 1], its slots into s_slot[c % 3]
     if (c < nch) {
       const uint32_t cs = chunk_lo(c), n = top - 32 * c - cs;
-      if (tid < 96) {
-        const uint32_t j = tid / 3, q = tid - 3 * j;
-        if (j < n) {
-          const float4* src = reinterpret_cast<const float4*>(a.rec + __ldg(a.sorted_gauss + cs + j)) + q;
-          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_rec[c & 1][tid]));
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-        }
-      } else if (tid < 128) {
-        const uint32_t j = tid - 96;
-        if (j < n) {
-          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_slot[c % 3][j]));
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(a.sorted_slot + cs + j) : "memory");
+#pragma unroll
+      for (int t = tid; t < 128; t += NT) {  // 96 record pieces, then 32 slots
+        if (t < 96) {
+          const uint32_t j = t / 3, q = t - 3 * j;
+          if (j < n) {
+            const float4* src = reinterpret_cast<const float4*>(a.rec + __ldg(a.sorted_gauss + cs + j)) + q;
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_rec[c & 1][t]));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+          }
+        } else {
+          const uint32_t j = t - 96;
+          if (j < n) {
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_slot[c % 3][j]));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(a.sorted_slot + cs + j) : "memory");
+          }
         }
       }
     }
