@@ -152,9 +152,12 @@ int fgs_last_transfer(const fgs_context* ctx, uint64_t out[2]);
  * and records the binning phase trace; FGS_FLAG_TIMING records CUDA events around every stage
  * (read with fgs_timing). FGS_FLAG_BLEND_COUNT makes the forward also write the per-pixel
  * contribution count (ForwardContext::blend_count, inc/splatting.hpp:299-301; debug name
- * "blend_count", u16[H*W]; also written with FGS_FLAG_COUNTERS). FGS_FLAG_KEEP_KEYS is reserved
+ * "blend_count", u16[H*W]; also written with FGS_FLAG_COUNTERS). FGS_FLAG_ROW_SCATTER /
+ * FGS_FLAG_SLOT_SCATTER force the binning scatter's work order (tile-row lists / source-order
+ * emission slots; default: by the intersection count; same keys either way). FGS_FLAG_KEEP_KEYS is reserved
  * (no effect). Default 0. */
-enum { FGS_FLAG_COUNTERS = 1, FGS_FLAG_KEEP_KEYS = 2, FGS_FLAG_TIMING = 4, FGS_FLAG_BLEND_COUNT = 8 };
+enum { FGS_FLAG_COUNTERS = 1, FGS_FLAG_KEEP_KEYS = 2, FGS_FLAG_TIMING = 4, FGS_FLAG_BLEND_COUNT = 8,
+       FGS_FLAG_ROW_SCATTER = 16, FGS_FLAG_SLOT_SCATTER = 32 };
 int fgs_set_flags(fgs_context* ctx, uint32_t flags);
 
 /* Device time per stage accumulated from CUDA events while FGS_FLAG_TIMING is set, and the
@@ -173,8 +176,9 @@ int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s);
  *   "key_tile"/"key_depth"/"key_gauss" u32[I] (pre-sort keys in the reference's emission order),
  *   "sorted_gauss" u32[I], "sorted_tile" u32[I], "offsets" u32[T+1] (tile ranges),
  *   "keys" u64[I] (depth key << 32 | Gaussian id, as the binning scatter wrote them into each tile's
- *   range), "rect" u16[N*4] (tile rectangle tx0, tx1, ty0, ty1 per Gaussian), "variants" u32[4]
- *   (forward pixels per lane, backward pixels per lane, K4b CTAs per SM, longest tile list),
+ *   range), "rect" u16[N*4] (tile rectangle tx0, tx1, ty0, ty1 per Gaussian), "variants" u32[5]
+ *   (forward pixels per lane, backward pixels per lane, K4b CTAs per SM, longest tile list, binning
+ *   scatter by tile-row lists),
  *   "aux_bytes" u64[1] (device bytes the render/backward path holds, backward scratch included),
  *   "compact_gauss"/"compact_offsets" u32[M], "final_T" f32[H*W], "last" u32[H*W],
  *   "counters" u64[4] (E_eval, E_contrib, culled evaluations, max CTA cycles; with

@@ -39,7 +39,6 @@ namespace {
 constexpr int kT = kBinThreads;       // threads per persistent CTA
 constexpr int kW = kBinThreads / 32;  // warps per persistent CTA
 constexpr int kItems = 8;             // items per thread per sub-tile (thread-contiguous)
-constexpr int kSub = 8192;            // emission slots per scatter sub-range
 constexpr int kSchedBuckets = 18;     // blend schedule: log2 list-length buckets
 constexpr int kPrivTiles = 16384;     // scatter: per-CTA shared tile counters up to this many tiles
 
@@ -102,9 +101,9 @@ __device__ __forceinline__ void cta_prefix(const uint32_t* part, int stride, int
 }
 
 // Debug phase profile (FGS_FLAG_COUNTERS): thread 0 of CTA `cta` adds the %globaltimer time since
-// its previous call to slot (ns, accumulated over the kernel's loops). Slots: 0 counts + row counts,
-// 1 compaction + tile offsets, 2 the two grid barriers, 3 scatter: rank search + offset staging,
-// 4 slot search + gathers, 5 shared-memory atomics, 6 global atomics, 7 key writes.
+// its previous call to slot (ns, accumulated over the kernel's loops). Slots: 0 counts, row counts
+// and row histograms, 1 compaction, tile offsets and row lists, 2 the two grid barriers, 3 scatter:
+// counter zeroing, 4 count pass, 5 (unused), 6 tile reservations (global atomics), 7 key pass.
 __device__ __forceinline__ void trace(unsigned long long* t, int cta, int slot) {
   if (t && static_cast<int>(blockIdx.x) == cta && threadIdx.x == 0) {
     static __shared__ unsigned long long prev;
@@ -281,6 +280,8 @@ __device__ void cta_upper_rank2(const uint32_t* offs, int m, uint32_t v0, uint32
 // tile with shared-memory atomics, then one global atomicAdd per (CTA, tile) reserves the
 // block, so a heavy tile sees one global atomic per CTA instead of one per intersection. All
 // loads and atomics of a thread's slots are issued before their results are used.
+constexpr int kSub = 8192;  // emission slots per source-order scatter sub-range
+
 template <bool PRIV>
 __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi, uint32_t* s_cnt, uint32_t* s_off,
                               uint32_t* s_res) {
@@ -354,6 +355,139 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
   }
   __syncthreads();  // s_cnt / s_off reused by the next range
   trace(a.trace, 0, 7);
+  trace(a.trace, 0, 7);
+}
+
+constexpr int kMaxRows = kMaxTileRows;  // tile rows the row-list phases keep in shared memory
+
+// The row lists' layout (every CTA, from the row histograms of all CTAs): s_start[ty] = first
+// entry of row ty in the concatenated row lists (s_start[tiles_y] = entries), s_cur[ty] = where
+// this CTA's entries of row ty begin (rows in order, CTAs in order within a row).
+__device__ void row_layout(const BinArgs& a, uint32_t* s_start, uint32_t* s_cur, uint32_t* s_warp) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+  for (int ty = warp; ty < a.tiles_y; ty += kW) {
+    uint32_t tot = 0, pre = 0;
+    for (int c = lane; c < G; c += 32) {
+      const uint32_t v = a.row_hist[static_cast<size_t>(c) * a.tiles_y + ty];
+      tot += v;
+      if (c < b) pre += v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      pre += __shfl_xor_sync(0xffffffffu, pre, o);
+    }
+    if (lane == 0) {
+      s_start[ty] = tot;
+      s_cur[ty] = pre;
+    }
+  }
+  __syncthreads();
+  // exclusive scan of the row totals (kMaxRows / kT = 4 rows per thread)
+  constexpr int R = kMaxRows / kT;
+  uint32_t v[R], sum = 0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int ty = tid * R + k;
+    v[k] = ty < a.tiles_y ? s_start[ty] : 0u;
+    sum += v[k];
+  }
+  uint32_t total;
+  uint32_t run = block_exclusive_scan(sum, s_warp, &total);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const int ty = tid * R + k;
+    if (ty < a.tiles_y) {
+      s_start[ty] = run;
+      s_cur[ty] += run;
+    }
+    run += v[k];
+  }
+  if (tid == 0) s_start[a.tiles_y] = total;
+  __syncthreads();
+}
+
+// The CTA's row-list entries for one tile-touching Gaussian i: listed once per tile row its
+// rectangle covers (positions from the CTA's per-row cursors; order within a row free).
+__device__ __forceinline__ void row_emit_one(const BinArgs& a, int i, uint32_t* s_cur) {
+  const ushort4 rc = a.rect[i];
+  for (int ty = rc.z; ty <= rc.w; ++ty) a.row_list[atomicAdd(s_cur + ty, 1u)] = static_cast<uint32_t>(i);
+}
+
+__device__ void row_emit(const BinArgs& a, int lo, int hi, uint32_t* s_cur) {
+  for (int i = lo + static_cast<int>(threadIdx.x); i < hi; i += kT)
+    if (a.touched[i]) row_emit_one(a, i, s_cur);
+  __syncthreads();
+}
+
+// Row of row-list entry e: the last row whose start is <= e (s_start ascending).
+__device__ __forceinline__ int row_of(const uint32_t* s_start, int rows, uint32_t e) {
+  int l = 0, h = rows - 1;
+  while (l < h) {
+    const int mid = (l + h + 1) >> 1;
+    if (s_start[mid] <= e) l = mid;
+    else h = mid - 1;
+  }
+  return l;
+}
+
+// Phase 3: the intersections of row-list entries [e0, e1) -- a contiguous run of the row-major
+// lists, so it spans one or a few tile rows and touches few tiles: the CTA counts its slots per
+// tile in shared memory, reserves each tile's block with one global atomicAdd on the tile's
+// cursor (few CTAs share a row, so little contention), then writes the keys at their positions.
+// Rows are taken in windows whose tiles fit the shared counters; a single row wider than that
+// falls back to one global atomic per slot.
+__device__ void scatter_rows(const BinArgs& a, uint32_t e0, uint32_t e1, const uint32_t* s_start, uint32_t* s_cnt) {
+  const int tid = threadIdx.x;
+  if (e0 >= e1) return;
+  const int tx = a.tiles_x;
+  int ty = row_of(s_start, a.tiles_y, e0);
+  const int ty_last = row_of(s_start, a.tiles_y, e1 - 1);
+  while (ty <= ty_last) {
+    // window of rows [ty, ty_end]
+    const int rows_fit = max(1, kPrivTiles / tx);
+    const int ty_end = min(ty_last, ty + rows_fit - 1);
+    const uint32_t w0 = max(e0, s_start[ty]), w1 = min(e1, s_start[ty_end + 1]);
+    const int span0 = ty * tx, span = (ty_end - ty + 1) * tx;
+    if (span <= kPrivTiles) {
+      for (int t = tid; t < span; t += kT) s_cnt[t] = 0;
+      __syncthreads();
+      trace(a.trace, 0, 3);
+      // (a thread's entries ascend, so its row only moves forward)
+      int r = ty;
+      for (uint32_t e = w0 + tid; e < w1; e += kT) {
+        while (s_start[r + 1] <= e) ++r;
+        const ushort4 rc = a.rect[a.row_list[e]];
+        for (int x = rc.x; x <= rc.y; ++x) atomicAdd(s_cnt + (r * tx + x - span0), 1u);
+      }
+      __syncthreads();
+      trace(a.trace, 0, 4);
+      for (int t = tid; t < span; t += kT)
+        if (s_cnt[t]) s_cnt[t] = atomicAdd(a.fill + span0 + t, s_cnt[t]);
+      __syncthreads();
+      trace(a.trace, 0, 6);
+      r = ty;
+      for (uint32_t e = w0 + tid; e < w1; e += kT) {
+        while (s_start[r + 1] <= e) ++r;
+        const uint32_t g = a.row_list[e];
+        const ushort4 rc = a.rect[g];
+        const uint64_t key = (static_cast<uint64_t>(a.depth_key[g]) << 32) | g;
+        for (int x = rc.x; x <= rc.y; ++x) a.keys[atomicAdd(s_cnt + (r * tx + x - span0), 1u)] = key;
+      }
+      __syncthreads();
+      trace(a.trace, 0, 7);
+    } else {
+      for (uint32_t e = w0 + tid; e < w1; e += kT) {
+        const int r = row_of(s_start, a.tiles_y, e);
+        const uint32_t g = a.row_list[e];
+        const ushort4 rc = a.rect[g];
+        const uint64_t key = (static_cast<uint64_t>(a.depth_key[g]) << 32) | g;
+        for (int x = rc.x; x <= rc.y; ++x) a.keys[atomicAdd(a.fill + r * tx + x, 1u)] = key;
+      }
+    }
+    ty = ty_end + 1;
+  }
 }
 
 // K2: one persistent cooperative kernel, two grid barriers.
@@ -366,12 +500,18 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
 //   phase 3: all CTAs scatter the I emission slots (balanced by intersections) into the tile
 //            ranges -- unless I exceeds the buffers' capacity (speculative launch: the host
 //            grows them and launches again).
-template <bool PRIV>
+// ROWS: phase 3 by row lists (few tiles per CTA: little contention on the tile cursors; wins for
+// large I, configs 3 and 4) or by emission slots in source order (no row-list passes; config 2).
+template <bool ROWS>
 __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
-  extern __shared__ uint32_t s_cnt[];  // [num_tiles] (PRIV)
+  extern __shared__ uint32_t s_cnt[];  // [min(num_tiles, kPrivTiles)] phase-3 tile counters
   __shared__ ScanSmem sm;
-  __shared__ uint32_t s_off[kSub];
+  __shared__ uint32_t s_rowoff[kW * 64];         // row_offsets scratch, 64 words per warp
+  __shared__ uint32_t s_big[2 * kMaxRows + 8];   // ROWS: s_start + s_cur; else the scatter's s_off
   __shared__ uint32_t s_res[2];
+  static_assert(2 * kMaxRows + 8 >= kSub, "s_off fits");
+  uint32_t* s_start = s_big;                     // row lists: first entry of every tile row
+  uint32_t* s_cur = s_big + kMaxRows + 4;        // this CTA's next entry of every tile row
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x;
   const int G = static_cast<int>(gridDim.x);
@@ -385,11 +525,24 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
   trace(a.trace, 0, -1);
   if (a.scatter_only) goto scatter;  // relaunch after the buffers grew: phases 1-2 are done
   {
+    // counts, and (ROWS) the CTA's row histogram (per tile row, the tile-touching Gaussians covering it)
+    if (ROWS) {
+      for (int t = tid; t < a.tiles_y; t += kT) s_cur[t] = 0;
+      __syncthreads();
+    }
     uint32_t c1 = 0, c2 = 0;
     for (int i = lo + tid; i < hi; i += kT) {
       const uint32_t t = a.touched[i];
       c1 += t > 0 ? 1u : 0u;
       c2 += t;
+      if (ROWS && t) {
+        const ushort4 rc = a.rect[i];
+        for (int ty = rc.z; ty <= rc.w; ++ty) atomicAdd(s_cur + ty, 1u);
+      }
+    }
+    if (ROWS) {
+      __syncthreads();
+      for (int t = tid; t < a.tiles_y; t += kT) a.row_hist[static_cast<size_t>(b) * a.tiles_y + t] = s_cur[t];
     }
     uint32_t t1, t2;
     block_exclusive_scan(c1, sm.warp_tmp, &t1);
@@ -429,7 +582,11 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
       if (lane == 0) a.scalars[kScalarBig] = big;
     }
     for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw)
-      row_offsets(a, ty, rowtot, hist, cur, bprefix, s_off + 64 * (tid >> 5));  // s_off: free until the scatter
+      row_offsets(a, ty, rowtot, hist, cur, bprefix, s_rowoff + 64 * (tid >> 5));
+    // the row lists' layout; their entries are written with the compaction (<= I entries: they
+    // fit the per-intersection buffers when I does)
+    if (ROWS) row_layout(a, s_start, s_cur, sm.warp_tmp);
+    const bool emit = ROWS && tot2 <= a.isect_cap;
     uint32_t run1 = p1, run2 = p2;
     int gchunk[kGradChunks];
 #pragma unroll
@@ -458,6 +615,7 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
           a.src_off[r0 + i] = off;
           ++pos;
           off += c[i];
+          if (emit) row_emit_one(a, r0 + i, s_cur);
         }
       }
       run1 += t1;
@@ -468,13 +626,35 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
   grid.sync();
   trace(a.trace, 0, 2);
   if (b == 0 && tid < 64) hist[tid] = 0;  // hist + cur: last read before this barrier
-scatter:
+  if (ROWS) {
+    const uint32_t I = a.scalars[kScalarI];
+    if (I > a.isect_cap || I == 0) return;
+    const uint32_t E = s_start[a.tiles_y];
+    scatter_rows(a, static_cast<uint32_t>(static_cast<uint64_t>(E) * b / G),
+                 static_cast<uint32_t>(static_cast<uint64_t>(E) * (b + 1) / G), s_start, s_cnt);
+    return;
+  }
+scatter : {
   const uint32_t I = a.scalars[kScalarI];
   if (I > a.isect_cap || I == 0) return;
-  const int m = static_cast<int>(a.scalars[kScalarM]);
-  const uint32_t s_lo = static_cast<uint32_t>(static_cast<uint64_t>(I) * b / gridDim.x);
-  const uint32_t s_hi = static_cast<uint32_t>(static_cast<uint64_t>(I) * (b + 1) / gridDim.x);
-  for (uint32_t x = s_lo; x < s_hi; x += kSub) scatter_range<PRIV>(a, m, x, min(s_hi, x + kSub), s_cnt, s_off, s_res);
+  if (ROWS) {
+    // relaunch after the buffers grew: phases 1-2 ran (row histograms in row_hist); the row
+    // lists are written now, then the scatter
+    row_layout(a, s_start, s_cur, sm.warp_tmp);
+    row_emit(a, lo, hi, s_cur);
+    grid.sync();
+    const uint32_t E = s_start[a.tiles_y];
+    scatter_rows(a, static_cast<uint32_t>(static_cast<uint64_t>(E) * b / G),
+                 static_cast<uint32_t>(static_cast<uint64_t>(E) * (b + 1) / G), s_start, s_cnt);
+  } else {
+    // the emission slots, balanced by intersections, in source order
+    const int m = static_cast<int>(a.scalars[kScalarM]);
+    const uint32_t s_lo = static_cast<uint32_t>(static_cast<uint64_t>(I) * b / G);
+    const uint32_t s_hi = static_cast<uint32_t>(static_cast<uint64_t>(I) * (b + 1) / G);
+    for (uint32_t x = s_lo; x < s_hi; x += kSub)
+      scatter_range<true>(a, m, x, min(s_hi, x + kSub), s_cnt, s_big, s_res);
+  }
+}
 }
 
 // Debug export: the reference's pre-sort key list (source order, ty-major, tx-minor).
@@ -501,32 +681,33 @@ int grid_size() {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(bin_kernel<true>), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kPrivTiles * 4);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin_kernel<true>, kT, kPrivTiles * 4);
-    int per_sm2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, bin_kernel<false>, kT, 0);
-    return (per_sm > 0 && per_sm2 > 0) ? sms : -1;  // -1: cooperative launch impossible
+    int ok = 1;
+    for (const void* f : {reinterpret_cast<const void*>(bin_kernel<true>), reinterpret_cast<const void*>(bin_kernel<false>)}) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrivTiles * 4);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kT, kPrivTiles * 4);
+      ok = ok && per_sm > 0;
+    }
+    return ok ? sms : -1;  // -1: cooperative launch impossible
   });
 }
 
 }  // namespace
 
 size_t bin_part_words(int tiles_y) { return static_cast<size_t>(std::max(grid_size(), 0)) * 2 + 64 + tiles_y; }
+size_t bin_row_hist_words(int tiles_y) { return static_cast<size_t>(std::max(grid_size(), 0)) * tiles_y; }
 
 cudaError_t bin_launch(BinArgs& a, cudaStream_t st) {
   const int g = grid_size();
   if (g < 2) return cudaErrorCooperativeLaunchTooLarge;
+  if (a.tiles_y > kMaxRows) return cudaErrorInvalidValue;
   void* args[] = {&a};
-  static const int priv_env = [] {
-    const char* v = std::getenv("FGS_SCATTER_PRIV");
-    return v ? std::atoi(v) : -1;
-  }();
-  if (a.num_tiles <= kPrivTiles && priv_env != 0)
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bin_kernel<true>), g, kT, args,
-                                       a.num_tiles * 4, st);
-  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bin_kernel<false>), g, kT, args, 0, st);
+  const size_t smem = static_cast<size_t>(std::min(a.num_tiles, kPrivTiles)) * 4;
+  // the source-order scatter needs every tile's counter in shared memory
+  const bool rows = a.row_scatter || a.num_tiles > kPrivTiles;
+  return cudaLaunchCooperativeKernel(rows ? reinterpret_cast<const void*>(bin_kernel<true>)
+                                          : reinterpret_cast<const void*>(bin_kernel<false>),
+                                     g, kT, args, smem, st);
 }
 
 cudaError_t debug_source_order_keys(BinArgs& a, uint32_t* key_tile, uint32_t* key_depth, uint32_t* key_gauss,

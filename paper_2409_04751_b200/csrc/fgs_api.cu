@@ -79,6 +79,11 @@ int rule_fwd_px(int64_t I, int64_t tiles, int64_t longest) {
   if (tiles < 1024) return 1;  // a small image: fewer CTAs than a few waves, use every warp
   return (longest > 512 && longest > 8 * std::max<int64_t>(mean, 1)) ? 1 : 2;
 }
+int rule_row_scatter(int64_t I) {
+  static const int e = env_int("FGS_ROW_SCATTER");
+  if (e == 1 || e == 2) return e == 1;
+  return I > 2000000 ? 1 : 0;
+}
 int rule_k4b_minb(int64_t m) {
   static const int e = env_int("FGS_K4B_MINB");
   if (e == 4 || e == 6) return e;
@@ -100,7 +105,7 @@ struct fgs_context {
   DevBuf<int32_t> radii;
   // per intersection
   DevBuf<uint64_t> keys;
-  DevBuf<uint32_t> sorted_gauss;
+  DevBuf<uint32_t> sorted_gauss, row_list, row_hist;
   DevBuf<uint32_t> sorted_slot;  // backward: emission slot per sorted entry
   DevBuf<float> ckpt;             // backward segments: forward checkpoints [slot][4][256]
   DevBuf<uint32_t> seg_items, tile_ckpt;
@@ -120,7 +125,7 @@ struct fgs_context {
   cudaEvent_t ev_k2 = nullptr;    // K2 done on the caller's stream
   cudaStream_t aux = nullptr;     // the scalars' readback, off the caller's stream so K3 follows K2 directly
   uint32_t longest = 0;     // longest tile list of the last forward
-  int var_fwd_px = 0, var_bwd_px = 0, var_k4b = 0;  // launch variants of the last calls (reported)
+  int var_fwd_px = 0, var_bwd_px = 0, var_k4b = 0, var_row_scatter = 0;  // launch variants (reported)
   // The device scalars alternate between two 16-word halves by frame parity; a frame's K3 zeroes
   // the other half for the next frame (whose previous readback finished before this frame began),
   // so no memset precedes K1. scalars_clean[h]: half h is known to be zero.
@@ -233,7 +238,7 @@ size_t cap_bytes(const DevBuf<T>& b) { return b.p ? b.cap * sizeof(T) : 0; }
 size_t path_bytes(const fgs_context* c) {
   return cap_bytes(c->rec) + cap_bytes(c->state) + cap_bytes(c->dkey) + cap_bytes(c->cval) + cap_bytes(c->coff) +
          cap_bytes(c->src_off) + cap_bytes(c->touched) + cap_bytes(c->scan_status) + cap_bytes(c->rect) +
-         cap_bytes(c->radii) + cap_bytes(c->keys) + cap_bytes(c->sorted_gauss) + cap_bytes(c->sorted_slot) + cap_bytes(c->ckpt) + cap_bytes(c->seg_items) + cap_bytes(c->tile_ckpt) +
+         cap_bytes(c->radii) + cap_bytes(c->keys) + cap_bytes(c->sorted_gauss) + cap_bytes(c->row_list) + cap_bytes(c->row_hist) + cap_bytes(c->sorted_slot) + cap_bytes(c->ckpt) + cap_bytes(c->seg_items) + cap_bytes(c->tile_ckpt) +
          cap_bytes(c->partial_tile) + cap_bytes(c->tile_offsets) + cap_bytes(c->fill) + cap_bytes(c->last) +
          cap_bytes(c->tile_order) + cap_bytes(c->rowdiff) + cap_bytes(c->final_T);
 }
@@ -337,7 +342,7 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->rec.release();
   ctx->state.release();
   for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->src_off, &ctx->touched, &ctx->scan_status,
-                  &ctx->sorted_gauss, &ctx->sorted_slot, &ctx->seg_items, &ctx->tile_ckpt, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
+                  &ctx->sorted_gauss, &ctx->row_list, &ctx->row_hist, &ctx->sorted_slot, &ctx->seg_items, &ctx->tile_ckpt, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
                   &ctx->scalars})
     b->release();
   ctx->keys.release();
@@ -424,6 +429,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   if (camera->width <= 0 || camera->height <= 0) return fail(ctx, FGS_EINVAL, "forward: empty image");
   if ((static_cast<int64_t>(camera->width) + 15) / 16 * ((static_cast<int64_t>(camera->height) + 15) / 16) > 65536)
     return fail(ctx, FGS_EINVAL, "forward: more than 65536 tiles");
+  if ((camera->height + 15) / 16 > fgs::kMaxTileRows)
+    return fail(ctx, FGS_EINVAL, "forward: more than 4096 tile rows (image taller than 65536 pixels)");
   const int sh_degree = options ? options->sh_degree : 3;
   if (sh_degree < 0 || sh_degree > 3) return fail(ctx, FGS_EINVAL, "forward: sh_degree must be 0..3");
   const int64_t n = scene->n;
@@ -453,6 +460,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   FGS_CHECK(ctx->fill.ensure(num_tiles));
   FGS_CHECK(ctx->tile_order.ensure(num_tiles));
   FGS_CHECK(ctx->tile_ckpt.ensure(num_tiles));
+  FGS_CHECK(ctx->row_hist.ensure(std::max<size_t>(fgs::bin_row_hist_words(tiles_y), 1)));
   const size_t ndiff = static_cast<size_t>(tiles_x + 1) * tiles_y;
   if (ctx->rowdiff.cap < ndiff || ctx->rowdiff_clean < ndiff) {
     FGS_CHECK(ctx->rowdiff.ensure(ndiff));
@@ -532,6 +540,14 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.tile_order = ctx->tile_order.p;
   bn.isect_cap = ctx->isect_cap;
   bn.keys = ctx->keys.p;
+  bn.row_list = ctx->row_list.p;
+  bn.row_hist = ctx->row_hist.p;
+  // binning scatter by tile-row lists when the frame has many intersections (configs 3-4:
+  // K2 0.159 -> 0.141 ms, 0.141 -> 0.127), by source-order slots otherwise (config 2: 0.046 vs
+  // 0.054); decided on the last frame's count, kept for the relaunch of the same frame
+  bn.row_scatter = (ctx->flags & FGS_FLAG_ROW_SCATTER) ? 1 : (ctx->flags & FGS_FLAG_SLOT_SCATTER) ? 0
+                                                          : rule_row_scatter(ctx->num_isect);
+  ctx->var_row_scatter = bn.row_scatter;
   bn.src_off = ctx->src_off.p;
   bn.trace = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p + 16 : nullptr;
   if (n > 0) {
@@ -643,12 +659,14 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     const size_t ni = static_cast<size_t>(I > 0 ? I : 1);
     FGS_CHECK(ctx->keys.ensure(ni));
     FGS_CHECK(ctx->sorted_gauss.ensure(ni));
+    FGS_CHECK(ctx->row_list.ensure(ni));
     size_t cap = ctx->keys.cap;
-    cap = std::min(cap, ctx->sorted_gauss.cap);
+    cap = std::min(cap, std::min(ctx->sorted_gauss.cap, ctx->row_list.cap));
     ctx->isect_cap = static_cast<int64_t>(cap);
     if (n > 0 && I > 0) {
       bn.isect_cap = ctx->isect_cap;
       bn.keys = ctx->keys.p;
+      bn.row_list = ctx->row_list.p;
       bn.scatter_only = 1;
       FGS_CHECK(fgs::bin_launch(bn, st));
       bn.scatter_only = 0;
@@ -1287,8 +1305,9 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   }
   if (nm == "offsets") return copy(ctx->tile_offsets.p, (nt + 1) * 4);
   if (nm == "variants") {  // launch variants of the last forward / backward, longest tile list
-    const uint32_t v[4] = {static_cast<uint32_t>(ctx->var_fwd_px), static_cast<uint32_t>(ctx->var_bwd_px),
-                           static_cast<uint32_t>(ctx->var_k4b), ctx->longest};
+    const uint32_t v[5] = {static_cast<uint32_t>(ctx->var_fwd_px), static_cast<uint32_t>(ctx->var_bwd_px),
+                           static_cast<uint32_t>(ctx->var_k4b), ctx->longest,
+                           static_cast<uint32_t>(ctx->var_row_scatter)};
     if (!dst) return sizeof(v);
     if (dst_bytes < static_cast<int64_t>(sizeof(v))) return -1;
     std::memcpy(dst, v, sizeof(v));

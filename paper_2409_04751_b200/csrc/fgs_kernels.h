@@ -125,6 +125,7 @@ struct BinArgs {
   int tiles_x, tiles_y, num_tiles;
   int64_t isect_cap;           // capacity of the per-intersection buffers (the scatter is skipped if I exceeds it)
   int scatter_only;            // relaunch: phases 1-2 already ran
+  int row_scatter;             // phase 3 by tile-row lists (large I) instead of source-order slots
   unsigned long long* trace;   // debug phase timestamps (FGS_FLAG_COUNTERS), 8 slots
   const uint32_t* touched;     // [n] tiles touched per Gaussian (K1)
   const uint32_t* depth_key;   // [n] depth key bits (K1)
@@ -138,12 +139,16 @@ struct BinArgs {
   uint32_t* tile_offsets;      // [num_tiles + 1]
   uint32_t* fill;              // [num_tiles] scatter cursors
   uint32_t* tile_order;        // [num_tiles] blend schedule (optional)
+  uint32_t* row_hist;          // [grid][tiles_y] per-CTA counts of (Gaussian, tile row) pairs
   // per intersection
-  uint64_t* keys;              // [I] (depth_key << 32 | emission slot), grouped by tile
+  uint64_t* keys;              // [I] (depth_key << 32 | Gaussian id), grouped by tile
+  uint32_t* row_list;          // [<= I] Gaussians per tile row (row-major), the scatter's work order
 };
 
-// Words of part_scan scratch bin_scan needs.
+// Words of part_scan scratch bin_scan needs; words of the per-CTA row histograms.
 size_t bin_part_words(int tiles_y);
+size_t bin_row_hist_words(int tiles_y);
+constexpr int kMaxTileRows = 4096;  // binning keeps per-row state in shared memory
 // K2 (one cooperative kernel): compaction + emission offsets + I and M (device scalars),
 // tile ranges + blend schedule, key scatter into the tile ranges (skipped if I > isect_cap).
 cudaError_t bin_launch(BinArgs& a, cudaStream_t st);

@@ -10,8 +10,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2409_04751_b200 import Rasterizer, RenderOptions, _lib, synthetic  # noqa: E402
 from tests._helpers import to_device  # noqa: E402
 
-NAMES = ["counts+rows", "compaction+offsets", "grid barriers", "scatter: rank search+staging",
-         "scatter: slot search+gathers", "scatter: smem atomics", "scatter: global atomics", "scatter: key writes"]
+NAMES = ["counts+rows+row hist", "compaction+offsets+row lists", "grid barriers", "scatter: zero counters",
+         "scatter: count pass", "(unused)", "scatter: tile reservations", "scatter: key pass"]
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 sc, deg, cams, _ = synthetic.config(cfg, **({"views": 1} if cfg >= 3 else {}))

@@ -112,9 +112,10 @@ def test_cfg1_full_scale_fwd_bwd_parity(rast, oracle_mod):
     check_grads(g, o)
 
 
-def test_cfg2_hot_path_key_list_and_counters(rast, oracle_mod):
-    """Config 2 full scale (1M clustered Gaussians). The pre-sort key list comes from the hot
-    path's own state: K2's compaction (the tile-touching Gaussians in source order with their
+@pytest.mark.parametrize("scatter", ["slots", "rows"])
+def test_cfg2_hot_path_key_list_and_counters(rast, oracle_mod, scatter):
+    """Config 2 full scale (1M clustered Gaussians), with either scatter work order (tile-row
+    lists or source-order slots). The pre-sort key list comes from the hot path's own state: K2's compaction (the tile-touching Gaussians in source order with their
     first emission slots) and K1's tile rectangles give the reference's emission order
     (splatting.hpp:216-221), and the 64-bit keys K2's scatter wrote into every tile's range are, per
     tile, exactly the reference's (depth key, source) keys of that tile. Then E_eval / E_contrib
@@ -132,10 +133,12 @@ def test_cfg2_hot_path_key_list_and_counters(rast, oracle_mod):
     assert I > 500_000
 
     ds = to_device(scene)
-    rast.set_flags(_lib.FGS_FLAG_COUNTERS)
+    force = _lib.FGS_FLAG_ROW_SCATTER if scatter == "rows" else _lib.FGS_FLAG_SLOT_SCATTER
+    rast.set_flags(_lib.FGS_FLAG_COUNTERS | force)
     try:
         _, st = rast.forward(ds, cam, RenderOptions(sh_degree=deg), want_stats=True)
         ev, ec = rast.debug("counters", np.uint64)[:2]
+        assert rast.debug("variants")[4] == (1 if scatter == "rows" else 0)
     finally:
         rast.set_flags(0)
     assert st.num_intersections == I
