@@ -584,6 +584,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   ba.tiles_y = tiles_y;
   ba.tile_offsets = ctx->tile_offsets.p;
   ba.rec = ctx->rec.p;
+  ba.num_rec = n;
   for (int k = 0; k < 3; ++k) ba.bg[k] = ctx->bg[k];
   ba.image = image;
   ba.final_T = ctx->final_T.p;

@@ -70,6 +70,7 @@ struct BlendArgs {
   const uint32_t* src_off;       // backward: first emission slot of each tile-touching Gaussian
   const ushort4* rect;           // backward: tile rectangle per Gaussian
   const SortedRec* rec;          // per-Gaussian records
+  int64_t num_rec;               // records (rows of the TMA record tensor)
   float bg[3];
   float* image;                  // H*W*3
   float* final_T;                // H*W

@@ -22,6 +22,8 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cuda.h>
+
 #include "fgs_sort.cuh"
 
 namespace fgs {
@@ -90,12 +92,15 @@ __device__ __forceinline__ void blend_apply(PixelState& p, float power, float ar
 // atomics) and the per-pixel blend count; kModeBlendCount: the per-pixel blend count only (the
 // reference's ForwardContext::blend_count, inc/splatting.hpp:299-301).
 constexpr int kModeCounters = 1, kModeBlendCount = 2;
-template <int MODE, int PX>
-__global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
+// TMA: the chunk's records are fetched by TMA gather4 (cp.async.bulk.tensor.2d ... tile::gather4:
+// 4 records of the 2D record tensor per instruction, 8 lanes issue one each, completion on a
+// per-warp mbarrier) instead of 3 x 16-byte cp.async per lane (profiles A/B).
+template <int MODE, int PX, bool TMA = false>
+__global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, const __grid_constant__ CUtensorMap tmap) {
   constexpr bool COUNTERS = MODE == kModeCounters;
   constexpr bool CONTRIB = MODE != 0;
   constexpr int NW = 8 / PX;
-  __shared__ __align__(16) uint64_t skeys[kSortCap];  // tile list sort; then the sorted ids and the raw records
+  __shared__ __align__(128) uint64_t skeys[kSortCap];  // tile list sort; then the sorted ids and the raw records
   __shared__ float4 s01[2][NW][32];  // record staging (s0, s1); the radix sort's digit counters before
   __shared__ float s2[NW][32];
   __shared__ uint32_t sk[NW][32];    // list index of each staged record
@@ -143,8 +148,12 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   // raw records of the warp's next chunk (32 x 48 bytes), filled by cp.async; they sit in the
   // part of the sort buffer the ids do not use (ids at word 0 for short lists, at 2 kRadixCap
   // for the radix range, in global memory otherwise)
-  float4* raw = reinterpret_cast<float4*>(s32 + (id_off == 0 ? 2 * kRadixCap : 0)) + warp * 96;
-  static_assert(sizeof(skeys) >= (2 * kRadixCap + NW * 96 * 4) * 4, "raw record buffers fit the sort buffer");
+  // (TMA: each gather4 group of 4 records at a 128-byte aligned 256-byte slot, record j at float4
+  // 16 (j / 4) + 3 (j % 4); else record j at float4 3 j)
+  constexpr int kRawF4 = TMA ? 128 : 96;
+  float4* raw = reinterpret_cast<float4*>(s32 + (id_off == 0 ? 2 * kRadixCap : 0)) + warp * kRawF4;
+  static_assert(sizeof(skeys) >= (2 * kRadixCap + NW * kRawF4 * 4) * 4, "raw record buffers fit the sort buffer");
+  const int rawj = TMA ? 16 * (lane >> 2) + 3 * (lane & 3) : 3 * lane;  // this lane's record
   const float fx = static_cast<float>(px) + 0.5f;
   const float bx0 = static_cast<float>(bx) + 0.5f, by0 = static_cast<float>(by) + 0.5f;
   unsigned long long warp_evals = 0;
@@ -164,17 +173,62 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     return d;
   };
   // issue the copies of chunk [base, base + 32)'s records into raw (one record per lane)
+  __shared__ __align__(8) uint64_t s_mbar[TMA ? NW : 1];
+  const uint32_t mbar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar[TMA ? warp : 0]));
+  uint32_t mbar_phase = 0;
+  bool tma_pending = false;
+  if (TMA && lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
   auto prefetch = [&](uint32_t base) {
-    const uint32_t k = base + lane;
-    if (k < hi) {
-      const uint32_t g = id_off >= 0 ? s32[id_off + (k - lo)] : __ldg(a.sorted_gauss + k);
-      const float4* src = reinterpret_cast<const float4*>(a.rec + g);
-      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(raw + lane * 3));
+    if constexpr (TMA) {
+      // lanes 0..ng-1 each gather 4 records (the last group repeats the chunk's last id)
+      const int n = static_cast<int>(min(hi - base, 32u)), ng = (n + 3) / 4;
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(ng * 192) : "memory");
+      if (lane < ng) {
+        int32_t g4[4];
 #pragma unroll
-      for (int q = 0; q < 3; ++q)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + q) : "memory");
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t k = base + min(4 * lane + q, n - 1);
+          g4[q] = static_cast<int32_t>(id_off >= 0 ? s32[id_off + (k - lo)] : __ldg(a.sorted_gauss + k));
+        }
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(raw + lane * 16));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+            "%4, %5, %6}], [%7];" ::"r"(dst),
+            "l"(&tmap), "r"(0), "r"(g4[0]), "r"(g4[1]), "r"(g4[2]), "r"(g4[3]), "r"(mbar)
+            : "memory");
+      }
+      tma_pending = true;
+    } else {
+      const uint32_t k = base + lane;
+      if (k < hi) {
+        const uint32_t g = id_off >= 0 ? s32[id_off + (k - lo)] : __ldg(a.sorted_gauss + k);
+        const float4* src = reinterpret_cast<const float4*>(a.rec + g);
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(raw + lane * 3));
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(src + q) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto await_chunk = [&]() {
+    if constexpr (TMA) {
+      if (tma_pending) {
+        asm volatile(
+            "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT_%=;\n}" ::"r"(mbar),
+            "r"(mbar_phase)
+            : "memory");
+        mbar_phase ^= 1u;
+        tma_pending = false;
+      }
+    } else {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+    }
   };
   const unsigned lt = (1u << lane) - 1u;
   prefetch(lo);
@@ -200,11 +254,11 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
   for (uint32_t base = lo; base < hi; base += 32) {
     if (__all_sync(0xffffffffu, all_done())) break;
     if (base > lo && (base - lo) % kSeg == 0) checkpoint(static_cast<int>((base - lo) / kSeg) - 1, false);
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    await_chunk();
     __syncwarp();
     // (the exact ellipse test, which the backward uses, costs the forward more than the ~13%
     // of pairs it removes at config 2)
-    const float4 ra = raw[lane * 3], rc = raw[lane * 3 + 2];
+    const float4 ra = raw[rawj], rc = raw[rawj + 2];
     const bool pass = base + lane < hi && rec_hits(ra, rc, bx0, bx0 + 7.0f, by0, by0 + (4.0f * PX - 1.0f));
     // survivors compacted, in list order, into the warp's staging slots
     const uint32_t mask = __ballot_sync(0xffffffffu, pass);
@@ -213,7 +267,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     if (pass) {
       const int pos = __popc(mask & lt);
       s0[warp][pos] = ra;
-      s1[warp][pos] = raw[lane * 3 + 1];
+      s1[warp][pos] = raw[rawj + 1];
       s2[warp][pos] = rc.x;
       sk[warp][pos] = base + lane;
     }
@@ -272,7 +326,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a) {
     else if (G == 4 && rem == 3) group(j0, std::integral_constant<int, G == 4 ? 3 : 1>{});
     __syncwarp();
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  await_chunk();  // (a warp that stopped early still has its last fetch in flight)
   if (hi - lo > kSeg) checkpoint(static_cast<int>((hi - lo + kSeg - 1) / kSeg) - 1, true);  // final: T, image value
   if (COUNTERS) {
     const long long t_cta = clock64() - t_start;
@@ -630,6 +684,43 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
 }
 }  // namespace
 
+namespace {
+// The record array as a 2D tensor (12 floats x N rows) for TMA gather4, rebuilt when the buffer
+// moves or grows. cuTensorMapEncodeTiled is reached through the runtime's driver entry point.
+struct RecTensorMap {
+  CUtensorMap map{};
+  const void* ptr = nullptr;
+  int64_t rows = 0;
+  bool ok = false;
+};
+
+bool encode_rec_map(RecTensorMap& m, const void* rec, int64_t rows) {
+  if (m.ok && m.ptr == rec && m.rows == rows) return true;
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<Encode>(nullptr);
+    return reinterpret_cast<Encode>(fn);
+  }();
+  if (!encode || rows <= 0) return false;
+  const cuuint64_t dims[2] = {12, static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {48};
+  const cuuint32_t box[2] = {12, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  m.ok = encode(&m.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(rec), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  m.ptr = rec;
+  m.rows = rows;
+  return m.ok;
+}
+}  // namespace
+
 int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStream_t st) {
   static PerDevice attrs;
   attrs.get([] {
@@ -638,7 +729,8 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStr
     // where the 8 warps of a tile re-read each chunk's records (config 2 blend 0.177 -> 0.172 ms).
     for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<kModeCounters, 1>),
                           reinterpret_cast<const void*>(blend_forward_kernel<kModeBlendCount, 1>),
-                          reinterpret_cast<const void*>(blend_forward_kernel<0, 1>)})
+                          reinterpret_cast<const void*>(blend_forward_kernel<0, 1>),
+                          reinterpret_cast<const void*>(blend_forward_kernel<0, 1, true>)})
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 78);
     for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<kModeCounters, 2>),
                           reinterpret_cast<const void*>(blend_forward_kernel<kModeBlendCount, 2>),
@@ -653,14 +745,25 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStr
   (void)num_isect;
   const int tiles = a.tiles_x * a.tiles_y;
   const int px = px_request == 1 ? 1 : 2;
+  // record staging by TMA gather4 (FGS_FWD_TMA=1; product kernel, 1 pixel per lane): the A/B of
+  // off by default
+  static const int env_tma = [] {
+    const char* v = std::getenv("FGS_FWD_TMA");
+    return v ? std::atoi(v) : 0;
+  }();
+  static thread_local RecTensorMap rec_map;
+  const bool tma = env_tma == 1 && px == 1 && !a.counters && !a.blend_count &&
+                   encode_rec_map(rec_map, a.rec, a.num_rec);
+  const CUtensorMap& tm = rec_map.map;
   if (px == 1) {
-    if (a.counters) blend_forward_kernel<kModeCounters, 1><<<tiles, 256, 0, st>>>(a);
-    else if (a.blend_count) blend_forward_kernel<kModeBlendCount, 1><<<tiles, 256, 0, st>>>(a);
-    else blend_forward_kernel<0, 1><<<tiles, 256, 0, st>>>(a);
+    if (a.counters) blend_forward_kernel<kModeCounters, 1><<<tiles, 256, 0, st>>>(a, tm);
+    else if (a.blend_count) blend_forward_kernel<kModeBlendCount, 1><<<tiles, 256, 0, st>>>(a, tm);
+    else if (tma) blend_forward_kernel<0, 1, true><<<tiles, 256, 0, st>>>(a, tm);
+    else blend_forward_kernel<0, 1><<<tiles, 256, 0, st>>>(a, tm);
   } else {
-    if (a.counters) blend_forward_kernel<kModeCounters, 2><<<tiles, 128, 0, st>>>(a);
-    else if (a.blend_count) blend_forward_kernel<kModeBlendCount, 2><<<tiles, 128, 0, st>>>(a);
-    else blend_forward_kernel<0, 2><<<tiles, 128, 0, st>>>(a);
+    if (a.counters) blend_forward_kernel<kModeCounters, 2><<<tiles, 128, 0, st>>>(a, tm);
+    else if (a.blend_count) blend_forward_kernel<kModeBlendCount, 2><<<tiles, 128, 0, st>>>(a, tm);
+    else blend_forward_kernel<0, 2><<<tiles, 128, 0, st>>>(a, tm);
   }
   return 1;
 }
