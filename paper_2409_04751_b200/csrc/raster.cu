@@ -320,10 +320,14 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
     constexpr int G = kGroup<PX>;
     int j0 = 0;
     for (; j0 + G <= nsurv; j0 += G) group(j0, std::integral_constant<int, G>{});
-    const int rem = nsurv - j0;  // warp-uniform
+    const int rem = nsurv - j0;  // warp-uniform, < G
     if (rem == 1) group(j0, std::integral_constant<int, 1>{});
     else if (rem == 2) group(j0, std::integral_constant<int, 2>{});
-    else if (G == 4 && rem == 3) group(j0, std::integral_constant<int, G == 4 ? 3 : 1>{});
+    else if (rem == 3) group(j0, std::integral_constant<int, (G > 3 ? 3 : 1)>{});
+    else if (rem == 4) group(j0, std::integral_constant<int, (G > 4 ? 4 : 1)>{});
+    else if (rem == 5) group(j0, std::integral_constant<int, (G > 5 ? 5 : 1)>{});
+    else if (rem == 6) group(j0, std::integral_constant<int, (G > 6 ? 6 : 1)>{});
+    else if (rem == 7) group(j0, std::integral_constant<int, (G > 7 ? 7 : 1)>{});
     __syncwarp();
   }
   await_chunk();  // (a warp that stopped early still has its last fetch in flight)
