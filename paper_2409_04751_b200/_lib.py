@@ -9,6 +9,9 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfgs.so")
+# FGS_LIB=checked selects libfgs_checked.so: the same sources built with -DFGS_CHECKED (device-side
+# bounds / invariant checks that trap; tests/test_checked_gpu.py)
+CHECKED_LIB_PATH = os.path.join(HERE, "libfgs_checked.so")
 
 FGS_OK, FGS_EINVAL, FGS_EDEGENERATE_QUAT, FGS_ECUDA, FGS_ENOMEM, FGS_ESTATE, FGS_ENONFINITE = range(7)
 FGS_FLAG_COUNTERS, FGS_FLAG_KEEP_KEYS, FGS_FLAG_TIMING, FGS_FLAG_BLEND_COUNT = 1, 2, 4, 8
@@ -81,11 +84,14 @@ EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load libfgs.so and declare its signatures. Raises if it has not been built."""
+def load(path: str | None = None):
+    """Load libfgs.so (libfgs_checked.so with FGS_LIB=checked) and declare its signatures. Raises
+    if it has not been built."""
     global _lib
     if _lib is not None:
         return _lib
+    if path is None:
+        path = CHECKED_LIB_PATH if os.environ.get("FGS_LIB") == "checked" else LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"{path} is missing: build it with `python -m paper_2409_04751_b200.build` "
                            "(there is no CPU fallback)")

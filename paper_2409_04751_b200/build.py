@@ -7,6 +7,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -49,28 +50,44 @@ def _programs_stale() -> bool:
     return any(not os.path.exists(o) or os.path.getmtime(o) < newest for o in outs)
 
 
-def build(verbose=False, force=False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "fgs.h")]
-    if not force and os.path.exists(OUT) and _programs_stale():
-        build_example(verbose)
-    newest = max(os.path.getmtime(p) for p in deps)
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
-        return OUT
+CHECKED_OUT = os.path.join(HERE, "libfgs_checked.so")
+
+
+def _build_lib(out, objdir, defines, deps, verbose, force):
+    """nvcc every source (in parallel) and link one shared library; skipped when up to date."""
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(p) for p in deps):
+        return False
+    os.makedirs(objdir, exist_ok=True)
     nvcc = _nvcc()
-    objs = []
+    cmds, objs = [], []
     for src, extra in SOURCES.items():
-        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
-        if verbose:
-            print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmds.append([nvcc, *ARCH, *COMMON, *defines, *extra, "-c", os.path.join(CSRC, src), "-o", obj])
         objs.append(obj)
-    cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", OUT, *objs, "-ldl"]
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        for cmd in cmds:
+            if verbose:
+                print(" ".join(cmd))
+        for r in ex.map(lambda c: subprocess.run(c, check=True), cmds):
+            pass
+    cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", out, *objs, "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    build_example(verbose)
+    return True
+
+
+def build(verbose=False, force=False, checked=True) -> str:
+    """libfgs.so (the product) and libfgs_checked.so (the same sources with -DFGS_CHECKED: device
+    bounds / invariant checks that trap, for tests/test_checked_gpu.py)."""
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "fgs.h")]
+    if not force and os.path.exists(OUT) and _programs_stale():
+        build_example(verbose)
+    built = _build_lib(OUT, OBJ, [], deps, verbose, force)
+    if checked:
+        _build_lib(CHECKED_OUT, OBJ + "_checked", ["-DFGS_CHECKED"], deps, verbose, force)
+    if built:
+        build_example(verbose)
     return OUT
 
 

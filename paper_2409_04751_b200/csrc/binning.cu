@@ -50,6 +50,17 @@ struct ScanSmem {
   uint32_t scalar[4];
 };
 
+#ifdef FGS_CHECKED
+// Checked build: key position p lies in tile t's range (and the buffer); a rectangle is in the grid.
+__device__ __forceinline__ bool key_slot_ok(const BinArgs& a, uint32_t t, uint32_t p) {
+  return t < static_cast<uint32_t>(a.num_tiles) && p >= a.tile_offsets[t] && p < a.tile_offsets[t + 1] &&
+         static_cast<int64_t>(p) < a.isect_cap;
+}
+__device__ __forceinline__ bool rect_ok(const BinArgs& a, ushort4 rc) {
+  return rc.x <= rc.y && rc.y < a.tiles_x && rc.z <= rc.w && rc.w < a.tiles_y;
+}
+#endif
+
 // Block-wide exclusive scan of one value per thread (kT threads).
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -325,6 +336,7 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
   for (int u = 0; u < U; ++u) {
     if (ev[u] >= hi) continue;
     const ushort4 rc = a.rect[gv[u]];
+    FGS_DCHECK(rect_ok(a, rc) && ev[u] >= s_off[tv[u]]);
     const int wx = rc.y - rc.x + 1;
     const int j = static_cast<int>(ev[u] - s_off[tv[u]]);
     tv[u] = static_cast<uint32_t>((rc.z + j / wx) * a.tiles_x + rc.x + j % wx);
@@ -351,6 +363,7 @@ __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi,
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     if (ev[u] >= hi) continue;
+    FGS_DCHECK(key_slot_ok(a, tv[u], pv[u]) && gv[u] < static_cast<uint32_t>(a.n));
     a.keys[pv[u]] = (static_cast<uint64_t>(dk[u]) << 32) | gv[u];
   }
   __syncthreads();  // s_cnt / s_off reused by the next range
@@ -412,7 +425,12 @@ __device__ void row_layout(const BinArgs& a, uint32_t* s_start, uint32_t* s_cur,
 // rectangle covers (positions from the CTA's per-row cursors; order within a row free).
 __device__ __forceinline__ void row_emit_one(const BinArgs& a, int i, uint32_t* s_cur) {
   const ushort4 rc = a.rect[i];
-  for (int ty = rc.z; ty <= rc.w; ++ty) a.row_list[atomicAdd(s_cur + ty, 1u)] = static_cast<uint32_t>(i);
+  FGS_DCHECK(rect_ok(a, rc));
+  for (int ty = rc.z; ty <= rc.w; ++ty) {
+    const uint32_t p = atomicAdd(s_cur + ty, 1u);
+    FGS_DCHECK(static_cast<int64_t>(p) < a.isect_cap);
+    a.row_list[p] = static_cast<uint32_t>(i);
+  }
 }
 
 __device__ void row_emit(const BinArgs& a, int lo, int hi, uint32_t* s_cur) {
@@ -473,7 +491,12 @@ __device__ void scatter_rows(const BinArgs& a, uint32_t e0, uint32_t e1, const u
         const uint32_t g = a.row_list[e];
         const ushort4 rc = a.rect[g];
         const uint64_t key = (static_cast<uint64_t>(a.depth_key[g]) << 32) | g;
-        for (int x = rc.x; x <= rc.y; ++x) a.keys[atomicAdd(s_cnt + (r * tx + x - span0), 1u)] = key;
+        FGS_DCHECK(rect_ok(a, rc) && r >= rc.z && r <= rc.w);
+        for (int x = rc.x; x <= rc.y; ++x) {
+          const uint32_t p = atomicAdd(s_cnt + (r * tx + x - span0), 1u);
+          FGS_DCHECK(key_slot_ok(a, static_cast<uint32_t>(r * tx + x), p));
+          a.keys[p] = key;
+        }
       }
       __syncthreads();
       trace(a.trace, 0, 7);
@@ -483,7 +506,12 @@ __device__ void scatter_rows(const BinArgs& a, uint32_t e0, uint32_t e1, const u
         const uint32_t g = a.row_list[e];
         const ushort4 rc = a.rect[g];
         const uint64_t key = (static_cast<uint64_t>(a.depth_key[g]) << 32) | g;
-        for (int x = rc.x; x <= rc.y; ++x) a.keys[atomicAdd(a.fill + r * tx + x, 1u)] = key;
+        FGS_DCHECK(rect_ok(a, rc) && r >= rc.z && r <= rc.w);
+        for (int x = rc.x; x <= rc.y; ++x) {
+          const uint32_t p = atomicAdd(a.fill + r * tx + x, 1u);
+          FGS_DCHECK(key_slot_ok(a, static_cast<uint32_t>(r * tx + x), p));
+          a.keys[p] = key;
+        }
       }
     }
     ty = ty_end + 1;

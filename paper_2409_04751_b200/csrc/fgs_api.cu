@@ -746,6 +746,9 @@ int backward_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera
   ba.seg_items = ctx->seg_items.p;
   ba.tile_ckpt = ctx->tile_ckpt.p;
   ba.num_seg_items = ctx->num_segs;
+  ba.num_rec = n;
+  ba.isect_cap = I;  // (bounds for the checked build)
+  ba.ckpt_cap = ctx->ckpt_cap;
   ba.counters = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p : nullptr;
   ba.partial_tile = ctx->partial_tile.p;
   ba.src_off = ctx->src_off.p;
@@ -786,6 +789,7 @@ int backward_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera
   pb.touched = ctx->touched.p;
   pb.coff = ctx->coff.p;
   pb.partials = ctx->partial_tile.p;
+  pb.num_isect = I;
   pb.d_means = grads->d_means;
   pb.d_rotations = grads->d_rotations;
   pb.d_log_scales = grads->d_log_scales;

@@ -2,11 +2,30 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <mutex>
 
 #include <cuda_runtime.h>
 
 namespace fgs {
+
+// Checked build (libfgs_checked.so, -DFGS_CHECKED): device-side bounds and invariant checks at
+// the kernels' indexing sites -- the memory / race checking this pool allows (compute-sanitizer is
+// closed on it). A failed check prints the site and traps (the launch fails with an error).
+#ifdef FGS_CHECKED
+#define FGS_DCHECK(cond)                                                                          \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("FGS_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,    \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                       \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define FGS_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // Forward-model constants (reference inc/core.hpp:43-53), rounded to float exactly as the
 // reference's S(...) casts do.

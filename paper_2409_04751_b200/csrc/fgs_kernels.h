@@ -53,6 +53,7 @@ struct PreprocessBackwardArgs {
   const uint32_t* touched;
   const uint32_t* coff;      // [m] first emission slot of cval[q]
   const float* partials;     // [I][9] K4a per-intersection sums by emission slot
+  int64_t num_isect;         // I (bounds of partials, checked build)
   float* d_means;
   float* d_rotations;
   float* d_log_scales;

@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
   const int bx = tx * kTile + ((warp & 1) << 3), by = ty * kTile + (warp >> 1) * 4 * PX;
   const int px = bx + (lane & 7);
   const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
+  FGS_DCHECK(tile < a.tiles_x * a.tiles_y && lo <= hi && static_cast<int64_t>(hi) <= a.isect_cap);
   const long long t_start = COUNTERS ? clock64() : 0;
   if (COUNTERS) span_start(a.tile_span, tile);
   // long list: reserve its segments' checkpoint slots (segments k = 1.. of the backward, then
@@ -193,7 +194,9 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint32_t k = base + min(4 * lane + q, n - 1);
+          FGS_DCHECK(k < hi && (id_off < 0 || id_off + (k - lo) < 2 * kSortCap));
           g4[q] = static_cast<int32_t>(id_off >= 0 ? s32[id_off + (k - lo)] : __ldg(a.sorted_gauss + k));
+          FGS_DCHECK(g4[q] >= 0 && g4[q] < a.num_rec);
         }
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(raw + lane * 16));
         asm volatile(
@@ -206,7 +209,9 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
     } else {
       const uint32_t k = base + lane;
       if (k < hi) {
+        FGS_DCHECK(id_off < 0 || id_off + (k - lo) < 2 * kSortCap);
         const uint32_t g = id_off >= 0 ? s32[id_off + (k - lo)] : __ldg(a.sorted_gauss + k);
+        FGS_DCHECK(g < a.num_rec);
         const float4* src = reinterpret_cast<const float4*>(a.rec + g);
         const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(raw + lane * 3));
 #pragma unroll
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
   auto checkpoint = [&](int k, bool fin) {
     const uint32_t slot0 = *reinterpret_cast<volatile const uint32_t*>(a.tile_ckpt + tile);
     if (slot0 == 0xFFFFFFFFu) return;
+    FGS_DCHECK(static_cast<int64_t>(slot0) + k < a.ckpt_cap);
     float* c = a.ckpt + static_cast<size_t>(slot0 + k) * (4 * kTile * kTile);
     const int lpix = ((warp >> 1) * 4 * PX + (lane >> 3)) * kTile + ((warp & 1) << 3) + (lane & 7);
 #pragma unroll
@@ -266,6 +272,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
     if (COUNTERS) warp_evals += nsurv;
     if (pass) {
       const int pos = __popc(mask & lt);
+      FGS_DCHECK(pos < 32);
       s0[warp][pos] = ra;
       s1[warp][pos] = raw[rawj + 1];
       s2[warp][pos] = rc.x;
@@ -428,10 +435,12 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
     seg = static_cast<int>(item >> 16);
     if (seg == static_cast<int>(kSegFinal)) return;  // a final-state slot: no work item
     tile = static_cast<int>(item & 0xFFFFu);
+    FGS_DCHECK(seg >= 1);
   } else {
     const uint32_t b = blockIdx.x - static_cast<uint32_t>(a.num_seg_items);
     tile = a.tile_order ? static_cast<int>(a.tile_order[b]) : static_cast<int>(b);
   }
+  FGS_DCHECK(tile >= 0 && tile < a.tiles_x * a.tiles_y);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (seg == 0) span_start(a.tile_span, tile);
@@ -443,10 +452,14 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   const uint32_t lo = tlo + static_cast<uint32_t>(seg) * kSeg;
   const uint32_t hi = min(thi, lo + static_cast<uint32_t>(kSeg));
   const int nseg = static_cast<int>((thi - tlo + kSeg - 1) / kSeg);
+  FGS_DCHECK(tlo <= thi && static_cast<int64_t>(thi) <= a.isect_cap && (seg == 0 || seg < nseg));
   const float* ck = nullptr;   // checkpoint at hi (state before entries >= hi), for hi < thi
   const float* fin = nullptr;  // the tile's final state (T, image value)
   if (nseg > 1) {
     const uint32_t slot0 = a.tile_ckpt[tile];
+    // the forward reserved this long list's slots (the host grows the buffers and re-renders
+    // until they fit)
+    FGS_DCHECK(slot0 != 0xFFFFFFFFu && static_cast<int64_t>(slot0) + nseg <= a.ckpt_cap);
     fin = a.ckpt + static_cast<size_t>(slot0 + nseg - 1) * (4 * kTile * kTile);
     if (seg + 1 < nseg) ck = a.ckpt + static_cast<size_t>(slot0 + seg) * (4 * kTile * kTile);
   }
@@ -469,6 +482,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
     if (px < a.width && py < a.height) {
       const size_t pix = static_cast<size_t>(py) * a.width + px;
       const uint32_t lp = a.last[pix];
+      FGS_DCHECK(lp >= tlo && lp <= thi);
       dl[u][0] = a.dl_dimage[pix * 3 + 0];
       dl[u][1] = a.dl_dimage[pix * 3 + 1];
       dl[u][2] = a.dl_dimage[pix * 3 + 2];
@@ -498,7 +512,9 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   // once) so the chunk loop fetches slots with plain asynchronous copies; entries past every
   // pixel's last contributor add nothing: zero sums at their slots
   for (uint32_t k = lo + tid; k < hi; k += NT) {
+    FGS_DCHECK(__ldg(a.sorted_gauss + k) < a.num_rec);
     const uint32_t e = emission_slot(a, __ldg(a.sorted_gauss + k), tx, ty);
+    FGS_DCHECK(static_cast<int64_t>(e) < a.isect_cap);
     if (k < top) {
       a.sorted_slot[k] = e;
     } else {
@@ -679,6 +695,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
 #pragma unroll
       for (int w = 0; w < NW; ++w)
         if ((s_mask[b][w] >> j) & 1u) sg = sg + s_part[b][w][idx];
+      FGS_DCHECK(static_cast<int64_t>(s_slot[c % 3][j]) < a.isect_cap);
       a.partial_tile[static_cast<size_t>(s_slot[c % 3][j]) * 9 + q] = sg;
     }
     prefetch(c + 2);

@@ -46,6 +46,24 @@ def test_sm100a_cubin_embedded(libfgs):
     assert "sm_100a" in out
 
 
+def test_checked_library_matches_and_checks():
+    """libfgs_checked.so (tests/test_checked_gpu.py) exports the same C ABI, and its kernels carry
+    the device checks: more trap sites in the SASS than the product library's."""
+    from paper_2409_04751_b200 import _lib
+
+    assert os.path.exists(_lib.CHECKED_LIB_PATH), "build libfgs_checked.so"
+    exported = subprocess.run(["nm", "-D", "--defined-only", _lib.CHECKED_LIB_PATH], capture_output=True,
+                              text=True).stdout
+    for name in declared_functions():
+        assert re.search(rf"\bT {name}\b", exported), name
+
+    def traps(path):
+        sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
+        return len(re.findall(r"\bBPT\.TRAP\b", sass))
+
+    assert traps(_lib.CHECKED_LIB_PATH) > traps(_lib.LIB_PATH) + 20
+
+
 def test_struct_layouts_match_header():
     import ctypes as C
 
