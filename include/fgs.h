@@ -170,6 +170,13 @@ int fgs_timing(fgs_context* ctx, double ms[6], uint64_t calls[2], uint64_t* laun
  * FMUL/FADD probe kernel; the denominator of the blend kernels' roofline. */
 int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s);
 
+/* Self-test of the fast correctly rounded exp / atan2 K1 and K4b use (csrc/fgs_crmath.cuh) against
+ * their definition (fp32 rounding of the double evaluation): which 0 = exp over the fp32 bit
+ * patterns [begin, begin + count); 1 = atan2 over `count` seeded pairs of random bit patterns;
+ * 2 = atan2 over seeded pairs of the camera domain. out = {checked, mismatches, slow-path count}.
+ * Synchronises. */
+int fgs_selftest_crmath(fgs_context* ctx, int which, uint64_t begin, uint64_t count, uint64_t seed, uint64_t out[3]);
+
 /* Parity/debug export of the last forward's state into host memory. Names:
  *   "state_u8" u8[N] (0 culled, 1 kept, 2 degenerate), "rec" f32[N*12] (splat records: mean_px,
  *   -conic.a/2, conic.b, -conic.c/2, alpha_max, colour, extent), "depth_key" u32[N], "radius" int32[N], "touched" u32[N],

@@ -10,7 +10,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfgs.so")
 # FGS_LIB=checked selects libfgs_checked.so: the same sources built with -DFGS_CHECKED (device-side
-# bounds / invariant checks that trap; tests/test_checked_gpu.py)
+# bounds / invariant checks that trap; tests/test_checked_gpu.py); FGS_LIB=<name>, an experiment
+# build libfgs_<name>.so (build.py --variant)
 CHECKED_LIB_PATH = os.path.join(HERE, "libfgs_checked.so")
 
 FGS_OK, FGS_EINVAL, FGS_EDEGENERATE_QUAT, FGS_ECUDA, FGS_ENOMEM, FGS_ESTATE, FGS_ENONFINITE = range(7)
@@ -79,7 +80,7 @@ EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs
            "fgs_timing", "fgs_measure_fp32_peak", "fgs_l1_dssim_loss", "fgs_adam_step", "fgs_train_step",
            "fgs_bruteforce_render", "fgs_bruteforce_render_f64", "fgs_last_transfer", "fgs_render_host_aos",
            "fgs_backward_host_aos", "fgs_comm_get_unique_id", "fgs_comm_init", "fgs_comm_init_all",
-           "fgs_comm_destroy", "fgs_allreduce_gradients", "fgs_fwd_bwd_views"]
+           "fgs_comm_destroy", "fgs_allreduce_gradients", "fgs_fwd_bwd_views", "fgs_selftest_crmath"]
 
 _lib = None
 
@@ -91,7 +92,8 @@ def load(path: str | None = None):
     if _lib is not None:
         return _lib
     if path is None:
-        path = CHECKED_LIB_PATH if os.environ.get("FGS_LIB") == "checked" else LIB_PATH
+        v = os.environ.get("FGS_LIB")
+        path = os.path.join(HERE, f"libfgs_{v}.so") if v else LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"{path} is missing: build it with `python -m paper_2409_04751_b200.build` "
                            "(there is no CPU fallback)")
@@ -121,6 +123,8 @@ def load(path: str | None = None):
     L.fgs_timing.argtypes = [vp, P(C.c_double), P(C.c_uint64), P(C.c_uint64), i32]
     L.fgs_timing.restype = i32
     L.fgs_measure_fp32_peak.argtypes = [vp, P(C.c_double)]
+    L.fgs_selftest_crmath.argtypes = [vp, i32, C.c_uint64, C.c_uint64, C.c_uint64, P(C.c_uint64)]
+    L.fgs_selftest_crmath.restype = i32
     L.fgs_measure_fp32_peak.restype = i32
     L.fgs_l1_dssim_loss.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_float, vp, P(C.c_double)]
     L.fgs_l1_dssim_loss.restype = i32

@@ -251,6 +251,13 @@ class Rasterizer:
         self._check(self._L.fgs_measure_fp32_peak(self._h, C.byref(v)))
         return v.value
 
+    def selftest_crmath(self, which: int, begin: int, count: int, seed: int = 0) -> dict:
+        """fgs_selftest_crmath: the fast correctly rounded exp (which 0) / atan2 (1, 2) against
+        their definition on the device."""
+        out = (C.c_uint64 * 3)()
+        self._check(self._L.fgs_selftest_crmath(self._h, int(which), int(begin), int(count), int(seed), out))
+        return {"checked": out[0], "mismatches": out[1], "slow": out[2]}
+
     def counts(self) -> dict:
         a = (C.c_int64 * 9)()
         self._check(self._L.fgs_last_counts(self._h, a))

@@ -124,5 +124,17 @@ def build_example(verbose=False):
     return EXAMPLE_BIN
 
 
+def build_variant(name: str, defines, verbose=False) -> str:
+    """Experiment builds: libfgs_<name>.so from the same sources with extra -D defines, loaded with
+    FGS_LIB=<name> (A/B timing of a code path on one GPU run; profiles/variants.sh)."""
+    out = os.path.join(HERE, f"libfgs_{name}.so")
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    _build_lib(out, OBJ + "_" + name, [d if d.startswith("-D") else "-D" + d for d in defines], deps, verbose, False)
+    return out
+
+
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv))
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":
+        print(build_variant(sys.argv[2], sys.argv[3:], verbose=True))
+    else:
+        print(build(verbose=True, force="--force" in sys.argv))

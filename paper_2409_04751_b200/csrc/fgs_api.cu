@@ -1269,6 +1269,23 @@ int fgs_measure_fp32_peak(fgs_context* ctx, double* ops_per_s) {
   return FGS_OK;
 }
 
+int fgs_selftest_crmath(fgs_context* ctx, int which, uint64_t begin, uint64_t count, uint64_t seed, uint64_t out[3]) {
+  if (!ctx || !out || which < 0 || which > 2) return FGS_EINVAL;
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  unsigned long long* d = nullptr;
+  FGS_CHECK(cudaMalloc(&d, 3 * sizeof(unsigned long long)));
+  cudaError_t e = cudaMemsetAsync(d, 0, 3 * sizeof(unsigned long long), ctx->stream);
+  if (e == cudaSuccess) {
+    fgs::crmath_selftest(which, begin, count, seed, d, ctx->stream);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d);
+  FGS_CHECK(e);
+  return FGS_OK;
+}
+
 int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst_bytes) {
   if (!ctx || !name || !ctx->have_fwd) return -1;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return -1;

@@ -99,6 +99,9 @@ struct BlendArgs {
 // K1 / K4b launches (preprocess.cu); host_scene: the scene arrays are pinned host memory read in
 // place over PCIe (separate instantiations, so profiles tell the two apart).
 void preprocess_launch(const PreprocessArgs& a, bool host_scene, cudaStream_t st);
+// fgs_crmath.cuh self-test (fgs_selftest_crmath): out_dev = u64[3] checked / mismatches / slow path
+void crmath_selftest(int which, uint64_t begin, uint64_t count, uint64_t seed, unsigned long long* out_dev,
+                     cudaStream_t st);
 void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene, int variant, cudaStream_t st);
 constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per K4b CTA
 

@@ -17,6 +17,7 @@
 //                         build_covariance_backward model.hpp:144-171
 
 #include "fgs_common.cuh"
+#include "fgs_crmath.cuh"
 #include "fgs_kernels.h"
 
 namespace fgs {
@@ -168,7 +169,7 @@ __device__ __forceinline__ bool quat_to_rot(const float4 q, float r[3][3]) {
 __device__ __forceinline__ bool build_covariance(const float4 q, const float s[3], float sigma[3][3]) {
   float r[3][3];
   if (!quat_to_rot(q, r)) return false;
-  const float sc[3] = {cr_expf(s[0]), cr_expf(s[1]), cr_expf(s[2])};
+  const float sc[3] = {cr_expf_fast(s[0]), cr_expf_fast(s[1]), cr_expf_fast(s[2])};
   float m[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -186,10 +187,10 @@ __device__ __forceinline__ bool build_covariance(const float4 q, const float s[3
 }
 
 // core.hpp:30-36
+// (one exp of -|x| serves both branches: the same two values, one evaluation per lane)
 __device__ __forceinline__ float sigmoid(float x) {
-  if (x >= 0.0f) return 1.0f / (1.0f + cr_expf(-x));
-  const float e = cr_expf(x);
-  return e / (1.0f + e);
+  const float e = cr_expf_fast(-fabsf(x));
+  return (x >= 0.0f ? 1.0f : e) / (1.0f + e);
 }
 
 // model.hpp:187-215 — SH basis factors Y[j] in the reference's association order.
@@ -344,7 +345,7 @@ __device__ __forceinline__ int project_covariance(const DevCamera& cam, const fl
   if (cam.model == kCamFisheye) {
     const float lz2 = x * x + y * y;
     if (z < 0.0f && lz2 < 1e-24f * z * z) return -1;
-    const float theta = cr_atan2f(sqrtf(lz2), z);
+    const float theta = cr_atan2f_fast(sqrtf(lz2), z);
     if (!(theta <= cam.fov_max + kFisheyeCullMargin)) return -1;
     prefetch_row(prefetch);
     P.ft = fisheye_terms(lz2, z, theta);
@@ -363,10 +364,10 @@ __device__ __forceinline__ int project_covariance(const DevCamera& cam, const fl
     const float s = x * x + z * z;
     if (s < 1e-24f * y * y) return -1;
     const float w = static_cast<float>(cam.width), h = static_cast<float>(cam.height);
-    float xp = w * (cr_atan2f(x, z) + kPi) / (2.0f * kPi);
+    float xp = w * (cr_atan2f_fast(x, z) + kPi) / (2.0f * kPi);
     if (xp >= w) xp -= w;
     P.pix[0] = xp;
-    P.pix[1] = h * (cr_atan2f(y, sqrtf(s)) + kPi / 2.0f) / kPi;
+    P.pix[1] = h * (cr_atan2f_fast(y, sqrtf(s)) + kPi / 2.0f) / kPi;
     prefetch_row(prefetch);
     panorama_jacobian(P.mu, cam, P.j);
   }
@@ -559,6 +560,7 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(PreprocessArgs a) {
       }
     }
     if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
+    crm::stage_tables();
     __syncthreads();
     const float* gm = reinterpret_cast<const float*>(s_geo[0]);
     const float* gl = reinterpret_cast<const float*>(s_geo[1]);
@@ -569,6 +571,7 @@ __global__ void __launch_bounds__(256, 4) preprocess_kernel(PreprocessArgs a) {
     stage = s_stage + (threadIdx.x >> 5) * (32 * kStageRow);
   } else {
     if (threadIdx.x < 2) s_counts[threadIdx.x] = 0;
+    crm::stage_tables();
     __syncthreads();
     if (valid) {
       for (int c = 0; c < 3; ++c) {
@@ -661,7 +664,7 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
       const float qn[4] = {q.x / n, q.y / n, q.z / n, q.w / n};
       float r[3][3];
       quat_to_rot(q, r);
-      const float sc[3] = {cr_expf(ls[0]), cr_expf(ls[1]), cr_expf(ls[2])};
+      const float sc[3] = {cr_expf_fast(ls[0]), cr_expf_fast(ls[1]), cr_expf_fast(ls[2])};
       float mm[3][3];
 #pragma unroll
       for (int u = 0; u < 3; ++u)
@@ -789,9 +792,39 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
 // One intersection's screen-space gradient (the blend backward's per-intersection sum at its
 // emission slot) added into acc.
 __device__ __forceinline__ void intersection_sum(const PreprocessBackwardArgs& a, uint32_t e, float* acc) {
+  FGS_DCHECK(static_cast<int64_t>(e) < a.num_isect);
   const float* p = a.partials + static_cast<size_t>(e) * 9;
 #pragma unroll
   for (int q = 0; q < 9; ++q) acc[q] = acc[q] + p[q];
+}
+
+// Slots [e, end) in order: the first ones singly up to a 4-entry boundary, then 4 entries (36
+// floats) per step as 9 independent 16-byte loads -- all in flight before the adds, which keep
+// the sequential order.
+__device__ __forceinline__ void intersection_sums(const PreprocessBackwardArgs& a, uint32_t e, uint32_t end,
+                                                  float* acc) {
+#ifdef FGS_K4B_NO_UNROLL
+  for (; e < end; ++e) intersection_sum(a, e, acc);
+#endif
+  for (; e < end && (e & 3u); ++e) intersection_sum(a, e, acc);
+  for (; e + 4 <= end; e += 4) {
+    FGS_DCHECK(static_cast<int64_t>(e) + 4 <= a.num_isect);
+    const float4* p4 = reinterpret_cast<const float4*>(a.partials + static_cast<size_t>(e) * 9);
+    float p[36];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const float4 v = __ldg(p4 + k);
+      p[4 * k] = v.x;
+      p[4 * k + 1] = v.y;
+      p[4 * k + 2] = v.z;
+      p[4 * k + 3] = v.w;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < 9; ++q) acc[q] = acc[q] + p[9 * u + q];
+  }
+  for (; e < end; ++e) intersection_sum(a, e, acc);
 }
 
 constexpr int kBwdThreads = kPreprocessBackwardThreads;
@@ -829,9 +862,19 @@ __device__ __forceinline__ void sh_rows_store(const PreprocessBackwardArgs& a, c
 // 0.305): the caller times both per context.
 template <bool HOST_SCENE, int MINB>
 __global__ void __launch_bounds__(kBwdThreads, MINB) preprocess_backward_kernel(PreprocessBackwardArgs a) {
-  __shared__ uint8_t vis[kBwdThreads];
+#ifdef FGS_K4B_OLD_ZERO
+  constexpr int kZeroRows = kBwdThreads;
+#else
+  constexpr int kZeroRows = 8 * kBwdThreads;  // rows per zero-fill round (one load of their tile counts)
+#endif
+  constexpr int kZR = kZeroRows / kBwdThreads;
+  __shared__ uint8_t vis[kZeroRows];
   __shared__ __align__(16) float s_shstage[kBwdThreads * 20];  // per-lane SH gradient factors
   const int tid = threadIdx.x, lane = tid & 31;
+#ifdef FGS_FAST_CRMATH
+  crm::stage_tables();
+  __syncthreads();
+#endif
   const int64_t q0 = a.q_begin + int64_t(blockIdx.x) * kBwdThreads;
   const int64_t q1 = q0 + kBwdThreads < a.q_end ? q0 + kBwdThreads : a.q_end;  // this CTA's slice of cval
   if (!a.accumulate) {
@@ -839,23 +882,32 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) preprocess_backward_kernel(
     const int64_t start = q0 <= a.q_begin ? a.id_begin : int64_t(a.cval[q0 - 1]) + 1;
     const int64_t end = q1 >= a.q_end ? a.id_end : int64_t(a.cval[q1 - 1]) + 1;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t c0 = start; c0 < end; c0 += kBwdThreads) {  // 128-row chunks
-      const int nloc = static_cast<int>(end - c0 < kBwdThreads ? end - c0 : kBwdThreads);
+    for (int64_t c0 = start; c0 < end; c0 += kZeroRows) {  // 1024-row rounds (a CTA spans ~N / CTAs rows)
+      const int nloc = static_cast<int>(end - c0 < kZeroRows ? end - c0 : kZeroRows);
       __syncthreads();
-      vis[tid] = tid < nloc && __ldg(a.touched + c0 + tid) > 0u;
+      uint8_t v8[kZR];
+#pragma unroll
+      for (int k = 0; k < kZR; ++k) {  // 8 independent loads in flight
+        const int r = tid + k * kBwdThreads;
+        v8[k] = r < nloc && __ldg(a.touched + c0 + r) > 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kZR; ++k) vis[tid + k * kBwdThreads] = v8[k];
       __syncthreads();
       if (a.aligned16) {
         float4* sh4 = reinterpret_cast<float4*>(a.d_sh + 48 * c0);
         for (int f = tid; f < nloc * 12; f += kBwdThreads)
           if (!vis[f / 12]) sh4[f] = z;
-        if (tid < nloc && !vis[tid]) reinterpret_cast<float4*>(a.d_rotations + 4 * c0)[tid] = z;
+        for (int r = tid; r < nloc; r += kBwdThreads)
+          if (!vis[r]) reinterpret_cast<float4*>(a.d_rotations + 4 * c0)[r] = z;
       } else {
         for (int f = tid; f < nloc * 48; f += kBwdThreads)
           if (!vis[f / 48]) a.d_sh[48 * c0 + f] = 0.f;
         for (int f = tid; f < nloc * 4; f += kBwdThreads)
           if (!vis[f / 4]) a.d_rotations[4 * c0 + f] = 0.f;
       }
-      if (tid < nloc && !vis[tid]) a.d_opacity[c0 + tid] = 0.f;
+      for (int r = tid; r < nloc; r += kBwdThreads)
+        if (!vis[r]) a.d_opacity[c0 + r] = 0.f;
       for (int f = tid; f < nloc * 3; f += kBwdThreads)
         if (!vis[f / 3]) {
           a.d_means[3 * c0 + f] = 0.f;
@@ -875,8 +927,7 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) preprocess_backward_kernel(
     const uint32_t cnt = valid ? a.touched[i] : 0u;
     const uint32_t base = valid ? a.coff[q0 + tid] : 0u;
     const bool big = cnt > 32;
-    if (!big)
-      for (uint32_t e = base; e < base + cnt; ++e) intersection_sum(a, e, sg);
+    if (!big) intersection_sums(a, base, base + cnt, sg);
     uint32_t bigs = __ballot_sync(0xffffffffu, big);
     while (bigs) {
       const int jl = __ffs(bigs) - 1;
@@ -897,6 +948,78 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) preprocess_backward_kernel(
     if (valid) gaussian_backward(a, i, sg, slot);
     sh_rows_store(a, s_shstage + (tid & ~31) * 20, valid);
   }
+}
+
+// Self-test of fgs_crmath.cuh against the definitions: which 0 = exp over the fp32 bit patterns
+// [begin, begin + count); 1 = atan2 over `count` seeded pairs of random bit patterns; 2 = over
+// seeded pairs of the fisheye / panorama domain (magnitudes 2^-30..2^30, both signs of x, ratios
+// near 1 and near j/16 boundaries). out: [checked, mismatches, slow-path evaluations].
+namespace {
+__device__ __forceinline__ uint32_t mix32(uint64_t v) {
+  v ^= v >> 33;
+  v *= 0xff51afd7ed558ccdull;
+  v ^= v >> 33;
+  v *= 0xc4ceb9fe1a85ec53ull;
+  v ^= v >> 33;
+  return static_cast<uint32_t>(v);
+}
+__device__ __forceinline__ bool same_bits(float a, float b) {
+  return __float_as_uint(a) == __float_as_uint(b) || (a != a && b != b);
+}
+__global__ void crmath_selftest_kernel(int which, uint64_t begin, uint64_t count, uint64_t seed,
+                                       unsigned long long* out) {
+  for (int t = threadIdx.x; t < 64 + 17; t += blockDim.x) crm::s_tab[t] = t < 64 ? crm::kExp2J[t] : crm::kAtanJ[t - 64];
+  __syncthreads();
+  unsigned long long bad = 0, slow = 0, n = 0;
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < count; k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t idx = begin + k;
+    bool ok;
+    if (which == 0) {
+      const float x = __uint_as_float(static_cast<uint32_t>(idx));
+      crm::exp_fast_path(x, &ok);
+      bad += !same_bits(cr_expf_fastpath(x), cr_expf(x));
+      slow += !ok;
+    } else {
+      const uint32_t h1 = mix32(idx * 2 + seed * 0x9E3779B97F4A7C15ull), h2 = mix32(idx * 2 + 1 + seed * 0x9E3779B97F4A7C15ull);
+      float y, x;
+      if (which == 1) {
+        y = __uint_as_float(h1);
+        x = __uint_as_float(h2);
+      } else {
+        const float m1 = 1.0f + (h1 & 0x7FFFFF) * 0x1p-23f, m2 = 1.0f + (h2 & 0x7FFFFF) * 0x1p-23f;
+        y = ldexpf(m1, static_cast<int>((h1 >> 23) % 61) - 30);
+        x = ldexpf(m2, static_cast<int>((h2 >> 23) % 61) - 30);
+        const uint32_t mode = (h1 ^ h2) >> 29;
+        if (mode == 1) x = y * (1.0f + static_cast<float>(static_cast<int>(h2 % 64) - 32) * 0x1p-23f);  // ratio ~1
+        if (mode == 2) y = x * ((h2 % 17) / 16.0f + static_cast<float>(static_cast<int>(h1 % 64) - 32) * 0x1p-22f);  // ~j/16
+        if (h2 & 1u) x = -x;
+        if (mode == 3 && (h1 & 2u)) y = -y;
+      }
+      crm::atan2_fast_path(y, x, &ok);
+      bad += !same_bits(cr_atan2f_fastpath(y, x), cr_atan2f(y, x));
+      slow += !ok;
+    }
+    ++n;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    slow += __shfl_xor_sync(0xffffffffu, slow, o);
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out + 0, n);
+    atomicAdd(out + 1, bad);
+    atomicAdd(out + 2, slow);
+  }
+}
+}  // namespace
+
+void crmath_selftest(int which, uint64_t begin, uint64_t count, uint64_t seed, unsigned long long* out_dev,
+                     cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  crmath_selftest_kernel<<<sms * 8, 256, 0, st>>>(which, begin, count, seed, out_dev);
 }
 
 void preprocess_launch(const PreprocessArgs& a, bool host_scene, cudaStream_t st) {

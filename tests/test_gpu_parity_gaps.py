@@ -248,3 +248,23 @@ def test_odd_n_flat_buffer_alignment(rast, oracle_mod):
     torch.cuda.synchronize()
     assert torch.equal(img_a, img_b)
     np.testing.assert_array_equal(ga, gb)
+
+
+def test_fast_correctly_rounded_math():
+    """csrc/fgs_crmath.cuh (K1 / K4b): the fast exp equals cr_expf on every one of the 2^32 fp32
+    inputs; the fast atan2 equals cr_atan2f on 2^28 random bit-pattern pairs and 2^28 pairs of
+    the camera domain; the slow path is rare (the exp's bound: < 1e-6 of finite in-range inputs)."""
+    from paper_2409_04751_b200 import Rasterizer
+
+    r = Rasterizer(0)
+    e = r.selftest_crmath(0, 0, 1 << 32)
+    assert e["checked"] == 1 << 32 and e["mismatches"] == 0, e
+    # slow path: |x| > 87, NaN, inf (every pattern above 87.0 = 0x42AE0000 in magnitude) plus the
+    # near-midpoint band of the in-range inputs
+    in_range = 2 * (0x42AE0000 + 1)
+    assert 0 <= e["slow"] - ((1 << 32) - in_range) < 1e-5 * in_range, e
+    for which, seed in ((1, 1), (2, 2)):
+        a = r.selftest_crmath(which, 0, 1 << 28, seed)
+        assert a["checked"] == 1 << 28 and a["mismatches"] == 0, (which, a)
+    cam = r.selftest_crmath(2, 0, 1 << 28, 3)
+    assert cam["slow"] < 5e-4 * cam["checked"], cam  # (1/1088 of the pairs have y = 0 exactly)
