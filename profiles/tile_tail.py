@@ -53,6 +53,13 @@ def main(cfg=2):
     r.backward(ds, cams[0], dl, BackwardOptions())
     torch.cuda.synchronize()
     off = r.debug("offsets")
+    c16 = r.debug("counters16", np.uint64).astype(np.float64)
+    span = r.debug("tile_span", np.uint64).reshape(-1, 2).astype(np.float64)
+    ok = span[:, 0] > 0
+    cta_ns = (span[ok, 1] - span[ok, 0]).sum()
+    sort_cyc = c16[4] + c16[5]
+    print(f"forward sort phase: {sort_cyc / 1.965 / cta_ns * 100:.1f} % of the summed CTA durations "
+          f"(short lists {c16[4] / max(sort_cyc, 1) * 100:.0f} %, long lists {int(c16[6])} of {int(c16[7])} tiles)")
     report("forward blend", r.debug("tile_span", np.uint64), off)
     report("backward blend", r.debug("tile_span_bwd", np.uint64), off)
     r.set_flags(0)
