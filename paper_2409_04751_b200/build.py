@@ -129,7 +129,7 @@ def build_variant(name: str, defines, verbose=False) -> str:
     FGS_LIB=<name> (A/B timing of a code path on one GPU run; profiles/variants.sh)."""
     out = os.path.join(HERE, f"libfgs_{name}.so")
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    _build_lib(out, OBJ + "_" + name, [d if d.startswith("-D") else "-D" + d for d in defines], deps, verbose, False)
+    _build_lib(out, OBJ + "_" + name, [d if d.startswith("-") else "-D" + d for d in defines], deps, verbose, False)
     return out
 
 

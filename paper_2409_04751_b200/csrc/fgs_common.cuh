@@ -71,10 +71,15 @@ struct SortedRec {
 
 // Correctly rounded fp32 exp / atan2 (double evaluation, one rounding): the definition the
 // oracle's parity mode uses.
+#ifdef FGS_ABL_FLOATMATH  // ablation build (timing only): fp32 libdevice transcendentals
+__device__ __forceinline__ float cr_expf(float x) { return expf(x); }
+__device__ __forceinline__ float cr_atan2f(float y, float x) { return atan2f(y, x); }
+#else
 __device__ __forceinline__ float cr_expf(float x) { return static_cast<float>(exp(static_cast<double>(x))); }
 __device__ __forceinline__ float cr_atan2f(float y, float x) {
   return static_cast<float>(atan2(static_cast<double>(y), static_cast<double>(x)));
 }
+#endif
 
 // The blend's decision chain in the reference's exact op order, FMA-free
 // (inc/splatting.hpp:284-287): power = -0.5*((a*dx)*dx + (c*dy)*dy) - (b*dx)*dy, from the record's

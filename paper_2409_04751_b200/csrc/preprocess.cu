@@ -536,7 +536,10 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
 // calls). Reads are then shaped for PCIe: the CTA's means and log-scales (3 KB runs each) are
 // copied through shared memory with 16-byte loads, and SH rows are fetched warp-cooperatively.
 template <bool HOST_SCENE>
-__global__ void __launch_bounds__(256, 4) preprocess_kernel(PreprocessArgs a) {
+#ifndef FGS_K1_MINB
+#define FGS_K1_MINB 4
+#endif
+__global__ void __launch_bounds__(256, FGS_K1_MINB) preprocess_kernel(PreprocessArgs a) {
   __shared__ unsigned s_counts[2];
   const int64_t i0 = int64_t(blockIdx.x) * blockDim.x;
   const int64_t i = i0 + threadIdx.x;
