@@ -106,7 +106,6 @@ struct fgs_context {
   // per intersection
   DevBuf<uint64_t> keys;
   DevBuf<uint32_t> sorted_gauss, row_list, row_hist;
-  DevBuf<uint32_t> sorted_slot;  // backward: emission slot per sorted entry
   DevBuf<float> ckpt;             // backward segments: forward checkpoints [slot][4][256]
   DevBuf<uint32_t> seg_items, tile_ckpt;
   int64_t ckpt_cap = 0;           // slots of ckpt / seg_items
@@ -238,7 +237,7 @@ size_t cap_bytes(const DevBuf<T>& b) { return b.p ? b.cap * sizeof(T) : 0; }
 size_t path_bytes(const fgs_context* c) {
   return cap_bytes(c->rec) + cap_bytes(c->state) + cap_bytes(c->dkey) + cap_bytes(c->cval) + cap_bytes(c->coff) +
          cap_bytes(c->src_off) + cap_bytes(c->touched) + cap_bytes(c->scan_status) + cap_bytes(c->rect) +
-         cap_bytes(c->radii) + cap_bytes(c->keys) + cap_bytes(c->sorted_gauss) + cap_bytes(c->row_list) + cap_bytes(c->row_hist) + cap_bytes(c->sorted_slot) + cap_bytes(c->ckpt) + cap_bytes(c->seg_items) + cap_bytes(c->tile_ckpt) +
+         cap_bytes(c->radii) + cap_bytes(c->keys) + cap_bytes(c->sorted_gauss) + cap_bytes(c->row_list) + cap_bytes(c->row_hist) + cap_bytes(c->ckpt) + cap_bytes(c->seg_items) + cap_bytes(c->tile_ckpt) +
          cap_bytes(c->partial_tile) + cap_bytes(c->tile_offsets) + cap_bytes(c->fill) + cap_bytes(c->last) +
          cap_bytes(c->tile_order) + cap_bytes(c->rowdiff) + cap_bytes(c->final_T);
 }
@@ -342,7 +341,7 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->rec.release();
   ctx->state.release();
   for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->src_off, &ctx->touched, &ctx->scan_status,
-                  &ctx->sorted_gauss, &ctx->row_list, &ctx->row_hist, &ctx->sorted_slot, &ctx->seg_items, &ctx->tile_ckpt, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
+                  &ctx->sorted_gauss, &ctx->row_list, &ctx->row_hist, &ctx->seg_items, &ctx->tile_ckpt, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
                   &ctx->scalars})
     b->release();
   ctx->keys.release();
@@ -724,7 +723,6 @@ int backward_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera
   cudaStream_t st = ctx->stream;
   const int64_t n = ctx->n, I = ctx->num_isect;
   if (n == 0) return FGS_OK;
-  FGS_CHECK(ctx->sorted_slot.ensure(static_cast<size_t>(I > 0 ? I : 1)));
   FGS_CHECK(ctx->partial_tile.ensure(static_cast<size_t>(I > 0 ? I : 1) * 9));
   ctx->aux_bytes = path_bytes(ctx);
 
@@ -741,7 +739,6 @@ int backward_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera
   ba.final_T = ctx->final_T.p;
   ba.last = ctx->last.p;
   ba.dl_dimage = dl_dimage;
-  ba.sorted_slot = ctx->sorted_slot.p;
   ba.ckpt = ctx->ckpt.p;
   ba.seg_items = ctx->seg_items.p;
   ba.tile_ckpt = ctx->tile_ckpt.p;

@@ -92,7 +92,6 @@ struct BlendArgs {
   int64_t isect_cap;
   // backward
   const float* dl_dimage;
-  uint32_t* sorted_slot;          // I: emission slot of each sorted entry (backward scratch)
   float* partial_tile;           // I x 9 per-intersection sums by emission slot (K4a -> K4b)
 };
 

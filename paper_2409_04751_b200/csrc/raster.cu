@@ -423,7 +423,8 @@ template <int PX, int MINB>
 __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArgs a) {
   constexpr int NT = 256 / PX, NW = 8 / PX;
   __shared__ float4 s_rec[2][96];          // chunk records, double buffered
-  __shared__ uint32_t s_slot[3][32];       // chunk entries' emission slots (read by the reduction)
+  __shared__ uint32_t s_ids[kSeg];         // the segment's Gaussian ids (entries below top)
+  __shared__ uint32_t s_eslot[kSeg];       // and their emission slots
   __shared__ float s_part[2][NW][32 * 9];  // per-warp sums of the chunk's entries
   __shared__ uint32_t s_mask[2][NW];       // per-warp survivor masks (bit j: entry cs + j)
   __shared__ uint32_t s_top[NW];
@@ -512,41 +513,35 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   // once) so the chunk loop fetches slots with plain asynchronous copies; entries past every
   // pixel's last contributor add nothing: zero sums at their slots
   for (uint32_t k = lo + tid; k < hi; k += NT) {
-    FGS_DCHECK(__ldg(a.sorted_gauss + k) < a.num_rec);
-    const uint32_t e = emission_slot(a, __ldg(a.sorted_gauss + k), tx, ty);
+    const uint32_t g = __ldg(a.sorted_gauss + k);
+    FGS_DCHECK(g < a.num_rec);
+    const uint32_t e = emission_slot(a, g, tx, ty);
     FGS_DCHECK(static_cast<int64_t>(e) < a.isect_cap);
     if (k < top) {
-      a.sorted_slot[k] = e;
+      s_ids[k - lo] = g;
+      s_eslot[k - lo] = e;
     } else {
       float* o = a.partial_tile + static_cast<size_t>(e) * 9;
 #pragma unroll
       for (int q = 0; q < 9; ++q) o[q] = 0.0f;
     }
   }
-  __syncthreads();  // sorted_slot written by this CTA is read back by its cp.async below
+  __syncthreads();  // ids / slots
   const int nch = static_cast<int>((top - lo + 31) / 32);
   // chunk c covers [max(lo, top - 32 (c + 1)), top - 32 c)
   auto chunk_lo = [&](int c) {
     return static_cast<uint32_t>(max(static_cast<int64_t>(lo), static_cast<int64_t>(top) - 32 * (c + 1)));
   };
-  auto prefetch = [&](int c) {  // records of chunk c into s_rec[c & 1], its slots into s_slot[c % 3]
+  auto prefetch = [&](int c) {  // records of chunk c into s_rec[c & 1] (ids from shared memory)
     if (c < nch) {
       const uint32_t cs = chunk_lo(c), n = top - 32 * c - cs;
 #pragma unroll
-      for (int t = tid; t < 128; t += NT) {  // 96 record pieces, then 32 slots
-        if (t < 96) {
-          const uint32_t j = t / 3, q = t - 3 * j;
-          if (j < n) {
-            const float4* src = reinterpret_cast<const float4*>(a.rec + __ldg(a.sorted_gauss + cs + j)) + q;
-            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_rec[c & 1][t]));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-          }
-        } else {
-          const uint32_t j = t - 96;
-          if (j < n) {
-            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_slot[c % 3][j]));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(a.sorted_slot + cs + j) : "memory");
-          }
+      for (int t = tid; t < 96; t += NT) {
+        const uint32_t j = t / 3, q = t - 3 * j;
+        if (j < n) {
+          const float4* src = reinterpret_cast<const float4*>(a.rec + s_ids[cs - lo + j]) + q;
+          const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_rec[c & 1][t]));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
         }
       }
     }
@@ -695,8 +690,9 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
 #pragma unroll
       for (int w = 0; w < NW; ++w)
         if ((s_mask[b][w] >> j) & 1u) sg = sg + s_part[b][w][idx];
-      FGS_DCHECK(static_cast<int64_t>(s_slot[c % 3][j]) < a.isect_cap);
-      a.partial_tile[static_cast<size_t>(s_slot[c % 3][j]) * 9 + q] = sg;
+      const uint32_t e = s_eslot[cs - lo + j];
+      FGS_DCHECK(static_cast<int64_t>(e) < a.isect_cap);
+      a.partial_tile[static_cast<size_t>(e) * 9 + q] = sg;
     }
     prefetch(c + 2);
   }
