@@ -216,6 +216,7 @@ __device__ void row_offsets(const BinArgs& a, int ty, const uint32_t* rowtot, co
       if (lane >= o) incl += y;
     }
     uint32_t off = carry + incl - sum;
+    const uint32_t off0 = off;
     // schedule slots: ranks within the row's bucket counts (warp-private shared counters), then
     // one global reservation per bucket for the whole row
     wsm[lane] = 0u;
@@ -236,11 +237,13 @@ __device__ void row_offsets(const BinArgs& a, int ty, const uint32_t* rowtot, co
     __syncwarp();
     if (lane < kSchedBuckets && wsm[lane]) wsm[32 + lane] = atomicAdd(cur + lane, wsm[lane]) + bprefix_lane;
     __syncwarp();
+    uint32_t o = off0;
 #pragma unroll
     for (int i = 0; i < kRowItems; ++i) {
       const int x = c0 + lane * kRowItems + i;
-      if (x < a.tiles_x)
-        a.tile_order[wsm[32 + sched_bucket(c[i])] + rk[i]] = static_cast<uint32_t>(ty * a.tiles_x + x);
+      if (x < a.tiles_x)  // the blend CTA's work item: tile and its range in one 16-byte load
+        a.tile_sched[wsm[32 + sched_bucket(c[i])] + rk[i]] = make_uint4(static_cast<uint32_t>(ty * a.tiles_x + x), o, o + c[i], 0u);
+      o += c[i];
     }
     __syncwarp();
     carry += __shfl_sync(0xffffffffu, incl, 31);

@@ -116,7 +116,8 @@ struct fgs_context {
   DevBuf<double> t_part;
   DevBuf<int> t_flag;
   // per tile / pixel
-  DevBuf<uint32_t> tile_offsets, fill, last, tile_order;
+  DevBuf<uint32_t> tile_offsets, fill, last;
+  DevBuf<uint4> tile_sched;
   DevBuf<int32_t> rowdiff;  // zero between frames (K2a zeroes what K1 added)
   size_t rowdiff_clean = 0; // entries known to be zero
   int64_t isect_cap = 0;    // capacity of the per-intersection buffers
@@ -239,7 +240,7 @@ size_t path_bytes(const fgs_context* c) {
          cap_bytes(c->src_off) + cap_bytes(c->touched) + cap_bytes(c->scan_status) + cap_bytes(c->rect) +
          cap_bytes(c->radii) + cap_bytes(c->keys) + cap_bytes(c->sorted_gauss) + cap_bytes(c->row_list) + cap_bytes(c->row_hist) + cap_bytes(c->ckpt) + cap_bytes(c->seg_items) + cap_bytes(c->tile_ckpt) +
          cap_bytes(c->partial_tile) + cap_bytes(c->tile_offsets) + cap_bytes(c->fill) + cap_bytes(c->last) +
-         cap_bytes(c->tile_order) + cap_bytes(c->rowdiff) + cap_bytes(c->final_T);
+         cap_bytes(c->tile_sched) + cap_bytes(c->rowdiff) + cap_bytes(c->final_T);
 }
 
 // Checkpoint slots for X backward segments (grows only).
@@ -341,9 +342,10 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->rec.release();
   ctx->state.release();
   for (auto* b : {&ctx->dkey, &ctx->cval, &ctx->coff, &ctx->src_off, &ctx->touched, &ctx->scan_status,
-                  &ctx->sorted_gauss, &ctx->row_list, &ctx->row_hist, &ctx->seg_items, &ctx->tile_ckpt, &ctx->tile_offsets, &ctx->fill, &ctx->last, &ctx->tile_order,
+                  &ctx->sorted_gauss, &ctx->row_list, &ctx->row_hist, &ctx->seg_items, &ctx->tile_ckpt, &ctx->tile_offsets, &ctx->fill, &ctx->last,
                   &ctx->scalars})
     b->release();
+  ctx->tile_sched.release();
   ctx->keys.release();
   ctx->t_part.release();
   ctx->t_flag.release();
@@ -457,7 +459,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   FGS_CHECK(ctx->radii.ensure(nn));
   FGS_CHECK(ctx->tile_offsets.ensure(num_tiles + 1));
   FGS_CHECK(ctx->fill.ensure(num_tiles));
-  FGS_CHECK(ctx->tile_order.ensure(num_tiles));
+  FGS_CHECK(ctx->tile_sched.ensure(num_tiles));
   FGS_CHECK(ctx->tile_ckpt.ensure(num_tiles));
   FGS_CHECK(ctx->row_hist.ensure(std::max<size_t>(fgs::bin_row_hist_words(tiles_y), 1)));
   const size_t ndiff = static_cast<size_t>(tiles_x + 1) * tiles_y;
@@ -536,7 +538,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.part_scan = ctx->scan_status.p;
   bn.tile_offsets = ctx->tile_offsets.p;
   bn.fill = ctx->fill.p;
-  bn.tile_order = ctx->tile_order.p;
+  bn.tile_sched = ctx->tile_sched.p;
   bn.isect_cap = ctx->isect_cap;
   bn.keys = ctx->keys.p;
   bn.row_list = ctx->row_list.p;
@@ -596,7 +598,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   } else {
     ctx->have_blend_count = false;
   }
-  ba.tile_order = n > 0 ? ctx->tile_order.p : nullptr;
+  ba.tile_sched = n > 0 ? ctx->tile_sched.p : nullptr;
   ba.scalars = scalars;
   ba.zero_next = ctx->scalars.p + 16 * (1 - half);
   if (ba.counters) {
@@ -750,7 +752,7 @@ int backward_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera
   ba.partial_tile = ctx->partial_tile.p;
   ba.src_off = ctx->src_off.p;
   ba.rect = ctx->rect.p;
-  ba.tile_order = I > 0 ? ctx->tile_order.p : nullptr;
+  ba.tile_sched = I > 0 ? ctx->tile_sched.p : nullptr;
   if (ba.counters) {
     const size_t nt = static_cast<size_t>(ctx->tiles_x) * ctx->tiles_y;
     FGS_CHECK(ctx->tile_span_bwd.ensure(2 * nt));

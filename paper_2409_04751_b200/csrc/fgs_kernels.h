@@ -80,7 +80,7 @@ struct BlendArgs {
   unsigned long long* counters;  // optional: E_eval, E_contrib, culled evals, max CTA cycles
   unsigned long long* tile_cycles;  // optional (with counters): per-tile CTA cycles
   unsigned long long* tile_span;    // optional (with counters): per tile [start, end] %globaltimer (ns)
-  const uint32_t* tile_order;    // optional: CTA -> tile (heaviest lists first)
+  const uint4* tile_sched;       // optional: CTA -> (tile, list begin, list end), heaviest lists first
   const uint32_t* scalars;       // forward: device scalars; exit if I > isect_cap (speculative launch)
   uint32_t* seg_cursor;          // forward: slot allocation cursor (scalars[kScalarSegPos])
   float* ckpt;                   // segment checkpoints [slot][4][256] (T, C0, C1, C2 per tile pixel)
@@ -142,7 +142,7 @@ struct BinArgs {
   uint32_t* part_scan;         // [2 * grid] CTA partials, [64] schedule histogram + cursors, [tiles_y] row totals
   uint32_t* tile_offsets;      // [num_tiles + 1]
   uint32_t* fill;              // [num_tiles] scatter cursors
-  uint32_t* tile_order;        // [num_tiles] blend schedule (optional)
+  uint4* tile_sched;           // [num_tiles] blend schedule: (tile, list begin, list end, 0)
   uint32_t* row_hist;          // [grid][tiles_y] per-CTA counts of (Gaussian, tile row) pairs
   // per intersection
   uint64_t* keys;              // [I] (depth_key << 32 | Gaussian id), grouped by tile

@@ -109,13 +109,22 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
   if (a.zero_next && blockIdx.x == 0 && threadIdx.x < 16) a.zero_next[threadIdx.x] = 0u;
   // speculative launch with buffers too small: the host grows them and launches again
   if (a.scalars && (a.scalars[kScalarI] > a.isect_cap || a.scalars[kScalarSegs] > a.ckpt_cap)) return;
-  const int tile = a.tile_order ? static_cast<int>(a.tile_order[blockIdx.x]) : static_cast<int>(blockIdx.x);
+  int tile = static_cast<int>(blockIdx.x);
+  uint32_t lo, hi;
+  if (a.tile_sched) {
+    const uint4 w = a.tile_sched[blockIdx.x];
+    tile = static_cast<int>(w.x);
+    lo = w.y;
+    hi = w.z;
+  } else {
+    lo = a.tile_offsets[tile];
+    hi = a.tile_offsets[tile + 1];
+  }
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bx = tx * kTile + ((warp & 1) << 3), by = ty * kTile + (warp >> 1) * 4 * PX;
   const int px = bx + (lane & 7);
-  const uint32_t lo = a.tile_offsets[tile], hi = a.tile_offsets[tile + 1];
-  FGS_DCHECK(tile < a.tiles_x * a.tiles_y && lo <= hi && static_cast<int64_t>(hi) <= a.isect_cap);
+  FGS_DCHECK(tile < a.tiles_x * a.tiles_y && lo == a.tile_offsets[tile] && hi == a.tile_offsets[tile + 1] && lo <= hi && static_cast<int64_t>(hi) <= a.isect_cap);
   const long long t_start = COUNTERS ? clock64() : 0;
   if (COUNTERS) span_start(a.tile_span, tile);
   // long list: reserve its segments' checkpoint slots (segments k = 1.. of the backward, then
@@ -431,15 +440,27 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   // work item: segment `seg` of a tile's list (the first num_seg_items CTAs take the segments
   // k >= 1 of long lists, the rest segment 0 of every tile, heaviest lists first)
   int tile, seg = 0;
+  uint32_t tlo, thi;  // the tile's list
   if (static_cast<int64_t>(blockIdx.x) < a.num_seg_items) {
     const uint32_t item = a.seg_items[blockIdx.x];
     seg = static_cast<int>(item >> 16);
     if (seg == static_cast<int>(kSegFinal)) return;  // a final-state slot: no work item
     tile = static_cast<int>(item & 0xFFFFu);
     FGS_DCHECK(seg >= 1);
+    tlo = a.tile_offsets[tile];
+    thi = a.tile_offsets[tile + 1];
   } else {
     const uint32_t b = blockIdx.x - static_cast<uint32_t>(a.num_seg_items);
-    tile = a.tile_order ? static_cast<int>(a.tile_order[b]) : static_cast<int>(b);
+    if (a.tile_sched) {
+      const uint4 w = a.tile_sched[b];
+      tile = static_cast<int>(w.x);
+      tlo = w.y;
+      thi = w.z;
+    } else {
+      tile = static_cast<int>(b);
+      tlo = a.tile_offsets[tile];
+      thi = a.tile_offsets[tile + 1];
+    }
   }
   FGS_DCHECK(tile >= 0 && tile < a.tiles_x * a.tiles_y);
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -448,7 +469,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   float bx0, bx1, by0, by1;
   bwd_box<PX>(tx, ty, warp, bx0, bx1, by0, by1);
   const int px = static_cast<int>(bx0) + (lane & 7);
-  const uint32_t tlo = a.tile_offsets[tile], thi = a.tile_offsets[tile + 1];
+  FGS_DCHECK(tlo == a.tile_offsets[tile] && thi == a.tile_offsets[tile + 1]);
   // this item's entries [lo, hi)
   const uint32_t lo = tlo + static_cast<uint32_t>(seg) * kSeg;
   const uint32_t hi = min(thi, lo + static_cast<uint32_t>(kSeg));
