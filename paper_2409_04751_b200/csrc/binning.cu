@@ -521,6 +521,20 @@ __device__ void scatter_rows(const BinArgs& a, uint32_t e0, uint32_t e1, const u
   }
 }
 
+// The frame's scalars (final since the second grid barrier) to the host's mapped buffer, by CTA 0
+// once its own scatter is done (so its scatter starts without waiting for the loads): one
+// 64-byte posted write of them, the sequence number and a hash binding the two (no fence: the
+// host accepts the block once the sequence number and the hash agree).
+__device__ __forceinline__ void publish_host_scalars(const BinArgs& a, int b) {
+  if (b != 0 || threadIdx.x >= 32 || !a.host_scalars) return;
+  const int tid = threadIdx.x;
+  const uint32_t v = tid < kScalarReadback ? *reinterpret_cast<volatile const uint32_t*>(a.scalars + tid) : 0u;
+  uint32_t h = host_block_hash_init(a.seq);
+  for (int t = 0; t < kScalarReadback; ++t) h = host_block_hash_step(h, __shfl_sync(0xffffffffu, v, t));
+  if (tid < kHostBlock)
+    a.host_scalars[tid] = tid < kScalarReadback ? v : (tid == kHostHash ? h : (tid == kHostSeq ? a.seq : 0u));
+}
+
 // K2: one persistent cooperative kernel, two grid barriers.
 //   phase 1: every CTA counts its chunk's tile-touching Gaussians and intersections; one warp
 //            per tile row turns K1's row-difference array into per-tile list lengths (fill[]),
@@ -659,15 +673,20 @@ __global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
   if (b == 0 && tid < 64) hist[tid] = 0;  // hist + cur: last read before this barrier
   if (ROWS) {
     const uint32_t I = a.scalars[kScalarI];
-    if (I > a.isect_cap || I == 0) return;
-    const uint32_t E = s_start[a.tiles_y];
-    scatter_rows(a, static_cast<uint32_t>(static_cast<uint64_t>(E) * b / G),
-                 static_cast<uint32_t>(static_cast<uint64_t>(E) * (b + 1) / G), s_start, s_cnt);
+    if (I <= a.isect_cap && I != 0) {
+      const uint32_t E = s_start[a.tiles_y];
+      scatter_rows(a, static_cast<uint32_t>(static_cast<uint64_t>(E) * b / G),
+                   static_cast<uint32_t>(static_cast<uint64_t>(E) * (b + 1) / G), s_start, s_cnt);
+    }
+    publish_host_scalars(a, b);
     return;
   }
 scatter : {
   const uint32_t I = a.scalars[kScalarI];
-  if (I > a.isect_cap || I == 0) return;
+  if (I > a.isect_cap || I == 0) {
+    if (!a.scatter_only) publish_host_scalars(a, b);
+    return;
+  }
   if (ROWS) {
     // relaunch after the buffers grew: phases 1-2 ran (row histograms in row_hist); the row
     // lists are written now, then the scatter
@@ -685,6 +704,7 @@ scatter : {
     for (uint32_t x = s_lo; x < s_hi; x += kSub)
       scatter_range<true>(a, m, x, min(s_hi, x + kSub), s_cnt, s_big, s_res);
   }
+  if (!a.scatter_only) publish_host_scalars(a, b);
 }
 }
 

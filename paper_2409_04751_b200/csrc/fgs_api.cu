@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -121,9 +122,9 @@ struct fgs_context {
   DevBuf<int32_t> rowdiff;  // zero between frames (K2a zeroes what K1 added)
   size_t rowdiff_clean = 0; // entries known to be zero
   int64_t isect_cap = 0;    // capacity of the per-intersection buffers
-  cudaEvent_t ev_scan = nullptr;  // after K2a's scalars reached the host
-  cudaEvent_t ev_k2 = nullptr;    // K2 done on the caller's stream
-  cudaStream_t aux = nullptr;     // the scalars' readback, off the caller's stream so K3 follows K2 directly
+  cudaEvent_t ev_k2 = nullptr;    // K2 done on the caller's stream (error detection while waiting)
+  uint32_t* d_hscalars = nullptr; // device view of h_scalars (mapped pinned memory K2 writes)
+  uint32_t frame_seq = 0;         // K2 writes it to h_scalars[kHostSeq] after the scalars
   uint32_t longest = 0;     // longest tile list of the last forward
   int var_fwd_px = 0, var_bwd_px = 0, var_k4b = 0, var_row_scatter = 0;  // launch variants (reported)
   // The device scalars alternate between two 16-word halves by frame parity; a frame's K3 zeroes
@@ -138,7 +139,7 @@ struct fgs_context {
   // [5] scan tile counter
   DevBuf<uint32_t> scalars;
   DevBuf<unsigned long long> counters, tile_cycles, tile_span, tile_span_bwd;
-  uint32_t* h_scalars = nullptr;  // pinned
+  uint32_t* h_scalars = nullptr;  // pinned, mapped: the frame's scalars, written by K2 over PCIe
   // host-call staging
   DevBuf<float> h_means, h_rot, h_ls, h_op, h_sh, h_img, h_dl, h_grad;
   DevBuf<uint8_t> h_aos;  // AoS scene upload (fgs_*_host_aos)
@@ -303,6 +304,32 @@ bool same_camera(const fgs_camera& a, const fgs_camera& b) {
 
 }  // namespace
 
+namespace {
+// Wait for K2's scalars of this frame in the mapped h_scalars (sequence number in kHostSeq),
+// watching K2's completion event for errors.
+bool host_block_ready(fgs_context* ctx) {
+  const volatile uint32_t* hs = ctx->h_scalars;
+  if (hs[fgs::kHostSeq] != ctx->frame_seq) return false;
+  std::atomic_thread_fence(std::memory_order_acquire);
+  uint32_t h = fgs::host_block_hash_init(ctx->frame_seq);
+  for (int t = 0; t < fgs::kScalarReadback; ++t) h = fgs::host_block_hash_step(h, hs[t]);
+  return h == hs[fgs::kHostHash] && hs[fgs::kHostSeq] == ctx->frame_seq;
+}
+int wait_host_scalars(fgs_context* ctx) {
+  for (uint64_t it = 0;; ++it) {
+    if (host_block_ready(ctx)) return FGS_OK;
+    if ((it & 1023) == 1023) {
+      const cudaError_t q = cudaEventQuery(ctx->ev_k2);
+      if (q == cudaSuccess) {  // K2 is done: its writes are visible
+        if (host_block_ready(ctx)) return FGS_OK;
+        return fail(ctx, FGS_ECUDA, "forward: binning finished without publishing its scalars");
+      }
+      if (q != cudaErrorNotReady) return fail(ctx, FGS_ECUDA, cudaGetErrorString(q));
+    }
+  }
+}
+}  // namespace
+
 extern "C" {
 
 int fgs_create(int device, fgs_context** out) {
@@ -312,15 +339,17 @@ int fgs_create(int device, fgs_context** out) {
   if (e != cudaSuccess) return FGS_ECUDA;
   auto* ctx = new fgs_context();
   ctx->device = device;
-  e = cudaMallocHost(&ctx->h_scalars, 16 * sizeof(uint32_t));
+  e = cudaHostAlloc(&ctx->h_scalars, 32 * sizeof(uint32_t), cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    std::memset(ctx->h_scalars, 0, 32 * sizeof(uint32_t));
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_hscalars), ctx->h_scalars, 0);
+  }
   if (e != cudaSuccess) {
     delete ctx;
     return FGS_ECUDA;
   }
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
-  cudaEventCreateWithFlags(&ctx->ev_scan, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ctx->ev_k2, cudaEventDisableTiming);
-  cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking);
   if (ctx->scalars.ensure(32) != cudaSuccess || cudaMemset(ctx->scalars.p, 0, 32 * sizeof(uint32_t)) != cudaSuccess || ctx->counters.ensure(24) != cudaSuccess ||
       false) {
     fgs_destroy(ctx);
@@ -361,12 +390,7 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->tile_span_bwd.release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
-  if (ctx->ev_scan) cudaEventDestroy(ctx->ev_scan);
   if (ctx->ev_k2) cudaEventDestroy(ctx->ev_k2);
-  if (ctx->aux) {
-    cudaStreamSynchronize(ctx->aux);
-    cudaStreamDestroy(ctx->aux);
-  }
   for (auto* v : {&ctx->pending, &ctx->spare})
     for (auto& es : *v)
       for (auto& e : es.e) cudaEventDestroy(e);
@@ -550,6 +574,8 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
                                                           : rule_row_scatter(ctx->num_isect);
   ctx->var_row_scatter = bn.row_scatter;
   bn.src_off = ctx->src_off.p;
+  bn.host_scalars = ctx->d_hscalars;
+  bn.seq = ++ctx->frame_seq;
   bn.trace = (ctx->flags & FGS_FLAG_COUNTERS) ? ctx->counters.p + 16 : nullptr;
   if (n > 0) {
     ctx->rowdiff_clean = 0;  // dirty until K2 has consumed K1's counts
@@ -560,16 +586,17 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   } else {
     FGS_CHECK(cudaMemsetAsync(ctx->tile_offsets.p, 0, sizeof(uint32_t) * (num_tiles + 1), st));
   }
-  // Large frames (GPU-bound): the readback goes on the side stream so K3 starts right after
-  // K2 (~6 us per frame at config 2). Small frames are bound by the host round trip, which
-  // the cross-stream hop would lengthen: the copy stays in order. (Last frame's I decides.)
-  cudaStream_t rb = ctx->num_isect >= (int64_t(1) << 18) ? ctx->aux : st;
-  if (rb != st) {
+  // The frame's scalars reach the host without a copy on any stream: K2's CTA 0 writes them
+  // into mapped pinned memory once they are final, then the frame's sequence number, and the
+  // host waits for that (below) while K3 is already queued behind K2. (A device-to-host copy on
+  // a side stream did the same until the application's streams outnumbered the GPU's hardware
+  // queues: the copy then shared K3's queue and K3 waited for it, +17 us per frame.)
+  const bool k2_ran = n > 0;
+  if (k2_ran) {
     FGS_CHECK(cudaEventRecord(ctx->ev_k2, st));
-    FGS_CHECK(cudaStreamWaitEvent(rb, ctx->ev_k2, 0));
+  } else {
+    FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, scalars, fgs::kScalarReadback * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   }
-  FGS_CHECK(cudaMemcpyAsync(ctx->h_scalars, scalars, fgs::kScalarReadback * sizeof(uint32_t), cudaMemcpyDeviceToHost, rb));
-  FGS_CHECK(cudaEventRecord(ctx->ev_scan, rb));
   if (timing) cudaEventRecord(ev[2], st);  // (no separate sort stage: K3 sorts each tile's list)
 
   // K3 (sort each tile's list + blend) is launched before the host knows I, against the
@@ -630,7 +657,12 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   const bool speculative = n > 0 && ctx->isect_cap > 0;
   if (speculative) launches += launch_blend();
 
-  FGS_CHECK(cudaEventSynchronize(ctx->ev_scan));
+  if (k2_ran) {
+    const int w = wait_host_scalars(ctx);
+    if (w != FGS_OK) return w;
+  } else {
+    FGS_CHECK(cudaStreamSynchronize(st));
+  }
   FGS_CHECK(cudaGetLastError());
   if (ctx->h_scalars[fgs::kScalarErr]) return fail(ctx, FGS_EDEGENERATE_QUAT, "degenerate rotation: quaternion has zero norm");
   const int64_t I = ctx->h_scalars[fgs::kScalarI];

@@ -116,6 +116,14 @@ constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, k
 // (fgs_fwd_bwd_views); K2 records where each range starts in the compacted list.
 constexpr int kGradChunks = 4;
 constexpr int kScalarReadback = kScalarChunkQ + kGradChunks - 1;  // scalars the host reads after K2
+// The host's mapped copy of the scalars (one 64-byte block K2 writes): [0, kScalarReadback) the
+// scalars, kHostHash a hash of them and the sequence number, kHostSeq the frame's sequence number.
+constexpr int kHostBlock = 16, kHostHash = 14, kHostSeq = 15;
+__host__ __device__ inline uint32_t host_block_hash_init(uint32_t seq) { return seq * 0x9E3779B1u + 0x7F4A7C15u; }
+__host__ __device__ inline uint32_t host_block_hash_step(uint32_t h, uint32_t v) {
+  h = (h ^ v) * 0x85EBCA6Bu;
+  return h ^ (h >> 13);
+}
 
 // Backward segments: a tile list longer than kSeg entries is split into ceil(L / kSeg) segments
 // that the blend backward processes as independent CTAs; the forward leaves each pixel's state
@@ -147,6 +155,8 @@ struct BinArgs {
   // per intersection
   uint64_t* keys;              // [I] (depth_key << 32 | Gaussian id), grouped by tile
   uint32_t* row_list;          // [<= I] Gaussians per tile row (row-major), the scatter's work order
+  uint32_t* host_scalars;      // mapped pinned memory: scalars[0, kScalarReadback) then seq at kHostSeq
+  uint32_t seq;                // this frame's sequence number
 };
 
 // Words of part_scan scratch bin_scan needs; words of the per-CTA row histograms.

@@ -1,13 +1,15 @@
 #!/bin/bash
 # A/B of experiment builds (python -m paper_2409_04751_b200.build --variant NAME -DFLAG...):
-# bash profiles/ab.sh <workload> <variant>... ("base" = libfgs.so); two interleaved rounds,
+# bash profiles/ab.sh <workload> <variant>... ("base" = libfgs.so, "env:VAR=value" = libfgs.so with
+# that environment); two interleaved rounds,
 # one bench line each -> gpurun_out/ab_<variant>_<round>.json, then a stage table.
 W=$1; shift
 mkdir -p gpurun_out
 for round in 1 2; do
   for v in "$@"; do
-    if [ "$v" = base ]; then lib=""; else lib=$v; fi
-    FGS_LIB=$lib python bench.py --workload $W --no-cpu-baseline --steps 300 > gpurun_out/ab_${v}_${round}.json 2> gpurun_out/ab_${v}_${round}.err
+    envs=""
+    if [ "$v" = base ]; then lib=""; elif [ "${v#env:}" != "$v" ]; then lib=""; envs="${v#env:}"; else lib=$v; fi
+    env $envs FGS_LIB=$lib python bench.py --workload $W --no-cpu-baseline --steps 300 > gpurun_out/ab_${v}_${round}.json 2> gpurun_out/ab_${v}_${round}.err
   done
 done
 python - "$@" <<'PY'
