@@ -107,13 +107,14 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
   float4 (*s0)[32] = s01[0];
   float4 (*s1)[32] = s01[1];
   if (a.zero_next && blockIdx.x == 0 && threadIdx.x < 16) a.zero_next[threadIdx.x] = 0u;
+  // the work item (loaded first: independent of the check below, so the two loads overlap)
+  uint4 w = make_uint4(blockIdx.x, 0u, 0u, 0u);
+  if (a.tile_sched) w = a.tile_sched[blockIdx.x];
   // speculative launch with buffers too small: the host grows them and launches again
   if (a.scalars && (a.scalars[kScalarI] > a.isect_cap || a.scalars[kScalarSegs] > a.ckpt_cap)) return;
-  int tile = static_cast<int>(blockIdx.x);
+  int tile = static_cast<int>(w.x);
   uint32_t lo, hi;
   if (a.tile_sched) {
-    const uint4 w = a.tile_sched[blockIdx.x];
-    tile = static_cast<int>(w.x);
     lo = w.y;
     hi = w.z;
   } else {
