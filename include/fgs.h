@@ -127,6 +127,18 @@ int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_came
 int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                       const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
 
+/* fgs_render_host for a stream of frames: returns once the frame is queued and its statistics
+ * are known (the binning's scalars), with the image (and radii) still being read back on a copy
+ * stream, so that the next frame's zero-copy scene reads (host -> device) overlap this frame's
+ * read-back (device -> host). `image` / `radii` are valid after fgs_wait, or after the next
+ * synchronous host call on this context; the scene arrays must stay unchanged until then. Two
+ * frames' device images alternate, so a third call waits for the first one's read-back. */
+int fgs_render_host_async(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                          const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats);
+/* Wait for every fgs_render_host_async read-back of this context (and order the context's stream
+ * after them). */
+int fgs_wait(fgs_context* ctx);
+
 /* A scene in array-of-structures form: n records of `stride` bytes in host memory, each holding
  * the float fields at the given byte offsets -- e.g. the reference's std::vector<Gaussian3D<float>>
  * (inc/model.hpp:18-36: mean 3, rotation 4 (w,x,y,z), log_scale 3, opacity_logit 1, sh 48 =

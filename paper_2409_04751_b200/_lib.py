@@ -80,7 +80,8 @@ EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs
            "fgs_timing", "fgs_measure_fp32_peak", "fgs_l1_dssim_loss", "fgs_adam_step", "fgs_train_step",
            "fgs_bruteforce_render", "fgs_bruteforce_render_f64", "fgs_last_transfer", "fgs_render_host_aos",
            "fgs_backward_host_aos", "fgs_comm_get_unique_id", "fgs_comm_init", "fgs_comm_init_all",
-           "fgs_comm_destroy", "fgs_allreduce_gradients", "fgs_fwd_bwd_views", "fgs_selftest_crmath"]
+           "fgs_comm_destroy", "fgs_allreduce_gradients", "fgs_fwd_bwd_views", "fgs_selftest_crmath",
+           "fgs_render_host_async", "fgs_wait"]
 
 _lib = None
 
@@ -112,8 +113,8 @@ def load(path: str | None = None):
     L.fgs_last_error.restype = C.c_char_p
     fwd = [vp, P(fgs_gaussians), P(fgs_camera), P(fgs_render_options), vp, vp, P(fgs_stats)]
     bwd = [vp, P(fgs_gaussians), P(fgs_camera), vp, P(fgs_backward_options), P(fgs_gradients)]
-    for name, args in (("fgs_forward", fwd), ("fgs_render_host", fwd), ("fgs_backward", bwd),
-                       ("fgs_backward_host", bwd)):
+    for name, args in (("fgs_forward", fwd), ("fgs_render_host", fwd), ("fgs_render_host_async", fwd),
+                       ("fgs_backward", bwd), ("fgs_backward_host", bwd)):
         getattr(L, name).argtypes = args
         getattr(L, name).restype = i32
     L.fgs_debug_get.argtypes = [vp, C.c_char_p, vp, C.c_int64]
@@ -123,6 +124,8 @@ def load(path: str | None = None):
     L.fgs_timing.argtypes = [vp, P(C.c_double), P(C.c_uint64), P(C.c_uint64), i32]
     L.fgs_timing.restype = i32
     L.fgs_measure_fp32_peak.argtypes = [vp, P(C.c_double)]
+    L.fgs_wait.argtypes = [vp]
+    L.fgs_wait.restype = i32
     L.fgs_selftest_crmath.argtypes = [vp, i32, C.c_uint64, C.c_uint64, C.c_uint64, P(C.c_uint64)]
     L.fgs_selftest_crmath.restype = i32
     L.fgs_measure_fp32_peak.restype = i32

@@ -202,6 +202,29 @@ class Rasterizer:
         self._check(rc)
         return image, r, (_stats(st) if st is not None else None)
 
+    def render_host_async(self, scene: Scene, camera: Camera, options: Optional[RenderOptions] = None, radii=None,
+                          image=None, want_stats=True):
+        """fgs_render_host_async: returns when the frame is queued (statistics known); `image` is
+        filled by the time wait() returns. The arrays are kept alive until then."""
+        s = scene.astype(np.float32)
+        if image is None:
+            image = np.empty((camera.height, camera.width, 3), np.float32)
+        r = np.empty(s.n, np.int32) if radii is True else radii
+        st = _lib.fgs_stats() if want_stats else None
+        g = self._gaussians(s)
+        cam = _camera_struct(camera)
+        o = _render_options(options, s.background)
+        rc = self._L.fgs_render_host_async(self._h, C.byref(g), C.byref(cam), C.byref(o), C.c_void_p(_ptr(image)),
+                                           C.c_void_p(_ptr(r)), C.byref(st) if st is not None else None)
+        self._check(rc)
+        self._inflight = getattr(self, "_inflight", [])[-1:] + [(s, image, r)]  # (two frames in flight)
+        return image, r, (_stats(st) if st is not None else None)
+
+    def wait(self):
+        """fgs_wait: every render_host_async image is in host memory."""
+        self._check(self._L.fgs_wait(self._h))
+        self._inflight = []
+
     def backward_host(self, scene: Scene, camera: Camera, dl_dimage, options: Optional[BackwardOptions] = None,
                       grads=None, accumulate=False):
         s = scene.astype(np.float32)

@@ -144,6 +144,14 @@ struct fgs_context {
   DevBuf<float> h_means, h_rot, h_ls, h_op, h_sh, h_img, h_dl, h_grad;
   DevBuf<uint8_t> h_aos;  // AoS scene upload (fgs_*_host_aos)
   DevBuf<int32_t> h_radii;
+  // fgs_render_host_async: device images / radii double-buffered by frame parity, read back on
+  // a copy stream (created on first use) while the next frame runs on the caller's stream
+  DevBuf<float> a_img[2];
+  DevBuf<int32_t> a_radii[2];
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_rendered = nullptr, ev_copied[2] = {nullptr, nullptr};
+  bool copy_recorded[2] = {false, false};
+  int async_parity = 0, async_last = -1;
   cudaEvent_t ev[5] = {};
   // stage timing (FGS_FLAG_TIMING): event sets pending accumulation
   struct EventSet {
@@ -360,6 +368,13 @@ int fgs_create(int device, fgs_context** out) {
 }
 
 int fgs_destroy(fgs_context* ctx) {
+  if (ctx && ctx->async_last >= 0) cudaEventSynchronize(ctx->ev_copied[ctx->async_last]);
+  if (ctx && ctx->copy_st) {
+    cudaStreamSynchronize(ctx->copy_st);
+    cudaStreamDestroy(ctx->copy_st);
+    cudaEventDestroy(ctx->ev_rendered);
+    for (auto& e : ctx->ev_copied) cudaEventDestroy(e);
+  }
   if (!ctx) return FGS_OK;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
@@ -382,6 +397,10 @@ int fgs_destroy(fgs_context* ctx) {
   ctx->rect.release();
   ctx->radii.release();
   ctx->h_radii.release();
+  for (int k = 0; k < 2; ++k) {
+    ctx->a_img[k].release();
+    ctx->a_radii[k].release();
+  }
   ctx->counters.release();
   ctx->tile_cycles.release();
   ctx->blend_count.release();
@@ -915,12 +934,27 @@ bool mapped_scene(const fgs_gaussians* s, fgs_gaussians* out) {
 }
 }  // namespace
 
-int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
-                    const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
+int fgs_wait(fgs_context* ctx) {
+  if (!ctx) return FGS_EINVAL;
+  if (ctx->async_last < 0) return FGS_OK;
+  FGS_CHECK(cudaSetDevice(ctx->device));
+  FGS_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[ctx->async_last], 0));
+  FGS_CHECK(cudaEventSynchronize(ctx->ev_copied[ctx->async_last]));
+  ctx->async_last = -1;
+  return FGS_OK;
+}
+
+namespace {
+int render_host_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                     const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats, bool async) {
   if (!ctx) return FGS_EINVAL;
   if (!scene || !camera || !image) return fail(ctx, FGS_EINVAL, "render: null argument");
   FGS_CHECK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
+  if (!async) {
+    const int w = fgs_wait(ctx);  // earlier asynchronous frames complete first
+    if (w != FGS_OK) return w;
+  }
   const size_t n = static_cast<size_t>(scene->n > 0 ? scene->n : 0), nn = n ? n : 1;
   const size_t npix = static_cast<size_t>(camera->width) * camera->height;
   FGS_CHECK(ctx->h_means.ensure(nn * 3));
@@ -943,12 +977,41 @@ int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_came
     dev = fgs_gaussians{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
   }
   ctx->scene_on_host = zero_copy;
-  int rc = fgs_forward(ctx, &dev, camera, options, ctx->h_img.p, radii ? ctx->h_radii.p : nullptr, stats);
+  float* dimg = ctx->h_img.p;
+  int32_t* drad = ctx->h_radii.p;
+  const int par = ctx->async_parity;
+  if (async) {
+    if (!ctx->copy_st) {
+      FGS_CHECK(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
+      FGS_CHECK(cudaEventCreateWithFlags(&ctx->ev_rendered, cudaEventDisableTiming));
+      for (auto& e : ctx->ev_copied) FGS_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    FGS_CHECK(ctx->a_img[par].ensure(npix * 3));
+    FGS_CHECK(ctx->a_radii[par].ensure(nn));
+    dimg = ctx->a_img[par].p;
+    drad = ctx->a_radii[par].p;
+    // the read-back of the frame that used this buffer pair two frames ago must be done first
+    if (ctx->copy_recorded[par]) FGS_CHECK(cudaStreamWaitEvent(st, ctx->ev_copied[par], 0));
+  }
+  int rc = fgs_forward(ctx, &dev, camera, options, dimg, radii ? drad : nullptr, stats);
   ctx->scene_on_host = false;
   if (rc != FGS_OK) return rc;
-  FGS_CHECK(cudaMemcpyAsync(image, ctx->h_img.p, npix * 3 * 4, cudaMemcpyDeviceToHost, st));
-  if (radii && n) FGS_CHECK(cudaMemcpyAsync(radii, ctx->h_radii.p, n * 4, cudaMemcpyDeviceToHost, st));
-  FGS_CHECK(cudaStreamSynchronize(st));
+  if (async) {
+    // the image (and radii) read back on the copy stream: device -> host while the caller's
+    // next frame reads its scene host -> device (PCIe is full duplex)
+    FGS_CHECK(cudaEventRecord(ctx->ev_rendered, st));
+    FGS_CHECK(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_rendered, 0));
+    FGS_CHECK(cudaMemcpyAsync(image, dimg, npix * 3 * 4, cudaMemcpyDeviceToHost, ctx->copy_st));
+    if (radii && n) FGS_CHECK(cudaMemcpyAsync(radii, drad, n * 4, cudaMemcpyDeviceToHost, ctx->copy_st));
+    FGS_CHECK(cudaEventRecord(ctx->ev_copied[par], ctx->copy_st));
+    ctx->copy_recorded[par] = true;
+    ctx->async_last = par;
+    ctx->async_parity = 1 - par;
+  } else {
+    FGS_CHECK(cudaMemcpyAsync(image, dimg, npix * 3 * 4, cudaMemcpyDeviceToHost, st));
+    if (radii && n) FGS_CHECK(cudaMemcpyAsync(radii, drad, n * 4, cudaMemcpyDeviceToHost, st));
+    FGS_CHECK(cudaStreamSynchronize(st));
+  }
   // bytes over PCIe: zero copy reads 40 B of geometry and the opacity of every Gaussian and,
   // per splat that survives the culls, the SH coefficients of the evaluated degree
   const int deg = options ? options->sh_degree : 3;
@@ -956,6 +1019,17 @@ int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_came
   ctx->h2d_bytes = zero_copy ? n * 44 + static_cast<uint64_t>(ctx->num_splats) * sh_bytes : n * 59 * 4;
   ctx->d2h_bytes = npix * 3 * 4 + (radii ? n * 4 : 0);
   return FGS_OK;
+}
+}  // namespace
+
+int fgs_render_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                    const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
+  return render_host_impl(ctx, scene, camera, options, image, radii, stats, false);
+}
+
+int fgs_render_host_async(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                          const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats) {
+  return render_host_impl(ctx, scene, camera, options, image, radii, stats, true);
 }
 
 namespace {

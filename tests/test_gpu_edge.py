@@ -404,3 +404,37 @@ def test_many_streams_and_interleaved_contexts(rast):
     torch.cuda.synchronize()
     assert st2.num_intersections == st0.num_intersections
     assert img2.cpu().numpy().tobytes() == img0.cpu().numpy().tobytes()
+
+
+def test_render_host_async_stream_of_frames(rast):
+    """fgs_render_host_async: frames queued back to back (two device images alternating, the
+    read-back of one overlapping the next frame's scene reads) give, after fgs_wait, the same
+    images, radii and statistics as the blocking call, frame by frame; a blocking call after
+    asynchronous ones sees them complete."""
+    import dataclasses
+
+    import torch
+    from paper_2409_04751_b200 import RenderOptions, Scene, synthetic
+
+    sc, deg, cams, _ = synthetic.config(1, n=50000)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).pin_memory().numpy()
+    hs = Scene(pin(sc.means), pin(sc.rotations), pin(sc.log_scales), pin(sc.opacity_logits), pin(sc.sh),
+               sc.background)
+    o = RenderOptions(sh_degree=deg)
+    views = [dataclasses.replace(cams[0], translation_wc=np.asarray(cams[0].translation_wc, np.float32)
+                                 + np.float32(0.05 * k)) for k in range(5)]
+    ref = [rast.render_host(hs, v, o) for v in views]
+    outs = []
+    for v in views:
+        img = torch.empty((v.height, v.width, 3), dtype=torch.float32).pin_memory().numpy()
+        outs.append(rast.render_host_async(hs, v, o, radii=True, image=img))
+    rast.wait()
+    for (img, radii, st), (ri, rr, rs) in zip(outs, ref):
+        assert img.tobytes() == ri.tobytes()
+        assert np.array_equal(radii, rr)
+        assert st.num_intersections == rs.num_intersections
+    # asynchronous frames, then a blocking one without an explicit wait
+    img_a = torch.empty_like(torch.from_numpy(ref[0][0])).pin_memory().numpy()
+    rast.render_host_async(hs, views[1], o, image=img_a)
+    img_b, _, _ = rast.render_host(hs, views[2], o)
+    assert img_a.tobytes() == ref[1][0].tobytes() and img_b.tobytes() == ref[2][0].tobytes()
