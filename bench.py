@@ -180,7 +180,7 @@ def run_ours(args, ws, rank, local):
     scene_bytes = scene.n * (236 if deg == 3 else 56)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if scene_bytes < 126e6 else None
 
-    def timed(fn, steps, warmup, sampler=None, finish=None):
+    def timed(fn, steps, warmup, sampler=None, finish=None, allow_flush=True):
         r.set_flags(0)
         for _ in range(warmup):
             fn()
@@ -193,7 +193,8 @@ def run_ours(args, ws, rank, local):
         r.timing(reset=True)
         if sampler:
             sampler.sample()
-        if flush is None:
+        use_flush = flush is not None and allow_flush
+        if not use_flush:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for i in range(steps):
@@ -220,7 +221,7 @@ def run_ours(args, ws, rank, local):
             sampler.sample()
         if dist is not None:
             dist.barrier()
-        ms = (e0.elapsed_time(e1) if flush is None else sum(a.elapsed_time(b) for a, b in ev)) / steps
+        ms = (e0.elapsed_time(e1) if not use_flush else sum(a.elapsed_time(b) for a, b in ev)) / steps
         if dist is not None:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -312,11 +313,19 @@ def run_ours(args, ws, rank, local):
                 k[0] += 1
             finish = r.wait
         else:
+            # forward + backward frames through the pipelined host calls: each frame's image and
+            # gradient read-backs overlap the next frame's scene reads and dL/dimage upload
+            hgr2 = [hgr, torch.zeros(59 * scene.n, dtype=torch.float32).pin_memory().numpy()]
+            k = [0]
+
             def step():
-                r.render_host(hs, cam, ropt, radii=None, image=himg, want_stats=False)
-                r.backward_host(hs, cam, hdl, bopt, grads=hgr)
+                r.render_host_async(hs, cam, ropt, radii=None, image=himg2[k[0] & 1], want_stats=False)
+                r.backward_host_async(hs, cam, hdl, bopt, grads=hgr2[k[0] & 1])
+                k[0] += 1
+            finish = r.wait
         e_steps = max(3, min(args.steps, 20))
-        ms_e2e, _ = timed(step, e_steps, 2, finish=finish)
+        # (no L2 flush: every step streams its inputs from host memory)
+        ms_e2e, _ = timed(step, e_steps, 2, finish=finish, allow_flush=False)
         # bytes actually moved over PCIe per step (pinned scene arrays are read in place by K1 /
         # K4b, only what they touch): measured by the library on the last step
         if FWD_ONLY[cfg]:
@@ -330,7 +339,9 @@ def run_ours(args, ws, rank, local):
         e2e = {"value": round(ws * 1000.0 / ms_e2e, 2), "unit": "FPS" if FWD_ONLY[cfg] else "views/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms_e2e, 3),
                "path": ("fgs_render_host_async (pipelined frames: each frame's image read-back overlaps "
-                        "the next frame's zero-copy scene reads)") if FWD_ONLY[cfg] else "fgs_render_host + fgs_backward_host"}
+                        "the next frame's zero-copy scene reads)") if FWD_ONLY[cfg] else
+                       ("fgs_render_host_async + fgs_backward_host_async (pipelined frames: image and gradient "
+                        "read-backs overlap the next frame's scene reads and dL/dimage upload)")}
 
     cpu = cpu_fb = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -135,8 +135,13 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
  * frames' device images alternate, so a third call waits for the first one's read-back. */
 int fgs_render_host_async(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
                           const fgs_render_options* options, float* image, int32_t* radii, fgs_stats* stats);
-/* Wait for every fgs_render_host_async read-back of this context (and order the context's stream
- * after them). */
+/* fgs_backward_host for a stream of frames: returns once the backward is queued, the gradients
+ * being read back on the copy stream (two device gradient buffers alternate); `grads` are valid
+ * after fgs_wait or the next synchronous host call. */
+int fgs_backward_host_async(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                            const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
+/* Wait for every fgs_render_host_async / fgs_backward_host_async read-back of this context (and
+ * order the context's stream after them). */
 int fgs_wait(fgs_context* ctx);
 
 /* A scene in array-of-structures form: n records of `stride` bytes in host memory, each holding

@@ -81,7 +81,7 @@ EXPORTS = ["fgs_create", "fgs_destroy", "fgs_set_stream", "fgs_last_error", "fgs
            "fgs_bruteforce_render", "fgs_bruteforce_render_f64", "fgs_last_transfer", "fgs_render_host_aos",
            "fgs_backward_host_aos", "fgs_comm_get_unique_id", "fgs_comm_init", "fgs_comm_init_all",
            "fgs_comm_destroy", "fgs_allreduce_gradients", "fgs_fwd_bwd_views", "fgs_selftest_crmath",
-           "fgs_render_host_async", "fgs_wait"]
+           "fgs_render_host_async", "fgs_backward_host_async", "fgs_wait"]
 
 _lib = None
 
@@ -114,7 +114,7 @@ def load(path: str | None = None):
     fwd = [vp, P(fgs_gaussians), P(fgs_camera), P(fgs_render_options), vp, vp, P(fgs_stats)]
     bwd = [vp, P(fgs_gaussians), P(fgs_camera), vp, P(fgs_backward_options), P(fgs_gradients)]
     for name, args in (("fgs_forward", fwd), ("fgs_render_host", fwd), ("fgs_render_host_async", fwd),
-                       ("fgs_backward", bwd), ("fgs_backward_host", bwd)):
+                       ("fgs_backward", bwd), ("fgs_backward_host", bwd), ("fgs_backward_host_async", bwd)):
         getattr(L, name).argtypes = args
         getattr(L, name).restype = i32
     L.fgs_debug_get.argtypes = [vp, C.c_char_p, vp, C.c_int64]

@@ -241,6 +241,25 @@ class Rasterizer:
         self._check(rc)
         return grads
 
+    def backward_host_async(self, scene: Scene, camera: Camera, dl_dimage, options: Optional[BackwardOptions] = None,
+                            grads=None, accumulate=False):
+        """fgs_backward_host_async: returns when the backward is queued; `grads` are filled by the
+        time wait() returns (the arrays are kept alive until then)."""
+        s = scene.astype(np.float32)
+        dl = np.ascontiguousarray(dl_dimage, np.float32)
+        if dl.shape != (camera.height, camera.width, 3):
+            raise InvalidArgument("rasterize_backward: image gradient shape does not match context")
+        if grads is None:
+            grads = np.zeros(59 * s.n, np.float32)
+        gs = _grad_struct(grads, s.n)
+        cam = _camera_struct(camera)
+        o = _backward_options(options, accumulate)
+        rc = self._L.fgs_backward_host_async(self._h, C.byref(self._gaussians(s)), C.byref(cam),
+                                             C.c_void_p(_ptr(dl)), C.byref(o), C.byref(gs))
+        self._check(rc)
+        self._inflight = getattr(self, "_inflight", [])[-3:] + [(s, dl, grads)]
+        return grads
+
     def last_transfer(self) -> dict:
         """PCIe bytes moved by the last render_host / backward_host call (zero copy reads only
         what the kernels touch when the scene arrays are pinned host memory)."""

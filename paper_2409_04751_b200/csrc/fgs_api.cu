@@ -152,6 +152,11 @@ struct fgs_context {
   cudaEvent_t ev_rendered = nullptr, ev_copied[2] = {nullptr, nullptr};
   bool copy_recorded[2] = {false, false};
   int async_parity = 0, async_last = -1;
+  // fgs_backward_host_async: device gradients double-buffered, read back on the copy stream
+  DevBuf<float> a_grad[2];
+  cudaEvent_t ev_bdone = nullptr, ev_gcopied[2] = {nullptr, nullptr};
+  bool gcopy_recorded[2] = {false, false};
+  int gasync_parity = 0, gasync_last = -1;
   cudaEvent_t ev[5] = {};
   // stage timing (FGS_FLAG_TIMING): event sets pending accumulation
   struct EventSet {
@@ -313,6 +318,18 @@ bool same_camera(const fgs_camera& a, const fgs_camera& b) {
 }  // namespace
 
 namespace {
+// The copy stream of the asynchronous host calls and its events (created on first use).
+cudaError_t ensure_copy_stream(fgs_context* ctx) {
+  if (ctx->copy_st) return cudaSuccess;
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking);
+  for (cudaEvent_t* ev : {&ctx->ev_rendered, &ctx->ev_bdone, &ctx->ev_copied[0], &ctx->ev_copied[1],
+                          &ctx->ev_gcopied[0], &ctx->ev_gcopied[1]})
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  return e;
+}
+}  // namespace
+
+namespace {
 // Wait for K2's scalars of this frame in the mapped h_scalars (sequence number in kHostSeq),
 // watching K2's completion event for errors.
 bool host_block_ready(fgs_context* ctx) {
@@ -368,12 +385,13 @@ int fgs_create(int device, fgs_context** out) {
 }
 
 int fgs_destroy(fgs_context* ctx) {
-  if (ctx && ctx->async_last >= 0) cudaEventSynchronize(ctx->ev_copied[ctx->async_last]);
   if (ctx && ctx->copy_st) {
     cudaStreamSynchronize(ctx->copy_st);
     cudaStreamDestroy(ctx->copy_st);
     cudaEventDestroy(ctx->ev_rendered);
+    cudaEventDestroy(ctx->ev_bdone);
     for (auto& e : ctx->ev_copied) cudaEventDestroy(e);
+    for (auto& e : ctx->ev_gcopied) cudaEventDestroy(e);
   }
   if (!ctx) return FGS_OK;
   cudaSetDevice(ctx->device);
@@ -400,6 +418,7 @@ int fgs_destroy(fgs_context* ctx) {
   for (int k = 0; k < 2; ++k) {
     ctx->a_img[k].release();
     ctx->a_radii[k].release();
+    ctx->a_grad[k].release();
   }
   ctx->counters.release();
   ctx->tile_cycles.release();
@@ -936,11 +955,16 @@ bool mapped_scene(const fgs_gaussians* s, fgs_gaussians* out) {
 
 int fgs_wait(fgs_context* ctx) {
   if (!ctx) return FGS_EINVAL;
-  if (ctx->async_last < 0) return FGS_OK;
+  if (ctx->async_last < 0 && ctx->gasync_last < 0) return FGS_OK;
   FGS_CHECK(cudaSetDevice(ctx->device));
-  FGS_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[ctx->async_last], 0));
-  FGS_CHECK(cudaEventSynchronize(ctx->ev_copied[ctx->async_last]));
+  for (cudaEvent_t e : {ctx->async_last >= 0 ? ctx->ev_copied[ctx->async_last] : nullptr,
+                        ctx->gasync_last >= 0 ? ctx->ev_gcopied[ctx->gasync_last] : nullptr}) {
+    if (!e) continue;
+    FGS_CHECK(cudaStreamWaitEvent(ctx->stream, e, 0));
+    FGS_CHECK(cudaEventSynchronize(e));
+  }
   ctx->async_last = -1;
+  ctx->gasync_last = -1;
   return FGS_OK;
 }
 
@@ -981,11 +1005,7 @@ int render_host_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_cam
   int32_t* drad = ctx->h_radii.p;
   const int par = ctx->async_parity;
   if (async) {
-    if (!ctx->copy_st) {
-      FGS_CHECK(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
-      FGS_CHECK(cudaEventCreateWithFlags(&ctx->ev_rendered, cudaEventDisableTiming));
-      for (auto& e : ctx->ev_copied) FGS_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
+    FGS_CHECK(ensure_copy_stream(ctx));
     FGS_CHECK(ctx->a_img[par].ensure(npix * 3));
     FGS_CHECK(ctx->a_radii[par].ensure(nn));
     dimg = ctx->a_img[par].p;
@@ -1035,15 +1055,34 @@ int fgs_render_host_async(fgs_context* ctx, const fgs_gaussians* scene, const fg
 namespace {
 // Host-buffer backward with the scene already on the device (dev) or mapped (zero_copy).
 int backward_host_dev(fgs_context* ctx, const fgs_gaussians& dev, bool zero_copy, const fgs_camera* camera,
-                      const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads);
+                      const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads,
+                      bool async = false);
+int backward_host_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, const float* dl_dimage,
+                       const fgs_backward_options* options, fgs_gradients* grads, bool async);
 }  // namespace
 
 int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, const float* dl_dimage,
                       const fgs_backward_options* options, fgs_gradients* grads) {
+  return backward_host_impl(ctx, scene, camera, dl_dimage, options, grads, false);
+}
+
+int fgs_backward_host_async(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera,
+                            const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads) {
+  return backward_host_impl(ctx, scene, camera, dl_dimage, options, grads, true);
+}
+
+namespace {
+
+int backward_host_impl(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* camera, const float* dl_dimage,
+                       const fgs_backward_options* options, fgs_gradients* grads, bool async) {
   if (!ctx) return FGS_EINVAL;
   if (!scene || !camera || !dl_dimage || !grads) return fail(ctx, FGS_EINVAL, "backward: null argument");
   FGS_CHECK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
+  if (!async && ctx->gasync_last >= 0) {
+    const int w = fgs_wait(ctx);
+    if (w != FGS_OK) return w;
+  }
   const size_t n = static_cast<size_t>(ctx->n), nn = n ? n : 1;
   if (static_cast<int64_t>(n) != scene->n)
     return fail(ctx, FGS_EINVAL, "backward: forward context was built for a different scene");
@@ -1066,14 +1105,13 @@ int fgs_backward_host(fgs_context* ctx, const fgs_gaussians* scene, const fgs_ca
     }
     dev = fgs_gaussians{scene->n, ctx->h_means.p, ctx->h_rot.p, ctx->h_ls.p, ctx->h_op.p, ctx->h_sh.p};
   }
-  const int rc = backward_host_dev(ctx, dev, zero_copy, camera, dl_dimage, options, grads);
+  const int rc = backward_host_dev(ctx, dev, zero_copy, camera, dl_dimage, options, grads, async);
   if (rc == FGS_OK && !zero_copy) ctx->h2d_bytes += n * 59 * 4;
   return rc;
 }
 
-namespace {
 int backward_host_dev(fgs_context* ctx, const fgs_gaussians& dev, bool zero_copy, const fgs_camera* camera,
-                      const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads) {
+                      const float* dl_dimage, const fgs_backward_options* options, fgs_gradients* grads, bool async) {
   cudaStream_t st = ctx->stream;
   const size_t n = static_cast<size_t>(ctx->n), nn = n ? n : 1;
   const size_t npix = static_cast<size_t>(camera->width) * camera->height;
@@ -1081,6 +1119,14 @@ int backward_host_dev(fgs_context* ctx, const fgs_gaussians& dev, bool zero_copy
   FGS_CHECK(ctx->h_grad.ensure(nn * 59));
   FGS_CHECK(cudaMemcpyAsync(ctx->h_dl.p, dl_dimage, npix * 3 * 4, cudaMemcpyHostToDevice, st));
   float* g = ctx->h_grad.p;
+  const int gp = ctx->gasync_parity;
+  if (async) {
+    FGS_CHECK(ensure_copy_stream(ctx));
+    FGS_CHECK(ctx->a_grad[gp].ensure(nn * 59));
+    g = ctx->a_grad[gp].p;
+    // the read-back of the call that used this buffer two calls ago must be done first
+    if (ctx->gcopy_recorded[gp]) FGS_CHECK(cudaStreamWaitEvent(st, ctx->ev_gcopied[gp], 0));
+  }
   fgs_gradients dg{g, g + 3 * nn, g + 7 * nn, g + 10 * nn, g + 11 * nn};
   const bool acc = options && options->accumulate;
   if (acc && n) {
@@ -1094,14 +1140,29 @@ int backward_host_dev(fgs_context* ctx, const fgs_gaussians& dev, bool zero_copy
   int rc = fgs_backward(ctx, &dev, camera, ctx->h_dl.p, options, &dg);
   ctx->scene_on_host = false;
   if (rc != FGS_OK) return rc;
-  if (n) {
-    FGS_CHECK(cudaMemcpyAsync(grads->d_means, dg.d_means, n * 3 * 4, cudaMemcpyDeviceToHost, st));
-    FGS_CHECK(cudaMemcpyAsync(grads->d_rotations, dg.d_rotations, n * 4 * 4, cudaMemcpyDeviceToHost, st));
-    FGS_CHECK(cudaMemcpyAsync(grads->d_log_scales, dg.d_log_scales, n * 3 * 4, cudaMemcpyDeviceToHost, st));
-    FGS_CHECK(cudaMemcpyAsync(grads->d_opacity_logits, dg.d_opacity_logits, n * 4, cudaMemcpyDeviceToHost, st));
-    FGS_CHECK(cudaMemcpyAsync(grads->d_sh, dg.d_sh, n * 48 * 4, cudaMemcpyDeviceToHost, st));
+  // the gradients back: on the copy stream for the asynchronous call (device -> host while the
+  // caller's next frame reads its scene and uploads its dL/dimage host -> device)
+  cudaStream_t cs = st;
+  if (async) {
+    FGS_CHECK(cudaEventRecord(ctx->ev_bdone, st));
+    FGS_CHECK(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_bdone, 0));
+    cs = ctx->copy_st;
   }
-  FGS_CHECK(cudaStreamSynchronize(st));
+  if (n) {
+    FGS_CHECK(cudaMemcpyAsync(grads->d_means, dg.d_means, n * 3 * 4, cudaMemcpyDeviceToHost, cs));
+    FGS_CHECK(cudaMemcpyAsync(grads->d_rotations, dg.d_rotations, n * 4 * 4, cudaMemcpyDeviceToHost, cs));
+    FGS_CHECK(cudaMemcpyAsync(grads->d_log_scales, dg.d_log_scales, n * 3 * 4, cudaMemcpyDeviceToHost, cs));
+    FGS_CHECK(cudaMemcpyAsync(grads->d_opacity_logits, dg.d_opacity_logits, n * 4, cudaMemcpyDeviceToHost, cs));
+    FGS_CHECK(cudaMemcpyAsync(grads->d_sh, dg.d_sh, n * 48 * 4, cudaMemcpyDeviceToHost, cs));
+  }
+  if (async) {
+    FGS_CHECK(cudaEventRecord(ctx->ev_gcopied[gp], cs));
+    ctx->gcopy_recorded[gp] = true;
+    ctx->gasync_last = gp;
+    ctx->gasync_parity = 1 - gp;
+  } else {
+    FGS_CHECK(cudaStreamSynchronize(st));
+  }
   ctx->h2d_bytes = npix * 3 * 4 + (zero_copy ? static_cast<uint64_t>(ctx->num_compact) * 44 : 0) +
                    (acc ? n * 59 * 4 : 0);
   ctx->d2h_bytes = n * 59 * 4;
