@@ -93,6 +93,18 @@ class Renderer {
     return out;
   }
 
+  // A stream of frames (fgs_render_host_async): the image goes into `image` (width * height * 3
+  // floats, caller-owned, ideally page-locked) -- valid after wait(); the scene must stay
+  // unchanged until then. Returns the frame's statistics.
+  fgs_stats render_async(const SceneSoA& scene, const fgs_camera& camera, float* image, int sh_degree = 3) {
+    fgs_render_options o{sh_degree, 1, {scene.background[0], scene.background[1], scene.background[2]}};
+    const fgs_gaussians g = scene.view();
+    fgs_stats st{};
+    throw_on(fgs_render_host_async(ctx_, &g, &camera, &o, image, nullptr, &st), ctx_);
+    return st;
+  }
+  void wait() { throw_on(fgs_wait(ctx_), ctx_); }
+
   fgs_context* handle() { return ctx_; }
 
  private:
