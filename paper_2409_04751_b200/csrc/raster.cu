@@ -499,6 +499,15 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   // (gradients.hpp:132, :143) kept only through its dot product with dL/dpixel. A pixel whose last
   // contributor lies past this segment starts from the forward's checkpoint at hi: T there, and
   // the suffix colour = (image value) - (colour accumulated before hi).
+  // the segment's Gaussian ids first (their loads in flight with the pixels' below; the emission
+  // slots after the pixels' state, so the two dependent-load chains overlap)
+  constexpr int kEnt = (kSeg + NT - 1) / NT;  // entries per thread
+  uint32_t gk[kEnt];
+#pragma unroll
+  for (int t = 0; t < kEnt; ++t) {
+    const uint32_t k = lo + tid + t * NT;
+    gk[t] = k < hi ? __ldg(a.sorted_gauss + k) : 0u;
+  }
   float T[PX], dl[PX][3], ds[PX], fy[PX];
   uint32_t last[PX];
   uint32_t mylast = lo;
@@ -535,28 +544,29 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   }
   const uint32_t wlast = __reduce_max_sync(0xffffffffu, mylast);
   if (lane == 0) s_top[warp] = wlast;
-  __syncthreads();
+  // every entry's emission slot (two dependent loads each, all in flight at once), with its id in
+  // shared memory for the chunk loop's record copies and the reduction's stores
+#pragma unroll
+  for (int t = 0; t < kEnt; ++t) {
+    const uint32_t k = lo + tid + t * NT;
+    if (k < hi) {
+      FGS_DCHECK(gk[t] < a.num_rec);
+      const uint32_t e = emission_slot(a, gk[t], tx, ty);
+      FGS_DCHECK(static_cast<int64_t>(e) < a.isect_cap);
+      s_ids[k - lo] = gk[t];
+      s_eslot[k - lo] = e;
+    }
+  }
+  __syncthreads();  // top, ids, slots
   uint32_t top = lo;
 #pragma unroll
   for (int w = 0; w < NW; ++w) top = max(top, s_top[w]);
-  // every entry's emission slot, computed up front (two dependent loads each, all in flight at
-  // once) so the chunk loop fetches slots with plain asynchronous copies; entries past every
-  // pixel's last contributor add nothing: zero sums at their slots
-  for (uint32_t k = lo + tid; k < hi; k += NT) {
-    const uint32_t g = __ldg(a.sorted_gauss + k);
-    FGS_DCHECK(g < a.num_rec);
-    const uint32_t e = emission_slot(a, g, tx, ty);
-    FGS_DCHECK(static_cast<int64_t>(e) < a.isect_cap);
-    if (k < top) {
-      s_ids[k - lo] = g;
-      s_eslot[k - lo] = e;
-    } else {
-      float* o = a.partial_tile + static_cast<size_t>(e) * 9;
+  // entries past every pixel's last contributor add nothing: zero sums at their slots
+  for (uint32_t k = top + tid; k < hi; k += NT) {
+    float* o = a.partial_tile + static_cast<size_t>(s_eslot[k - lo]) * 9;
 #pragma unroll
-      for (int q = 0; q < 9; ++q) o[q] = 0.0f;
-    }
+    for (int q = 0; q < 9; ++q) o[q] = 0.0f;
   }
-  __syncthreads();  // ids / slots
   const int nch = static_cast<int>((top - lo + 31) / 32);
   // chunk c covers [max(lo, top - 32 (c + 1)), top - 32 c)
   auto chunk_lo = [&](int c) {
