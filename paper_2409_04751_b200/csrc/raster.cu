@@ -837,13 +837,16 @@ int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStrea
   const int tiles = a.tiles_x * a.tiles_y;
   const int px = env == 1 || env == 2 ? env
                  : (tiles >= 1024 && num_isect >= 32 * static_cast<int64_t>(tiles) ? 2 : 1);
-  // 2 pixels per lane: fitted to 6 CTAs per SM (72 registers, no spills; measured faster at
-  // configs 1, 2 and 4) or 8 (64, spills); identical results. FGS_BWD_MINB=6|8 overrides.
+  // 2 pixels per lane: fitted to 8 CTAs per SM (64 registers, a few spills) or 6 (77, none);
+  // identical results. Since the segment's ids / slots moved to shared memory, 8 is faster at
+  // every config (config 2 0.2526 -> 0.2463 ms, config 1 0.1276 -> 0.1240, configs 3 / 4 -0.4 %
+  // / -0.1 %; it was 7 % slower before). FGS_BWD_MINB=6|8 overrides.
   static const int env_minb = [] {
     const char* v = std::getenv("FGS_BWD_MINB");
     return v ? std::atoi(v) : 0;
   }();
-  const int minb = env_minb == 6 || env_minb == 8 ? env_minb : (variant == 2 ? 8 : 6);
+  const int minb = env_minb == 6 || env_minb == 8 ? env_minb : 8;
+  (void)variant;
   if (px_used) *px_used = px;
   // one CTA per (tile, segment): the long lists' segments k >= 1 first, then every tile's first
   const int grid = tiles + static_cast<int>(a.num_seg_items);
