@@ -778,6 +778,13 @@ bool encode_rec_map(RecTensorMap& m, const void* rec, int64_t rows) {
 }
 }  // namespace
 
+namespace {
+int env_carveout(const char* name, int dflt) {  // (experiments: a percent from the environment)
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+}  // namespace
+
 int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStream_t st) {
   static PerDevice attrs;
   attrs.get([] {
@@ -788,7 +795,7 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStr
                           reinterpret_cast<const void*>(blend_forward_kernel<kModeBlendCount, 1>),
                           reinterpret_cast<const void*>(blend_forward_kernel<0, 1>),
                           reinterpret_cast<const void*>(blend_forward_kernel<0, 1, true>)})
-      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 78);
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, env_carveout("FGS_FWD1_CARVEOUT", 78));
     for (const void* f : {reinterpret_cast<const void*>(blend_forward_kernel<kModeCounters, 2>),
                           reinterpret_cast<const void*>(blend_forward_kernel<kModeBlendCount, 2>),
                           reinterpret_cast<const void*>(blend_forward_kernel<0, 2>)})
@@ -847,6 +854,18 @@ int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStrea
   }();
   const int minb = env_minb == 6 || env_minb == 8 ? env_minb : 8;
   (void)variant;
+  static PerDevice attrs;
+  attrs.get([] {
+    // shared-memory carveout of the backward blends (FGS_BWD_CARVEOUT=percent; default: the
+    // driver's choice)
+    const char* v = std::getenv("FGS_BWD_CARVEOUT");
+    if (v && *v)
+      for (const void* f : {reinterpret_cast<const void*>(blend_backward_kernel<1, 4>),
+                            reinterpret_cast<const void*>(blend_backward_kernel<2, 6>),
+                            reinterpret_cast<const void*>(blend_backward_kernel<2, 8>)})
+        cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(v));
+    return 1;
+  });
   if (px_used) *px_used = px;
   // one CTA per (tile, segment): the long lists' segments k >= 1 first, then every tile's first
   const int grid = tiles + static_cast<int>(a.num_seg_items);
