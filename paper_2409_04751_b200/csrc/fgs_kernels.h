@@ -129,7 +129,10 @@ __host__ __device__ inline uint32_t host_block_hash_step(uint32_t h, uint32_t v)
 // that the blend backward processes as independent CTAs; the forward leaves each pixel's state
 // (T and accumulated colour) at every segment boundary, plus its final (T, colour), in one
 // checkpoint slot per segment (4 x 256 floats, SoA over the tile's pixels).
-constexpr int kSeg = 256;
+#ifndef FGS_SEG  // (experiment builds: 128 / 192 / 512 measured slower forward + backward at config 2)
+#define FGS_SEG 256
+#endif
+constexpr int kSeg = FGS_SEG;
 constexpr uint32_t kSegFinal = 0xFFFFu;  // item marker of a tile's final-state slot
 
 struct BinArgs {
