@@ -32,7 +32,13 @@ namespace {
 
 // forward: splats whose alphas are computed together (measured: 4 for 1 pixel per lane, 3 for 2)
 template <int PX>
-constexpr int kGroup = PX == 1 ? 4 : 3;
+#ifndef FGS_FWD_G1  // (build knobs; re-measured late round 2: 3 / 5 at 1 pixel, 2 / 4 at 2 pixels slower)
+#define FGS_FWD_G1 4
+#endif
+#ifndef FGS_FWD_G2
+#define FGS_FWD_G2 3
+#endif
+constexpr int kGroup = PX == 1 ? FGS_FWD_G1 : FGS_FWD_G2;
 
 struct PixelState {
   float T, C0, C1, C2;
