@@ -526,6 +526,7 @@ __device__ void scatter_rows(const BinArgs& a, uint32_t e0, uint32_t e1, const u
 // 64-byte posted write of them, the sequence number and a hash binding the two (no fence: the
 // host accepts the block once the sequence number and the hash agree).
 __device__ __forceinline__ void publish_host_scalars(const BinArgs& a, int b) {
+  pdl_trigger();  // (this CTA's part of K2 is done)
   if (b != 0 || threadIdx.x >= 32 || !a.host_scalars) return;
   const int tid = threadIdx.x;
   const uint32_t v = tid < kScalarReadback ? *reinterpret_cast<volatile const uint32_t*>(a.scalars + tid) : 0u;

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <mutex>
+#include <utility>
 
 #include <cuda_runtime.h>
 
@@ -26,6 +27,41 @@ namespace fgs {
   do {                   \
   } while (0)
 #endif
+
+// Programmatic dependent launch: the next kernel of the stream may start its CTAs while this
+// one's last CTAs finish (each CTA signals when its own output is written); the dependent waits
+// for the whole primary grid (and its memory) before reading any of it. Both are no-ops for a
+// kernel launched without the attribute. FGS_NO_PDL builds the plain launches (A/B).
+__device__ __forceinline__ void pdl_wait() {
+#ifndef FGS_NO_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#ifndef FGS_NO_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+#ifdef FGS_NO_PDL
+  kernel<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+  return cudaGetLastError();
+#else
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+#endif
+}
 
 // Forward-model constants (reference inc/core.hpp:43-53), rounded to float exactly as the
 // reference's S(...) casts do.

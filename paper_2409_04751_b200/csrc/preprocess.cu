@@ -874,6 +874,7 @@ __global__ void __launch_bounds__(kBwdThreads, MINB) preprocess_backward_kernel(
   __shared__ uint8_t vis[kZeroRows];
   __shared__ __align__(16) float s_shstage[kBwdThreads * 20];  // per-lane SH gradient factors
   const int tid = threadIdx.x, lane = tid & 31;
+  pdl_wait();  // (a programmatic dependent of K4a)
 #ifdef FGS_FAST_CRMATH
   crm::stage_tables();
   __syncthreads();
@@ -1044,8 +1045,8 @@ void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene
   const int64_t mq = a.q_end - a.q_begin;
   const int blocks = mq > 0 ? div_up(static_cast<int>(mq), kBwdThreads) : 1;
   if (host_scene) preprocess_backward_kernel<true, 6><<<blocks, kBwdThreads, 0, st>>>(a);
-  else if (variant == 2) preprocess_backward_kernel<false, 4><<<blocks, kBwdThreads, 0, st>>>(a);
-  else preprocess_backward_kernel<false, 6><<<blocks, kBwdThreads, 0, st>>>(a);
+  else if (variant == 2) launch_pdl(preprocess_backward_kernel<false, 4>, dim3(blocks), dim3(kBwdThreads), 0, st, a);
+  else launch_pdl(preprocess_backward_kernel<false, 6>, dim3(blocks), dim3(kBwdThreads), 0, st, a);
 }
 
 }  // namespace fgs

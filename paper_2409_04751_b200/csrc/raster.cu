@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
   __shared__ uint32_t sk[NW][32];    // list index of each staged record
   float4 (*s0)[32] = s01[0];
   float4 (*s1)[32] = s01[1];
+  pdl_wait();  // (a programmatic dependent of K2: everything below reads K2's output)
   if (a.zero_next && blockIdx.x == 0 && threadIdx.x < 16) a.zero_next[threadIdx.x] = 0u;
   // the work item (loaded first: independent of the check below, so the two loads overlap)
   uint4 w = make_uint4(blockIdx.x, 0u, 0u, 0u);
@@ -399,6 +400,7 @@ __global__ void __launch_bounds__(256 / PX) blend_forward_kernel(BlendArgs a, co
       if (CONTRIB && a.blend_count) a.blend_count[pix] = static_cast<uint16_t>(min(p.contrib, 65535u));
     }
   }
+  pdl_trigger();
 }
 
 // alpha_raw's guard test: the fast-exp product lies within the error bound of a threshold.
@@ -452,6 +454,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   __shared__ float s_part[2][NW][32 * 9];  // per-warp sums of the chunk's entries
   __shared__ uint32_t s_mask[2][NW];       // per-warp survivor masks (bit j: entry cs + j)
   __shared__ uint32_t s_top[NW];
+  pdl_wait();  // (a programmatic dependent of the forward's K3)
   // work item: segment `seg` of a tile's list (the first num_seg_items CTAs take the segments
   // k >= 1 of long lists, the rest segment 0 of every tile, heaviest lists first)
   int tile, seg = 0;
@@ -744,6 +747,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   if (seg == 0) span_end(a.tile_span, tile);
+  pdl_trigger();
 }
 }  // namespace
 
@@ -829,11 +833,11 @@ int blend_forward(const BlendArgs& a, int64_t num_isect, int px_request, cudaStr
     if (a.counters) blend_forward_kernel<kModeCounters, 1><<<tiles, 256, 0, st>>>(a, tm);
     else if (a.blend_count) blend_forward_kernel<kModeBlendCount, 1><<<tiles, 256, 0, st>>>(a, tm);
     else if (tma) blend_forward_kernel<0, 1, true><<<tiles, 256, 0, st>>>(a, tm);
-    else blend_forward_kernel<0, 1><<<tiles, 256, 0, st>>>(a, tm);
+    else launch_pdl(blend_forward_kernel<0, 1>, dim3(tiles), dim3(256), 0, st, a, tm);
   } else {
     if (a.counters) blend_forward_kernel<kModeCounters, 2><<<tiles, 128, 0, st>>>(a, tm);
     else if (a.blend_count) blend_forward_kernel<kModeBlendCount, 2><<<tiles, 128, 0, st>>>(a, tm);
-    else blend_forward_kernel<0, 2><<<tiles, 128, 0, st>>>(a, tm);
+    else launch_pdl(blend_forward_kernel<0, 2>, dim3(tiles), dim3(128), 0, st, a, tm);
   }
   return 1;
 }
@@ -875,9 +879,9 @@ int blend_backward(const BlendArgs& a, int64_t num_isect, int variant, cudaStrea
   if (px_used) *px_used = px;
   // one CTA per (tile, segment): the long lists' segments k >= 1 first, then every tile's first
   const int grid = tiles + static_cast<int>(a.num_seg_items);
-  if (px == 1) blend_backward_kernel<1, 4><<<grid, 256, 0, st>>>(a);
-  else if (minb == 8) blend_backward_kernel<2, 8><<<grid, 128, 0, st>>>(a);
-  else blend_backward_kernel<2, 6><<<grid, 128, 0, st>>>(a);
+  if (px == 1) launch_pdl(blend_backward_kernel<1, 4>, dim3(grid), dim3(256), 0, st, a);
+  else if (minb == 8) launch_pdl(blend_backward_kernel<2, 8>, dim3(grid), dim3(128), 0, st, a);
+  else launch_pdl(blend_backward_kernel<2, 6>, dim3(grid), dim3(128), 0, st, a);
   return 1;
 }
 
