@@ -119,7 +119,7 @@ struct fgs_context {
   // per tile / pixel
   DevBuf<uint32_t> tile_offsets, fill, last;
   DevBuf<uint4> tile_sched;
-  DevBuf<int32_t> rowdiff;  // zero between frames (K2a zeroes what K1 added)
+  DevBuf<int32_t> rowdiff;  // zero between frames (K2 zeroes what K1 added)
   size_t rowdiff_clean = 0; // entries known to be zero
   int64_t isect_cap = 0;    // capacity of the per-intersection buffers
   cudaEvent_t ev_k2 = nullptr;    // K2 done on the caller's stream (error detection while waiting)

@@ -503,7 +503,7 @@ __device__ __forceinline__ void preprocess_one(const PreprocessArgs& a, int64_t 
     if (tx1 >= tx0 && ty1 >= ty0) {
       touched = static_cast<uint32_t>((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
       rect = make_ushort4(tx0, tx1, ty0, ty1);
-      // per-tile counts for K2a: +1 / -1 at both ends of every covered row
+      // per-tile counts for K2: +1 / -1 at both ends of every covered row
       const int rw = a.tiles_x + 1;
       for (int ty = ty0; ty <= ty1; ++ty) {
         atomicAdd(a.rowdiff + ty * rw + tx0, 1);
@@ -784,7 +784,7 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
   }
 }
 
-// K4b: one thread per Gaussian that touched a tile, taken in source order from the K2a
+// K4b: one thread per Gaussian that touched a tile, taken in source order from the K2
 // compaction list (cval), 128 per CTA. K4a left one 9-float gradient sum per intersection at
 // its emission slot; the Gaussian's slots [coff[q], +touched[g]) are contiguous in ascending
 // tile order and are summed here in that order:
