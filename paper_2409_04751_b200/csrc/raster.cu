@@ -443,6 +443,16 @@ __device__ __forceinline__ uint32_t emission_slot(const BlendArgs& a, uint32_t g
   return a.src_off[g] + static_cast<uint32_t>((ty - rc.z) * (rc.y - rc.x + 1) + (tx - rc.x));
 }
 
+// K4a's reduce-scatter: before the stage of width `half`, slot i (< 2 half) holds the sum of the
+// slots t == i (mod 2 half); the stage pairs slots i and i + half, i.e. t == i (mod half). With
+// NG splats' 9 values at SQ q + c, the pair needs a shuffle only if one of those t is a value.
+template <int NG, int NV, int SQ>
+__host__ __device__ constexpr bool live_slot(int i, int half) {
+  for (int t = i; t < NV; t += half)
+    if (t % SQ < 9 && t / SQ < NG) return true;
+  return false;
+}
+
 // MINB: CTAs per SM the register allocation is fitted to (a launch-bounds variant: same code,
 // same results, different occupancy).
 template <int PX, int MINB>
@@ -660,6 +670,9 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
       // Branch-free: every lane evaluates all steps and gates them (a non-contributing step
       // leaves T and the suffix colour unchanged and gives zero gradients; all operands are
       // finite: conic <= 1/0.3, one_m >= 0.01).
+      // value slots: splat q's component c at 9 q + c (3 splats), 16 q + c (1 or 2 splats: the
+      // reduce-scatter below then skips the pairs of slots that are both zero)
+      constexpr int SQ = NG == 3 ? 9 : 16;
       float v[32];
       bool contrib_any = false;
 #pragma unroll
@@ -669,7 +682,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
         const float b2 = rec[3 * js[q] + 2].x;
         const float dx = __fsub_rn(fx, r0.x);
 #pragma unroll
-        for (int c9 = 5; c9 < 9; ++c9) v[9 * q + c9] = 0.0f;
+        for (int c9 = 5; c9 < 9; ++c9) v[SQ * q + c9] = 0.0f;
         float p0 = 0.0f, p1 = 0.0f, p2 = 0.0f;
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
@@ -680,15 +693,15 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
           const float inv = fast_rcp(1.0f - alpha);
           const float Tb = T[u] * inv;
           const float w = cc ? alpha * Tb : 0.0f;
-          v[9 * q + 5] += dl[u][0] * w;
-          v[9 * q + 6] += dl[u][1] * w;
-          v[9 * q + 7] += dl[u][2] * w;
+          v[SQ * q + 5] += dl[u][0] * w;
+          v[SQ * q + 6] += dl[u][1] * w;
+          v[SQ * q + 7] += dl[u][2] * w;
           const float dot_c = dl[u][0] * r1.z + dl[u][1] * r1.w + dl[u][2] * b2;
           // clamped contributions carry no geometric gradient
           const float d_alpha = (cc && !(ar[q][u] > kAlphaClamp)) ? dot_c * Tb - ds[u] * inv : 0.0f;
           ds[u] = fmaf(dot_c, w, ds[u]);
           T[u] = cc ? Tb : T[u];
-          v[9 * q + 8] += d_alpha * ex[q][u];
+          v[SQ * q + 8] += d_alpha * ex[q][u];
           // the mean / conic terms through the lane's moments of dpower (its pixels share dx)
           const float dp = d_alpha * alpha;
           p0 += dp;
@@ -696,34 +709,41 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
           p2 = fmaf(dp * dy, dy, p2);
         }
         // sum_u dp (a dx + b dy), sum_u dp (b dx + c dy), -1/2 sum dp dx^2, -sum dp dx dy, -1/2 sum dp dy^2
-        v[9 * q + 0] = fmaf((-2.0f * r0.z) * dx, p0, r0.w * p1);  // conic a = -2 (record's -a/2)
-        v[9 * q + 1] = fmaf(r0.w * dx, p0, (-2.0f * r1.x) * p1);
-        v[9 * q + 2] = (-0.5f * dx * dx) * p0;
-        v[9 * q + 3] = -dx * p1;
-        v[9 * q + 4] = -0.5f * p2;
+        v[SQ * q + 0] = fmaf((-2.0f * r0.z) * dx, p0, r0.w * p1);  // conic a = -2 (record's -a/2)
+        v[SQ * q + 1] = fmaf(r0.w * dx, p0, (-2.0f * r1.x) * p1);
+        v[SQ * q + 2] = (-0.5f * dx * dx) * p0;
+        v[SQ * q + 3] = -dx * p1;
+        v[SQ * q + 4] = -0.5f * p2;
       }
+      // (one splat's 9 values: a 16-wide reduce-scatter over the half-warps, then one shuffle
+      // across them -- 16 shuffles instead of 31; two splats: 24)
+      constexpr int NV = NG == 1 ? 16 : 32;
 #pragma unroll
-      for (int q = 9 * NG; q < 32; ++q) v[q] = 0.0f;
+      for (int s = 0; s < NV; ++s)
+        if (!(s % SQ < 9 && s / SQ < NG)) v[s] = 0.0f;
       if (__any_sync(0xffffffffu, contrib_any)) {
 #pragma unroll
-        for (int half = 16; half >= 1; half >>= 1) {
+        for (int half = NV / 2; half >= 1; half >>= 1) {
           const bool up = (lane & half) != 0;
 #pragma unroll
           for (int i = 0; i < half; ++i) {
+            if (!live_slot<NG, NV, SQ>(i, half)) continue;
             const float send = up ? v[i] : v[i + half];
             const float keep = up ? v[i + half] : v[i];
             v[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
           }
         }
+        if (NV == 16) v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
       } else {
         v[0] = 0.0f;
       }
-      // lane l now holds component l % 9 of splat l / 9 (l < 9 NG)
-      const int q = lane / 9;
+      // lane l now holds slot l % NV: component (l % NV) % SQ of splat (l % NV) / SQ
+      const int sl = lane & (NV - 1);
+      const int q = sl / SQ, c = sl - SQ * q;
       int jq = js[0];  // (no dynamic register indexing)
 #pragma unroll
       for (int t = 1; t < NG; ++t) jq = q == t ? js[t] : jq;
-      if (lane < 9 * NG) part[jq * 9 + (lane - 9 * q)] = v[0];
+      if (c < 9 && q < NG && lane < NV) part[jq * 9 + c] = v[0];
     };
     const int nsurv = __popc(mask);
     for (int t = 0; t + 3 <= nsurv; t += 3) group(std::integral_constant<int, 3>{});
