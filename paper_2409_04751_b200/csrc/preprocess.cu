@@ -588,8 +588,8 @@ __global__ void __launch_bounds__(256, FGS_K1_MINB) preprocess_kernel(Preprocess
   if (threadIdx.x < 2 && s_counts[threadIdx.x]) atomicAdd(a.state_counts + threadIdx.x, s_counts[threadIdx.x]);
 }
 
-// K4b per-Gaussian chain rule for Gaussian i with its summed screen-space gradient sg[9]
-// (mean_px 2, conic 3, colour 3, alpha 1); writes (or adds) its 59 gradient values.
+// K4b per-Gaussian chain rule for Gaussian i with its summed screen-space values sg[9] (power
+// moments 5, colour 3, alpha 1; K4a); writes (or adds) its 59 gradient values.
 // shstage: this lane's 20-float slot -- the SH gradient rows are Y (x) dcolour, so the lane leaves
 // Y[16] (band-masked), dcolour[3] (clamp-masked) and i there and the warp writes the rows as
 // contiguous 192-byte runs afterwards (sh_rows_store).
@@ -607,14 +607,19 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
     project_covariance(cam, m, q, ls, P);
     const float det = P.det;
     const float conic[3] = {P.sp[1][1] / det, -P.sp[0][1] / det, P.sp[0][0] / det};
+    // sg[0..4]: the summed moments M = sum dpower-gradient x (dx, dy, dx^2, dx dy, dy^2) over the
+    // Gaussian's pixels (K4a); dL/dmean_px = (a M0 + b M1, b M0 + c M1) and dL/dconic =
+    // -(M2 / 2, M3, M4 / 2) (gradients.hpp:153-156 per pixel, summed with the conic factored out)
+    const float dmx = conic[0] * sg[0] + conic[1] * sg[1], dmy = conic[1] * sg[0] + conic[2] * sg[1];
     // mean_backward (gradients.hpp:177-181): J^T dmean_px
     float direct[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) direct[k] = P.j[0][k] * sg[0] + P.j[1][k] * sg[1];
+    for (int k = 0; k < 3; ++k) direct[k] = P.j[0][k] * dmx + P.j[1][k] * dmy;
     // gradients.hpp:239-243: dSigma_p = (-Q) Gq Q, b-slot cotangent halved
     const float nq[2][2] = {{-conic[0], -conic[1]}, {-conic[1], -conic[2]}};
     const float Q[2][2] = {{conic[0], conic[1]}, {conic[1], conic[2]}};
-    const float gq[2][2] = {{sg[2], sg[3] / 2.0f}, {sg[3] / 2.0f, sg[4]}};
+    const float h3 = -0.5f * sg[3];
+    const float gq[2][2] = {{-0.5f * sg[2], h3}, {h3, -0.5f * sg[4]}};
     float tmp[2][2], dsp[2][2];
 #pragma unroll
     for (int r = 0; r < 2; ++r)

@@ -420,9 +420,10 @@ __device__ __forceinline__ bool near_threshold(float ar) {
 //     once per CTA by cp.async, two chunks ahead;
 //   * each warp culls the chunk against its block (box test on K1's extent, then the exact
 //     ellipse test), and for every surviving splat, latest first, recovers T_before =
-//     T_after / (1 - alpha), accumulates the suffix colour and forms the 9 per-pixel gradients
-//     (mean_px 2, conic 3, colour 3, alpha_max 1), summed over the lane's pixels and then the warp
-//     by a butterfly reduce-scatter; the warp's 9 sums per surviving entry and its survivor mask
+//     T_after / (1 - alpha), accumulates the suffix colour and forms 9 per-pixel values (the
+//     power-gradient moments dp (dx, dy, dx^2, dx dy, dy^2) -- the mean / conic gradients are
+//     linear in them, K4b applies the conic --, colour 3, alpha_max 1), summed over the lane's
+//     pixels and then the warp by a butterfly reduce-scatter; the warp's 9 sums per surviving entry and its survivor mask
 //     go to shared memory;
 //   * after one CTA barrier per chunk, the CTA adds, per entry, the sums of the warps whose mask
 //     has it, in warp order, and stores the 9 values at the intersection's emission slot (K4b
@@ -708,12 +709,14 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
           p1 = fmaf(dp, dy, p1);
           p2 = fmaf(dp * dy, dy, p2);
         }
-        // sum_u dp (a dx + b dy), sum_u dp (b dx + c dy), -1/2 sum dp dx^2, -sum dp dx dy, -1/2 sum dp dy^2
-        v[SQ * q + 0] = fmaf((-2.0f * r0.z) * dx, p0, r0.w * p1);  // conic a = -2 (record's -a/2)
-        v[SQ * q + 1] = fmaf(r0.w * dx, p0, (-2.0f * r1.x) * p1);
-        v[SQ * q + 2] = (-0.5f * dx * dx) * p0;
-        v[SQ * q + 3] = -dx * p1;
-        v[SQ * q + 4] = -0.5f * p2;
+        // the moments sum_u dp (dx, dy, dx^2, dx dy, dy^2); the mean / conic gradients are linear
+        // in them with the splat's conic as coefficients (K4b forms them from the summed moments)
+        const float m0 = dx * p0;
+        v[SQ * q + 0] = m0;
+        v[SQ * q + 1] = p1;
+        v[SQ * q + 2] = dx * m0;
+        v[SQ * q + 3] = dx * p1;
+        v[SQ * q + 4] = p2;
       }
       // (one splat's 9 values: a 16-wide reduce-scatter over the half-warps, then one shuffle
       // across them -- 16 shuffles instead of 31; two splats: 24)
