@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(256, FGS_K1_MINB) preprocess_kernel(Preprocess
 }
 
 // K4b per-Gaussian chain rule for Gaussian i with its summed screen-space values sg[9] (power
-// moments 5, colour 3, alpha 1; K4a); writes (or adds) its 59 gradient values.
+// moments 5, colour 3, sum of dpower; K4a); writes (or adds) its 59 gradient values.
 // shstage: this lane's 20-float slot -- the SH gradient rows are Y (x) dcolour, so the lane leaves
 // Y[16] (band-masked), dcolour[3] (clamp-masked) and i there and the warp writes the rows as
 // contiguous 192-byte runs afterwards (sh_rows_store).
@@ -729,7 +729,8 @@ __device__ __forceinline__ void gaussian_backward(const PreprocessBackwardArgs& 
     const float4 rb = a.rec[i].b;
     const float colour[3] = {rb.z, rb.w, a.rec[i].c.x};
     const float al = rb.y;
-    out[10] = sg[8] * al * (1.0f - al);
+    // sg[8] = sum dp = al * dL/dal (K4a), so dL/dlogit = dL/dal * al (1 - al) = sg[8] (1 - al)
+    out[10] = sg[8] * (1.0f - al);
     // SH: eval_sh_dc_backward (model.hpp:219-227) + higher bands (build extension)
     float dir[3];
     view_dir(cam, m, dir);

@@ -422,7 +422,8 @@ __device__ __forceinline__ bool near_threshold(float ar) {
 //     ellipse test), and for every surviving splat, latest first, recovers T_before =
 //     T_after / (1 - alpha), accumulates the suffix colour and forms 9 per-pixel values (the
 //     power-gradient moments dp (dx, dy, dx^2, dx dy, dy^2) -- the mean / conic gradients are
-//     linear in them, K4b applies the conic --, colour 3, alpha_max 1), summed over the lane's
+//     linear in them, K4b applies the conic --, colour 3, and dp itself, alpha_max times the
+//     alpha_max gradient), summed over the lane's
 //     pixels and then the warp by a butterfly reduce-scatter; the warp's 9 sums per surviving entry and its survivor mask
 //     go to shared memory;
 //   * after one CTA barrier per chunk, the CTA adds, per entry, the sums of the warps whose mask
@@ -683,7 +684,7 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
         const float b2 = rec[3 * js[q] + 2].x;
         const float dx = __fsub_rn(fx, r0.x);
 #pragma unroll
-        for (int c9 = 5; c9 < 9; ++c9) v[SQ * q + c9] = 0.0f;
+        for (int c9 = 5; c9 < 8; ++c9) v[SQ * q + c9] = 0.0f;
         float p0 = 0.0f, p1 = 0.0f, p2 = 0.0f;
 #pragma unroll
         for (int u = 0; u < PX; ++u) {
@@ -702,7 +703,6 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
           const float d_alpha = (cc && !(ar[q][u] > kAlphaClamp)) ? dot_c * Tb - ds[u] * inv : 0.0f;
           ds[u] = fmaf(dot_c, w, ds[u]);
           T[u] = cc ? Tb : T[u];
-          v[SQ * q + 8] += d_alpha * ex[q][u];
           // the mean / conic terms through the lane's moments of dpower (its pixels share dx)
           const float dp = d_alpha * alpha;
           p0 += dp;
@@ -717,6 +717,9 @@ __global__ void __launch_bounds__(256 / PX, MINB) blend_backward_kernel(BlendArg
         v[SQ * q + 2] = dx * m0;
         v[SQ * q + 3] = dx * p1;
         v[SQ * q + 4] = p2;
+        // sum dp = alpha_max * dL/dalpha_max (dp = d_alpha * alpha_max * exp(power) unclamped,
+        // 0 clamped): K4b's opacity-logit gradient is then sum dp (1 - alpha_max)
+        v[SQ * q + 8] = p0;
       }
       // (one splat's 9 values: a 16-wide reduce-scatter over the half-warps, then one shuffle
       // across them -- 16 shuffles instead of 31; two splats: 24)
