@@ -28,6 +28,8 @@
 
 #include <cooperative_groups.h>
 
+#include <utility>
+
 #include "fgs_kernels.h"
 
 namespace cg = cooperative_groups;
@@ -709,6 +711,187 @@ scatter : {
 }
 }
 
+// ---- K2 with CTA-local compaction (the slot order for scenes of <= grid x 8192 Gaussians) ----
+// Each CTA owns one contiguous range of Gaussians (<= kLocG) for the whole kernel. Phase 1 loads
+// its touched counts once and compacts them in shared memory (local position and local
+// intersection prefix of every tile-touching Gaussian, kept across the grid barriers); phase 2
+// only adds the CTAs' prefix to write cval / coff / src_off (no second pass over touched[]);
+// phase 3 scatters the CTA's own intersections from the shared list: one binary search per
+// thread over the compacted offsets, then a forward walk (no global rank search, no staging of
+// coff, no per-slot Gaussian lookups), shared-memory counts per tile, one global atomicAdd per
+// (CTA, tile), then the keys. Same outputs as bin_kernel<false> (the key positions inside a
+// tile's range differ, the per-tile sort orders them).
+constexpr int kLocG = kT * kItems;  // Gaussians per CTA
+constexpr int kLocalSmem = (kLocG + 1 + kLocG / 2) * 4;  // dynamic shared memory before the tile counters
+
+// The CTA's tile-touching Gaussians of [lo, hi) compacted in shared memory: s_lo[q] = their
+// local exclusive intersection prefix, s_lg[q] = local index; returns (count, intersections).
+__device__ __forceinline__ uint2 local_compact(const BinArgs& a, int lo, int hi, uint32_t* s_lo, uint16_t* s_lg,
+                                               ScanSmem& sm) {
+  const int tid = threadIdx.x, r0 = lo + tid * kItems;
+  uint32_t c[kItems], s1 = 0, s2 = 0;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    c[i] = r0 + i < hi ? a.touched[r0 + i] : 0u;
+    s1 += c[i] > 0 ? 1u : 0u;
+    s2 += c[i];
+  }
+  uint32_t m, r;
+  uint32_t pos = block_exclusive_scan(s1, sm.warp_tmp, &m);
+  uint32_t off = block_exclusive_scan(s2, sm.warp_tmp2, &r);
+#pragma unroll
+  for (int i = 0; i < kItems; ++i)
+    if (c[i]) {
+      s_lo[pos] = off;
+      s_lg[pos] = static_cast<uint16_t>(tid * kItems + i);
+      ++pos;
+      off += c[i];
+    }
+  if (tid == 0) s_lo[m] = r;  // sentinel
+  __syncthreads();
+  return make_uint2(m, r);
+}
+
+// Phase 3 of the local variant: the CTA's R intersections from its compacted list (m entries),
+// in passes of <= kSub.
+__device__ void scatter_local(const BinArgs& a, int lo, uint32_t m, uint32_t R, const uint32_t* s_lo,
+                              const uint16_t* s_lg, uint32_t* s_cnt) {
+  constexpr int U = kSub / kT;
+  const int tid = threadIdx.x;
+  for (uint32_t x0 = 0; x0 < R; x0 += kSub) {
+    const uint32_t hi = min(R, x0 + kSub);
+    for (int t = tid; t < a.num_tiles; t += kT) s_cnt[t] = 0;
+    __syncthreads();
+    trace(a.trace, 0, 3);
+    uint32_t ev[U], gv[U], tv[U], pv[U], dk[U];
+    {
+      const uint32_t un = (hi - x0 + kT - 1) / kT;
+      const uint32_t e0 = x0 + static_cast<uint32_t>(tid) * un;
+      int l = 0, h = static_cast<int>(m) - 1;  // largest q with s_lo[q] <= e0
+      while (l < h) {
+        const int mid = (l + h + 1) >> 1;
+        if (s_lo[mid] <= e0) l = mid;
+        else h = mid - 1;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ev[u] = u < static_cast<int>(un) ? e0 + u : hi;  // hi: no slot
+        if (ev[u] < hi)
+          while (s_lo[l + 1] <= ev[u]) ++l;  // (s_lo[m] = R > ev)
+        tv[u] = static_cast<uint32_t>(l);
+        gv[u] = static_cast<uint32_t>(lo + s_lg[l]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) dk[u] = ev[u] < hi ? a.depth_key[gv[u]] : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (ev[u] >= hi) continue;
+      const ushort4 rc = a.rect[gv[u]];
+      FGS_DCHECK(rect_ok(a, rc) && ev[u] >= s_lo[tv[u]] && gv[u] < static_cast<uint32_t>(a.n));
+      const int wx = rc.y - rc.x + 1;
+      const int j = static_cast<int>(ev[u] - s_lo[tv[u]]);
+      tv[u] = static_cast<uint32_t>((rc.z + j / wx) * a.tiles_x + rc.x + j % wx);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) pv[u] = ev[u] < hi ? atomicAdd(s_cnt + tv[u], 1u) : 1u;
+    __syncthreads();
+    trace(a.trace, 0, 4);
+    // the slot that took local position 0 reserves the CTA's block of tile tv[u]
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (pv[u] == 0) s_cnt[tv[u]] = atomicAdd(a.fill + tv[u], s_cnt[tv[u]]);
+    __syncthreads();
+    trace(a.trace, 0, 6);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (ev[u] >= hi) continue;
+      pv[u] += s_cnt[tv[u]];
+      FGS_DCHECK(key_slot_ok(a, tv[u], pv[u]));
+      a.keys[pv[u]] = (static_cast<uint64_t>(dk[u]) << 32) | gv[u];
+    }
+    __syncthreads();  // s_cnt reused by the next pass
+    trace(a.trace, 0, 7);
+  }
+}
+
+__global__ void __launch_bounds__(kT, 1) bin_local_kernel(BinArgs a) {
+  extern __shared__ uint32_t s_dyn[];  // [kLocG + 1] s_lo, [kLocG / 2] s_lg, [num_tiles] tile counters
+  __shared__ ScanSmem sm;
+  __shared__ uint32_t s_rowoff[kW * 64];
+  uint32_t* s_lo = s_dyn;
+  uint16_t* s_lg = reinterpret_cast<uint16_t*>(s_dyn + kLocG + 1);
+  uint32_t* s_cnt = s_dyn + kLocG + 1 + kLocG / 2;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x), nw = G * kW;
+  uint32_t* hist = a.part_scan + 2 * G;
+  uint32_t* cur = hist + 32;
+  uint32_t* rowtot = cur + 32;
+  const int lo = static_cast<int>(static_cast<int64_t>(a.n) * b / G);
+  const int hi = static_cast<int>(static_cast<int64_t>(a.n) * (b + 1) / G);
+  trace(a.trace, 0, -1);
+  const uint2 mr = local_compact(a, lo, hi, s_lo, s_lg, sm);
+  if (!a.scatter_only) {
+    if (tid == 0) {
+      a.part_scan[2 * b] = mr.x;
+      a.part_scan[2 * b + 1] = mr.y;
+    }
+    for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw) row_counts(a, ty, hist, rowtot);
+    trace(a.trace, 0, 0);
+    grid.sync();
+    trace(a.trace, 0, 2);
+    uint32_t p1, tot1, p2, tot2;
+    cta_prefix(a.part_scan, 2, G, sm.warp_tmp, p1, tot1);
+    cta_prefix(a.part_scan + 1, 2, G, sm.warp_tmp, p2, tot2);
+    const uint32_t hk = lane < kSchedBuckets ? hist[lane] : 0u;
+    uint32_t incl = hk;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (b == 0 && tid == 0) {
+      a.scalars[kScalarM] = tot1;
+      a.scalars[kScalarI] = tot2;
+    }
+    if (b == 0 && tid < 32) {
+      uint32_t big = lane < kSchedBuckets && 16 - lane >= 8 ? hk : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) big += __shfl_xor_sync(0xffffffffu, big, o);
+      if (lane == 0) a.scalars[kScalarBig] = big;
+    }
+    // gradient-chunk boundaries c N / C inside this CTA's range: the compacted position there
+    if (tid > 0 && tid < kGradChunks) {
+      const int gc = static_cast<int>(static_cast<int64_t>(a.n) * tid / kGradChunks);
+      if (gc >= lo && gc < hi) {
+        uint32_t q = 0, h = mr.x;  // first compacted entry with id >= gc
+        while (q < h) {
+          const uint32_t mid = (q + h) >> 1;
+          if (lo + static_cast<int>(s_lg[mid]) < gc) q = mid + 1;
+          else h = mid;
+        }
+        a.scalars[kScalarChunkQ + tid - 1] = p1 + q;
+      }
+    }
+    for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw)
+      row_offsets(a, ty, rowtot, hist, cur, incl - hk, s_rowoff + 64 * (tid >> 5));
+    for (uint32_t q = tid; q < mr.x; q += kT) {
+      const uint32_t g = static_cast<uint32_t>(lo + s_lg[q]), off = p2 + s_lo[q];
+      a.cval[p1 + q] = g;
+      a.coff[p1 + q] = off;
+      a.src_off[g] = off;
+    }
+    trace(a.trace, 0, 1);
+    grid.sync();
+    trace(a.trace, 0, 2);
+    if (b == 0 && tid < 64) hist[tid] = 0;  // hist + cur: last read before this barrier
+  }
+  const uint32_t I = a.scalars[kScalarI];
+  if (I <= a.isect_cap && I != 0) scatter_local(a, lo, mr.x, mr.y, s_lo, s_lg, s_cnt);
+  if (!a.scatter_only) publish_host_scalars(a, b);
+}
+
 // Debug export: the reference's pre-sort key list (source order, ty-major, tx-minor).
 __global__ void __launch_bounds__(kT, 1) debug_keys_kernel(BinArgs a, uint32_t* key_tile, uint32_t* key_depth,
                                                            uint32_t* key_gauss) {
@@ -734,10 +917,13 @@ int grid_size() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int ok = 1;
-    for (const void* f : {reinterpret_cast<const void*>(bin_kernel<true>), reinterpret_cast<const void*>(bin_kernel<false>)}) {
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrivTiles * 4);
+    const std::pair<const void*, int> ks[] = {{reinterpret_cast<const void*>(bin_kernel<true>), kPrivTiles * 4},
+                                              {reinterpret_cast<const void*>(bin_kernel<false>), kPrivTiles * 4},
+                                              {reinterpret_cast<const void*>(bin_local_kernel), kLocalSmem + kPrivTiles * 4}};
+    for (const auto& k : ks) {
+      cudaFuncSetAttribute(k.first, cudaFuncAttributeMaxDynamicSharedMemorySize, k.second);
       int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kT, kPrivTiles * 4);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.first, kT, k.second);
       ok = ok && per_sm > 0;
     }
     return ok ? sms : -1;  // -1: cooperative launch impossible
@@ -757,6 +943,8 @@ cudaError_t bin_launch(BinArgs& a, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(std::min(a.num_tiles, kPrivTiles)) * 4;
   // the source-order scatter needs every tile's counter in shared memory
   const bool rows = a.row_scatter || a.num_tiles > kPrivTiles;
+  if (!rows && a.fast && static_cast<int64_t>(a.n) <= static_cast<int64_t>(g) * kLocG)
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bin_local_kernel), g, kT, args, kLocalSmem + smem, st);
   return cudaLaunchCooperativeKernel(rows ? reinterpret_cast<const void*>(bin_kernel<true>)
                                           : reinterpret_cast<const void*>(bin_kernel<false>),
                                      g, kT, args, smem, st);

@@ -85,6 +85,13 @@ int rule_row_scatter(int64_t I) {
   if (e == 1 || e == 2) return e == 1;
   return I > 2000000 ? 1 : 0;
 }
+// K2 on the slot order: bin_local_kernel (each CTA compacts and scatters its own range of
+// Gaussians from shared memory) for scenes of <= 148 x 8192 Gaussians; FGS_BIN_FAST=1 takes
+// bin_kernel's global slot order (intersection-balanced ranges, global rank search).
+int rule_bin_fast() {
+  static const int e = env_int("FGS_BIN_FAST");
+  return e == 1 ? 0 : 1;
+}
 int rule_k4b_minb(int64_t m) {
   static const int e = env_int("FGS_K4B_MINB");
   if (e == 4 || e == 6) return e;
@@ -611,6 +618,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.row_scatter = (ctx->flags & FGS_FLAG_ROW_SCATTER) ? 1 : (ctx->flags & FGS_FLAG_SLOT_SCATTER) ? 0
                                                           : rule_row_scatter(ctx->num_isect);
   ctx->var_row_scatter = bn.row_scatter;
+  bn.fast = rule_bin_fast();
   bn.src_off = ctx->src_off.p;
   bn.host_scalars = ctx->d_hscalars;
   bn.seq = ++ctx->frame_seq;

@@ -141,6 +141,7 @@ struct BinArgs {
   int64_t isect_cap;           // capacity of the per-intersection buffers (the scatter is skipped if I exceeds it)
   int scatter_only;            // relaunch: phases 1-2 already ran
   int row_scatter;             // phase 3 by tile-row lists (large I) instead of source-order slots
+  int fast;                    // slot order by CTA-local compaction (bin_local_kernel) when the scene fits
   unsigned long long* trace;   // debug phase timestamps (FGS_FLAG_COUNTERS), 8 slots
   const uint32_t* touched;     // [n] tiles touched per Gaussian (K1)
   const uint32_t* depth_key;   // [n] depth key bits (K1)

@@ -11,7 +11,7 @@ from paper_2409_04751_b200 import Rasterizer, RenderOptions, _lib, synthetic  # 
 from tests._helpers import to_device  # noqa: E402
 
 NAMES = ["counts+rows+row hist", "compaction+offsets+row lists", "grid barriers", "scatter: zero counters",
-         "scatter: count pass", "(unused)", "scatter: tile reservations", "scatter: key pass"]
+         "scatter: count pass", "(fast: sub-chunk prefix)", "scatter: tile reservations", "scatter: key pass"]
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 sc, deg, cams, _ = synthetic.config(cfg, **({"views": 1} if cfg >= 3 else {}))
