@@ -242,7 +242,7 @@ def run_ours(args, ws, rank, local):
     r.backward(ds, cam, dl_dev[0], bopt, grads=grads)
     vv = r.debug("variants").tolist()
     variants = {"fwd_pixels_per_lane": vv[0], "bwd_pixels_per_lane": vv[1], "k4b_ctas_per_sm": vv[2],
-                "longest_tile_list": vv[3], "binning_scatter": "tile-row lists" if vv[4] else "source-order slots",
+                "longest_tile_list": vv[3], "binning_scatter": "tile-row lists" if vv[4] else ("CTA-local slots" if vv[5] else "source-order slots"),
                 "rule": "deterministic from frame statistics (fgs_api.cu rule_*)"}
     counters_all = r.debug("counters", np.uint64).tolist()
     counters = counters_all[:2]

@@ -171,10 +171,12 @@ int fgs_last_transfer(const fgs_context* ctx, uint64_t out[2]);
  * contribution count (ForwardContext::blend_count, inc/splatting.hpp:299-301; debug name
  * "blend_count", u16[H*W]; also written with FGS_FLAG_COUNTERS). FGS_FLAG_ROW_SCATTER /
  * FGS_FLAG_SLOT_SCATTER force the binning scatter's work order (tile-row lists / source-order
- * emission slots; default: by the intersection count; same keys either way). FGS_FLAG_KEEP_KEYS is reserved
- * (no effect). Default 0. */
+ * emission slots; default: by the intersection count; same keys either way). On the slot order,
+ * scenes of <= 148 x 8192 Gaussians take the CTA-local binning kernel; FGS_FLAG_GLOBAL_SLOTS forces
+ * the global slot order instead (same outputs). FGS_FLAG_KEEP_KEYS is reserved (no effect).
+ * Default 0. */
 enum { FGS_FLAG_COUNTERS = 1, FGS_FLAG_KEEP_KEYS = 2, FGS_FLAG_TIMING = 4, FGS_FLAG_BLEND_COUNT = 8,
-       FGS_FLAG_ROW_SCATTER = 16, FGS_FLAG_SLOT_SCATTER = 32 };
+       FGS_FLAG_ROW_SCATTER = 16, FGS_FLAG_SLOT_SCATTER = 32, FGS_FLAG_GLOBAL_SLOTS = 64 };
 int fgs_set_flags(fgs_context* ctx, uint32_t flags);
 
 /* Device time per stage accumulated from CUDA events while FGS_FLAG_TIMING is set, and the

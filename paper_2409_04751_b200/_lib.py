@@ -16,7 +16,7 @@ CHECKED_LIB_PATH = os.path.join(HERE, "libfgs_checked.so")
 
 FGS_OK, FGS_EINVAL, FGS_EDEGENERATE_QUAT, FGS_ECUDA, FGS_ENOMEM, FGS_ESTATE, FGS_ENONFINITE = range(7)
 FGS_FLAG_COUNTERS, FGS_FLAG_KEEP_KEYS, FGS_FLAG_TIMING, FGS_FLAG_BLEND_COUNT = 1, 2, 4, 8
-FGS_FLAG_ROW_SCATTER, FGS_FLAG_SLOT_SCATTER = 16, 32
+FGS_FLAG_ROW_SCATTER, FGS_FLAG_SLOT_SCATTER, FGS_FLAG_GLOBAL_SLOTS = 16, 32, 64
 
 
 class fgs_camera(C.Structure):

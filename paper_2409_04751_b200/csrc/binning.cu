@@ -17,6 +17,11 @@
 //      phase 3: each intersection (Gaussian g, tile t) claims a position in tile t's range
 //               (per-CTA shared-memory counts, one global atomicAdd per (CTA, tile)) and its
 //               64-bit key (depth_key << 32 | g) is written there;
+//   K2 bin_local_kernel (same phases and outputs; scenes of <= 148 x 8192 Gaussians, configs 0-2):
+//      each CTA compacts its own range of Gaussians once in shared memory (phase 1), writes the
+//      compacted list with the CTAs' prefix added (phase 2) and scatters its own intersections
+//      from the shared list (phase 3), with no global rank search or second pass over touched[];
+//      larger scenes take bin_kernel's slot order or tile-row lists;
 //   [host reads I and the frame's scalars, off the critical path; K3 is already queued]
 //   K3 (raster.cu) sorts each tile's keys at the start of its CTA (fgs_sort.cuh).
 //
@@ -943,7 +948,8 @@ cudaError_t bin_launch(BinArgs& a, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(std::min(a.num_tiles, kPrivTiles)) * 4;
   // the source-order scatter needs every tile's counter in shared memory
   const bool rows = a.row_scatter || a.num_tiles > kPrivTiles;
-  if (!rows && a.fast && static_cast<int64_t>(a.n) <= static_cast<int64_t>(g) * kLocG)
+  a.fast = !rows && a.fast && static_cast<int64_t>(a.n) <= static_cast<int64_t>(g) * kLocG;  // (reported back)
+  if (a.fast)
     return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bin_local_kernel), g, kT, args, kLocalSmem + smem, st);
   return cudaLaunchCooperativeKernel(rows ? reinterpret_cast<const void*>(bin_kernel<true>)
                                           : reinterpret_cast<const void*>(bin_kernel<false>),

@@ -133,7 +133,7 @@ struct fgs_context {
   uint32_t* d_hscalars = nullptr; // device view of h_scalars (mapped pinned memory K2 writes)
   uint32_t frame_seq = 0;         // K2 writes it to h_scalars[kHostSeq] after the scalars
   uint32_t longest = 0;     // longest tile list of the last forward
-  int var_fwd_px = 0, var_bwd_px = 0, var_k4b = 0, var_row_scatter = 0;  // launch variants (reported)
+  int var_fwd_px = 0, var_bwd_px = 0, var_k4b = 0, var_row_scatter = 0, var_bin_local = 0;  // launch variants (reported)
   // The device scalars alternate between two 16-word halves by frame parity; a frame's K3 zeroes
   // the other half for the next frame (whose previous readback finished before this frame began),
   // so no memset precedes K1. scalars_clean[h]: half h is known to be zero.
@@ -618,7 +618,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
   bn.row_scatter = (ctx->flags & FGS_FLAG_ROW_SCATTER) ? 1 : (ctx->flags & FGS_FLAG_SLOT_SCATTER) ? 0
                                                           : rule_row_scatter(ctx->num_isect);
   ctx->var_row_scatter = bn.row_scatter;
-  bn.fast = rule_bin_fast();
+  bn.fast = (ctx->flags & FGS_FLAG_GLOBAL_SLOTS) ? 0 : rule_bin_fast();
   bn.src_off = ctx->src_off.p;
   bn.host_scalars = ctx->d_hscalars;
   bn.seq = ++ctx->frame_seq;
@@ -627,6 +627,7 @@ int fgs_forward(fgs_context* ctx, const fgs_gaussians* scene, const fgs_camera* 
     ctx->rowdiff_clean = 0;  // dirty until K2 has consumed K1's counts
     nvtxMarkA("K2 binning");
     FGS_CHECK(fgs::bin_launch(bn, st));
+    ctx->var_bin_local = bn.fast;
     ctx->rowdiff_clean = ndiff;
     ++launches;
   } else {
@@ -1501,9 +1502,9 @@ int64_t fgs_debug_get(fgs_context* ctx, const char* name, void* dst, int64_t dst
   }
   if (nm == "offsets") return copy(ctx->tile_offsets.p, (nt + 1) * 4);
   if (nm == "variants") {  // launch variants of the last forward / backward, longest tile list
-    const uint32_t v[5] = {static_cast<uint32_t>(ctx->var_fwd_px), static_cast<uint32_t>(ctx->var_bwd_px),
+    const uint32_t v[6] = {static_cast<uint32_t>(ctx->var_fwd_px), static_cast<uint32_t>(ctx->var_bwd_px),
                            static_cast<uint32_t>(ctx->var_k4b), ctx->longest,
-                           static_cast<uint32_t>(ctx->var_row_scatter)};
+                           static_cast<uint32_t>(ctx->var_row_scatter), static_cast<uint32_t>(ctx->var_bin_local)};
     if (!dst) return sizeof(v);
     if (dst_bytes < static_cast<int64_t>(sizeof(v))) return -1;
     std::memcpy(dst, v, sizeof(v));

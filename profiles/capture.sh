@@ -12,6 +12,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
   python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches_$R.log 2>&1
 python profiles/ncu_driver.py
 ncu --set full --clock-control none --import-source on \
-  -k regex:"preprocess_kernel|bin_kernel|blend_|preprocess_backward" -s 98 -c 5 \
+  -k regex:"preprocess_kernel|bin_|blend_|preprocess_backward" -s 98 -c 5 \
   -o gpurun_out/full_$R -f python profiles/ncu_driver.py > gpurun_out/ncu_full_$R.log 2>&1
 echo capture-done

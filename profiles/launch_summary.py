@@ -34,7 +34,7 @@ if __name__ == "__main__":
 
 def step_share(res, names):
     """Mean-time share of each kernel within one step made of the given kernels (one launch
-    each), e.g. the device-resident forward: preprocess_kernel<0>, bin_kernel, blend_forward."""
+    each), e.g. the device-resident forward: preprocess_kernel<0>, bin_local_kernel (or bin_kernel), blend_forward."""
     pick = {}
     for k, n, m, t, sh in res:
         for want in names:
@@ -46,7 +46,7 @@ def step_share(res, names):
 
 if __name__ == "__main__" and len(sys.argv) > 1:
     res, _ = summarise(sys.argv[1])
-    for title, names in (("forward step (device-resident)", ["void preprocess_kernel<0>", "void bin_kernel",
+    for title, names in (("forward step (device-resident)", ["void preprocess_kernel<0>", "bin_local_kernel", "void bin_kernel",
                                                             "void blend_forward_kernel<0"]),
                          ("backward step", ["void blend_backward_kernel", "void preprocess_backward_kernel<0"])):
         sh, tot = step_share(res, names)

@@ -30,7 +30,7 @@ METRICS = [
 # bench.py stage -> kernels it times
 STAGES = {
     "preprocess": ["preprocess_kernel"],
-    "binning+sort": ["bin_kernel"],
+    "binning+sort": ["bin_"],
     "raster": ["blend_forward_kernel"],
     "raster_backward": ["blend_backward_kernel"],
     "preprocess_backward": ["preprocess_backward_kernel"],

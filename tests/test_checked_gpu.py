@@ -31,6 +31,7 @@ CASES = [
     pytest.param(0, 0, 1, 0, {}, id="cfg0"),
     pytest.param(0, 0, 1, 0, {"FGS_FWD_PX": "2", "FGS_BWD_PX": "2"}, id="cfg0-px2"),
     pytest.param(1, 0, 1, 0, {}, id="cfg1"),
+    pytest.param(1, 0, 1, 96, {}, id="cfg1-global-slots"),
     pytest.param(2, 0, 1, 16, {}, id="cfg2-rows"),
     pytest.param(2, 0, 1, 32, {"FGS_BWD_MINB": "8", "FGS_K4B_MINB": "4"}, id="cfg2-slots-minb8"),
     pytest.param(2, 0, 1, 0, {"FGS_FWD_PX": "1", "FGS_FWD_TMA": "1", "FGS_BWD_PX": "1", "FGS_K4B_MINB": "6"},

@@ -112,7 +112,7 @@ def test_cfg1_full_scale_fwd_bwd_parity(rast, oracle_mod):
     check_grads(g, o)
 
 
-@pytest.mark.parametrize("scatter", ["slots", "rows"])
+@pytest.mark.parametrize("scatter", ["slots", "rows", "local"])
 def test_cfg2_hot_path_key_list_and_counters(rast, oracle_mod, scatter):
     """Config 2 full scale (1M clustered Gaussians), with either scatter work order (tile-row
     lists or source-order slots). The pre-sort key list comes from the hot path's own state: K2's compaction (the tile-touching Gaussians in source order with their
@@ -133,12 +133,14 @@ def test_cfg2_hot_path_key_list_and_counters(rast, oracle_mod, scatter):
     assert I > 500_000
 
     ds = to_device(scene)
-    force = _lib.FGS_FLAG_ROW_SCATTER if scatter == "rows" else _lib.FGS_FLAG_SLOT_SCATTER
+    force = {"rows": _lib.FGS_FLAG_ROW_SCATTER, "local": _lib.FGS_FLAG_SLOT_SCATTER,
+             "slots": _lib.FGS_FLAG_SLOT_SCATTER | _lib.FGS_FLAG_GLOBAL_SLOTS}[scatter]
     rast.set_flags(_lib.FGS_FLAG_COUNTERS | force)
     try:
         _, st = rast.forward(ds, cam, RenderOptions(sh_degree=deg), want_stats=True)
         ev, ec = rast.debug("counters", np.uint64)[:2]
-        assert rast.debug("variants")[4] == (1 if scatter == "rows" else 0)
+        vv = rast.debug("variants")
+        assert vv[4] == (1 if scatter == "rows" else 0) and vv[5] == (1 if scatter == "local" else 0)
     finally:
         rast.set_flags(0)
     assert st.num_intersections == I
