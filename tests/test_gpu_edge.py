@@ -482,3 +482,40 @@ def test_backward_host_async_stream_of_frames(rast):
     rast.render_host(hs, views[1], o)
     rast.backward_host(hs, views[1], dl, BackwardOptions(), grads=acc_ref, accumulate=True)
     assert acc.tobytes() == acc_ref.tobytes()
+
+
+@pytest.mark.parametrize("scatter", ["local", "slots", "rows"])
+def test_huge_splats_every_binning_path(rast, oracle_mod, scatter):
+    """Splats that each cover most of the tile grid: every binning CTA scatters more than one
+    8192-intersection pass (bin_local_kernel's multi-pass scatter, the global slot order's
+    sub-ranges, the tile-row lists' windows), against the oracle's ranges, order and image."""
+    import torch
+    from paper_2409_04751_b200 import RenderOptions, Scene, _lib
+
+    rng = np.random.default_rng(21)
+    n = 2000
+    d = rng.standard_normal((n, 3)) * np.array([0.15, 0.15, 0.0]) + np.array([0.0, 0.0, 1.0])
+    means = (d / np.linalg.norm(d, axis=1, keepdims=True) * rng.uniform(4.0, 8.0, size=(n, 1))).astype(np.float32)
+    q = rng.standard_normal((n, 4))
+    sh = np.zeros((n, 48), np.float32)
+    sh[:, [0, 16, 32]] = rng.normal(0, 0.3, size=(n, 3))
+    sc = Scene(means, (q / np.linalg.norm(q, axis=1, keepdims=True)).astype(np.float32),
+               rng.normal(0.6, 0.2, size=(n, 3)).astype(np.float32), rng.normal(-4.0, 0.5, size=n).astype(np.float32),
+               sh, np.zeros(3, np.float32))
+    cam = small_fisheye(640, 480)
+    flags = {"local": _lib.FGS_FLAG_SLOT_SCATTER, "slots": _lib.FGS_FLAG_SLOT_SCATTER | _lib.FGS_FLAG_GLOBAL_SLOTS,
+             "rows": _lib.FGS_FLAG_ROW_SCATTER}[scatter]
+    rast.set_flags(flags)
+    try:
+        img, st = rast.forward(to_device(sc), cam, RenderOptions(sh_degree=0), want_stats=True)
+        torch.cuda.synchronize()
+        vv = rast.debug("variants")
+        assert vv[4] == (scatter == "rows") and vv[5] == (scatter == "local")
+        res = oracle_mod.render(sc, cam, sh_degree=0)
+        assert st.num_intersections == res.num_intersections
+        assert res.num_intersections > 148 * 8192  # > one scatter pass per binning CTA
+        np.testing.assert_array_equal(rast.debug("offsets"), res.get("offsets"))
+        np.testing.assert_array_equal(rast.debug("sorted_gauss"), res.get("source")[res.get("refs")])
+        assert np.abs(img.cpu().numpy().astype(np.float64) - res.image).max() <= 1e-3
+    finally:
+        rast.set_flags(0)
