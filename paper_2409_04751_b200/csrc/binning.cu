@@ -301,7 +301,7 @@ __device__ void cta_upper_rank2(const uint32_t* offs, int m, uint32_t v0, uint32
 // tile with shared-memory atomics, then one global atomicAdd per (CTA, tile) reserves the
 // block, so a heavy tile sees one global atomic per CTA instead of one per intersection. All
 // loads and atomics of a thread's slots are issued before their results are used.
-constexpr int kSub = 8192;  // emission slots per source-order scatter sub-range
+constexpr int kSub = 8 * kT;  // emission slots per source-order scatter sub-range
 
 template <bool PRIV>
 __device__ void scatter_range(const BinArgs& a, int m, uint32_t lo, uint32_t hi, uint32_t* s_cnt, uint32_t* s_off,
@@ -556,7 +556,7 @@ __device__ __forceinline__ void publish_host_scalars(const BinArgs& a, int b) {
 // ROWS: phase 3 by row lists (few tiles per CTA: little contention on the tile cursors; wins for
 // large I, configs 3 and 4) or by emission slots in source order (no row-list passes; config 2).
 template <bool ROWS>
-__global__ void __launch_bounds__(kT, 1) bin_kernel(BinArgs a) {
+__global__ void __launch_bounds__(kT, kBinCtasPerSm) bin_kernel(BinArgs a) {
   extern __shared__ uint32_t s_cnt[];  // [min(num_tiles, kPrivTiles)] phase-3 tile counters
   __shared__ ScanSmem sm;
   __shared__ uint32_t s_rowoff[kW * 64];         // row_offsets scratch, 64 words per warp
@@ -820,7 +820,7 @@ __device__ void scatter_local(const BinArgs& a, int lo, uint32_t m, uint32_t R, 
   }
 }
 
-__global__ void __launch_bounds__(kT, 1) bin_local_kernel(BinArgs a) {
+__global__ void __launch_bounds__(kT, kBinCtasPerSm) bin_local_kernel(BinArgs a) {
   extern __shared__ uint32_t s_dyn[];  // [kLocG + 1] s_lo, [kLocG / 2] s_lg, [num_tiles] tile counters
   __shared__ ScanSmem sm;
   __shared__ uint32_t s_rowoff[kW * 64];
@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(kT, 1) bin_local_kernel(BinArgs a) {
 }
 
 // Debug export: the reference's pre-sort key list (source order, ty-major, tx-minor).
-__global__ void __launch_bounds__(kT, 1) debug_keys_kernel(BinArgs a, uint32_t* key_tile, uint32_t* key_depth,
+__global__ void __launch_bounds__(kT, kBinCtasPerSm) debug_keys_kernel(BinArgs a, uint32_t* key_tile, uint32_t* key_depth,
                                                            uint32_t* key_gauss) {
   const int m = static_cast<int>(a.scalars[kScalarM]);
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
@@ -929,9 +929,9 @@ int grid_size() {
       cudaFuncSetAttribute(k.first, cudaFuncAttributeMaxDynamicSharedMemorySize, k.second);
       int per_sm = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k.first, kT, k.second);
-      ok = ok && per_sm > 0;
+      ok = ok && per_sm >= kBinCtasPerSm;
     }
-    return ok ? sms : -1;  // -1: cooperative launch impossible
+    return ok ? sms * kBinCtasPerSm : -1;  // -1: cooperative launch impossible
   });
 }
 

@@ -105,7 +105,14 @@ void preprocess_backward_launch(const PreprocessBackwardArgs& a, bool host_scene
 constexpr int kPreprocessBackwardThreads = 128;  // tile-touching Gaussians per K4b CTA
 
 // ---- binning / sorting (binning.cu) ----
-constexpr int kBinThreads = 1024;
+#ifndef FGS_BIN_THREADS
+#define FGS_BIN_THREADS 1024
+#endif
+#ifndef FGS_BIN_CTAS_PER_SM
+#define FGS_BIN_CTAS_PER_SM 1
+#endif
+constexpr int kBinThreads = FGS_BIN_THREADS;          // K2 CTA size (experiment builds: 512 x 2 per SM)
+constexpr int kBinCtasPerSm = FGS_BIN_CTAS_PER_SM;
 constexpr int kScalarI = 0, kScalarErr = 1, kScalarKept = 2, kScalarDegen = 3, kScalarM = 4, kScalarI2 = 5, kScalarBig = 6,
               kScalarSegs = 7,    // backward segment slots of the frame (K2: sum over long lists of ceil(L / kSeg))
               kScalarSegPos = 8,  // K3's slot allocation cursor
