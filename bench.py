@@ -288,6 +288,11 @@ def run_ours(args, ws, rank, local):
                                else f"MEASURED_PEAKS.json hbm_gbs ({peak_src})")
         return roof
 
+    # (K1's figure counts every Gaussian's 192-byte SH row; K1 reads the rows of Gaussians that
+    # project near the image only, and is issue / latency-bound, not HBM-bound: DESIGN.md §8)
+    if "preprocess" in rooflines:
+        rooflines["preprocess"]["note"] = ("issue/latency-bound (ncu: ~76% issue, ~155 MB DRAM per launch at "
+                                           "config 2); the algorithmic bytes count all SH rows")
     roof = dominant(primary_stages)
     # the metric's second half (fwd+bwd views/s): dominant stage of forward + backward
     roof_fb = dominant(["preprocess", "binning+sort", "raster", "raster_backward", "preprocess_backward"])

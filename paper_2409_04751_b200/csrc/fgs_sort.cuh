@@ -121,6 +121,11 @@ __device__ __forceinline__ void ce(uint64_t* s, int i, int p) {
 }
 
 constexpr int kChunk = 256;  // keys per warp register chunk (E = 8)
+#ifndef FGS_SORT_WARP_MAX
+#define FGS_SORT_WARP_MAX 256
+#endif
+constexpr int kWarpSortMax = FGS_SORT_WARP_MAX;  // longer lists: the CTA sorts (one warp below)
+static_assert(kWarpSortMax <= kChunk, "one warp sorts at most one register chunk");
 
 // Register phase over the shared array s[0, n) (n a multiple of the chunk 32*E): every warp
 // loads its chunks, runs a full sort (first) or the half-cleaner stages j < 32E of a merge
@@ -336,7 +341,7 @@ __device__ int sort_tile_list(uint64_t* keys, uint32_t* sorted_gauss, uint32_t l
   uint32_t* s32 = reinterpret_cast<uint32_t*>(s);
   uint64_t* g = keys + lo;
   if (L <= 0) return 0;
-  if (L <= kChunk) {
+  if (L <= kWarpSortMax) {
     if (tid < 32) {
       auto run = [&](auto e_tag) {
         constexpr int E = decltype(e_tag)::value;
