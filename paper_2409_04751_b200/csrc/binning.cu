@@ -731,13 +731,17 @@ constexpr int kLocalSmem = (kLocG + 1 + kLocG / 2) * 4;  // dynamic shared memor
 
 // The CTA's tile-touching Gaussians of [lo, hi) compacted in shared memory: s_lo[q] = their
 // local exclusive intersection prefix, s_lg[q] = local index; returns (count, intersections).
+// `between` runs while the touched loads are in flight (the row warps' phase-1 work).
+template <typename F>
 __device__ __forceinline__ uint2 local_compact(const BinArgs& a, int lo, int hi, uint32_t* s_lo, uint16_t* s_lg,
-                                               ScanSmem& sm) {
+                                               ScanSmem& sm, F&& between) {
   const int tid = threadIdx.x, r0 = lo + tid * kItems;
   uint32_t c[kItems], s1 = 0, s2 = 0;
 #pragma unroll
+  for (int i = 0; i < kItems; ++i) c[i] = r0 + i < hi ? a.touched[r0 + i] : 0u;
+  between();
+#pragma unroll
   for (int i = 0; i < kItems; ++i) {
-    c[i] = r0 + i < hi ? a.touched[r0 + i] : 0u;
     s1 += c[i] > 0 ? 1u : 0u;
     s2 += c[i];
   }
@@ -836,13 +840,17 @@ __global__ void __launch_bounds__(kT, kBinCtasPerSm) bin_local_kernel(BinArgs a)
   const int lo = static_cast<int>(static_cast<int64_t>(a.n) * b / G);
   const int hi = static_cast<int>(static_cast<int64_t>(a.n) * (b + 1) / G);
   trace(a.trace, 0, -1);
-  const uint2 mr = local_compact(a, lo, hi, s_lo, s_lg, sm);
+  // the tile rows' counts by the CTAs' last warps (rows b, b + G, ... of CTA b), overlapping the
+  // touched loads of the local compaction
+  const uint2 mr = local_compact(a, lo, hi, s_lo, s_lg, sm, [&] {
+    if (!a.scatter_only)
+      for (int ty = b + G * (kW - 1 - (tid >> 5)); ty < a.tiles_y; ty += nw) row_counts(a, ty, hist, rowtot);
+  });
   if (!a.scatter_only) {
     if (tid == 0) {
       a.part_scan[2 * b] = mr.x;
       a.part_scan[2 * b + 1] = mr.y;
     }
-    for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw) row_counts(a, ty, hist, rowtot);
     trace(a.trace, 0, 0);
     grid.sync();
     trace(a.trace, 0, 2);
