@@ -854,9 +854,6 @@ __global__ void __launch_bounds__(kT, kBinCtasPerSm) bin_local_kernel(BinArgs a)
     trace(a.trace, 0, 0);
     grid.sync();
     trace(a.trace, 0, 2);
-    uint32_t p1, tot1, p2, tot2;
-    cta_prefix(a.part_scan, 2, G, sm.warp_tmp, p1, tot1);
-    cta_prefix(a.part_scan + 1, 2, G, sm.warp_tmp, p2, tot2);
     const uint32_t hk = lane < kSchedBuckets ? hist[lane] : 0u;
     uint32_t incl = hk;
 #pragma unroll
@@ -864,10 +861,34 @@ __global__ void __launch_bounds__(kT, kBinCtasPerSm) bin_local_kernel(BinArgs a)
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    if (b == 0 && tid == 0) {
-      a.scalars[kScalarM] = tot1;
-      a.scalars[kScalarI] = tot2;
+    // the row warps (the CTAs' last warps) write their rows' offsets and schedule slots while
+    // warp 0 sums the CTAs' partials (no block scans); one barrier hands the prefix to the CTA
+    for (int ty = b + G * (kW - 1 - (tid >> 5)); ty < a.tiles_y; ty += nw)
+      row_offsets(a, ty, rowtot, hist, cur, incl - hk, s_rowoff + 64 * (tid >> 5));
+    if (tid < 32) {
+      uint32_t v4[4] = {0u, 0u, 0u, 0u};  // p1, p2, tot1, tot2
+      for (int c = lane; c < G; c += 32) {
+        const uint32_t m1 = a.part_scan[2 * c], m2 = a.part_scan[2 * c + 1];
+        v4[2] += m1;
+        v4[3] += m2;
+        if (c < b) {
+          v4[0] += m1;
+          v4[1] += m2;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v4[k] = __reduce_add_sync(0xffffffffu, v4[k]);
+      if (lane == 0) {
+        sm.scalar[0] = v4[0];
+        sm.scalar[1] = v4[1];
+        if (b == 0) {
+          a.scalars[kScalarM] = v4[2];
+          a.scalars[kScalarI] = v4[3];
+        }
+      }
     }
+    __syncthreads();
+    const uint32_t p1 = sm.scalar[0], p2 = sm.scalar[1];
     if (b == 0 && tid < 32) {
       uint32_t big = lane < kSchedBuckets && 16 - lane >= 8 ? hk : 0u;
 #pragma unroll
@@ -887,8 +908,6 @@ __global__ void __launch_bounds__(kT, kBinCtasPerSm) bin_local_kernel(BinArgs a)
         a.scalars[kScalarChunkQ + tid - 1] = p1 + q;
       }
     }
-    for (int ty = b + G * (tid >> 5); ty < a.tiles_y; ty += nw)
-      row_offsets(a, ty, rowtot, hist, cur, incl - hk, s_rowoff + 64 * (tid >> 5));
     for (uint32_t q = tid; q < mr.x; q += kT) {
       const uint32_t g = static_cast<uint32_t>(lo + s_lg[q]), off = p2 + s_lo[q];
       a.cval[p1 + q] = g;
