@@ -331,7 +331,8 @@ struct Proj {
 // view, so its load after the projection finds it there.
 // The SH row is requested early only for Gaussians whose centre projects within this many pixels
 // of the image (0: every Gaussian in the field of view). At config 2 about 40 % of the field of
-// view falls outside the image rectangle; K1 0.0608 -> 0.0594 ms at a 32-pixel margin (128: 0.0597).
+// view falls outside the image rectangle; K1 0.0608 -> 0.0594 ms at a 32-pixel margin (8 / 64 / 128:
+// within 0.5 % of it).
 #ifndef FGS_K1_PF_MARGIN
 #define FGS_K1_PF_MARGIN 32
 #endif
